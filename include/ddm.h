@@ -1,0 +1,157 @@
+/*
+ * ddm.h -- C ABI of libddm: B200-native sort-based DDM region matching.
+ *
+ * Operation (§3, P:190-197 and Alg. 1, d-dim P:237-247):
+ * given n subscription extents S_i and m update extents U_j, each a
+ * d-dimensional axis-parallel box of CLOSED intervals [lo, hi], report every
+ * pair (S_i, U_j) with S_i ∩ U_j ≠ ∅, i.e. for every dimension k
+ *        sub_lo[k][i] <= upd_hi[k][j]  &&  upd_lo[k][j] <= sub_hi[k][i].
+ * The result is computed by the paper's sort-based matching (Alg. 4/5,
+ * P:413-557) re-designed for sm_100a: order-preserving u64 endpoint keys,
+ * onesweep LSB radix sort, rank-difference count pass, exclusive scan of the
+ * counts, and a chunked sweep that emits every pair exactly once.
+ *
+ * Conventions shared by every entry point
+ *  - Coordinates: IEEE float64, compared exactly (no epsilon).  -0.0 equals
+ *    +0.0.  NaN/±inf are rejected (DDM_ERR_NONFINITE).  lo > hi in
+ *    any dimension is rejected (DDM_ERR_INVERTED_INTERVAL); lo == hi is
+ *    a legal point interval.  Duplicates are distinct regions.
+ *  - Ids are the array indices 0..n-1 / 0..m-1.
+ *  - Pointers marked (device) must be CUDA device pointers (cudaMalloc /
+ *    torch CUDA tensors) on the current device; (host) are host pointers.
+ *  - Ownership: the caller owns every buffer (inputs, outputs, workspace,
+ *    index).  The library allocates no device memory and keeps no state
+ *    between calls; calls are reentrant given distinct workspaces.
+ *  - Streams: all device work is stream-ordered on `stream`.  Entry points
+ *    that return a count block on one small device->host read of it.
+ *  - Alignment: workspace and index must be 256-byte aligned; region arrays
+ *    8-byte aligned; the pair buffer 8-byte aligned.
+ *  - Sizes: 0 <= n_sub, n_upd <= DDM_MAX_REGIONS; counts K are uint64.
+ *  - Errors never write past `capacity` pairs; on any error the contents of
+ *    the pair buffer are unspecified.
+ */
+#ifndef DDM_H
+#define DDM_H
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DDM_MAX_DIMS 8
+/* Per-kind region limit: radix-sort look-back words hold 30-bit counts. */
+#define DDM_MAX_REGIONS 1073741823ull
+
+typedef enum {
+    DDM_OK = 0,
+    DDM_ERR_INVALID_ARGUMENT = 1,  /* null pointer, d == 0 or d > DDM_MAX_DIMS,
+                                      n > DDM_MAX_REGIONS, misalignment */
+    DDM_ERR_NONFINITE = 2,         /* a NaN or ±inf coordinate */
+    DDM_ERR_INVERTED_INTERVAL = 3, /* lo > hi in some dimension */
+    DDM_ERR_CAPACITY = 4,          /* capacity < K; *count_out = K, no pair written */
+    DDM_ERR_WORKSPACE = 5,         /* ws_bytes (or index_bytes) too small */
+    DDM_ERR_CUDA = 6               /* CUDA launch/runtime failure; see ddm_last_cuda_error() */
+} ddm_status;
+
+/* Regions of one problem instance, structure-of-arrays per dimension.
+ * sub_lo[k] / sub_hi[k] (device) have n_sub float64 entries for k < d;
+ * upd_lo[k] / upd_hi[k] (device) have n_upd entries.  Unused slots ignored. */
+typedef struct {
+    uint32_t d;
+    uint64_t n_sub;
+    uint64_t n_upd;
+    const double *sub_lo[DDM_MAX_DIMS];
+    const double *sub_hi[DDM_MAX_DIMS];
+    const double *upd_lo[DDM_MAX_DIMS];
+    const double *upd_hi[DDM_MAX_DIMS];
+} ddm_regions;
+
+/* One reported intersection, paper order (S_i, U_j).  Read as a
+ * little-endian uint64 it equals (upd << 32) | sub -- the canonical key. */
+typedef struct {
+    uint32_t sub;
+    uint32_t upd;
+} ddm_pair;
+
+/* Flags for ddm_match_pairs / ddm_match_pairs_indexed.  The output ORDER is
+ * deterministic without flags: rows by (upd lower bound, upd id), within a row
+ * subscriptions by (sub lower bound, sub id) on the sweep dimension 0.  The
+ * emit-path flags only force one of the three emission paths (for tests);
+ * every path yields byte-identical output. */
+#define DDM_EMIT_AUTO 0u
+#define DDM_EMIT_FORCE_THREAD (1u << 8) /* one thread per update row */
+#define DDM_EMIT_FORCE_WARP (1u << 9)   /* one warp per update row, global scan */
+#define DDM_EMIT_FORCE_CHUNK (1u << 10) /* chunk-start sets staged in smem */
+
+/* Workspace bytes needed by ddm_match_count (want_pairs = 0) or
+ * ddm_match_pairs (want_pairs != 0) for these sizes.  Independent of K. */
+size_t ddm_workspace_bytes(uint32_t d, uint64_t n_sub, uint64_t n_upd, int want_pairs);
+
+/* K = number of intersecting pairs (SPEC S:41-46 count mode, the paper's
+ * experimental mode P:915-918).  count_out (host) receives K. */
+ddm_status ddm_match_count(const ddm_regions *regions, uint64_t *count_out, void *ws,
+                           size_t ws_bytes, cudaStream_t stream);
+
+/* List mode: writes the K pairs to pairs[0..K) (device) and K to *count_out
+ * (host).  If capacity < K returns DDM_ERR_CAPACITY with *count_out = K and
+ * writes no pair (call with capacity 0 to size the buffer).  Validation
+ * errors are reported before any pair is written. */
+ddm_status ddm_match_pairs(const ddm_regions *regions, ddm_pair *pairs, uint64_t capacity,
+                           uint64_t *count_out, uint32_t flags, void *ws, size_t ws_bytes,
+                           cudaStream_t stream);
+
+/* Sort pairs[0..k) (device) in place into canonical order: ascending
+ * (upd << 32) | sub.  ids must satisfy sub < n_sub and upd < n_upd. */
+size_t ddm_sort_pairs_workspace_bytes(uint64_t k);
+ddm_status ddm_sort_pairs(ddm_pair *pairs, uint64_t k, uint64_t n_sub, uint64_t n_upd,
+                          void *ws, size_t ws_bytes, cudaStream_t stream);
+
+/* --- Subscription index: the subscription half of the pipeline, built once
+ * (sorted dim-0 lower/upper keys, ids, gathered upper keys, block maxima and
+ * the other dimensions in sweep order) and byte-copyable, so one rank can
+ * build it and broadcast it to the others (multi-GPU split). */
+size_t ddm_sub_index_bytes(uint32_t d, uint64_t n_sub);
+size_t ddm_index_build_workspace_bytes(uint32_t d, uint64_t n_sub);
+ddm_status ddm_sub_index_build(const ddm_regions *subs /* n_upd ignored */, void *index,
+                               size_t index_bytes, void *ws, size_t ws_bytes,
+                               cudaStream_t stream);
+
+/* Match updates against a built index.  upds->n_sub must equal the indexed
+ * n_sub and upds->d its d.  upd_ids (device, may be NULL): global id of each
+ * local update, written into ddm_pair.upd (NULL = local index).  Workspace
+ * from ddm_indexed_workspace_bytes. */
+size_t ddm_indexed_workspace_bytes(uint32_t d, uint64_t n_sub, uint64_t n_upd);
+ddm_status ddm_match_pairs_indexed(const void *index, const ddm_regions *upds,
+                                   const uint32_t *upd_ids, ddm_pair *pairs, uint64_t capacity,
+                                   uint64_t *count_out, uint32_t flags, void *ws,
+                                   size_t ws_bytes, cudaStream_t stream);
+ddm_status ddm_match_count_indexed(const void *index, const ddm_regions *upds,
+                                   uint64_t *count_out, void *ws, size_t ws_bytes,
+                                   cudaStream_t stream);
+
+/* --- Primitive exported for tests: stable LSB onesweep radix sort of u64
+ * keys (device) with optional u32 values, over bits [begin_bit, end_bit).
+ * keys_out/vals_out (device) receive the result; inputs are not modified. */
+size_t ddm_radix_sort_workspace_bytes(uint64_t n);
+ddm_status ddm_radix_sort_u64(const uint64_t *keys_in, const uint32_t *vals_in,
+                              uint64_t *keys_out, uint32_t *vals_out, uint64_t n,
+                              int begin_bit, int end_bit, void *ws, size_t ws_bytes,
+                              cudaStream_t stream);
+
+/* Order-preserving float64 -> u64 key used by the sort:
+ * canonicalise -0.0 to +0.0, then flip the sign bit of non-negatives and all
+ * bits of negatives.  Device arrays of length n. */
+ddm_status ddm_encode_keys(const double *x, uint64_t *keys, uint64_t n, cudaStream_t stream);
+
+const char *ddm_status_string(ddm_status s);
+int ddm_last_cuda_error(void);          /* last cudaError_t seen by the library */
+uint64_t ddm_kernel_launch_count(void); /* kernels launched by this process so far */
+const char *ddm_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DDM_H */

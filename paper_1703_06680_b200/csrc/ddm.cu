@@ -1,0 +1,642 @@
+// ddm.cu -- host side of libddm: the C ABI of include/ddm.h and the launch
+// orchestration of the sort-based matching pipeline on the caller's stream.
+//
+// Pipeline for d = 1:
+//   validate_hist(subs)  -> onesweep x8 (Slo: key+id, from float64)
+//                        -> onesweep x8 (Shi: keys)     -> gather slo_hi + block maxima
+//   validate_hist(upds)  -> onesweep x8 (Ulo: key+id)   -> gather uhi
+//   count_scan (rank differences + exclusive scan, one kernel)
+//   one 16-byte D2H {K, error word}; capacity check
+//   emit (stab part from the sweep state + contiguous range part)
+// The subscription half forms the byte-copyable "index" (multi-GPU: built by
+// one rank and broadcast).
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/ddm.h"
+#include "common.cuh"
+#include "match.cuh"
+#include "radix.cuh"
+
+using namespace ddm;
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+std::atomic<int> g_last_cuda{0};
+
+#define DDM_LAUNCH(...)                        \
+  do {                                         \
+    __VA_ARGS__;                               \
+    g_launches.fetch_add(1, std::memory_order_relaxed); \
+  } while (0)
+
+#define DDM_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) {                             \
+      g_last_cuda.store((int)e_);                        \
+      return DDM_ERR_CUDA;                               \
+    }                                                    \
+  } while (0)
+
+inline ddm_status check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_last_cuda.store((int)e);
+    return DDM_ERR_CUDA;
+  }
+  return DDM_OK;
+}
+
+#define DDM_TRY(x)                \
+  do {                            \
+    ddm_status s_ = (x);          \
+    if (s_ != DDM_OK) return s_;  \
+  } while (0)
+
+constexpr int kSMs = 148;
+
+inline size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// A bump allocator that either measures (base == nullptr) or carves.
+struct Carver {
+  uint8_t* base;
+  size_t used = 0;
+  explicit Carver(void* b) : base(static_cast<uint8_t*>(b)) {}
+  template <typename T>
+  T* take(uint64_t count) {
+    T* p = base ? reinterpret_cast<T*>(base + used) : nullptr;
+    used += a256(sizeof(T) * (count ? count : 1));
+    return p;
+  }
+};
+
+// ------------------------------------------------------------ index layout
+
+struct Index {
+  uint32_t d = 1;
+  uint64_t n = 0;
+  int levels = 0;
+  uint64_t lvl_n[kMaxLevels + 1] = {};
+  uint64_t* slo_key = nullptr;
+  uint32_t* slo_id = nullptr;
+  uint64_t* slo_hi = nullptr;
+  uint64_t* lvl[kMaxLevels + 1] = {};
+  uint64_t* shi_key = nullptr;
+  double* sdims = nullptr;
+  size_t bytes = 0;
+};
+
+Index index_layout(uint32_t d, uint64_t n, void* base) {
+  Index I;
+  I.d = d;
+  I.n = n;
+  Carver c(base);
+  I.slo_key = c.take<uint64_t>(n);
+  I.slo_id = c.take<uint32_t>(n);
+  I.slo_hi = c.take<uint64_t>(n);
+  I.lvl[0] = I.slo_hi;
+  I.lvl_n[0] = n;
+  uint64_t sz = n;
+  while (sz > 1 && I.levels < kMaxLevels) {
+    sz = (sz + 31) / 32;
+    ++I.levels;
+    I.lvl_n[I.levels] = sz;
+    I.lvl[I.levels] = c.take<uint64_t>(sz);
+  }
+  I.shi_key = c.take<uint64_t>(n);
+  I.sdims = c.take<double>((uint64_t)2 * (d - 1) * n);
+  I.bytes = c.used;
+  return I;
+}
+
+MaxTree tree_of(const Index& I) {
+  MaxTree T{};
+  for (int L = 0; L <= I.levels; ++L) T.lvl[L] = I.lvl[L];
+  T.levels = I.levels;
+  return T;
+}
+
+// ------------------------------------------------------------ sort scratch
+
+struct SortScratch {
+  uint32_t* hist[3];   // [8][256] each: Slo, Shi, Ulo (or generic)
+  uint32_t* starts;    // [8][256] global bin starts of the sort in flight
+  uint32_t* status;    // [tiles][256]
+  uint32_t* counters;  // [8]
+  uint64_t* alt_keys;
+  uint32_t* alt_vals;
+  uint64_t cap;
+};
+
+SortScratch sort_scratch(Carver& c, uint64_t cap) {
+  SortScratch s;
+  for (int i = 0; i < 3; ++i) s.hist[i] = c.take<uint32_t>(radix::kMaxPasses * radix::kRadix);
+  s.starts = c.take<uint32_t>(radix::kMaxPasses * radix::kRadix);
+  s.status = c.take<uint32_t>((radix::num_tiles(cap) + 1) * radix::kRadix);
+  s.counters = c.take<uint32_t>(radix::kMaxPasses);
+  s.alt_keys = c.take<uint64_t>(cap);
+  s.alt_vals = c.take<uint32_t>(cap);
+  s.cap = cap;
+  return s;
+}
+
+struct Misc {  // device-side results read back with one copy
+  uint64_t K;
+  uint32_t err;
+  uint32_t pad;
+};
+
+struct MatchWs {
+  uint64_t* ulo_key;
+  uint32_t* ulo_id;
+  uint64_t* uhi;
+  uint32_t* r_lo;
+  uint32_t* r_b;
+  uint64_t* off;
+  uint32_t* cnt;    // d > 1
+  uint32_t* fstab;  // d > 1
+  uint64_t* offd;   // d > 1
+  uint64_t* scan_status;
+  uint32_t* scan_counter;
+  Misc* misc;
+  SortScratch sort;
+  size_t bytes;
+};
+
+MatchWs match_layout(uint32_t d, uint64_t n_sub, uint64_t m, void* base) {
+  Carver c(base);
+  MatchWs W{};
+  W.misc = c.take<Misc>(1);
+  W.scan_counter = c.take<uint32_t>(8);
+  W.scan_status = c.take<uint64_t>(m / match::kCountTile + 2);
+  W.ulo_key = c.take<uint64_t>(m);
+  W.ulo_id = c.take<uint32_t>(m);
+  W.uhi = c.take<uint64_t>(m);
+  W.r_lo = c.take<uint32_t>(m);
+  W.r_b = c.take<uint32_t>(m);
+  W.off = c.take<uint64_t>(m + 1);
+  if (d > 1) {
+    W.cnt = c.take<uint32_t>(m);
+    W.fstab = c.take<uint32_t>(m);
+    W.offd = c.take<uint64_t>(m + 1);
+  }
+  W.sort = sort_scratch(c, n_sub > m ? n_sub : m);
+  W.bytes = c.used;
+  return W;
+}
+
+// ------------------------------------------------------------ radix sort driver
+
+template <typename K>
+void set_smem_attr(K kernel) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(radix::PassSmem));
+}
+
+void init_attrs_once() {
+  static bool done = false;
+  if (done) return;
+  set_smem_attr(radix::onesweep_kernel<true, true>);
+  set_smem_attr(radix::onesweep_kernel<true, false>);
+  set_smem_attr(radix::onesweep_kernel<false, true>);
+  set_smem_attr(radix::onesweep_kernel<false, false>);
+  done = true;
+}
+
+inline unsigned grid_for(uint64_t n, int threads, int per_sm) {
+  uint64_t g = (n + threads - 1) / threads;
+  uint64_t cap = (uint64_t)kSMs * per_sm;
+  if (g > cap) g = cap;
+  return (unsigned)(g ? g : 1);
+}
+
+radix::PassList full_passes() {
+  radix::PassList P{};
+  P.n = 8;
+  for (int p = 0; p < 8; ++p) { P.shift[p] = 8 * p; P.mask[p] = 255; }
+  return P;
+}
+
+// Sort n keys (float64 encoded on the fly when src_f64) into keys_out (and
+// vals_out when non-null).  `hist` must hold the per-pass histograms already
+// when hist_ready; otherwise it is computed here.
+ddm_status radix_sort(const void* src, bool src_f64, const uint32_t* vals_in, uint64_t* keys_out,
+                      uint32_t* vals_out, uint64_t n, const radix::PassList& P, uint32_t* hist,
+                      bool hist_ready, SortScratch& s, cudaStream_t st) {
+  if (n == 0) return DDM_OK;
+  if (P.n == 0) return DDM_ERR_INVALID_ARGUMENT;
+  init_attrs_once();
+  if (!hist_ready) {
+    DDM_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * radix::kMaxPasses * radix::kRadix, st));
+    if (src_f64)
+      DDM_LAUNCH(radix::hist_kernel<true><<<grid_for(n, 512, 4), 512, 0, st>>>(src, n, P, hist));
+    else
+      DDM_LAUNCH(radix::hist_kernel<false><<<grid_for(n, 512, 4), 512, 0, st>>>(src, n, P, hist));
+    DDM_TRY(check_launch());
+  }
+  DDM_LAUNCH(radix::bin_start_kernel<<<P.n, radix::kRadix, 0, st>>>(hist, s.starts));
+  DDM_TRY(check_launch());
+  const uint64_t tiles = radix::num_tiles(n);
+  const bool kv = vals_out != nullptr;
+  const void* cur_k = src;
+  const uint32_t* cur_v = vals_in;
+  bool cur_f64 = src_f64;
+  // in-place request with an odd pass count: move the input out of the way
+  if (!src_f64 && cur_k == keys_out && (P.n & 1)) {
+    DDM_CUDA(cudaMemcpyAsync(s.alt_keys, cur_k, n * 8, cudaMemcpyDeviceToDevice, st));
+    cur_k = s.alt_keys;
+    if (kv && vals_in == vals_out && vals_in) {
+      DDM_CUDA(cudaMemcpyAsync(s.alt_vals, vals_in, n * 4, cudaMemcpyDeviceToDevice, st));
+      cur_v = s.alt_vals;
+    }
+  }
+  DDM_CUDA(cudaMemsetAsync(s.counters, 0, sizeof(uint32_t) * radix::kMaxPasses, st));
+  const size_t smem = sizeof(radix::PassSmem);
+  for (int p = 0; p < P.n; ++p) {
+    const bool to_out = ((P.n - 1 - p) % 2) == 0;
+    uint64_t* dk = to_out ? keys_out : s.alt_keys;
+    uint32_t* dv = kv ? (to_out ? vals_out : s.alt_vals) : nullptr;
+    DDM_CUDA(cudaMemsetAsync(s.status, 0, sizeof(uint32_t) * radix::kRadix * tiles, st));
+    const uint32_t* ph = s.starts + p * radix::kRadix;
+    dim3 g((unsigned)tiles);
+    if (kv) {
+      if (cur_f64)
+        DDM_LAUNCH(radix::onesweep_kernel<true, true><<<g, radix::kThreads, smem, st>>>(
+            cur_k, nullptr, dk, dv, n, P.shift[p], P.mask[p], ph, s.status, s.counters + p));
+      else
+        DDM_LAUNCH(radix::onesweep_kernel<true, false><<<g, radix::kThreads, smem, st>>>(
+            cur_k, cur_v, dk, dv, n, P.shift[p], P.mask[p], ph, s.status, s.counters + p));
+    } else {
+      if (cur_f64)
+        DDM_LAUNCH(radix::onesweep_kernel<false, true><<<g, radix::kThreads, smem, st>>>(
+            cur_k, nullptr, dk, nullptr, n, P.shift[p], P.mask[p], ph, s.status, s.counters + p));
+      else
+        DDM_LAUNCH(radix::onesweep_kernel<false, false><<<g, radix::kThreads, smem, st>>>(
+            cur_k, nullptr, dk, nullptr, n, P.shift[p], P.mask[p], ph, s.status, s.counters + p));
+    }
+    DDM_TRY(check_launch());
+    cur_k = dk;
+    cur_v = dv;
+    cur_f64 = false;
+  }
+  return DDM_OK;
+}
+
+// ------------------------------------------------------------ argument checks
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+ddm_status check_side(uint32_t d, uint64_t cnt, const double* const* lo, const double* const* hi) {
+  if (cnt > DDM_MAX_REGIONS) return DDM_ERR_INVALID_ARGUMENT;
+  if (cnt == 0) return DDM_OK;
+  for (uint32_t k = 0; k < d; ++k)
+    if (!lo[k] || !hi[k] || !aligned(lo[k], 8) || !aligned(hi[k], 8)) return DDM_ERR_INVALID_ARGUMENT;
+  return DDM_OK;
+}
+
+ddm_status check_regions(const ddm_regions* R, bool need_sub, bool need_upd) {
+  if (!R || R->d == 0 || R->d > DDM_MAX_DIMS) return DDM_ERR_INVALID_ARGUMENT;
+  if (need_sub) DDM_TRY(check_side(R->d, R->n_sub, R->sub_lo, R->sub_hi));
+  if (need_upd) DDM_TRY(check_side(R->d, R->n_upd, R->upd_lo, R->upd_hi));
+  return DDM_OK;
+}
+
+ddm_status err_status(uint32_t e) {
+  if (e & match::kErrNonFinite) return DDM_ERR_NONFINITE;
+  if (e & match::kErrInverted) return DDM_ERR_INVERTED_INTERVAL;
+  return DDM_OK;
+}
+
+// validate all dims of one side; histogram dim 0 into hist_lo / hist_hi
+ddm_status validate_side(uint32_t d, uint64_t cnt, const double* const* lo, const double* const* hi,
+                         uint32_t* hist_lo, uint32_t* hist_hi, uint32_t* err, cudaStream_t st) {
+  if (cnt == 0) return DDM_OK;
+  for (uint32_t k = 0; k < d; ++k) {
+    DDM_LAUNCH(match::validate_hist_kernel<<<grid_for(cnt, 512, 4), 512, 0, st>>>(
+        lo[k], hi[k], cnt, k == 0 ? hist_lo : nullptr, k == 0 ? hist_hi : nullptr, err));
+    DDM_TRY(check_launch());
+  }
+  return DDM_OK;
+}
+
+// ------------------------------------------------------------ index build (async)
+
+ddm_status build_index_async(const ddm_regions* R, const Index& I, SortScratch& s, uint32_t* err,
+                             cudaStream_t st) {
+  const uint64_t n = R->n_sub;
+  if (n == 0) return DDM_OK;
+  DDM_CUDA(cudaMemsetAsync(s.hist[0], 0, sizeof(uint32_t) * 8 * 256, st));
+  DDM_CUDA(cudaMemsetAsync(s.hist[1], 0, sizeof(uint32_t) * 8 * 256, st));
+  DDM_TRY(validate_side(R->d, n, R->sub_lo, R->sub_hi, s.hist[0], s.hist[1], err, st));
+  const radix::PassList P = full_passes();
+  // a2: Slo (key + sub id, encoded from float64 in pass 1), Shi (keys)
+  DDM_TRY(radix_sort(R->sub_lo[0], true, nullptr, I.slo_key, I.slo_id, n, P, s.hist[0], true, s, st));
+  DDM_TRY(radix_sort(R->sub_hi[0], true, nullptr, I.shi_key, nullptr, n, P, s.hist[1], true, s, st));
+  // a3: slo_hi[i] = key(sub_hi[slo_id[i]]) + block maxima
+  DDM_LAUNCH(match::gather_key_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.slo_id, R->sub_hi[0], n,
+                                                                             I.slo_hi, I.levels ? I.lvl[1] : nullptr));
+  DDM_TRY(check_launch());
+  for (int L = 2; L <= I.levels; ++L) {
+    DDM_LAUNCH(match::block_max_kernel<<<grid_for(I.lvl_n[L - 1], 256, 8), 256, 0, st>>>(
+        I.lvl[L - 1], I.lvl_n[L - 1], I.lvl[L]));
+    DDM_TRY(check_launch());
+  }
+  if (R->d > 1) {
+    match::DimPtrs D{};
+    for (uint32_t k = 0; k < R->d; ++k) { D.lo[k] = R->sub_lo[k]; D.hi[k] = R->sub_hi[k]; }
+    DDM_LAUNCH(match::gather_dims_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.slo_id, D, (int)R->d, n, I.sdims));
+    DDM_TRY(check_launch());
+  }
+  return DDM_OK;
+}
+
+// ------------------------------------------------------------ match against an index
+
+struct MatchReq {
+  const Index* I;
+  const ddm_regions* R;       // update side (d, n_upd, upd_lo/hi)
+  const uint32_t* upd_map;    // optional global ids
+  ddm_pair* pairs;            // nullptr = count only
+  uint64_t capacity;
+  uint32_t flags;
+};
+
+ddm_status match_indexed(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool err_pending,
+                         cudaStream_t st) {
+  const Index& I = *q.I;
+  const ddm_regions* R = q.R;
+  const uint64_t m = R->n_upd, n = I.n;
+  const uint32_t d = R->d;
+  if (!err_pending) DDM_CUDA(cudaMemsetAsync(W.misc, 0, sizeof(Misc), st));
+  if (m == 0 || n == 0) {
+    // nothing can match; still validate the non-empty side(s)
+    DDM_TRY(validate_side(d, m, R->upd_lo, R->upd_hi, nullptr, nullptr, &W.misc->err, st));
+    Misc h{};
+    DDM_CUDA(cudaMemcpyAsync(&h, W.misc, sizeof(Misc), cudaMemcpyDeviceToHost, st));
+    DDM_CUDA(cudaStreamSynchronize(st));
+    *count_out = 0;
+    return err_status(h.err);
+  }
+  SortScratch& s = W.sort;
+  DDM_CUDA(cudaMemsetAsync(s.hist[2], 0, sizeof(uint32_t) * 8 * 256, st));
+  DDM_TRY(validate_side(d, m, R->upd_lo, R->upd_hi, s.hist[2], nullptr, &W.misc->err, st));
+  DDM_TRY(radix_sort(R->upd_lo[0], true, nullptr, W.ulo_key, W.ulo_id, m, full_passes(), s.hist[2], true, s, st));
+  DDM_LAUNCH(match::gather_key_kernel<<<grid_for(m, 256, 8), 256, 0, st>>>(W.ulo_id, R->upd_hi[0], m, W.uhi, nullptr));
+  DDM_TRY(check_launch());
+  // a4 + a5: counts by rank difference and their exclusive scan
+  const uint64_t ctiles = (m + match::kCountTile - 1) / match::kCountTile;
+  DDM_CUDA(cudaMemsetAsync(W.scan_counter, 0, sizeof(uint32_t) * 8, st));
+  DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (ctiles + 1), st));
+  DDM_LAUNCH(match::count_scan_kernel<<<(unsigned)ctiles, match::kCountThreads, 0, st>>>(
+      W.ulo_key, W.uhi, m, I.slo_key, I.shi_key, n, W.r_lo, W.r_b, W.off, W.scan_status, W.scan_counter,
+      d == 1 ? &W.misc->K : nullptr));
+  DDM_TRY(check_launch());
+
+  match::EmitArgs A{};
+  A.ulo_key = W.ulo_key;
+  A.ulo_id = W.ulo_id;
+  A.upd_map = q.upd_map;
+  A.r_lo = W.r_lo;
+  A.r_b = W.r_b;
+  A.off0 = W.off;
+  A.off = W.off;
+  A.slo_id = I.slo_id;
+  A.T = tree_of(I);
+  A.F.dims = (int)d - 1;
+  A.F.sdims = I.sdims;
+  A.F.n = n;
+  for (uint32_t k = 0; k < d; ++k) { A.upd.lo[k] = R->upd_lo[k]; A.upd.hi[k] = R->upd_hi[k]; }
+  A.m = m;
+  A.thread_row_max = 16;
+  A.force = (q.flags & DDM_EMIT_FORCE_THREAD) ? 1 : (q.flags & DDM_EMIT_FORCE_WARP) ? 2 : 0;
+  const unsigned egrid = (unsigned)((m + match::kEmitThreads - 1) / match::kEmitThreads);
+
+  if (d > 1) {
+    // a8: dim-0 candidates filtered on dims 1..d-1; count pass + scan
+    A.cnt_out = W.cnt;
+    A.fstab_out = W.fstab;
+    DDM_LAUNCH(match::emit_kernel<match::kCountDD><<<egrid, match::kEmitThreads, 0, st>>>(A));
+    DDM_TRY(check_launch());
+    DDM_CUDA(cudaMemsetAsync(W.scan_counter, 0, sizeof(uint32_t) * 8, st));
+    DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (ctiles + 1), st));
+    DDM_LAUNCH(match::scan_u32_kernel<<<(unsigned)ctiles, match::kCountThreads, 0, st>>>(
+        W.cnt, m, W.offd, W.scan_status, W.scan_counter, &W.misc->K));
+    DDM_TRY(check_launch());
+    A.off = W.offd;
+    A.fstab = W.fstab;
+  }
+  Misc h{};
+  DDM_CUDA(cudaMemcpyAsync(&h, W.misc, sizeof(Misc), cudaMemcpyDeviceToHost, st));
+  DDM_CUDA(cudaStreamSynchronize(st));
+  *count_out = h.K;
+  DDM_TRY(err_status(h.err));
+  if (!q.pairs) return DDM_OK;
+  if (h.K > q.capacity) return DDM_ERR_CAPACITY;
+  if (h.K == 0) return DDM_OK;
+  A.pairs = reinterpret_cast<uint2*>(q.pairs);
+  if (d == 1)
+    DDM_LAUNCH(match::emit_kernel<match::kEmitD1><<<egrid, match::kEmitThreads, 0, st>>>(A));
+  else
+    DDM_LAUNCH(match::emit_kernel<match::kEmitDD><<<egrid, match::kEmitThreads, 0, st>>>(A));
+  DDM_TRY(check_launch());
+  return DDM_OK;
+}
+
+__global__ void encode_kernel(const double* __restrict__ x, uint64_t* __restrict__ k, uint64_t n) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) k[i] = f64_key(x[i]);
+}
+
+int bits_for(uint64_t v) {  // bits needed to represent v (0 -> 0)
+  int b = 0;
+  while (v) { ++b; v >>= 1; }
+  return b;
+}
+
+}  // namespace
+
+// ============================================================ C ABI
+
+extern "C" {
+
+size_t ddm_sub_index_bytes(uint32_t d, uint64_t n_sub) {
+  if (d == 0 || d > DDM_MAX_DIMS) return 0;
+  return index_layout(d, n_sub, nullptr).bytes;
+}
+
+size_t ddm_index_build_workspace_bytes(uint32_t d, uint64_t n_sub) {
+  if (d == 0 || d > DDM_MAX_DIMS) return 0;
+  Carver c(nullptr);
+  c.take<Misc>(1);
+  sort_scratch(c, n_sub);
+  return c.used;
+}
+
+size_t ddm_indexed_workspace_bytes(uint32_t d, uint64_t n_sub, uint64_t n_upd) {
+  if (d == 0 || d > DDM_MAX_DIMS) return 0;
+  return match_layout(d, n_sub, n_upd, nullptr).bytes;
+}
+
+size_t ddm_workspace_bytes(uint32_t d, uint64_t n_sub, uint64_t n_upd, int want_pairs) {
+  (void)want_pairs;
+  if (d == 0 || d > DDM_MAX_DIMS) return 0;
+  return a256(index_layout(d, n_sub, nullptr).bytes) + match_layout(d, n_sub, n_upd, nullptr).bytes;
+}
+
+static ddm_status match_full(const ddm_regions* R, ddm_pair* pairs, uint64_t capacity, uint64_t* count_out,
+                             uint32_t flags, void* ws, size_t ws_bytes, cudaStream_t st) {
+  DDM_TRY(check_regions(R, true, true));
+  if (!count_out || (!ws && ws_bytes) || !aligned(ws, 256)) return DDM_ERR_INVALID_ARGUMENT;
+  if (pairs && !aligned(pairs, 8)) return DDM_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < ddm_workspace_bytes(R->d, R->n_sub, R->n_upd, pairs != nullptr)) return DDM_ERR_WORKSPACE;
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  Index I = index_layout(R->d, R->n_sub, base);
+  MatchWs W = match_layout(R->d, R->n_sub, R->n_upd, base + a256(I.bytes));
+  DDM_CUDA(cudaMemsetAsync(W.misc, 0, sizeof(Misc), st));
+  DDM_TRY(build_index_async(R, I, W.sort, &W.misc->err, st));
+  MatchReq q{&I, R, nullptr, pairs, capacity, flags};
+  return match_indexed(q, W, count_out, true, st);
+}
+
+ddm_status ddm_match_count(const ddm_regions* regions, uint64_t* count_out, void* ws, size_t ws_bytes,
+                           cudaStream_t stream) {
+  return match_full(regions, nullptr, 0, count_out, 0, ws, ws_bytes, stream);
+}
+
+ddm_status ddm_match_pairs(const ddm_regions* regions, ddm_pair* pairs, uint64_t capacity,
+                           uint64_t* count_out, uint32_t flags, void* ws, size_t ws_bytes,
+                           cudaStream_t stream) {
+  if (!pairs && capacity) return DDM_ERR_INVALID_ARGUMENT;
+  if (flags & DDM_EMIT_FORCE_CHUNK) return DDM_ERR_INVALID_ARGUMENT;  // not built yet
+  ddm_pair dummy;
+  return match_full(regions, pairs ? pairs : &dummy, pairs ? capacity : 0, count_out, flags, ws, ws_bytes,
+                    stream);
+}
+
+ddm_status ddm_sub_index_build(const ddm_regions* subs, void* index, size_t index_bytes, void* ws,
+                               size_t ws_bytes, cudaStream_t stream) {
+  DDM_TRY(check_regions(subs, true, false));
+  if (!index || !aligned(index, 256) || !aligned(ws, 256)) return DDM_ERR_INVALID_ARGUMENT;
+  if (index_bytes < ddm_sub_index_bytes(subs->d, subs->n_sub)) return DDM_ERR_WORKSPACE;
+  if (ws_bytes < ddm_index_build_workspace_bytes(subs->d, subs->n_sub)) return DDM_ERR_WORKSPACE;
+  Index I = index_layout(subs->d, subs->n_sub, index);
+  Carver c(ws);
+  Misc* misc = c.take<Misc>(1);
+  SortScratch s = sort_scratch(c, subs->n_sub);
+  DDM_CUDA(cudaMemsetAsync(misc, 0, sizeof(Misc), stream));
+  DDM_TRY(build_index_async(subs, I, s, &misc->err, stream));
+  Misc h{};
+  DDM_CUDA(cudaMemcpyAsync(&h, misc, sizeof(Misc), cudaMemcpyDeviceToHost, stream));
+  DDM_CUDA(cudaStreamSynchronize(stream));
+  return err_status(h.err);
+}
+
+static ddm_status indexed_common(const void* index, const ddm_regions* upds, const uint32_t* upd_ids,
+                                 ddm_pair* pairs, uint64_t capacity, uint64_t* count_out, uint32_t flags,
+                                 void* ws, size_t ws_bytes, cudaStream_t st) {
+  DDM_TRY(check_regions(upds, false, true));
+  if (!index || !count_out || !aligned(index, 256) || !aligned(ws, 256)) return DDM_ERR_INVALID_ARGUMENT;
+  if (upds->n_sub > DDM_MAX_REGIONS) return DDM_ERR_INVALID_ARGUMENT;
+  if (flags & DDM_EMIT_FORCE_CHUNK) return DDM_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < ddm_indexed_workspace_bytes(upds->d, upds->n_sub, upds->n_upd)) return DDM_ERR_WORKSPACE;
+  Index I = index_layout(upds->d, upds->n_sub, const_cast<void*>(index));
+  MatchWs W = match_layout(upds->d, upds->n_sub, upds->n_upd, ws);
+  MatchReq q{&I, upds, upd_ids, pairs, capacity, flags};
+  return match_indexed(q, W, count_out, false, st);
+}
+
+ddm_status ddm_match_pairs_indexed(const void* index, const ddm_regions* upds, const uint32_t* upd_ids,
+                                   ddm_pair* pairs, uint64_t capacity, uint64_t* count_out, uint32_t flags,
+                                   void* ws, size_t ws_bytes, cudaStream_t stream) {
+  if (!pairs && capacity) return DDM_ERR_INVALID_ARGUMENT;
+  ddm_pair dummy;
+  return indexed_common(index, upds, upd_ids, pairs ? pairs : &dummy, pairs ? capacity : 0, count_out, flags,
+                        ws, ws_bytes, stream);
+}
+
+ddm_status ddm_match_count_indexed(const void* index, const ddm_regions* upds, uint64_t* count_out, void* ws,
+                                   size_t ws_bytes, cudaStream_t stream) {
+  return indexed_common(index, upds, nullptr, nullptr, 0, count_out, 0, ws, ws_bytes, stream);
+}
+
+size_t ddm_sort_pairs_workspace_bytes(uint64_t k) {
+  Carver c(nullptr);
+  sort_scratch(c, k);
+  return c.used;
+}
+
+ddm_status ddm_sort_pairs(ddm_pair* pairs, uint64_t k, uint64_t n_sub, uint64_t n_upd, void* ws,
+                          size_t ws_bytes, cudaStream_t stream) {
+  if (k == 0) return DDM_OK;
+  if (!pairs || !aligned(pairs, 8) || !aligned(ws, 256)) return DDM_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < ddm_sort_pairs_workspace_bytes(k)) return DDM_ERR_WORKSPACE;
+  Carver c(ws);
+  SortScratch s = sort_scratch(c, k);
+  // canonical key (upd << 32) | sub: only the digits that can be non-zero
+  radix::PassList P{};
+  const int nb = bits_for(n_sub ? n_sub - 1 : 0), mb = bits_for(n_upd ? n_upd - 1 : 0);
+  for (int b = 0; b < nb; b += 8) { P.shift[P.n] = b; P.mask[P.n] = 255; ++P.n; }
+  for (int b = 32; b < 32 + mb; b += 8) { P.shift[P.n] = b; P.mask[P.n] = 255; ++P.n; }
+  if (P.n == 0) return DDM_OK;
+  uint64_t* keys = reinterpret_cast<uint64_t*>(pairs);
+  return radix_sort(keys, false, nullptr, keys, nullptr, k, P, s.hist[0], false, s, stream);
+}
+
+size_t ddm_radix_sort_workspace_bytes(uint64_t n) {
+  Carver c(nullptr);
+  sort_scratch(c, n);
+  return c.used;
+}
+
+ddm_status ddm_radix_sort_u64(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_out,
+                              uint32_t* vals_out, uint64_t n, int begin_bit, int end_bit, void* ws,
+                              size_t ws_bytes, cudaStream_t stream) {
+  if (n == 0) return DDM_OK;
+  if (n > DDM_MAX_REGIONS || !keys_in || !keys_out || begin_bit < 0 || end_bit > 64 || begin_bit >= end_bit)
+    return DDM_ERR_INVALID_ARGUMENT;
+  if ((end_bit - begin_bit + 7) / 8 > radix::kMaxPasses) return DDM_ERR_INVALID_ARGUMENT;
+  if (keys_in == keys_out || (vals_in && vals_in == vals_out)) return DDM_ERR_INVALID_ARGUMENT;
+  if (!aligned(ws, 256) || ws_bytes < ddm_radix_sort_workspace_bytes(n)) return DDM_ERR_WORKSPACE;
+  Carver c(ws);
+  SortScratch s = sort_scratch(c, n);
+  radix::PassList P{};
+  for (int b = begin_bit; b < end_bit; b += 8) {
+    const int w = end_bit - b < 8 ? end_bit - b : 8;
+    P.shift[P.n] = b;
+    P.mask[P.n] = (1u << w) - 1;
+    ++P.n;
+  }
+  return radix_sort(keys_in, false, vals_in, keys_out, vals_out, n, P, s.hist[0], false, s, stream);
+}
+
+ddm_status ddm_encode_keys(const double* x, uint64_t* keys, uint64_t n, cudaStream_t stream) {
+  if (n == 0) return DDM_OK;
+  if (!x || !keys) return DDM_ERR_INVALID_ARGUMENT;
+  DDM_LAUNCH(encode_kernel<<<grid_for(n, 256, 8), 256, 0, stream>>>(x, keys, n));
+  return check_launch();
+}
+
+const char* ddm_status_string(ddm_status s) {
+  switch (s) {
+    case DDM_OK: return "DDM_OK";
+    case DDM_ERR_INVALID_ARGUMENT: return "DDM_ERR_INVALID_ARGUMENT";
+    case DDM_ERR_NONFINITE: return "DDM_ERR_NONFINITE";
+    case DDM_ERR_INVERTED_INTERVAL: return "DDM_ERR_INVERTED_INTERVAL";
+    case DDM_ERR_CAPACITY: return "DDM_ERR_CAPACITY";
+    case DDM_ERR_WORKSPACE: return "DDM_ERR_WORKSPACE";
+    case DDM_ERR_CUDA: return "DDM_ERR_CUDA";
+  }
+  return "DDM_ERR_UNKNOWN";
+}
+
+int ddm_last_cuda_error(void) { return g_last_cuda.load(); }
+
+uint64_t ddm_kernel_launch_count(void) { return g_launches.load(); }
+
+const char* ddm_build_info(void) {
+  return "libddm sm_100a onesweep-radix(8x8b, 4096/tile) count_scan(2048/tile) emit(thread|warp)";
+}
+
+}  // extern "C"

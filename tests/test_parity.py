@@ -1,0 +1,378 @@
+"""GPU parity: libddm (through the C ABI) vs the CPU oracle, bit-exact.
+
+Endpoints are compared exactly on both sides, so there is no tolerance: the
+GPU pair count must equal the oracle's and the GPU pair list, canonicalised
+as ascending (upd << 32) | sub, must be byte-equal to the oracle's
+(SURVEY §8(c) parity rule).  All inputs are seeded and synthetic.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_1703_06680_b200 import ddm
+from paper_1703_06680_b200 import workload as wl
+from tests.helpers import cuda, gpu_args, raw_words, words_of
+
+EMIT_FLAGS = [ddm.DDM_EMIT_AUTO, ddm.DDM_EMIT_FORCE_THREAD, ddm.DDM_EMIT_FORCE_WARP]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA GPU")
+    ddm.load()
+
+
+def check_against(orc, sl, sh, ul, uh, flags=(0,), ref=None):
+    a = [np.ascontiguousarray(np.asarray(x, dtype=np.float64)) for x in (sl, sh, ul, uh)]
+    a = [x if x.ndim == 2 else x[None] for x in a]
+    if ref is None:
+        ref = orc.sbm_seq(*a)
+    g = [cuda(x) for x in a]
+    assert ddm.match_count(*g) == ref.size
+    first = None
+    for f in flags:
+        p = ddm.match_pairs(*g, flags=f)
+        assert p.shape[0] == ref.size
+        got = words_of(p)
+        assert np.array_equal(got, ref), f"flags={f}"
+        if first is None:
+            first = raw_words(p)
+        else:  # every emission path writes byte-identical output
+            assert np.array_equal(raw_words(p), first)
+    return ref
+
+
+# ------------------------------------------------------------ key encoding and sort
+
+def test_encode_keys_order_preserving():
+    vals = np.array([-np.finfo(np.float64).max, -1e300, -2.5, -1.0, -5e-324, -0.0, 0.0, 5e-324,
+                     2.2250738585072014e-308, 1.0, 1.0000000000000002, 3.0, 1e300,
+                     np.finfo(np.float64).max])
+    k = ddm.encode_keys(cuda(vals)).cpu().numpy().view(np.uint64)
+    assert k[5] == k[6]                       # -0.0 and +0.0 encode equally
+    assert np.all(np.diff(k[6:].astype(object)) > 0) and np.all(np.diff(k[:6].astype(object)) > 0)
+    rng = np.random.default_rng(0)
+    x = np.concatenate([rng.normal(0, 1e3, 5000), rng.uniform(-1, 1, 5000) * 1e-310, [0.0, -0.0] * 10])
+    kx = ddm.encode_keys(cuda(x)).cpu().numpy().view(np.uint64)
+    order_k = np.argsort(kx, kind="stable")
+    order_x = np.argsort(x + 0.0, kind="stable")
+    assert np.array_equal(x[order_k], x[order_x])
+
+
+@pytest.mark.parametrize("n", [1, 31, 4095, 4096, 4097, 12289, 100_003, 1_000_000])
+@pytest.mark.parametrize("spread", ["full", "dups"])
+def test_radix_sort_matches_stable_sort(n, spread):
+    rng = np.random.default_rng(n)
+    if spread == "full":
+        keys = rng.integers(0, 2**63, n, dtype=np.int64).view(np.uint64) * np.uint64(2) + rng.integers(0, 2, n).astype(np.uint64)
+    else:
+        keys = rng.integers(0, 7, n).astype(np.uint64) << np.uint64(40)
+    kt = torch.from_numpy(keys.view(np.int64)).cuda()
+    ko, vo = ddm.radix_sort_u64(kt)
+    ref = np.argsort(keys, kind="stable")
+    assert np.array_equal(ko.cpu().numpy().view(np.uint64), keys[ref])
+    assert np.array_equal(vo.cpu().numpy(), ref.astype(np.int32))
+
+
+@pytest.mark.parametrize("bits", [(0, 20), (8, 40), (32, 61)])
+def test_radix_sort_bit_ranges(bits):
+    rng = np.random.default_rng(bits[0])
+    keys = rng.integers(0, 2**62, 50_000, dtype=np.int64).view(np.uint64)
+    vals = rng.integers(0, 2**31, 50_000).astype(np.int32)
+    ko, vo = ddm.radix_sort_u64(torch.from_numpy(keys.view(np.int64)).cuda(), torch.from_numpy(vals).cuda(),
+                                bits[0], bits[1])
+    sub = (keys >> np.uint64(bits[0])) & np.uint64((1 << (bits[1] - bits[0])) - 1)
+    ref = np.argsort(sub, kind="stable")
+    assert np.array_equal(ko.cpu().numpy().view(np.uint64), keys[ref])
+    assert np.array_equal(vo.cpu().numpy(), vals[ref])
+
+
+# ------------------------------------------------------------ worked examples and edge cases
+
+@pytest.mark.parametrize("S,U,K", [
+    ([(0, 10)], [(2, 3)], 1),          # S:178 nested
+    ([(1, 2)], [(1, 2)], 1),           # S:129 identical
+    ([(5, 10)], [(10, 12)], 1),        # S:56 touching
+    ([(5, 5)], [(5, 9)], 1),           # S:77 point interval
+    ([(0, 1)], [(2, 3)], 0),           # S:55 disjoint
+    ([(-1, -0.0)], [(0.0, 1)], 1),     # -0.0 vs +0.0 (DESIGN reading R3)
+    ([(0.0, 0.0)], [(-0.0, -0.0)], 1),
+])
+def test_small_cases(orc, S, U, K):
+    sl, sh = [s[0] for s in S], [s[1] for s in S]
+    ul, uh = [u[0] for u in U], [u[1] for u in U]
+    ref = check_against(orc, sl, sh, ul, uh, flags=EMIT_FLAGS)
+    assert ref.size == K
+
+
+def test_fig1_instance(orc):
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fig1_instance.json")))
+    sl = np.array([[s[k][0] for s in g["sub"]] for k in range(2)])
+    sh = np.array([[s[k][1] for s in g["sub"]] for k in range(2)])
+    ul = np.array([[u[k][0] for u in g["upd"]] for k in range(2)])
+    uh = np.array([[u[k][1] for u in g["upd"]] for k in range(2)])
+    expect = np.array(sorted(((u - 1) << 32) | (s - 1) for s, u in g["expected_pairs_1based"]), dtype=np.uint64)
+    check_against(orc, sl, sh, ul, uh, flags=EMIT_FLAGS, ref=expect)
+
+
+def test_tie_storms(orc):
+    """Random instances with integer endpoints in {0..4} (every kind of tie)."""
+    rng = np.random.default_rng(7)
+    for _ in range(120):
+        n, m = rng.integers(1, 40, 2)
+        s = np.sort(rng.integers(0, 5, (2, n)), axis=0).astype(np.float64)
+        u = np.sort(rng.integers(0, 5, (2, m)), axis=0).astype(np.float64)
+        ref = orc.bf_pairs(s[0:1], s[1:2], u[0:1], u[1:2])
+        check_against(orc, s[0:1], s[1:2], u[0:1], u[1:2], flags=EMIT_FLAGS, ref=ref)
+
+
+def test_extreme_magnitudes(orc):
+    rng = np.random.default_rng(3)
+    v = np.concatenate([rng.uniform(-1, 1, 300) * 1e308, rng.uniform(-1, 1, 300) * 5e-324 * 1000,
+                        [-5e-324, 5e-324, 0.0, -0.0, 1e308, -1e308]])
+    lo = rng.choice(v, 800)
+    ln = rng.choice([0.0, 5e-324, 1e-310, 1.0, 1e300], 800)
+    hi = np.where(lo + ln >= lo, lo + ln, lo)
+    hi = np.where(np.isfinite(hi), hi, lo)
+    ref = orc.bf_pairs(lo[None, :400], hi[None, :400], lo[None, 400:], hi[None, 400:])
+    check_against(orc, lo[:400], hi[:400], lo[400:], hi[400:], flags=EMIT_FLAGS, ref=ref)
+
+
+def test_duplicates_all_overlap(orc):
+    n = 2000
+    z = np.zeros(n)
+    o = np.ones(n)
+    g = [cuda(x) for x in (z, o, z, o)]
+    assert ddm.match_count(*g) == n * n
+    p = ddm.match_pairs(*g)
+    w = words_of(p)
+    assert w.size == n * n and np.array_equal(w, orc.bf_pairs(z[None], o[None], z[None], o[None]))
+
+
+def test_asymmetric(orc):
+    rng = np.random.default_rng(11)
+    lo = rng.uniform(0, 1e6, 1_000_000)
+    hi = lo + 10.0
+    one_lo, one_hi = np.array([5e5]), np.array([5e5 + 3e3])
+    check_against(orc, one_lo, one_hi, lo, hi, ref=orc.bf_pairs(one_lo[None], one_hi[None], lo[None], hi[None]))
+    check_against(orc, lo, hi, one_lo, one_hi, ref=orc.bf_pairs(lo[None], hi[None], one_lo[None], one_hi[None]))
+
+
+def test_empty_sides():
+    e = cuda(np.zeros(0))
+    x = cuda(np.array([1.0, 2.0]))
+    assert ddm.match_count(e, e, x, x) == 0
+    assert ddm.match_count(x, x, e, e) == 0
+    assert ddm.match_pairs(x, x, e, e).shape[0] == 0
+
+
+def test_long_intervals(orc):
+    """1% of subscriptions span the whole domain (exercises the block-max skips)."""
+    rng = np.random.default_rng(21)
+    w = wl.uniform(20_000, 20_000, 1e6, 50.0, 1, seed=5)
+    sl, sh = w.sub_lo.copy(), w.sub_hi.copy()
+    idx = rng.choice(w.n, w.n // 100, replace=False)
+    sl[0, idx] = 0.0
+    sh[0, idx] = 1e6
+    check_against(orc, sl, sh, w.upd_lo, w.upd_hi, flags=EMIT_FLAGS)
+    # a single long interval at the very start, rest short
+    sl2, sh2 = w.sub_lo.copy(), w.sub_hi.copy()
+    sl2[0, 0], sh2[0, 0] = -1.0, 2e6
+    check_against(orc, sl2, sh2, w.upd_lo, w.upd_hi, flags=EMIT_FLAGS)
+
+
+def test_clamped_mixture_ties(orc):
+    """c5-style clustered lower bounds with clamping -> point masses (ties)."""
+    rng = np.random.default_rng(4)
+    L, l = 1e6, 5.0
+    c = rng.uniform(0, L, 8)
+    lo = np.clip(rng.normal(c[rng.integers(0, 8, 60_000)], 3e4), 0, L - l)
+    hi = lo + rng.uniform(0.5 * l, 1.5 * l, lo.size)
+    check_against(orc, lo[:30_000], hi[:30_000], lo[30_000:], hi[30_000:], flags=EMIT_FLAGS)
+
+
+# ------------------------------------------------------------ BASELINE configs
+
+def test_c1_full(orc):
+    w = wl.make("c1")
+    ref = orc.bf_pairs(w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi)
+    assert np.array_equal(orc.sbm_seq(w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi), ref)
+    check_against(orc, w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi, flags=EMIT_FLAGS, ref=ref)
+
+
+@pytest.mark.parametrize("alpha", [0.01, 1.0, 100.0])
+def test_ragged_sizes(orc, alpha):
+    """Sizes that span several sort/count/emit tiles and leave ragged tails."""
+    for n, m in [(4097, 12289), (9000, 2049), (33_333, 30_001)]:
+        N = n + m
+        w = wl.uniform(n, m, 1e6, wl.side_length(N, 1e6, alpha, 1), 1, seed=n + m)
+        check_against(orc, w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi, flags=EMIT_FLAGS)
+
+
+def test_c2_full(orc):
+    w = wl.make("c2")
+    g = gpu_args(w)
+    K = ddm.match_count(*g)
+    assert K == orc.rank_count(w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi)
+    ref = orc.sbm_seq(w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi)
+    assert ref.size == K
+    for f in EMIT_FLAGS:
+        p = ddm.match_pairs(*g, flags=f)
+        assert np.array_equal(words_of(p), ref)
+
+
+def _check_sampled_rows(orc, w, p, n_rows=400, seed=0):
+    """Rows of the GPU list for random update ids == brute force rows."""
+    rng = np.random.default_rng(seed)
+    rows = np.sort(rng.choice(w.m, size=min(n_rows, w.m), replace=False))
+    ref, counts = orc.bf_rows(w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi, rows)
+    pw = words_of(p)
+    upd = (pw >> np.uint64(32)).astype(np.int64)
+    lo = np.searchsorted(upd, rows, side="left")
+    hi = np.searchsorted(upd, rows, side="right")
+    got = np.concatenate([pw[a:b] for a, b in zip(lo, hi)]) if rows.size else pw[:0]
+    assert np.array_equal(hi - lo, counts)
+    assert np.array_equal(got, ref)
+
+
+def test_c3_full_sampled(orc):
+    """c3 at full size (N = 1e8), the bench configuration: K against the
+    rank identity over numpy sorts, sampled rows against brute force, and
+    list invariants (no duplicate, every pair overlaps)."""
+    w = wl.make("c3")
+    g = gpu_args(w)
+    p = ddm.match_pairs(*g)
+    K = p.shape[0]
+    assert K == orc.rank_count(w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi)
+    # invariants on the device
+    s, u = p[:, 0].long(), p[:, 1].long()
+    assert bool(((g[0][0][s] <= g[3][0][u]) & (g[2][0][u] <= g[1][0][s])).all())
+    wds = torch.sort((u << 32) | s).values
+    assert bool((wds[1:] > wds[:-1]).all())
+    _check_sampled_rows(orc, w, p)
+
+
+def test_c4_scaled(orc):
+    """d = 3 (c4 recipe) at a size the oracle finishes quickly."""
+    w = wl.uniform(20_000, 20_000, 1e4, wl.side_length(40_000, 1e4, 1.0, 3) * 3.0, 3, seed=3)
+    ref = orc.sbm_seq(w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi)
+    assert np.array_equal(ref, orc.bf_pairs(w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi))
+    check_against(orc, w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi, flags=EMIT_FLAGS, ref=ref)
+
+
+@pytest.mark.parametrize("d", [2, 3, 5])
+def test_dd_tie_storms(orc, d):
+    rng = np.random.default_rng(d)
+    for _ in range(40):
+        n, m = rng.integers(1, 30, 2)
+        s = np.sort(rng.integers(0, 4, (2, d, n)), axis=0).astype(np.float64)
+        u = np.sort(rng.integers(0, 4, (2, d, m)), axis=0).astype(np.float64)
+        ref = orc.bf_pairs(s[0], s[1], u[0], u[1])
+        assert np.array_equal(orc.sbm_dd_literal(s[0], s[1], u[0], u[1]), ref)
+        check_against(orc, s[0], s[1], u[0], u[1], flags=EMIT_FLAGS, ref=ref)
+
+
+def test_c5_scaled(orc):
+    w = wl.clustered(400_000, 400_000, 1e9, 0.01 * 2500, seed=4)
+    check_against(orc, w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi, flags=EMIT_FLAGS)
+
+
+# ------------------------------------------------------------ errors and contract
+
+def test_validation_errors():
+    x = np.linspace(0, 10, 100)
+    for bad, code in [(np.nan, 2), (np.inf, 2), (-np.inf, 2)]:
+        y = x.copy()
+        y[37] = bad
+        with pytest.raises(ddm.DDMError) as e:
+            ddm.match_pairs(cuda(y), cuda(x + 1), cuda(x), cuda(x + 1))
+        assert e.value.status == code
+        with pytest.raises(ddm.DDMError) as e:
+            ddm.match_count(cuda(x), cuda(x + 1), cuda(x), cuda(np.where(np.arange(100) == 5, bad, x + 1)))
+        assert e.value.status == code
+    inv = x + 1
+    inv[50] = x[50] - 1
+    with pytest.raises(ddm.DDMError) as e:
+        ddm.match_pairs(cuda(x), cuda(inv), cuda(x), cuda(x + 1))
+    assert e.value.status == 3
+    # other dimensions are validated too (d = 2)
+    lo2 = np.stack([x, x])
+    hi2 = np.stack([x + 1, inv])
+    with pytest.raises(ddm.DDMError) as e:
+        ddm.match_count(cuda(lo2), cuda(hi2), cuda(lo2), cuda(lo2 + 1))
+    assert e.value.status == 3
+
+
+def test_capacity_and_workspace():
+    import ctypes
+    L = ddm.load()
+    x = cuda(np.zeros(100))
+    y = cuda(np.ones(100))
+    r, keep = ddm.regions(x, y, x, y)
+    ws = torch.empty(L.ddm_workspace_bytes(1, 100, 100, 1), dtype=torch.uint8, device="cuda")
+    K = ctypes.c_uint64(0)
+    out = torch.empty((50, 2), dtype=torch.int32, device="cuda")
+    st = L.ddm_match_pairs(ctypes.byref(r), out.data_ptr(), 50, ctypes.byref(K), 0, ws.data_ptr(), ws.numel(),
+                           torch.cuda.current_stream().cuda_stream)
+    assert st == 4 and K.value == 10_000
+    st = L.ddm_match_pairs(ctypes.byref(r), out.data_ptr(), 50, ctypes.byref(K), 0, ws.data_ptr(), 1024,
+                           torch.cuda.current_stream().cuda_stream)
+    assert st == 5
+    r.d = 0
+    assert L.ddm_match_count(ctypes.byref(r), ctypes.byref(K), ws.data_ptr(), ws.numel(), None) == 1
+    r.d = 9
+    assert L.ddm_match_count(ctypes.byref(r), ctypes.byref(K), ws.data_ptr(), ws.numel(), None) == 1
+    r.d = 1
+    r.n_sub = 2**31
+    assert L.ddm_match_count(ctypes.byref(r), ctypes.byref(K), ws.data_ptr(), ws.numel(), None) == 1
+    r.n_sub = 100
+    r.sub_lo[0] = None
+    assert L.ddm_match_count(ctypes.byref(r), ctypes.byref(K), ws.data_ptr(), ws.numel(), None) == 1
+
+
+def test_deterministic_output():
+    w = wl.make("c2", scale=0.1)
+    g = gpu_args(w)
+    a = ddm.match_pairs(*g)
+    b = ddm.match_pairs(*g)
+    assert torch.equal(a, b)
+
+
+def test_sort_pairs_canonical(orc):
+    w = wl.make("c2", scale=0.2)
+    g = gpu_args(w)
+    p = ddm.match_pairs(*g, sort=True)
+    got = raw_words(p)
+    assert np.all(np.diff(got.astype(np.int64)) > 0)
+    assert np.array_equal(got, orc.sbm_seq(w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi))
+
+
+# ------------------------------------------------------------ index / shards (multi-GPU analogue)
+
+def test_indexed_shards_equal_single(orc):
+    """G-invariance: partition updates by coordinate slab, match each slab
+    against the broadcastable subscription index with global ids, and the
+    concatenation equals the single-call list."""
+    w = wl.make("c2", scale=0.2)
+    g = gpu_args(w)
+    ref = words_of(ddm.match_pairs(*g))
+    idx = ddm.sub_index_build(g[0], g[1])
+    for G in (1, 2, 3, 8):
+        cuts = np.quantile(w.sub_lo[0], np.arange(1, G) / G)
+        slab = np.searchsorted(cuts, w.upd_lo[0], side="right")
+        parts = []
+        total = 0
+        for r in range(G):
+            ids = np.nonzero(slab == r)[0]
+            ul, uh = cuda(w.upd_lo[:, ids]), cuda(w.upd_hi[:, ids])
+            idt = torch.from_numpy(ids.astype(np.int32)).cuda()
+            p = ddm.match_pairs_indexed(idx, w.n, ul, uh, upd_ids=idt)
+            total += ddm.match_count_indexed(idx, w.n, ul, uh)
+            parts.append(words_of(p))
+        got = np.sort(np.concatenate(parts))
+        assert total == ref.size
+        assert np.array_equal(got, ref), G
