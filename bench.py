@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""bench.py -- B200 DDM sort-based matching benchmark (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ddm|reference] [--config c3]
+
+A step is one pass of the whole hot path (validate +
+encode, sort Slo/Shi/Ulo, gathers, rank-difference counts, scan, chunked
+sweep + pair emission) over one synthetic BASELINE workload already resident
+in HBM, through the C ABI (`ddm_match_pairs`), with the pair list written to a
+preallocated device buffer.  Default workload: BASELINE configs[2] = c3
+(d=1, n=m=5e7, N=1e8), the configuration the north star's roofline target is
+quoted on.  Rank 0 prints one JSON line.
+
+N > 1 (torchrun, one process per GPU, NCCL): updates are sharded by
+coordinate slab; each step rank 0 builds the subscription index, broadcasts
+it (NCCL over NVLink), every rank matches its slab, and the count is
+all-reduced.  Total work is fixed -> "scaling": "strong".
+
+--impl reference: the CPU oracle (oracle/, Alg. 5+6 Parallel-SBM on all host
+cores) on a bounded window sample of the same workload (the reference arm of
+this tier; rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "regions matched/sec and pairs emitted/sec per GPU; % of HBM roofline, 1/2/4/8 B200"
+FALLBACK_HBM_GBS = 6650.0
+CPU_SAMPLE_FRAC = {"c1": 1.0, "c2": 0.5, "c3": 0.04, "c4": 0.02, "c5": 0.004}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ddm", choices=["ddm", "reference"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling of SM clocks / throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def workload_config(w, extra=None):
+    d = {"workload": w.name, "d": w.d, "n_sub": w.n, "n_upd": w.m, "L": w.L, "l": w.l, "seed": w.seed,
+         "coords": "float64", "mode": "pairs (list)", "l2": "inputs larger than L2 (no flush needed)"
+         if 32 * w.d * (w.n + w.m) > 126e6 else "L2 flushed between steps"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+# ---------------------------------------------------------------- reference arm (CPU oracle)
+
+def cpu_sample(w, frac):
+    from paper_1703_06680_b200 import workload as wl
+    return wl.window_sample(w, frac) if frac < 1.0 else w
+
+
+def time_oracle(sample, reps=1):
+    import oracle
+    P = oracle.max_threads()
+    best = None
+    K = 0
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        pairs = oracle.par_sbm(sample.sub_lo, sample.sub_hi, sample.upd_lo, sample.upd_hi, P=P, canonicalize=False)
+        dt = time.perf_counter() - t0
+        K = pairs.size
+        best = dt if best is None else min(best, dt)
+    return best, K, P
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    from paper_1703_06680_b200 import workload as wl
+    w = wl.make(args.config)
+    frac = CPU_SAMPLE_FRAC[args.config]
+    s = cpu_sample(w, frac)
+    import oracle
+    P = oracle.max_threads()
+    for _ in range(args.warmup):
+        time_oracle(s)
+    times, K = [], 0
+    for _ in range(args.steps):
+        dt, K, P = time_oracle(s)
+        times.append(dt)
+    t = float(np.sum(times))
+    regions = (s.n + s.m) * args.steps
+    val = regions / t
+    sample = f"{s.name}: regions with dim-0 lower bound in [0, {frac:g} L) ({s.n + s.m} regions, K={K})"
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "regions/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "pairs_per_s": K * args.steps / t,
+            "config": workload_config(w, {"parallelism": f"OpenMP x{P} (Alg. 5+6)", "sample": sample}),
+            "cpu_baseline": {"value": val, "unit": "regions/s", "cores": P, "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": "regions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+
+def run_ddm(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1703_06680_b200 import ddm, workload as wl
+    from paper_1703_06680_b200 import dist as ddist
+
+    rank, world, local = env_rank()
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    ddm.load()
+    w = wl.make(args.config)
+    hbm_peak, peak_src = peaks()
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    if world == 1:
+        g = [torch.from_numpy(a).to(dev) for a in (w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi)]
+        M = ddm.Matcher(w.d, w.n, w.m, dev)
+        K = M.count(*g)
+        out = torch.empty((max(K, 1), 2), dtype=torch.int32, device=dev)
+
+        def step():
+            return M.pairs_into(out, *g)
+    else:
+        cuts = ddist.slab_cuts(w.upd_lo[0], world)
+        ul, uh, ids = ddist.local_updates(w.upd_lo, w.upd_hi, rank, world, cuts)
+        sub = [torch.from_numpy(a).to(dev) for a in (w.sub_lo, w.sub_hi)] if rank == 0 else [None, None]
+        upd = [torch.from_numpy(a).to(dev) for a in (ul, uh)]
+        uid = torch.from_numpy(ids).to(dev)
+        # capacity from an untimed count against a freshly built index
+        SM0 = ddist.ShardedMatcher(w.d, w.n, ul.shape[1], 1, dev)
+        if rank == 0:
+            SM0.build_index(*sub)
+        dist.broadcast(SM0.index, src=0)
+        cap = ddm.match_count_indexed(SM0.index, w.n, *upd)
+        del SM0
+        SM = ddist.ShardedMatcher(w.d, w.n, ul.shape[1], cap, dev)
+
+        def step():
+            return SM.step(sub[0], sub[1], upd[0], upd[1], uid).k_total
+
+    for _ in range(max(args.warmup, 0)):
+        K = step()
+    sync_all()
+    clocks = Clocks(local)
+    clocks.start()
+    l0 = ddm.launch_count()
+    ddm.profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sync_all()
+    e0.record(stream)
+    for _ in range(args.steps):
+        K = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    prof = ddm.profile_read()
+    ddm.profile_enable(False)
+    launches = ddm.launch_count() - l0
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        lt = torch.tensor([launches], dtype=torch.int64, device=dev)
+        dist.all_reduce(lt, op=dist.ReduceOp.SUM)
+        launches = int(lt.item())
+    ms_step = ms / args.steps
+    regions = w.n + w.m
+    value = regions / (ms_step * 1e-3)
+
+    # roofline of the dominant kernel class (measured live above)
+    dom = max(prof.items(), key=lambda kv: kv[1]["total_ms"]) if prof else None
+    roof = None
+    phases = {}
+    if dom:
+        name, st = dom
+        avg_ms = st["total_ms"] / st["launches"]
+        bytes_per_launch = st["bytes"] / st["launches"]
+        achieved = bytes_per_launch / (avg_ms * 1e-3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get(args.config, {}).get(name)
+        roof = {"bound": "hbm", "kernel": name, "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(achieved / hbm_peak, 4), "traffic": traffic, "peak_source": peak_src,
+                "bytes_per_launch": bytes_per_launch, "avg_launch_ms": round(avg_ms, 4),
+                "share_of_step": round(st["total_ms"] / (ms_step * args.steps), 3)}
+        tot_bytes = sum(v["bytes"] for v in prof.values())
+        phases = {k: {"ms_per_step": round(v["total_ms"] / args.steps, 4), "launches_per_step": v["launches"] / args.steps,
+                      "GBps": round(v["bytes"] / (v["total_ms"] * 1e-3) / 1e9, 1) if v["total_ms"] else None}
+                  for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["total_ms"])}
+        pipeline_frac = tot_bytes / args.steps / (ms_step * 1e-3) / (hbm_peak * 1e9)
+        literal_floor = 16.0 * w.d * regions + 8.0 * K
+        phases_summary = {"pipeline_bytes_per_step": tot_bytes / args.steps,
+                          "pipeline_frac_of_peak": round(pipeline_frac, 4),
+                          "literal_floor_bytes": literal_floor,
+                          "literal_floor_frac": round(literal_floor / (ms_step * 1e-3) / (hbm_peak * 1e9), 4)}
+    else:
+        phases_summary = {}
+
+    # e2e through the public API with host buffers (N=1): H2D inputs, match, D2H pairs
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        host = [torch.from_numpy(a).pin_memory() for a in (w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi)]
+        dbuf = [torch.empty_like(h, device=dev) for h in host]
+        hout = torch.empty((max(K, 1), 2), dtype=torch.int32).pin_memory()
+        h2d = sum(h.numel() * 8 for h in host)
+        d2h = K * 8
+
+        def e2e_step():
+            for d_, h_ in zip(dbuf, host):
+                d_.copy_(h_, non_blocking=True)
+            k = M.pairs_into(out, *dbuf)
+            hout[:k].copy_(out[:k], non_blocking=True)
+            return k
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_e2e = max(3, min(args.steps, 5))
+        a.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        e_ms = a.elapsed_time(b) / n_e2e
+        e2e = {"value": regions / (e_ms * 1e-3), "unit": "regions/s", "ms_per_step": round(e_ms, 3),
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "api": "paper_1703_06680_b200.ddm.Matcher.pairs_into (ddm_match_pairs) on pinned host buffers"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        frac = CPU_SAMPLE_FRAC[args.config]
+        s = cpu_sample(w, frac)
+        dt, ks, P = time_oracle(s)
+        cpu = {"value": (s.n + s.m) / dt, "unit": "regions/s", "cores": P, "kind": "oracle",
+               "sample": f"{s.name}: regions with dim-0 lower bound in [0, {frac:g} L) ({s.n + s.m} regions, "
+                         f"K={ks}); oracle.par_sbm (Alg. 5+6, list mode), {dt:.2f} s"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "regions/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                "config": workload_config(w, {"parallelism": "single GPU" if world == 1 else
+                                              f"updates sharded by slab x{world}, sub index broadcast (NCCL)",
+                                              "K": K, "timing": "CUDA events on the launching stream, max over ranks"}),
+                "pairs_per_s": K / (ms_step * 1e-3), "regions_per_s_per_gpu": value / world,
+                "roofline": roof, "pipeline": phases_summary, "phases": phases, "cpu_baseline": cpu, "e2e": e2e,
+                "clocks": clk, "gpu_launches": launches, "build": ddm.build_info()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ddm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -146,6 +146,20 @@ ddm_status ddm_radix_sort_u64(const uint64_t *keys_in, const uint32_t *vals_in,
  * bits of negatives.  Device arrays of length n. */
 ddm_status ddm_encode_keys(const double *x, uint64_t *keys, uint64_t n, cudaStream_t stream);
 
+/* Per-kernel-class timing with CUDA events recorded on the launching stream
+ * around every library launch while enabled (enable(1) also resets).
+ * ddm_profile_read synchronises the recorded events and fills up to cap
+ * entries; returns the number of kernel classes (or -1 on a CUDA error).
+ * bytes = the algorithmic DRAM bytes of those launches. */
+typedef struct {
+    char name[32];
+    uint64_t launches;
+    double total_ms;
+    double bytes;
+} ddm_kernel_stat;
+void ddm_profile_enable(int on);
+int ddm_profile_read(ddm_kernel_stat *out, int cap);
+
 const char *ddm_status_string(ddm_status s);
 int ddm_last_cuda_error(void);          /* last cudaError_t seen by the library */
 uint64_t ddm_kernel_launch_count(void); /* kernels launched by this process so far */

@@ -11,7 +11,11 @@
 // The subscription half forms the byte-copyable "index" (multi-GPU: built by
 // one rank and broadcast).
 #include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/ddm.h"
@@ -26,10 +30,53 @@ namespace {
 std::atomic<uint64_t> g_launches{0};
 std::atomic<int> g_last_cuda{0};
 
-#define DDM_LAUNCH(...)                        \
-  do {                                         \
-    __VA_ARGS__;                               \
-    g_launches.fetch_add(1, std::memory_order_relaxed); \
+// Optional per-launch timing with CUDA events on the launching stream
+// (ddm_profile_enable / ddm_profile_read): bench.py uses it to measure the
+// dominant kernel's average duration live inside its timed region.
+struct ProfRec {
+  const char* name;
+  double bytes;
+  int e0, e1;
+};
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<ProfRec> recs;
+  int next = 0;
+  int take() {
+    if (next >= (int)ev.size()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return -1;
+      ev.push_back(e);
+    }
+    return next++;
+  }
+} g_prof;
+std::mutex g_prof_mu;
+
+inline int prof_begin(cudaStream_t st) {
+  if (!g_prof.on) return -1;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  const int e = g_prof.take();
+  if (e >= 0) cudaEventRecord(g_prof.ev[e], st);
+  return e;
+}
+inline void prof_end(const char* name, double bytes, cudaStream_t st, int e0) {
+  if (e0 < 0) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  const int e1 = g_prof.take();
+  if (e1 < 0) return;
+  cudaEventRecord(g_prof.ev[e1], st);
+  g_prof.recs.push_back({name, bytes, e0, e1});
+}
+
+// NAME: kernel class; BYTES: algorithmic DRAM bytes of this launch
+#define DDM_LAUNCH(NAME, BYTES, ST, ...)                  \
+  do {                                                    \
+    const int e0_ = prof_begin(ST);                       \
+    __VA_ARGS__;                                          \
+    prof_end(NAME, (double)(BYTES), ST, e0_);             \
+    g_launches.fetch_add(1, std::memory_order_relaxed);   \
   } while (0)
 
 #define DDM_CUDA(call)                                   \
@@ -152,14 +199,15 @@ struct Misc {  // device-side results read back with one copy
 struct MatchWs {
   uint64_t* ulo_key;
   uint32_t* ulo_id;
-  uint64_t* uhi;
   uint32_t* r_lo;
   uint32_t* r_b;
   uint64_t* off;
+  uint32_t* cnt0;   // dim-0 counts
   uint32_t* cnt;    // d > 1
   uint32_t* fstab;  // d > 1
   uint64_t* offd;   // d > 1
   uint64_t* scan_status;
+  uint64_t* part;
   uint32_t* scan_counter;
   Misc* misc;
   SortScratch sort;
@@ -172,12 +220,13 @@ MatchWs match_layout(uint32_t d, uint64_t n_sub, uint64_t m, void* base) {
   W.misc = c.take<Misc>(1);
   W.scan_counter = c.take<uint32_t>(8);
   W.scan_status = c.take<uint64_t>(m / match::kCountTile + 2);
+  W.part = c.take<uint64_t>(4 * (m / match::kCountTile + 2));
   W.ulo_key = c.take<uint64_t>(m);
   W.ulo_id = c.take<uint32_t>(m);
-  W.uhi = c.take<uint64_t>(m);
   W.r_lo = c.take<uint32_t>(m);
   W.r_b = c.take<uint32_t>(m);
   W.off = c.take<uint64_t>(m + 1);
+  W.cnt0 = c.take<uint32_t>(m);
   if (d > 1) {
     W.cnt = c.take<uint32_t>(m);
     W.fstab = c.take<uint32_t>(m);
@@ -190,19 +239,62 @@ MatchWs match_layout(uint32_t d, uint64_t n_sub, uint64_t m, void* base) {
 
 // ------------------------------------------------------------ radix sort driver
 
-template <typename K>
-void set_smem_attr(K kernel) {
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(radix::PassSmem));
+int g_radix_items = 0;  // items per thread of the onesweep pass (env DDM_RADIX_ITEMS)
+
+int radix_items() {
+  if (!g_radix_items) {
+    const char* e = getenv("DDM_RADIX_ITEMS");
+    int v = e ? atoi(e) : 0;
+    g_radix_items = (v == 8 || v == 12 || v == 16) ? v : 8;
+  }
+  return g_radix_items;
+}
+
+template <int ITEMS, bool KV, bool F64>
+void set_attr() {
+  cudaFuncSetAttribute(radix::onesweep_kernel<ITEMS, KV, F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(radix::PassSmem<ITEMS, KV>));
+}
+
+template <int ITEMS>
+void set_attrs_items() {
+  set_attr<ITEMS, true, true>();
+  set_attr<ITEMS, true, false>();
+  set_attr<ITEMS, false, true>();
+  set_attr<ITEMS, false, false>();
 }
 
 void init_attrs_once() {
   static bool done = false;
   if (done) return;
-  set_smem_attr(radix::onesweep_kernel<true, true>);
-  set_smem_attr(radix::onesweep_kernel<true, false>);
-  set_smem_attr(radix::onesweep_kernel<false, true>);
-  set_smem_attr(radix::onesweep_kernel<false, false>);
+  set_attrs_items<8>();
+  set_attrs_items<12>();
+  set_attrs_items<16>();
+  cudaFuncSetAttribute(match::count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(match::CountSmem));
+  cudaFuncSetAttribute(match::emit_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(match::ChunkSmem));
+  if (const char* e = getenv("DDM_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(e));
   done = true;
+}
+
+template <int ITEMS>
+void launch_pass(bool kv, bool f64, uint64_t tiles, cudaStream_t st, const void* ki, const uint32_t* vi,
+                 uint64_t* ko, uint32_t* vo, uint64_t n, int shift, uint32_t mask, const uint32_t* starts,
+                 uint32_t* status, uint32_t* counter) {
+  dim3 g((unsigned)tiles);
+  if (kv && f64)
+    radix::onesweep_kernel<ITEMS, true, true><<<g, radix::kThreads, sizeof(radix::PassSmem<ITEMS, true>), st>>>(
+        ki, vi, ko, vo, n, shift, mask, starts, status, counter);
+  else if (kv)
+    radix::onesweep_kernel<ITEMS, true, false><<<g, radix::kThreads, sizeof(radix::PassSmem<ITEMS, true>), st>>>(
+        ki, vi, ko, vo, n, shift, mask, starts, status, counter);
+  else if (f64)
+    radix::onesweep_kernel<ITEMS, false, true><<<g, radix::kThreads, sizeof(radix::PassSmem<ITEMS, false>), st>>>(
+        ki, vi, ko, vo, n, shift, mask, starts, status, counter);
+  else
+    radix::onesweep_kernel<ITEMS, false, false><<<g, radix::kThreads, sizeof(radix::PassSmem<ITEMS, false>), st>>>(
+        ki, vi, ko, vo, n, shift, mask, starts, status, counter);
 }
 
 inline unsigned grid_for(uint64_t n, int threads, int per_sm) {
@@ -231,14 +323,14 @@ ddm_status radix_sort(const void* src, bool src_f64, const uint32_t* vals_in, ui
   if (!hist_ready) {
     DDM_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * radix::kMaxPasses * radix::kRadix, st));
     if (src_f64)
-      DDM_LAUNCH(radix::hist_kernel<true><<<grid_for(n, 512, 4), 512, 0, st>>>(src, n, P, hist));
+      DDM_LAUNCH("radix_hist", 8.0 * n, st, radix::hist_kernel<true><<<grid_for(n, 512, 4), 512, 0, st>>>(src, n, P, hist));
     else
-      DDM_LAUNCH(radix::hist_kernel<false><<<grid_for(n, 512, 4), 512, 0, st>>>(src, n, P, hist));
+      DDM_LAUNCH("radix_hist", 8.0 * n, st, radix::hist_kernel<false><<<grid_for(n, 512, 4), 512, 0, st>>>(src, n, P, hist));
     DDM_TRY(check_launch());
   }
-  DDM_LAUNCH(radix::bin_start_kernel<<<P.n, radix::kRadix, 0, st>>>(hist, s.starts));
+  DDM_LAUNCH("radix_bin_start", 0, st, radix::bin_start_kernel<<<P.n, radix::kRadix, 0, st>>>(hist, s.starts));
   DDM_TRY(check_launch());
-  const uint64_t tiles = radix::num_tiles(n);
+  const uint64_t tiles = radix::num_tiles(n, radix_items());
   const bool kv = vals_out != nullptr;
   const void* cur_k = src;
   const uint32_t* cur_v = vals_in;
@@ -253,29 +345,24 @@ ddm_status radix_sort(const void* src, bool src_f64, const uint32_t* vals_in, ui
     }
   }
   DDM_CUDA(cudaMemsetAsync(s.counters, 0, sizeof(uint32_t) * radix::kMaxPasses, st));
-  const size_t smem = sizeof(radix::PassSmem);
+  const int items = radix_items();
   for (int p = 0; p < P.n; ++p) {
     const bool to_out = ((P.n - 1 - p) % 2) == 0;
     uint64_t* dk = to_out ? keys_out : s.alt_keys;
     uint32_t* dv = kv ? (to_out ? vals_out : s.alt_vals) : nullptr;
     DDM_CUDA(cudaMemsetAsync(s.status, 0, sizeof(uint32_t) * radix::kRadix * tiles, st));
     const uint32_t* ph = s.starts + p * radix::kRadix;
-    dim3 g((unsigned)tiles);
-    if (kv) {
-      if (cur_f64)
-        DDM_LAUNCH(radix::onesweep_kernel<true, true><<<g, radix::kThreads, smem, st>>>(
-            cur_k, nullptr, dk, dv, n, P.shift[p], P.mask[p], ph, s.status, s.counters + p));
-      else
-        DDM_LAUNCH(radix::onesweep_kernel<true, false><<<g, radix::kThreads, smem, st>>>(
-            cur_k, cur_v, dk, dv, n, P.shift[p], P.mask[p], ph, s.status, s.counters + p));
-    } else {
-      if (cur_f64)
-        DDM_LAUNCH(radix::onesweep_kernel<false, true><<<g, radix::kThreads, smem, st>>>(
-            cur_k, nullptr, dk, nullptr, n, P.shift[p], P.mask[p], ph, s.status, s.counters + p));
-      else
-        DDM_LAUNCH(radix::onesweep_kernel<false, false><<<g, radix::kThreads, smem, st>>>(
-            cur_k, nullptr, dk, nullptr, n, P.shift[p], P.mask[p], ph, s.status, s.counters + p));
-    }
+    const char* pname = kv ? (cur_f64 ? "onesweep_kv_f64" : "onesweep_kv") : (cur_f64 ? "onesweep_k_f64" : "onesweep_k");
+    const double pbytes = (double)n * ((cur_f64 ? 8.0 : 8.0 + (kv && cur_v ? 4.0 : 0.0)) + 8.0 + (kv ? 4.0 : 0.0));
+    if (items == 16)
+      DDM_LAUNCH(pname, pbytes, st, launch_pass<16>(kv, cur_f64, tiles, st, cur_k, cur_v, dk, dv, n, P.shift[p], P.mask[p], ph,
+                                                    s.status, s.counters + p));
+    else if (items == 12)
+      DDM_LAUNCH(pname, pbytes, st, launch_pass<12>(kv, cur_f64, tiles, st, cur_k, cur_v, dk, dv, n, P.shift[p], P.mask[p], ph,
+                                                    s.status, s.counters + p));
+    else
+      DDM_LAUNCH(pname, pbytes, st, launch_pass<8>(kv, cur_f64, tiles, st, cur_k, cur_v, dk, dv, n, P.shift[p], P.mask[p], ph,
+                                                   s.status, s.counters + p));
     DDM_TRY(check_launch());
     cur_k = dk;
     cur_v = dv;
@@ -314,7 +401,7 @@ ddm_status validate_side(uint32_t d, uint64_t cnt, const double* const* lo, cons
                          uint32_t* hist_lo, uint32_t* hist_hi, uint32_t* err, cudaStream_t st) {
   if (cnt == 0) return DDM_OK;
   for (uint32_t k = 0; k < d; ++k) {
-    DDM_LAUNCH(match::validate_hist_kernel<<<grid_for(cnt, 512, 4), 512, 0, st>>>(
+    DDM_LAUNCH("validate_hist", 16.0 * cnt, st, match::validate_hist_kernel<<<grid_for(cnt, 512, 4), 512, 0, st>>>(
         lo[k], hi[k], cnt, k == 0 ? hist_lo : nullptr, k == 0 ? hist_hi : nullptr, err));
     DDM_TRY(check_launch());
   }
@@ -335,18 +422,18 @@ ddm_status build_index_async(const ddm_regions* R, const Index& I, SortScratch& 
   DDM_TRY(radix_sort(R->sub_lo[0], true, nullptr, I.slo_key, I.slo_id, n, P, s.hist[0], true, s, st));
   DDM_TRY(radix_sort(R->sub_hi[0], true, nullptr, I.shi_key, nullptr, n, P, s.hist[1], true, s, st));
   // a3: slo_hi[i] = key(sub_hi[slo_id[i]]) + block maxima
-  DDM_LAUNCH(match::gather_key_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.slo_id, R->sub_hi[0], n,
+  DDM_LAUNCH("gather_slo_hi", 20.0 * n, st, match::gather_key_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.slo_id, R->sub_hi[0], n,
                                                                              I.slo_hi, I.levels ? I.lvl[1] : nullptr));
   DDM_TRY(check_launch());
   for (int L = 2; L <= I.levels; ++L) {
-    DDM_LAUNCH(match::block_max_kernel<<<grid_for(I.lvl_n[L - 1], 256, 8), 256, 0, st>>>(
+    DDM_LAUNCH("block_max", 8.0 * I.lvl_n[L - 1], st, match::block_max_kernel<<<grid_for(I.lvl_n[L - 1], 256, 8), 256, 0, st>>>(
         I.lvl[L - 1], I.lvl_n[L - 1], I.lvl[L]));
     DDM_TRY(check_launch());
   }
   if (R->d > 1) {
     match::DimPtrs D{};
     for (uint32_t k = 0; k < R->d; ++k) { D.lo[k] = R->sub_lo[k]; D.hi[k] = R->sub_hi[k]; }
-    DDM_LAUNCH(match::gather_dims_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.slo_id, D, (int)R->d, n, I.sdims));
+    DDM_LAUNCH("gather_dims", 36.0 * (R->d - 1) * n, st, match::gather_dims_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.slo_id, D, (int)R->d, n, I.sdims));
     DDM_TRY(check_launch());
   }
   return DDM_OK;
@@ -380,18 +467,22 @@ ddm_status match_indexed(const MatchReq& q, MatchWs& W, uint64_t* count_out, boo
     return err_status(h.err);
   }
   SortScratch& s = W.sort;
+  init_attrs_once();
   DDM_CUDA(cudaMemsetAsync(s.hist[2], 0, sizeof(uint32_t) * 8 * 256, st));
   DDM_TRY(validate_side(d, m, R->upd_lo, R->upd_hi, s.hist[2], nullptr, &W.misc->err, st));
   DDM_TRY(radix_sort(R->upd_lo[0], true, nullptr, W.ulo_key, W.ulo_id, m, full_passes(), s.hist[2], true, s, st));
-  DDM_LAUNCH(match::gather_key_kernel<<<grid_for(m, 256, 8), 256, 0, st>>>(W.ulo_id, R->upd_hi[0], m, W.uhi, nullptr));
-  DDM_TRY(check_launch());
-  // a4 + a5: counts by rank difference and their exclusive scan
+  // a4: counts by rank difference; a5: their exclusive scan (K = off[m])
   const uint64_t ctiles = (m + match::kCountTile - 1) / match::kCountTile;
+  DDM_LAUNCH("count_partition", 0, st, match::count_partition_kernel<<<(unsigned)((ctiles + 255) / 256), 256, 0, st>>>(
+      W.ulo_key, m, I.slo_key, I.shi_key, n, W.part));
+  DDM_TRY(check_launch());
+  DDM_LAUNCH("count", 48.0 * m + 16.0 * n, st, match::count_kernel<<<(unsigned)ctiles, match::kCountThreads, sizeof(match::CountSmem), st>>>(
+      W.ulo_key, W.ulo_id, R->upd_hi[0], m, I.slo_key, I.shi_key, n, W.part, W.r_lo, W.r_b, W.cnt0));
+  DDM_TRY(check_launch());
   DDM_CUDA(cudaMemsetAsync(W.scan_counter, 0, sizeof(uint32_t) * 8, st));
   DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (ctiles + 1), st));
-  DDM_LAUNCH(match::count_scan_kernel<<<(unsigned)ctiles, match::kCountThreads, 0, st>>>(
-      W.ulo_key, W.uhi, m, I.slo_key, I.shi_key, n, W.r_lo, W.r_b, W.off, W.scan_status, W.scan_counter,
-      d == 1 ? &W.misc->K : nullptr));
+  DDM_LAUNCH("scan", 12.0 * m, st, match::scan_u32_kernel<<<(unsigned)ctiles, match::kCountThreads, 0, st>>>(
+      W.cnt0, m, W.off, W.scan_status, W.scan_counter, d == 1 ? &W.misc->K : nullptr));
   DDM_TRY(check_launch());
 
   match::EmitArgs A{};
@@ -417,11 +508,11 @@ ddm_status match_indexed(const MatchReq& q, MatchWs& W, uint64_t* count_out, boo
     // a8: dim-0 candidates filtered on dims 1..d-1; count pass + scan
     A.cnt_out = W.cnt;
     A.fstab_out = W.fstab;
-    DDM_LAUNCH(match::emit_kernel<match::kCountDD><<<egrid, match::kEmitThreads, 0, st>>>(A));
+    DDM_LAUNCH("count_dd", 44.0 * m, st, match::emit_kernel<match::kCountDD><<<egrid, match::kEmitThreads, 0, st>>>(A));
     DDM_TRY(check_launch());
     DDM_CUDA(cudaMemsetAsync(W.scan_counter, 0, sizeof(uint32_t) * 8, st));
     DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (ctiles + 1), st));
-    DDM_LAUNCH(match::scan_u32_kernel<<<(unsigned)ctiles, match::kCountThreads, 0, st>>>(
+    DDM_LAUNCH("scan", 12.0 * m, st, match::scan_u32_kernel<<<(unsigned)ctiles, match::kCountThreads, 0, st>>>(
         W.cnt, m, W.offd, W.scan_status, W.scan_counter, &W.misc->K));
     DDM_TRY(check_launch());
     A.off = W.offd;
@@ -436,10 +527,14 @@ ddm_status match_indexed(const MatchReq& q, MatchWs& W, uint64_t* count_out, boo
   if (h.K > q.capacity) return DDM_ERR_CAPACITY;
   if (h.K == 0) return DDM_OK;
   A.pairs = reinterpret_cast<uint2*>(q.pairs);
-  if (d == 1)
-    DDM_LAUNCH(match::emit_kernel<match::kEmitD1><<<egrid, match::kEmitThreads, 0, st>>>(A));
+  const bool per_row = (q.flags & (DDM_EMIT_FORCE_THREAD | DDM_EMIT_FORCE_WARP)) != 0;
+  if (d == 1 && !per_row)
+    DDM_LAUNCH("emit", 44.0 * m + 8.0 * h.K, st, match::emit_chunk_kernel<<<(unsigned)((m + match::kChunkRows - 1) / match::kChunkRows),
+                                          match::kChunkRows, sizeof(match::ChunkSmem), st>>>(A));
+  else if (d == 1)
+    DDM_LAUNCH("emit", 44.0 * m + 8.0 * h.K, st, match::emit_kernel<match::kEmitD1><<<egrid, match::kEmitThreads, 0, st>>>(A));
   else
-    DDM_LAUNCH(match::emit_kernel<match::kEmitDD><<<egrid, match::kEmitThreads, 0, st>>>(A));
+    DDM_LAUNCH("emit_dd", 44.0 * m + 8.0 * h.K, st, match::emit_kernel<match::kEmitDD><<<egrid, match::kEmitThreads, 0, st>>>(A));
   DDM_TRY(check_launch());
   return DDM_OK;
 }
@@ -509,7 +604,6 @@ ddm_status ddm_match_pairs(const ddm_regions* regions, ddm_pair* pairs, uint64_t
                            uint64_t* count_out, uint32_t flags, void* ws, size_t ws_bytes,
                            cudaStream_t stream) {
   if (!pairs && capacity) return DDM_ERR_INVALID_ARGUMENT;
-  if (flags & DDM_EMIT_FORCE_CHUNK) return DDM_ERR_INVALID_ARGUMENT;  // not built yet
   ddm_pair dummy;
   return match_full(regions, pairs ? pairs : &dummy, pairs ? capacity : 0, count_out, flags, ws, ws_bytes,
                     stream);
@@ -539,7 +633,6 @@ static ddm_status indexed_common(const void* index, const ddm_regions* upds, con
   DDM_TRY(check_regions(upds, false, true));
   if (!index || !count_out || !aligned(index, 256) || !aligned(ws, 256)) return DDM_ERR_INVALID_ARGUMENT;
   if (upds->n_sub > DDM_MAX_REGIONS) return DDM_ERR_INVALID_ARGUMENT;
-  if (flags & DDM_EMIT_FORCE_CHUNK) return DDM_ERR_INVALID_ARGUMENT;
   if (ws_bytes < ddm_indexed_workspace_bytes(upds->d, upds->n_sub, upds->n_upd)) return DDM_ERR_WORKSPACE;
   Index I = index_layout(upds->d, upds->n_sub, const_cast<void*>(index));
   MatchWs W = match_layout(upds->d, upds->n_sub, upds->n_upd, ws);
@@ -614,7 +707,7 @@ ddm_status ddm_radix_sort_u64(const uint64_t* keys_in, const uint32_t* vals_in, 
 ddm_status ddm_encode_keys(const double* x, uint64_t* keys, uint64_t n, cudaStream_t stream) {
   if (n == 0) return DDM_OK;
   if (!x || !keys) return DDM_ERR_INVALID_ARGUMENT;
-  DDM_LAUNCH(encode_kernel<<<grid_for(n, 256, 8), 256, 0, stream>>>(x, keys, n));
+  DDM_LAUNCH("encode", 16.0 * n, stream, encode_kernel<<<grid_for(n, 256, 8), 256, 0, stream>>>(x, keys, n));
   return check_launch();
 }
 
@@ -634,6 +727,37 @@ const char* ddm_status_string(ddm_status s) {
 int ddm_last_cuda_error(void) { return g_last_cuda.load(); }
 
 uint64_t ddm_kernel_launch_count(void) { return g_launches.load(); }
+
+void ddm_profile_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof.on = on != 0;
+  g_prof.recs.clear();
+  g_prof.next = 0;
+}
+
+int ddm_profile_read(ddm_kernel_stat* out, int cap) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  std::vector<ddm_kernel_stat> agg;
+  for (const ProfRec& r : g_prof.recs) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(g_prof.ev[r.e1]) != cudaSuccess) return -1;
+    if (cudaEventElapsedTime(&ms, g_prof.ev[r.e0], g_prof.ev[r.e1]) != cudaSuccess) return -1;
+    ddm_kernel_stat* hit = nullptr;
+    for (auto& a : agg)
+      if (strncmp(a.name, r.name, sizeof(a.name)) == 0) hit = &a;
+    if (!hit) {
+      agg.push_back(ddm_kernel_stat{});
+      hit = &agg.back();
+      strncpy(hit->name, r.name, sizeof(hit->name) - 1);
+    }
+    hit->launches += 1;
+    hit->total_ms += ms;
+    hit->bytes += r.bytes;
+  }
+  const int k = (int)agg.size() < cap ? (int)agg.size() : cap;
+  for (int i = 0; i < k; ++i) out[i] = agg[i];
+  return (int)agg.size();
+}
 
 const char* ddm_build_info(void) {
   return "libddm sm_100a onesweep-radix(8x8b, 4096/tile) count_scan(2048/tile) emit(thread|warp)";

@@ -181,115 +181,189 @@ constexpr uint64_t kScanAgg = 1ull << 62;
 constexpr uint64_t kScanPre = 2ull << 62;
 constexpr uint64_t kScanVal = (1ull << 62) - 1;
 
-// Block-level: given this tile's aggregate, return the exclusive prefix of
-// all preceding tiles (single thread, tid 0; result broadcast via smem).
-__device__ __forceinline__ uint64_t lookback_u64(uint64_t* status, uint32_t tile, uint64_t agg) {
+// Decoupled look-back by one whole warp: 32 predecessors are examined per
+// step (lane k reads tile - 1 - k), so the walk over tiles that have
+// published only their aggregate costs one round trip per 32 tiles.
+// Call with all 32 lanes of one warp; returns the exclusive prefix.
+__device__ __forceinline__ uint64_t lookback_warp_u64(uint64_t* status, uint32_t tile, uint64_t agg) {
+  const int lane = threadIdx.x & 31;
   if (tile == 0) {
-    st_relaxed_u64(status, kScanPre | agg);
+    if (lane == 0) st_relaxed_u64(status, kScanPre | agg);
     return 0;
   }
-  st_relaxed_u64(status + tile, kScanAgg | agg);
+  if (lane == 0) st_relaxed_u64(status + tile, kScanAgg | agg);
   uint64_t excl = 0;
-  int64_t p = (int64_t)tile - 1;
+  int64_t base = (int64_t)tile - 1;
   while (true) {
-    const uint64_t s = ld_relaxed_u64(status + p);
-    if ((s & ~kScanVal) == 0) continue;
-    excl += s & kScanVal;
-    if (s & kScanPre) break;
-    --p;
+    const int64_t p = base - lane;
+    const uint64_t s = p >= 0 ? ld_relaxed_u64(status + p) : kScanPre;
+    const unsigned pre = __ballot_sync(kFull, (s & kScanPre) != 0);
+    const unsigned unpub = __ballot_sync(kFull, (s & ~kScanVal) == 0);
+    const int first = pre ? __ffs(pre) - 1 : 31;
+    const unsigned need = first == 31 ? kFull : ((2u << first) - 1u);
+    if (unpub & need) continue;  // some needed predecessor not published yet
+    excl += warp_sum<uint64_t>(lane <= first && p >= 0 ? (s & kScanVal) : 0);
+    if (pre) break;
+    base -= 32;
   }
-  st_relaxed_u64(status + tile, kScanPre | (excl + agg));
+  if (lane == 0) st_relaxed_u64(status + tile, kScanPre | (excl + agg));
   return excl;
 }
 
 constexpr int kCountThreads = 256;
 constexpr int kCountItems = 8;
 constexpr int kCountTile = kCountThreads * kCountItems;
+constexpr int kCountWin = 4096;  // smem window (keys) per sorted array
+constexpr int kCountExt = 1024;  // Slo window extension past r_lo(a_last) for the r_b searches
 
-// a4 + a5 fused (G5 + G6): for every update j (in sorted Ulo order) compute
-// r_lo, r_b and cnt = r_b - r_hi (rank difference, I2), then the exclusive
-// scan off[j] = sum_{i<j} cnt[i] with a single-pass decoupled look-back;
-// off[m] = K.  Each thread owns 8 consecutive updates: the first is located
-// by binary search inside the tile's window, the rest by galloping forward
-// (a is sorted, so r_lo and r_hi are monotone -- a merge path).
-__global__ void __launch_bounds__(kCountThreads) count_scan_kernel(
-    const uint64_t* __restrict__ ulo_key, const uint64_t* __restrict__ uhi, uint64_t m,
-    const uint64_t* __restrict__ slo_key, const uint64_t* __restrict__ shi_key, uint64_t n,
-    uint32_t* __restrict__ r_lo_out, uint32_t* __restrict__ r_b_out, uint64_t* __restrict__ off,
-    uint64_t* __restrict__ status, uint32_t* __restrict__ tile_counter, uint64_t* __restrict__ k_out) {
-  __shared__ uint64_t scan_tmp[kCountThreads / 32 + 1];
-  __shared__ uint64_t win[4];
-  __shared__ uint64_t prefix;
-  __shared__ uint32_t tile_id;
+// first index in [lo, end) with a[i] > x (UPPER) or a[i] >= x (!UPPER),
+// galloping forward from lo; `end` if none.
+template <bool UPPER, typename P>
+__device__ __forceinline__ uint64_t gallop(P a, uint64_t lo, uint64_t end, uint64_t x) {
+  uint64_t hi = end, step = 1;
+  // short linear probe first: consecutive sorted queries usually move by ~1
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (lo >= end) return end;
+    const uint64_t v = a[lo];
+    if (UPPER ? v > x : v >= x) return lo;
+    ++lo;
+  }
+  while (true) {
+    const uint64_t p = lo + step - 1;
+    if (p >= end) break;
+    const uint64_t v = a[p];
+    if (UPPER ? v > x : v >= x) { hi = p; break; }
+    lo = p + 1;
+    step <<= 1;
+  }
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    const uint64_t v = a[mid];
+    if (UPPER ? v <= x : v < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// A sorted global array g[0..n) with the slice [base, base+len) staged in smem.
+struct Window {
+  const uint64_t* s;
+  const uint64_t* g;
+  uint64_t base, n;
+  uint32_t len;
+  // search from `start` (all entries before start are known to be "before" x)
+  template <bool UPPER>
+  __device__ __forceinline__ uint64_t search(uint64_t start, uint64_t x) const {
+    const uint64_t end = base + len;
+    if (start >= base && start < end) {
+      const uint64_t last = s[len - 1];
+      if (end == n || (UPPER ? last > x : last >= x))
+        return base + gallop<UPPER>(s, start - base, len, x);
+      start = end;
+    }
+    return gallop<UPPER>(g, start, n, x);
+  }
+};
+
+// Per count tile: r_lo(a_first), r_lo(a_last), r_hi(a_first), r_hi(a_last)
+// (merge-path partition of the sorted updates against Slo and Shi).
+__global__ void __launch_bounds__(256) count_partition_kernel(const uint64_t* __restrict__ ulo_key, uint64_t m,
+                                                              const uint64_t* __restrict__ slo_key,
+                                                              const uint64_t* __restrict__ shi_key, uint64_t n,
+                                                              uint64_t* __restrict__ part) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t tiles = (m + kCountTile - 1) / kCountTile;
+  if (t >= tiles) return;
+  const uint64_t j0 = t * kCountTile, j1 = umin64(m, j0 + kCountTile) - 1;
+  const uint64_t af = ulo_key[j0], al = ulo_key[j1];
+  part[4 * t + 0] = ub(slo_key, 0, n, af);
+  part[4 * t + 1] = ub(slo_key, 0, n, al);
+  part[4 * t + 2] = lb(shi_key, 0, n, af);
+  part[4 * t + 3] = lb(shi_key, 0, n, al);
+}
+
+struct CountSmem {
+  uint64_t ws[kCountWin];
+  uint64_t wh[kCountWin];
+};
+
+// a4 (G5): for every update j (in sorted Ulo order) compute r_lo, r_b and
+// cnt = r_b - r_hi (rank difference, I2); the exclusive scan of cnt (a5) is
+// scan_u32_kernel.  b_j = key(upd_hi[ulo_id[j]]) is gathered here (a3).  The tile's slices of Slo and Shi are staged in shared memory;
+// each thread owns 8 consecutive updates and gallops forward (a is sorted, so
+// r_lo and r_hi are monotone: a merge path), falling back to global memory
+// for any search that leaves the staged window.
+__global__ void __launch_bounds__(kCountThreads) count_kernel(
+    const uint64_t* __restrict__ ulo_key, const uint32_t* __restrict__ ulo_id, const double* __restrict__ upd_hi,
+    uint64_t m, const uint64_t* __restrict__ slo_key, const uint64_t* __restrict__ shi_key, uint64_t n,
+    const uint64_t* __restrict__ part, uint32_t* __restrict__ r_lo_out, uint32_t* __restrict__ r_b_out,
+    uint32_t* __restrict__ cnt_out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CountSmem& S = *reinterpret_cast<CountSmem*>(smem_raw);
   const int tid = threadIdx.x;
-  if (tid == 0) tile_id = atomicAdd(tile_counter, 1u);
-  __syncthreads();
-  const uint32_t tile = tile_id;
+  const uint32_t tile = blockIdx.x;
   const uint64_t j0 = (uint64_t)tile * kCountTile;
   const uint64_t jn = umin64(kCountTile, m - j0);
-  if (tid < 4) {
-    const uint64_t a = ulo_key[(tid & 1) ? j0 + jn - 1 : j0];
-    win[tid] = tid < 2 ? ub(slo_key, 0, n, a) : lb(shi_key, 0, n, a);
-  }
+  const uint64_t p0 = part[4 * tile + 0], p1 = part[4 * tile + 1], h0 = part[4 * tile + 2], h1 = part[4 * tile + 3];
+  Window WS{S.ws, slo_key, p0, n, (uint32_t)umin64(umin64(kCountWin, p1 - p0 + kCountExt), n - p0)};
+  Window WH{S.wh, shi_key, h0, n, (uint32_t)umin64(kCountWin, h1 - h0 + 1 < n - h0 ? h1 - h0 + 1 : n - h0)};
+  for (uint32_t i = tid; i < WS.len; i += kCountThreads) S.ws[i] = __ldcs(slo_key + p0 + i);
+  for (uint32_t i = tid; i < WH.len; i += kCountThreads) S.wh[i] = __ldcs(shi_key + h0 + i);
   __syncthreads();
+
   const uint64_t t0 = (uint64_t)tid * kCountItems;
   uint32_t cnt[kCountItems];
-  uint64_t local = 0;
+#pragma unroll
+  for (int i = 0; i < kCountItems; ++i) cnt[i] = 0;
   if (t0 < jn) {
     const uint64_t j = j0 + t0;
     const int ni = (int)umin64(kCountItems, jn - t0);
-    uint64_t rl = ub(slo_key, win[0], win[1], ulo_key[j]);
-    uint64_t rh = lb(shi_key, win[2], win[3], ulo_key[j]);
-    uint64_t rb = rl, prev_b = 0;
+    uint64_t a[kCountItems], b[kCountItems];
+#pragma unroll
+    for (int i = 0; i < kCountItems; ++i) {
+      a[i] = i < ni ? __ldcs(ulo_key + j + i) : 0;
+      b[i] = i < ni ? f64_key(upd_hi[__ldcs(ulo_id + j + i)]) : 0;  // a3: b of the sorted update
+    }
+    uint64_t rl = p0, rh = h0, rb = p0, prev_b = 0;
+    // locate the thread's first update by binary search inside the windows
+    if (WS.len && (WS.base + WS.len == n || S.ws[WS.len - 1] > a[0])) rl = p0 + ub(S.ws, 0, WS.len, a[0]);
+    if (WH.len && (WH.base + WH.len == n || S.wh[WH.len - 1] >= a[0])) rh = h0 + lb(S.wh, 0, WH.len, a[0]);
     uint32_t ol[kCountItems], ob[kCountItems];
 #pragma unroll
     for (int i = 0; i < kCountItems; ++i) {
       if (i < ni) {
-        const uint64_t a = ulo_key[j + i], b = uhi[j + i];
-        if (i) {
-          rl = ub_gallop(slo_key, n, rl, a);
-          // lb(Shi, a): gallop over entries < a
-          uint64_t lo = rh, hi = n, step = 1;
-          while (true) {
-            const uint64_t probe = lo + step - 1;
-            if (probe >= n) break;
-            if (shi_key[probe] >= a) { hi = probe; break; }
-            lo = probe + 1;
-            step <<= 1;
-          }
-          rh = lb(shi_key, lo, hi, a);
-        }
-        const uint64_t start = (i && b >= prev_b && rb > rl) ? rb : rl;
-        rb = ub_gallop(slo_key, n, start, b);
-        prev_b = b;
+        rl = WS.search<true>(rl, a[i]);
+        rh = WH.search<false>(rh, a[i]);
+        const uint64_t start = (i && b[i] >= prev_b && rb > rl) ? rb : rl;
+        rb = WS.search<true>(start, b[i]);
+        prev_b = b[i];
         ol[i] = (uint32_t)rl;
         ob[i] = (uint32_t)rb;
         cnt[i] = (uint32_t)(rb > rh ? rb - rh : 0);
-        local += cnt[i];
-      } else {
-        cnt[i] = 0;
       }
     }
+    if (ni == kCountItems) {
+      uint4* dl = reinterpret_cast<uint4*>(r_lo_out + j);
+      uint4* db = reinterpret_cast<uint4*>(r_b_out + j);
+      dl[0] = make_uint4(ol[0], ol[1], ol[2], ol[3]);
+      dl[1] = make_uint4(ol[4], ol[5], ol[6], ol[7]);
+      db[0] = make_uint4(ob[0], ob[1], ob[2], ob[3]);
+      db[1] = make_uint4(ob[4], ob[5], ob[6], ob[7]);
+    } else {
 #pragma unroll
-    for (int i = 0; i < kCountItems; ++i)
-      if (i < ni) { r_lo_out[j + i] = ol[i]; r_b_out[j + i] = ob[i]; }
+      for (int i = 0; i < kCountItems; ++i)
+        if (i < ni) { r_lo_out[j + i] = ol[i]; r_b_out[j + i] = ob[i]; }
+    }
+  }
+  if (t0 + kCountItems <= jn) {
+    uint4* d = reinterpret_cast<uint4*>(cnt_out + j0 + t0);
+    d[0] = make_uint4(cnt[0], cnt[1], cnt[2], cnt[3]);
+    d[1] = make_uint4(cnt[4], cnt[5], cnt[6], cnt[7]);
   } else {
 #pragma unroll
-    for (int i = 0; i < kCountItems; ++i) cnt[i] = 0;
-  }
-  uint64_t agg;
-  const uint64_t texcl = block_excl_scan<kCountThreads>(local, scan_tmp, &agg);
-  if (tid == 0) prefix = lookback_u64(status, tile, agg);
-  __syncthreads();
-  uint64_t run = prefix + texcl;
-#pragma unroll
-  for (int i = 0; i < kCountItems; ++i) {
-    if (t0 + i < jn) off[j0 + t0 + i] = run;
-    run += cnt[i];
-  }
-  if (j0 + jn == m && tid == 0) {
-    off[m] = prefix + agg;
-    if (k_out) *k_out = prefix + agg;
+    for (int i = 0; i < kCountItems; ++i)
+      if (t0 + i < jn) cnt_out[j0 + t0 + i] = cnt[i];
   }
 }
 
@@ -318,7 +392,10 @@ __global__ void __launch_bounds__(kCountThreads) scan_u32_kernel(const uint32_t*
   }
   uint64_t agg;
   const uint64_t texcl = block_excl_scan<kCountThreads>(local, scan_tmp, &agg);
-  if (tid == 0) prefix = lookback_u64(status, tile, agg);
+  if (tid < 32) {
+    const uint64_t e = lookback_warp_u64(status, tile, agg);
+    if (tid == 0) prefix = e;
+  }
   __syncthreads();
   uint64_t run = prefix + texcl;
 #pragma unroll
@@ -523,6 +600,176 @@ __global__ void __launch_bounds__(kEmitThreads) emit_kernel(EmitArgs A) {
   const uint32_t nq = qn;
   for (uint32_t q = warp; q < nq; q += kEmitThreads / 32)
     row_warp<MODE>(A, (uint64_t)blockIdx.x * kEmitThreads + queue[q], lane);
+}
+
+// ------------------------------------------------------------ chunked sweep (a6 + a7)
+//
+// One CTA per tile of kChunkRows consecutive updates (sorted order), the
+// GPU form of Alg. 5's segments with Alg. 6's initial set
+// at the tile's first query point x_t = a_{j0}:
+//   A_t = Stab(x_t) = { S : S.lo <= x_t <= S.hi }  -- the chunk-start set,
+// found by one warp walking Slo backwards from r_lo(x_t) with the block-max
+// skips, and known to hold exactly r_lo - r_hi members (I4).  Every stab
+// member of a later row j (a_j >= x_t) is either in A_t or in the Slo slice
+// [r_lo(x_t), r_lo(a_j)), and every range member is in [r_lo(a_j), r_b(a_j)),
+// so the tile stages A_t and the contiguous Slo slice (ids + upper keys) in
+// shared memory once and all its rows are swept from there: short rows by one
+// thread, long rows by one warp (ballot/popc compaction), every store
+// coalesced.  Output is byte-identical to the per-row paths.
+
+constexpr int kChunkRows = 256;
+constexpr int kChunkSlice = 3072;
+constexpr int kChunkAct = 1024;
+
+struct ChunkSmem {
+  uint64_t shi[kChunkSlice];
+  uint64_t ahi[kChunkAct];
+  uint32_t sid[kChunkSlice];
+  uint32_t aid[kChunkAct];
+  uint32_t queue[kChunkRows];
+  uint64_t red[kChunkRows / 32];
+  uint32_t qn;
+  uint32_t nact;
+  uint32_t slen;
+};
+
+// (id, upper key) of Slo position i: from the staged slice when inside it.
+__device__ __forceinline__ uint64_t c_hi(const ChunkSmem& S, const EmitArgs& A, uint64_t rl0, uint64_t i) {
+  const uint64_t k = i - rl0;
+  return k < S.slen ? S.shi[k] : A.T.lvl[0][i];
+}
+__device__ __forceinline__ uint32_t c_id(const ChunkSmem& S, const EmitArgs& A, uint64_t rl0, uint64_t i) {
+  const uint64_t k = i - rl0;
+  return k < S.slen ? S.sid[k] : A.slo_id[i];
+}
+
+__device__ __forceinline__ void chunk_row_thread(const ChunkSmem& S, const EmitArgs& A, uint64_t j, uint64_t rl0) {
+  const uint64_t a = A.ulo_key[j];
+  const uint32_t lid = A.ulo_id[j];
+  const uint32_t uid = A.upd_map ? A.upd_map[lid] : lid;
+  const uint64_t rl = A.r_lo[j], rb = A.r_b[j];
+  const uint64_t o = A.off[j];
+  const uint32_t stab = (uint32_t)((A.off[j + 1] - o) - (rb - rl));
+  // members of A_t still alive at a (ascending Slo order)
+  uint32_t w = 0;
+  for (uint32_t k = 0; k < S.nact && w < stab; ++k)
+    if (S.ahi[k] >= a) A.pairs[o + (w++)] = make_uint2(S.aid[k], uid);
+  // the rest of the stab part lies in the slice [rl0, rl): walk it backwards
+  uint32_t need = stab - w;
+  for (uint64_t i = rl; need; ) {
+    --i;
+    if (c_hi(S, A, rl0, i) >= a) A.pairs[o + w + (--need)] = make_uint2(c_id(S, A, rl0, i), uid);
+  }
+  for (uint64_t i = rl; i < rb; ++i) A.pairs[o + stab + (i - rl)] = make_uint2(c_id(S, A, rl0, i), uid);
+}
+
+__device__ __forceinline__ void chunk_row_warp(const ChunkSmem& S, const EmitArgs& A, uint64_t j, uint64_t rl0,
+                                               int lane) {
+  const uint64_t a = A.ulo_key[j];
+  const uint32_t lid = A.ulo_id[j];
+  const uint32_t uid = A.upd_map ? A.upd_map[lid] : lid;
+  const uint64_t rl = A.r_lo[j], rb = A.r_b[j];
+  const uint64_t o = A.off[j];
+  const uint32_t stab = (uint32_t)((A.off[j + 1] - o) - (rb - rl));
+  uint32_t w = 0;
+  for (uint32_t k0 = 0; k0 < S.nact && w < stab; k0 += 32) {
+    const uint32_t k = k0 + lane;
+    const bool alive = k < S.nact && S.ahi[k] >= a;
+    const unsigned mm = __ballot_sync(kFull, alive);
+    if (alive) A.pairs[o + w + __popc(mm & lanemask_lt())] = make_uint2(S.aid[k], uid);
+    w += __popc(mm);
+  }
+  uint32_t need = stab - w;
+  int64_t hi_excl = (int64_t)rl;
+  while (need) {  // 32-wide windows walking the slice backwards
+    const int64_t base = hi_excl - 32;
+    const int64_t i = base + lane;
+    const bool member = i >= (int64_t)rl0 && c_hi(S, A, rl0, (uint64_t)i) >= a;
+    const unsigned mm = __ballot_sync(kFull, member);
+    need -= __popc(mm);
+    if (member) A.pairs[o + w + need + __popc(mm & lanemask_lt())] = make_uint2(c_id(S, A, rl0, (uint64_t)i), uid);
+    hi_excl = base;
+  }
+  for (uint64_t i = rl + lane; i < rb; i += 32) A.pairs[o + stab + (i - rl)] = make_uint2(c_id(S, A, rl0, i), uid);
+}
+
+__global__ void __launch_bounds__(kChunkRows) emit_chunk_kernel(EmitArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ChunkSmem& S = *reinterpret_cast<ChunkSmem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t j0 = (uint64_t)blockIdx.x * kChunkRows;
+  const uint64_t jn = umin64(kChunkRows, A.m - j0);
+  const uint64_t rl0 = A.r_lo[j0];
+  // slice end: max r_b over the tile
+  uint64_t rmax = tid < jn ? A.r_b[j0 + tid] : 0;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const uint64_t v = __shfl_xor_sync(kFull, rmax, o);
+    rmax = v > rmax ? v : rmax;
+  }
+  if (lane == 0) S.red[warp] = rmax;
+  if (tid == 0) S.qn = 0;
+  __syncthreads();
+  if (tid == 0) {
+    uint64_t r = 0;
+    for (int w = 0; w < kChunkRows / 32; ++w) r = S.red[w] > r ? S.red[w] : r;
+    S.slen = (uint32_t)umin64(kChunkSlice, r > rl0 ? r - rl0 : 0);
+  }
+  // a6: the chunk-start set A_t = Stab(x_t), |A_t| = stab(j0) known exactly
+  const uint64_t x = A.ulo_key[j0];
+  const uint32_t nact = (uint32_t)((A.off[j0 + 1] - A.off[j0]) - (A.r_b[j0] - rl0));
+  const bool fits = nact <= kChunkAct;
+  if (warp == 0 && fits) {
+    int64_t hi_excl = (int64_t)rl0;
+    uint32_t rem = nact;
+    while (rem) {
+      const int64_t i = hi_excl - 1;
+      if ((i & 31) == 31) {
+        const int L = skip_levels(A.T, i, x);
+        if (L) { hi_excl -= (int64_t)1 << (5 * L); continue; }
+      }
+      const int64_t base = i & ~31ll;
+      const int64_t idx = base + lane;
+      uint64_t h = 0;
+      const bool member = idx < hi_excl && (h = A.T.lvl[0][idx]) >= x;
+      const unsigned mm = __ballot_sync(kFull, member);
+      rem -= __popc(mm);
+      if (member) {
+        const uint32_t pos = rem + __popc(mm & lanemask_lt());
+        S.ahi[pos] = h;
+        S.aid[pos] = A.slo_id[idx];
+      }
+      hi_excl = base;
+    }
+    if (lane == 0) S.nact = nact;
+  }
+  __syncthreads();
+  // stage the Slo slice [rl0, rl0 + slen): ids and upper keys
+  const uint32_t slen = S.slen;
+  for (uint32_t k = tid; k < slen; k += kChunkRows) {
+    S.shi[k] = __ldcs(A.T.lvl[0] + rl0 + k);
+    S.sid[k] = __ldcs(A.slo_id + rl0 + k);
+  }
+  __syncthreads();
+  const uint64_t j = j0 + tid;
+  if (!fits) {  // chunk-start set too large for shared memory: per-row global walks
+    if (j < A.m) {
+      const uint64_t c0 = A.off[j + 1] - A.off[j];
+      if (c0 <= A.thread_row_max) row_thread<kEmitD1>(A, j);
+      else S.queue[atomicAdd(&S.qn, 1u)] = tid;
+    }
+    __syncthreads();
+    for (uint32_t q = warp; q < S.qn; q += kChunkRows / 32) row_warp<kEmitD1>(A, j0 + S.queue[q], lane);
+    return;
+  }
+  if (j < A.m) {
+    const uint64_t c = A.off[j + 1] - A.off[j];
+    if (c <= A.thread_row_max && nact <= 32) chunk_row_thread(S, A, j, rl0);
+    else if (c) S.queue[atomicAdd(&S.qn, 1u)] = tid;
+  }
+  __syncthreads();
+  const uint32_t nq = S.qn;
+  for (uint32_t q = warp; q < nq; q += kChunkRows / 32) chunk_row_warp(S, A, j0 + S.queue[q], rl0, lane);
 }
 
 // ------------------------------------------------------------ pair canonical key

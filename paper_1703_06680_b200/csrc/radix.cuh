@@ -24,8 +24,10 @@ constexpr int kDigitBits = 8;
 constexpr int kRadix = 1 << kDigitBits;
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 16;
-constexpr int kTile = kThreads * kItems;
+constexpr int kItemsMax = 16;
+constexpr int kTileMax = kThreads * kItemsMax;
+// Resident CTAs per SM the pass kernel is compiled for, by items per thread.
+__host__ __device__ constexpr int min_blocks_for(int items) { return items <= 8 ? 5 : items <= 12 ? 4 : 3; }
 constexpr int kMaxPasses = 8;
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagPre = 2u << 30;
@@ -76,10 +78,12 @@ __global__ void __launch_bounds__(kRadix) bin_start_kernel(const uint32_t* __res
 
 // ---------------------------------------------------------------- one pass
 
+template <int ITEMS, bool HAS_VALS>
 struct PassSmem {
+  static constexpr int kTile = kThreads * ITEMS;
   uint64_t keys[kTile];
-  uint32_t vals[kTile];
-  uint32_t wbase[kWarps][kRadix];  // early counts -> per-warp running positions
+  uint32_t vals[HAS_VALS ? kTile : 4];
+  alignas(16) uint32_t wbase[kWarps][kRadix];  // early counts -> per-warp running positions
   uint32_t match[kWarps][kRadix];  // per-warp peer masks (atomicOr match)
   long long digit_base[kRadix];
   uint32_t scan_tmp[kWarps + 1];
@@ -91,14 +95,17 @@ struct PassSmem {
 // tile's aggregate is published before the stable ranking runs and successor
 // tiles' look-backs never wait for it.  Stable ranks within a warp come from
 // a per-item peer mask (smem atomicOr match) and per-warp running bases.
-template <bool HAS_VALS, bool SRC_F64>
-__global__ void __launch_bounds__(kThreads, 3)
+template <int ITEMS, bool HAS_VALS, bool SRC_F64>
+__global__ void __launch_bounds__(kThreads, min_blocks_for(ITEMS))
     onesweep_kernel(const void* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                     uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint64_t n,
                     int shift, uint32_t dmask, const uint32_t* __restrict__ bin_start,
                     uint32_t* __restrict__ status, uint32_t* __restrict__ tile_counter) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  PassSmem& S = *reinterpret_cast<PassSmem*>(smem_raw);
+  using Smem = PassSmem<ITEMS, HAS_VALS>;
+  constexpr int kItems = ITEMS;
+  constexpr int kTile = Smem::kTile;
+  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   {
@@ -186,16 +193,29 @@ __global__ void __launch_bounds__(kThreads, 3)
     __syncwarp();
   }
 
-  // decoupled look-back for digit `tid`
+  // decoupled look-back for digit `tid`: read kLB predecessors per step
   uint32_t excl = 0;
   if (tile > 0) {
+    constexpr int kLB = 8;
     int64_t p = (int64_t)tile - 1;
     while (true) {
-      const uint32_t s = ld_relaxed_u32(status + (uint64_t)p * kRadix + tid);
-      if ((s & ~kValMask) == 0) continue;  // predecessor not published yet
-      excl += s & kValMask;
-      if (s & kFlagPre) break;
-      --p;
+      uint32_t sv[kLB];
+#pragma unroll
+      for (int k = 0; k < kLB; ++k)
+        sv[k] = p - k >= 0 ? ld_relaxed_u32(status + (uint64_t)(p - k) * kRadix + tid) : kFlagPre;
+      int consumed = 0;
+      bool hit_pre = false;
+#pragma unroll
+      for (int q = 0; q < kLB; ++q) {
+        if (hit_pre || consumed != q) break;
+        const uint32_t v = sv[q];
+        if ((v & ~kValMask) == 0) break;  // not published yet: re-read from here
+        excl += v & kValMask;
+        consumed = q + 1;
+        hit_pre = (v & kFlagPre) != 0;
+      }
+      if (hit_pre) break;
+      p -= consumed;
     }
     st_relaxed_u32(my_status, kFlagPre | (excl + total));
   }
@@ -218,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 3)
 
 // ---------------------------------------------------------------- host side
 
-inline uint64_t num_tiles(uint64_t n) { return (n + kTile - 1) / kTile; }
+inline uint64_t num_tiles(uint64_t n, int items = 8) { return (n + (uint64_t)kThreads * items - 1) / ((uint64_t)kThreads * items); }
 
 // Workspace carve for one sort of up to n keys: histograms, status words,
 // tile counters, and the ping-pong key/value buffers.

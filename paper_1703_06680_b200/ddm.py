@@ -40,6 +40,11 @@ class DDMError(RuntimeError):
         super().__init__(f"{where}: {name}{extra}")
 
 
+class _KernelStat(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_uint64), ("total_ms", ctypes.c_double),
+                ("bytes", ctypes.c_double)]
+
+
 class _Regions(ctypes.Structure):
     _fields_ = [("d", ctypes.c_uint32), ("n_sub", ctypes.c_uint64), ("n_upd", ctypes.c_uint64),
                 ("sub_lo", ctypes.c_void_p * DDM_MAX_DIMS), ("sub_hi", ctypes.c_void_p * DDM_MAX_DIMS),
@@ -82,6 +87,8 @@ def load() -> ctypes.CDLL:
         "ddm_last_cuda_error": ([], i32),
         "ddm_kernel_launch_count": ([], u64),
         "ddm_build_info": ([], ctypes.c_char_p),
+        "ddm_profile_enable": ([i32], None),
+        "ddm_profile_read": ([ctypes.POINTER(_KernelStat), i32], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -95,7 +102,8 @@ EXPORTED = ["ddm_workspace_bytes", "ddm_match_count", "ddm_match_pairs", "ddm_so
             "ddm_sort_pairs", "ddm_sub_index_bytes", "ddm_index_build_workspace_bytes", "ddm_sub_index_build",
             "ddm_indexed_workspace_bytes", "ddm_match_pairs_indexed", "ddm_match_count_indexed",
             "ddm_radix_sort_workspace_bytes", "ddm_radix_sort_u64", "ddm_encode_keys", "ddm_status_string",
-            "ddm_last_cuda_error", "ddm_kernel_launch_count", "ddm_build_info"]
+            "ddm_last_cuda_error", "ddm_kernel_launch_count", "ddm_build_info", "ddm_profile_enable",
+            "ddm_profile_read"]
 
 
 def _check(st: int, where: str):
@@ -316,3 +324,19 @@ def launch_count() -> int:
 
 def build_info() -> str:
     return load().ddm_build_info().decode()
+
+
+def profile_enable(on: bool = True) -> None:
+    """Record CUDA events around every library launch (resets the record)."""
+    load().ddm_profile_enable(1 if on else 0)
+
+
+def profile_read() -> dict:
+    """{kernel class: {"launches", "total_ms", "bytes"}} of the recorded launches."""
+    L = load()
+    buf = (_KernelStat * 64)()
+    k = L.ddm_profile_read(buf, 64)
+    if k < 0:
+        raise DDMError(6, "ddm_profile_read")
+    return {buf[i].name.decode(): {"launches": int(buf[i].launches), "total_ms": float(buf[i].total_ms),
+                                   "bytes": float(buf[i].bytes)} for i in range(min(k, 64))}

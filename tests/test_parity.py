@@ -15,7 +15,7 @@ from paper_1703_06680_b200 import ddm
 from paper_1703_06680_b200 import workload as wl
 from tests.helpers import cuda, gpu_args, raw_words, words_of
 
-EMIT_FLAGS = [ddm.DDM_EMIT_AUTO, ddm.DDM_EMIT_FORCE_THREAD, ddm.DDM_EMIT_FORCE_WARP]
+EMIT_FLAGS = [ddm.DDM_EMIT_AUTO, ddm.DDM_EMIT_FORCE_THREAD, ddm.DDM_EMIT_FORCE_WARP, ddm.DDM_EMIT_FORCE_CHUNK]
 
 
 @pytest.fixture(scope="module", autouse=True)
