@@ -4,8 +4,8 @@
 // Pipeline for d = 1:
 //   validate_hist(subs)  -> onesweep x8 (Slo: key+id, from float64)
 //                        -> onesweep x8 (Shi: keys)     -> gather slo_hi + block maxima
-//   validate_hist(upds)  -> onesweep x8 (Ulo: key+id)   -> gather uhi
-//   count_scan (rank differences + exclusive scan, one kernel)
+//   validate_hist(upds)  -> onesweep x8 (Ulo: key+id)
+//   count (rank differences, b gathered in-kernel) -> scan of the 256-row tile sums
 //   one 16-byte D2H {K, error word}; capacity check
 //   emit (stab part from the sweep state + contiguous range part)
 // The subscription half forms the byte-copyable "index" (multi-GPU: built by
@@ -201,14 +201,13 @@ struct MatchWs {
   uint32_t* ulo_id;
   uint32_t* r_lo;
   uint32_t* r_b;
-  uint64_t* off;
-  uint32_t* cnt0;   // dim-0 counts
-  uint32_t* cnt;    // d > 1
-  uint32_t* fstab;  // d > 1
-  uint64_t* offd;   // d > 1
+  uint32_t* cnt0;      // dim-0 counts (rank differences)
+  uint32_t* cnt;       // d > 1: filtered counts
+  uint32_t* fstab;     // d > 1: filtered stab counts
+  uint64_t* tile_sum;  // per 256-row tile count sums
+  uint64_t* tile_off;  // their exclusive scan: output offset of each row tile
   uint64_t* scan_status;
   uint64_t* part;
-  uint32_t* scan_counter;
   Misc* misc;
   SortScratch sort;
   size_t bytes;
@@ -217,20 +216,20 @@ struct MatchWs {
 MatchWs match_layout(uint32_t d, uint64_t n_sub, uint64_t m, void* base) {
   Carver c(base);
   MatchWs W{};
+  const uint64_t rtiles = m / match::kRowTile + 2;
   W.misc = c.take<Misc>(1);
-  W.scan_counter = c.take<uint32_t>(8);
-  W.scan_status = c.take<uint64_t>(m / match::kCountTile + 2);
+  W.scan_status = c.take<uint64_t>(rtiles / (match::kScanThreads * match::kScanItems) + 2);
   W.part = c.take<uint64_t>(4 * (m / match::kCountTile + 2));
+  W.tile_sum = c.take<uint64_t>(rtiles);
+  W.tile_off = c.take<uint64_t>(rtiles);
   W.ulo_key = c.take<uint64_t>(m);
   W.ulo_id = c.take<uint32_t>(m);
   W.r_lo = c.take<uint32_t>(m);
   W.r_b = c.take<uint32_t>(m);
-  W.off = c.take<uint64_t>(m + 1);
   W.cnt0 = c.take<uint32_t>(m);
   if (d > 1) {
     W.cnt = c.take<uint32_t>(m);
     W.fstab = c.take<uint32_t>(m);
-    W.offd = c.take<uint64_t>(m + 1);
   }
   W.sort = sort_scratch(c, n_sub > m ? n_sub : m);
   W.bytes = c.used;
@@ -471,18 +470,21 @@ ddm_status match_indexed(const MatchReq& q, MatchWs& W, uint64_t* count_out, boo
   DDM_CUDA(cudaMemsetAsync(s.hist[2], 0, sizeof(uint32_t) * 8 * 256, st));
   DDM_TRY(validate_side(d, m, R->upd_lo, R->upd_hi, s.hist[2], nullptr, &W.misc->err, st));
   DDM_TRY(radix_sort(R->upd_lo[0], true, nullptr, W.ulo_key, W.ulo_id, m, full_passes(), s.hist[2], true, s, st));
-  // a4: counts by rank difference; a5: their exclusive scan (K = off[m])
+  // a4: counts by rank difference (+ the row-tile sums); a5: exclusive scan
+  // of the row-tile sums -> output offset of every 256-row tile, K
   const uint64_t ctiles = (m + match::kCountTile - 1) / match::kCountTile;
+  const uint64_t rtiles = (m + match::kRowTile - 1) / match::kRowTile;
+  const unsigned stiles = (unsigned)((rtiles + match::kScanThreads * match::kScanItems - 1) /
+                                     (match::kScanThreads * match::kScanItems));
   DDM_LAUNCH("count_partition", 0, st, match::count_partition_kernel<<<(unsigned)((ctiles + 255) / 256), 256, 0, st>>>(
       W.ulo_key, m, I.slo_key, I.shi_key, n, W.part));
   DDM_TRY(check_launch());
-  DDM_LAUNCH("count", 48.0 * m + 16.0 * n, st, match::count_kernel<<<(unsigned)ctiles, match::kCountThreads, sizeof(match::CountSmem), st>>>(
-      W.ulo_key, W.ulo_id, R->upd_hi[0], m, I.slo_key, I.shi_key, n, W.part, W.r_lo, W.r_b, W.cnt0));
+  DDM_LAUNCH("count", 56.0 * m + 16.0 * n, st, match::count_kernel<<<(unsigned)ctiles, match::kCountThreads, sizeof(match::CountSmem), st>>>(
+      W.ulo_key, W.ulo_id, R->upd_hi[0], m, I.slo_key, I.shi_key, n, W.part, W.r_lo, W.r_b, W.cnt0, W.tile_sum));
   DDM_TRY(check_launch());
-  DDM_CUDA(cudaMemsetAsync(W.scan_counter, 0, sizeof(uint32_t) * 8, st));
-  DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (ctiles + 1), st));
-  DDM_LAUNCH("scan", 12.0 * m, st, match::scan_u32_kernel<<<(unsigned)ctiles, match::kCountThreads, 0, st>>>(
-      W.cnt0, m, W.off, W.scan_status, W.scan_counter, d == 1 ? &W.misc->K : nullptr));
+  DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (stiles + 1), st));
+  DDM_LAUNCH("scan", 16.0 * rtiles, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
+      W.tile_sum, rtiles, W.tile_off, W.scan_status, d == 1 ? &W.misc->K : nullptr));
   DDM_TRY(check_launch());
 
   match::EmitArgs A{};
@@ -491,8 +493,9 @@ ddm_status match_indexed(const MatchReq& q, MatchWs& W, uint64_t* count_out, boo
   A.upd_map = q.upd_map;
   A.r_lo = W.r_lo;
   A.r_b = W.r_b;
-  A.off0 = W.off;
-  A.off = W.off;
+  A.cnt0 = W.cnt0;
+  A.cnt = W.cnt0;
+  A.tile_off = W.tile_off;
   A.slo_id = I.slo_id;
   A.T = tree_of(I);
   A.F.dims = (int)d - 1;
@@ -501,21 +504,23 @@ ddm_status match_indexed(const MatchReq& q, MatchWs& W, uint64_t* count_out, boo
   for (uint32_t k = 0; k < d; ++k) { A.upd.lo[k] = R->upd_lo[k]; A.upd.hi[k] = R->upd_hi[k]; }
   A.m = m;
   A.thread_row_max = 16;
-  A.force = (q.flags & DDM_EMIT_FORCE_THREAD) ? 1 : (q.flags & DDM_EMIT_FORCE_WARP) ? 2 : 0;
-  const unsigned egrid = (unsigned)((m + match::kEmitThreads - 1) / match::kEmitThreads);
+  A.force = (q.flags & DDM_EMIT_FORCE_THREAD) ? 1 : (q.flags & DDM_EMIT_FORCE_WARP) ? 2
+            : (q.flags & DDM_EMIT_FORCE_CHUNK) ? 3 : 0;
+  const unsigned egrid = (unsigned)rtiles;
 
   if (d > 1) {
     // a8: dim-0 candidates filtered on dims 1..d-1; count pass + scan
     A.cnt_out = W.cnt;
     A.fstab_out = W.fstab;
-    DDM_LAUNCH("count_dd", 44.0 * m, st, match::emit_kernel<match::kCountDD><<<egrid, match::kEmitThreads, 0, st>>>(A));
+    DDM_LAUNCH("count_dd", 44.0 * m, st, match::emit_kernel<match::kCountDD><<<egrid, match::kRowTile, 0, st>>>(A));
     DDM_TRY(check_launch());
-    DDM_CUDA(cudaMemsetAsync(W.scan_counter, 0, sizeof(uint32_t) * 8, st));
-    DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (ctiles + 1), st));
-    DDM_LAUNCH("scan", 12.0 * m, st, match::scan_u32_kernel<<<(unsigned)ctiles, match::kCountThreads, 0, st>>>(
-        W.cnt, m, W.offd, W.scan_status, W.scan_counter, &W.misc->K));
+    DDM_LAUNCH("row_tile_sum", 4.0 * m, st, match::row_tile_sum_kernel<<<egrid, match::kRowTile, 0, st>>>(W.cnt, m, W.tile_sum));
     DDM_TRY(check_launch());
-    A.off = W.offd;
+    DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (stiles + 1), st));
+    DDM_LAUNCH("scan", 16.0 * rtiles, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
+        W.tile_sum, rtiles, W.tile_off, W.scan_status, &W.misc->K));
+    DDM_TRY(check_launch());
+    A.cnt = W.cnt;
     A.fstab = W.fstab;
   }
   Misc h{};
@@ -529,12 +534,12 @@ ddm_status match_indexed(const MatchReq& q, MatchWs& W, uint64_t* count_out, boo
   A.pairs = reinterpret_cast<uint2*>(q.pairs);
   const bool per_row = (q.flags & (DDM_EMIT_FORCE_THREAD | DDM_EMIT_FORCE_WARP)) != 0;
   if (d == 1 && !per_row)
-    DDM_LAUNCH("emit", 44.0 * m + 8.0 * h.K, st, match::emit_chunk_kernel<<<(unsigned)((m + match::kChunkRows - 1) / match::kChunkRows),
-                                          match::kChunkRows, sizeof(match::ChunkSmem), st>>>(A));
+    DDM_LAUNCH("emit", 44.0 * m + 8.0 * h.K, st,
+               match::emit_chunk_kernel<<<egrid, match::kRowTile, sizeof(match::ChunkSmem), st>>>(A));
   else if (d == 1)
-    DDM_LAUNCH("emit", 44.0 * m + 8.0 * h.K, st, match::emit_kernel<match::kEmitD1><<<egrid, match::kEmitThreads, 0, st>>>(A));
+    DDM_LAUNCH("emit", 44.0 * m + 8.0 * h.K, st, match::emit_kernel<match::kEmitD1><<<egrid, match::kRowTile, 0, st>>>(A));
   else
-    DDM_LAUNCH("emit_dd", 44.0 * m + 8.0 * h.K, st, match::emit_kernel<match::kEmitDD><<<egrid, match::kEmitThreads, 0, st>>>(A));
+    DDM_LAUNCH("emit_dd", 44.0 * m + 8.0 * h.K, st, match::emit_kernel<match::kEmitDD><<<egrid, match::kRowTile, 0, st>>>(A));
   DDM_TRY(check_launch());
   return DDM_OK;
 }
@@ -760,7 +765,7 @@ int ddm_profile_read(ddm_kernel_stat* out, int cap) {
 }
 
 const char* ddm_build_info(void) {
-  return "libddm sm_100a onesweep-radix(8x8b, 4096/tile) count_scan(2048/tile) emit(thread|warp)";
+  return "libddm sm_100a onesweep-radix(8x8b) count(merge-path, 2048/tile) scan(row tiles) emit(chunk|thread|warp)";
 }
 
 }  // extern "C"

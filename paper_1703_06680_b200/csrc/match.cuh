@@ -175,6 +175,20 @@ __device__ __forceinline__ uint64_t ub_gallop(const uint64_t* __restrict__ a, ui
   return ub(a, lo, hi, x);
 }
 
+// lower bound of x in a[0..n) knowing a[start-1] < x: exponential probe.
+__device__ __forceinline__ uint64_t gallop_lb(const uint64_t* __restrict__ a, uint64_t n, uint64_t start,
+                                              uint64_t x) {
+  uint64_t lo = start, hi = n, step = 1;
+  while (true) {
+    const uint64_t probe = lo + step - 1;
+    if (probe >= n) break;
+    if (a[probe] >= x) { hi = probe; break; }
+    lo = probe + 1;
+    step <<= 1;
+  }
+  return lb(a, lo, hi, x);
+}
+
 // ------------------------------------------------------------ decoupled look-back scan
 
 constexpr uint64_t kScanAgg = 1ull << 62;
@@ -201,7 +215,10 @@ __device__ __forceinline__ uint64_t lookback_warp_u64(uint64_t* status, uint32_t
     const unsigned unpub = __ballot_sync(kFull, (s & ~kScanVal) == 0);
     const int first = pre ? __ffs(pre) - 1 : 31;
     const unsigned need = first == 31 ? kFull : ((2u << first) - 1u);
-    if (unpub & need) continue;  // some needed predecessor not published yet
+    if (unpub & need) {  // some needed predecessor not published yet: back off
+      __nanosleep(64);
+      continue;
+    }
     excl += warp_sum<uint64_t>(lane <= first && p >= 0 ? (s & kScanVal) : 0);
     if (pre) break;
     base -= 32;
@@ -215,56 +232,8 @@ constexpr int kCountItems = 8;
 constexpr int kCountTile = kCountThreads * kCountItems;
 constexpr int kCountWin = 4096;  // smem window (keys) per sorted array
 constexpr int kCountExt = 1024;  // Slo window extension past r_lo(a_last) for the r_b searches
-
-// first index in [lo, end) with a[i] > x (UPPER) or a[i] >= x (!UPPER),
-// galloping forward from lo; `end` if none.
-template <bool UPPER, typename P>
-__device__ __forceinline__ uint64_t gallop(P a, uint64_t lo, uint64_t end, uint64_t x) {
-  uint64_t hi = end, step = 1;
-  // short linear probe first: consecutive sorted queries usually move by ~1
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    if (lo >= end) return end;
-    const uint64_t v = a[lo];
-    if (UPPER ? v > x : v >= x) return lo;
-    ++lo;
-  }
-  while (true) {
-    const uint64_t p = lo + step - 1;
-    if (p >= end) break;
-    const uint64_t v = a[p];
-    if (UPPER ? v > x : v >= x) { hi = p; break; }
-    lo = p + 1;
-    step <<= 1;
-  }
-  while (lo < hi) {
-    const uint64_t mid = (lo + hi) >> 1;
-    const uint64_t v = a[mid];
-    if (UPPER ? v <= x : v < x) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
-
-// A sorted global array g[0..n) with the slice [base, base+len) staged in smem.
-struct Window {
-  const uint64_t* s;
-  const uint64_t* g;
-  uint64_t base, n;
-  uint32_t len;
-  // search from `start` (all entries before start are known to be "before" x)
-  template <bool UPPER>
-  __device__ __forceinline__ uint64_t search(uint64_t start, uint64_t x) const {
-    const uint64_t end = base + len;
-    if (start >= base && start < end) {
-      const uint64_t last = s[len - 1];
-      if (end == n || (UPPER ? last > x : last >= x))
-        return base + gallop<UPPER>(s, start - base, len, x);
-      start = end;
-    }
-    return gallop<UPPER>(g, start, n, x);
-  }
-};
+constexpr int kRowTile = 256;    // rows per emit CTA == granularity of the row-offset scan
+static_assert(kCountTile % kRowTile == 0, "count tile holds whole row tiles");
 
 // Per count tile: r_lo(a_first), r_lo(a_last), r_hi(a_first), r_hi(a_last)
 // (merge-path partition of the sorted updates against Slo and Shi).
@@ -288,17 +257,41 @@ struct CountSmem {
   uint64_t wh[kCountWin];
 };
 
-// a4 (G5): for every update j (in sorted Ulo order) compute r_lo, r_b and
-// cnt = r_b - r_hi (rank difference, I2); the exclusive scan of cnt (a5) is
-// scan_u32_kernel.  b_j = key(upd_hi[ulo_id[j]]) is gathered here (a3).  The tile's slices of Slo and Shi are staged in shared memory;
-// each thread owns 8 consecutive updates and gallops forward (a is sorted, so
-// r_lo and r_hi are monotone: a merge path), falling back to global memory
-// for any search that leaves the staged window.
-__global__ void __launch_bounds__(kCountThreads) count_kernel(
+// Advance a merge cursor: pos is an absolute index into the sorted array g
+// with every entry before pos "before" x (<= x for UPPER, < x otherwise);
+// returns the first index whose entry is "after" x.  The array's slice
+// [base, base+len) is staged in W (shared memory): short linear steps, then
+// a binary search inside the window, then (rarely) a gallop in global memory.
+template <bool UPPER>
+__device__ __forceinline__ uint64_t advance(const uint64_t* W, uint64_t base, uint32_t len, const uint64_t* g,
+                                            uint64_t n, uint64_t pos, uint64_t x) {
+  uint32_t k = pos >= base ? (uint32_t)umin64(pos - base, len) : 0;
+#pragma unroll 1
+  for (int s = 0; s < 6 && k < len; ++s) {
+    const uint64_t v = W[k];
+    if (UPPER ? v > x : v >= x) return base + k;
+    ++k;
+  }
+  if (k < len) {
+    const uint64_t v = W[len - 1];
+    if (UPPER ? v > x : v >= x) return base + (UPPER ? ub(W, k, len, x) : lb(W, k, len, x));
+  }
+  if (base + len >= n) return n;
+  return UPPER ? ub_gallop(g, n, base + len, x) : gallop_lb(g, n, base + len, x);
+}
+
+// a4 (G5): for every update j (sorted Ulo order) r_lo = #{S.lo <= a},
+// r_b = #{S.lo <= b} and cnt = r_b - r_hi with r_hi = #{S.hi < a} (the rank
+// difference of I2).  b_j = key(upd_hi[ulo_id[j]]) is gathered here (a3).
+// Each thread owns 8 consecutive updates: a binary search locates its first
+// one in the tile's staged Slo/Shi windows, then the cursors only move
+// forward (a is sorted: a merge path).  Also writes the count sum of every
+// 256-row tile (for the row-offset scan, a5).
+__global__ void __launch_bounds__(kCountThreads, 2) count_kernel(
     const uint64_t* __restrict__ ulo_key, const uint32_t* __restrict__ ulo_id, const double* __restrict__ upd_hi,
     uint64_t m, const uint64_t* __restrict__ slo_key, const uint64_t* __restrict__ shi_key, uint64_t n,
     const uint64_t* __restrict__ part, uint32_t* __restrict__ r_lo_out, uint32_t* __restrict__ r_b_out,
-    uint32_t* __restrict__ cnt_out) {
+    uint32_t* __restrict__ cnt_out, uint64_t* __restrict__ row_tile_sum) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CountSmem& S = *reinterpret_cast<CountSmem*>(smem_raw);
   const int tid = threadIdx.x;
@@ -306,38 +299,50 @@ __global__ void __launch_bounds__(kCountThreads) count_kernel(
   const uint64_t j0 = (uint64_t)tile * kCountTile;
   const uint64_t jn = umin64(kCountTile, m - j0);
   const uint64_t p0 = part[4 * tile + 0], p1 = part[4 * tile + 1], h0 = part[4 * tile + 2], h1 = part[4 * tile + 3];
-  Window WS{S.ws, slo_key, p0, n, (uint32_t)umin64(umin64(kCountWin, p1 - p0 + kCountExt), n - p0)};
-  Window WH{S.wh, shi_key, h0, n, (uint32_t)umin64(kCountWin, h1 - h0 + 1 < n - h0 ? h1 - h0 + 1 : n - h0)};
-  for (uint32_t i = tid; i < WS.len; i += kCountThreads) S.ws[i] = __ldcs(slo_key + p0 + i);
-  for (uint32_t i = tid; i < WH.len; i += kCountThreads) S.wh[i] = __ldcs(shi_key + h0 + i);
+  const uint64_t t0 = (uint64_t)tid * kCountItems;
+  const int ni = t0 < jn ? (int)umin64(kCountItems, jn - t0) : 0;
+  const uint64_t j = j0 + t0;
+  // issue this thread's loads first (the random upd_hi gather overlaps the
+  // window staging below)
+  uint64_t a[kCountItems], b[kCountItems];
+  {
+    uint32_t id[kCountItems];
+#pragma unroll
+    for (int i = 0; i < kCountItems; ++i) id[i] = i < ni ? __ldcs(ulo_id + j + i) : 0;
+    double hv[kCountItems];
+#pragma unroll
+    for (int i = 0; i < kCountItems; ++i) hv[i] = i < ni ? upd_hi[id[i]] : 0.0;
+#pragma unroll
+    for (int i = 0; i < kCountItems; ++i) a[i] = i < ni ? __ldcs(ulo_key + j + i) : 0;
+#pragma unroll
+    for (int i = 0; i < kCountItems; ++i) b[i] = f64_key(hv[i]);
+  }
+  const uint32_t ls = (uint32_t)umin64(umin64(kCountWin, p1 - p0 + kCountExt), n - p0);
+  const uint32_t lh = (uint32_t)umin64(kCountWin, umin64(h1 - h0 + 1, n - h0));
+  for (uint32_t i = tid; i < ls; i += kCountThreads) S.ws[i] = __ldcs(slo_key + p0 + i);
+  for (uint32_t i = tid; i < lh; i += kCountThreads) S.wh[i] = __ldcs(shi_key + h0 + i);
   __syncthreads();
 
-  const uint64_t t0 = (uint64_t)tid * kCountItems;
   uint32_t cnt[kCountItems];
 #pragma unroll
   for (int i = 0; i < kCountItems; ++i) cnt[i] = 0;
-  if (t0 < jn) {
-    const uint64_t j = j0 + t0;
-    const int ni = (int)umin64(kCountItems, jn - t0);
-    uint64_t a[kCountItems], b[kCountItems];
-#pragma unroll
-    for (int i = 0; i < kCountItems; ++i) {
-      a[i] = i < ni ? __ldcs(ulo_key + j + i) : 0;
-      b[i] = i < ni ? f64_key(upd_hi[__ldcs(ulo_id + j + i)]) : 0;  // a3: b of the sorted update
-    }
-    uint64_t rl = p0, rh = h0, rb = p0, prev_b = 0;
-    // locate the thread's first update by binary search inside the windows
-    if (WS.len && (WS.base + WS.len == n || S.ws[WS.len - 1] > a[0])) rl = p0 + ub(S.ws, 0, WS.len, a[0]);
-    if (WH.len && (WH.base + WH.len == n || S.wh[WH.len - 1] >= a[0])) rh = h0 + lb(S.wh, 0, WH.len, a[0]);
+  if (ni > 0) {
+    // first update: binary search inside the windows (falls back to global)
+    uint64_t rl = advance<true>(S.ws, p0, ls, slo_key, n,
+                                p0 + ((ls && S.ws[ls - 1] > a[0]) ? ub(S.ws, 0, ls, a[0]) : ls), a[0]);
+    uint64_t rh = advance<false>(S.wh, h0, lh, shi_key, n,
+                                 h0 + ((lh && S.wh[lh - 1] >= a[0]) ? lb(S.wh, 0, lh, a[0]) : lh), a[0]);
+    uint64_t rb = rl;
     uint32_t ol[kCountItems], ob[kCountItems];
 #pragma unroll
     for (int i = 0; i < kCountItems; ++i) {
       if (i < ni) {
-        rl = WS.search<true>(rl, a[i]);
-        rh = WH.search<false>(rh, a[i]);
-        const uint64_t start = (i && b[i] >= prev_b && rb > rl) ? rb : rl;
-        rb = WS.search<true>(start, b[i]);
-        prev_b = b[i];
+        if (i) {
+          rl = advance<true>(S.ws, p0, ls, slo_key, n, rl, a[i]);
+          rh = advance<false>(S.wh, h0, lh, shi_key, n, rh, a[i]);
+        }
+        const uint64_t start = (i && b[i] >= b[i - 1] && rb > rl) ? rb : rl;
+        rb = advance<true>(S.ws, p0, ls, slo_key, n, start, b[i]);
         ol[i] = (uint32_t)rl;
         ob[i] = (uint32_t)rb;
         cnt[i] = (uint32_t)(rb > rh ? rb - rh : 0);
@@ -346,52 +351,61 @@ __global__ void __launch_bounds__(kCountThreads) count_kernel(
     if (ni == kCountItems) {
       uint4* dl = reinterpret_cast<uint4*>(r_lo_out + j);
       uint4* db = reinterpret_cast<uint4*>(r_b_out + j);
+      uint4* dc = reinterpret_cast<uint4*>(cnt_out + j);
       dl[0] = make_uint4(ol[0], ol[1], ol[2], ol[3]);
       dl[1] = make_uint4(ol[4], ol[5], ol[6], ol[7]);
       db[0] = make_uint4(ob[0], ob[1], ob[2], ob[3]);
       db[1] = make_uint4(ob[4], ob[5], ob[6], ob[7]);
+      dc[0] = make_uint4(cnt[0], cnt[1], cnt[2], cnt[3]);
+      dc[1] = make_uint4(cnt[4], cnt[5], cnt[6], cnt[7]);
     } else {
 #pragma unroll
       for (int i = 0; i < kCountItems; ++i)
-        if (i < ni) { r_lo_out[j + i] = ol[i]; r_b_out[j + i] = ob[i]; }
+        if (i < ni) { r_lo_out[j + i] = ol[i]; r_b_out[j + i] = ob[i]; cnt_out[j + i] = cnt[i]; }
     }
   }
-  if (t0 + kCountItems <= jn) {
-    uint4* d = reinterpret_cast<uint4*>(cnt_out + j0 + t0);
-    d[0] = make_uint4(cnt[0], cnt[1], cnt[2], cnt[3]);
-    d[1] = make_uint4(cnt[4], cnt[5], cnt[6], cnt[7]);
-  } else {
-#pragma unroll
-    for (int i = 0; i < kCountItems; ++i)
-      if (t0 + i < jn) cnt_out[j0 + t0 + i] = cnt[i];
-  }
-}
-
-// Generic exclusive scan of u32 counts: off[j] = sum_{i<j} cnt[i], off[m] = total.
-__global__ void __launch_bounds__(kCountThreads) scan_u32_kernel(const uint32_t* __restrict__ cnt, uint64_t m,
-                                                                 uint64_t* __restrict__ off,
-                                                                 uint64_t* __restrict__ status,
-                                                                 uint32_t* __restrict__ tile_counter,
-                                                                 uint64_t* __restrict__ k_out) {
-  __shared__ uint64_t scan_tmp[kCountThreads / 32 + 1];
-  __shared__ uint64_t prefix;
-  __shared__ uint32_t tile_id;
-  const int tid = threadIdx.x;
-  if (tid == 0) tile_id = atomicAdd(tile_counter, 1u);
-  __syncthreads();
-  const uint32_t tile = tile_id;
-  const uint64_t j0 = (uint64_t)tile * kCountTile;
-  const uint64_t jn = umin64(kCountTile, m - j0);
-  uint32_t c[kCountItems];
+  // per 256-row tile sums (each row tile = 32 consecutive threads = one warp)
   uint64_t local = 0;
 #pragma unroll
-  for (int it = 0; it < kCountItems; ++it) {
-    const uint64_t t = (uint64_t)tid * kCountItems + it;
-    c[it] = t < jn ? cnt[j0 + t] : 0;
-    local += c[it];
+  for (int i = 0; i < kCountItems; ++i) local += cnt[i];
+  local = warp_sum<uint64_t>(local);
+  const uint64_t rt = (j0 + (uint64_t)(tid >> 5) * kRowTile);
+  if ((tid & 31) == 0 && rt < m) row_tile_sum[rt / kRowTile] = local;
+}
+
+// Sum of the counts of each 256-row tile (used after the d > 1 count pass).
+__global__ void __launch_bounds__(kRowTile) row_tile_sum_kernel(const uint32_t* __restrict__ cnt, uint64_t m,
+                                                                uint64_t* __restrict__ row_tile_sum) {
+  __shared__ uint64_t tmp[kRowTile / 32 + 1];
+  const uint64_t j = (uint64_t)blockIdx.x * kRowTile + threadIdx.x;
+  uint64_t total;
+  block_excl_scan<kRowTile>((uint64_t)(j < m ? cnt[j] : 0), tmp, &total);
+  if (threadIdx.x == 0) row_tile_sum[blockIdx.x] = total;
+}
+
+// a5: exclusive scan of the row-tile sums (T = ceil(m/256) values) -> the
+// output offset of each tile's first row; total K.  One CTA per 4096 sums,
+// chained by decoupled look-back (a few CTAs even at m = 1e9).
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 8;
+__global__ void __launch_bounds__(kScanThreads) scan_u64_kernel(const uint64_t* __restrict__ in, uint64_t T,
+                                                                uint64_t* __restrict__ out,
+                                                                uint64_t* __restrict__ status,
+                                                                uint64_t* __restrict__ k_out) {
+  __shared__ uint64_t scan_tmp[kScanThreads / 32 + 1];
+  __shared__ uint64_t prefix;
+  const int tid = threadIdx.x;
+  const uint32_t tile = blockIdx.x;  // tiles are processed in launch order; look-back only reads lower ids
+  const uint64_t base = (uint64_t)tile * kScanThreads * kScanItems + (uint64_t)tid * kScanItems;
+  uint64_t v[kScanItems];
+  uint64_t local = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = base + i < T ? in[base + i] : 0;
+    local += v[i];
   }
   uint64_t agg;
-  const uint64_t texcl = block_excl_scan<kCountThreads>(local, scan_tmp, &agg);
+  const uint64_t texcl = block_excl_scan<kScanThreads>(local, scan_tmp, &agg);
   if (tid < 32) {
     const uint64_t e = lookback_warp_u64(status, tile, agg);
     if (tid == 0) prefix = e;
@@ -399,15 +413,11 @@ __global__ void __launch_bounds__(kCountThreads) scan_u32_kernel(const uint32_t*
   __syncthreads();
   uint64_t run = prefix + texcl;
 #pragma unroll
-  for (int it = 0; it < kCountItems; ++it) {
-    const uint64_t t = (uint64_t)tid * kCountItems + it;
-    if (t < jn) off[j0 + t] = run;
-    run += c[it];
+  for (int i = 0; i < kScanItems; ++i) {
+    if (base + i < T) out[base + i] = run;
+    run += v[i];
   }
-  if (j0 + jn == m && tid == 0) {
-    off[m] = prefix + agg;
-    if (k_out) *k_out = prefix + agg;
-  }
+  if (tile == gridDim.x - 1 && tid == 0 && k_out) *k_out = prefix + agg;
 }
 
 // ------------------------------------------------------------ sweep + emit (a6 + a7, a8)
@@ -452,8 +462,9 @@ struct EmitArgs {
   const uint32_t* upd_map;  // optional: global id of each local update
   const uint32_t* r_lo;
   const uint32_t* r_b;
-  const uint64_t* off0;     // dim-0 row offsets (stab0 = cnt0 - range)
-  const uint64_t* off;      // output row offsets (== off0 for d == 1)
+  const uint32_t* cnt0;     // dim-0 candidate count per row (stab0 = cnt0 - range)
+  const uint32_t* cnt;      // output pairs per row (== cnt0 for d == 1)
+  const uint64_t* tile_off; // output offset of each 256-row tile
   const uint32_t* fstab;    // d > 1 emit: filtered stab count per row
   uint32_t* cnt_out;        // d > 1 count pass: filtered row count
   uint32_t* fstab_out;      // d > 1 count pass: filtered stab count
@@ -464,29 +475,51 @@ struct EmitArgs {
   uint2* pairs;             // {sub, upd}
   uint64_t m;
   uint32_t thread_row_max;  // rows with <= this many dim-0 candidates go thread-per-row
-  uint32_t force;           // 0 auto, 1 thread, 2 warp
+  uint32_t force;           // 0 auto, 1 thread, 2 warp, 3 chunk (staged) for every tile
 };
 
 enum EmitMode { kEmitD1 = 0, kCountDD = 1, kEmitDD = 2 };
 
-constexpr int kEmitThreads = 256;
+// Row offsets of one 256-row tile: ro[t] = tile_off + exclusive scan of cnt.
+struct RowSmem {
+  uint64_t ro[kRowTile + 1];
+  uint64_t tmp[kRowTile / 32 + 1];
+  uint32_t queue[kRowTile];
+  uint32_t qn;
+};
+
+template <int MODE>
+__device__ __forceinline__ void row_offsets(const EmitArgs& A, RowSmem& R, uint64_t j0) {
+  const uint64_t j = j0 + threadIdx.x;
+  if (MODE == kCountDD) {
+    if (threadIdx.x == 0) R.qn = 0;
+    __syncthreads();
+    return;
+  }
+  uint64_t total;
+  const uint64_t e = block_excl_scan<kRowTile>((uint64_t)(j < A.m ? A.cnt[j] : 0), R.tmp, &total);
+  const uint64_t base = A.tile_off[j0 / kRowTile];
+  R.ro[threadIdx.x] = base + e;
+  if (threadIdx.x == 0) {
+    R.ro[kRowTile] = base + total;
+    R.qn = 0;
+  }
+  __syncthreads();
+}
 
 // ---- one row, one thread
 template <int MODE>
-__device__ __forceinline__ void row_thread(const EmitArgs& A, uint64_t j) {
+__device__ __forceinline__ void row_thread(const EmitArgs& A, uint64_t j, uint64_t o) {
   const uint64_t a = A.ulo_key[j];
   const uint32_t lid = A.ulo_id[j];
   const uint32_t uid = A.upd_map ? A.upd_map[lid] : lid;
   const uint32_t rl = A.r_lo[j], rb = A.r_b[j];
-  const uint64_t c0 = A.off0[j + 1] - A.off0[j];
-  const uint32_t stab0 = (uint32_t)(c0 - (rb - rl));
+  const uint32_t stab0 = A.cnt0[j] - (rb - rl);
   UpdBox q;
   if (MODE != kEmitD1)
     for (int k = 0; k < A.F.dims; ++k) { q.lo[k] = A.upd.lo[k + 1][lid]; q.hi[k] = A.upd.hi[k + 1][lid]; }
-  const uint64_t o = MODE == kCountDD ? 0 : A.off[j];
   uint32_t fst = MODE == kEmitDD ? A.fstab[j] : stab0;  // write cursor (backwards) for the stab part
   uint32_t nst = 0;                                      // filtered stab members (count pass)
-  // stab part: backwards from rl-1, exactly stab0 dim-0 members
   int64_t i = (int64_t)rl - 1;
   uint32_t rem = stab0;
   while (rem) {
@@ -505,7 +538,6 @@ __device__ __forceinline__ void row_thread(const EmitArgs& A, uint64_t j) {
     }
     --i;
   }
-  // range part: Slo[rl, rb)
   if (MODE == kEmitD1) {
     for (uint32_t k = rl; k < rb; ++k) A.pairs[o + stab0 + (k - rl)] = make_uint2(A.slo_id[k], uid);
   } else {
@@ -523,17 +555,15 @@ __device__ __forceinline__ void row_thread(const EmitArgs& A, uint64_t j) {
 
 // ---- one row, one warp (coalesced 32-wide windows, ballot/popc compaction)
 template <int MODE>
-__device__ __forceinline__ void row_warp(const EmitArgs& A, uint64_t j, int lane) {
+__device__ __forceinline__ void row_warp(const EmitArgs& A, uint64_t j, uint64_t o, int lane) {
   const uint64_t a = A.ulo_key[j];
   const uint32_t lid = A.ulo_id[j];
   const uint32_t uid = A.upd_map ? A.upd_map[lid] : lid;
   const uint32_t rl = A.r_lo[j], rb = A.r_b[j];
-  const uint64_t c0 = A.off0[j + 1] - A.off0[j];
-  const uint32_t stab0 = (uint32_t)(c0 - (rb - rl));
+  const uint32_t stab0 = A.cnt0[j] - (rb - rl);
   UpdBox q;
   if (MODE != kEmitD1)
     for (int k = 0; k < A.F.dims; ++k) { q.lo[k] = A.upd.lo[k + 1][lid]; q.hi[k] = A.upd.hi[k + 1][lid]; }
-  const uint64_t o = MODE == kCountDD ? 0 : A.off[j];
   uint32_t fst = MODE == kEmitDD ? A.fstab[j] : stab0;
   uint32_t nst = 0;
   int64_t hi_excl = rl;
@@ -583,28 +613,29 @@ __device__ __forceinline__ void row_warp(const EmitArgs& A, uint64_t j, int lane
 // by whole warps, so both sparse (alpha ~ 1: ~1 pair per row) and dense rows
 // (alpha = 100: ~100 pairs per row) stream coalesced stores.
 template <int MODE>
-__global__ void __launch_bounds__(kEmitThreads) emit_kernel(EmitArgs A) {
-  __shared__ uint32_t queue[kEmitThreads];
-  __shared__ uint32_t qn;
+__global__ void __launch_bounds__(kRowTile) emit_kernel(EmitArgs A) {
+  __shared__ RowSmem R;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) qn = 0;
-  __syncthreads();
-  const uint64_t j = (uint64_t)blockIdx.x * kEmitThreads + tid;
+  const uint64_t j0 = (uint64_t)blockIdx.x * kRowTile;
+  row_offsets<MODE>(A, R, j0);
+  const uint64_t j = j0 + tid;
   if (j < A.m) {
-    const uint64_t c0 = A.off0[j + 1] - A.off0[j];
+    const uint32_t c0 = A.cnt0[j];
     const bool thread_row = A.force == 1 || (A.force == 0 && c0 <= A.thread_row_max);
-    if (thread_row) row_thread<MODE>(A, j);
-    else queue[atomicAdd(&qn, 1u)] = tid;
+    if (thread_row) row_thread<MODE>(A, j, MODE == kCountDD ? 0 : R.ro[tid]);
+    else if (c0) R.queue[atomicAdd(&R.qn, 1u)] = tid;
   }
   __syncthreads();
-  const uint32_t nq = qn;
-  for (uint32_t q = warp; q < nq; q += kEmitThreads / 32)
-    row_warp<MODE>(A, (uint64_t)blockIdx.x * kEmitThreads + queue[q], lane);
+  const uint32_t nq = R.qn;
+  for (uint32_t q = warp; q < nq; q += kRowTile / 32) {
+    const uint32_t t = R.queue[q];
+    row_warp<MODE>(A, j0 + t, MODE == kCountDD ? 0 : R.ro[t], lane);
+  }
 }
 
 // ------------------------------------------------------------ chunked sweep (a6 + a7)
 //
-// One CTA per tile of kChunkRows consecutive updates (sorted order), the
+// One CTA per tile of kRowTile consecutive updates (sorted order), the
 // GPU form of Alg. 5's segments with Alg. 6's initial set
 // at the tile's first query point x_t = a_{j0}:
 //   A_t = Stab(x_t) = { S : S.lo <= x_t <= S.hi }  -- the chunk-start set,
@@ -614,21 +645,18 @@ __global__ void __launch_bounds__(kEmitThreads) emit_kernel(EmitArgs A) {
 // [r_lo(x_t), r_lo(a_j)), and every range member is in [r_lo(a_j), r_b(a_j)),
 // so the tile stages A_t and the contiguous Slo slice (ids + upper keys) in
 // shared memory once and all its rows are swept from there: short rows by one
-// thread, long rows by one warp (ballot/popc compaction), every store
-// coalesced.  Output is byte-identical to the per-row paths.
+// thread, long rows by one warp (ballot/popc compaction).  Output is
+// byte-identical to the per-row paths.
 
-constexpr int kChunkRows = 256;
-constexpr int kChunkSlice = 3072;
-constexpr int kChunkAct = 1024;
+constexpr int kChunkSlice = 1280;
+constexpr int kChunkAct = 512;
 
 struct ChunkSmem {
   uint64_t shi[kChunkSlice];
   uint64_t ahi[kChunkAct];
   uint32_t sid[kChunkSlice];
   uint32_t aid[kChunkAct];
-  uint32_t queue[kChunkRows];
-  uint64_t red[kChunkRows / 32];
-  uint32_t qn;
+  RowSmem R;
   uint32_t nact;
   uint32_t slen;
 };
@@ -643,34 +671,33 @@ __device__ __forceinline__ uint32_t c_id(const ChunkSmem& S, const EmitArgs& A, 
   return k < S.slen ? S.sid[k] : A.slo_id[i];
 }
 
-__device__ __forceinline__ void chunk_row_thread(const ChunkSmem& S, const EmitArgs& A, uint64_t j, uint64_t rl0) {
+__device__ __forceinline__ void chunk_row_thread(const ChunkSmem& S, const EmitArgs& A, uint64_t j, uint64_t o,
+                                                 uint64_t rl0) {
   const uint64_t a = A.ulo_key[j];
   const uint32_t lid = A.ulo_id[j];
   const uint32_t uid = A.upd_map ? A.upd_map[lid] : lid;
   const uint64_t rl = A.r_lo[j], rb = A.r_b[j];
-  const uint64_t o = A.off[j];
-  const uint32_t stab = (uint32_t)((A.off[j + 1] - o) - (rb - rl));
+  const uint32_t stab = (uint32_t)(A.cnt[j] - (rb - rl));
   // members of A_t still alive at a (ascending Slo order)
   uint32_t w = 0;
   for (uint32_t k = 0; k < S.nact && w < stab; ++k)
     if (S.ahi[k] >= a) A.pairs[o + (w++)] = make_uint2(S.aid[k], uid);
   // the rest of the stab part lies in the slice [rl0, rl): walk it backwards
   uint32_t need = stab - w;
-  for (uint64_t i = rl; need; ) {
+  for (uint64_t i = rl; need;) {
     --i;
     if (c_hi(S, A, rl0, i) >= a) A.pairs[o + w + (--need)] = make_uint2(c_id(S, A, rl0, i), uid);
   }
   for (uint64_t i = rl; i < rb; ++i) A.pairs[o + stab + (i - rl)] = make_uint2(c_id(S, A, rl0, i), uid);
 }
 
-__device__ __forceinline__ void chunk_row_warp(const ChunkSmem& S, const EmitArgs& A, uint64_t j, uint64_t rl0,
-                                               int lane) {
+__device__ __forceinline__ void chunk_row_warp(const ChunkSmem& S, const EmitArgs& A, uint64_t j, uint64_t o,
+                                               uint64_t rl0, int lane) {
   const uint64_t a = A.ulo_key[j];
   const uint32_t lid = A.ulo_id[j];
   const uint32_t uid = A.upd_map ? A.upd_map[lid] : lid;
   const uint64_t rl = A.r_lo[j], rb = A.r_b[j];
-  const uint64_t o = A.off[j];
-  const uint32_t stab = (uint32_t)((A.off[j + 1] - o) - (rb - rl));
+  const uint32_t stab = (uint32_t)(A.cnt[j] - (rb - rl));
   uint32_t w = 0;
   for (uint32_t k0 = 0; k0 < S.nact && w < stab; k0 += 32) {
     const uint32_t k = k0 + lane;
@@ -693,83 +720,83 @@ __device__ __forceinline__ void chunk_row_warp(const ChunkSmem& S, const EmitArg
   for (uint64_t i = rl + lane; i < rb; i += 32) A.pairs[o + stab + (i - rl)] = make_uint2(c_id(S, A, rl0, i), uid);
 }
 
-__global__ void __launch_bounds__(kChunkRows) emit_chunk_kernel(EmitArgs A) {
+__global__ void __launch_bounds__(kRowTile) emit_chunk_kernel(EmitArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ChunkSmem& S = *reinterpret_cast<ChunkSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint64_t j0 = (uint64_t)blockIdx.x * kChunkRows;
-  const uint64_t jn = umin64(kChunkRows, A.m - j0);
+  const uint64_t j0 = (uint64_t)blockIdx.x * kRowTile;
+  const uint64_t jn = umin64(kRowTile, A.m - j0);
   const uint64_t rl0 = A.r_lo[j0];
-  // slice end: max r_b over the tile
-  uint64_t rmax = tid < jn ? A.r_b[j0 + tid] : 0;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const uint64_t v = __shfl_xor_sync(kFull, rmax, o);
-    rmax = v > rmax ? v : rmax;
-  }
-  if (lane == 0) S.red[warp] = rmax;
-  if (tid == 0) S.qn = 0;
-  __syncthreads();
-  if (tid == 0) {
-    uint64_t r = 0;
-    for (int w = 0; w < kChunkRows / 32; ++w) r = S.red[w] > r ? S.red[w] : r;
-    S.slen = (uint32_t)umin64(kChunkSlice, r > rl0 ? r - rl0 : 0);
-  }
+  // slice [rl0, rl0 + slen): covers the stab candidates of every row (up to
+  // r_lo of the last row) and, when room allows, the range parts; entries past
+  // the slice are read from global memory.
+  const uint32_t slen = (uint32_t)umin64(kChunkSlice, A.r_b[j0 + jn - 1] - rl0);
   // a6: the chunk-start set A_t = Stab(x_t), |A_t| = stab(j0) known exactly
   const uint64_t x = A.ulo_key[j0];
-  const uint32_t nact = (uint32_t)((A.off[j0 + 1] - A.off[j0]) - (A.r_b[j0] - rl0));
-  const bool fits = nact <= kChunkAct;
-  if (warp == 0 && fits) {
-    int64_t hi_excl = (int64_t)rl0;
-    uint32_t rem = nact;
-    while (rem) {
-      const int64_t i = hi_excl - 1;
-      if ((i & 31) == 31) {
-        const int L = skip_levels(A.T, i, x);
-        if (L) { hi_excl -= (int64_t)1 << (5 * L); continue; }
-      }
-      const int64_t base = i & ~31ll;
-      const int64_t idx = base + lane;
-      uint64_t h = 0;
-      const bool member = idx < hi_excl && (h = A.T.lvl[0][idx]) >= x;
-      const unsigned mm = __ballot_sync(kFull, member);
-      rem -= __popc(mm);
-      if (member) {
-        const uint32_t pos = rem + __popc(mm & lanemask_lt());
-        S.ahi[pos] = h;
-        S.aid[pos] = A.slo_id[idx];
-      }
-      hi_excl = base;
-    }
-    if (lane == 0) S.nact = nact;
+  const uint32_t nact = A.cnt[j0] - (A.r_b[j0] - (uint32_t)rl0);
+  row_offsets<kEmitD1>(A, S.R, j0);
+  // sparse tiles (a few pairs per row) gain nothing from staging: rows go
+  // straight to the per-row walks; so do tiles whose A_t exceeds smem
+  const bool sparse = A.force == 0 && S.R.ro[kRowTile] - S.R.ro[0] <= 4ull * kRowTile;
+  const bool fits = nact <= kChunkAct && !sparse;
+  if (tid == 0) {
+    S.slen = slen;
+    S.nact = nact;
   }
-  __syncthreads();
-  // stage the Slo slice [rl0, rl0 + slen): ids and upper keys
-  const uint32_t slen = S.slen;
-  for (uint32_t k = tid; k < slen; k += kChunkRows) {
-    S.shi[k] = __ldcs(A.T.lvl[0] + rl0 + k);
-    S.sid[k] = __ldcs(A.slo_id + rl0 + k);
+  if (warp == 0) {
+    if (fits) {  // warp 0 walks Slo backwards from r_lo(x_t) with block-max skips
+      int64_t hi_excl = (int64_t)rl0;
+      uint32_t rem = nact;
+      while (rem) {
+        const int64_t i = hi_excl - 1;
+        if ((i & 31) == 31) {
+          const int L = skip_levels(A.T, i, x);
+          if (L) { hi_excl -= (int64_t)1 << (5 * L); continue; }
+        }
+        const int64_t base = i & ~31ll;
+        const int64_t idx = base + lane;
+        uint64_t h = 0;
+        const bool member = idx < hi_excl && (h = A.T.lvl[0][idx]) >= x;
+        const unsigned mm = __ballot_sync(kFull, member);
+        rem -= __popc(mm);
+        if (member) {
+          const uint32_t pos = rem + __popc(mm & lanemask_lt());
+          S.ahi[pos] = h;
+          S.aid[pos] = A.slo_id[idx];
+        }
+        hi_excl = base;
+      }
+    }
+  } else if (fits) {  // the other warps stage the Slo slice meanwhile
+    for (uint32_t k = tid - 32; k < slen; k += kRowTile - 32) {
+      S.shi[k] = __ldcs(A.T.lvl[0] + rl0 + k);
+      S.sid[k] = __ldcs(A.slo_id + rl0 + k);
+    }
   }
   __syncthreads();
   const uint64_t j = j0 + tid;
   if (!fits) {  // chunk-start set too large for shared memory: per-row global walks
     if (j < A.m) {
-      const uint64_t c0 = A.off[j + 1] - A.off[j];
-      if (c0 <= A.thread_row_max) row_thread<kEmitD1>(A, j);
-      else S.queue[atomicAdd(&S.qn, 1u)] = tid;
+      const uint32_t c0 = A.cnt0[j];
+      if (c0 <= A.thread_row_max) row_thread<kEmitD1>(A, j, S.R.ro[tid]);
+      else if (c0) S.R.queue[atomicAdd(&S.R.qn, 1u)] = tid;
     }
     __syncthreads();
-    for (uint32_t q = warp; q < S.qn; q += kChunkRows / 32) row_warp<kEmitD1>(A, j0 + S.queue[q], lane);
+    for (uint32_t q = warp; q < S.R.qn; q += kRowTile / 32)
+      row_warp<kEmitD1>(A, j0 + S.R.queue[q], S.R.ro[S.R.queue[q]], lane);
     return;
   }
   if (j < A.m) {
-    const uint64_t c = A.off[j + 1] - A.off[j];
-    if (c <= A.thread_row_max && nact <= 32) chunk_row_thread(S, A, j, rl0);
-    else if (c) S.queue[atomicAdd(&S.qn, 1u)] = tid;
+    const uint32_t c = A.cnt[j];
+    if (c <= A.thread_row_max && nact <= 32) chunk_row_thread(S, A, j, S.R.ro[tid], rl0);
+    else if (c) S.R.queue[atomicAdd(&S.R.qn, 1u)] = tid;
   }
   __syncthreads();
-  const uint32_t nq = S.qn;
-  for (uint32_t q = warp; q < nq; q += kChunkRows / 32) chunk_row_warp(S, A, j0 + S.queue[q], rl0, lane);
+  const uint32_t nq = S.R.qn;
+  for (uint32_t q = warp; q < nq; q += kRowTile / 32) {
+    const uint32_t t = S.R.queue[q];
+    chunk_row_warp(S, A, j0 + t, S.R.ro[t], rl0, lane);
+  }
 }
 
 // ------------------------------------------------------------ pair canonical key

@@ -215,6 +215,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for(ITEMS))
         hit_pre = (v & kFlagPre) != 0;
       }
       if (hit_pre) break;
+      if (consumed == 0) __nanosleep(32);  // predecessor not published yet: back off
       p -= consumed;
     }
     st_relaxed_u32(my_status, kFlagPre | (excl + total));
