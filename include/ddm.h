@@ -85,6 +85,11 @@ typedef struct {
 #define DDM_EMIT_FORCE_THREAD (1u << 8) /* one thread per update row */
 #define DDM_EMIT_FORCE_WARP (1u << 9)   /* one warp per update row, global scan */
 #define DDM_EMIT_FORCE_CHUNK (1u << 10) /* chunk-start sets staged in smem */
+/* Sort selection: by default the value-bucketed MSD sort (payload carried,
+ * no gathers) runs and falls back to the LSB radix sort + gathers if some
+ * bucket exceeds shared memory; this flag forces the LSB path.  Output is
+ * identical either way. */
+#define DDM_SORT_LSB (1u << 12)
 
 /* Workspace bytes needed by ddm_match_count (want_pairs = 0) or
  * ddm_match_pairs (want_pairs != 0) for these sizes.  Independent of K. */

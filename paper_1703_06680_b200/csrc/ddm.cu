@@ -11,6 +11,7 @@
 // The subscription half forms the byte-copyable "index" (multi-GPU: built by
 // one rank and broadcast).
 #include <atomic>
+#include <cmath>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -22,6 +23,7 @@
 #include "common.cuh"
 #include "match.cuh"
 #include "radix.cuh"
+#include "msd.cuh"
 
 using namespace ddm;
 
@@ -168,6 +170,15 @@ MaxTree tree_of(const Index& I) {
 
 // ------------------------------------------------------------ sort scratch
 
+// bucket bits of the MSD sort: ~768 records per bucket on average
+int msd_bits(uint64_t n) {
+  if (n <= 768) return 1;
+  const double b = std::log2((double)n / 768.0);
+  int r = (int)std::lround(b);
+  return r < 1 ? 1 : r > 24 ? 24 : r;
+}
+
+
 struct SortScratch {
   uint32_t* hist[3];   // [8][256] each: Slo, Shi, Ulo (or generic)
   uint32_t* starts;    // [8][256] global bin starts of the sort in flight
@@ -175,6 +186,16 @@ struct SortScratch {
   uint32_t* counters;  // [8]
   uint64_t* alt_keys;
   uint32_t* alt_vals;
+  // value-bucketed MSD sort
+  uint32_t* bhist;     // [NB] bucket histogram
+  uint32_t* bstarts;   // [NB + 1]
+  uint32_t* span_lo;   // [spans + 1]
+  uint32_t* dh;        // [3][256] digit histograms of the bucket id
+  uint64_t* bstatus;   // bucket-scan look-back words
+  uint64_t* mm;        // [3][2] min/max keys (Slo, Shi, Ulo)
+  uint64_t* alt_keys2;
+  uint64_t* alt_v64[2];
+  uint32_t* alt_vals2;
   uint64_t cap;
 };
 
@@ -186,6 +207,17 @@ SortScratch sort_scratch(Carver& c, uint64_t cap) {
   s.counters = c.take<uint32_t>(radix::kMaxPasses);
   s.alt_keys = c.take<uint64_t>(cap);
   s.alt_vals = c.take<uint32_t>(cap);
+  const uint64_t nb = 1ull << msd_bits(cap);
+  s.bhist = c.take<uint32_t>(nb);
+  s.bstarts = c.take<uint32_t>(nb + 1);
+  s.span_lo = c.take<uint32_t>(cap / msd::kSpan + 2);
+  s.dh = c.take<uint32_t>(3 * 256);
+  s.bstatus = c.take<uint64_t>(nb / (msd::kThreads * msd::kBScanItems) + 2);
+  s.mm = c.take<uint64_t>(6);
+  s.alt_keys2 = c.take<uint64_t>(cap);
+  s.alt_v64[0] = c.take<uint64_t>(cap);
+  s.alt_v64[1] = c.take<uint64_t>(cap);
+  s.alt_vals2 = c.take<uint32_t>(cap);
   s.cap = cap;
   return s;
 }
@@ -193,11 +225,16 @@ SortScratch sort_scratch(Carver& c, uint64_t cap) {
 struct Misc {  // device-side results read back with one copy
   uint64_t K;
   uint32_t err;
-  uint32_t pad;
+  uint32_t overflow;  // an MSD bucket exceeded shared memory: redo with the LSB sort
 };
+
+constexpr ddm_status kRetryLSB = (ddm_status)100;  // internal
+
+
 
 struct MatchWs {
   uint64_t* ulo_key;
+  uint64_t* uhi;       // upper keys in Ulo order (MSD path)
   uint32_t* ulo_id;
   uint32_t* r_lo;
   uint32_t* r_b;
@@ -223,6 +260,7 @@ MatchWs match_layout(uint32_t d, uint64_t n_sub, uint64_t m, void* base) {
   W.tile_sum = c.take<uint64_t>(rtiles);
   W.tile_off = c.take<uint64_t>(rtiles);
   W.ulo_key = c.take<uint64_t>(m);
+  W.uhi = c.take<uint64_t>(m);
   W.ulo_id = c.take<uint32_t>(m);
   W.r_lo = c.take<uint32_t>(m);
   W.r_b = c.take<uint32_t>(m);
@@ -273,6 +311,18 @@ void init_attrs_once() {
                        (int)sizeof(match::CountSmem));
   cudaFuncSetAttribute(match::emit_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(match::ChunkSmem));
+  cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(msd::PassSmem<msd::kItems, true, true>));
+  cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(msd::PassSmem<msd::kItems, true, true>));
+  cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(msd::PassSmem<msd::kItems, false, false>));
+  cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(msd::PassSmem<msd::kItems, false, false>));
+  cudaFuncSetAttribute(msd::local_sort_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(msd::LocalSmem<true, true>));
+  cudaFuncSetAttribute(msd::local_sort_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(msd::LocalSmem<false, false>));
   if (const char* e = getenv("DDM_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(e));
   done = true;
 }
@@ -370,6 +420,83 @@ ddm_status radix_sort(const void* src, bool src_f64, const uint32_t* vals_in, ui
   return DDM_OK;
 }
 
+// Value-bucketed MSD sort (msd.cuh) of n float64 keys `src` with optional
+// payload: the upper coordinate `v64_src` (encoded to keys) and the index.
+// mm = the keys' [min, max] (from validation).  Sets *overflow on a bucket
+// too large for shared memory (caller falls back to radix_sort + gather).
+template <bool PAY>
+ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, const uint64_t* mm, uint64_t* out_key,
+                      uint64_t* out_v64, uint32_t* out_v32, SortScratch& s, uint32_t* overflow, cudaStream_t st) {
+  const int bits = msd_bits(n);
+  const uint32_t nb = 1u << bits;
+  const int passes = (bits + 7) / 8;
+  DDM_CUDA(cudaMemsetAsync(s.bhist, 0, sizeof(uint32_t) * nb, st));
+  DDM_CUDA(cudaMemsetAsync(s.dh, 0, sizeof(uint32_t) * 3 * 256, st));
+  DDM_LAUNCH("msd_hist", 8.0 * n, st, msd::bucket_hist_kernel<true><<<grid_for(n, 256, 8), 256, 0, st>>>(src, n, mm, bits, s.bhist));
+  DDM_TRY(check_launch());
+  DDM_LAUNCH("msd_digit_hist", 4.0 * nb, st, msd::digit_hist_kernel<<<grid_for(nb, 256, 2), 256, 0, st>>>(s.bhist, nb, passes, s.dh));
+  DDM_TRY(check_launch());
+  DDM_LAUNCH("radix_bin_start", 0, st, radix::bin_start_kernel<<<passes, radix::kRadix, 0, st>>>(s.dh, s.starts));
+  DDM_TRY(check_launch());
+  const unsigned bt = (unsigned)((nb + msd::kThreads * msd::kBScanItems - 1) / (msd::kThreads * msd::kBScanItems));
+  DDM_CUDA(cudaMemsetAsync(s.bstatus, 0, sizeof(uint64_t) * (bt + 1), st));
+  DDM_LAUNCH("msd_bucket_scan", 8.0 * nb, st, msd::bucket_scan_kernel<<<bt, msd::kThreads, 0, st>>>(s.bhist, nb, s.bstarts, s.bstatus));
+  DDM_TRY(check_launch());
+  const uint32_t spans = (uint32_t)((n + msd::kSpan - 1) / msd::kSpan);
+  DDM_LAUNCH("msd_spans", 0, st, msd::span_kernel<<<(spans + 256) / 256, 256, 0, st>>>(s.bstarts, nb, n, spans, s.span_lo));
+  DDM_TRY(check_launch());
+  uint64_t* bk[2] = {s.alt_keys, s.alt_keys2};
+  uint64_t* bv[2] = {s.alt_v64[0], s.alt_v64[1]};
+  uint32_t* bi[2] = {s.alt_vals, s.alt_vals2};
+  const uint64_t tiles = (n + msd::kTile - 1) / msd::kTile;
+  DDM_CUDA(cudaMemsetAsync(s.counters, 0, sizeof(uint32_t) * radix::kMaxPasses, st));
+  for (int p = 0; p < passes; ++p) {
+    DDM_CUDA(cudaMemsetAsync(s.status, 0, sizeof(uint32_t) * radix::kRadix * tiles, st));
+    const int o = p & 1, q = (p - 1) & 1;
+    const double bytes = (double)n * (PAY ? (p == 0 ? 16.0 + 20.0 : 40.0) : 16.0);
+    if (p == 0) {
+      if (PAY)
+        DDM_LAUNCH("msd_pass_pay", bytes, st, msd::msd_pass_kernel<msd::kItems, true, true, true>
+                   <<<(unsigned)tiles, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, true, true>), st>>>(
+                       src, v64_src, nullptr, bk[o], bv[o], bi[o], n, mm, bits, 8 * p, s.starts + p * 256, s.status,
+                       s.counters + p));
+      else
+        DDM_LAUNCH("msd_pass", bytes, st, msd::msd_pass_kernel<msd::kItems, false, false, true>
+                   <<<(unsigned)tiles, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, false, false>), st>>>(
+                       src, nullptr, nullptr, bk[o], nullptr, nullptr, n, mm, bits, 8 * p, s.starts + p * 256, s.status,
+                       s.counters + p));
+    } else {
+      if (PAY)
+        DDM_LAUNCH("msd_pass_pay", bytes, st, msd::msd_pass_kernel<msd::kItems, true, true, false>
+                   <<<(unsigned)tiles, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, true, true>), st>>>(
+                       bk[q], bv[q], bi[q], bk[o], bv[o], bi[o], n, mm, bits, 8 * p, s.starts + p * 256, s.status,
+                       s.counters + p));
+      else
+        DDM_LAUNCH("msd_pass", bytes, st, msd::msd_pass_kernel<msd::kItems, false, false, false>
+                   <<<(unsigned)tiles, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, false, false>), st>>>(
+                       bk[q], nullptr, nullptr, bk[o], nullptr, nullptr, n, mm, bits, 8 * p, s.starts + p * 256, s.status,
+                       s.counters + p));
+    }
+    DDM_TRY(check_launch());
+  }
+  const int l = (passes - 1) & 1;
+  if (PAY)
+    DDM_LAUNCH("msd_local_pay", 40.0 * n, st, msd::local_sort_kernel<true, true>
+               <<<spans, msd::kThreads, sizeof(msd::LocalSmem<true, true>), st>>>(
+                   bk[l], bv[l], bi[l], out_key, out_v64, out_v32, s.bstarts, nb, s.span_lo, mm, bits, overflow));
+  else
+    DDM_LAUNCH("msd_local", 16.0 * n, st, msd::local_sort_kernel<false, false>
+               <<<spans, msd::kThreads, sizeof(msd::LocalSmem<false, false>), st>>>(
+                   bk[l], nullptr, nullptr, out_key, nullptr, nullptr, s.bstarts, nb, s.span_lo, mm, bits, overflow));
+  return check_launch();
+}
+
+ddm_status init_minmax(uint64_t* mm, cudaStream_t st) {  // [min, max] x 3 = [~0, 0] x 3
+  DDM_CUDA(cudaMemsetAsync(mm, 0xff, 6 * sizeof(uint64_t), st));
+  for (int k = 0; k < 3; ++k) DDM_CUDA(cudaMemsetAsync(mm + 2 * k + 1, 0, sizeof(uint64_t), st));
+  return DDM_OK;
+}
+
 // ------------------------------------------------------------ argument checks
 
 bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
@@ -397,11 +524,13 @@ ddm_status err_status(uint32_t e) {
 
 // validate all dims of one side; histogram dim 0 into hist_lo / hist_hi
 ddm_status validate_side(uint32_t d, uint64_t cnt, const double* const* lo, const double* const* hi,
-                         uint32_t* hist_lo, uint32_t* hist_hi, uint32_t* err, cudaStream_t st) {
+                         uint32_t* hist_lo, uint32_t* hist_hi, uint32_t* err, cudaStream_t st,
+                         uint64_t* mm_lo = nullptr, uint64_t* mm_hi = nullptr) {
   if (cnt == 0) return DDM_OK;
   for (uint32_t k = 0; k < d; ++k) {
     DDM_LAUNCH("validate_hist", 16.0 * cnt, st, match::validate_hist_kernel<<<grid_for(cnt, 512, 4), 512, 0, st>>>(
-        lo[k], hi[k], cnt, k == 0 ? hist_lo : nullptr, k == 0 ? hist_hi : nullptr, err));
+        lo[k], hi[k], cnt, k == 0 ? hist_lo : nullptr, k == 0 ? hist_hi : nullptr, err, k == 0 ? mm_lo : nullptr,
+        k == 0 ? mm_hi : nullptr));
     DDM_TRY(check_launch());
   }
   return DDM_OK;
@@ -409,25 +538,40 @@ ddm_status validate_side(uint32_t d, uint64_t cnt, const double* const* lo, cons
 
 // ------------------------------------------------------------ index build (async)
 
-ddm_status build_index_async(const ddm_regions* R, const Index& I, SortScratch& s, uint32_t* err,
+ddm_status build_index_async(const ddm_regions* R, const Index& I, SortScratch& s, Misc* misc, bool use_msd,
                              cudaStream_t st) {
+  init_attrs_once();
   const uint64_t n = R->n_sub;
   if (n == 0) return DDM_OK;
-  DDM_CUDA(cudaMemsetAsync(s.hist[0], 0, sizeof(uint32_t) * 8 * 256, st));
-  DDM_CUDA(cudaMemsetAsync(s.hist[1], 0, sizeof(uint32_t) * 8 * 256, st));
-  DDM_TRY(validate_side(R->d, n, R->sub_lo, R->sub_hi, s.hist[0], s.hist[1], err, st));
-  const radix::PassList P = full_passes();
-  // a2: Slo (key + sub id, encoded from float64 in pass 1), Shi (keys)
-  DDM_TRY(radix_sort(R->sub_lo[0], true, nullptr, I.slo_key, I.slo_id, n, P, s.hist[0], true, s, st));
-  DDM_TRY(radix_sort(R->sub_hi[0], true, nullptr, I.shi_key, nullptr, n, P, s.hist[1], true, s, st));
-  // a3: slo_hi[i] = key(sub_hi[slo_id[i]]) + block maxima
-  DDM_LAUNCH("gather_slo_hi", 20.0 * n, st, match::gather_key_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.slo_id, R->sub_hi[0], n,
-                                                                             I.slo_hi, I.levels ? I.lvl[1] : nullptr));
-  DDM_TRY(check_launch());
-  for (int L = 2; L <= I.levels; ++L) {
-    DDM_LAUNCH("block_max", 8.0 * I.lvl_n[L - 1], st, match::block_max_kernel<<<grid_for(I.lvl_n[L - 1], 256, 8), 256, 0, st>>>(
-        I.lvl[L - 1], I.lvl_n[L - 1], I.lvl[L]));
+  if (use_msd) {
+    DDM_TRY(init_minmax(s.mm, st));
+    DDM_TRY(validate_side(R->d, n, R->sub_lo, R->sub_hi, nullptr, nullptr, &misc->err, st, s.mm + 0, s.mm + 2));
+    // a2 + a3: Slo with the upper key and the id as payload, then Shi keys
+    DDM_TRY(msd_sort_t<true>(R->sub_lo[0], R->sub_hi[0], n, s.mm + 0, I.slo_key, I.slo_hi, I.slo_id, s,
+                             &misc->overflow, st));
+    DDM_TRY(msd_sort_t<false>(R->sub_hi[0], nullptr, n, s.mm + 2, I.shi_key, nullptr, nullptr, s, &misc->overflow, st));
+    for (int L = 1; L <= I.levels; ++L) {
+      DDM_LAUNCH("block_max", 8.0 * I.lvl_n[L - 1], st, match::block_max_kernel<<<grid_for(I.lvl_n[L - 1], 256, 8), 256, 0, st>>>(
+          I.lvl[L - 1], I.lvl_n[L - 1], I.lvl[L]));
+      DDM_TRY(check_launch());
+    }
+  } else {
+    DDM_CUDA(cudaMemsetAsync(s.hist[0], 0, sizeof(uint32_t) * 8 * 256, st));
+    DDM_CUDA(cudaMemsetAsync(s.hist[1], 0, sizeof(uint32_t) * 8 * 256, st));
+    DDM_TRY(validate_side(R->d, n, R->sub_lo, R->sub_hi, s.hist[0], s.hist[1], &misc->err, st));
+    const radix::PassList P = full_passes();
+    // a2: Slo (key + sub id, encoded from float64 in pass 1), Shi (keys)
+    DDM_TRY(radix_sort(R->sub_lo[0], true, nullptr, I.slo_key, I.slo_id, n, P, s.hist[0], true, s, st));
+    DDM_TRY(radix_sort(R->sub_hi[0], true, nullptr, I.shi_key, nullptr, n, P, s.hist[1], true, s, st));
+    // a3: slo_hi[i] = key(sub_hi[slo_id[i]]) + block maxima
+    DDM_LAUNCH("gather_slo_hi", 20.0 * n, st, match::gather_key_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.slo_id, R->sub_hi[0], n,
+                                                                               I.slo_hi, I.levels ? I.lvl[1] : nullptr));
     DDM_TRY(check_launch());
+    for (int L = 2; L <= I.levels; ++L) {
+      DDM_LAUNCH("block_max", 8.0 * I.lvl_n[L - 1], st, match::block_max_kernel<<<grid_for(I.lvl_n[L - 1], 256, 8), 256, 0, st>>>(
+          I.lvl[L - 1], I.lvl_n[L - 1], I.lvl[L]));
+      DDM_TRY(check_launch());
+    }
   }
   if (R->d > 1) {
     match::DimPtrs D{};
@@ -449,7 +593,7 @@ struct MatchReq {
   uint32_t flags;
 };
 
-ddm_status match_indexed(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool err_pending,
+ddm_status match_indexed(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool err_pending, bool use_msd,
                          cudaStream_t st) {
   const Index& I = *q.I;
   const ddm_regions* R = q.R;
@@ -467,9 +611,17 @@ ddm_status match_indexed(const MatchReq& q, MatchWs& W, uint64_t* count_out, boo
   }
   SortScratch& s = W.sort;
   init_attrs_once();
-  DDM_CUDA(cudaMemsetAsync(s.hist[2], 0, sizeof(uint32_t) * 8 * 256, st));
-  DDM_TRY(validate_side(d, m, R->upd_lo, R->upd_hi, s.hist[2], nullptr, &W.misc->err, st));
-  DDM_TRY(radix_sort(R->upd_lo[0], true, nullptr, W.ulo_key, W.ulo_id, m, full_passes(), s.hist[2], true, s, st));
+  if (use_msd) {
+    if (!err_pending) DDM_TRY(init_minmax(s.mm, st));
+    DDM_TRY(validate_side(d, m, R->upd_lo, R->upd_hi, nullptr, nullptr, &W.misc->err, st, s.mm + 4));
+    // a2 + a3: Ulo with the upper key and the id as payload
+    DDM_TRY(msd_sort_t<true>(R->upd_lo[0], R->upd_hi[0], m, s.mm + 4, W.ulo_key, W.uhi, W.ulo_id, s,
+                             &W.misc->overflow, st));
+  } else {
+    DDM_CUDA(cudaMemsetAsync(s.hist[2], 0, sizeof(uint32_t) * 8 * 256, st));
+    DDM_TRY(validate_side(d, m, R->upd_lo, R->upd_hi, s.hist[2], nullptr, &W.misc->err, st));
+    DDM_TRY(radix_sort(R->upd_lo[0], true, nullptr, W.ulo_key, W.ulo_id, m, full_passes(), s.hist[2], true, s, st));
+  }
   // a4: counts by rank difference (+ the row-tile sums); a5: exclusive scan
   // of the row-tile sums -> output offset of every 256-row tile, K
   const uint64_t ctiles = (m + match::kCountTile - 1) / match::kCountTile;
@@ -480,7 +632,8 @@ ddm_status match_indexed(const MatchReq& q, MatchWs& W, uint64_t* count_out, boo
       W.ulo_key, m, I.slo_key, I.shi_key, n, W.part));
   DDM_TRY(check_launch());
   DDM_LAUNCH("count", 56.0 * m + 16.0 * n, st, match::count_kernel<<<(unsigned)ctiles, match::kCountThreads, sizeof(match::CountSmem), st>>>(
-      W.ulo_key, W.ulo_id, R->upd_hi[0], m, I.slo_key, I.shi_key, n, W.part, W.r_lo, W.r_b, W.cnt0, W.tile_sum));
+      W.ulo_key, W.ulo_id, R->upd_hi[0], use_msd ? W.uhi : nullptr, m, I.slo_key, I.shi_key, n, W.part, W.r_lo, W.r_b,
+      W.cnt0, W.tile_sum));
   DDM_TRY(check_launch());
   DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (stiles + 1), st));
   DDM_LAUNCH("scan", 16.0 * rtiles, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
@@ -528,6 +681,7 @@ ddm_status match_indexed(const MatchReq& q, MatchWs& W, uint64_t* count_out, boo
   DDM_CUDA(cudaStreamSynchronize(st));
   *count_out = h.K;
   DDM_TRY(err_status(h.err));
+  if (h.overflow) return kRetryLSB;  // degenerate bucket: nothing written yet, redo with the LSB sort
   if (!q.pairs) return DDM_OK;
   if (h.K > q.capacity) return DDM_ERR_CAPACITY;
   if (h.K == 0) return DDM_OK;
@@ -594,10 +748,17 @@ static ddm_status match_full(const ddm_regions* R, ddm_pair* pairs, uint64_t cap
   uint8_t* base = static_cast<uint8_t*>(ws);
   Index I = index_layout(R->d, R->n_sub, base);
   MatchWs W = match_layout(R->d, R->n_sub, R->n_upd, base + a256(I.bytes));
-  DDM_CUDA(cudaMemsetAsync(W.misc, 0, sizeof(Misc), st));
-  DDM_TRY(build_index_async(R, I, W.sort, &W.misc->err, st));
   MatchReq q{&I, R, nullptr, pairs, capacity, flags};
-  return match_indexed(q, W, count_out, true, st);
+  const bool lsb_only = (flags & DDM_SORT_LSB) != 0;
+  for (int attempt = lsb_only ? 1 : 0; attempt < 2; ++attempt) {
+    const bool use_msd = attempt == 0;
+    DDM_CUDA(cudaMemsetAsync(W.misc, 0, sizeof(Misc), st));
+    if (use_msd) DDM_TRY(init_minmax(W.sort.mm, st));
+    DDM_TRY(build_index_async(R, I, W.sort, W.misc, use_msd, st));
+    const ddm_status r = match_indexed(q, W, count_out, true, use_msd, st);
+    if (r != kRetryLSB) return r;
+  }
+  return DDM_ERR_CUDA;
 }
 
 ddm_status ddm_match_count(const ddm_regions* regions, uint64_t* count_out, void* ws, size_t ws_bytes,
@@ -624,11 +785,15 @@ ddm_status ddm_sub_index_build(const ddm_regions* subs, void* index, size_t inde
   Carver c(ws);
   Misc* misc = c.take<Misc>(1);
   SortScratch s = sort_scratch(c, subs->n_sub);
-  DDM_CUDA(cudaMemsetAsync(misc, 0, sizeof(Misc), stream));
-  DDM_TRY(build_index_async(subs, I, s, &misc->err, stream));
   Misc h{};
-  DDM_CUDA(cudaMemcpyAsync(&h, misc, sizeof(Misc), cudaMemcpyDeviceToHost, stream));
-  DDM_CUDA(cudaStreamSynchronize(stream));
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const bool use_msd = attempt == 0;
+    DDM_CUDA(cudaMemsetAsync(misc, 0, sizeof(Misc), stream));
+    DDM_TRY(build_index_async(subs, I, s, misc, use_msd, stream));
+    DDM_CUDA(cudaMemcpyAsync(&h, misc, sizeof(Misc), cudaMemcpyDeviceToHost, stream));
+    DDM_CUDA(cudaStreamSynchronize(stream));
+    if (h.err || !h.overflow) break;
+  }
   return err_status(h.err);
 }
 
@@ -642,7 +807,11 @@ static ddm_status indexed_common(const void* index, const ddm_regions* upds, con
   Index I = index_layout(upds->d, upds->n_sub, const_cast<void*>(index));
   MatchWs W = match_layout(upds->d, upds->n_sub, upds->n_upd, ws);
   MatchReq q{&I, upds, upd_ids, pairs, capacity, flags};
-  return match_indexed(q, W, count_out, false, st);
+  if (!(flags & DDM_SORT_LSB)) {
+    const ddm_status r = match_indexed(q, W, count_out, false, true, st);
+    if (r != kRetryLSB) return r;
+  }
+  return match_indexed(q, W, count_out, false, false, st);
 }
 
 ddm_status ddm_match_pairs_indexed(const void* index, const ddm_regions* upds, const uint32_t* upd_ids,

@@ -30,7 +30,9 @@ __global__ void __launch_bounds__(512) validate_hist_kernel(const double* __rest
                                                             const double* __restrict__ hi,
                                                             uint64_t n, uint32_t* __restrict__ hist_lo,
                                                             uint32_t* __restrict__ hist_hi,
-                                                            uint32_t* __restrict__ err) {
+                                                            uint32_t* __restrict__ err,
+                                                            uint64_t* __restrict__ mm_lo,
+                                                            uint64_t* __restrict__ mm_hi) {
   __shared__ uint32_t hl[8][256];
   __shared__ uint32_t hh[8][256];
   __shared__ uint32_t serr;
@@ -41,12 +43,20 @@ __global__ void __launch_bounds__(512) validate_hist_kernel(const double* __rest
   if (threadIdx.x == 0) serr = 0;
   __syncthreads();
   uint32_t e = 0;
+  uint64_t lmin = ~0ull, lmax = 0, hmin = ~0ull, hmax = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const double x = __ldcs(lo + i), y = __ldcs(hi + i);
     const uint64_t bx = (uint64_t)__double_as_longlong(x), by = (uint64_t)__double_as_longlong(y);
     if (!f64_finite_bits(bx) || !f64_finite_bits(by)) e |= kErrNonFinite;
     else if (!(x <= y)) e |= kErrInverted;
+    if (mm_lo) {
+      const uint64_t kx = f64_key(x), ky = f64_key(y);
+      lmin = kx < lmin ? kx : lmin;
+      lmax = kx > lmax ? kx : lmax;
+      hmin = ky < hmin ? ky : hmin;
+      hmax = ky > hmax ? ky : hmax;
+    }
     if (hist_lo) {
       const uint64_t k = f64_key(x);
 #pragma unroll
@@ -60,6 +70,24 @@ __global__ void __launch_bounds__(512) validate_hist_kernel(const double* __rest
   }
   e = __reduce_or_sync(kFull, e);
   if ((threadIdx.x & 31) == 0 && e) atomicOr(&serr, e);
+  if (mm_lo) {  // min/max keys (value-bucketed MSD sort); non-finite values are rejected anyway
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      uint64_t t;
+      t = __shfl_xor_sync(kFull, lmin, o); lmin = t < lmin ? t : lmin;
+      t = __shfl_xor_sync(kFull, lmax, o); lmax = t > lmax ? t : lmax;
+      t = __shfl_xor_sync(kFull, hmin, o); hmin = t < hmin ? t : hmin;
+      t = __shfl_xor_sync(kFull, hmax, o); hmax = t > hmax ? t : hmax;
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin((unsigned long long*)&mm_lo[0], (unsigned long long)lmin);
+      atomicMax((unsigned long long*)&mm_lo[1], (unsigned long long)lmax);
+      if (mm_hi) {
+        atomicMin((unsigned long long*)&mm_hi[0], (unsigned long long)hmin);
+        atomicMax((unsigned long long*)&mm_hi[1], (unsigned long long)hmax);
+      }
+    }
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) {
     if (hist_lo && (&hl[0][0])[i]) atomicAdd(hist_lo + i, (&hl[0][0])[i]);
@@ -289,7 +317,7 @@ __device__ __forceinline__ uint64_t advance(const uint64_t* W, uint64_t base, ui
 // 256-row tile (for the row-offset scan, a5).
 __global__ void __launch_bounds__(kCountThreads, 2) count_kernel(
     const uint64_t* __restrict__ ulo_key, const uint32_t* __restrict__ ulo_id, const double* __restrict__ upd_hi,
-    uint64_t m, const uint64_t* __restrict__ slo_key, const uint64_t* __restrict__ shi_key, uint64_t n,
+    const uint64_t* __restrict__ uhi, uint64_t m, const uint64_t* __restrict__ slo_key, const uint64_t* __restrict__ shi_key, uint64_t n,
     const uint64_t* __restrict__ part, uint32_t* __restrict__ r_lo_out, uint32_t* __restrict__ r_b_out,
     uint32_t* __restrict__ cnt_out, uint64_t* __restrict__ row_tile_sum) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -305,7 +333,13 @@ __global__ void __launch_bounds__(kCountThreads, 2) count_kernel(
   // issue this thread's loads first (the random upd_hi gather overlaps the
   // window staging below)
   uint64_t a[kCountItems], b[kCountItems];
-  {
+  if (uhi) {  // upper keys already in sorted order (MSD sort payload)
+#pragma unroll
+    for (int i = 0; i < kCountItems; ++i) {
+      a[i] = i < ni ? __ldcs(ulo_key + j + i) : 0;
+      b[i] = i < ni ? __ldcs(uhi + j + i) : 0;
+    }
+  } else {  // gather them (LSB sort path)
     uint32_t id[kCountItems];
 #pragma unroll
     for (int i = 0; i < kCountItems; ++i) id[i] = i < ni ? __ldcs(ulo_id + j + i) : 0;

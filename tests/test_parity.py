@@ -15,7 +15,8 @@ from paper_1703_06680_b200 import ddm
 from paper_1703_06680_b200 import workload as wl
 from tests.helpers import cuda, gpu_args, raw_words, words_of
 
-EMIT_FLAGS = [ddm.DDM_EMIT_AUTO, ddm.DDM_EMIT_FORCE_THREAD, ddm.DDM_EMIT_FORCE_WARP, ddm.DDM_EMIT_FORCE_CHUNK]
+EMIT_FLAGS = [ddm.DDM_EMIT_AUTO, ddm.DDM_EMIT_FORCE_THREAD, ddm.DDM_EMIT_FORCE_WARP, ddm.DDM_EMIT_FORCE_CHUNK,
+              ddm.DDM_SORT_LSB, ddm.DDM_SORT_LSB | ddm.DDM_EMIT_FORCE_CHUNK]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -376,3 +377,34 @@ def test_indexed_shards_equal_single(orc):
         got = np.sort(np.concatenate(parts))
         assert total == ref.size
         assert np.array_equal(got, ref), G
+
+
+def test_msd_overflow_falls_back_to_lsb(orc):
+    """A bucket larger than shared memory (here: 12000 equal lower bounds plus a
+    spread) makes the MSD sort hand over to the LSB sort: same result."""
+    rng = np.random.default_rng(9)
+    lo = np.concatenate([np.full(12000, 5.0), rng.uniform(0, 100, 3000)])
+    hi = lo + rng.uniform(0, 2, lo.size)
+    ul = rng.uniform(0, 100, 5000)
+    uh = ul + 1.0
+    ref = orc.sbm_seq(lo[None], hi[None], ul[None], uh[None])
+    check_against(orc, lo, hi, ul, uh, flags=(0, ddm.DDM_SORT_LSB), ref=ref)
+    # and the same on the update side
+    ref2 = orc.sbm_seq(ul[None], uh[None], lo[None], hi[None])
+    check_against(orc, ul, uh, lo, hi, flags=(0, ddm.DDM_SORT_LSB), ref=ref2)
+
+
+@pytest.mark.parametrize("n", [1, 700, 769, 5000, 70_000, 300_000])
+def test_msd_sizes(orc, n):
+    """Bucket-bit choices from 1 to ~9 bits, ragged spans and tails."""
+    w = wl.uniform(n, max(1, n // 2), 1e5, 3.0, 1, seed=n)
+    check_against(orc, w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi, flags=(0, ddm.DDM_SORT_LSB))
+
+
+def test_msd_negative_and_wide_ranges(orc):
+    rng = np.random.default_rng(2)
+    lo = np.concatenate([rng.uniform(-1e300, 1e300, 2000), rng.normal(0, 1, 20000), [-0.0, 0.0] * 50])
+    hi = lo + np.abs(rng.normal(0, 0.5, lo.size))
+    ul = rng.normal(0, 1, 8000)
+    uh = ul + 0.1
+    check_against(orc, lo, hi, ul, uh, flags=(0, ddm.DDM_SORT_LSB))
