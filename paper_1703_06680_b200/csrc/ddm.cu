@@ -187,11 +187,7 @@ struct SortScratch {
   uint64_t* alt_keys;
   uint32_t* alt_vals;
   // value-bucketed MSD sort
-  uint32_t* bhist;     // [NB] bucket histogram
-  uint32_t* bstarts;   // [NB + 1]
-  uint32_t* span_lo;   // [spans + 1]
   uint32_t* dh;        // [3][256] digit histograms of the bucket id
-  uint64_t* bstatus;   // bucket-scan look-back words
   uint64_t* mm;        // [3][2] min/max keys (Slo, Shi, Ulo)
   uint64_t* alt_keys2;
   uint64_t* alt_v64[2];
@@ -207,12 +203,7 @@ SortScratch sort_scratch(Carver& c, uint64_t cap) {
   s.counters = c.take<uint32_t>(radix::kMaxPasses);
   s.alt_keys = c.take<uint64_t>(cap);
   s.alt_vals = c.take<uint32_t>(cap);
-  const uint64_t nb = 1ull << msd_bits(cap);
-  s.bhist = c.take<uint32_t>(nb);
-  s.bstarts = c.take<uint32_t>(nb + 1);
-  s.span_lo = c.take<uint32_t>(cap / msd::kSpan + 2);
   s.dh = c.take<uint32_t>(3 * 256);
-  s.bstatus = c.take<uint64_t>(nb / (msd::kThreads * msd::kBScanItems) + 2);
   s.mm = c.take<uint64_t>(6);
   s.alt_keys2 = c.take<uint64_t>(cap);
   s.alt_v64[0] = c.take<uint64_t>(cap);
@@ -430,21 +421,13 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, cons
   const int bits = msd_bits(n);
   const uint32_t nb = 1u << bits;
   const int passes = (bits + 7) / 8;
-  DDM_CUDA(cudaMemsetAsync(s.bhist, 0, sizeof(uint32_t) * nb, st));
   DDM_CUDA(cudaMemsetAsync(s.dh, 0, sizeof(uint32_t) * 3 * 256, st));
-  DDM_LAUNCH("msd_hist", 8.0 * n, st, msd::bucket_hist_kernel<true><<<grid_for(n, 256, 8), 256, 0, st>>>(src, n, mm, bits, s.bhist));
-  DDM_TRY(check_launch());
-  DDM_LAUNCH("msd_digit_hist", 4.0 * nb, st, msd::digit_hist_kernel<<<grid_for(nb, 256, 2), 256, 0, st>>>(s.bhist, nb, passes, s.dh));
+  DDM_LAUNCH("msd_hist", 8.0 * n, st, msd::msd_hist_kernel<true><<<grid_for(n, 512, 4), 512, 0, st>>>(src, n, mm, bits, passes, s.dh));
   DDM_TRY(check_launch());
   DDM_LAUNCH("radix_bin_start", 0, st, radix::bin_start_kernel<<<passes, radix::kRadix, 0, st>>>(s.dh, s.starts));
   DDM_TRY(check_launch());
-  const unsigned bt = (unsigned)((nb + msd::kThreads * msd::kBScanItems - 1) / (msd::kThreads * msd::kBScanItems));
-  DDM_CUDA(cudaMemsetAsync(s.bstatus, 0, sizeof(uint64_t) * (bt + 1), st));
-  DDM_LAUNCH("msd_bucket_scan", 8.0 * nb, st, msd::bucket_scan_kernel<<<bt, msd::kThreads, 0, st>>>(s.bhist, nb, s.bstarts, s.bstatus));
-  DDM_TRY(check_launch());
   const uint32_t spans = (uint32_t)((n + msd::kSpan - 1) / msd::kSpan);
-  DDM_LAUNCH("msd_spans", 0, st, msd::span_kernel<<<(spans + 256) / 256, 256, 0, st>>>(s.bstarts, nb, n, spans, s.span_lo));
-  DDM_TRY(check_launch());
+  (void)nb;
   uint64_t* bk[2] = {s.alt_keys, s.alt_keys2};
   uint64_t* bv[2] = {s.alt_v64[0], s.alt_v64[1]};
   uint32_t* bi[2] = {s.alt_vals, s.alt_vals2};
@@ -483,11 +466,11 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, cons
   if (PAY)
     DDM_LAUNCH("msd_local_pay", 40.0 * n, st, msd::local_sort_kernel<true, true>
                <<<spans, msd::kThreads, sizeof(msd::LocalSmem<true, true>), st>>>(
-                   bk[l], bv[l], bi[l], out_key, out_v64, out_v32, s.bstarts, nb, s.span_lo, mm, bits, overflow));
+                   bk[l], bv[l], bi[l], out_key, out_v64, out_v32, n, mm, bits, overflow));
   else
     DDM_LAUNCH("msd_local", 16.0 * n, st, msd::local_sort_kernel<false, false>
                <<<spans, msd::kThreads, sizeof(msd::LocalSmem<false, false>), st>>>(
-                   bk[l], nullptr, nullptr, out_key, nullptr, nullptr, s.bstarts, nb, s.span_lo, mm, bits, overflow));
+                   bk[l], nullptr, nullptr, out_key, nullptr, nullptr, n, mm, bits, overflow));
   return check_launch();
 }
 

@@ -32,7 +32,8 @@ constexpr int kRadix = 256;
 constexpr int kItems = 8;
 constexpr int kTile = kThreads * kItems;
 constexpr int kSpan = 2048;      // nominal records per local-sort CTA
-constexpr int kCap = 4096;       // records a local-sort CTA can hold
+constexpr int kCap = 2560;       // records a local-sort CTA can hold
+constexpr int kCapPow2 = 4096;   // bitonic network size bound (next power of two >= kCap)
 constexpr int kFineBins = 4096;  // value bins of the in-smem counting sort
 constexpr int kMaxBinRun = 64;   // larger bins (ties, clusters) -> bitonic sort of the group
 
@@ -42,114 +43,58 @@ __device__ __forceinline__ double key_to_f64(uint64_t k) {
   return __longlong_as_double((long long)b);
 }
 
-// Monotone value -> bucket map: floor((x/2 - min/2) * scale), clamped.
+// Monotone value -> bucket map: round((x/2 - min/2) * scale), clamped to
+// [0, NB-1].  Every step (x/2, fma, fmin/fmax, round-to-nearest via the
+// 1.5*2^52 magic add) is monotone non-decreasing in x, so bucket order never
+// contradicts key order; fmax(NaN, 0) = 0 guards degenerate scales.
 struct Bucketer {
-  double hmin, scale;
-  uint32_t last;
+  double a, b, top;  // u = fma(x, a, b) = (x*0.5 - min*0.5) * scale
   __device__ __forceinline__ void init(const uint64_t* mm, int bits) {
     const double xmin = key_to_f64(mm[0]), xmax = key_to_f64(mm[1]);
-    hmin = xmin * 0.5;
+    const double hmin = xmin * 0.5;
     const double range = xmax * 0.5 - hmin;
     const double nb = (double)(1ull << bits);
-    double s = range > 0.0 ? nb / range : 0.0;
-    if (!(s <= 1.7976931348623157e308)) s = 1.7976931348623157e308;
-    scale = s;
-    last = (uint32_t)((1ull << bits) - 1);
-  }
-  __device__ __forceinline__ uint32_t of_value(double x, double sc) const {
-    const uint32_t b = __double2uint_rz((x * 0.5 - hmin) * sc);  // saturating; NaN -> 0
-    return b;
+    double s = range > 0.0 ? (nb - 1.0) / range : 0.0;
+    if (!(s <= 1e300)) s = 1e300;
+    a = 0.5 * s;
+    b = -hmin * s;
+    top = nb - 1.0;
   }
   __device__ __forceinline__ uint32_t operator()(uint64_t key) const {
-    const uint32_t b = of_value(key_to_f64(key), scale);
-    return b > last ? last : b;
+    const double x = key_to_f64(key);
+    double u = fma(x, a, b);
+    u = fmin(fmax(u, 0.0), top);
+    return (uint32_t)__double_as_longlong(u + 6755399441055744.0);
   }
 };
 
 // ---------------------------------------------------------------- histograms
 
-// Full bucket histogram of the keys (float64 source encoded on the fly).
+// Per-pass digit histograms of the bucket ids (digit p = bits [8p, 8p+8)),
+// straight from the data with shared-memory counters.  out: [passes][256].
 template <bool SRC_F64>
-__global__ void __launch_bounds__(256) bucket_hist_kernel(const void* __restrict__ src, uint64_t n,
-                                                          const uint64_t* __restrict__ mm, int bits,
-                                                          uint32_t* __restrict__ hist) {
+__global__ void __launch_bounds__(512) msd_hist_kernel(const void* __restrict__ src, uint64_t n,
+                                                       const uint64_t* __restrict__ mm, int bits, int passes,
+                                                       uint32_t* __restrict__ out) {
+  __shared__ uint32_t sh[3][kRadix];
   Bucketer B;
   B.init(mm, bits);
+  for (int i = threadIdx.x; i < 3 * kRadix; i += blockDim.x) (&sh[0][0])[i] = 0;
+  __syncthreads();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint64_t k = SRC_F64 ? f64_key(__ldcs(reinterpret_cast<const double*>(src) + i))
                                : __ldcs(reinterpret_cast<const uint64_t*>(src) + i);
-    atomicAdd(hist + B(k), 1u);
-  }
-}
-
-// Per-pass digit histograms (digit p = bits [8p, 8p+8) of the bucket id)
-// from the full bucket histogram.  out: [passes][256], zeroed.
-__global__ void __launch_bounds__(256) digit_hist_kernel(const uint32_t* __restrict__ hist, uint32_t nb,
-                                                         int passes, uint32_t* __restrict__ out) {
-  __shared__ uint32_t sh[3][kRadix];
-  for (int i = threadIdx.x; i < 3 * kRadix; i += blockDim.x) (&sh[0][0])[i] = 0;
-  __syncthreads();
-  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
-    const uint32_t c = hist[b];
-    if (c)
-      for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(b >> (8 * p)) & 255], c);
+    const uint32_t b = B(k);
+    atomicAdd(&sh[0][b & 255], 1u);
+    if (passes > 1) atomicAdd(&sh[1][(b >> 8) & 255], 1u);
+    if (passes > 2) atomicAdd(&sh[2][(b >> 16) & 255], 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) {
     const uint32_t v = (&sh[0][0])[i];
     if (v) atomicAdd(out + i, v);
   }
-}
-
-// exclusive scan of nb u32 counts -> starts[0..nb] (starts[nb] = n), one CTA
-// per 4096 counts, decoupled look-back (u64 status words).
-constexpr int kBScanItems = 16;
-__global__ void __launch_bounds__(kThreads) bucket_scan_kernel(const uint32_t* __restrict__ cnt, uint32_t nb,
-                                                               uint32_t* __restrict__ starts,
-                                                               uint64_t* __restrict__ status) {
-  __shared__ uint64_t tmp[kWarps + 1];
-  __shared__ uint64_t prefix;
-  const int tid = threadIdx.x;
-  const uint32_t tile = blockIdx.x;
-  const uint64_t base = (uint64_t)tile * kThreads * kBScanItems + (uint64_t)tid * kBScanItems;
-  uint32_t v[kBScanItems];
-  uint64_t local = 0;
-#pragma unroll
-  for (int i = 0; i < kBScanItems; ++i) {
-    v[i] = base + i < nb ? cnt[base + i] : 0;
-    local += v[i];
-  }
-  uint64_t agg;
-  const uint64_t ex = block_excl_scan<kThreads>(local, tmp, &agg);
-  if (tid < 32) {
-    const uint64_t e = match::lookback_warp_u64(status, tile, agg);
-    if (tid == 0) prefix = e;
-  }
-  __syncthreads();
-  uint64_t run = prefix + ex;
-#pragma unroll
-  for (int i = 0; i < kBScanItems; ++i) {
-    if (base + i < nb) starts[base + i] = (uint32_t)run;
-    run += v[i];
-  }
-  if (tile == gridDim.x - 1 && tid == 0) starts[nb] = (uint32_t)(prefix + agg);
-}
-
-// span_lo[c] = first bucket start >= c * kSpan (c = 0..spans); whole buckets
-// per local-sort CTA.
-__global__ void __launch_bounds__(256) span_kernel(const uint32_t* __restrict__ starts, uint32_t nb, uint64_t n,
-                                                   uint32_t spans, uint32_t* __restrict__ span_lo) {
-  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c > spans) return;
-  const uint64_t p = umin64((uint64_t)c * kSpan, n);
-  uint32_t lo = 0, hi = nb;  // first index in starts[0..nb] with starts[i] >= p
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (starts[mid] < p) lo = mid + 1;
-    else hi = mid;
-  }
-  span_lo[c] = c == spans ? (uint32_t)n : starts[lo];
 }
 
 // ---------------------------------------------------------------- multisplit pass
@@ -160,6 +105,7 @@ struct PassSmem {
   uint64_t keys[kT];
   uint64_t v64[V64 ? kT : 2];
   uint32_t v32[V32 ? kT : 4];
+  uint8_t dg[kT];
   alignas(16) uint32_t wbase[kWarps][kRadix];
   uint32_t match[kWarps][kRadix];
   long long digit_base[kRadix];
@@ -265,6 +211,7 @@ __global__ void __launch_bounds__(kThreads, 3)
       S.keys[pos] = key[i];
       if (V64) S.v64[pos] = hv[i];
       if (V32) S.v32[pos] = iv[i];
+      S.dg[pos] = (uint8_t)d;
     }
     __syncwarp();
   }
@@ -303,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 3)
     const uint32_t p = i * kThreads + tid;
     if (p < tile_valid) {
       const uint64_t k = S.keys[p];
-      const uint32_t d = (BK(k) >> shift) & 255u;
+      const uint32_t d = S.dg[p];
       const uint64_t dst = (uint64_t)(S.digit_base[d] + (long long)p);
       k_out[dst] = k;
       if (V64) v64_out[dst] = S.v64[p];
@@ -320,80 +267,65 @@ struct LocalSmem {
   uint64_t v64[V64 ? kCap : 2];
   uint32_t v32[V32 ? kCap : 4];
   uint32_t bin[kFineBins + 1];
-  uint16_t perm[kCap];     // sorted position -> staged index
-  uint16_t binof[kCap];    // staged index -> fine bin
+  uint16_t perm[kCapPow2];  // sorted position -> staged index
   uint64_t red[2 * kWarps];
   uint32_t flag;
+  uint64_t bound[2];
 };
 
 // Stable sort of records [e0, e0 + c) by key inside shared memory (c <= kCap).
 // Records arrive in (bucket, original-order) order.  Counting sort over fine
-// value bins (monotone in the key), then a stable insertion sort by
-// (key, staged index) inside each bin; if some bin is large (ties, dense
-// clusters) the whole group is bitonic-sorted on (key, staged index) instead.
+// bins of the key range of this group (integer, monotone), then a stable
+// insertion sort by (key, staged index) inside each bin; if some bin is large
+// (ties, dense clusters) the group is bitonic-sorted on (key, staged index).
 template <bool V64, bool V32>
-__device__ void local_sort_group(LocalSmem<V64, V32>& S, const Bucketer& BK, int bits, const uint64_t* __restrict__ k_in,
+__device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restrict__ k_in,
                                  const uint64_t* __restrict__ v64_in, const uint32_t* __restrict__ v32_in,
                                  uint64_t* __restrict__ k_out, uint64_t* __restrict__ v64_out,
                                  uint32_t* __restrict__ v32_out, uint64_t e0, uint32_t c) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint64_t kmin = ~0ull, kmax = 0;
   for (uint32_t i = tid; i < c; i += kThreads) {
-    S.keys[i] = __ldcs(k_in + e0 + i);
+    const uint64_t k = __ldcs(k_in + e0 + i);
+    S.keys[i] = k;
+    kmin = k < kmin ? k : kmin;
+    kmax = k > kmax ? k : kmax;
     if (V64) S.v64[i] = __ldcs(v64_in + e0 + i);
     if (V32) S.v32[i] = __ldcs(v32_in + e0 + i);
   }
   for (uint32_t b = tid; b <= kFineBins; b += kThreads) S.bin[b] = 0;
   if (tid == 0) S.flag = 0;
-  __syncthreads();
-  // fine value coordinate u = (x/2 - min/2) * scale * 2^20 (monotone); this
-  // group's [umin, umax] selects the bin width
-  const double fscale = BK.scale * 1048576.0;
-  uint64_t umin = ~0ull, umax = 0;
-  for (uint32_t i = tid; i < c; i += kThreads) {
-    const double x = key_to_f64(S.keys[i]);
-    const uint64_t u = (uint64_t)__double2ull_rz((x * 0.5 - BK.hmin) * fscale);
-    umin = u < umin ? u : umin;
-    umax = u > umax ? u : umax;
-  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
-    const uint64_t a = __shfl_xor_sync(kFull, umin, o), b = __shfl_xor_sync(kFull, umax, o);
-    umin = a < umin ? a : umin;
-    umax = b > umax ? b : umax;
+    const uint64_t x = __shfl_xor_sync(kFull, kmin, o), y = __shfl_xor_sync(kFull, kmax, o);
+    kmin = x < kmin ? x : kmin;
+    kmax = y > kmax ? y : kmax;
   }
-  if (lane == 0) { S.red[warp] = umin; S.red[kWarps + warp] = umax; }
+  if (lane == 0) { S.red[warp] = kmin; S.red[kWarps + warp] = kmax; }
   __syncthreads();
-  umin = ~0ull;
-  umax = 0;
+  kmin = ~0ull;
+  kmax = 0;
 #pragma unroll
   for (int w = 0; w < kWarps; ++w) {
-    umin = S.red[w] < umin ? S.red[w] : umin;
-    umax = S.red[kWarps + w] > umax ? S.red[kWarps + w] : umax;
+    kmin = S.red[w] < kmin ? S.red[w] : kmin;
+    kmax = S.red[kWarps + w] > kmax ? S.red[kWarps + w] : kmax;
   }
   int sh = 0;
-  while (((umax - umin) >> sh) >= (uint64_t)kFineBins) ++sh;
-  // histogram of fine bins
-  for (uint32_t i = tid; i < c; i += kThreads) {
-    const double x = key_to_f64(S.keys[i]);
-    const uint64_t u = (uint64_t)__double2ull_rz((x * 0.5 - BK.hmin) * fscale);
-    const uint32_t b = (uint32_t)((u - umin) >> sh);
-    S.binof[i] = (uint16_t)b;
-    atomicAdd(&S.bin[b], 1u);
-  }
+  while (((kmax - kmin) >> sh) >= (uint64_t)kFineBins) ++sh;
+  for (uint32_t i = tid; i < c; i += kThreads) atomicAdd(&S.bin[(uint32_t)((S.keys[i] - kmin) >> sh)], 1u);
   __syncthreads();
-  // exclusive scan over bins (16 per thread) + large-bin detection
-  {
+  {  // exclusive scan over the bins (16 per thread) + large-bin detection
     constexpr int kPer = kFineBins / kThreads;
-    uint32_t v[kPer], s = 0;
+    uint32_t v[kPer], sum = 0;
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
       v[q] = S.bin[tid * kPer + q];
-      s += v[q];
+      sum += v[q];
       if (v[q] > kMaxBinRun) S.flag = 1;
     }
     __shared__ uint32_t tmp[kWarps + 1];
     uint32_t tot;
-    uint32_t ex = block_excl_scan<kThreads>(s, tmp, &tot);
+    uint32_t ex = block_excl_scan<kThreads>(sum, tmp, &tot);
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
       S.bin[tid * kPer + q] = ex;
@@ -401,15 +333,13 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const Bucketer& BK, int
     }
   }
   __syncthreads();
-  const bool bitonic = S.flag != 0;
-  if (!bitonic) {
-    // scatter staged indices into bins (order inside a bin fixed below)
+  if (S.flag == 0) {
     for (uint32_t i = tid; i < c; i += kThreads) {
-      const uint32_t pos = atomicAdd(&S.bin[S.binof[i]], 1u);
+      const uint32_t pos = atomicAdd(&S.bin[(uint32_t)((S.keys[i] - kmin) >> sh)], 1u);
       S.perm[pos] = (uint16_t)i;
     }
     __syncthreads();
-    // bins are [bin_end(b-1), bin_end(b)) now; insertion sort by (key, index)
+    // bin b now spans [end(b-1), end(b)); stable insertion sort by (key, index)
     for (uint32_t b = tid; b < kFineBins; b += kThreads) {
       const uint32_t lo = b ? S.bin[b - 1] : 0, hi = S.bin[b];
       for (uint32_t x = lo + 1; x < hi; ++x) {
@@ -438,7 +368,6 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const Bucketer& BK, int
           const uint32_t l = i ^ j;
           if (l > i) {
             const uint16_t a = S.perm[i], b = S.perm[l];
-            // padding (0xffff) sorts last
             const bool a_gt_b = (a == 0xffff) ? (b != 0xffff)
                                 : (b == 0xffff) ? false
                                 : (S.keys[a] > S.keys[b] || (S.keys[a] == S.keys[b] && a > b));
@@ -452,58 +381,82 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const Bucketer& BK, int
   }
   __syncthreads();
   for (uint32_t i = tid; i < c; i += kThreads) {
-    const uint16_t s = S.perm[i];
-    k_out[e0 + i] = S.keys[s];
-    if (V64) v64_out[e0 + i] = S.v64[s];
-    if (V32) v32_out[e0 + i] = S.v32[s];
+    const uint16_t t = S.perm[i];
+    k_out[e0 + i] = S.keys[t];
+    if (V64) v64_out[e0 + i] = S.v64[t];
+    if (V32) v32_out[e0 + i] = S.v32[t];
   }
   __syncthreads();
 }
 
-// One CTA per span of ~kSpan records made of whole buckets (span_lo); groups
-// of consecutive buckets holding <= kCap records are sorted in smem.  A bucket
-// larger than kCap sets *overflow (the caller falls back to the LSB sort).
+// First bucket boundary at or after p (p == 0 or bucket(p) != bucket(p-1)),
+// searching forward in 256-wide windows; n if none.  Whole CTA, uniform.
+__device__ __forceinline__ uint64_t next_boundary(const uint64_t* __restrict__ keys, uint64_t n, uint64_t p,
+                                                  const Bucketer& BK, uint64_t* slot) {
+  if (p == 0) return 0;
+  const int tid = threadIdx.x;
+  if (tid == 0) *slot = ~0ull;
+  __syncthreads();
+  for (uint64_t base = p; base < n; base += kThreads) {
+    const uint64_t q = base + tid;
+    const bool edge = q < n && BK(keys[q]) != BK(keys[q - 1]);
+    if (edge) atomicMin((unsigned long long*)slot, (unsigned long long)q);
+    __syncthreads();
+    const uint64_t r = *slot;
+    __syncthreads();
+    if (r != ~0ull) return r;
+  }
+  return n;
+}
+
+// Last bucket boundary in (lo, hi] scanning backwards; lo if none.
+__device__ __forceinline__ uint64_t prev_boundary(const uint64_t* __restrict__ keys, uint64_t lo, uint64_t hi,
+                                                  const Bucketer& BK, uint64_t* slot) {
+  const int tid = threadIdx.x;
+  if (tid == 0) *slot = 0;
+  __syncthreads();
+  for (int64_t top = (int64_t)hi; top > (int64_t)lo; top -= kThreads) {
+    const int64_t q = top - tid;
+    const bool edge = q > (int64_t)lo && BK(keys[q]) != BK(keys[q - 1]);
+    if (edge) atomicMax((unsigned long long*)slot, (unsigned long long)q);
+    __syncthreads();
+    const uint64_t r = *slot;
+    __syncthreads();
+    if (r) return r;
+  }
+  return lo;
+}
+
+// CTA c sorts the whole buckets starting in [c*kSpan, (c+1)*kSpan): it finds
+// its first and last bucket boundaries from the (bucket-grouped) keys and
+// sorts groups of consecutive buckets holding <= kCap records in smem.  A
+// single bucket larger than kCap sets *overflow (caller redoes with LSB).
 template <bool V64, bool V32>
 __global__ void __launch_bounds__(kThreads) local_sort_kernel(const uint64_t* __restrict__ k_in,
                                                               const uint64_t* __restrict__ v64_in,
                                                               const uint32_t* __restrict__ v32_in,
                                                               uint64_t* __restrict__ k_out,
                                                               uint64_t* __restrict__ v64_out,
-                                                              uint32_t* __restrict__ v32_out,
-                                                              const uint32_t* __restrict__ starts, uint32_t nb,
-                                                              const uint32_t* __restrict__ span_lo,
+                                                              uint32_t* __restrict__ v32_out, uint64_t n,
                                                               const uint64_t* __restrict__ mm, int bits,
                                                               uint32_t* __restrict__ overflow) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocalSmem<V64, V32>& S = *reinterpret_cast<LocalSmem<V64, V32>*>(smem_raw);
-  __shared__ uint64_t g_end;
   Bucketer BK;
   BK.init(mm, bits);
-  uint64_t e0 = span_lo[blockIdx.x];
-  const uint64_t e1 = span_lo[blockIdx.x + 1];
+  const uint64_t s0 = (uint64_t)blockIdx.x * kSpan;
+  uint64_t e0 = next_boundary(k_in, n, s0, BK, &S.bound[0]);
+  const uint64_t e1 = next_boundary(k_in, n, umin64(s0 + kSpan, n), BK, &S.bound[1]);
   while (e0 < e1) {
     uint64_t g1 = e1;
     if (e1 - e0 > kCap) {
-      // largest bucket start in (e0, e0 + kCap]
-      if (threadIdx.x == 0) {
-        uint32_t lo = 0, hi = nb + 1;  // first index with starts[i] > e0 + kCap
-        while (lo < hi) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (starts[mid] <= e0 + kCap) lo = mid + 1;
-          else hi = mid;
-        }
-        const uint64_t s = lo ? starts[lo - 1] : 0;
-        g_end = s > e0 ? s : ~0ull;
-      }
-      __syncthreads();
-      g1 = g_end;
-      __syncthreads();
-      if (g1 == ~0ull) {  // one bucket alone exceeds the capacity
+      g1 = prev_boundary(k_in, e0, e0 + kCap, BK, &S.bound[0]);
+      if (g1 == e0) {  // one bucket alone exceeds the capacity
         if (threadIdx.x == 0) atomicOr(overflow, 1u);
         return;
       }
     }
-    local_sort_group<V64, V32>(S, BK, bits, k_in, v64_in, v32_in, k_out, v64_out, v32_out, e0, (uint32_t)(g1 - e0));
+    local_sort_group<V64, V32>(S, k_in, v64_in, v32_in, k_out, v64_out, v32_out, e0, (uint32_t)(g1 - e0));
     e0 = g1;
   }
 }
