@@ -9,7 +9,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libddm.so")
 SOURCES = ["ddm.cu"]
-HEADERS = ["common.cuh", "radix.cuh", "match.cuh", "msd.cuh"]
+HEADERS = ["common.cuh", "radix.cuh", "match.cuh", "msd.cuh", "dd.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

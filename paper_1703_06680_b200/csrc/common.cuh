@@ -20,6 +20,12 @@ __device__ __forceinline__ uint64_t f64_key(double x) {
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
+// inverse of f64_key (keys of finite doubles; -0 was canonicalised to +0)
+__device__ __forceinline__ double key_to_f64(uint64_t k) {
+  const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
 __device__ __forceinline__ bool f64_finite_bits(uint64_t b) {
   return (b & 0x7ff0000000000000ull) != 0x7ff0000000000000ull;
 }

@@ -24,6 +24,7 @@
 #include "match.cuh"
 #include "radix.cuh"
 #include "msd.cuh"
+#include "dd.cuh"
 
 using namespace ddm;
 
@@ -135,6 +136,8 @@ struct Index {
   uint64_t* lvl[kMaxLevels + 1] = {};
   uint64_t* shi_key = nullptr;
   double* sdims = nullptr;
+  float4* box12 = nullptr;  // d > 1: widened float32 boxes in Slo order (dd.cuh)
+  float2* box0 = nullptr;
   size_t bytes = 0;
 };
 
@@ -157,6 +160,10 @@ Index index_layout(uint32_t d, uint64_t n, void* base) {
   }
   I.shi_key = c.take<uint64_t>(n);
   I.sdims = c.take<double>((uint64_t)2 * (d - 1) * n);
+  if (d > 1) {
+    I.box12 = c.take<float4>(n);
+    I.box0 = c.take<float2>(n);
+  }
   I.bytes = c.used;
   return I;
 }
@@ -314,6 +321,8 @@ void init_attrs_once() {
                        (int)sizeof(msd::LocalSmem<true, true>));
   cudaFuncSetAttribute(msd::local_sort_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(msd::LocalSmem<false, false>));
+  cudaFuncSetAttribute(dd::dd_tile_kernel<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(dd::Smem<4>));
+  cudaFuncSetAttribute(dd::dd_tile_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(dd::Smem<4>));
   if (const char* e = getenv("DDM_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(e));
   done = true;
 }
@@ -559,10 +568,28 @@ ddm_status build_index_async(const ddm_regions* R, const Index& I, SortScratch& 
   if (R->d > 1) {
     match::DimPtrs D{};
     for (uint32_t k = 0; k < R->d; ++k) { D.lo[k] = R->sub_lo[k]; D.hi[k] = R->sub_hi[k]; }
-    DDM_LAUNCH("gather_dims", 36.0 * (R->d - 1) * n, st, match::gather_dims_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.slo_id, D, (int)R->d, n, I.sdims));
+    DDM_LAUNCH("gather_dims", 36.0 * (R->d - 1) * n, st, match::gather_dims_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.slo_id, D, (int)R->d, n, I.sdims,
+                                                                                   use_msd ? &misc->overflow : nullptr));
+    DDM_TRY(check_launch());
+    DDM_LAUNCH("dd_boxes", 24.0 * n + 16.0 * (R->d > 2 ? 2 : 1) * n + 24.0 * n, st,
+               dd::box_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.slo_key, I.slo_hi, I.sdims, (int)R->d, n, I.box12,
+                                                                   I.box0, use_msd ? &misc->overflow : nullptr));
     DDM_TRY(check_launch());
   }
   return DDM_OK;
+}
+
+// ------------------------------------------------------------ d > 1 tiled filter (dd.cuh)
+
+constexpr int kDDRows = 4;  // rows per thread of the d > 1 tile kernel (1024-row tiles)
+
+void launch_dd_any(bool emit, const dd::Args& a, cudaStream_t st) {
+  constexpr int kRows = dd::kThreads * kDDRows;
+  const unsigned grid = (unsigned)((a.m + kRows - 1) / kRows);
+  if (emit)
+    dd::dd_tile_kernel<kDDRows, true><<<grid, dd::kThreads, sizeof(dd::Smem<kDDRows>), st>>>(a);
+  else
+    dd::dd_tile_kernel<kDDRows, false><<<grid, dd::kThreads, sizeof(dd::Smem<kDDRows>), st>>>(a);
 }
 
 // ------------------------------------------------------------ match against an index
@@ -618,10 +645,12 @@ ddm_status match_indexed(const MatchReq& q, MatchWs& W, uint64_t* count_out, boo
       W.ulo_key, W.ulo_id, R->upd_hi[0], use_msd ? W.uhi : nullptr, m, I.slo_key, I.shi_key, n, W.part, W.r_lo, W.r_b,
       W.cnt0, W.tile_sum));
   DDM_TRY(check_launch());
-  DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (stiles + 1), st));
-  DDM_LAUNCH("scan", 16.0 * rtiles, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
-      W.tile_sum, rtiles, W.tile_off, W.scan_status, d == 1 ? &W.misc->K : nullptr));
-  DDM_TRY(check_launch());
+  if (d == 1) {
+    DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (stiles + 1), st));
+    DDM_LAUNCH("scan", 16.0 * rtiles, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
+        W.tile_sum, rtiles, W.tile_off, W.scan_status, &W.misc->K));
+    DDM_TRY(check_launch());
+  }
 
   match::EmitArgs A{};
   A.ulo_key = W.ulo_key;
@@ -644,8 +673,40 @@ ddm_status match_indexed(const MatchReq& q, MatchWs& W, uint64_t* count_out, boo
             : (q.flags & DDM_EMIT_FORCE_CHUNK) ? 3 : 0;
   const unsigned egrid = (unsigned)rtiles;
 
-  if (d > 1) {
-    // a8: dim-0 candidates filtered on dims 1..d-1; count pass + scan
+  const bool per_row = (q.flags & (DDM_EMIT_FORCE_THREAD | DDM_EMIT_FORCE_WARP)) != 0;
+  dd::Args D{};
+  if (d > 1 && !per_row) {
+    // a8: tiled dim-0 sweep with the exact filter on dims 1..d-1 (dd.cuh):
+    // count pass -> 256-row tile sums -> scan; the emit pass runs after the sync
+    D.ulo_key = W.ulo_key;
+    D.ulo_id = W.ulo_id;
+    D.upd_map = q.upd_map;
+    D.r_lo = W.r_lo;
+    D.r_b = W.r_b;
+    D.cnt0 = W.cnt0;
+    D.slo_key = I.slo_key;
+    D.slo_id = I.slo_id;
+    for (uint32_t k = 0; k < d; ++k) { D.upd.lo[k] = R->upd_lo[k]; D.upd.hi[k] = R->upd_hi[k]; }
+    D.T = tree_of(I);
+    D.sdims = I.sdims;
+    D.box12 = I.box12;
+    D.box0 = I.box0;
+    D.n = n;
+    D.m = m;
+    D.d = (int)d;
+    D.abort_flag = &W.misc->overflow;
+    D.cnt_out = W.cnt;
+    D.tile_sum = W.tile_sum;
+    D.cnt = W.cnt;
+    D.tile_off = W.tile_off;
+    DDM_LAUNCH("dd_count", 24.0 * m, st, launch_dd_any(false, D, st));
+    DDM_TRY(check_launch());
+    DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (stiles + 1), st));
+    DDM_LAUNCH("scan", 16.0 * rtiles, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
+        W.tile_sum, rtiles, W.tile_off, W.scan_status, &W.misc->K));
+    DDM_TRY(check_launch());
+  } else if (d > 1) {
+    // a8, per-row form (forced by the emit-path flags; cross-check of the tiled form)
     A.cnt_out = W.cnt;
     A.fstab_out = W.fstab;
     DDM_LAUNCH("count_dd", 44.0 * m, st, match::emit_kernel<match::kCountDD><<<egrid, match::kRowTile, 0, st>>>(A));
@@ -669,8 +730,10 @@ ddm_status match_indexed(const MatchReq& q, MatchWs& W, uint64_t* count_out, boo
   if (h.K > q.capacity) return DDM_ERR_CAPACITY;
   if (h.K == 0) return DDM_OK;
   A.pairs = reinterpret_cast<uint2*>(q.pairs);
-  const bool per_row = (q.flags & (DDM_EMIT_FORCE_THREAD | DDM_EMIT_FORCE_WARP)) != 0;
-  if (d == 1 && !per_row)
+  D.pairs = A.pairs;
+  if (d > 1 && !per_row)
+    DDM_LAUNCH("dd_emit", 24.0 * m + 8.0 * h.K, st, launch_dd_any(true, D, st));
+  else if (d == 1 && !per_row)
     DDM_LAUNCH("emit", 44.0 * m + 8.0 * h.K, st,
                match::emit_chunk_kernel<<<egrid, match::kRowTile, sizeof(match::ChunkSmem), st>>>(A));
   else if (d == 1)

@@ -157,7 +157,9 @@ struct DimPtrs {
 };
 
 __global__ void __launch_bounds__(256) gather_dims_kernel(const uint32_t* __restrict__ idx, DimPtrs src,
-                                                          int d, uint64_t n, double* __restrict__ out) {
+                                                          int d, uint64_t n, double* __restrict__ out,
+                                                          const uint32_t* __restrict__ abort_flag) {
+  if (abort_flag && *abort_flag) return;  // MSD bucket overflow: idx is not a permutation, attempt discarded
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint32_t s = __ldcs(idx + i);

@@ -37,11 +37,6 @@ constexpr int kCapPow2 = 4096;   // bitonic network size bound (next power of tw
 constexpr int kFineBins = 4096;  // value bins of the in-smem counting sort
 constexpr int kMaxBinRun = 64;   // larger bins (ties, clusters) -> bitonic sort of the group
 
-// inverse of f64_key (keys of finite doubles; -0 was canonicalised to +0)
-__device__ __forceinline__ double key_to_f64(uint64_t k) {
-  const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
-  return __longlong_as_double((long long)b);
-}
 
 // Monotone value -> bucket map: round((x/2 - min/2) * scale), clamped to
 // [0, NB-1].  Every step (x/2, fma, fmin/fmax, round-to-nearest via the

@@ -33,16 +33,21 @@ def check_against(orc, sl, sh, ul, uh, flags=(0,), ref=None):
         ref = orc.sbm_seq(*a)
     g = [cuda(x) for x in a]
     assert ddm.match_count(*g) == ref.size
-    first = None
+    first = {}
+    per_row = ddm.DDM_EMIT_FORCE_THREAD | ddm.DDM_EMIT_FORCE_WARP
     for f in flags:
         p = ddm.match_pairs(*g, flags=f)
         assert p.shape[0] == ref.size
         got = words_of(p)
         assert np.array_equal(got, ref), f"flags={f}"
-        if first is None:
-            first = raw_words(p)
-        else:  # every emission path writes byte-identical output
-            assert np.array_equal(raw_words(p), first)
+        # d = 1: every emission path writes byte-identical output (rows by
+        # sweep order, each row in Slo order).  d > 1: the tiled filter and
+        # the per-row filter each write a deterministic order of their own.
+        fam = "rows" if (a[0].shape[0] > 1 and f & per_row) else "main"
+        if fam not in first:
+            first[fam] = raw_words(p)
+        else:
+            assert np.array_equal(raw_words(p), first[fam]), f"flags={f}"
     return ref
 
 
@@ -265,7 +270,7 @@ def test_c4_scaled(orc):
     check_against(orc, w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi, flags=EMIT_FLAGS, ref=ref)
 
 
-@pytest.mark.parametrize("d", [2, 3, 5])
+@pytest.mark.parametrize("d", [2, 3, 4, 5, 8])
 def test_dd_tie_storms(orc, d):
     rng = np.random.default_rng(d)
     for _ in range(40):
@@ -275,6 +280,71 @@ def test_dd_tie_storms(orc, d):
         ref = orc.bf_pairs(s[0], s[1], u[0], u[1])
         assert np.array_equal(orc.sbm_dd_literal(s[0], s[1], u[0], u[1]), ref)
         check_against(orc, s[0], s[1], u[0], u[1], flags=EMIT_FLAGS, ref=ref)
+
+
+def test_c4_full_sampled(orc):
+    """c4 at full size (d = 3, N = 1e7): sampled rows against brute force
+    (Alg. 2 with the d-dim conjunction), list invariants on the device, the
+    count entry point equal to the list length, and K within 5 sigma of the
+    closed form n*m*p^3."""
+    w = wl.make("c4")
+    g = gpu_args(w)
+    p = ddm.match_pairs(*g)
+    K = p.shape[0]
+    assert ddm.match_count(*g) == K
+    E = wl.expected_pairs_uniform(w.n, w.m, w.L, w.l, 3)
+    assert abs(K - E) <= 5 * wl.stddev_bound(E)
+    s, u = p[:, 0].long(), p[:, 1].long()
+    ok = torch.ones(K, dtype=torch.bool, device=p.device)
+    for k in range(3):
+        ok &= (g[0][k][s] <= g[3][k][u]) & (g[2][k][u] <= g[1][k][s])
+    assert bool(ok.all())
+    wds = torch.sort((u << 32) | s).values
+    assert bool((wds[1:] > wds[:-1]).all())
+    _check_sampled_rows(orc, w, p, n_rows=1500)
+
+
+def test_dd_chunks_and_long_intervals(orc):
+    """d = 2 and 3 with tiles whose candidate sets span many shared-memory
+    chunks, long intervals in every dimension (A_t walk skips, dim-1 bin
+    ranges covering all bins), negative coordinates and point extents."""
+    rng = np.random.default_rng(33)
+    for d in (2, 3):
+        n, m = 6000, 7000
+        sl = rng.uniform(-500.0, 500.0, (d, n))
+        ul = rng.uniform(-500.0, 500.0, (d, m))
+        sh = sl + rng.uniform(0.0, 120.0, (d, n))
+        uh = ul + rng.uniform(0.0, 120.0, (d, m))
+        big = rng.choice(n, 40, replace=False)
+        sl[:, big[:20]] = -1e4
+        sh[:, big[:20]] = 1e4
+        sh[1, big[20:]] = sl[1, big[20:]] + 900.0
+        pts = rng.choice(m, 50, replace=False)
+        uh[:, pts] = ul[:, pts]
+        ref = orc.bf_pairs(sl, sh, ul, uh)
+        assert np.array_equal(orc.sbm_seq(sl, sh, ul, uh), ref)
+        check_against(orc, sl, sh, ul, uh, flags=EMIT_FLAGS, ref=ref)
+
+
+def test_dd_degenerate_dim1(orc):
+    """All dim-1 coordinates equal (zero-width bin range) and all dim-0
+    coordinates equal (every sub a candidate of every row)."""
+    rng = np.random.default_rng(34)
+    n, m = 1500, 1300
+    sl = np.stack([rng.uniform(0, 100, n), np.full(n, 7.0)])
+    ul = np.stack([rng.uniform(0, 100, m), np.full(m, 7.0)])
+    check_against(orc, sl, sl + 3.0, ul, ul + 3.0, flags=EMIT_FLAGS)
+    sl = np.stack([np.full(n, 1.0), rng.uniform(0, 100, n)])
+    ul = np.stack([np.full(m, 1.0), rng.uniform(0, 100, m)])
+    check_against(orc, sl, sl + 0.5, ul, ul + 0.5, flags=EMIT_FLAGS)
+
+
+def test_dd_deterministic_output():
+    w = wl.make("c4", scale=0.02)
+    g = gpu_args(w)
+    a = ddm.match_pairs(*g)
+    b = ddm.match_pairs(*g)
+    assert torch.equal(a, b)
 
 
 def test_c5_scaled(orc):
