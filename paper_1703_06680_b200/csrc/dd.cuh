@@ -25,12 +25,16 @@
 // re-tested exactly (float64 coordinates / order-preserving keys, Alg. 1 on
 // every dimension) before it is counted or written.
 //
-// Bins.  Each chunk is counting-sorted (stably, deterministically) into kBins
-// bins of its float32 dim-1 lower bounds; a row only scans the bins whose
-// lower bounds can pass its float test on dim 1:
-//   lo1(U) <= hi1(S) <= lo1(S) + maxlen  =>  lo1(S) >= rd(lo1(U) - maxlen)
-// with maxlen the chunk's largest float32 dim-1 length rounded up and a
-// monotone bucketer, so [bin(rd(lo1(U) - maxlen)), bin(hi1(U))] covers them.
+// Cells.  Each chunk is counting-sorted (stably, deterministically) into a
+// kG x kG grid of cells over its float32 (dim-1, dim-2) lower bounds; a row
+// only scans the cells whose lower bounds can pass its float test on both:
+//   lo_k(U) <= hi_k(S) <= lo_k(S) + maxlen_k  =>  lo_k(S) >= rd(lo_k(U) - maxlen_k)
+// with maxlen_k the chunk's largest float32 length on dim k rounded up and a
+// monotone bucketer per dimension, so the cell rectangle
+// [bin(rd(lo_k(U) - maxlen_k)), bin(hi_k(U))] (k = 1, 2) covers them.  With
+// d = 2 every dim-2 value is -inf/+inf and all cells share one dim-2 bin.
+// Cells are stored dim-2 major, so each dim-2 bin of the rectangle is one
+// contiguous run of slots.
 // Two passes run the identical enumeration: a count pass (row counts + 256-row
 // tile sums for the offset scan) and an emit pass writing each row at its
 // offset, so the output is deterministic.
@@ -43,26 +47,26 @@ namespace dd {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kBins = 128;
-constexpr int kWin = 1024;  // A_t walk window (positions per step), 4 per thread
-constexpr int kCap = 1024;  // candidates per shared-memory chunk
+constexpr int kG = 16;              // cells per dimension (dims 1 and 2)
+constexpr int kCells = kG * kG;
+constexpr int kWin = 1024;          // A_t walk window (positions per step), 4 per thread
+constexpr int kCap = 1024;          // candidates per shared-memory chunk
 constexpr int kRounds = kCap / kThreads;
+constexpr int kList = 8;            // queued float passes per lane before an exact batch
 static_assert(kCap >= kWin, "a whole walk window must fit one chunk");
+static_assert(kCells == kThreads, "one thread per cell in the cell scans");
 
 // ------------------------------------------------------------ index boxes
 
-// Widened float32 boxes of the subscriptions in Slo order (dims 0..2; a
-// missing dim 2 is (-inf, +inf)): box12[i] = (lo1, hi1, lo2, hi2),
-// box0[i] = (lo0, hi0), lower bounds rounded down, upper bounds rounded up.
-__global__ void __launch_bounds__(256) box_kernel(const uint64_t* __restrict__ slo_key,
-                                                  const uint64_t* __restrict__ slo_hi,
-                                                  const double* __restrict__ sdims, int d, uint64_t n,
-                                                  float4* __restrict__ box12, float2* __restrict__ box0,
+// Widened float32 boxes of the subscriptions on dims 1 and 2, in Slo order
+// (a missing dim 2 is (-inf, +inf)): box12[i] = (lo1, hi1, lo2, hi2), lower
+// bounds rounded down, upper bounds rounded up.
+__global__ void __launch_bounds__(256) box_kernel(const double* __restrict__ sdims, int d, uint64_t n,
+                                                  float4* __restrict__ box12,
                                                   const uint32_t* __restrict__ abort_flag) {
   if (abort_flag && *abort_flag) return;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    box0[i] = make_float2(__double2float_rd(key_to_f64(slo_key[i])), __double2float_ru(key_to_f64(slo_hi[i])));
     float4 b;
     b.x = __double2float_rd(sdims[i]);
     b.y = __double2float_ru(sdims[n + i]);
@@ -92,7 +96,6 @@ struct Args {
   MaxTree T;
   const double* sdims;       // [(d-1)][2][n] other dims of the subs in Slo order
   const float4* box12;       // widened float32 boxes (box_kernel)
-  const float2* box0;
   uint64_t n, m;
   int d;
   const uint32_t* abort_flag;  // non-zero: an MSD bucket overflowed, inputs are not sorted -> no-op
@@ -108,45 +111,48 @@ struct Args {
 template <int R>
 struct Smem {
   static constexpr int kRows = kThreads * R;
-  float4 c12[kCap];     // chunk boxes in bin order
-  float2 c0[kCap];
-  uint32_t cpos[kCap];  // Slo position of each binned slot
-  uint32_t fpos[kCap];  // Slo positions in fill order
-  uint64_t ra[kRows];   // row exact data: lower key, upper key, offset, local id, output id
-  uint64_t rb[kRows];
-  uint64_t roff[kRows];
-  uint32_t rlid[kRows];
-  uint32_t ruid[kRows];
-  uint16_t wc[kRounds * kWarps * kBins];  // per (round, warp, bin) counts -> prefixes
-  uint32_t bstart[kBins + 1];
-  float red[3 * kWarps];
+  float4 c12[kCap];          // chunk boxes in cell order
+  float4 rbox[kRows];        // widened row boxes (lo1, hi1, lo2, hi2)
+  uint32_t cpos[kCap];       // Slo position of each slot (cell order)
+  uint32_t fpos[kCap];       // Slo positions in fill order
+  uint16_t wc[kWarps * kCells];  // per (warp, cell) counts of one ranking round -> prefixes
+  uint16_t lst[kList * kThreads];  // per-lane queues of float passes: (row q << 12) | slot
+  uint32_t cstart[kCells + 1];
+  uint32_t run[kCells];      // slots already assigned per cell (earlier rounds)
+  float red[6 * kWarps];
   uint64_t scan64[kWarps + 1];
   uint32_t scan32[kWarps + 1];
   uint32_t rbmax;
 };
 
-// Monotone float bucketer over one chunk's dim-1 lower bounds.
+// Monotone float bucketer over one chunk's lower bounds on one dimension.
 struct Bins {
   float mn, scale;
   __device__ __forceinline__ int operator()(float x) const {
     float u = floorf((x - mn) * scale);
-    u = fminf(fmaxf(u, 0.0f), (float)(kBins - 1));  // fmaxf(NaN, 0) = 0
+    u = fminf(fmaxf(u, 0.0f), (float)(kG - 1));  // fmaxf(NaN, 0) = 0
     return (int)u;
+  }
+  __device__ __forceinline__ void init(float lo, float hi) {
+    mn = lo;
+    float sc = hi > lo ? (float)kG / (hi - lo) : 0.0f;
+    if (!(sc <= 1e30f)) sc = 1e30f;
+    scale = sc;
   }
 };
 
 template <int R>
-struct Rows {  // widened float32 row boxes (dims 0..2) + hit counters
-  float lo0[R], hi0[R], lo1[R], hi1[R], lo2[R], hi2[R];
+struct Rows {
   uint32_t hits[R];
+  uint64_t off[R];
   bool valid[R];
 };
 
-// Exact Alg. 1 test on every dimension for the sub at Slo position p and row r.
-template <int R>
-__device__ __forceinline__ bool exact_hit(const Args& A, const Smem<R>& S, uint32_t p, int r) {
-  if (!(A.slo_key[p] <= S.rb[r] && A.T.lvl[0][p] >= S.ra[r])) return false;  // dim 0 (keys)
-  const uint32_t lid = S.rlid[r];
+// Exact Alg. 1 test on every dimension for the sub at Slo position p and the
+// update at sorted position j (local id lid); global reads (rare: only float
+// passes get here).
+__device__ __forceinline__ bool exact_hit(const Args& A, uint32_t p, uint64_t j, uint32_t lid) {
+  if (!(A.slo_key[p] <= f64_key(A.upd.hi[0][lid]) && A.T.lvl[0][p] >= A.ulo_key[j])) return false;  // dim 0
   for (int k = 1; k < A.d; ++k) {
     const double slo = A.sdims[(uint64_t)(k - 1) * 2 * A.n + p];
     const double shi = A.sdims[(uint64_t)(k - 1) * 2 * A.n + A.n + p];
@@ -155,112 +161,163 @@ __device__ __forceinline__ bool exact_hit(const Args& A, const Smem<R>& S, uint3
   return true;
 }
 
+// Exact re-test of this lane's queued float passes, in queue order.
+template <int R, bool EMIT>
+__device__ __forceinline__ void flush_list(const Args& A, Smem<R>& S, Rows<R>& rw, uint32_t nl) {
+  const int tid = threadIdx.x;
+  const uint64_t j0 = (uint64_t)blockIdx.x * (kThreads * R);
+  for (uint32_t e = 0; e < nl; ++e) {
+    const uint32_t v = S.lst[e * kThreads + tid];
+    const int q = (int)(v >> 12);
+    const uint32_t p = S.cpos[v & 4095u];
+    const uint64_t j = j0 + (uint64_t)q * kThreads + tid;
+    const uint32_t lid = A.ulo_id[j];
+    if (!exact_hit(A, p, j, lid)) continue;
+#pragma unroll
+    for (int qq = 0; qq < R; ++qq)
+      if (qq == q) {
+        if (EMIT) A.pairs[rw.off[qq] + rw.hits[qq]] = make_uint2(A.slo_id[p], A.upd_map ? A.upd_map[lid] : lid);
+        ++rw.hits[qq];
+      }
+  }
+}
+
 template <int R, bool EMIT>
 __device__ void process_chunk(const Args& A, Smem<R>& S, Rows<R>& rw, uint32_t fill) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // 1. float boxes of the staged candidates; chunk min/max lo1, max length
-  float4 b12[kRounds];
-  float2 b0[kRounds];
-  float mn = __int_as_float(0x7f800000), mx = -mn, ml = 0.0f;
+  // 1. chunk min/max lower bound and max length (rounded up) on dims 1, 2
+  float mn1 = __int_as_float(0x7f800000), mx1 = -mn1, ml1 = 0.0f;
+  float mn2 = mn1, mx2 = -mn1, ml2 = 0.0f;
+  int cell[kRounds];
 #pragma unroll
   for (int r = 0; r < kRounds; ++r) {
     const uint32_t s = r * kThreads + tid;
     if (s < fill) {
-      const uint32_t p = S.fpos[s];
-      b12[r] = A.box12[p];
-      b0[r] = A.box0[p];
-      mn = fminf(mn, b12[r].x);
-      mx = fmaxf(mx, b12[r].x);
-      ml = fmaxf(ml, __fsub_ru(b12[r].y, b12[r].x));
+      const float4 b = A.box12[S.fpos[s]];
+      mn1 = fminf(mn1, b.x);
+      mx1 = fmaxf(mx1, b.x);
+      ml1 = fmaxf(ml1, __fsub_ru(b.y, b.x));
+      mn2 = fminf(mn2, b.z);
+      mx2 = fmaxf(mx2, b.z);
+      ml2 = fmaxf(ml2, __fsub_ru(b.w, b.z));
+      S.c12[s] = b;  // fill-order staging (re-placed in step 3)
     }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
-    mn = fminf(mn, __shfl_xor_sync(kFull, mn, o));
-    mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
-    ml = fmaxf(ml, __shfl_xor_sync(kFull, ml, o));
+    mn1 = fminf(mn1, __shfl_xor_sync(kFull, mn1, o));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(kFull, mx1, o));
+    ml1 = fmaxf(ml1, __shfl_xor_sync(kFull, ml1, o));
+    mn2 = fminf(mn2, __shfl_xor_sync(kFull, mn2, o));
+    mx2 = fmaxf(mx2, __shfl_xor_sync(kFull, mx2, o));
+    ml2 = fmaxf(ml2, __shfl_xor_sync(kFull, ml2, o));
   }
-  if (lane == 0) { S.red[warp] = mn; S.red[kWarps + warp] = mx; S.red[2 * kWarps + warp] = ml; }
-  for (int i = tid; i < kRounds * kWarps * kBins / 2; i += kThreads) reinterpret_cast<uint32_t*>(S.wc)[i] = 0;
+  if (lane == 0) {
+    S.red[warp] = mn1; S.red[kWarps + warp] = mx1; S.red[2 * kWarps + warp] = ml1;
+    S.red[3 * kWarps + warp] = mn2; S.red[4 * kWarps + warp] = mx2; S.red[5 * kWarps + warp] = ml2;
+  }
+  S.run[tid] = 0;
   __syncthreads();
 #pragma unroll
   for (int w = 0; w < kWarps; ++w) {
-    mn = fminf(mn, S.red[w]);
-    mx = fmaxf(mx, S.red[kWarps + w]);
-    ml = fmaxf(ml, S.red[2 * kWarps + w]);
+    mn1 = fminf(mn1, S.red[w]);
+    mx1 = fmaxf(mx1, S.red[kWarps + w]);
+    ml1 = fmaxf(ml1, S.red[2 * kWarps + w]);
+    mn2 = fminf(mn2, S.red[3 * kWarps + w]);
+    mx2 = fmaxf(mx2, S.red[4 * kWarps + w]);
+    ml2 = fmaxf(ml2, S.red[5 * kWarps + w]);
   }
-  Bins B;
-  B.mn = mn;
-  {
-    float sc = mx > mn ? (float)kBins / (mx - mn) : 0.0f;
-    if (!(sc <= 1e30f)) sc = 1e30f;
-    B.scale = sc;
-  }
-  // 2. stable ranking by bin: counts per (round, warp, bin)
-  int bn[kRounds];
-  uint32_t rk[kRounds];
-#pragma unroll
-  for (int r = 0; r < kRounds; ++r) {
-    const uint32_t s = r * kThreads + tid;
-    const bool v = s < fill;
-    bn[r] = v ? B(b12[r].x) : kBins;  // kBins = "no bin"
-    const unsigned peers = __match_any_sync(kFull, bn[r]);
-    rk[r] = __popc(peers & lanemask_lt());
-    if (v && rk[r] == 0) S.wc[(r * kWarps + warp) * kBins + bn[r]] = (uint16_t)__popc(peers);
-  }
-  __syncthreads();
-  uint32_t tot = 0;  // per bin: total, and exclusive prefix over (round, warp) in place
-  if (tid < kBins) {
-#pragma unroll 8
-    for (int q = 0; q < kRounds * kWarps; ++q) {
-      const uint32_t c = S.wc[q * kBins + tid];
-      S.wc[q * kBins + tid] = (uint16_t)tot;
-      tot += c;
-    }
-  }
-  {
-    uint32_t total;
-    const uint32_t ex = block_excl_scan<kThreads, uint32_t>(tid < kBins ? tot : 0u, S.scan32, &total);
-    if (tid < kBins) S.bstart[tid] = ex;
-    if (tid == 0) S.bstart[kBins] = total;
-  }
-  __syncthreads();
-  // 3. place every candidate at its binned slot
+  Bins B1, B2;
+  B1.init(mn1, mx1);
+  B2.init(mn2, mx2);
+  // 2. cells, totals per cell (order-free), then the cell starts
 #pragma unroll
   for (int r = 0; r < kRounds; ++r) {
     const uint32_t s = r * kThreads + tid;
     if (s < fill) {
-      const uint32_t q = S.bstart[bn[r]] + S.wc[(r * kWarps + warp) * kBins + bn[r]] + rk[r];
-      S.c12[q] = b12[r];
-      S.c0[q] = b0[r];
-      S.cpos[q] = S.fpos[s];
+      const float4 b = S.c12[s];
+      cell[r] = B2(b.z) * kG + B1(b.x);
+      atomicAdd(&S.run[cell[r]], 1u);
+    } else {
+      cell[r] = kCells;  // "no cell"
     }
   }
   __syncthreads();
-  // 4. every row scans the bins that can pass its dim-1 float test
+  {
+    uint32_t total;
+    const uint32_t ex = block_excl_scan<kThreads, uint32_t>(S.run[tid], S.scan32, &total);
+    S.cstart[tid] = ex;
+    if (tid == 0) S.cstart[kCells] = total;
+    S.run[tid] = ex;  // running slot cursor per cell
+  }
+  __syncthreads();
+  // 3. stable placement, one round of kThreads slots at a time: rank among
+  // the round's earlier warps (per-warp counts) and lanes (match_any)
+  float4 keep[kRounds];
+  uint32_t kpos[kRounds];
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    const uint32_t s = r * kThreads + tid;
+    if (s < fill) { keep[r] = S.c12[s]; kpos[r] = S.fpos[s]; }
+  }
+  __syncthreads();  // c12 is rewritten in cell order below
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    for (int i = tid; i < kWarps * kCells / 2; i += kThreads) reinterpret_cast<uint32_t*>(S.wc)[i] = 0;
+    __syncthreads();
+    const unsigned peers = __match_any_sync(kFull, cell[r]);
+    const uint32_t rk = __popc(peers & lanemask_lt());
+    if (cell[r] < kCells && rk == 0) S.wc[warp * kCells + cell[r]] = (uint16_t)__popc(peers);
+    __syncthreads();
+    {  // thread = cell: exclusive prefix over warps, advance the running cursor
+      uint32_t acc = S.run[tid];
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        const uint32_t c = S.wc[w * kCells + tid];
+        S.wc[w * kCells + tid] = (uint16_t)(acc - S.cstart[tid]);
+        acc += c;
+      }
+      S.run[tid] = acc;
+    }
+    __syncthreads();
+    if (cell[r] < kCells) {
+      const uint32_t q = S.cstart[cell[r]] + S.wc[warp * kCells + cell[r]] + rk;
+      S.c12[q] = keep[r];
+      S.cpos[q] = kpos[r];
+    }
+    __syncthreads();  // wc is zeroed again by the next round
+  }
+  // 4. every row scans the cells that can pass its float test on dims 1, 2
+  // (one contiguous run per dim-2 bin).  Float passes are queued per lane and
+  // re-tested exactly in batches (the exact test reads global memory;
+  // batching keeps one lane's rare pass from stalling its warp every time).
+  uint32_t nl = 0;
 #pragma unroll
   for (int q = 0; q < R; ++q) {
     if (!rw.valid[q]) continue;
-    const int bl = B(__fsub_rd(rw.lo1[q], ml));
-    const int bh = B(rw.hi1[q]);
-    const uint32_t k1 = S.bstart[bh + 1];
-    for (uint32_t k = S.bstart[bl]; k < k1; ++k) {
-      const float4 f = S.c12[k];
-      if (!(f.x <= rw.hi1[q] && rw.lo1[q] <= f.y && f.z <= rw.hi2[q] && rw.lo2[q] <= f.w)) continue;
-      const float2 g = S.c0[k];
-      if (!(g.x <= rw.hi0[q] && rw.lo0[q] <= g.y)) continue;
-      const int row = q * kThreads + tid;
-      const uint32_t p = S.cpos[k];
-      if (!exact_hit<R>(A, S, p, row)) continue;
-      if (EMIT) A.pairs[S.roff[row] + rw.hits[q]] = make_uint2(A.slo_id[p], S.ruid[row]);
-      ++rw.hits[q];
+    const float4 u = S.rbox[q * kThreads + tid];
+    const int b1l = B1(__fsub_rd(u.x, ml1)), b1h = B1(u.y);
+    const int b2l = B2(__fsub_rd(u.z, ml2)), b2h = B2(u.w);
+    for (int b2 = b2l; b2 <= b2h; ++b2) {
+      const uint32_t k1 = S.cstart[b2 * kG + b1h + 1];
+      for (uint32_t k = S.cstart[b2 * kG + b1l]; k < k1; ++k) {
+        const float4 f = S.c12[k];
+        if (!(f.x <= u.y && u.x <= f.y && f.z <= u.w && u.z <= f.w)) continue;
+        if (nl == kList) {
+          flush_list<R, EMIT>(A, S, rw, nl);
+          nl = 0;
+        }
+        S.lst[nl * kThreads + tid] = (uint16_t)((q << 12) | k);
+        ++nl;
+      }
     }
   }
+  flush_list<R, EMIT>(A, S, rw, nl);
   __syncthreads();
 }
 
 template <int R, bool EMIT>
-__global__ void __launch_bounds__(kThreads, 3) dd_tile_kernel(Args A) {
+__global__ void __launch_bounds__(kThreads, 4) dd_tile_kernel(Args A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<R>& S = *reinterpret_cast<Smem<R>*>(smem_raw);
   constexpr int kRows = kThreads * R;
@@ -275,23 +332,17 @@ __global__ void __launch_bounds__(kThreads, 3) dd_tile_kernel(Args A) {
 #pragma unroll
   for (int q = 0; q < R; ++q) {
     const uint64_t j = j0 + (uint64_t)q * kThreads + tid;
-    const int row = q * kThreads + tid;
     rw.valid[q] = j < A.m;
     rw.hits[q] = 0;
+    rw.off[q] = 0;
     if (rw.valid[q]) {
       const uint32_t lid = A.ulo_id[j];
-      const uint64_t a = A.ulo_key[j];
-      const double hi0 = A.upd.hi[0][lid];
-      S.ra[row] = a;
-      S.rb[row] = f64_key(hi0);
-      S.rlid[row] = lid;
-      S.ruid[row] = A.upd_map ? A.upd_map[lid] : lid;
-      rw.lo0[q] = __double2float_rd(key_to_f64(a));
-      rw.hi0[q] = __double2float_ru(hi0);
-      rw.lo1[q] = __double2float_rd(A.upd.lo[1][lid]);
-      rw.hi1[q] = __double2float_ru(A.upd.hi[1][lid]);
-      rw.lo2[q] = A.d > 2 ? __double2float_rd(A.upd.lo[2][lid]) : -kInf;
-      rw.hi2[q] = A.d > 2 ? __double2float_ru(A.upd.hi[2][lid]) : kInf;
+      float4 u;
+      u.x = __double2float_rd(A.upd.lo[1][lid]);
+      u.y = __double2float_ru(A.upd.hi[1][lid]);
+      u.z = A.d > 2 ? __double2float_rd(A.upd.lo[2][lid]) : -kInf;
+      u.w = A.d > 2 ? __double2float_ru(A.upd.hi[2][lid]) : kInf;
+      S.rbox[q * kThreads + tid] = u;
       const uint32_t rb = A.r_b[j];
       rbmax = rb > rbmax ? rb : rbmax;
     }
@@ -302,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 3) dd_tile_kernel(Args A) {
       const uint64_t j = j0 + (uint64_t)q * kThreads + tid;
       uint64_t total;
       const uint64_t e = block_excl_scan<kThreads, uint64_t>(rw.valid[q] ? (uint64_t)A.cnt[j] : 0ull, S.scan64, &total);
-      if (rw.valid[q]) S.roff[q * kThreads + tid] = A.tile_off[(j0 >> 8) + q] + e;
+      if (rw.valid[q]) rw.off[q] = A.tile_off[(j0 >> 8) + q] + e;
     }
   }
   rbmax = __reduce_max_sync(kFull, rbmax);

@@ -136,8 +136,7 @@ struct Index {
   uint64_t* lvl[kMaxLevels + 1] = {};
   uint64_t* shi_key = nullptr;
   double* sdims = nullptr;
-  float4* box12 = nullptr;  // d > 1: widened float32 boxes in Slo order (dd.cuh)
-  float2* box0 = nullptr;
+  float4* box12 = nullptr;  // d > 1: widened float32 boxes (dims 1, 2) in Slo order (dd.cuh)
   size_t bytes = 0;
 };
 
@@ -162,7 +161,6 @@ Index index_layout(uint32_t d, uint64_t n, void* base) {
   I.sdims = c.take<double>((uint64_t)2 * (d - 1) * n);
   if (d > 1) {
     I.box12 = c.take<float4>(n);
-    I.box0 = c.take<float2>(n);
   }
   I.bytes = c.used;
   return I;
@@ -571,9 +569,9 @@ ddm_status build_index_async(const ddm_regions* R, const Index& I, SortScratch& 
     DDM_LAUNCH("gather_dims", 36.0 * (R->d - 1) * n, st, match::gather_dims_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.slo_id, D, (int)R->d, n, I.sdims,
                                                                                    use_msd ? &misc->overflow : nullptr));
     DDM_TRY(check_launch());
-    DDM_LAUNCH("dd_boxes", 24.0 * n + 16.0 * (R->d > 2 ? 2 : 1) * n + 24.0 * n, st,
-               dd::box_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.slo_key, I.slo_hi, I.sdims, (int)R->d, n, I.box12,
-                                                                   I.box0, use_msd ? &misc->overflow : nullptr));
+    DDM_LAUNCH("dd_boxes", 16.0 * (R->d > 2 ? 2 : 1) * n + 16.0 * n, st,
+               dd::box_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.sdims, (int)R->d, n, I.box12,
+                                                                   use_msd ? &misc->overflow : nullptr));
     DDM_TRY(check_launch());
   }
   return DDM_OK;
@@ -690,7 +688,6 @@ ddm_status match_indexed(const MatchReq& q, MatchWs& W, uint64_t* count_out, boo
     D.T = tree_of(I);
     D.sdims = I.sdims;
     D.box12 = I.box12;
-    D.box0 = I.box0;
     D.n = n;
     D.m = m;
     D.d = (int)d;
