@@ -194,6 +194,8 @@ struct SortScratch {
   // value-bucketed MSD sort
   uint32_t* dh;        // [3][256] digit histograms of the bucket id
   uint64_t* mm;        // [3][2] min/max keys (Slo, Shi, Ulo)
+  uint32_t* ccount;    // [kCoarse] coarse-bin population of the sort in flight
+  uint32_t* cbase;     // [kCoarse + 1] its bucket map
   uint64_t* alt_keys2;
   uint64_t* alt_v64[2];
   uint32_t* alt_vals2;
@@ -210,6 +212,8 @@ SortScratch sort_scratch(Carver& c, uint64_t cap) {
   s.alt_vals = c.take<uint32_t>(cap);
   s.dh = c.take<uint32_t>(3 * 256);
   s.mm = c.take<uint64_t>(6);
+  s.ccount = c.take<uint32_t>(msd::kCoarse + 1);
+  s.cbase = c.take<uint32_t>(msd::kCoarse + 2);
   s.alt_keys2 = c.take<uint64_t>(cap);
   s.alt_v64[0] = c.take<uint64_t>(cap);
   s.alt_v64[1] = c.take<uint64_t>(cap);
@@ -428,8 +432,17 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, cons
   const int bits = msd_bits(n);
   const uint32_t nb = 1u << bits;
   const int passes = (bits + 7) / 8;
+  // bucket map equalised to the data (coarse population -> bucket allocation)
+  DDM_CUDA(cudaMemsetAsync(s.ccount, 0, sizeof(uint32_t) * (msd::kCoarse + 1), st));
+  const msd::MapRef M{mm, s.cbase};
+  DDM_LAUNCH("msd_coarse", 8.0 * n / msd::kSampleStride, st,
+             msd::coarse_hist_kernel<true><<<grid_for((n + msd::kSampleStride - 1) / msd::kSampleStride, 512, 4), 512, 0, st>>>(
+                 src, n, M, s.ccount));
+  DDM_TRY(check_launch());
+  DDM_LAUNCH("msd_map", 0, st, msd::map_build_kernel<<<1, 1024, 0, st>>>(s.ccount, bits, s.cbase));
+  DDM_TRY(check_launch());
   DDM_CUDA(cudaMemsetAsync(s.dh, 0, sizeof(uint32_t) * 3 * 256, st));
-  DDM_LAUNCH("msd_hist", 8.0 * n, st, msd::msd_hist_kernel<true><<<grid_for(n, 512, 4), 512, 0, st>>>(src, n, mm, bits, passes, s.dh));
+  DDM_LAUNCH("msd_hist", 8.0 * n, st, msd::msd_hist_kernel<true><<<grid_for(n, 512, 4), 512, 0, st>>>(src, n, M, bits, passes, s.dh));
   DDM_TRY(check_launch());
   DDM_LAUNCH("radix_bin_start", 0, st, radix::bin_start_kernel<<<passes, radix::kRadix, 0, st>>>(s.dh, s.starts));
   DDM_TRY(check_launch());
@@ -448,23 +461,23 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, cons
       if (PAY)
         DDM_LAUNCH("msd_pass_pay", bytes, st, msd::msd_pass_kernel<msd::kItems, true, true, true>
                    <<<(unsigned)tiles, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, true, true>), st>>>(
-                       src, v64_src, nullptr, bk[o], bv[o], bi[o], n, mm, bits, 8 * p, s.starts + p * 256, s.status,
+                       src, v64_src, nullptr, bk[o], bv[o], bi[o], n, M, bits, 8 * p, s.starts + p * 256, s.status,
                        s.counters + p));
       else
         DDM_LAUNCH("msd_pass", bytes, st, msd::msd_pass_kernel<msd::kItems, false, false, true>
                    <<<(unsigned)tiles, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, false, false>), st>>>(
-                       src, nullptr, nullptr, bk[o], nullptr, nullptr, n, mm, bits, 8 * p, s.starts + p * 256, s.status,
+                       src, nullptr, nullptr, bk[o], nullptr, nullptr, n, M, bits, 8 * p, s.starts + p * 256, s.status,
                        s.counters + p));
     } else {
       if (PAY)
         DDM_LAUNCH("msd_pass_pay", bytes, st, msd::msd_pass_kernel<msd::kItems, true, true, false>
                    <<<(unsigned)tiles, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, true, true>), st>>>(
-                       bk[q], bv[q], bi[q], bk[o], bv[o], bi[o], n, mm, bits, 8 * p, s.starts + p * 256, s.status,
+                       bk[q], bv[q], bi[q], bk[o], bv[o], bi[o], n, M, bits, 8 * p, s.starts + p * 256, s.status,
                        s.counters + p));
       else
         DDM_LAUNCH("msd_pass", bytes, st, msd::msd_pass_kernel<msd::kItems, false, false, false>
                    <<<(unsigned)tiles, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, false, false>), st>>>(
-                       bk[q], nullptr, nullptr, bk[o], nullptr, nullptr, n, mm, bits, 8 * p, s.starts + p * 256, s.status,
+                       bk[q], nullptr, nullptr, bk[o], nullptr, nullptr, n, M, bits, 8 * p, s.starts + p * 256, s.status,
                        s.counters + p));
     }
     DDM_TRY(check_launch());
@@ -473,11 +486,11 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, cons
   if (PAY)
     DDM_LAUNCH("msd_local_pay", 40.0 * n, st, msd::local_sort_kernel<true, true>
                <<<spans, msd::kThreads, sizeof(msd::LocalSmem<true, true>), st>>>(
-                   bk[l], bv[l], bi[l], out_key, out_v64, out_v32, n, mm, bits, overflow));
+                   bk[l], bv[l], bi[l], out_key, out_v64, out_v32, n, M, bits, overflow));
   else
     DDM_LAUNCH("msd_local", 16.0 * n, st, msd::local_sort_kernel<false, false>
                <<<spans, msd::kThreads, sizeof(msd::LocalSmem<false, false>), st>>>(
-                   bk[l], nullptr, nullptr, out_key, nullptr, nullptr, n, mm, bits, overflow));
+                   bk[l], nullptr, nullptr, out_key, nullptr, nullptr, n, M, bits, overflow));
   return check_launch();
 }
 

@@ -38,30 +38,130 @@ constexpr int kFineBins = 4096;  // value bins of the in-smem counting sort
 constexpr int kMaxBinRun = 64;   // larger bins (ties, clusters) -> bitonic sort of the group
 
 
-// Monotone value -> bucket map: round((x/2 - min/2) * scale), clamped to
-// [0, NB-1].  Every step (x/2, fma, fmin/fmax, round-to-nearest via the
-// 1.5*2^52 magic add) is monotone non-decreasing in x, so bucket order never
-// contradicts key order; fmax(NaN, 0) = 0 guards degenerate scales.
+// Value -> bucket map, equalised to the data.  t(x) = (x/2 - min/2) * kCoarse /
+// (max/2 - min/2) places x among kCoarse equal-width coarse bins (c =
+// clamp(floor(t))); coarse bin c owns the buckets [base[c], base[c+1]),
+// allocated in proportion to its population (map_build_kernel), and x goes to
+// base[c] + floor(frac(t) * alloc_c).  Every step (x/2, fma, floor, the clamps,
+// a non-negative scale) is monotone non-decreasing in x and bin c's buckets
+// all precede bin c+1's, so bucket order never contradicts key order; the
+// equalisation keeps buckets near their nominal size on skewed (clustered)
+// inputs.
+constexpr int kCoarse = 2048;
+
+struct MapRef {
+  const uint64_t* mm;    // [min key, max key] (validation)
+  const uint32_t* base;  // [kCoarse + 2]: first bucket of every coarse bin, then the "linear" flag
+};
+
+// The map is a heuristic: ANY monotone map gives the same sorted result (only
+// bucket sizes change), so it is built from a sample, and when the sample
+// shows no coarse bin denser than kLinearMax x the mean, the plain linear map
+// round(t * NB / kCoarse) is used instead (cheaper per element).
+constexpr uint32_t kSampleChunk = 2048;  // coarse_hist reads 1 chunk of this size ...
+constexpr uint32_t kSampleStride = 16;   // ... out of every kSampleStride
+constexpr double kLinearMax = 1.5;
+
 struct Bucketer {
-  double a, b, top;  // u = fma(x, a, b) = (x*0.5 - min*0.5) * scale
-  __device__ __forceinline__ void init(const uint64_t* mm, int bits) {
-    const double xmin = key_to_f64(mm[0]), xmax = key_to_f64(mm[1]);
+  double a, b;   // t = fma(x, a, b) in [0, kCoarse] over [min, max]
+  double la;     // linear map: bucket = round(t * la)
+  const uint32_t* base;
+  uint32_t top;
+  bool linear;
+  __device__ __forceinline__ void init(MapRef M, int bits) {
+    const double xmin = key_to_f64(M.mm[0]), xmax = key_to_f64(M.mm[1]);
     const double hmin = xmin * 0.5;
     const double range = xmax * 0.5 - hmin;
-    const double nb = (double)(1ull << bits);
-    double s = range > 0.0 ? (nb - 1.0) / range : 0.0;
+    double s = range > 0.0 ? (double)kCoarse / range : 0.0;
     if (!(s <= 1e300)) s = 1e300;
     a = 0.5 * s;
     b = -hmin * s;
-    top = nb - 1.0;
+    top = (1u << bits) - 1u;
+    la = (double)top / (double)kCoarse;
+    base = M.base;
+    linear = M.base == nullptr || M.base[kCoarse + 1] != 0;
+  }
+  __device__ __forceinline__ double pos(uint64_t key, int* c) const {
+    const double t = fma(key_to_f64(key), a, b);
+    const double tc = fmin(fmax(floor(t), 0.0), (double)(kCoarse - 1));
+    *c = (int)tc;
+    return t - tc;
+  }
+  __device__ __forceinline__ int coarse(uint64_t key) const {
+    int c;
+    pos(key, &c);
+    return c;
   }
   __device__ __forceinline__ uint32_t operator()(uint64_t key) const {
-    const double x = key_to_f64(key);
-    double u = fma(x, a, b);
-    u = fmin(fmax(u, 0.0), top);
-    return (uint32_t)__double_as_longlong(u + 6755399441055744.0);
+    if (linear) {  // round-to-nearest via the 1.5*2^52 magic add; clamps make it total
+      double u = fma(key_to_f64(key), a * la, b * la);
+      u = fmin(fmax(u, 0.0), (double)top);
+      return (uint32_t)__double_as_longlong(u + 6755399441055744.0);
+    }
+    int c;
+    const double f = pos(key, &c);
+    const uint32_t b0 = __ldg(base + c), al = __ldg(base + c + 1) - b0;
+    uint32_t u = 0;
+    if (al) u = (uint32_t)fmin(fmax(floor(f * (double)al), 0.0), (double)(al - 1));
+    const uint32_t r = b0 + u;
+    return r < top ? r : top;
   }
 };
+
+// Coarse-bin population of a sample (chunks of kSampleChunk, one in every
+// kSampleStride): counts[kCoarse] (zeroed), counts[kCoarse] = sample size.
+template <bool SRC_F64>
+__global__ void __launch_bounds__(512) coarse_hist_kernel(const void* __restrict__ src, uint64_t n, MapRef M,
+                                                          uint32_t* __restrict__ counts) {
+  __shared__ uint32_t sh[kCoarse];
+  __shared__ uint32_t tot;
+  Bucketer B;
+  B.init(MapRef{M.mm, nullptr}, 1);
+  for (int i = threadIdx.x; i < kCoarse; i += blockDim.x) sh[i] = 0;
+  if (threadIdx.x == 0) tot = 0;
+  __syncthreads();
+  const uint64_t chunks = (n + kSampleChunk - 1) / kSampleChunk;
+  uint32_t mine = 0;
+  for (uint64_t ch = (uint64_t)blockIdx.x * kSampleStride; ch < chunks; ch += (uint64_t)gridDim.x * kSampleStride) {
+    const uint64_t e = umin64(n, (ch + 1) * kSampleChunk);
+    for (uint64_t i = ch * kSampleChunk + threadIdx.x; i < e; i += blockDim.x) {
+      const uint64_t k = SRC_F64 ? f64_key(__ldcs(reinterpret_cast<const double*>(src) + i))
+                                 : __ldcs(reinterpret_cast<const uint64_t*>(src) + i);
+      atomicAdd(&sh[B.coarse(k)], 1u);
+      ++mine;
+    }
+  }
+  atomicAdd(&tot, mine);
+  __syncthreads();
+  for (int i = threadIdx.x; i < kCoarse; i += blockDim.x)
+    if (sh[i]) atomicAdd(counts + i, sh[i]);
+  if (threadIdx.x == 0 && tot) atomicAdd(counts + kCoarse, tot);
+}
+
+// base[c] = floor(cum_c * NB / total) with cum_c the sampled population of
+// bins < c, so base[0] = 0, base[kCoarse] = NB and every bin gets buckets in
+// proportion to its population; base[kCoarse + 1] = 1 when the linear map is
+// good enough (no bin above kLinearMax x the mean).  One CTA, 1024 threads.
+__global__ void __launch_bounds__(1024) map_build_kernel(const uint32_t* __restrict__ counts, int bits,
+                                                         uint32_t* __restrict__ base) {
+  __shared__ uint64_t tmp[1024 / 32 + 1];
+  __shared__ uint32_t cmax;
+  const int t = threadIdx.x;
+  if (t == 0) cmax = 0;
+  __syncthreads();
+  const uint64_t c0 = counts[2 * t], c1 = counts[2 * t + 1];
+  atomicMax(&cmax, (uint32_t)(c0 > c1 ? c0 : c1));
+  uint64_t total;
+  const uint64_t ex = block_excl_scan<1024, uint64_t>(c0 + c1, tmp, &total);
+  const uint64_t nb = 1ull << bits;
+  const uint64_t nn = total ? total : 1;
+  base[2 * t] = (uint32_t)(ex * nb / nn);
+  base[2 * t + 1] = (uint32_t)((ex + c0) * nb / nn);
+  if (t == 0) {
+    base[kCoarse] = (uint32_t)nb;
+    base[kCoarse + 1] = (double)cmax * kCoarse <= kLinearMax * (double)nn ? 1u : 0u;
+  }
+}
 
 // ---------------------------------------------------------------- histograms
 
@@ -69,11 +169,11 @@ struct Bucketer {
 // straight from the data with shared-memory counters.  out: [passes][256].
 template <bool SRC_F64>
 __global__ void __launch_bounds__(512) msd_hist_kernel(const void* __restrict__ src, uint64_t n,
-                                                       const uint64_t* __restrict__ mm, int bits, int passes,
+                                                       MapRef M, int bits, int passes,
                                                        uint32_t* __restrict__ out) {
   __shared__ uint32_t sh[3][kRadix];
   Bucketer B;
-  B.init(mm, bits);
+  B.init(M, bits);
   for (int i = threadIdx.x; i < 3 * kRadix; i += blockDim.x) (&sh[0][0])[i] = 0;
   __syncthreads();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -116,7 +216,7 @@ template <int ITEMS, bool V64, bool V32, bool SRC_F64>
 __global__ void __launch_bounds__(kThreads, 3)
     msd_pass_kernel(const void* __restrict__ k_in, const void* __restrict__ v64_in, const uint32_t* __restrict__ v32_in,
                     uint64_t* __restrict__ k_out, uint64_t* __restrict__ v64_out, uint32_t* __restrict__ v32_out,
-                    uint64_t n, const uint64_t* __restrict__ mm, int bits, int shift,
+                    uint64_t n, MapRef M, int bits, int shift,
                     const uint32_t* __restrict__ bin_start, uint32_t* __restrict__ status,
                     uint32_t* __restrict__ tile_counter) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -125,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 3)
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   Bucketer BK;
-  BK.init(mm, bits);
+  BK.init(M, bits);
   {
     uint4* z = reinterpret_cast<uint4*>(&S.wbase[0][0]);
     constexpr int kZ = 2 * kWarps * kRadix / 4;
@@ -433,12 +533,12 @@ __global__ void __launch_bounds__(kThreads) local_sort_kernel(const uint64_t* __
                                                               uint64_t* __restrict__ k_out,
                                                               uint64_t* __restrict__ v64_out,
                                                               uint32_t* __restrict__ v32_out, uint64_t n,
-                                                              const uint64_t* __restrict__ mm, int bits,
+                                                              MapRef M, int bits,
                                                               uint32_t* __restrict__ overflow) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocalSmem<V64, V32>& S = *reinterpret_cast<LocalSmem<V64, V32>*>(smem_raw);
   Bucketer BK;
-  BK.init(mm, bits);
+  BK.init(M, bits);
   const uint64_t s0 = (uint64_t)blockIdx.x * kSpan;
   uint64_t e0 = next_boundary(k_in, n, s0, BK, &S.bound[0]);
   const uint64_t e1 = next_boundary(k_in, n, umin64(s0 + kSpan, n), BK, &S.bound[1]);
