@@ -348,6 +348,16 @@ void launch_pass(bool kv, bool f64, uint64_t tiles, cudaStream_t st, const void*
         ki, vi, ko, vo, n, shift, mask, starts, status, counter);
 }
 
+// Resident CTAs of a kernel for a persistent grid: occupancy x SM count.
+unsigned persistent_grid(const void* fn, int threads, size_t smem, uint64_t work_tiles) {
+  int dev = 0, sms = kSMs, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, smem) != cudaSuccess || per < 1) per = 1;
+  const uint64_t g = (uint64_t)sms * per;
+  return (unsigned)(work_tiles < g ? (work_tiles ? work_tiles : 1) : g);
+}
+
 inline unsigned grid_for(uint64_t n, int threads, int per_sm) {
   uint64_t g = (n + threads - 1) / threads;
   uint64_t cap = (uint64_t)kSMs * per_sm;
@@ -460,23 +470,23 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, cons
     if (p == 0) {
       if (PAY)
         DDM_LAUNCH("msd_pass_pay", bytes, st, msd::msd_pass_kernel<msd::kItems, true, true, true>
-                   <<<(unsigned)tiles, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, true, true>), st>>>(
+                   <<<persistent_grid((const void*)msd::msd_pass_kernel<msd::kItems, true, true, true>, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, true, true>), tiles), msd::kThreads, sizeof(msd::PassSmem<msd::kItems, true, true>), st>>>(
                        src, v64_src, nullptr, bk[o], bv[o], bi[o], n, M, bits, 8 * p, s.starts + p * 256, s.status,
                        s.counters + p));
       else
         DDM_LAUNCH("msd_pass", bytes, st, msd::msd_pass_kernel<msd::kItems, false, false, true>
-                   <<<(unsigned)tiles, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, false, false>), st>>>(
+                   <<<persistent_grid((const void*)msd::msd_pass_kernel<msd::kItems, false, false, true>, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, false, false>), tiles), msd::kThreads, sizeof(msd::PassSmem<msd::kItems, false, false>), st>>>(
                        src, nullptr, nullptr, bk[o], nullptr, nullptr, n, M, bits, 8 * p, s.starts + p * 256, s.status,
                        s.counters + p));
     } else {
       if (PAY)
         DDM_LAUNCH("msd_pass_pay", bytes, st, msd::msd_pass_kernel<msd::kItems, true, true, false>
-                   <<<(unsigned)tiles, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, true, true>), st>>>(
+                   <<<persistent_grid((const void*)msd::msd_pass_kernel<msd::kItems, true, true, false>, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, true, true>), tiles), msd::kThreads, sizeof(msd::PassSmem<msd::kItems, true, true>), st>>>(
                        bk[q], bv[q], bi[q], bk[o], bv[o], bi[o], n, M, bits, 8 * p, s.starts + p * 256, s.status,
                        s.counters + p));
       else
         DDM_LAUNCH("msd_pass", bytes, st, msd::msd_pass_kernel<msd::kItems, false, false, false>
-                   <<<(unsigned)tiles, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, false, false>), st>>>(
+                   <<<persistent_grid((const void*)msd::msd_pass_kernel<msd::kItems, false, false, false>, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, false, false>), tiles), msd::kThreads, sizeof(msd::PassSmem<msd::kItems, false, false>), st>>>(
                        bk[q], nullptr, nullptr, bk[o], nullptr, nullptr, n, M, bits, 8 * p, s.starts + p * 256, s.status,
                        s.counters + p));
     }

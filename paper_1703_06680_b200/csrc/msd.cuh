@@ -212,6 +212,42 @@ struct PassSmem {
 // the onesweep scheme of radix.cuh (early counts, atomicOr match ranking,
 // decoupled look-back) with a 64-bit and a 32-bit payload.  SRC_F64: the
 // first pass, keys/v64 come from float64 arrays (encoded), v32 = index.
+//
+// Persistent and software-pipelined: a CTA claims tiles in increasing order
+// from an atomic counter; once its current tile is ranked into shared memory
+// it claims the next one and issues that tile's loads into registers, so the
+// look-back wait and the scatter of the current tile overlap the next tile's
+// HBM reads.  (Forward progress: the lowest unfinished tile is always some
+// CTA's current tile, and it only waits on lower, finished tiles.)
+template <int ITEMS, bool V64, bool V32, bool SRC_F64>
+struct TileRegs {
+  uint64_t key[ITEMS];
+  uint64_t hv[V64 ? ITEMS : 1];
+  uint32_t iv[V32 ? ITEMS : 1];
+  __device__ __forceinline__ void load(const void* __restrict__ k_in, const void* __restrict__ v64_in,
+                                       const uint32_t* __restrict__ v32_in, uint64_t wb0, uint64_t n, int lane) {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint64_t idx = wb0 + i * 32 + lane;
+      if (idx < n) {
+        if (SRC_F64) {
+          key[i] = f64_key(__ldcs(reinterpret_cast<const double*>(k_in) + idx));
+          if (V64) hv[i] = f64_key(__ldcs(reinterpret_cast<const double*>(v64_in) + idx));
+          if (V32) iv[i] = (uint32_t)idx;
+        } else {
+          key[i] = __ldcs(reinterpret_cast<const uint64_t*>(k_in) + idx);
+          if (V64) hv[i] = __ldcs(reinterpret_cast<const uint64_t*>(v64_in) + idx);
+          if (V32) iv[i] = __ldcs(v32_in + idx);
+        }
+      } else {
+        key[i] = 0;
+        if (V64) hv[i] = 0;
+        if (V32) iv[i] = 0;
+      }
+    }
+  }
+};
+
 template <int ITEMS, bool V64, bool V32, bool SRC_F64>
 __global__ void __launch_bounds__(kThreads, 3)
     msd_pass_kernel(const void* __restrict__ k_in, const void* __restrict__ v64_in, const uint32_t* __restrict__ v32_in,
@@ -224,143 +260,135 @@ __global__ void __launch_bounds__(kThreads, 3)
   constexpr int kT = Smem::kT;
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t num_tiles = (n + kT - 1) / kT;
   Bucketer BK;
   BK.init(M, bits);
-  {
-    uint4* z = reinterpret_cast<uint4*>(&S.wbase[0][0]);
-    constexpr int kZ = 2 * kWarps * kRadix / 4;
-#pragma unroll
-    for (int i = tid; i < kZ; i += kThreads) z[i] = make_uint4(0, 0, 0, 0);
-  }
   if (tid == 0) S.tile_id = atomicAdd(tile_counter, 1u);
   __syncthreads();
-  const uint32_t tile = S.tile_id;
-  const uint64_t tile_base = (uint64_t)tile * kT;
-  const uint64_t wb0 = tile_base + (uint64_t)warp * (32 * ITEMS);
-  const uint32_t tile_valid = (uint32_t)umin64(kT, n - tile_base);
+  uint32_t tile = S.tile_id;
+  if (tile >= num_tiles) return;
+  TileRegs<ITEMS, V64, V32, SRC_F64> R;
+  R.load(k_in, v64_in, v32_in, (uint64_t)tile * kT + (uint64_t)warp * (32 * ITEMS), n, lane);
 
-  uint64_t key[ITEMS], hv[ITEMS];
-  uint32_t iv[ITEMS], dg[ITEMS];
+  while (true) {
+    const uint64_t tile_base = (uint64_t)tile * kT;
+    const uint64_t wb0 = tile_base + (uint64_t)warp * (32 * ITEMS);
+    const uint32_t tile_valid = (uint32_t)umin64(kT, n - tile_base);
+    {
+      uint4* z = reinterpret_cast<uint4*>(&S.wbase[0][0]);
+      constexpr int kZ = 2 * kWarps * kRadix / 4;
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const uint64_t idx = wb0 + i * 32 + lane;
-    if (idx < n) {
-      if (SRC_F64) {
-        key[i] = f64_key(__ldcs(reinterpret_cast<const double*>(k_in) + idx));
-        if (V64) hv[i] = f64_key(__ldcs(reinterpret_cast<const double*>(v64_in) + idx));
-        if (V32) iv[i] = (uint32_t)idx;
-      } else {
-        key[i] = __ldcs(reinterpret_cast<const uint64_t*>(k_in) + idx);
-        if (V64) hv[i] = __ldcs(reinterpret_cast<const uint64_t*>(v64_in) + idx);
-        if (V32) iv[i] = __ldcs(v32_in + idx);
+      for (int i = tid; i < kZ; i += kThreads) z[i] = make_uint4(0, 0, 0, 0);
+    }
+    __syncthreads();
+    uint32_t dg[ITEMS];
+    uint32_t* wb = S.wbase[warp];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      dg[i] = (BK(R.key[i]) >> shift) & 255u;
+      if (wb0 + i * 32 + lane < n) atomicAdd(&wb[dg[i]], 1u);
+    }
+    __syncthreads();
+    uint32_t total = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t c = S.wbase[w][tid];
+      S.wbase[w][tid] = total;
+      total += c;
+    }
+    uint32_t* my_status = status + (uint64_t)tile * kRadix + tid;
+    st_relaxed_u32(my_status, (tile == 0 ? radix::kFlagPre : radix::kFlagAgg) | total);
+    uint32_t dummy;
+    const uint32_t tstart = block_excl_scan<kThreads>(total, S.scan_tmp, &dummy);
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) S.wbase[w][tid] += tstart;
+    __syncthreads();
+
+    uint32_t* mmask = S.match[warp];
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const bool valid = wb0 + i * 32 + lane < n;
+      const uint32_t d = dg[i];
+      if (valid) atomicOr(&mmask[d], 1u << lane);
+      __syncwarp();
+      uint32_t peers = 0, base = 0;
+      if (valid) {
+        peers = mmask[d];
+        base = wb[d];
       }
-    } else {
-      key[i] = 0;
-      if (V64) hv[i] = 0;
-      if (V32) iv[i] = 0;
-    }
-  }
-  uint32_t* wb = S.wbase[warp];
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    dg[i] = (BK(key[i]) >> shift) & 255u;
-    if (wb0 + i * 32 + lane < n) atomicAdd(&wb[dg[i]], 1u);
-  }
-  __syncthreads();
-  uint32_t total = 0;
-#pragma unroll
-  for (int w = 0; w < kWarps; ++w) {
-    const uint32_t c = S.wbase[w][tid];
-    S.wbase[w][tid] = total;
-    total += c;
-  }
-  uint32_t* my_status = status + (uint64_t)tile * kRadix + tid;
-  st_relaxed_u32(my_status, (tile == 0 ? radix::kFlagPre : radix::kFlagAgg) | total);
-  uint32_t dummy;
-  const uint32_t tstart = block_excl_scan<kThreads>(total, S.scan_tmp, &dummy);
-#pragma unroll
-  for (int w = 0; w < kWarps; ++w) S.wbase[w][tid] += tstart;
-  __syncthreads();
-
-  uint32_t* mmask = S.match[warp];
-  const unsigned lt = lanemask_lt();
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const bool valid = wb0 + i * 32 + lane < n;
-    const uint32_t d = dg[i];
-    if (valid) atomicOr(&mmask[d], 1u << lane);
-    __syncwarp();
-    uint32_t peers = 0, base = 0;
-    if (valid) {
-      peers = mmask[d];
-      base = wb[d];
-    }
-    __syncwarp();
-    if (valid) {
-      const unsigned before = peers & lt;
-      if (before == 0) {
-        wb[d] = base + __popc(peers);
-        mmask[d] = 0;
+      __syncwarp();
+      if (valid) {
+        const unsigned before = peers & lt;
+        if (before == 0) {
+          wb[d] = base + __popc(peers);
+          mmask[d] = 0;
+        }
+        const uint32_t pos = base + __popc(before);
+        S.keys[pos] = R.key[i];
+        if (V64) S.v64[pos] = R.hv[i];
+        if (V32) S.v32[pos] = R.iv[i];
+        S.dg[pos] = (uint8_t)d;
       }
-      const uint32_t pos = base + __popc(before);
-      S.keys[pos] = key[i];
-      if (V64) S.v64[pos] = hv[i];
-      if (V32) S.v32[pos] = iv[i];
-      S.dg[pos] = (uint8_t)d;
+      __syncwarp();
     }
-    __syncwarp();
-  }
+    // claim the next tile and start its loads (the current tile now lives in smem)
+    if (tid == 0) S.tile_id = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const uint32_t next = S.tile_id;
+    if (next < num_tiles) R.load(k_in, v64_in, v32_in, (uint64_t)next * kT + (uint64_t)warp * (32 * ITEMS), n, lane);
 
-  uint32_t excl = 0;
-  if (tile > 0) {
-    constexpr int kLB = 8;
-    int64_t p = (int64_t)tile - 1;
-    while (true) {
-      uint32_t sv[kLB];
+    uint32_t excl = 0;
+    if (tile > 0) {
+      constexpr int kLB = 8;
+      int64_t p = (int64_t)tile - 1;
+      while (true) {
+        uint32_t sv[kLB];
 #pragma unroll
-      for (int k = 0; k < kLB; ++k)
-        sv[k] = p - k >= 0 ? ld_relaxed_u32(status + (uint64_t)(p - k) * kRadix + tid) : radix::kFlagPre;
-      int consumed = 0;
-      bool hit_pre = false;
+        for (int k = 0; k < kLB; ++k)
+          sv[k] = p - k >= 0 ? ld_relaxed_u32(status + (uint64_t)(p - k) * kRadix + tid) : radix::kFlagPre;
+        int consumed = 0;
+        bool hit_pre = false;
 #pragma unroll
-      for (int q = 0; q < kLB; ++q) {
-        if (hit_pre || consumed != q) break;
-        const uint32_t v = sv[q];
-        if ((v & ~radix::kValMask) == 0) break;
-        excl += v & radix::kValMask;
-        consumed = q + 1;
-        hit_pre = (v & radix::kFlagPre) != 0;
+        for (int q = 0; q < kLB; ++q) {
+          if (hit_pre || consumed != q) break;
+          const uint32_t v = sv[q];
+          if ((v & ~radix::kValMask) == 0) break;
+          excl += v & radix::kValMask;
+          consumed = q + 1;
+          hit_pre = (v & radix::kFlagPre) != 0;
+        }
+        if (hit_pre) break;
+        if (consumed == 0) __nanosleep(32);
+        p -= consumed;
       }
-      if (hit_pre) break;
-      if (consumed == 0) __nanosleep(32);
-      p -= consumed;
+      st_relaxed_u32(my_status, radix::kFlagPre | (excl + total));
     }
-    st_relaxed_u32(my_status, radix::kFlagPre | (excl + total));
-  }
-  S.digit_base[tid] = (long long)bin_start[tid] + (long long)excl - (long long)tstart;
-  __syncthreads();
+    S.digit_base[tid] = (long long)bin_start[tid] + (long long)excl - (long long)tstart;
+    __syncthreads();
 
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const uint32_t p = i * kThreads + tid;
-    if (p < tile_valid) {
-      const uint64_t k = S.keys[p];
-      const uint32_t d = S.dg[p];
-      const uint64_t dst = (uint64_t)(S.digit_base[d] + (long long)p);
-      k_out[dst] = k;
-      if (V64) v64_out[dst] = S.v64[p];
-      if (V32) v32_out[dst] = S.v32[p];
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t p = i * kThreads + tid;
+      if (p < tile_valid) {
+        const uint64_t k = S.keys[p];
+        const uint32_t d = S.dg[p];
+        const uint64_t dst = (uint64_t)(S.digit_base[d] + (long long)p);
+        k_out[dst] = k;
+        if (V64) v64_out[dst] = S.v64[p];
+        if (V32) v32_out[dst] = S.v32[p];
+      }
     }
+    if (next >= num_tiles) break;
+    tile = next;  // (the next iteration's first barrier orders these reads before any smem rewrite)
   }
 }
 
 // ---------------------------------------------------------------- local sort
 
 template <bool V64, bool V32>
-struct LocalSmem {
+struct LocalSmem {  // keys only: payloads are gathered from global by the permutation
   uint64_t keys[kCap];
-  uint64_t v64[V64 ? kCap : 2];
-  uint32_t v32[V32 ? kCap : 4];
   uint32_t bin[kFineBins + 1];
   uint16_t perm[kCapPow2];  // sorted position -> staged index
   uint64_t red[2 * kWarps];
@@ -385,8 +413,6 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
     S.keys[i] = k;
     kmin = k < kmin ? k : kmin;
     kmax = k > kmax ? k : kmax;
-    if (V64) S.v64[i] = __ldcs(v64_in + e0 + i);
-    if (V32) S.v32[i] = __ldcs(v32_in + e0 + i);
   }
   for (uint32_t b = tid; b <= kFineBins; b += kThreads) S.bin[b] = 0;
   if (tid == 0) S.flag = 0;
@@ -475,11 +501,13 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
     }
   }
   __syncthreads();
+  // payloads follow the permutation straight from global memory (the group's
+  // payload is a ~20 KB window: every sector is fetched from DRAM once)
   for (uint32_t i = tid; i < c; i += kThreads) {
     const uint16_t t = S.perm[i];
     k_out[e0 + i] = S.keys[t];
-    if (V64) v64_out[e0 + i] = S.v64[t];
-    if (V32) v32_out[e0 + i] = S.v32[t];
+    if (V64) v64_out[e0 + i] = v64_in[e0 + t];
+    if (V32) v32_out[e0 + i] = v32_in[e0 + t];
   }
   __syncthreads();
 }
