@@ -91,6 +91,8 @@ inline void prof_end(const char* name, double bytes, cudaStream_t st, int e0) {
     }                                                    \
   } while (0)
 
+#define DDM_CUDA_RET(call) DDM_CUDA(call)
+
 inline ddm_status check_launch() {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -184,6 +186,8 @@ int msd_bits(uint64_t n) {
 }
 
 
+// LSB onesweep scratch (the fallback path and the exported primitives).  The
+// alternate key/value buffers are set per use (they alias an MSD chain's).
 struct SortScratch {
   uint32_t* hist[3];   // [8][256] each: Slo, Shi, Ulo (or generic)
   uint32_t* starts;    // [8][256] global bin starts of the sort in flight
@@ -191,35 +195,82 @@ struct SortScratch {
   uint32_t* counters;  // [8]
   uint64_t* alt_keys;
   uint32_t* alt_vals;
-  // value-bucketed MSD sort
-  uint32_t* dh;        // [3][256] digit histograms of the bucket id
-  uint64_t* mm;        // [3][2] min/max keys (Slo, Shi, Ulo)
-  uint32_t* ccount;    // [kCoarse] coarse-bin population of the sort in flight
-  uint32_t* cbase;     // [kCoarse + 1] its bucket map
-  uint64_t* alt_keys2;
-  uint64_t* alt_v64[2];
-  uint32_t* alt_vals2;
-  uint64_t cap;
 };
 
-SortScratch sort_scratch(Carver& c, uint64_t cap) {
-  SortScratch s;
+SortScratch sort_scratch(Carver& c, uint64_t cap, bool own_alt) {
+  SortScratch s{};
   for (int i = 0; i < 3; ++i) s.hist[i] = c.take<uint32_t>(radix::kMaxPasses * radix::kRadix);
   s.starts = c.take<uint32_t>(radix::kMaxPasses * radix::kRadix);
   s.status = c.take<uint32_t>((radix::num_tiles(cap) + 1) * radix::kRadix);
   s.counters = c.take<uint32_t>(radix::kMaxPasses);
-  s.alt_keys = c.take<uint64_t>(cap);
-  s.alt_vals = c.take<uint32_t>(cap);
+  if (own_alt) {
+    s.alt_keys = c.take<uint64_t>(cap);
+    s.alt_vals = c.take<uint32_t>(cap);
+  }
+  return s;
+}
+
+// Scratch of one MSD sort chain: its own buffers, so the Slo, Shi and Ulo
+// sorts can run concurrently on separate streams.
+struct MsdScratch {
+  uint32_t* dh;        // [3][256] digit histograms of the bucket id
+  uint32_t* starts;    // [3][256] global digit starts
+  uint32_t* status;    // [tiles][256] look-back words
+  uint32_t* counters;  // [8] tile counters
+  uint32_t* ccount;    // [kCoarse + 1] sampled coarse-bin population
+  uint32_t* cbase;     // [kCoarse + 2] bucket map
+  uint64_t* k[2];      // ping-pong record buffers
+  uint64_t* v64[2];
+  uint32_t* v32[2];
+};
+
+MsdScratch msd_scratch(Carver& c, uint64_t cap, bool kv) {
+  MsdScratch s{};
   s.dh = c.take<uint32_t>(3 * 256);
-  s.mm = c.take<uint64_t>(6);
+  s.starts = c.take<uint32_t>(3 * 256);
+  s.status = c.take<uint32_t>(((cap + msd::kTile - 1) / msd::kTile + 1) * radix::kRadix);
+  s.counters = c.take<uint32_t>(radix::kMaxPasses);
   s.ccount = c.take<uint32_t>(msd::kCoarse + 1);
   s.cbase = c.take<uint32_t>(msd::kCoarse + 2);
-  s.alt_keys2 = c.take<uint64_t>(cap);
-  s.alt_v64[0] = c.take<uint64_t>(cap);
-  s.alt_v64[1] = c.take<uint64_t>(cap);
-  s.alt_vals2 = c.take<uint32_t>(cap);
-  s.cap = cap;
+  for (int i = 0; i < 2; ++i) {
+    s.k[i] = c.take<uint64_t>(cap);
+    if (kv) {
+      s.v64[i] = c.take<uint64_t>(cap);
+      s.v32[i] = c.take<uint32_t>(cap);
+    }
+  }
   return s;
+}
+
+// Side streams for the concurrent sort chains (per device, created once).
+struct SideStreams {
+  cudaStream_t s[2] = {nullptr, nullptr};
+};
+std::mutex g_side_mu;
+SideStreams g_side[64];
+
+ddm_status side_streams(cudaStream_t out[2]) {
+  int dev = 0;
+  DDM_CUDA_RET(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return DDM_ERR_CUDA;
+  std::lock_guard<std::mutex> lk(g_side_mu);
+  SideStreams& S = g_side[dev];
+  for (int i = 0; i < 2; ++i) {
+    if (!S.s[i]) DDM_CUDA_RET(cudaStreamCreateWithFlags(&S.s[i], cudaStreamNonBlocking));
+    out[i] = S.s[i];
+  }
+  return DDM_OK;
+}
+
+// `to` waits for everything enqueued on `from` so far.
+ddm_status stream_join(cudaStream_t to, cudaStream_t from) {
+  cudaEvent_t e;
+  DDM_CUDA_RET(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  const cudaError_t r1 = cudaEventRecord(e, from);
+  const cudaError_t r2 = r1 == cudaSuccess ? cudaStreamWaitEvent(to, e, 0) : r1;
+  cudaEventDestroy(e);  // released once the recorded work completes
+  DDM_CUDA_RET(r2);
+  return DDM_OK;
 }
 
 struct Misc {  // device-side results read back with one copy
@@ -246,15 +297,18 @@ struct MatchWs {
   uint64_t* scan_status;
   uint64_t* part;
   Misc* misc;
-  SortScratch sort;
+  uint64_t* mm;        // [3][2] min/max keys (Slo, Shi, Ulo)
+  MsdScratch slo, shi, ulo;  // MSD chains (slo/shi only with the index scratch)
+  SortScratch sort;    // LSB fallback
   size_t bytes;
 };
 
-MatchWs match_layout(uint32_t d, uint64_t n_sub, uint64_t m, void* base) {
+MatchWs match_layout(uint32_t d, uint64_t n_sub, uint64_t m, void* base, bool index_scratch) {
   Carver c(base);
   MatchWs W{};
   const uint64_t rtiles = m / match::kRowTile + 2;
   W.misc = c.take<Misc>(1);
+  W.mm = c.take<uint64_t>(6);
   W.scan_status = c.take<uint64_t>(rtiles / (match::kScanThreads * match::kScanItems) + 2);
   W.part = c.take<uint64_t>(4 * (m / match::kCountTile + 2));
   W.tile_sum = c.take<uint64_t>(rtiles);
@@ -269,9 +323,22 @@ MatchWs match_layout(uint32_t d, uint64_t n_sub, uint64_t m, void* base) {
     W.cnt = c.take<uint32_t>(m);
     W.fstab = c.take<uint32_t>(m);
   }
-  W.sort = sort_scratch(c, n_sub > m ? n_sub : m);
+  W.ulo = msd_scratch(c, m, true);
+  if (index_scratch) {
+    W.slo = msd_scratch(c, n_sub, true);
+    W.shi = msd_scratch(c, n_sub, false);
+  }
+  W.sort = sort_scratch(c, index_scratch && n_sub > m ? n_sub : m, false);
   W.bytes = c.used;
   return W;
+}
+
+// LSB scratch whose alternate buffers alias an MSD chain's first record buffer.
+SortScratch lsb_with(const SortScratch& s, const MsdScratch& m) {
+  SortScratch r = s;
+  r.alt_keys = m.k[0];
+  r.alt_vals = m.v32[0];
+  return r;
 }
 
 // ------------------------------------------------------------ radix sort driver
@@ -354,6 +421,11 @@ unsigned persistent_grid(const void* fn, int threads, size_t smem, uint64_t work
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, smem) != cudaSuccess || per < 1) per = 1;
+  static const int cap = [] {  // DDM_PASS_CTAS_PER_SM: leave SM slots to concurrent chains
+    const char* e = getenv("DDM_PASS_CTAS_PER_SM");
+    return e ? atoi(e) : 0;
+  }();
+  if (cap > 0 && per > cap) per = cap;
   const uint64_t g = (uint64_t)sms * per;
   return (unsigned)(work_tiles < g ? (work_tiles ? work_tiles : 1) : g);
 }
@@ -438,7 +510,7 @@ ddm_status radix_sort(const void* src, bool src_f64, const uint32_t* vals_in, ui
 // too large for shared memory (caller falls back to radix_sort + gather).
 template <bool PAY>
 ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, const uint64_t* mm, uint64_t* out_key,
-                      uint64_t* out_v64, uint32_t* out_v32, SortScratch& s, uint32_t* overflow, cudaStream_t st) {
+                      uint64_t* out_v64, uint32_t* out_v32, MsdScratch& s, uint32_t* overflow, cudaStream_t st) {
   const int bits = msd_bits(n);
   const uint32_t nb = 1u << bits;
   const int passes = (bits + 7) / 8;
@@ -458,9 +530,9 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, cons
   DDM_TRY(check_launch());
   const uint32_t spans = (uint32_t)((n + msd::kSpan - 1) / msd::kSpan);
   (void)nb;
-  uint64_t* bk[2] = {s.alt_keys, s.alt_keys2};
-  uint64_t* bv[2] = {s.alt_v64[0], s.alt_v64[1]};
-  uint32_t* bi[2] = {s.alt_vals, s.alt_vals2};
+  uint64_t* bk[2] = {s.k[0], s.k[1]};
+  uint64_t* bv[2] = {s.v64[0], s.v64[1]};
+  uint32_t* bi[2] = {s.v32[0], s.v32[1]};
   const uint64_t tiles = (n + msd::kTile - 1) / msd::kTile;
   DDM_CUDA(cudaMemsetAsync(s.counters, 0, sizeof(uint32_t) * radix::kMaxPasses, st));
   for (int p = 0; p < passes; ++p) {
@@ -551,24 +623,33 @@ ddm_status validate_side(uint32_t d, uint64_t cnt, const double* const* lo, cons
 
 // ------------------------------------------------------------ index build (async)
 
-ddm_status build_index_async(const ddm_regions* R, const Index& I, SortScratch& s, Misc* misc, bool use_msd,
-                             cudaStream_t st) {
+// Subscription half: validate, sort Slo (key + upper key + id) and Shi (keys),
+// block maxima, other dimensions in Slo order.  MSD path: the Shi chain runs
+// on a side stream concurrently with the Slo chain; `st` has joined it on
+// return.  mm[0..3] must hold the [min, max] initial values (init_minmax).
+ddm_status build_index_async(const ddm_regions* R, const Index& I, MsdScratch& slo, MsdScratch& shi,
+                             const SortScratch& lsb, uint64_t* mm, Misc* misc, bool use_msd, cudaStream_t st) {
   init_attrs_once();
   const uint64_t n = R->n_sub;
   if (n == 0) return DDM_OK;
   if (use_msd) {
-    DDM_TRY(init_minmax(s.mm, st));
-    DDM_TRY(validate_side(R->d, n, R->sub_lo, R->sub_hi, nullptr, nullptr, &misc->err, st, s.mm + 0, s.mm + 2));
-    // a2 + a3: Slo with the upper key and the id as payload, then Shi keys
-    DDM_TRY(msd_sort_t<true>(R->sub_lo[0], R->sub_hi[0], n, s.mm + 0, I.slo_key, I.slo_hi, I.slo_id, s,
+    DDM_TRY(validate_side(R->d, n, R->sub_lo, R->sub_hi, nullptr, nullptr, &misc->err, st, mm + 0, mm + 2));
+    cudaStream_t side[2];
+    DDM_TRY(side_streams(side));
+    DDM_TRY(stream_join(side[0], st));
+    // a2 + a3: Slo with the upper key and the id as payload (st) || Shi keys (side stream)
+    DDM_TRY(msd_sort_t<false>(R->sub_hi[0], nullptr, n, mm + 2, I.shi_key, nullptr, nullptr, shi, &misc->overflow,
+                              side[0]));
+    DDM_TRY(msd_sort_t<true>(R->sub_lo[0], R->sub_hi[0], n, mm + 0, I.slo_key, I.slo_hi, I.slo_id, slo,
                              &misc->overflow, st));
-    DDM_TRY(msd_sort_t<false>(R->sub_hi[0], nullptr, n, s.mm + 2, I.shi_key, nullptr, nullptr, s, &misc->overflow, st));
     for (int L = 1; L <= I.levels; ++L) {
       DDM_LAUNCH("block_max", 8.0 * I.lvl_n[L - 1], st, match::block_max_kernel<<<grid_for(I.lvl_n[L - 1], 256, 8), 256, 0, st>>>(
           I.lvl[L - 1], I.lvl_n[L - 1], I.lvl[L]));
       DDM_TRY(check_launch());
     }
+    DDM_TRY(stream_join(st, side[0]));
   } else {
+    SortScratch s = lsb_with(lsb, slo);
     DDM_CUDA(cudaMemsetAsync(s.hist[0], 0, sizeof(uint32_t) * 8 * 256, st));
     DDM_CUDA(cudaMemsetAsync(s.hist[1], 0, sizeof(uint32_t) * 8 * 256, st));
     DDM_TRY(validate_side(R->d, n, R->sub_lo, R->sub_hi, s.hist[0], s.hist[1], &misc->err, st));
@@ -624,34 +705,39 @@ struct MatchReq {
   uint32_t flags;
 };
 
-ddm_status match_indexed(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool err_pending, bool use_msd,
-                         cudaStream_t st) {
+// Update side, a1 + a2 (+ a3): validate every dimension, sort Ulo with the
+// upper key and the id as payload (MSD) or key + id (LSB fallback).  With
+// n_sub == 0 only the validation runs.  mm[4..5] must hold init values.
+ddm_status upd_sort_async(const ddm_regions* R, MatchWs& W, uint64_t n_sub, bool use_msd, cudaStream_t st) {
+  const uint64_t m = R->n_upd;
+  const uint32_t d = R->d;
+  if (m == 0) return DDM_OK;
+  init_attrs_once();
+  if (n_sub == 0) return validate_side(d, m, R->upd_lo, R->upd_hi, nullptr, nullptr, &W.misc->err, st);
+  if (use_msd) {
+    DDM_TRY(validate_side(d, m, R->upd_lo, R->upd_hi, nullptr, nullptr, &W.misc->err, st, W.mm + 4));
+    return msd_sort_t<true>(R->upd_lo[0], R->upd_hi[0], m, W.mm + 4, W.ulo_key, W.uhi, W.ulo_id, W.ulo,
+                            &W.misc->overflow, st);
+  }
+  SortScratch s = lsb_with(W.sort, W.ulo);
+  DDM_CUDA(cudaMemsetAsync(s.hist[2], 0, sizeof(uint32_t) * 8 * 256, st));
+  DDM_TRY(validate_side(d, m, R->upd_lo, R->upd_hi, s.hist[2], nullptr, &W.misc->err, st));
+  return radix_sort(R->upd_lo[0], true, nullptr, W.ulo_key, W.ulo_id, m, full_passes(), s.hist[2], true, s, st);
+}
+
+// a4..a8 against a built index, with the updates already sorted on `st`:
+// counts, scan, one D2H of {K, error, overflow}, then the emission.
+ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool use_msd, cudaStream_t st) {
   const Index& I = *q.I;
   const ddm_regions* R = q.R;
   const uint64_t m = R->n_upd, n = I.n;
   const uint32_t d = R->d;
-  if (!err_pending) DDM_CUDA(cudaMemsetAsync(W.misc, 0, sizeof(Misc), st));
-  if (m == 0 || n == 0) {
-    // nothing can match; still validate the non-empty side(s)
-    DDM_TRY(validate_side(d, m, R->upd_lo, R->upd_hi, nullptr, nullptr, &W.misc->err, st));
+  if (m == 0 || n == 0) {  // nothing can match; the non-empty side(s) were validated
     Misc h{};
     DDM_CUDA(cudaMemcpyAsync(&h, W.misc, sizeof(Misc), cudaMemcpyDeviceToHost, st));
     DDM_CUDA(cudaStreamSynchronize(st));
     *count_out = 0;
     return err_status(h.err);
-  }
-  SortScratch& s = W.sort;
-  init_attrs_once();
-  if (use_msd) {
-    if (!err_pending) DDM_TRY(init_minmax(s.mm, st));
-    DDM_TRY(validate_side(d, m, R->upd_lo, R->upd_hi, nullptr, nullptr, &W.misc->err, st, s.mm + 4));
-    // a2 + a3: Ulo with the upper key and the id as payload
-    DDM_TRY(msd_sort_t<true>(R->upd_lo[0], R->upd_hi[0], m, s.mm + 4, W.ulo_key, W.uhi, W.ulo_id, s,
-                             &W.misc->overflow, st));
-  } else {
-    DDM_CUDA(cudaMemsetAsync(s.hist[2], 0, sizeof(uint32_t) * 8 * 256, st));
-    DDM_TRY(validate_side(d, m, R->upd_lo, R->upd_hi, s.hist[2], nullptr, &W.misc->err, st));
-    DDM_TRY(radix_sort(R->upd_lo[0], true, nullptr, W.ulo_key, W.ulo_id, m, full_passes(), s.hist[2], true, s, st));
   }
   // a4: counts by rank difference (+ the row-tile sums); a5: exclusive scan
   // of the row-tile sums -> output offset of every 256-row tile, K
@@ -786,23 +872,40 @@ size_t ddm_sub_index_bytes(uint32_t d, uint64_t n_sub) {
   return index_layout(d, n_sub, nullptr).bytes;
 }
 
+// index build workspace: Misc, mm, the Slo / Shi MSD chains, LSB scratch
+struct BuildWs {
+  Misc* misc;
+  uint64_t* mm;
+  MsdScratch slo, shi;
+  SortScratch lsb;
+  size_t bytes;
+};
+static BuildWs build_layout(uint64_t n_sub, void* base) {
+  Carver c(base);
+  BuildWs B{};
+  B.misc = c.take<Misc>(1);
+  B.mm = c.take<uint64_t>(6);
+  B.slo = msd_scratch(c, n_sub, true);
+  B.shi = msd_scratch(c, n_sub, false);
+  B.lsb = sort_scratch(c, n_sub, false);
+  B.bytes = c.used;
+  return B;
+}
+
 size_t ddm_index_build_workspace_bytes(uint32_t d, uint64_t n_sub) {
   if (d == 0 || d > DDM_MAX_DIMS) return 0;
-  Carver c(nullptr);
-  c.take<Misc>(1);
-  sort_scratch(c, n_sub);
-  return c.used;
+  return build_layout(n_sub, nullptr).bytes;
 }
 
 size_t ddm_indexed_workspace_bytes(uint32_t d, uint64_t n_sub, uint64_t n_upd) {
   if (d == 0 || d > DDM_MAX_DIMS) return 0;
-  return match_layout(d, n_sub, n_upd, nullptr).bytes;
+  return match_layout(d, n_sub, n_upd, nullptr, false).bytes;
 }
 
 size_t ddm_workspace_bytes(uint32_t d, uint64_t n_sub, uint64_t n_upd, int want_pairs) {
   (void)want_pairs;
   if (d == 0 || d > DDM_MAX_DIMS) return 0;
-  return a256(index_layout(d, n_sub, nullptr).bytes) + match_layout(d, n_sub, n_upd, nullptr).bytes;
+  return a256(index_layout(d, n_sub, nullptr).bytes) + match_layout(d, n_sub, n_upd, nullptr, true).bytes;
 }
 
 static ddm_status match_full(const ddm_regions* R, ddm_pair* pairs, uint64_t capacity, uint64_t* count_out,
@@ -813,15 +916,27 @@ static ddm_status match_full(const ddm_regions* R, ddm_pair* pairs, uint64_t cap
   if (ws_bytes < ddm_workspace_bytes(R->d, R->n_sub, R->n_upd, pairs != nullptr)) return DDM_ERR_WORKSPACE;
   uint8_t* base = static_cast<uint8_t*>(ws);
   Index I = index_layout(R->d, R->n_sub, base);
-  MatchWs W = match_layout(R->d, R->n_sub, R->n_upd, base + a256(I.bytes));
+  MatchWs W = match_layout(R->d, R->n_sub, R->n_upd, base + a256(I.bytes), true);
   MatchReq q{&I, R, nullptr, pairs, capacity, flags};
   const bool lsb_only = (flags & DDM_SORT_LSB) != 0;
   for (int attempt = lsb_only ? 1 : 0; attempt < 2; ++attempt) {
     const bool use_msd = attempt == 0;
     DDM_CUDA(cudaMemsetAsync(W.misc, 0, sizeof(Misc), st));
-    if (use_msd) DDM_TRY(init_minmax(W.sort.mm, st));
-    DDM_TRY(build_index_async(R, I, W.sort, W.misc, use_msd, st));
-    const ddm_status r = match_indexed(q, W, count_out, true, use_msd, st);
+    DDM_TRY(init_minmax(W.mm, st));
+    if (use_msd) {
+      // the update chain (side stream 1) runs concurrently with the index
+      // build (Slo on st, Shi on side stream 0); st joins both before a4
+      cudaStream_t side[2];
+      DDM_TRY(side_streams(side));
+      DDM_TRY(stream_join(side[1], st));
+      DDM_TRY(upd_sort_async(R, W, R->n_sub, true, side[1]));
+      DDM_TRY(build_index_async(R, I, W.slo, W.shi, W.sort, W.mm, W.misc, true, st));
+      DDM_TRY(stream_join(st, side[1]));
+    } else {
+      DDM_TRY(build_index_async(R, I, W.slo, W.shi, W.sort, W.mm, W.misc, false, st));
+      DDM_TRY(upd_sort_async(R, W, R->n_sub, false, st));
+    }
+    const ddm_status r = match_sorted(q, W, count_out, use_msd, st);
     if (r != kRetryLSB) return r;
   }
   return DDM_ERR_CUDA;
@@ -848,15 +963,14 @@ ddm_status ddm_sub_index_build(const ddm_regions* subs, void* index, size_t inde
   if (index_bytes < ddm_sub_index_bytes(subs->d, subs->n_sub)) return DDM_ERR_WORKSPACE;
   if (ws_bytes < ddm_index_build_workspace_bytes(subs->d, subs->n_sub)) return DDM_ERR_WORKSPACE;
   Index I = index_layout(subs->d, subs->n_sub, index);
-  Carver c(ws);
-  Misc* misc = c.take<Misc>(1);
-  SortScratch s = sort_scratch(c, subs->n_sub);
+  BuildWs B = build_layout(subs->n_sub, ws);
   Misc h{};
   for (int attempt = 0; attempt < 2; ++attempt) {
     const bool use_msd = attempt == 0;
-    DDM_CUDA(cudaMemsetAsync(misc, 0, sizeof(Misc), stream));
-    DDM_TRY(build_index_async(subs, I, s, misc, use_msd, stream));
-    DDM_CUDA(cudaMemcpyAsync(&h, misc, sizeof(Misc), cudaMemcpyDeviceToHost, stream));
+    DDM_CUDA(cudaMemsetAsync(B.misc, 0, sizeof(Misc), stream));
+    DDM_TRY(init_minmax(B.mm, stream));
+    DDM_TRY(build_index_async(subs, I, B.slo, B.shi, B.lsb, B.mm, B.misc, use_msd, stream));
+    DDM_CUDA(cudaMemcpyAsync(&h, B.misc, sizeof(Misc), cudaMemcpyDeviceToHost, stream));
     DDM_CUDA(cudaStreamSynchronize(stream));
     if (h.err || !h.overflow) break;
   }
@@ -871,13 +985,17 @@ static ddm_status indexed_common(const void* index, const ddm_regions* upds, con
   if (upds->n_sub > DDM_MAX_REGIONS) return DDM_ERR_INVALID_ARGUMENT;
   if (ws_bytes < ddm_indexed_workspace_bytes(upds->d, upds->n_sub, upds->n_upd)) return DDM_ERR_WORKSPACE;
   Index I = index_layout(upds->d, upds->n_sub, const_cast<void*>(index));
-  MatchWs W = match_layout(upds->d, upds->n_sub, upds->n_upd, ws);
+  MatchWs W = match_layout(upds->d, upds->n_sub, upds->n_upd, ws, false);
   MatchReq q{&I, upds, upd_ids, pairs, capacity, flags};
-  if (!(flags & DDM_SORT_LSB)) {
-    const ddm_status r = match_indexed(q, W, count_out, false, true, st);
+  for (int attempt = (flags & DDM_SORT_LSB) ? 1 : 0; attempt < 2; ++attempt) {
+    const bool use_msd = attempt == 0;
+    DDM_CUDA(cudaMemsetAsync(W.misc, 0, sizeof(Misc), st));
+    DDM_TRY(init_minmax(W.mm, st));
+    DDM_TRY(upd_sort_async(upds, W, upds->n_sub, use_msd, st));
+    const ddm_status r = match_sorted(q, W, count_out, use_msd, st);
     if (r != kRetryLSB) return r;
   }
-  return match_indexed(q, W, count_out, false, false, st);
+  return DDM_ERR_CUDA;
 }
 
 ddm_status ddm_match_pairs_indexed(const void* index, const ddm_regions* upds, const uint32_t* upd_ids,
@@ -896,7 +1014,7 @@ ddm_status ddm_match_count_indexed(const void* index, const ddm_regions* upds, u
 
 size_t ddm_sort_pairs_workspace_bytes(uint64_t k) {
   Carver c(nullptr);
-  sort_scratch(c, k);
+  sort_scratch(c, k, true);
   return c.used;
 }
 
@@ -906,7 +1024,7 @@ ddm_status ddm_sort_pairs(ddm_pair* pairs, uint64_t k, uint64_t n_sub, uint64_t 
   if (!pairs || !aligned(pairs, 8) || !aligned(ws, 256)) return DDM_ERR_INVALID_ARGUMENT;
   if (ws_bytes < ddm_sort_pairs_workspace_bytes(k)) return DDM_ERR_WORKSPACE;
   Carver c(ws);
-  SortScratch s = sort_scratch(c, k);
+  SortScratch s = sort_scratch(c, k, true);
   // canonical key (upd << 32) | sub: only the digits that can be non-zero
   radix::PassList P{};
   const int nb = bits_for(n_sub ? n_sub - 1 : 0), mb = bits_for(n_upd ? n_upd - 1 : 0);
@@ -919,7 +1037,7 @@ ddm_status ddm_sort_pairs(ddm_pair* pairs, uint64_t k, uint64_t n_sub, uint64_t 
 
 size_t ddm_radix_sort_workspace_bytes(uint64_t n) {
   Carver c(nullptr);
-  sort_scratch(c, n);
+  sort_scratch(c, n, true);
   return c.used;
 }
 
@@ -933,7 +1051,7 @@ ddm_status ddm_radix_sort_u64(const uint64_t* keys_in, const uint32_t* vals_in, 
   if (keys_in == keys_out || (vals_in && vals_in == vals_out)) return DDM_ERR_INVALID_ARGUMENT;
   if (!aligned(ws, 256) || ws_bytes < ddm_radix_sort_workspace_bytes(n)) return DDM_ERR_WORKSPACE;
   Carver c(ws);
-  SortScratch s = sort_scratch(c, n);
+  SortScratch s = sort_scratch(c, n, true);
   radix::PassList P{};
   for (int b = begin_bit; b < end_bit; b += 8) {
     const int w = end_bit - b < 8 ? end_bit - b : 8;

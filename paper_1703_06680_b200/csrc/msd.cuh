@@ -391,6 +391,7 @@ struct LocalSmem {  // keys only: payloads are gathered from global by the permu
   uint64_t keys[kCap];
   uint32_t bin[kFineBins + 1];
   uint16_t perm[kCapPow2];  // sorted position -> staged index
+  uint16_t grp[kCap];       // staged indices grouped by fine bin (unordered within a bin)
   uint64_t red[2 * kWarps];
   uint32_t flag;
   uint64_t bound[2];
@@ -431,8 +432,10 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
     kmin = S.red[w] < kmin ? S.red[w] : kmin;
     kmax = S.red[kWarps + w] > kmax ? S.red[kWarps + w] : kmax;
   }
-  int sh = 0;
-  while (((kmax - kmin) >> sh) >= (uint64_t)kFineBins) ++sh;
+  // smallest shift with (kmax - kmin) >> sh < kFineBins
+  const uint64_t range = kmax - kmin;
+  const int sh = range ? max(0, 64 - __clzll((long long)range) - 12) : 0;
+  static_assert(kFineBins == 4096, "shift formula assumes 12-bit fine bins");
   for (uint32_t i = tid; i < c; i += kThreads) atomicAdd(&S.bin[(uint32_t)((S.keys[i] - kmin) >> sh)], 1u);
   __syncthreads();
   {  // exclusive scan over the bins (16 per thread) + large-bin detection
@@ -455,27 +458,25 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
   }
   __syncthreads();
   if (S.flag == 0) {
+    // group the staged indices by fine bin (any order inside a bin) ...
     for (uint32_t i = tid; i < c; i += kThreads) {
       const uint32_t pos = atomicAdd(&S.bin[(uint32_t)((S.keys[i] - kmin) >> sh)], 1u);
-      S.perm[pos] = (uint16_t)i;
+      S.grp[pos] = (uint16_t)i;
     }
     __syncthreads();
-    // bin b now spans [end(b-1), end(b)); stable insertion sort by (key, index)
-    for (uint32_t b = tid; b < kFineBins; b += kThreads) {
+    // ... then every record's rank = its bin's start + #{bin members before it
+    // in (key, staged index) order}; bin b spans [end(b-1), end(b)), <= kMaxBinRun
+    for (uint32_t i = tid; i < c; i += kThreads) {
+      const uint64_t kv = S.keys[i];
+      const uint32_t b = (uint32_t)((kv - kmin) >> sh);
       const uint32_t lo = b ? S.bin[b - 1] : 0, hi = S.bin[b];
-      for (uint32_t x = lo + 1; x < hi; ++x) {
-        const uint16_t v = S.perm[x];
-        const uint64_t kv = S.keys[v];
-        uint32_t y = x;
-        while (y > lo) {
-          const uint16_t w = S.perm[y - 1];
-          const uint64_t kw = S.keys[w];
-          if (kw < kv || (kw == kv && w < v)) break;
-          S.perm[y] = w;
-          --y;
-        }
-        S.perm[y] = v;
+      uint32_t r = lo;
+      for (uint32_t x = lo; x < hi; ++x) {
+        const uint32_t w = S.grp[x];
+        const uint64_t kw = S.keys[w];
+        r += (kw < kv || (kw == kv && w < i)) ? 1u : 0u;
       }
+      S.perm[r] = (uint16_t)i;
     }
   } else {
     // bitonic sort of (key, index) over the next power of two
