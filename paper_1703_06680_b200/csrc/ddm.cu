@@ -249,7 +249,12 @@ struct SideStreams {
 std::mutex g_side_mu;
 SideStreams g_side[64];
 
-ddm_status side_streams(cudaStream_t out[2]) {
+ddm_status side_streams(cudaStream_t out[2], cudaStream_t st) {
+  static const bool serial = getenv("DDM_SERIAL") != nullptr;  // debug/profiling: one stream
+  if (serial) {
+    out[0] = out[1] = st;
+    return DDM_OK;
+  }
   int dev = 0;
   DDM_CUDA_RET(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) return DDM_ERR_CUDA;
@@ -264,6 +269,7 @@ ddm_status side_streams(cudaStream_t out[2]) {
 
 // `to` waits for everything enqueued on `from` so far.
 ddm_status stream_join(cudaStream_t to, cudaStream_t from) {
+  if (to == from) return DDM_OK;
   cudaEvent_t e;
   DDM_CUDA_RET(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   const cudaError_t r1 = cudaEventRecord(e, from);
@@ -635,7 +641,7 @@ ddm_status build_index_async(const ddm_regions* R, const Index& I, MsdScratch& s
   if (use_msd) {
     DDM_TRY(validate_side(R->d, n, R->sub_lo, R->sub_hi, nullptr, nullptr, &misc->err, st, mm + 0, mm + 2));
     cudaStream_t side[2];
-    DDM_TRY(side_streams(side));
+    DDM_TRY(side_streams(side, st));
     DDM_TRY(stream_join(side[0], st));
     // a2 + a3: Slo with the upper key and the id as payload (st) || Shi keys (side stream)
     DDM_TRY(msd_sort_t<false>(R->sub_hi[0], nullptr, n, mm + 2, I.shi_key, nullptr, nullptr, shi, &misc->overflow,
@@ -927,7 +933,7 @@ static ddm_status match_full(const ddm_regions* R, ddm_pair* pairs, uint64_t cap
       // the update chain (side stream 1) runs concurrently with the index
       // build (Slo on st, Shi on side stream 0); st joins both before a4
       cudaStream_t side[2];
-      DDM_TRY(side_streams(side));
+      DDM_TRY(side_streams(side, st));
       DDM_TRY(stream_join(side[1], st));
       DDM_TRY(upd_sort_async(R, W, R->n_sub, true, side[1]));
       DDM_TRY(build_index_async(R, I, W.slo, W.shi, W.sort, W.mm, W.misc, true, st));
