@@ -152,7 +152,10 @@ ddm_status ddm_radix_sort_u64(const uint64_t *keys_in, const uint32_t *vals_in,
 ddm_status ddm_encode_keys(const double *x, uint64_t *keys, uint64_t n, cudaStream_t stream);
 
 /* Per-kernel-class timing with CUDA events recorded on the launching stream
- * around every library launch while enabled (enable(1) also resets).
+ * around every library launch while enabled (enable(1) also resets).  While
+ * enabled, the sort chains that normally run concurrently on internal side
+ * streams all run on the caller's stream, so the recorded intervals of
+ * different kernels never overlap.
  * ddm_profile_read synchronises the recorded events and fills up to cap
  * entries; returns the number of kernel classes (or -1 on a CUDA error).
  * bytes = the algorithmic DRAM bytes of those launches. */

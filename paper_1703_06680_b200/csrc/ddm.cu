@@ -250,8 +250,10 @@ std::mutex g_side_mu;
 SideStreams g_side[64];
 
 ddm_status side_streams(cudaStream_t out[2], cudaStream_t st) {
-  static const bool serial = getenv("DDM_SERIAL") != nullptr;  // debug/profiling: one stream
-  if (serial) {
+  // one stream while profiling (per-kernel event intervals must not overlap)
+  // or when DDM_SERIAL is set (debugging)
+  static const bool serial = getenv("DDM_SERIAL") != nullptr;
+  if (serial || g_prof.on) {
     out[0] = out[1] = st;
     return DDM_OK;
   }

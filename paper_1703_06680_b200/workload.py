@@ -131,12 +131,16 @@ def make(name: str, scale: float = 1.0) -> Workload:
 
 
 def window_sample(w: Workload, frac: float) -> Workload:
-    """The regions whose dim-0 lower bound lies in [0, frac*L): same density,
-    same alpha, ~frac of the regions (the bounded CPU-baseline sample)."""
-    cut = frac * w.L
-    s = w.sub_lo[0] < cut
-    u = w.upd_lo[0] < cut
-    return Workload(f"{w.name}[lo<{frac:g}L]", w.d, w.L, w.l, w.seed,
+    """The regions whose dim-0 lower bound lies in a window of width frac*L
+    centred on the median subscription lower bound: same local density and
+    alpha, a bounded slice of the workload (the CPU-baseline sample).  For the
+    uniform configs that is ~frac of the regions; for the clustered c5 the
+    window sits inside the populated part of the domain."""
+    x0 = float(np.median(w.sub_lo[0])) - 0.5 * frac * w.L if w.n else 0.0
+    x1 = x0 + frac * w.L
+    s = (w.sub_lo[0] >= x0) & (w.sub_lo[0] < x1)
+    u = (w.upd_lo[0] >= x0) & (w.upd_lo[0] < x1)
+    return Workload(f"{w.name}[{x0:.6g}<=lo<{x1:.6g}]", w.d, w.L, w.l, w.seed,
                     np.ascontiguousarray(w.sub_lo[:, s]), np.ascontiguousarray(w.sub_hi[:, s]),
                     np.ascontiguousarray(w.upd_lo[:, u]), np.ascontiguousarray(w.upd_hi[:, u]))
 

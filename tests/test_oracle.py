@@ -302,4 +302,7 @@ def test_clustered_generator_in_domain():
 def test_window_sample():
     w = wl.make("c2", scale=0.01)
     s = wl.window_sample(w, 0.25)
-    assert s.n < w.n and np.all(s.sub_lo[0] < 0.25 * w.L)
+    width = np.ptp(np.concatenate([s.sub_lo[0], s.upd_lo[0]]))
+    assert 0 < s.n < w.n and 0 < s.m < w.m and width < 0.25 * w.L
+    c = wl.clustered(20_000, 20_000, 1e9, 0.01 * 2500, seed=4)
+    assert wl.window_sample(c, 0.01).n > 0  # the window sits where the clusters are
