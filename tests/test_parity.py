@@ -347,6 +347,45 @@ def test_dd_deterministic_output():
     assert torch.equal(a, b)
 
 
+def test_c5_full_windows(orc):
+    """c5 at full size (N = 1e9, clustered, the bench configuration): the list
+    invariants on the device, count == list length, sampled rows against
+    brute force over all 5e8 subscriptions, and three exact slices: every
+    update whose lower bound lies in a window, matched by the oracle's
+    Parallel-SBM against every subscription that can reach the window (lower
+    bound within the longest subscription length of it), must have exactly
+    the GPU's rows."""
+    w = wl.make("c5")
+    g = gpu_args(w)
+    p = ddm.match_pairs(*g)
+    K = p.shape[0]
+    assert ddm.match_count(*g) == K
+    s, u = p[:, 0].long(), p[:, 1].long()
+    assert bool(((g[0][0][s] <= g[3][0][u]) & (g[2][0][u] <= g[1][0][s])).all())
+    wds = torch.sort((u << 32) | s).values
+    assert bool((wds[1:] > wds[:-1]).all())
+    del s, wds
+    _check_sampled_rows(orc, w, p, n_rows=120)
+    gpu_u = u.cpu().numpy()
+    words = raw_words(p)
+    del p, g, u
+    torch.cuda.empty_cache()
+    # a sub overlapping an update of [x0, x1) has x0 - len(S) <= S.lo <= U.hi < x1 + len(U)
+    margin = max(float(np.max(w.sub_hi[0] - w.sub_lo[0])), float(np.max(w.upd_hi[0] - w.upd_lo[0]))) + 1.0
+    for q in (0.25, 0.5, 0.75):
+        x0 = float(np.quantile(w.upd_lo[0][::97], q))
+        x1 = x0 + 2e6
+        ui = np.nonzero((w.upd_lo[0] >= x0) & (w.upd_lo[0] < x1))[0]
+        si = np.nonzero((w.sub_lo[0] >= x0 - margin) & (w.sub_lo[0] < x1 + margin))[0]
+        loc = orc.par_sbm(w.sub_lo[:, si], w.sub_hi[:, si], w.upd_lo[:, ui], w.upd_hi[:, ui], canonicalize=False)
+        ref = np.sort((ui[(loc >> np.uint64(32)).astype(np.int64)].astype(np.uint64) << np.uint64(32))
+                      | si[(loc & np.uint64(0xffffffff)).astype(np.int64)].astype(np.uint64))
+        inwin = np.zeros(w.m, dtype=bool)
+        inwin[ui] = True
+        got = np.sort(words[inwin[gpu_u]])
+        assert ui.size > 1000 and np.array_equal(got, ref), f"window at quantile {q}"
+
+
 def test_c5_scaled(orc):
     w = wl.clustered(400_000, 400_000, 1e9, 0.01 * 2500, seed=4)
     check_against(orc, w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi, flags=EMIT_FLAGS)
