@@ -517,14 +517,19 @@ ddm_status radix_sort(const void* src, bool src_f64, const uint32_t* vals_in, ui
 // mm = the keys' [min, max] (from validation).  Sets *overflow on a bucket
 // too large for shared memory (caller falls back to radix_sort + gather).
 template <bool PAY>
-ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, const uint64_t* mm, uint64_t* out_key,
-                      uint64_t* out_v64, uint32_t* out_v32, MsdScratch& s, uint32_t* overflow, cudaStream_t st) {
+ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint64_t* mm, uint64_t* out_key,
+                      uint64_t* out_v64, uint32_t* out_v32, MsdScratch& s, uint32_t* overflow, uint32_t* err,
+                      cudaStream_t st) {
   const int bits = msd_bits(n);
   const uint32_t nb = 1u << bits;
   const int passes = (bits + 7) / 8;
   // bucket map equalised to the data (coarse population -> bucket allocation)
   DDM_CUDA(cudaMemsetAsync(s.ccount, 0, sizeof(uint32_t) * (msd::kCoarse + 1), st));
   const msd::MapRef M{mm, s.cbase};
+  const unsigned sgrid = grid_for((n + msd::kSampleStride - 1) / msd::kSampleStride, 512, 4);
+  DDM_LAUNCH("msd_sample", 8.0 * n / msd::kSampleStride, st,
+             msd::sample_minmax_kernel<true><<<sgrid, 512, 0, st>>>(src, n, mm));
+  DDM_TRY(check_launch());
   DDM_LAUNCH("msd_coarse", 8.0 * n / msd::kSampleStride, st,
              msd::coarse_hist_kernel<true><<<grid_for((n + msd::kSampleStride - 1) / msd::kSampleStride, 512, 4), 512, 0, st>>>(
                  src, n, M, s.ccount));
@@ -552,23 +557,23 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, cons
         DDM_LAUNCH("msd_pass_pay", bytes, st, msd::msd_pass_kernel<msd::kItems, true, true, true>
                    <<<persistent_grid((const void*)msd::msd_pass_kernel<msd::kItems, true, true, true>, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, true, true>), tiles), msd::kThreads, sizeof(msd::PassSmem<msd::kItems, true, true>), st>>>(
                        src, v64_src, nullptr, bk[o], bv[o], bi[o], n, M, bits, 8 * p, s.starts + p * 256, s.status,
-                       s.counters + p));
+                       s.counters + p, err));
       else
         DDM_LAUNCH("msd_pass", bytes, st, msd::msd_pass_kernel<msd::kItems, false, false, true>
                    <<<persistent_grid((const void*)msd::msd_pass_kernel<msd::kItems, false, false, true>, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, false, false>), tiles), msd::kThreads, sizeof(msd::PassSmem<msd::kItems, false, false>), st>>>(
                        src, nullptr, nullptr, bk[o], nullptr, nullptr, n, M, bits, 8 * p, s.starts + p * 256, s.status,
-                       s.counters + p));
+                       s.counters + p, err));
     } else {
       if (PAY)
         DDM_LAUNCH("msd_pass_pay", bytes, st, msd::msd_pass_kernel<msd::kItems, true, true, false>
                    <<<persistent_grid((const void*)msd::msd_pass_kernel<msd::kItems, true, true, false>, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, true, true>), tiles), msd::kThreads, sizeof(msd::PassSmem<msd::kItems, true, true>), st>>>(
                        bk[q], bv[q], bi[q], bk[o], bv[o], bi[o], n, M, bits, 8 * p, s.starts + p * 256, s.status,
-                       s.counters + p));
+                       s.counters + p, err));
       else
         DDM_LAUNCH("msd_pass", bytes, st, msd::msd_pass_kernel<msd::kItems, false, false, false>
                    <<<persistent_grid((const void*)msd::msd_pass_kernel<msd::kItems, false, false, false>, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, false, false>), tiles), msd::kThreads, sizeof(msd::PassSmem<msd::kItems, false, false>), st>>>(
                        bk[q], nullptr, nullptr, bk[o], nullptr, nullptr, n, M, bits, 8 * p, s.starts + p * 256, s.status,
-                       s.counters + p));
+                       s.counters + p, err));
     }
     DDM_TRY(check_launch());
   }
@@ -618,9 +623,9 @@ ddm_status err_status(uint32_t e) {
 // validate all dims of one side; histogram dim 0 into hist_lo / hist_hi
 ddm_status validate_side(uint32_t d, uint64_t cnt, const double* const* lo, const double* const* hi,
                          uint32_t* hist_lo, uint32_t* hist_hi, uint32_t* err, cudaStream_t st,
-                         uint64_t* mm_lo = nullptr, uint64_t* mm_hi = nullptr) {
+                         uint64_t* mm_lo = nullptr, uint64_t* mm_hi = nullptr, uint32_t k_begin = 0) {
   if (cnt == 0) return DDM_OK;
-  for (uint32_t k = 0; k < d; ++k) {
+  for (uint32_t k = k_begin; k < d; ++k) {
     DDM_LAUNCH("validate_hist", 16.0 * cnt, st, match::validate_hist_kernel<<<grid_for(cnt, 512, 4), 512, 0, st>>>(
         lo[k], hi[k], cnt, k == 0 ? hist_lo : nullptr, k == 0 ? hist_hi : nullptr, err, k == 0 ? mm_lo : nullptr,
         k == 0 ? mm_hi : nullptr));
@@ -641,15 +646,17 @@ ddm_status build_index_async(const ddm_regions* R, const Index& I, MsdScratch& s
   const uint64_t n = R->n_sub;
   if (n == 0) return DDM_OK;
   if (use_msd) {
-    DDM_TRY(validate_side(R->d, n, R->sub_lo, R->sub_hi, nullptr, nullptr, &misc->err, st, mm + 0, mm + 2));
+    // a1 for dims 1..d-1 here; dim 0 is validated inside the first Slo pass,
+    // which reads lo and hi anyway (the sort's key range comes from a sample)
+    DDM_TRY(validate_side(R->d, n, R->sub_lo, R->sub_hi, nullptr, nullptr, &misc->err, st, nullptr, nullptr, 1));
     cudaStream_t side[2];
     DDM_TRY(side_streams(side, st));
     DDM_TRY(stream_join(side[0], st));
     // a2 + a3: Slo with the upper key and the id as payload (st) || Shi keys (side stream)
     DDM_TRY(msd_sort_t<false>(R->sub_hi[0], nullptr, n, mm + 2, I.shi_key, nullptr, nullptr, shi, &misc->overflow,
-                              side[0]));
+                              nullptr, side[0]));
     DDM_TRY(msd_sort_t<true>(R->sub_lo[0], R->sub_hi[0], n, mm + 0, I.slo_key, I.slo_hi, I.slo_id, slo,
-                             &misc->overflow, st));
+                             &misc->overflow, &misc->err, st));
     for (int L = 1; L <= I.levels; ++L) {
       DDM_LAUNCH("block_max", 8.0 * I.lvl_n[L - 1], st, match::block_max_kernel<<<grid_for(I.lvl_n[L - 1], 256, 8), 256, 0, st>>>(
           I.lvl[L - 1], I.lvl_n[L - 1], I.lvl[L]));
@@ -723,9 +730,9 @@ ddm_status upd_sort_async(const ddm_regions* R, MatchWs& W, uint64_t n_sub, bool
   init_attrs_once();
   if (n_sub == 0) return validate_side(d, m, R->upd_lo, R->upd_hi, nullptr, nullptr, &W.misc->err, st);
   if (use_msd) {
-    DDM_TRY(validate_side(d, m, R->upd_lo, R->upd_hi, nullptr, nullptr, &W.misc->err, st, W.mm + 4));
+    DDM_TRY(validate_side(d, m, R->upd_lo, R->upd_hi, nullptr, nullptr, &W.misc->err, st, nullptr, nullptr, 1));
     return msd_sort_t<true>(R->upd_lo[0], R->upd_hi[0], m, W.mm + 4, W.ulo_key, W.uhi, W.ulo_id, W.ulo,
-                            &W.misc->overflow, st);
+                            &W.misc->overflow, &W.misc->err, st);
   }
   SortScratch s = lsb_with(W.sort, W.ulo);
   DDM_CUDA(cudaMemsetAsync(s.hist[2], 0, sizeof(uint32_t) * 8 * 256, st));

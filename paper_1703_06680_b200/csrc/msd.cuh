@@ -108,6 +108,36 @@ struct Bucketer {
   }
 };
 
+// [min, max] key of the same sample (chunks of kSampleChunk, one in every
+// kSampleStride) into mm[0], mm[1] (initialised to [~0, 0]).  Keys outside
+// the sampled range are clamped into the first / last bucket by the
+// Bucketer, so the sample only shapes bucket sizes, never the result.
+template <bool SRC_F64>
+__global__ void __launch_bounds__(512) sample_minmax_kernel(const void* __restrict__ src, uint64_t n,
+                                                            uint64_t* __restrict__ mm) {
+  const uint64_t chunks = (n + kSampleChunk - 1) / kSampleChunk;
+  uint64_t lo = ~0ull, hi = 0;
+  for (uint64_t ch = (uint64_t)blockIdx.x * kSampleStride; ch < chunks; ch += (uint64_t)gridDim.x * kSampleStride) {
+    const uint64_t e = umin64(n, (ch + 1) * kSampleChunk);
+    for (uint64_t i = ch * kSampleChunk + threadIdx.x; i < e; i += blockDim.x) {
+      const uint64_t k = SRC_F64 ? f64_key(__ldcs(reinterpret_cast<const double*>(src) + i))
+                                 : __ldcs(reinterpret_cast<const uint64_t*>(src) + i);
+      lo = k < lo ? k : lo;
+      hi = k > hi ? k : hi;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const uint64_t a = __shfl_xor_sync(kFull, lo, o), b = __shfl_xor_sync(kFull, hi, o);
+    lo = a < lo ? a : lo;
+    hi = b > hi ? b : hi;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (lo != ~0ull) atomicMin((unsigned long long*)&mm[0], (unsigned long long)lo);
+    if (hi != 0) atomicMax((unsigned long long*)&mm[1], (unsigned long long)hi);
+  }
+}
+
 // Coarse-bin population of a sample (chunks of kSampleChunk, one in every
 // kSampleStride): counts[kCoarse] (zeroed), counts[kCoarse] = sample size.
 template <bool SRC_F64>
@@ -224,25 +254,41 @@ struct TileRegs {
   uint64_t key[ITEMS];
   uint64_t hv[V64 ? ITEMS : 1];
   uint32_t iv[V32 ? ITEMS : 1];
+  uint32_t err = 0;  // a1 on the fly (first pass over float64 lo/hi): 1 non-finite, 2 lo > hi
+  // Issue the loads only: registers receive raw bits, converted by finish()
+  // when the tile is processed, so a prefetch never waits for its data.
   __device__ __forceinline__ void load(const void* __restrict__ k_in, const void* __restrict__ v64_in,
                                        const uint32_t* __restrict__ v32_in, uint64_t wb0, uint64_t n, int lane) {
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const uint64_t idx = wb0 + i * 32 + lane;
       if (idx < n) {
-        if (SRC_F64) {
-          key[i] = f64_key(__ldcs(reinterpret_cast<const double*>(k_in) + idx));
-          if (V64) hv[i] = f64_key(__ldcs(reinterpret_cast<const double*>(v64_in) + idx));
-          if (V32) iv[i] = (uint32_t)idx;
-        } else {
-          key[i] = __ldcs(reinterpret_cast<const uint64_t*>(k_in) + idx);
-          if (V64) hv[i] = __ldcs(reinterpret_cast<const uint64_t*>(v64_in) + idx);
-          if (V32) iv[i] = __ldcs(v32_in + idx);
-        }
+        key[i] = __ldcs(reinterpret_cast<const uint64_t*>(k_in) + idx);
+        if (V64) hv[i] = __ldcs(reinterpret_cast<const uint64_t*>(v64_in) + idx);
+        if (V32) iv[i] = SRC_F64 ? (uint32_t)idx : __ldcs(v32_in + idx);
       } else {
-        key[i] = 0;
-        if (V64) hv[i] = 0;
+        key[i] = SRC_F64 ? 0x8000000000000000ull : 0;  // (encodes to key 0 below)
+        if (V64) hv[i] = SRC_F64 ? 0x8000000000000000ull : 0;
         if (V32) iv[i] = 0;
+      }
+    }
+  }
+  // float64 bits -> order-preserving keys (first pass), validating lo/hi
+  __device__ __forceinline__ void finish(uint64_t wb0, uint64_t n, int lane) {
+    if (!SRC_F64) return;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const bool valid = wb0 + i * 32 + lane < n;
+      const uint64_t bx = key[i];
+      if (valid && !f64_finite_bits(bx)) err |= 1u;
+      key[i] = valid ? f64_key(__longlong_as_double((long long)bx)) : 0;
+      if (V64) {
+        const uint64_t by = hv[i];
+        if (valid) {
+          if (!f64_finite_bits(by)) err |= 1u;
+          else if (!(__longlong_as_double((long long)bx) <= __longlong_as_double((long long)by))) err |= 2u;
+        }
+        hv[i] = valid ? f64_key(__longlong_as_double((long long)by)) : 0;
       }
     }
   }
@@ -254,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                     uint64_t* __restrict__ k_out, uint64_t* __restrict__ v64_out, uint32_t* __restrict__ v32_out,
                     uint64_t n, MapRef M, int bits, int shift,
                     const uint32_t* __restrict__ bin_start, uint32_t* __restrict__ status,
-                    uint32_t* __restrict__ tile_counter) {
+                    uint32_t* __restrict__ tile_counter, uint32_t* __restrict__ err) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   using Smem = PassSmem<ITEMS, V64, V32>;
   constexpr int kT = Smem::kT;
@@ -274,6 +320,7 @@ __global__ void __launch_bounds__(kThreads, 3)
     const uint64_t tile_base = (uint64_t)tile * kT;
     const uint64_t wb0 = tile_base + (uint64_t)warp * (32 * ITEMS);
     const uint32_t tile_valid = (uint32_t)umin64(kT, n - tile_base);
+    R.finish(wb0, n, lane);
     {
       uint4* z = reinterpret_cast<uint4*>(&S.wbase[0][0]);
       constexpr int kZ = 2 * kWarps * kRadix / 4;
@@ -381,6 +428,10 @@ __global__ void __launch_bounds__(kThreads, 3)
     }
     if (next >= num_tiles) break;
     tile = next;  // (the next iteration's first barrier orders these reads before any smem rewrite)
+  }
+  if (SRC_F64 && err) {
+    const uint32_t e = __reduce_or_sync(kFull, R.err);
+    if (lane == 0 && e) atomicOr(err, e);
   }
 }
 
