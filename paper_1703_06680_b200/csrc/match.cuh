@@ -287,25 +287,40 @@ struct CountSmem {
   uint64_t wh[kCountWin];
 };
 
+// First window position at or after k whose entry is "after" x (> x for
+// UPPER, >= x otherwise), given every entry before k is not: gallop forward
+// from the cursor (1, 2, 4, ... steps), then binary search the last gap; len
+// when the window holds no such entry.  Cursors of consecutive sorted
+// queries move by a few positions, so this is O(1) probes per query.
+template <bool UPPER>
+__device__ __forceinline__ uint32_t wseek(const uint64_t* W, uint32_t k, uint32_t len, uint64_t x) {
+  uint32_t lo = k, hi = len, step = 1;
+  while (lo < len) {
+    const uint32_t probe = min(lo + step - 1, len - 1);
+    const uint64_t v = W[probe];
+    if (UPPER ? v > x : v >= x) { hi = probe; break; }
+    lo = probe + 1;
+    step <<= 1;
+  }
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    const uint64_t v = W[mid];
+    if (UPPER ? v > x : v >= x) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
 // Advance a merge cursor: pos is an absolute index into the sorted array g
-// with every entry before pos "before" x (<= x for UPPER, < x otherwise);
-// returns the first index whose entry is "after" x.  The array's slice
-// [base, base+len) is staged in W (shared memory): short linear steps, then
-// a binary search inside the window, then (rarely) a gallop in global memory.
+// with every entry before pos "before" x; returns the first index whose entry
+// is "after" x.  The slice [base, base+len) is staged in W (shared memory);
+// past it (rare) a gallop in global memory.
 template <bool UPPER>
 __device__ __forceinline__ uint64_t advance(const uint64_t* W, uint64_t base, uint32_t len, const uint64_t* g,
                                             uint64_t n, uint64_t pos, uint64_t x) {
-  uint32_t k = pos >= base ? (uint32_t)umin64(pos - base, len) : 0;
-#pragma unroll 1
-  for (int s = 0; s < 6 && k < len; ++s) {
-    const uint64_t v = W[k];
-    if (UPPER ? v > x : v >= x) return base + k;
-    ++k;
-  }
-  if (k < len) {
-    const uint64_t v = W[len - 1];
-    if (UPPER ? v > x : v >= x) return base + (UPPER ? ub(W, k, len, x) : lb(W, k, len, x));
-  }
+  const uint32_t k = pos >= base ? (uint32_t)umin64(pos - base, len) : 0;
+  const uint32_t r = wseek<UPPER>(W, k, len, x);
+  if (r < len) return base + r;
   if (base + len >= n) return n;
   return UPPER ? ub_gallop(g, n, base + len, x) : gallop_lb(g, n, base + len, x);
 }
@@ -335,11 +350,22 @@ __global__ void __launch_bounds__(kCountThreads, 2) count_kernel(
   // issue this thread's loads first (the random upd_hi gather overlaps the
   // window staging below)
   uint64_t a[kCountItems], b[kCountItems];
-  if (uhi) {  // upper keys already in sorted order (MSD sort payload)
+  if (uhi && ni == kCountItems) {  // upper keys already in sorted order (MSD sort payload)
+    // 16-byte loads through L1: a thread's 8 consecutive keys share lines with
+    // its neighbours', so later loads hit L1 instead of refetching from L2
+    const ulonglong2* pa = reinterpret_cast<const ulonglong2*>(ulo_key + j);
+    const ulonglong2* pb = reinterpret_cast<const ulonglong2*>(uhi + j);
+#pragma unroll
+    for (int i = 0; i < kCountItems / 2; ++i) {
+      const ulonglong2 va = __ldg(pa + i), vb = __ldg(pb + i);
+      a[2 * i] = va.x; a[2 * i + 1] = va.y;
+      b[2 * i] = vb.x; b[2 * i + 1] = vb.y;
+    }
+  } else if (uhi) {
 #pragma unroll
     for (int i = 0; i < kCountItems; ++i) {
-      a[i] = i < ni ? __ldcs(ulo_key + j + i) : 0;
-      b[i] = i < ni ? __ldcs(uhi + j + i) : 0;
+      a[i] = i < ni ? __ldg(ulo_key + j + i) : 0;
+      b[i] = i < ni ? __ldg(uhi + j + i) : 0;
     }
   } else {  // gather them (LSB sort path)
     uint32_t id[kCountItems];
