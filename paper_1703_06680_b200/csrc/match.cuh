@@ -260,7 +260,7 @@ __device__ __forceinline__ uint64_t lookback_warp_u64(uint64_t* status, uint32_t
 constexpr int kCountThreads = 256;
 constexpr int kCountItems = 8;
 constexpr int kCountTile = kCountThreads * kCountItems;
-constexpr int kCountWin = 4096;  // smem window (keys) per sorted array
+constexpr int kCountWin = 3072;  // smem window (keys) per sorted array
 constexpr int kCountExt = 1024;  // Slo window extension past r_lo(a_last) for the r_b searches
 constexpr int kRowTile = 256;    // rows per emit CTA == granularity of the row-offset scan
 static_assert(kCountTile % kRowTile == 0, "count tile holds whole row tiles");
@@ -332,7 +332,7 @@ __device__ __forceinline__ uint64_t advance(const uint64_t* W, uint64_t base, ui
 // one in the tile's staged Slo/Shi windows, then the cursors only move
 // forward (a is sorted: a merge path).  Also writes the count sum of every
 // 256-row tile (for the row-offset scan, a5).
-__global__ void __launch_bounds__(kCountThreads, 2) count_kernel(
+__global__ void __launch_bounds__(kCountThreads, 4) count_kernel(
     const uint64_t* __restrict__ ulo_key, const uint32_t* __restrict__ ulo_id, const double* __restrict__ upd_hi,
     const uint64_t* __restrict__ uhi, uint64_t m, const uint64_t* __restrict__ slo_key, const uint64_t* __restrict__ shi_key, uint64_t n,
     const uint64_t* __restrict__ part, uint32_t* __restrict__ r_lo_out, uint32_t* __restrict__ r_b_out,
