@@ -854,7 +854,10 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
   D.pairs = A.pairs;
   if (d > 1 && !per_row)
     DDM_LAUNCH("dd_emit", 24.0 * m + 8.0 * h.K, st, launch_dd_any(true, D, st));
-  else if (d == 1 && !per_row)
+  // sparse outputs (a few pairs per row on average, e.g. alpha ~ 1) gain
+  // nothing from staging chunk-start sets: the light per-row kernel (higher
+  // occupancy) is used unless the chunk path is forced
+  else if (d == 1 && !per_row && (h.K > 4ull * m || (q.flags & DDM_EMIT_FORCE_CHUNK)))
     DDM_LAUNCH("emit", 44.0 * m + 8.0 * h.K, st,
                match::emit_chunk_kernel<<<egrid, match::kRowTile, sizeof(match::ChunkSmem), st>>>(A));
   else if (d == 1)

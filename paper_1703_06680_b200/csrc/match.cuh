@@ -584,6 +584,27 @@ __device__ __forceinline__ void row_thread(const EmitArgs& A, uint64_t j, uint64
   uint32_t nst = 0;                                      // filtered stab members (count pass)
   int64_t i = (int64_t)rl - 1;
   uint32_t rem = stab0;
+  if (MODE == kEmitD1) {
+    // 4 positions of one aligned 32-block per step, loaded together (the walk
+    // is otherwise a chain of dependent global loads)
+    while (rem) {
+      if ((i & 31) == 31) {
+        const int L = skip_levels(A.T, i, a);
+        if (L) { i -= (int64_t)1 << (5 * L); continue; }
+      }
+      const int c = (int)min((int64_t)4, (i & 31) + 1);
+      uint64_t h[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) h[u] = u < c ? A.T.lvl[0][i - u] : 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (u < c && rem && h[u] >= a) {
+          --rem;
+          A.pairs[o + rem] = make_uint2(A.slo_id[i - u], uid);
+        }
+      i -= c;
+    }
+  }
   while (rem) {
     if ((i & 31) == 31) {
       const int L = skip_levels(A.T, i, a);

@@ -13,7 +13,7 @@ g = [torch.from_numpy(a).cuda() for a in (w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi
 M = ddm.Matcher(w.d, w.n, w.m)
 K = M.count(*g)
 out = torch.empty((K, 2), dtype=torch.int32, device="cuda")
-for flags in (0, ddm.DDM_EMIT_FORCE_THREAD, ddm.DDM_EMIT_FORCE_WARP):
+for flags in (0, ddm.DDM_EMIT_FORCE_CHUNK, ddm.DDM_EMIT_FORCE_THREAD, ddm.DDM_EMIT_FORCE_WARP):
     for i in range(3):
         M.pairs_into(out, *g, flags=flags)
     torch.cuda.synchronize()
@@ -23,6 +23,11 @@ for flags in (0, ddm.DDM_EMIT_FORCE_THREAD, ddm.DDM_EMIT_FORCE_WARP):
         a.record(); M.pairs_into(out, *g, flags=flags); b.record(); torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
     t = np.median(ts)
+    ddm.profile_enable(True)
+    M.pairs_into(out, *g, flags=flags)
+    pr = ddm.profile_read()
+    ddm.profile_enable(False)
+    print("   emit ms:", round(pr.get("emit", {}).get("total_ms", 0.0), 3))
     print(f"{cfg} flags={flags} K={K} pairs: {t:.3f} ms  regions/s={(w.n+w.m)/t*1e3:.3e} pairs/s={K/t*1e3:.3e}", flush=True)
 ts = []
 for i in range(5):
