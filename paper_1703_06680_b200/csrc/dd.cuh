@@ -35,9 +35,16 @@
 // d = 2 every dim-2 value is -inf/+inf and all cells share one dim-2 bin.
 // Cells are stored dim-2 major, so each dim-2 bin of the rectangle is one
 // contiguous run of slots.
-// Two passes run the identical enumeration: a count pass (row counts + 256-row
-// tile sums for the offset scan) and an emit pass writing each row at its
-// offset, so the output is deterministic.
+// Output (one pass).  Each hit is staged as (row, its index within the row,
+// sub id) in a per-tile global staging slot; when the tile is done it learns
+// its output offset by decoupled look-back over the tiles' pair totals (tile
+// ids are claimed in order, so predecessors are always running) and writes
+// every staged pair straight to offset + row prefix + index: deterministic
+// order (rows in sweep order, each row in enumeration order) without a second
+// enumeration.  A tile whose hits overflow its staging slot re-runs its
+// enumeration writing pairs directly at their now-known offsets.  The
+// count-only entry point runs the enumeration without staging (row counts ->
+// 256-row tile sums -> scan).
 #pragma once
 #include "common.cuh"
 #include "match.cuh"
@@ -102,11 +109,18 @@ struct Args {
   // count pass
   uint32_t* cnt_out;
   uint64_t* tile_sum;        // per 256-row tile
-  // emit pass
-  const uint32_t* cnt;
-  const uint64_t* tile_off;
+  // fused pass
+  const uint32_t* err_flag;   // non-zero: validation failed earlier on the stream -> no-op
+  uint2* stage;               // [tiles][kStageCap] staged hits: {sub id, (row << 16) | index in row}
+  uint64_t* status;           // [tiles] look-back words (zeroed)
+  uint32_t* tile_counter;     // dynamic tile ids (zeroed)
+  uint64_t* k_out;            // total K (written by the last tile)
   uint2* pairs;
+  uint64_t capacity;          // pairs at or past capacity are never written
 };
+
+constexpr uint32_t kStageCap = 8192;  // staged hits per tile (c4 averages ~4100 per 1024-row tile)
+enum { kEmCount = 0, kEmDirect = 1, kEmStage = 2 };
 
 template <int R>
 struct Smem {
@@ -123,6 +137,11 @@ struct Smem {
   uint64_t scan64[kWarps + 1];
   uint32_t scan32[kWarps + 1];
   uint32_t rbmax;
+  uint32_t nout;     // staged hits of this tile
+  uint32_t ovf;      // staging overflowed -> re-enumerate in direct mode
+  uint32_t tile;     // dynamic tile id
+  uint64_t excl;     // the tile's output offset (look-back)
+  uint32_t rowoff[kRows];  // exclusive prefix of the row counts inside the tile
 };
 
 // Monotone float bucketer over one chunk's lower bounds on one dimension.
@@ -162,10 +181,9 @@ __device__ __forceinline__ bool exact_hit(const Args& A, uint32_t p, uint64_t j,
 }
 
 // Exact re-test of this lane's queued float passes, in queue order.
-template <int R, bool EMIT>
-__device__ __forceinline__ void flush_list(const Args& A, Smem<R>& S, Rows<R>& rw, uint32_t nl) {
+template <int R, int EM>
+__device__ __forceinline__ void flush_list(const Args& A, Smem<R>& S, Rows<R>& rw, uint32_t nl, uint64_t j0) {
   const int tid = threadIdx.x;
-  const uint64_t j0 = (uint64_t)blockIdx.x * (kThreads * R);
   for (uint32_t e = 0; e < nl; ++e) {
     const uint32_t v = S.lst[e * kThreads + tid];
     const int q = (int)(v >> 12);
@@ -176,14 +194,24 @@ __device__ __forceinline__ void flush_list(const Args& A, Smem<R>& S, Rows<R>& r
 #pragma unroll
     for (int qq = 0; qq < R; ++qq)
       if (qq == q) {
-        if (EMIT) A.pairs[rw.off[qq] + rw.hits[qq]] = make_uint2(A.slo_id[p], A.upd_map ? A.upd_map[lid] : lid);
+        const uint32_t seq = rw.hits[qq];
+        if (EM == kEmDirect) {
+          const uint64_t pos = rw.off[qq] + seq;
+          if (pos < A.capacity) A.pairs[pos] = make_uint2(A.slo_id[p], A.upd_map ? A.upd_map[lid] : lid);
+        } else if (EM == kEmStage) {
+          const uint32_t slot = atomicAdd(&S.nout, 1u);
+          if (slot < kStageCap && seq < 65536u)
+            A.stage[(uint64_t)S.tile * kStageCap + slot] = make_uint2(A.slo_id[p], ((uint32_t)(q * kThreads + tid) << 16) | seq);
+          else
+            S.ovf = 1;
+        }
         ++rw.hits[qq];
       }
   }
 }
 
-template <int R, bool EMIT>
-__device__ void process_chunk(const Args& A, Smem<R>& S, Rows<R>& rw, uint32_t fill) {
+template <int R, int EM>
+__device__ void process_chunk(const Args& A, Smem<R>& S, Rows<R>& rw, uint32_t fill, uint64_t j0) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // 1. chunk min/max lower bound and max length (rounded up) on dims 1, 2
   float mn1 = __int_as_float(0x7f800000), mx1 = -mn1, ml1 = 0.0f;
@@ -304,7 +332,7 @@ __device__ void process_chunk(const Args& A, Smem<R>& S, Rows<R>& rw, uint32_t f
         const float4 f = S.c12[k];
         if (!(f.x <= u.y && u.x <= f.y && f.z <= u.w && u.z <= f.w)) continue;
         if (nl == kList) {
-          flush_list<R, EMIT>(A, S, rw, nl);
+          flush_list<R, EM>(A, S, rw, nl, j0);
           nl = 0;
         }
         S.lst[nl * kThreads + tid] = (uint16_t)((q << 12) | k);
@@ -312,62 +340,21 @@ __device__ void process_chunk(const Args& A, Smem<R>& S, Rows<R>& rw, uint32_t f
       }
     }
   }
-  flush_list<R, EMIT>(A, S, rw, nl);
+  flush_list<R, EM>(A, S, rw, nl, j0);
   __syncthreads();
 }
 
-template <int R, bool EMIT>
-__global__ void __launch_bounds__(kThreads, 4) dd_tile_kernel(Args A) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Smem<R>& S = *reinterpret_cast<Smem<R>*>(smem_raw);
-  constexpr int kRows = kThreads * R;
+// Every dim-0 candidate of the tile's rows (A_t by a CTA-wide backward walk
+// over Slo in windows of kWin positions with aligned runs of 32^L positions
+// whose block max < x_t skipped, then the Slo slice [rl0, rbmax)), pushed
+// through process_chunk.  hi_excl > 0 bounds the walk on inconsistent inputs.
+template <int R, int EM>
+__device__ void enumerate(const Args& A, Smem<R>& S, Rows<R>& rw, uint64_t j0, uint32_t rbmax) {
   const int tid = threadIdx.x;
-  const uint64_t j0 = (uint64_t)blockIdx.x * kRows;
-  if (A.abort_flag && *A.abort_flag) return;  // this attempt is discarded (ddm.cu retries with LSB)
-  const float kInf = __int_as_float(0x7f800000);
-  if (tid == 0) S.rbmax = 0;
-  __syncthreads();
-  Rows<R> rw;
-  uint32_t rbmax = 0;
-#pragma unroll
-  for (int q = 0; q < R; ++q) {
-    const uint64_t j = j0 + (uint64_t)q * kThreads + tid;
-    rw.valid[q] = j < A.m;
-    rw.hits[q] = 0;
-    rw.off[q] = 0;
-    if (rw.valid[q]) {
-      const uint32_t lid = A.ulo_id[j];
-      float4 u;
-      u.x = __double2float_rd(A.upd.lo[1][lid]);
-      u.y = __double2float_ru(A.upd.hi[1][lid]);
-      u.z = A.d > 2 ? __double2float_rd(A.upd.lo[2][lid]) : -kInf;
-      u.w = A.d > 2 ? __double2float_ru(A.upd.hi[2][lid]) : kInf;
-      S.rbox[q * kThreads + tid] = u;
-      const uint32_t rb = A.r_b[j];
-      rbmax = rb > rbmax ? rb : rbmax;
-    }
-  }
-  if (EMIT) {  // row offsets: tile_off of each 256-row tile + exclusive scan of the counts
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const uint64_t j = j0 + (uint64_t)q * kThreads + tid;
-      uint64_t total;
-      const uint64_t e = block_excl_scan<kThreads, uint64_t>(rw.valid[q] ? (uint64_t)A.cnt[j] : 0ull, S.scan64, &total);
-      if (rw.valid[q]) rw.off[q] = A.tile_off[(j0 >> 8) + q] + e;
-    }
-  }
-  rbmax = __reduce_max_sync(kFull, rbmax);
-  if ((tid & 31) == 0) atomicMax(&S.rbmax, rbmax);
-  __syncthreads();
-  rbmax = S.rbmax;
   const uint64_t rl0 = A.r_lo[j0];
   const uint64_t x = A.ulo_key[j0];
   const uint32_t nact = A.cnt0[j0] - (A.r_b[j0] - (uint32_t)rl0);  // |A_t| = stab(x_t) (I4)
-
   uint32_t fill = 0;
-  // a6: A_t by a CTA-wide backward walk over Slo (windows of kWin positions,
-  // aligned runs of 32^L positions with block max < x_t skipped).  hi_excl > 0
-  // bounds the walk even on inconsistent inputs.
   int64_t hi_excl = (int64_t)rl0;
   uint32_t rem = nact;
   while (rem && hi_excl > 0) {
@@ -388,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, 4) dd_tile_kernel(Args A) {
     uint32_t total;
     const uint32_t ex = block_excl_scan<kThreads, uint32_t>(c, S.scan32, &total);
     if (fill + total > (uint32_t)kCap) {  // uniform
-      process_chunk<R, EMIT>(A, S, rw, fill);
+      process_chunk<R, EM>(A, S, rw, fill, j0);
       fill = 0;
     }
     uint32_t o = fill + ex;
@@ -400,7 +387,6 @@ __global__ void __launch_bounds__(kThreads, 4) dd_tile_kernel(Args A) {
     hi_excl = base;
     __syncthreads();
   }
-  // the contiguous Slo slice [rl0, rbmax)
   for (uint64_t p = rl0; p < rbmax;) {
     const uint32_t take = (uint32_t)umin64(kCap - fill, rbmax - p);
     for (uint32_t t = tid; t < take; t += kThreads) S.fpos[fill + t] = (uint32_t)(p + t);
@@ -408,13 +394,60 @@ __global__ void __launch_bounds__(kThreads, 4) dd_tile_kernel(Args A) {
     p += take;
     __syncthreads();
     if (fill == (uint32_t)kCap) {
-      process_chunk<R, EMIT>(A, S, rw, fill);
+      process_chunk<R, EM>(A, S, rw, fill, j0);
       fill = 0;
     }
   }
-  if (fill) process_chunk<R, EMIT>(A, S, rw, fill);
+  if (fill) process_chunk<R, EM>(A, S, rw, fill, j0);
+}
 
-  if (!EMIT) {
+// FUSED = false: count pass (row counts + 256-row tile sums).  FUSED = true:
+// the single pass with staged hits and look-back-ordered output (see top).
+template <int R, bool FUSED>
+__global__ void __launch_bounds__(kThreads, 4) dd_tile_kernel(Args A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem<R>& S = *reinterpret_cast<Smem<R>*>(smem_raw);
+  constexpr int kRows = kThreads * R;
+  const int tid = threadIdx.x;
+  if (A.abort_flag && *A.abort_flag) return;  // this attempt is discarded (ddm.cu retries with LSB)
+  if (FUSED && A.err_flag && *A.err_flag) return;  // invalid input: nothing may be written
+  const float kInf = __int_as_float(0x7f800000);
+  if (tid == 0) {
+    S.rbmax = 0;
+    S.nout = 0;
+    S.ovf = 0;
+    S.tile = FUSED ? atomicAdd(A.tile_counter, 1u) : blockIdx.x;
+  }
+  __syncthreads();
+  const uint32_t tile = S.tile;
+  const uint64_t j0 = (uint64_t)tile * kRows;
+  Rows<R> rw;
+  uint32_t rbmax = 0;
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const uint64_t j = j0 + (uint64_t)q * kThreads + tid;
+    rw.valid[q] = j < A.m;
+    rw.hits[q] = 0;
+    rw.off[q] = 0;
+    if (rw.valid[q]) {
+      const uint32_t lid = A.ulo_id[j];
+      float4 u;
+      u.x = __double2float_rd(A.upd.lo[1][lid]);
+      u.y = __double2float_ru(A.upd.hi[1][lid]);
+      u.z = A.d > 2 ? __double2float_rd(A.upd.lo[2][lid]) : -kInf;
+      u.w = A.d > 2 ? __double2float_ru(A.upd.hi[2][lid]) : kInf;
+      S.rbox[q * kThreads + tid] = u;
+      const uint32_t rb = A.r_b[j];
+      rbmax = rb > rbmax ? rb : rbmax;
+    }
+  }
+  rbmax = __reduce_max_sync(kFull, rbmax);
+  if ((tid & 31) == 0) atomicMax(&S.rbmax, rbmax);
+  __syncthreads();
+  rbmax = S.rbmax;
+
+  if (!FUSED) {
+    enumerate<R, kEmCount>(A, S, rw, j0, rbmax);
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       const uint64_t j = j0 + (uint64_t)q * kThreads + tid;
@@ -423,6 +456,48 @@ __global__ void __launch_bounds__(kThreads, 4) dd_tile_kernel(Args A) {
       block_excl_scan<kThreads, uint64_t>(rw.valid[q] ? (uint64_t)rw.hits[q] : 0ull, S.scan64, &total);
       if (tid == 0 && j0 + (uint64_t)q * kThreads < A.m) A.tile_sum[(j0 >> 8) + q] = total;
     }
+    return;
+  }
+
+  enumerate<R, kEmStage>(A, S, rw, j0, rbmax);
+  // row prefix inside the tile (rows q*256 + tid, q-major) and the tile total
+  uint64_t run = 0;
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    uint64_t total;
+    const uint64_t e = block_excl_scan<kThreads, uint64_t>(rw.valid[q] ? (uint64_t)rw.hits[q] : 0ull, S.scan64, &total);
+    rw.off[q] = run + e;  // relative to the tile's offset for now
+    S.rowoff[q * kThreads + tid] = (uint32_t)(run + e);
+    run += total;
+  }
+  // decoupled look-back over the tiles' totals -> this tile's output offset
+  if (tid < 32) {
+    const uint64_t e = match::lookback_warp_u64(A.status, tile, run);
+    if (tid == 0) S.excl = e;
+  }
+  __syncthreads();
+  const uint64_t excl = S.excl;
+  const uint32_t num_tiles = (uint32_t)((A.m + kRows - 1) / kRows);
+  if (tile == num_tiles - 1 && tid == 0) *A.k_out = excl + run;
+  if (!S.ovf) {
+    const uint32_t nout = S.nout;
+    for (uint32_t e = tid; e < nout; e += kThreads) {
+      const uint2 h = A.stage[(uint64_t)tile * kStageCap + e];
+      const uint32_t row = h.y >> 16;
+      const uint64_t pos = excl + S.rowoff[row] + (h.y & 0xffffu);
+      if (pos < A.capacity) {
+        const uint32_t lid = A.ulo_id[j0 + row];
+        A.pairs[pos] = make_uint2(h.x, A.upd_map ? A.upd_map[lid] : lid);
+      }
+    }
+  } else {  // staging overflowed: enumerate again, writing at the known offsets
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      rw.off[q] += excl;
+      rw.hits[q] = 0;
+    }
+    __syncthreads();
+    enumerate<R, kEmDirect>(A, S, rw, j0, rbmax);
   }
 }
 

@@ -444,6 +444,29 @@ def test_capacity_and_workspace():
     assert L.ddm_match_count(ctypes.byref(r), ctypes.byref(K), ws.data_ptr(), ws.numel(), None) == 1
 
 
+def test_capacity_dd_never_writes_past_capacity(orc):
+    """d > 1 (single fused pass): capacity < K reports DDM_ERR_CAPACITY with the
+    exact K and writes nothing at or past `capacity`; then the full call works."""
+    import ctypes
+    L = ddm.load()
+    w = wl.uniform(3000, 3000, 100.0, 20.0, 2, seed=7)
+    g = gpu_args(w)
+    ref = orc.sbm_seq(w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi)
+    r, keep = ddm.regions(*g)
+    ws = torch.empty(L.ddm_workspace_bytes(2, w.n, w.m, 1), dtype=torch.uint8, device="cuda")
+    K = ctypes.c_uint64(0)
+    cap = ref.size // 3
+    out = torch.full((ref.size, 2), -7, dtype=torch.int32, device="cuda")
+    st = L.ddm_match_pairs(ctypes.byref(r), out.data_ptr(), cap, ctypes.byref(K), 0, ws.data_ptr(), ws.numel(),
+                           torch.cuda.current_stream().cuda_stream)
+    assert st == 4 and K.value == ref.size
+    assert bool((out[cap:] == -7).all())
+    st = L.ddm_match_pairs(ctypes.byref(r), out.data_ptr(), ref.size, ctypes.byref(K), 0, ws.data_ptr(),
+                           ws.numel(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert st == 0 and np.array_equal(words_of(out), ref)
+
+
 def test_deterministic_output():
     w = wl.make("c2", scale=0.1)
     g = gpu_args(w)
