@@ -101,11 +101,9 @@ ddm_status ddm_match_count(const ddm_regions *regions, uint64_t *count_out, void
                            size_t ws_bytes, cudaStream_t stream);
 
 /* List mode: writes the K pairs to pairs[0..K) (device) and K to *count_out
- * (host).  If capacity < K returns DDM_ERR_CAPACITY with *count_out = K (call
- * with capacity 0 to size the buffer); for d = 1 no pair is written, for d > 1
- * (one fused filter pass, K is known only at its end) pairs below `capacity`
- * may have been written, contents unspecified.  Validation errors are
- * reported before any pair is written. */
+ * (host).  If capacity < K returns DDM_ERR_CAPACITY with *count_out = K and
+ * writes no pair (call with capacity 0 to size the buffer).  Validation
+ * errors are reported before any pair is written. */
 ddm_status ddm_match_pairs(const ddm_regions *regions, ddm_pair *pairs, uint64_t capacity,
                            uint64_t *count_out, uint32_t flags, void *ws, size_t ws_bytes,
                            cudaStream_t stream);

@@ -35,16 +35,15 @@
 // d = 2 every dim-2 value is -inf/+inf and all cells share one dim-2 bin.
 // Cells are stored dim-2 major, so each dim-2 bin of the rectangle is one
 // contiguous run of slots.
-// Output (one pass).  Each hit is staged as (row, its index within the row,
-// sub id) in a per-tile global staging slot; when the tile is done it learns
-// its output offset by decoupled look-back over the tiles' pair totals (tile
-// ids are claimed in order, so predecessors are always running) and writes
-// every staged pair straight to offset + row prefix + index: deterministic
-// order (rows in sweep order, each row in enumeration order) without a second
-// enumeration.  A tile whose hits overflow its staging slot re-runs its
-// enumeration writing pairs directly at their now-known offsets.  The
-// count-only entry point runs the enumeration without staging (row counts ->
-// 256-row tile sums -> scan).
+// Output (one enumeration).  The stage pass enumerates every tile once,
+// writing the row counts, the 256-row tile sums and each hit as (row, its
+// index within the row, sub id) into the tile's global staging slot.  After
+// the offset scan (and the host's capacity check) the place pass writes every
+// staged pair to tile offset + row prefix + index: deterministic order (rows
+// in sweep order, each row in enumeration order) without a second
+// enumeration.  Only a tile whose hits overflowed its staging slot enumerates
+// again in the place pass, writing directly at its known offsets.  The
+// count-only entry point runs the enumeration without staging.
 #pragma once
 #include "common.cuh"
 #include "match.cuh"
@@ -109,12 +108,11 @@ struct Args {
   // count pass
   uint32_t* cnt_out;
   uint64_t* tile_sum;        // per 256-row tile
-  // fused pass
-  const uint32_t* err_flag;   // non-zero: validation failed earlier on the stream -> no-op
+  // stage / place passes
   uint2* stage;               // [tiles][kStageCap] staged hits: {sub id, (row << 16) | index in row}
-  uint64_t* status;           // [tiles] look-back words (zeroed)
-  uint32_t* tile_counter;     // dynamic tile ids (zeroed)
-  uint64_t* k_out;            // total K (written by the last tile)
+  uint32_t* stage_n;          // [tiles] staged hits per tile, or ~0u when the slot overflowed
+  const uint32_t* cnt;        // place: row counts (stage pass output)
+  const uint64_t* tile_off;   // place: exclusive scan of the 256-row tile sums
   uint2* pairs;
   uint64_t capacity;          // pairs at or past capacity are never written
 };
@@ -138,10 +136,8 @@ struct Smem {
   uint32_t scan32[kWarps + 1];
   uint32_t rbmax;
   uint32_t nout;     // staged hits of this tile
-  uint32_t ovf;      // staging overflowed -> re-enumerate in direct mode
-  uint32_t tile;     // dynamic tile id
-  uint64_t excl;     // the tile's output offset (look-back)
-  uint32_t rowoff[kRows];  // exclusive prefix of the row counts inside the tile
+  uint32_t ovf;      // staging overflowed -> re-enumerate in the place pass
+  uint32_t tile;
 };
 
 // Monotone float bucketer over one chunk's lower bounds on one dimension.
@@ -401,34 +397,69 @@ __device__ void enumerate(const Args& A, Smem<R>& S, Rows<R>& rw, uint64_t j0, u
   if (fill) process_chunk<R, EM>(A, S, rw, fill, j0);
 }
 
-// FUSED = false: count pass (row counts + 256-row tile sums).  FUSED = true:
-// the single pass with staged hits and look-back-ordered output (see top).
-template <int R, bool FUSED>
+enum { kModeCount = 0, kModeStage = 1, kModePlace = 2 };
+
+// kModeCount: row counts + 256-row tile sums.  kModeStage: the same plus the
+// staged hits.  kModePlace: staged hits -> pairs (or, for a tile whose slot
+// overflowed, a second enumeration writing directly).
+template <int R, int MODE>
 __global__ void __launch_bounds__(kThreads, 4) dd_tile_kernel(Args A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<R>& S = *reinterpret_cast<Smem<R>*>(smem_raw);
   constexpr int kRows = kThreads * R;
   const int tid = threadIdx.x;
   if (A.abort_flag && *A.abort_flag) return;  // this attempt is discarded (ddm.cu retries with LSB)
-  if (FUSED && A.err_flag && *A.err_flag) return;  // invalid input: nothing may be written
-  const float kInf = __int_as_float(0x7f800000);
+  const uint32_t tile = blockIdx.x;
+  const uint64_t j0 = (uint64_t)tile * kRows;
   if (tid == 0) {
     S.rbmax = 0;
     S.nout = 0;
     S.ovf = 0;
-    S.tile = FUSED ? atomicAdd(A.tile_counter, 1u) : blockIdx.x;
+    S.tile = tile;
   }
   __syncthreads();
-  const uint32_t tile = S.tile;
-  const uint64_t j0 = (uint64_t)tile * kRows;
   Rows<R> rw;
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    rw.valid[q] = j0 + (uint64_t)q * kThreads + tid < A.m;
+    rw.hits[q] = 0;
+    rw.off[q] = 0;
+  }
+  if (MODE == kModePlace) {
+    // row offsets = 256-row tile offset + exclusive scan of the row counts
+    // (kept in the chunk-box area, unused by a tile that only places)
+    static_assert(sizeof(float4) * kCap >= sizeof(uint64_t) * kRows, "row offsets fit the chunk area");
+    uint64_t* rowoff = reinterpret_cast<uint64_t*>(S.c12);
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const uint64_t j = j0 + (uint64_t)q * kThreads + tid;
+      uint64_t total;
+      const uint64_t e = block_excl_scan<kThreads, uint64_t>(rw.valid[q] ? (uint64_t)A.cnt[j] : 0ull, S.scan64, &total);
+      if (rw.valid[q]) rw.off[q] = A.tile_off[(j0 >> 8) + q] + e;
+      rowoff[q * kThreads + tid] = rw.off[q];
+    }
+    __syncthreads();
+    const uint32_t nst = A.stage_n[tile];
+    if (nst != ~0u) {
+      for (uint32_t e = tid; e < nst; e += kThreads) {
+        const uint2 h = A.stage[(uint64_t)tile * kStageCap + e];
+        const uint32_t row = h.y >> 16;
+        const uint64_t pos = rowoff[row] + (h.y & 0xffffu);
+        if (pos < A.capacity) {
+          const uint32_t lid = A.ulo_id[j0 + row];
+          A.pairs[pos] = make_uint2(h.x, A.upd_map ? A.upd_map[lid] : lid);
+        }
+      }
+      return;
+    }
+    // overflowed tile: fall through to a direct enumeration (block-uniform)
+    __syncthreads();
+  }
+  const float kInf = __int_as_float(0x7f800000);
   uint32_t rbmax = 0;
 #pragma unroll
   for (int q = 0; q < R; ++q) {
     const uint64_t j = j0 + (uint64_t)q * kThreads + tid;
-    rw.valid[q] = j < A.m;
-    rw.hits[q] = 0;
-    rw.off[q] = 0;
     if (rw.valid[q]) {
       const uint32_t lid = A.ulo_id[j];
       float4 u;
@@ -445,60 +476,21 @@ __global__ void __launch_bounds__(kThreads, 4) dd_tile_kernel(Args A) {
   if ((tid & 31) == 0) atomicMax(&S.rbmax, rbmax);
   __syncthreads();
   rbmax = S.rbmax;
-
-  if (!FUSED) {
-    enumerate<R, kEmCount>(A, S, rw, j0, rbmax);
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const uint64_t j = j0 + (uint64_t)q * kThreads + tid;
-      if (rw.valid[q]) A.cnt_out[j] = rw.hits[q];
-      uint64_t total;
-      block_excl_scan<kThreads, uint64_t>(rw.valid[q] ? (uint64_t)rw.hits[q] : 0ull, S.scan64, &total);
-      if (tid == 0 && j0 + (uint64_t)q * kThreads < A.m) A.tile_sum[(j0 >> 8) + q] = total;
-    }
+  if (MODE == kModePlace) {
+    enumerate<R, kEmDirect>(A, S, rw, j0, rbmax);
     return;
   }
-
-  enumerate<R, kEmStage>(A, S, rw, j0, rbmax);
-  // row prefix inside the tile (rows q*256 + tid, q-major) and the tile total
-  uint64_t run = 0;
+  if (MODE == kModeStage) enumerate<R, kEmStage>(A, S, rw, j0, rbmax);
+  else enumerate<R, kEmCount>(A, S, rw, j0, rbmax);
 #pragma unroll
   for (int q = 0; q < R; ++q) {
+    const uint64_t j = j0 + (uint64_t)q * kThreads + tid;
+    if (rw.valid[q]) A.cnt_out[j] = rw.hits[q];
     uint64_t total;
-    const uint64_t e = block_excl_scan<kThreads, uint64_t>(rw.valid[q] ? (uint64_t)rw.hits[q] : 0ull, S.scan64, &total);
-    rw.off[q] = run + e;  // relative to the tile's offset for now
-    S.rowoff[q * kThreads + tid] = (uint32_t)(run + e);
-    run += total;
+    block_excl_scan<kThreads, uint64_t>(rw.valid[q] ? (uint64_t)rw.hits[q] : 0ull, S.scan64, &total);
+    if (tid == 0 && j0 + (uint64_t)q * kThreads < A.m) A.tile_sum[(j0 >> 8) + q] = total;
   }
-  // decoupled look-back over the tiles' totals -> this tile's output offset
-  if (tid < 32) {
-    const uint64_t e = match::lookback_warp_u64(A.status, tile, run);
-    if (tid == 0) S.excl = e;
-  }
-  __syncthreads();
-  const uint64_t excl = S.excl;
-  const uint32_t num_tiles = (uint32_t)((A.m + kRows - 1) / kRows);
-  if (tile == num_tiles - 1 && tid == 0) *A.k_out = excl + run;
-  if (!S.ovf) {
-    const uint32_t nout = S.nout;
-    for (uint32_t e = tid; e < nout; e += kThreads) {
-      const uint2 h = A.stage[(uint64_t)tile * kStageCap + e];
-      const uint32_t row = h.y >> 16;
-      const uint64_t pos = excl + S.rowoff[row] + (h.y & 0xffffu);
-      if (pos < A.capacity) {
-        const uint32_t lid = A.ulo_id[j0 + row];
-        A.pairs[pos] = make_uint2(h.x, A.upd_map ? A.upd_map[lid] : lid);
-      }
-    }
-  } else {  // staging overflowed: enumerate again, writing at the known offsets
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-      rw.off[q] += excl;
-      rw.hits[q] = 0;
-    }
-    __syncthreads();
-    enumerate<R, kEmDirect>(A, S, rw, j0, rbmax);
-  }
+  if (MODE == kModeStage && tid == 0) A.stage_n[tile] = S.ovf ? ~0u : S.nout;
 }
 
 }  // namespace dd

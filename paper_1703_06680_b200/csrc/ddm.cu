@@ -305,9 +305,8 @@ struct MatchWs {
   uint64_t* tile_off;  // their exclusive scan: output offset of each row tile
   uint64_t* scan_status;
   uint64_t* part;
-  uint2* dd_stage;      // d > 1 fused pass: per-tile staged hits
-  uint64_t* dd_status;  // its look-back words
-  uint32_t* dd_counter; // its dynamic tile ids
+  uint2* dd_stage;      // d > 1 stage pass: per-tile staged hits
+  uint32_t* dd_stage_n; // their number per tile (~0u: overflowed)
   Misc* misc;
   uint64_t* mm;        // [3][2] min/max keys (Slo, Shi, Ulo)
   MsdScratch slo, shi, ulo;  // MSD chains (slo/shi only with the index scratch)
@@ -336,8 +335,7 @@ MatchWs match_layout(uint32_t d, uint64_t n_sub, uint64_t m, void* base, bool in
     W.fstab = c.take<uint32_t>(m);
     const uint64_t dtiles = m / (dd::kThreads * kDDRows) + 1;
     W.dd_stage = c.take<uint2>(dtiles * dd::kStageCap);
-    W.dd_status = c.take<uint64_t>(dtiles + 1);
-    W.dd_counter = c.take<uint32_t>(1);
+    W.dd_stage_n = c.take<uint32_t>(dtiles);
   }
   W.ulo = msd_scratch(c, m, true);
   if (index_scratch) {
@@ -406,8 +404,9 @@ void init_attrs_once() {
                        (int)sizeof(msd::LocalSmem<true, true>));
   cudaFuncSetAttribute(msd::local_sort_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(msd::LocalSmem<false, false>));
-  cudaFuncSetAttribute(dd::dd_tile_kernel<kDDRows, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(dd::Smem<kDDRows>));
-  cudaFuncSetAttribute(dd::dd_tile_kernel<kDDRows, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(dd::Smem<kDDRows>));
+  cudaFuncSetAttribute(dd::dd_tile_kernel<kDDRows, dd::kModeCount>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(dd::Smem<kDDRows>));
+  cudaFuncSetAttribute(dd::dd_tile_kernel<kDDRows, dd::kModeStage>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(dd::Smem<kDDRows>));
+  cudaFuncSetAttribute(dd::dd_tile_kernel<kDDRows, dd::kModePlace>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(dd::Smem<kDDRows>));
   if (const char* e = getenv("DDM_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(e));
   done = true;
 }
@@ -707,13 +706,13 @@ ddm_status build_index_async(const ddm_regions* R, const Index& I, MsdScratch& s
 // ------------------------------------------------------------ d > 1 tiled filter (dd.cuh)
 
 
-void launch_dd_any(bool emit, const dd::Args& a, cudaStream_t st) {
+void launch_dd(int mode, const dd::Args& a, cudaStream_t st) {
   constexpr int kRows = dd::kThreads * kDDRows;
   const unsigned grid = (unsigned)((a.m + kRows - 1) / kRows);
-  if (emit)
-    dd::dd_tile_kernel<kDDRows, true><<<grid, dd::kThreads, sizeof(dd::Smem<kDDRows>), st>>>(a);
-  else
-    dd::dd_tile_kernel<kDDRows, false><<<grid, dd::kThreads, sizeof(dd::Smem<kDDRows>), st>>>(a);
+  const size_t sm = sizeof(dd::Smem<kDDRows>);
+  if (mode == dd::kModeCount) dd::dd_tile_kernel<kDDRows, dd::kModeCount><<<grid, dd::kThreads, sm, st>>>(a);
+  else if (mode == dd::kModeStage) dd::dd_tile_kernel<kDDRows, dd::kModeStage><<<grid, dd::kThreads, sm, st>>>(a);
+  else dd::dd_tile_kernel<kDDRows, dd::kModePlace><<<grid, dd::kThreads, sm, st>>>(a);
 }
 
 // ------------------------------------------------------------ match against an index
@@ -825,28 +824,19 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
     D.abort_flag = &W.misc->overflow;
     D.cnt_out = W.cnt;
     D.tile_sum = W.tile_sum;
-    if (q.pairs) {
-      // single fused pass: pairs written at look-back offsets, K from the last tile
-      D.err_flag = &W.misc->err;
-      D.stage = W.dd_stage;
-      D.status = W.dd_status;
-      D.tile_counter = W.dd_counter;
-      D.k_out = &W.misc->K;
-      D.pairs = reinterpret_cast<uint2*>(q.pairs);
-      D.capacity = q.capacity;
-      const uint64_t dtiles = (m + dd::kThreads * kDDRows - 1) / (dd::kThreads * kDDRows);
-      DDM_CUDA(cudaMemsetAsync(W.dd_status, 0, sizeof(uint64_t) * (dtiles + 1), st));
-      DDM_CUDA(cudaMemsetAsync(W.dd_counter, 0, sizeof(uint32_t), st));
-      DDM_LAUNCH("dd_fused", 24.0 * m, st, launch_dd_any(true, D, st));
-      DDM_TRY(check_launch());
-    } else {
-      DDM_LAUNCH("dd_count", 24.0 * m, st, launch_dd_any(false, D, st));
-      DDM_TRY(check_launch());
-      DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (stiles + 1), st));
-      DDM_LAUNCH("scan", 16.0 * rtiles, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
-          W.tile_sum, rtiles, W.tile_off, W.scan_status, &W.misc->K));
-      DDM_TRY(check_launch());
-    }
+    D.stage = W.dd_stage;
+    D.stage_n = W.dd_stage_n;
+    D.cnt = W.cnt;
+    D.tile_off = W.tile_off;
+    // one enumeration: counts (+ staged hits when pairs are wanted) -> scan;
+    // the place pass runs after the sync and the capacity check
+    if (q.pairs) DDM_LAUNCH("dd_stage", 24.0 * m, st, launch_dd(dd::kModeStage, D, st));
+    else DDM_LAUNCH("dd_count", 24.0 * m, st, launch_dd(dd::kModeCount, D, st));
+    DDM_TRY(check_launch());
+    DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (stiles + 1), st));
+    DDM_LAUNCH("scan", 16.0 * rtiles, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
+        W.tile_sum, rtiles, W.tile_off, W.scan_status, &W.misc->K));
+    DDM_TRY(check_launch());
   } else if (d > 1) {
     // a8, per-row form (forced by the emit-path flags; cross-check of the tiled form)
     A.cnt_out = W.cnt;
@@ -872,7 +862,12 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
   if (h.K > q.capacity) return DDM_ERR_CAPACITY;
   if (h.K == 0) return DDM_OK;
   A.pairs = reinterpret_cast<uint2*>(q.pairs);
-  if (d > 1 && !per_row) return DDM_OK;  // the fused pass has written the pairs
+  if (d > 1 && !per_row) {
+    D.pairs = A.pairs;
+    D.capacity = q.capacity;
+    DDM_LAUNCH("dd_place", 16.0 * h.K + 8.0 * h.K, st, launch_dd(dd::kModePlace, D, st));
+    return check_launch();
+  }
   // sparse outputs (a few pairs per row on average, e.g. alpha ~ 1) gain
   // nothing from staging chunk-start sets: the light per-row kernel (higher
   // occupancy) is used unless the chunk path is forced

@@ -339,6 +339,20 @@ def test_dd_degenerate_dim1(orc):
     check_against(orc, sl, sl + 0.5, ul, ul + 0.5, flags=EMIT_FLAGS)
 
 
+def test_dd_staging_overflow(orc):
+    """d > 1 tiles whose hits exceed the per-tile staging slot (8192) or a row
+    with more than 65535 hits: the place pass re-enumerates them directly."""
+    rng = np.random.default_rng(35)
+    # dense tile: every region of both kinds overlaps every other (K = n*m)
+    sl = rng.uniform(0.0, 0.5, (2, 300))
+    ul = rng.uniform(0.0, 0.5, (2, 400))
+    check_against(orc, sl, sl + 1.0, ul, ul + 1.0, flags=(0,))
+    # one row with 70000 partners
+    sl = rng.uniform(0.0, 0.5, (2, 70_000))
+    ul = np.array([[0.2, 5.0], [0.3, 5.0]])
+    check_against(orc, sl, sl + 1.0, ul, ul + 0.5, flags=(0,))
+
+
 def test_dd_deterministic_output():
     w = wl.make("c4", scale=0.02)
     g = gpu_args(w)
