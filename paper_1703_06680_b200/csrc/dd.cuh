@@ -26,7 +26,7 @@
 // every dimension) before it is counted or written.
 //
 // Cells.  Each chunk is counting-sorted (stably, deterministically) into a
-// kG x kG grid of cells over its float32 (dim-1, dim-2) lower bounds; a row
+// kG1 x kG2 grid of cells over its float32 (dim-1, dim-2) lower bounds; a row
 // only scans the cells whose lower bounds can pass its float test on both:
 //   lo_k(U) <= hi_k(S) <= lo_k(S) + maxlen_k  =>  lo_k(S) >= rd(lo_k(U) - maxlen_k)
 // with maxlen_k the chunk's largest float32 length on dim k rounded up and a
@@ -53,14 +53,16 @@ namespace dd {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kG = 16;              // cells per dimension (dims 1 and 2)
-constexpr int kCells = kG * kG;
+constexpr int kG1 = 32;             // cells along dim 1
+constexpr int kG2 = 16;             // cells along dim 2
+constexpr int kCells = kG1 * kG2;
+constexpr int kCPT = kCells / 256;  // cells per thread in the cell scans
 constexpr int kWin = 1024;          // A_t walk window (positions per step), 4 per thread
 constexpr int kCap = 1024;          // candidates per shared-memory chunk
 constexpr int kRounds = kCap / kThreads;
 constexpr int kList = 8;            // queued float passes per lane before an exact batch
 static_assert(kCap >= kWin, "a whole walk window must fit one chunk");
-static_assert(kCells == kThreads, "one thread per cell in the cell scans");
+static_assert(kCells == kThreads * kCPT, "whole cells per thread in the cell scans");
 
 // ------------------------------------------------------------ index boxes
 
@@ -140,17 +142,19 @@ struct Smem {
   uint32_t tile;
 };
 
-// Monotone float bucketer over one chunk's lower bounds on one dimension.
+// Monotone float bucketer over one chunk's lower bounds on one dimension
+// (G bins).
+template <int G>
 struct Bins {
   float mn, scale;
   __device__ __forceinline__ int operator()(float x) const {
     float u = floorf((x - mn) * scale);
-    u = fminf(fmaxf(u, 0.0f), (float)(kG - 1));  // fmaxf(NaN, 0) = 0
+    u = fminf(fmaxf(u, 0.0f), (float)(G - 1));  // fmaxf(NaN, 0) = 0
     return (int)u;
   }
   __device__ __forceinline__ void init(float lo, float hi) {
     mn = lo;
-    float sc = hi > lo ? (float)kG / (hi - lo) : 0.0f;
+    float sc = hi > lo ? (float)G / (hi - lo) : 0.0f;
     if (!(sc <= 1e30f)) sc = 1e30f;
     scale = sc;
   }
@@ -240,7 +244,8 @@ __device__ void process_chunk(const Args& A, Smem<R>& S, Rows<R>& rw, uint32_t f
     S.red[warp] = mn1; S.red[kWarps + warp] = mx1; S.red[2 * kWarps + warp] = ml1;
     S.red[3 * kWarps + warp] = mn2; S.red[4 * kWarps + warp] = mx2; S.red[5 * kWarps + warp] = ml2;
   }
-  S.run[tid] = 0;
+#pragma unroll
+  for (int c = 0; c < kCPT; ++c) S.run[tid * kCPT + c] = 0;
   __syncthreads();
 #pragma unroll
   for (int w = 0; w < kWarps; ++w) {
@@ -251,7 +256,8 @@ __device__ void process_chunk(const Args& A, Smem<R>& S, Rows<R>& rw, uint32_t f
     mx2 = fmaxf(mx2, S.red[4 * kWarps + w]);
     ml2 = fmaxf(ml2, S.red[5 * kWarps + w]);
   }
-  Bins B1, B2;
+  Bins<kG1> B1;
+  Bins<kG2> B2;
   B1.init(mn1, mx1);
   B2.init(mn2, mx2);
   // 2. cells, totals per cell (order-free), then the cell starts
@@ -260,7 +266,7 @@ __device__ void process_chunk(const Args& A, Smem<R>& S, Rows<R>& rw, uint32_t f
     const uint32_t s = r * kThreads + tid;
     if (s < fill) {
       const float4 b = S.c12[s];
-      cell[r] = B2(b.z) * kG + B1(b.x);
+      cell[r] = B2(b.z) * kG1 + B1(b.x);
       atomicAdd(&S.run[cell[r]], 1u);
     } else {
       cell[r] = kCells;  // "no cell"
@@ -268,11 +274,18 @@ __device__ void process_chunk(const Args& A, Smem<R>& S, Rows<R>& rw, uint32_t f
   }
   __syncthreads();
   {
+    uint32_t v[kCPT], sum = 0;
+#pragma unroll
+    for (int c = 0; c < kCPT; ++c) { v[c] = S.run[tid * kCPT + c]; sum += v[c]; }
     uint32_t total;
-    const uint32_t ex = block_excl_scan<kThreads, uint32_t>(S.run[tid], S.scan32, &total);
-    S.cstart[tid] = ex;
+    uint32_t ex = block_excl_scan<kThreads, uint32_t>(sum, S.scan32, &total);
+#pragma unroll
+    for (int c = 0; c < kCPT; ++c) {
+      S.cstart[tid * kCPT + c] = ex;
+      S.run[tid * kCPT + c] = ex;  // running slot cursor per cell
+      ex += v[c];
+    }
     if (tid == 0) S.cstart[kCells] = total;
-    S.run[tid] = ex;  // running slot cursor per cell
   }
   __syncthreads();
   // 3. stable placement, one round of kThreads slots at a time: rank among
@@ -293,15 +306,18 @@ __device__ void process_chunk(const Args& A, Smem<R>& S, Rows<R>& rw, uint32_t f
     const uint32_t rk = __popc(peers & lanemask_lt());
     if (cell[r] < kCells && rk == 0) S.wc[warp * kCells + cell[r]] = (uint16_t)__popc(peers);
     __syncthreads();
-    {  // thread = cell: exclusive prefix over warps, advance the running cursor
-      uint32_t acc = S.run[tid];
+#pragma unroll
+    for (int cc = 0; cc < kCPT; ++cc) {  // per cell: exclusive prefix over warps, advance the cursor
+      const int cl = tid * kCPT + cc;
+      uint32_t acc = S.run[cl];
+      const uint32_t c0 = S.cstart[cl];
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) {
-        const uint32_t c = S.wc[w * kCells + tid];
-        S.wc[w * kCells + tid] = (uint16_t)(acc - S.cstart[tid]);
+        const uint32_t c = S.wc[w * kCells + cl];
+        S.wc[w * kCells + cl] = (uint16_t)(acc - c0);
         acc += c;
       }
-      S.run[tid] = acc;
+      S.run[cl] = acc;
     }
     __syncthreads();
     if (cell[r] < kCells) {
@@ -323,8 +339,8 @@ __device__ void process_chunk(const Args& A, Smem<R>& S, Rows<R>& rw, uint32_t f
     const int b1l = B1(__fsub_rd(u.x, ml1)), b1h = B1(u.y);
     const int b2l = B2(__fsub_rd(u.z, ml2)), b2h = B2(u.w);
     for (int b2 = b2l; b2 <= b2h; ++b2) {
-      const uint32_t k1 = S.cstart[b2 * kG + b1h + 1];
-      for (uint32_t k = S.cstart[b2 * kG + b1l]; k < k1; ++k) {
+      const uint32_t k1 = S.cstart[b2 * kG1 + b1h + 1];
+      for (uint32_t k = S.cstart[b2 * kG1 + b1l]; k < k1; ++k) {
         const float4 f = S.c12[k];
         if (!(f.x <= u.y && u.x <= f.y && f.z <= u.w && u.z <= f.w)) continue;
         if (nl == kList) {
