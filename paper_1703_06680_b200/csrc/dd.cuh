@@ -60,7 +60,7 @@ constexpr int kCPT = kCells / 256;  // cells per thread in the cell scans
 constexpr int kWin = 1024;          // A_t walk window (positions per step), 4 per thread
 constexpr int kCap = 1024;          // candidates per shared-memory chunk
 constexpr int kRounds = kCap / kThreads;
-constexpr int kList = 8;            // queued float passes per lane before an exact batch
+constexpr int kList = 4;            // queued float passes per lane before an exact batch
 static_assert(kCap >= kWin, "a whole walk window must fit one chunk");
 static_assert(kCells == kThreads * kCPT, "whole cells per thread in the cell scans");
 
@@ -103,6 +103,8 @@ struct Args {
   match::DimPtrs upd;        // update coordinates, all dims
   MaxTree T;
   const double* sdims;       // [(d-1)][2][n] other dims of the subs in Slo order
+  const double* udims;       // [(d-1)][2][m] other dims of the updates in Ulo order
+  const uint64_t* uhi;       // dim-0 upper keys in Ulo order (nullptr: from upd.hi[0])
   const float4* box12;       // widened float32 boxes (box_kernel)
   uint64_t n, m;
   int d;
@@ -168,14 +170,17 @@ struct Rows {
 };
 
 // Exact Alg. 1 test on every dimension for the sub at Slo position p and the
-// update at sorted position j (local id lid); global reads (rare: only float
-// passes get here).
+// update at sorted position j (only float passes get here).  Both sides are
+// read in sweep order (sdims / udims), so these reads stay local.
 __device__ __forceinline__ bool exact_hit(const Args& A, uint32_t p, uint64_t j, uint32_t lid) {
-  if (!(A.slo_key[p] <= f64_key(A.upd.hi[0][lid]) && A.T.lvl[0][p] >= A.ulo_key[j])) return false;  // dim 0
+  const uint64_t b = A.uhi ? A.uhi[j] : f64_key(A.upd.hi[0][lid]);
+  if (!(A.slo_key[p] <= b && A.T.lvl[0][p] >= A.ulo_key[j])) return false;  // dim 0 (keys)
   for (int k = 1; k < A.d; ++k) {
     const double slo = A.sdims[(uint64_t)(k - 1) * 2 * A.n + p];
     const double shi = A.sdims[(uint64_t)(k - 1) * 2 * A.n + A.n + p];
-    if (!(slo <= A.upd.hi[k][lid] && A.upd.lo[k][lid] <= shi)) return false;
+    const double ulo = A.udims[(uint64_t)(k - 1) * 2 * A.m + j];
+    const double uhi = A.udims[(uint64_t)(k - 1) * 2 * A.m + A.m + j];
+    if (!(slo <= uhi && ulo <= shi)) return false;
   }
   return true;
 }
@@ -477,12 +482,11 @@ __global__ void __launch_bounds__(kThreads, 4) dd_tile_kernel(Args A) {
   for (int q = 0; q < R; ++q) {
     const uint64_t j = j0 + (uint64_t)q * kThreads + tid;
     if (rw.valid[q]) {
-      const uint32_t lid = A.ulo_id[j];
       float4 u;
-      u.x = __double2float_rd(A.upd.lo[1][lid]);
-      u.y = __double2float_ru(A.upd.hi[1][lid]);
-      u.z = A.d > 2 ? __double2float_rd(A.upd.lo[2][lid]) : -kInf;
-      u.w = A.d > 2 ? __double2float_ru(A.upd.hi[2][lid]) : kInf;
+      u.x = __double2float_rd(A.udims[j]);
+      u.y = __double2float_ru(A.udims[A.m + j]);
+      u.z = A.d > 2 ? __double2float_rd(A.udims[2 * A.m + j]) : -kInf;
+      u.w = A.d > 2 ? __double2float_ru(A.udims[3 * A.m + j]) : kInf;
       S.rbox[q * kThreads + tid] = u;
       const uint32_t rb = A.r_b[j];
       rbmax = rb > rbmax ? rb : rbmax;

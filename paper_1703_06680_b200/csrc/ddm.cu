@@ -306,6 +306,7 @@ struct MatchWs {
   uint64_t* scan_status;
   uint64_t* part;
   uint2* dd_stage;      // d > 1 stage pass: per-tile staged hits
+  double* udims;        // d > 1: dims 1..d-1 of the updates in Ulo order
   uint32_t* dd_stage_n; // their number per tile (~0u: overflowed)
   Misc* misc;
   uint64_t* mm;        // [3][2] min/max keys (Slo, Shi, Ulo)
@@ -335,6 +336,7 @@ MatchWs match_layout(uint32_t d, uint64_t n_sub, uint64_t m, void* base, bool in
     W.fstab = c.take<uint32_t>(m);
     const uint64_t dtiles = m / (dd::kThreads * kDDRows) + 1;
     W.dd_stage = c.take<uint2>(dtiles * dd::kStageCap);
+    W.udims = c.take<double>((uint64_t)2 * (d - 1) * m);
     W.dd_stage_n = c.take<uint32_t>(dtiles);
   }
   W.ulo = msd_scratch(c, m, true);
@@ -817,7 +819,16 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
     for (uint32_t k = 0; k < d; ++k) { D.upd.lo[k] = R->upd_lo[k]; D.upd.hi[k] = R->upd_hi[k]; }
     D.T = tree_of(I);
     D.sdims = I.sdims;
+    D.udims = W.udims;
+    D.uhi = use_msd ? W.uhi : nullptr;
     D.box12 = I.box12;
+    {  // dims 1..d-1 of the updates gathered into sweep order (exact re-tests stay local)
+      match::DimPtrs U{};
+      for (uint32_t k = 0; k < d; ++k) { U.lo[k] = R->upd_lo[k]; U.hi[k] = R->upd_hi[k]; }
+      DDM_LAUNCH("gather_dims", 36.0 * (d - 1) * m, st, match::gather_dims_kernel<<<grid_for(m, 256, 8), 256, 0, st>>>(
+          W.ulo_id, U, (int)d, m, W.udims, &W.misc->overflow));
+      DDM_TRY(check_launch());
+    }
     D.n = n;
     D.m = m;
     D.d = (int)d;
