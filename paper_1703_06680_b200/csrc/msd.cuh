@@ -34,7 +34,8 @@ constexpr int kTile = kThreads * kItems;
 constexpr int kSpan = 2048;      // nominal records per local-sort CTA
 constexpr int kCap = 2560;       // records a local-sort CTA can hold
 constexpr int kCapPow2 = 4096;   // bitonic network size bound (next power of two >= kCap)
-constexpr int kFineBins = 4096;  // value bins of the in-smem counting sort
+constexpr int kFineBinBits = 11;
+constexpr int kFineBins = 1 << kFineBinBits;  // value bins of the in-smem counting sort
 constexpr int kMaxBinRun = 64;   // larger bins (ties, clusters) -> bitonic sort of the group
 
 
@@ -485,8 +486,7 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
   }
   // smallest shift with (kmax - kmin) >> sh < kFineBins
   const uint64_t range = kmax - kmin;
-  const int sh = range ? max(0, 64 - __clzll((long long)range) - 12) : 0;
-  static_assert(kFineBins == 4096, "shift formula assumes 12-bit fine bins");
+  const int sh = range ? max(0, 64 - __clzll((long long)range) - kFineBinBits) : 0;
   for (uint32_t i = tid; i < c; i += kThreads) atomicAdd(&S.bin[(uint32_t)((S.keys[i] - kmin) >> sh)], 1u);
   __syncthreads();
   {  // exclusive scan over the bins (16 per thread) + large-bin detection
