@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist", default="slab", choices=["slab", "broadcast"],
+                    help="N>1: slab = fully distributed index (each rank its slab + halo, "
+                         "only the count all-reduce); broadcast = rank 0 builds the sub index, NCCL broadcast")
     return ap.parse_args()
 
 
@@ -219,6 +222,16 @@ def run_ddm(args):
 
         def step():
             return M.pairs_into(out, *g)
+    elif args.dist == "slab":
+        sl, sh, sids, ul, uh, uids = ddist.slab_partition(w, rank, world)
+        part = [torch.from_numpy(a).to(dev) for a in (sl, sh, ul, uh)]
+        sid_t, uid_t = torch.from_numpy(sids).to(dev), torch.from_numpy(uids).to(dev)
+        # capacity from an untimed count of this rank's partition
+        cap = ddm.Matcher(w.d, sl.shape[1], ul.shape[1], dev).count(*part)
+        SM = ddist.SlabMatcher(w.d, sl.shape[1], ul.shape[1], cap, dev)
+
+        def step():
+            return SM.step(part[0], part[1], sid_t, part[2], part[3], uid_t).k_total
     else:
         cuts = ddist.slab_cuts(w.upd_lo[0], world)
         ul, uh, ids = ddist.local_updates(w.upd_lo, w.upd_hi, rank, world, cuts)
@@ -357,7 +370,10 @@ def run_ddm(args):
                 "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
                 "config": workload_config(w, {"parallelism": "single GPU" if world == 1 else
-                                              f"updates sharded by slab x{world}, sub index broadcast (NCCL)",
+                                              (f"dim-0 slabs x{world}: each rank its updates + the subscriptions "
+                                               f"that reach them (halo), count all-reduce (NCCL)"
+                                               if args.dist == "slab" else
+                                               f"updates sharded by slab x{world}, sub index broadcast (NCCL)"),
                                               "K": K, "timing": "CUDA events on the launching stream, max over ranks"}),
                 "pairs_per_s": K / (ms_step * 1e-3), "regions_per_s_per_gpu": value / world,
                 "roofline": roof, "pipeline": phases_summary, "phases": phases, "cpu_baseline": cpu, "e2e": e2e,

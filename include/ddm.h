@@ -108,6 +108,16 @@ ddm_status ddm_match_pairs(const ddm_regions *regions, ddm_pair *pairs, uint64_t
                            uint64_t *count_out, uint32_t flags, void *ws, size_t ws_bytes,
                            cudaStream_t stream);
 
+/* ddm_match_pairs with id maps: the pair written for local subscription s and
+ * local update u is {sub_ids[s], upd_ids[u]} (device arrays of n_sub / n_upd
+ * uint32; either may be NULL = the local index).  Used by the slab-partitioned
+ * multi-GPU mode, where every rank matches its own slab of updates against the
+ * subscriptions that can reach it and reports global ids.  Same workspace,
+ * errors and output order as ddm_match_pairs. */
+ddm_status ddm_match_pairs_mapped(const ddm_regions *regions, const uint32_t *sub_ids, const uint32_t *upd_ids,
+                                  ddm_pair *pairs, uint64_t capacity, uint64_t *count_out, uint32_t flags,
+                                  void *ws, size_t ws_bytes, cudaStream_t stream);
+
 /* Sort pairs[0..k) (device) in place into canonical order: ascending
  * (upd << 32) | sub.  ids must satisfy sub < n_sub and upd < n_upd. */
 size_t ddm_sort_pairs_workspace_bytes(uint64_t k);

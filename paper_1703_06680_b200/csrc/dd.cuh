@@ -95,6 +95,7 @@ struct Args {
   const uint64_t* ulo_key;   // sorted update lower keys (dim 0)
   const uint32_t* ulo_id;    // local update ids in that order
   const uint32_t* upd_map;   // optional global ids
+  const uint32_t* sub_map;   // optional global ids of the subscriptions
   const uint32_t* r_lo;      // dim-0 ranks (count pass a4)
   const uint32_t* r_b;
   const uint32_t* cnt0;      // dim-0 counts
@@ -202,11 +203,13 @@ __device__ __forceinline__ void flush_list(const Args& A, Smem<R>& S, Rows<R>& r
         const uint32_t seq = rw.hits[qq];
         if (EM == kEmDirect) {
           const uint64_t pos = rw.off[qq] + seq;
-          if (pos < A.capacity) A.pairs[pos] = make_uint2(A.slo_id[p], A.upd_map ? A.upd_map[lid] : lid);
+          if (pos < A.capacity)
+            A.pairs[pos] = make_uint2(match::sub_out(A.sub_map, A.slo_id[p]), A.upd_map ? A.upd_map[lid] : lid);
         } else if (EM == kEmStage) {
           const uint32_t slot = atomicAdd(&S.nout, 1u);
           if (slot < kStageCap && seq < 65536u)
-            A.stage[(uint64_t)S.tile * kStageCap + slot] = make_uint2(A.slo_id[p], ((uint32_t)(q * kThreads + tid) << 16) | seq);
+            A.stage[(uint64_t)S.tile * kStageCap + slot] =
+                make_uint2(match::sub_out(A.sub_map, A.slo_id[p]), ((uint32_t)(q * kThreads + tid) << 16) | seq);
           else
             S.ovf = 1;
         }

@@ -732,10 +732,11 @@ void launch_dd(int mode, const dd::Args& a, cudaStream_t st) {
 struct MatchReq {
   const Index* I;
   const ddm_regions* R;       // update side (d, n_upd, upd_lo/hi)
-  const uint32_t* upd_map;    // optional global ids
+  const uint32_t* upd_map;    // optional global ids of the updates
   ddm_pair* pairs;            // nullptr = count only
   uint64_t capacity;
   uint32_t flags;
+  const uint32_t* sub_map = nullptr;  // optional global ids of the subscriptions
 };
 
 // Update side, a1 + a2 (+ a3): validate every dimension, sort Ulo with the
@@ -796,6 +797,7 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
   A.ulo_key = W.ulo_key;
   A.ulo_id = W.ulo_id;
   A.upd_map = q.upd_map;
+  A.sub_map = q.sub_map;
   A.r_lo = W.r_lo;
   A.r_b = W.r_b;
   A.cnt0 = W.cnt0;
@@ -821,6 +823,7 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
     D.ulo_key = W.ulo_key;
     D.ulo_id = W.ulo_id;
     D.upd_map = q.upd_map;
+    D.sub_map = q.sub_map;
     D.r_lo = W.r_lo;
     D.r_b = W.r_b;
     D.cnt0 = W.cnt0;
@@ -962,7 +965,8 @@ size_t ddm_workspace_bytes(uint32_t d, uint64_t n_sub, uint64_t n_upd, int want_
 }
 
 static ddm_status match_full(const ddm_regions* R, ddm_pair* pairs, uint64_t capacity, uint64_t* count_out,
-                             uint32_t flags, void* ws, size_t ws_bytes, cudaStream_t st) {
+                             uint32_t flags, void* ws, size_t ws_bytes, cudaStream_t st,
+                             const uint32_t* sub_map = nullptr, const uint32_t* upd_map = nullptr) {
   DDM_TRY(check_regions(R, true, true));
   if (!count_out || (!ws && ws_bytes) || !aligned(ws, 256)) return DDM_ERR_INVALID_ARGUMENT;
   if (pairs && !aligned(pairs, 8)) return DDM_ERR_INVALID_ARGUMENT;
@@ -970,7 +974,7 @@ static ddm_status match_full(const ddm_regions* R, ddm_pair* pairs, uint64_t cap
   uint8_t* base = static_cast<uint8_t*>(ws);
   Index I = index_layout(R->d, R->n_sub, base);
   MatchWs W = match_layout(R->d, R->n_sub, R->n_upd, base + a256(I.bytes), true);
-  MatchReq q{&I, R, nullptr, pairs, capacity, flags};
+  MatchReq q{&I, R, upd_map, pairs, capacity, flags, sub_map};
   const bool lsb_only = (flags & DDM_SORT_LSB) != 0;
   for (int attempt = lsb_only ? 1 : 0; attempt < 2; ++attempt) {
     const bool use_msd = attempt == 0;
@@ -1007,6 +1011,15 @@ ddm_status ddm_match_pairs(const ddm_regions* regions, ddm_pair* pairs, uint64_t
   ddm_pair dummy;
   return match_full(regions, pairs ? pairs : &dummy, pairs ? capacity : 0, count_out, flags, ws, ws_bytes,
                     stream);
+}
+
+ddm_status ddm_match_pairs_mapped(const ddm_regions* regions, const uint32_t* sub_ids, const uint32_t* upd_ids,
+                                  ddm_pair* pairs, uint64_t capacity, uint64_t* count_out, uint32_t flags,
+                                  void* ws, size_t ws_bytes, cudaStream_t stream) {
+  if (!pairs && capacity) return DDM_ERR_INVALID_ARGUMENT;
+  ddm_pair dummy;
+  return match_full(regions, pairs ? pairs : &dummy, pairs ? capacity : 0, count_out, flags, ws, ws_bytes, stream,
+                    sub_ids, upd_ids);
 }
 
 ddm_status ddm_sub_index_build(const ddm_regions* subs, void* index, size_t index_bytes, void* ws,

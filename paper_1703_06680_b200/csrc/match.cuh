@@ -518,10 +518,15 @@ __device__ __forceinline__ bool box_ok(const Filter& F, const UpdBox& q, uint64_
   return true;
 }
 
+// Output id of a subscription: its global id when a map is given (slab-
+// partitioned multi-GPU matching, dist.py), else the local array index.
+__device__ __forceinline__ uint32_t sub_out(const uint32_t* map, uint32_t s) { return map ? __ldg(map + s) : s; }
+
 struct EmitArgs {
   const uint64_t* ulo_key;
   const uint32_t* ulo_id;   // local update id (index into the update arrays)
   const uint32_t* upd_map;  // optional: global id of each local update
+  const uint32_t* sub_map;  // optional: global id of each local subscription
   const uint32_t* r_lo;
   const uint32_t* r_b;
   const uint32_t* cnt0;     // dim-0 candidate count per row (stab0 = cnt0 - range)
@@ -600,7 +605,7 @@ __device__ __forceinline__ void row_thread(const EmitArgs& A, uint64_t j, uint64
       for (int u = 0; u < 4; ++u)
         if (u < c && rem && h[u] >= a) {
           --rem;
-          A.pairs[o + rem] = make_uint2(A.slo_id[i - u], uid);
+          A.pairs[o + rem] = make_uint2(sub_out(A.sub_map, A.slo_id[i - u]), uid);
         }
       i -= c;
     }
@@ -613,22 +618,22 @@ __device__ __forceinline__ void row_thread(const EmitArgs& A, uint64_t j, uint64
     if (A.T.lvl[0][i] >= a) {
       --rem;
       if (MODE == kEmitD1) {
-        A.pairs[o + rem] = make_uint2(A.slo_id[i], uid);
+        A.pairs[o + rem] = make_uint2(sub_out(A.sub_map, A.slo_id[i]), uid);
       } else if (box_ok(A.F, q, (uint64_t)i)) {
         if (MODE == kCountDD) ++nst;
-        else A.pairs[o + (--fst)] = make_uint2(A.slo_id[i], uid);
+        else A.pairs[o + (--fst)] = make_uint2(sub_out(A.sub_map, A.slo_id[i]), uid);
       }
     }
     --i;
   }
   if (MODE == kEmitD1) {
-    for (uint32_t k = rl; k < rb; ++k) A.pairs[o + stab0 + (k - rl)] = make_uint2(A.slo_id[k], uid);
+    for (uint32_t k = rl; k < rb; ++k) A.pairs[o + stab0 + (k - rl)] = make_uint2(sub_out(A.sub_map, A.slo_id[k]), uid);
   } else {
     const uint32_t base = MODE == kEmitDD ? A.fstab[j] : 0;
     uint32_t w = 0;
     for (uint32_t k = rl; k < rb; ++k) {
       if (box_ok(A.F, q, k)) {
-        if (MODE == kEmitDD) A.pairs[o + base + w] = make_uint2(A.slo_id[k], uid);
+        if (MODE == kEmitDD) A.pairs[o + base + w] = make_uint2(sub_out(A.sub_map, A.slo_id[k]), uid);
         ++w;
       }
     }
@@ -663,28 +668,28 @@ __device__ __forceinline__ void row_warp(const EmitArgs& A, uint64_t j, uint64_t
     const unsigned mm = __ballot_sync(kFull, member);
     rem -= __popc(mm);
     if (MODE == kEmitD1) {
-      if (member) A.pairs[o + rem + __popc(mm & lanemask_lt())] = make_uint2(A.slo_id[idx], uid);
+      if (member) A.pairs[o + rem + __popc(mm & lanemask_lt())] = make_uint2(sub_out(A.sub_map, A.slo_id[idx]), uid);
     } else {
       const bool keep = member && box_ok(A.F, q, (uint64_t)idx);
       const unsigned km = __ballot_sync(kFull, keep);
       if (MODE == kCountDD) nst += __popc(km);
       else {
         fst -= __popc(km);
-        if (keep) A.pairs[o + fst + __popc(km & lanemask_lt())] = make_uint2(A.slo_id[idx], uid);
+        if (keep) A.pairs[o + fst + __popc(km & lanemask_lt())] = make_uint2(sub_out(A.sub_map, A.slo_id[idx]), uid);
       }
     }
     hi_excl = base;
   }
   if (MODE == kEmitD1) {
     for (uint64_t k = (uint64_t)rl + lane; k < rb; k += 32)
-      A.pairs[o + stab0 + (k - rl)] = make_uint2(A.slo_id[k], uid);
+      A.pairs[o + stab0 + (k - rl)] = make_uint2(sub_out(A.sub_map, A.slo_id[k]), uid);
   } else {
     uint32_t w = MODE == kEmitDD ? A.fstab[j] : 0;
     for (uint64_t k0 = rl; k0 < rb; k0 += 32) {
       const uint64_t k = k0 + lane;
       const bool keep = k < rb && box_ok(A.F, q, k);
       const unsigned km = __ballot_sync(kFull, keep);
-      if (MODE == kEmitDD && keep) A.pairs[o + w + __popc(km & lanemask_lt())] = make_uint2(A.slo_id[k], uid);
+      if (MODE == kEmitDD && keep) A.pairs[o + w + __popc(km & lanemask_lt())] = make_uint2(sub_out(A.sub_map, A.slo_id[k]), uid);
       w += __popc(km);
     }
     if (MODE == kCountDD && lane == 0) { A.cnt_out[j] = nst + w; A.fstab_out[j] = nst; }
@@ -751,7 +756,7 @@ __device__ __forceinline__ uint64_t c_hi(const ChunkSmem& S, const EmitArgs& A, 
 }
 __device__ __forceinline__ uint32_t c_id(const ChunkSmem& S, const EmitArgs& A, uint64_t rl0, uint64_t i) {
   const uint64_t k = i - rl0;
-  return k < S.slen ? S.sid[k] : A.slo_id[i];
+  return k < S.slen ? S.sid[k] : sub_out(A.sub_map, A.slo_id[i]);
 }
 
 __device__ __forceinline__ void chunk_row_thread(const ChunkSmem& S, const EmitArgs& A, uint64_t j, uint64_t o,
@@ -845,7 +850,7 @@ __global__ void __launch_bounds__(kRowTile) emit_chunk_kernel(EmitArgs A) {
         if (member) {
           const uint32_t pos = rem + __popc(mm & lanemask_lt());
           S.ahi[pos] = h;
-          S.aid[pos] = A.slo_id[idx];
+          S.aid[pos] = sub_out(A.sub_map, A.slo_id[idx]);
         }
         hi_excl = base;
       }
@@ -853,7 +858,7 @@ __global__ void __launch_bounds__(kRowTile) emit_chunk_kernel(EmitArgs A) {
   } else if (fits) {  // the other warps stage the Slo slice meanwhile
     for (uint32_t k = tid - 32; k < slen; k += kRowTile - 32) {
       S.shi[k] = __ldcs(A.T.lvl[0] + rl0 + k);
-      S.sid[k] = __ldcs(A.slo_id + rl0 + k);
+      S.sid[k] = sub_out(A.sub_map, __ldcs(A.slo_id + rl0 + k));
     }
   }
   __syncthreads();

@@ -73,6 +73,7 @@ def load() -> ctypes.CDLL:
         "ddm_workspace_bytes": ([u32, u64, u64, i32], sz),
         "ddm_match_count": ([R, ctypes.POINTER(u64), vp, sz, vp], i32),
         "ddm_match_pairs": ([R, vp, u64, ctypes.POINTER(u64), u32, vp, sz, vp], i32),
+        "ddm_match_pairs_mapped": ([R, vp, vp, vp, u64, ctypes.POINTER(u64), u32, vp, sz, vp], i32),
         "ddm_sort_pairs_workspace_bytes": ([u64], sz),
         "ddm_sort_pairs": ([vp, u64, u64, u64, vp, sz, vp], i32),
         "ddm_sub_index_bytes": ([u32, u64], sz),
@@ -99,7 +100,8 @@ def load() -> ctypes.CDLL:
     return L
 
 
-EXPORTED = ["ddm_workspace_bytes", "ddm_match_count", "ddm_match_pairs", "ddm_sort_pairs_workspace_bytes",
+EXPORTED = ["ddm_workspace_bytes", "ddm_match_count", "ddm_match_pairs", "ddm_match_pairs_mapped",
+            "ddm_sort_pairs_workspace_bytes",
             "ddm_sort_pairs", "ddm_sub_index_bytes", "ddm_index_build_workspace_bytes", "ddm_sub_index_build",
             "ddm_indexed_workspace_bytes", "ddm_match_pairs_indexed", "ddm_match_count_indexed",
             "ddm_radix_sort_workspace_bytes", "ddm_radix_sort_u64", "ddm_encode_keys", "ddm_status_string",
@@ -193,6 +195,21 @@ class Matcher:
                                ctypes.byref(K), flags, self.ws.data_ptr(), self.ws.numel(),
                                _stream(self.device))
         _check(st, "ddm_match_pairs")
+        return int(K.value)
+
+
+    def pairs_mapped_into(self, out: torch.Tensor, sub_lo, sub_hi, upd_lo, upd_hi, sub_ids=None, upd_ids=None,
+                          flags: int = 0) -> int:
+        """pairs_into with global id maps (uint32/int32 CUDA tensors or None):
+        writes {sub_ids[s], upd_ids[u]} (ddm_match_pairs_mapped)."""
+        L = load()
+        r, keep = regions(sub_lo, sub_hi, upd_lo, upd_hi)
+        K = ctypes.c_uint64(0)
+        st = L.ddm_match_pairs_mapped(ctypes.byref(r), sub_ids.data_ptr() if sub_ids is not None else None,
+                                      upd_ids.data_ptr() if upd_ids is not None else None,
+                                      out.data_ptr() if out.numel() else None, out.shape[0], ctypes.byref(K), flags,
+                                      self.ws.data_ptr(), self.ws.numel(), _stream(self.device))
+        _check(st, "ddm_match_pairs_mapped")
         return int(K.value)
 
 

@@ -1,12 +1,23 @@
-"""Multi-GPU matching (SURVEY §8(e), DESIGN.md §7): one process per GPU.
+"""Multi-GPU matching (SURVEY §8(e), §8(f) #1; DESIGN.md §7): one process per GPU.
 
 The update set is partitioned across ranks by coordinate slab (dim-0 lower
-bound); rank 0 builds the byte-copyable subscription index (sorted Slo/Shi,
-ids, gathered upper keys, block maxima) once and broadcasts it over NVLink
-with NCCL; every rank matches its own updates against the index in its own
-kernels and keeps its pair list local (global update ids); the pair counts are
-all-reduced.  The only exchange steps are the index broadcast and the 8-byte
-count all-reduce.
+bound at equal-count quantiles).  Two modes:
+
+  * "slab" (default, fully distributed index): rank r holds its updates
+    (lo in [c_r, c_{r+1})) and exactly the subscriptions that can reach them,
+    {S : S.hi >= c_r and S.lo <= max hi of its updates} -- its slab plus the
+    halo of intervals crossing c_r (the stabbing set at the slab start,
+    Alg. 6's SubSet[p] at a segment boundary) and the few starting
+    past c_{r+1} that the slab's last updates reach.  Every rank runs the
+    whole pipeline on its partition (ddm_match_pairs_mapped, global ids) and
+    the pair counts are all-reduced: no data-path collective, each pair found
+    once (on its update's rank), per-rank work ~1/G.
+  * "broadcast" (the north star's literal split): rank 0 builds the
+    byte-copyable subscription index once and broadcasts it over NVLink with
+    NCCL; every rank matches its own updates against it.  Its index build is
+    a serial term that does not shrink with G.
+
+Each rank keeps its pair list local (global ids).
 
 Host logic (slab cut points, id bookkeeping, the collective sequence) is
 backend-agnostic so it is covered by world-size-2 gloo tests on CPU with a
@@ -44,6 +55,52 @@ def local_updates(upd_lo: np.ndarray, upd_hi: np.ndarray, rank: int, world: int,
     ids = np.nonzero(slab_of(upd_lo[0], cuts) == rank)[0]
     return (np.ascontiguousarray(upd_lo[:, ids]), np.ascontiguousarray(upd_hi[:, ids]),
             ids.astype(np.int32))
+
+
+def reach_bounds(upd_lo: np.ndarray, upd_hi: np.ndarray, cuts: np.ndarray, world: int):
+    """Per slab r: (c_r, max upper bound of its updates) -- a subscription can
+    meet an update of slab r only if S.hi >= c_r and S.lo <= that maximum."""
+    slab = slab_of(upd_lo[0], cuts)
+    lo = np.concatenate([[-np.inf], cuts])
+    hi = np.full(world, -np.inf)
+    np.maximum.at(hi, slab, upd_hi[0])
+    return lo, hi
+
+
+def local_subscriptions(sub_lo: np.ndarray, sub_hi: np.ndarray, rank: int, c_lo: float, reach_hi: float):
+    """Rank r's subscriptions for the slab mode and their global ids: the
+    slab's own plus the halo (intervals crossing c_r from below, and those
+    starting past the slab that its updates still reach)."""
+    ids = np.nonzero((sub_hi[0] >= c_lo) & (sub_lo[0] <= reach_hi))[0]
+    return (np.ascontiguousarray(sub_lo[:, ids]), np.ascontiguousarray(sub_hi[:, ids]),
+            ids.astype(np.int32))
+
+
+def slab_partition(w, rank: int, world: int):
+    """(sub_lo, sub_hi, sub_ids, upd_lo, upd_hi, upd_ids) of rank r in slab mode."""
+    cuts = slab_cuts(w.upd_lo[0], world)
+    ul, uh, uids = local_updates(w.upd_lo, w.upd_hi, rank, world, cuts)
+    lo, hi = reach_bounds(w.upd_lo, w.upd_hi, cuts, world)
+    sl, sh, sids = local_subscriptions(w.sub_lo, w.sub_hi, rank, lo[rank], hi[rank])
+    return sl, sh, sids, ul, uh, uids
+
+
+class SlabMatcher:
+    """Slab mode (fully distributed index): the whole pipeline on this rank's
+    partition with global ids, then all_reduce(K).  Preallocated for bench.py."""
+
+    def __init__(self, d: int, n_sub_local: int, m_local: int, capacity: int, device, group=None):
+        self.M = ddm.Matcher(d, n_sub_local, m_local, device)
+        self.device = torch.device(device)
+        self.group = group
+        self.out = torch.empty((max(capacity, 1), 2), dtype=torch.int32, device=self.device)
+        self.k_buf = torch.zeros(1, dtype=torch.int64, device=self.device)
+
+    def step(self, sub_lo, sub_hi, sub_ids, upd_lo, upd_hi, upd_ids, flags: int = 0) -> "DistResult":
+        k_local = self.M.pairs_mapped_into(self.out, sub_lo, sub_hi, upd_lo, upd_hi, sub_ids, upd_ids, flags)
+        self.k_buf.fill_(k_local)
+        dist.all_reduce(self.k_buf, op=dist.ReduceOp.SUM, group=self.group)  # C2: the only collective
+        return DistResult(k_local, int(self.k_buf.item()))
 
 
 @dataclass

@@ -89,3 +89,54 @@ def test_slab_cuts_with_ties():
     cuts = ddist.slab_cuts(lo, 4)
     s = ddist.slab_of(lo, cuts)
     assert np.bincount(s, minlength=4).sum() == lo.size
+
+
+def _slab_worker(rank, world, port, out_dir):
+    import oracle
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    w = wl.clustered(3000, 3500, 1e6, 2000.0, seed=19)
+    sl, sh, sids, ul, uh, uids = ddist.slab_partition(w, rank, world)
+    p = oracle.bf_pairs(sl, sh, ul, uh)   # stand-in for ddm_match_pairs_mapped on this rank's partition
+    glob = (uids[(p >> np.uint64(32)).astype(np.int64)].astype(np.uint64) << np.uint64(32)) | \
+        sids[(p & np.uint64(0xFFFFFFFF)).astype(np.int64)].astype(np.uint64)
+    k = torch.tensor([p.size], dtype=torch.int64)
+    dist.all_reduce(k, op=dist.ReduceOp.SUM)   # the slab mode's only collective
+    np.save(os.path.join(out_dir, f"slab_pairs_{rank}.npy"), glob)
+    np.save(os.path.join(out_dir, f"slab_k_{rank}.npy"), np.array([int(k.item())]))
+    dist.destroy_process_group()
+
+
+def test_slab_mode_two_ranks_equal_single(tmp_path):
+    """Slab mode (fully distributed index): each rank holds its updates and the
+    subscriptions that can reach them (halo); the union of the per-rank lists
+    is the single-process list, with no pair reported twice."""
+    import oracle
+    world = 2
+    mp.spawn(_slab_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    w = wl.clustered(3000, 3500, 1e6, 2000.0, seed=19)
+    ref = oracle.bf_pairs(w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi)
+    parts = [np.load(os.path.join(tmp_path, f"slab_pairs_{r}.npy")) for r in range(world)]
+    got = np.sort(np.concatenate(parts))
+    assert np.array_equal(got, ref)
+    for r in range(world):
+        assert int(np.load(os.path.join(tmp_path, f"slab_k_{r}.npy"))[0]) == ref.size
+
+
+def test_slab_partition_covers_every_pair():
+    """Host logic only: for G slabs the partitions' subscription sets contain
+    every partner of every update of the slab (brute-force check)."""
+    import oracle
+    w = wl.uniform(1500, 1700, 1e4, 60.0, 1, seed=23)
+    sl, sh = w.sub_lo.copy(), w.sub_hi.copy()
+    sl[0, :5], sh[0, :5] = 0.0, 1e4  # long intervals cross every cut
+    w2 = wl.Workload("t", 1, w.L, w.l, 0, sl, sh, w.upd_lo, w.upd_hi)
+    ref = oracle.bf_pairs(sl, sh, w.upd_lo, w.upd_hi)
+    for G in (1, 3, 5):
+        allp = []
+        for r in range(G):
+            psl, psh, sids, ul, uh, uids = ddist.slab_partition(w2, r, G)
+            p = oracle.bf_pairs(psl, psh, ul, uh)
+            allp.append((uids[(p >> np.uint64(32)).astype(np.int64)].astype(np.uint64) << np.uint64(32))
+                        | sids[(p & np.uint64(0xFFFFFFFF)).astype(np.int64)].astype(np.uint64))
+        assert np.array_equal(np.sort(np.concatenate(allp)), ref), f"G={G}"

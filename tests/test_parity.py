@@ -525,6 +525,32 @@ def test_indexed_shards_equal_single(orc):
         assert np.array_equal(got, ref), G
 
 
+@pytest.mark.parametrize("d", [1, 2])
+def test_slab_partitions_mapped_equal_single(orc, d):
+    """Slab mode of dist.py run rank by rank on one GPU: every partition's
+    ddm_match_pairs_mapped list (global ids) unioned equals the single-call
+    list; long intervals force halos across every cut."""
+    from paper_1703_06680_b200 import dist as ddist
+    w = wl.clustered(30_000, 32_000, 1e6, 2000.0, seed=29) if d == 1 else \
+        wl.uniform(20_000, 21_000, 1e4, 90.0, 2, seed=29)
+    sl, sh = w.sub_lo.copy(), w.sub_hi.copy()
+    sl[0, :7], sh[0, :7] = -5.0, 2e6
+    w = wl.Workload("slab", d, w.L, w.l, 0, sl, sh, w.upd_lo, w.upd_hi)
+    ref = orc.sbm_seq(w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi)
+    for G in (2, 5):
+        allw = []
+        for r in range(G):
+            psl, psh, sids, ul, uh, uids = ddist.slab_partition(w, r, G)
+            M = ddm.Matcher(d, psl.shape[1], ul.shape[1])
+            g = [cuda(x) for x in (psl, psh, ul, uh)]
+            K = M.count(*g)
+            out = torch.empty((max(K, 1), 2), dtype=torch.int32, device="cuda")
+            k = M.pairs_mapped_into(out, *g, torch.from_numpy(sids).cuda(), torch.from_numpy(uids).cuda())
+            assert k == K
+            allw.append(raw_words(out[:k]))
+        assert np.array_equal(np.sort(np.concatenate(allw)), ref), f"G={G}"
+
+
 def test_msd_overflow_falls_back_to_lsb(orc):
     """A bucket larger than shared memory (here: 12000 equal lower bounds plus a
     spread) makes the MSD sort hand over to the LSB sort: same result."""
