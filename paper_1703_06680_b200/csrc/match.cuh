@@ -786,26 +786,48 @@ __device__ __forceinline__ void chunk_row_warp(const ChunkSmem& S, const EmitArg
   const uint32_t uid = A.upd_map ? A.upd_map[lid] : lid;
   const uint64_t rl = A.r_lo[j], rb = A.r_b[j];
   const uint32_t stab = (uint32_t)(A.cnt[j] - (rb - rl));
+  uint2* const row = A.pairs + o;  // this row's output
   uint32_t w = 0;
-  for (uint32_t k0 = 0; k0 < S.nact && w < stab; k0 += 32) {
+  const uint32_t nact = S.nact;
+  for (uint32_t k0 = 0; k0 < nact && w < stab; k0 += 32) {
     const uint32_t k = k0 + lane;
-    const bool alive = k < S.nact && S.ahi[k] >= a;
+    const bool alive = k < nact && S.ahi[k] >= a;
     const unsigned mm = __ballot_sync(kFull, alive);
-    if (alive) A.pairs[o + w + __popc(mm & lanemask_lt())] = make_uint2(S.aid[k], uid);
+    if (alive) row[w + __popc(mm & lanemask_lt())] = make_uint2(S.aid[k], uid);
     w += __popc(mm);
   }
+  // the rest of the stab part lies in the slice [rl0, rl): 32-wide windows
+  // walking backwards, window-relative 32-bit indices (rl - rl0 <= slen here
+  // unless the row's stab walk leaves the staged slice)
   uint32_t need = stab - w;
-  int64_t hi_excl = (int64_t)rl;
-  while (need) {  // 32-wide windows walking the slice backwards
-    const int64_t base = hi_excl - 32;
-    const int64_t i = base + lane;
-    const bool member = i >= (int64_t)rl0 && c_hi(S, A, rl0, (uint64_t)i) >= a;
+  int32_t hi_excl = (int32_t)(rl - rl0);
+  const int32_t slen = (int32_t)S.slen;
+  while (need) {
+    const int32_t base = hi_excl - 32;
+    const int32_t k = base + lane;
+    bool member = false;
+    uint32_t id = 0;
+    if (k >= 0) {
+      if (k < slen) {
+        member = S.shi[k] >= a;
+        if (member) id = S.sid[k];
+      } else {
+        member = A.T.lvl[0][rl0 + k] >= a;
+        if (member) id = sub_out(A.sub_map, A.slo_id[rl0 + k]);
+      }
+    }
     const unsigned mm = __ballot_sync(kFull, member);
     need -= __popc(mm);
-    if (member) A.pairs[o + w + need + __popc(mm & lanemask_lt())] = make_uint2(c_id(S, A, rl0, (uint64_t)i), uid);
+    if (member) row[w + need + __popc(mm & lanemask_lt())] = make_uint2(id, uid);
     hi_excl = base;
   }
-  for (uint64_t i = rl + lane; i < rb; i += 32) A.pairs[o + stab + (i - rl)] = make_uint2(c_id(S, A, rl0, i), uid);
+  // the range part [rl, rb): staged slice first, then global memory
+  uint2* const rng = row + stab;
+  const uint32_t nr = (uint32_t)(rb - rl);
+  const uint32_t k0 = (uint32_t)(rl - rl0);
+  const uint32_t in_slice = k0 < (uint32_t)slen ? min(nr, (uint32_t)slen - k0) : 0u;
+  for (uint32_t t = lane; t < in_slice; t += 32) rng[t] = make_uint2(S.sid[k0 + t], uid);
+  for (uint32_t t = in_slice + lane; t < nr; t += 32) rng[t] = make_uint2(sub_out(A.sub_map, A.slo_id[rl + t]), uid);
 }
 
 __global__ void __launch_bounds__(kRowTile) emit_chunk_kernel(EmitArgs A) {
