@@ -66,54 +66,77 @@ def peaks():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+_SAMPLER = r"""
+import sys, time, pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+print("max", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=True)
+while True:
+    try:
+        print(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+              pynvml.nvmlDeviceGetCurrentClocksEventReasons(h), flush=True)
+    except pynvml.NVMLError:
+        pass
+    time.sleep(0.002)
+"""
+
+
 class Clocks:
-    """SM clocks and throttle reasons sampled DURING the timed region: an NVML
-    polling thread (every 2 ms, so even a 20 ms region gets samples); falls
-    back to an `nvidia-smi -lms` child if NVML is unavailable."""
+    """SM clocks and throttle reasons sampled DURING the timed region by an
+    NVML polling child process (every 2 ms; a separate process so the GIL of
+    the launching thread cannot starve it)."""
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.sm, self.mx, self.reasons = [], [], set()
-        self.stop_ev = None
-        self.th = None
+        self.p = None
+        self.f = None
 
     def start(self):
-        import threading
+        import subprocess
+        import tempfile
+        self.f = tempfile.TemporaryFile("w+")
         try:
-            import pynvml
-            pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
-            self.mx.append(float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)))
-        except Exception:  # noqa: BLE001 -- no NVML: no samples, stated in the line
-            self.th = None
+            self.p = subprocess.Popen([sys.executable, "-c", _SAMPLER, str(self.gpu)], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
             return
-        self.stop_ev = threading.Event()
-
-        def poll():
-            while not self.stop_ev.is_set():
-                try:
-                    self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
-                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                    for nm, bit in self.REASONS.items():
-                        if r & bit:
-                            self.reasons.add(nm)
-                except Exception:  # noqa: BLE001
-                    pass
-                time.sleep(0.002)
-
-        self.th = threading.Thread(target=poll, daemon=True)
-        self.th.start()
+        t0 = time.time()  # wait for the first sample so the region is covered from its start
+        while time.time() - t0 < 20:
+            self.f.seek(0)
+            if len(self.f.read().splitlines()) >= 2:
+                break
+            time.sleep(0.01)
 
     def stop(self) -> dict:
-        if self.th is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
-        self.stop_ev.set()
-        self.th.join(timeout=2)
-        sm = self.sm
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(self.mx) if self.mx else None,
-                "reasons": sorted(self.reasons), "samples": len(sm), "source": "NVML, 2 ms polling"}
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml sampler unavailable"], "samples": 0}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.p.kill()
+        self.f.seek(0)
+        lines = self.f.read().splitlines()
+        mx, sm, reasons = None, [], set()
+        for ln in lines:
+            parts = ln.split()
+            if parts and parts[0] == "max":
+                mx = float(parts[1])
+                continue
+            try:
+                sm.append(float(parts[0]))
+                r = int(parts[1])
+            except (ValueError, IndexError):
+                continue
+            for nm, bit in self.REASONS.items():
+                if r & bit:
+                    reasons.add(nm)
+        sm = sm[1:] if len(sm) > 1 else sm  # the first sample predates the region
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm), "source": "NVML child process, 2 ms polling"}
 
 
 def workload_config(w, extra=None):
