@@ -553,13 +553,22 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
     }
   }
   __syncthreads();
-  // payloads follow the permutation straight from global memory (the group's
-  // payload is a ~20 KB window: every sector is fetched from DRAM once)
-  for (uint32_t i = tid; i < c; i += kThreads) {
-    const uint16_t t = S.perm[i];
-    k_out[e0 + i] = S.keys[t];
-    if (V64) v64_out[e0 + i] = v64_in[e0 + t];
-    if (V32) v32_out[e0 + i] = v32_in[e0 + t];
+  for (uint32_t i = tid; i < c; i += kThreads) k_out[e0 + i] = S.keys[S.perm[i]];
+  // payloads: staged coalesced through the key buffer (free now), then read
+  // back in permutation order -- random global gathers would cost one L1
+  // request per element
+  if (V64) {
+    __syncthreads();
+    for (uint32_t i = tid; i < c; i += kThreads) S.keys[i] = __ldcs(v64_in + e0 + i);
+    __syncthreads();
+    for (uint32_t i = tid; i < c; i += kThreads) v64_out[e0 + i] = S.keys[S.perm[i]];
+  }
+  if (V32) {
+    uint32_t* b32 = reinterpret_cast<uint32_t*>(S.keys);
+    __syncthreads();
+    for (uint32_t i = tid; i < c; i += kThreads) b32[i] = __ldcs(v32_in + e0 + i);
+    __syncthreads();
+    for (uint32_t i = tid; i < c; i += kThreads) v32_out[e0 + i] = b32[S.perm[i]];
   }
   __syncthreads();
 }
