@@ -207,14 +207,26 @@ __global__ void __launch_bounds__(512) msd_hist_kernel(const void* __restrict__ 
   B.init(M, bits);
   for (int i = threadIdx.x; i < 3 * kRadix; i += blockDim.x) (&sh[0][0])[i] = 0;
   __syncthreads();
+  // 8 independent loads in flight per thread, then the bucket math + counts
+  constexpr int U = 8;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint64_t k = SRC_F64 ? f64_key(__ldcs(reinterpret_cast<const double*>(src) + i))
-                               : __ldcs(reinterpret_cast<const uint64_t*>(src) + i);
-    const uint32_t b = B(k);
-    atomicAdd(&sh[0][b & 255], 1u);
-    if (passes > 1) atomicAdd(&sh[1][(b >> 8) & 255], 1u);
-    if (passes > 2) atomicAdd(&sh[2][(b >> 16) & 255], 1u);
+  const uint64_t* s64 = reinterpret_cast<const uint64_t*>(src);
+  for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+    uint64_t raw[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = i0 + u * stride;
+      raw[u] = i < n ? __ldcs(s64 + i) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (i0 + u * stride >= n) break;
+      const uint64_t k = SRC_F64 ? f64_key(__longlong_as_double((long long)raw[u])) : raw[u];
+      const uint32_t b = B(k);
+      atomicAdd(&sh[0][b & 255], 1u);
+      if (passes > 1) atomicAdd(&sh[1][(b >> 8) & 255], 1u);
+      if (passes > 2) atomicAdd(&sh[2][(b >> 16) & 255], 1u);
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) {
