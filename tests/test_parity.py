@@ -500,13 +500,16 @@ def test_sort_pairs_canonical(orc):
 
 # ------------------------------------------------------------ index / shards (multi-GPU analogue)
 
-def test_indexed_shards_equal_single(orc):
+@pytest.mark.parametrize("d", [1, 3])
+def test_indexed_shards_equal_single(orc, d):
     """G-invariance: partition updates by coordinate slab, match each slab
     against the broadcastable subscription index with global ids, and the
-    concatenation equals the single-call list."""
-    w = wl.make("c2", scale=0.2)
+    concatenation equals the single-call list; d = 3 runs the
+    tiled filter against the index's boxes and other dimensions."""
+    w = wl.make("c2", scale=0.2) if d == 1 else wl.make("c4", scale=0.01)
     g = gpu_args(w)
     ref = words_of(ddm.match_pairs(*g))
+    assert np.array_equal(ref, orc.sbm_seq(w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi))
     idx = ddm.sub_index_build(g[0], g[1])
     for G in (1, 2, 3, 8):
         cuts = np.quantile(w.sub_lo[0], np.arange(1, G) / G)
