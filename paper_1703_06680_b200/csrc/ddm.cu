@@ -782,7 +782,9 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
   DDM_LAUNCH("count_partition", 0, st, match::count_partition_kernel<<<(unsigned)((ctiles + 255) / 256), 256, 0, st>>>(
       W.ulo_key, m, I.slo_key, I.shi_key, n, W.part));
   DDM_TRY(check_launch());
-  DDM_LAUNCH("count", 56.0 * m + 16.0 * n, st, match::count_kernel<<<(unsigned)ctiles, match::kCountThreads, sizeof(match::CountSmem), st>>>(
+  // algorithmic bytes: sorted a and b (16 B, gathered b on the LSB path:
+  // 4 B id + ~32 B sector), r_lo / r_b / cnt written (12 B), Slo + Shi read once (16 B)
+  DDM_LAUNCH("count", (use_msd ? 28.0 : 48.0) * m + 16.0 * n, st, match::count_kernel<<<(unsigned)ctiles, match::kCountThreads, sizeof(match::CountSmem), st>>>(
       W.ulo_key, W.ulo_id, R->upd_hi[0], use_msd ? W.uhi : nullptr, m, I.slo_key, I.shi_key, n, W.part, W.r_lo, W.r_b,
       W.cnt0, W.tile_sum));
   DDM_TRY(check_launch());
@@ -896,10 +898,10 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
   // nothing from staging chunk-start sets: the light per-row kernel (higher
   // occupancy) is used unless the chunk path is forced
   if (d == 1 && !per_row && (h.K > 4ull * m || (q.flags & DDM_EMIT_FORCE_CHUNK)))
-    DDM_LAUNCH("emit", 44.0 * m + 8.0 * h.K, st,
+    DDM_LAUNCH("emit", 24.0 * m + 8.0 * h.K + 12.0 * n, st,
                match::emit_chunk_kernel<<<egrid, match::kRowTile, sizeof(match::ChunkSmem), st>>>(A));
   else if (d == 1)
-    DDM_LAUNCH("emit", 44.0 * m + 8.0 * h.K, st, match::emit_kernel<match::kEmitD1><<<egrid, match::kRowTile, 0, st>>>(A));
+    DDM_LAUNCH("emit", 24.0 * m + 8.0 * h.K + 12.0 * n, st, match::emit_kernel<match::kEmitD1><<<egrid, match::kRowTile, 0, st>>>(A));
   else
     DDM_LAUNCH("emit_dd", 44.0 * m + 8.0 * h.K, st, match::emit_kernel<match::kEmitDD><<<egrid, match::kRowTile, 0, st>>>(A));
   DDM_TRY(check_launch());
