@@ -20,8 +20,13 @@
  *  - Pointers marked (device) must be CUDA device pointers (cudaMalloc /
  *    torch CUDA tensors) on the current device; (host) are host pointers.
  *  - Ownership: the caller owns every buffer (inputs, outputs, workspace,
- *    index).  The library allocates no device memory and keeps no state
- *    between calls; calls are reentrant given distinct workspaces.
+ *    index).  The library allocates no device memory.  Per process it keeps
+ *    two internal side streams per device (the sort chains run concurrently
+ *    on them, joined back into `stream` by events) and a cache of CUDA graphs:
+ *    from the second identical full-match call (same sizes, pointers,
+ *    workspace, flags and stream) the pre-sync half is replayed as one graph
+ *    launch (DDM_GRAPHS=0 disables).  Graphs read the buffers' current
+ *    contents.  Calls are reentrant given distinct workspaces.
  *  - Streams: all device work is stream-ordered on `stream`.  Entry points
  *    that return a count block on one small device->host read of it.
  *  - Alignment: workspace and index must be 256-byte aligned; region arrays

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 #include <cstdio>
 #include <cstdlib>
@@ -89,13 +90,15 @@ inline void prof_end(const char* name, double bytes, cudaStream_t st, int e0) {
     g_launches.fetch_add(1, std::memory_order_relaxed);   \
   } while (0)
 
-#define DDM_CUDA(call)                                   \
-  do {                                                   \
-    cudaError_t e_ = (call);                             \
-    if (e_ != cudaSuccess) {                             \
-      g_last_cuda.store((int)e_);                        \
-      return DDM_ERR_CUDA;                               \
-    }                                                    \
+#define DDM_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      g_last_cuda.store((int)e_);                                                        \
+      if (getenv("DDM_DEBUG")) fprintf(stderr, "libddm: %s at ddm.cu:%d (%s)\n", cudaGetErrorString(e_), \
+                                       __LINE__, #call);                                 \
+      return DDM_ERR_CUDA;                                                               \
+    }                                                                                    \
   } while (0)
 
 #define DDM_CUDA_RET(call) DDM_CUDA(call)
@@ -103,6 +106,7 @@ inline void prof_end(const char* name, double bytes, cudaStream_t st, int e0) {
 inline ddm_status check_launch() {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
+    if (getenv("DDM_DEBUG")) fprintf(stderr, "libddm: launch error %s\n", cudaGetErrorString(e));
     g_last_cuda.store((int)e);
     return DDM_ERR_CUDA;
   }
@@ -761,24 +765,34 @@ ddm_status upd_sort_async(const ddm_regions* R, MatchWs& W, uint64_t n_sub, bool
 
 // a4..a8 against a built index, with the updates already sorted on `st`:
 // counts, scan, one D2H of {K, error, overflow}, then the emission.
-ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool use_msd, cudaStream_t st) {
+// a4..a8 against a built index with the updates already sorted on `st`.
+// Phase PRE enqueues the counts and the offset scan (everything before the
+// host needs K: capturable in a CUDA graph); phase POST reads {K, error,
+// overflow} back (the call's one sync) and enqueues the emission.
+enum MatchPhase { kPhasePre = 1, kPhasePost = 2, kPhaseAll = 3 };
+
+ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool use_msd, cudaStream_t st,
+                        int phase = kPhaseAll) {
   const Index& I = *q.I;
   const ddm_regions* R = q.R;
   const uint64_t m = R->n_upd, n = I.n;
   const uint32_t d = R->d;
   if (m == 0 || n == 0) {  // nothing can match; the non-empty side(s) were validated
+    if (!(phase & kPhasePost)) return DDM_OK;
     Misc h{};
     DDM_CUDA(cudaMemcpyAsync(&h, W.misc, sizeof(Misc), cudaMemcpyDeviceToHost, st));
     DDM_CUDA(cudaStreamSynchronize(st));
     *count_out = 0;
     return err_status(h.err);
   }
+  const bool pre = (phase & kPhasePre) != 0;
   // a4: counts by rank difference (+ the row-tile sums); a5: exclusive scan
   // of the row-tile sums -> output offset of every 256-row tile, K
   const uint64_t ctiles = (m + match::kCountTile - 1) / match::kCountTile;
   const uint64_t rtiles = (m + match::kRowTile - 1) / match::kRowTile;
   const unsigned stiles = (unsigned)((rtiles + match::kScanThreads * match::kScanItems - 1) /
                                      (match::kScanThreads * match::kScanItems));
+  if (pre) {
   DDM_LAUNCH("count_partition", 0, st, match::count_partition_kernel<<<(unsigned)((ctiles + 255) / 256), 256, 0, st>>>(
       W.ulo_key, m, I.slo_key, I.shi_key, n, W.part));
   DDM_TRY(check_launch());
@@ -788,7 +802,8 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
       W.ulo_key, W.ulo_id, R->upd_hi[0], use_msd ? W.uhi : nullptr, m, I.slo_key, I.shi_key, n, W.part, W.r_lo, W.r_b,
       W.cnt0, W.tile_sum));
   DDM_TRY(check_launch());
-  if (d == 1) {
+  }
+  if (pre && d == 1) {
     DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (stiles + 1), st));
     DDM_LAUNCH("scan", 16.0 * rtiles, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
         W.tile_sum, rtiles, W.tile_off, W.scan_status, &W.misc->K));
@@ -837,7 +852,7 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
     D.udims = W.udims;
     D.uhi = use_msd ? W.uhi : nullptr;
     D.box12 = I.box12;
-    {  // dims 1..d-1 of the updates gathered into sweep order (exact re-tests stay local)
+    if (pre) {  // dims 1..d-1 of the updates gathered into sweep order (exact re-tests stay local)
       match::DimPtrs U{};
       for (uint32_t k = 0; k < d; ++k) { U.lo[k] = R->upd_lo[k]; U.hi[k] = R->upd_hi[k]; }
       DDM_LAUNCH("gather_dims", 36.0 * (d - 1) * m, st, match::gather_dims_kernel<<<grid_for(m, 256, 8), 256, 0, st>>>(
@@ -856,14 +871,16 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
     D.tile_off = W.tile_off;
     // one enumeration: counts (+ staged hits when pairs are wanted) -> scan;
     // the place pass runs after the sync and the capacity check
-    if (q.pairs) DDM_LAUNCH("dd_stage", 24.0 * m, st, launch_dd(dd::kModeStage, D, st));
-    else DDM_LAUNCH("dd_count", 24.0 * m, st, launch_dd(dd::kModeCount, D, st));
-    DDM_TRY(check_launch());
-    DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (stiles + 1), st));
-    DDM_LAUNCH("scan", 16.0 * rtiles, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
-        W.tile_sum, rtiles, W.tile_off, W.scan_status, &W.misc->K));
-    DDM_TRY(check_launch());
-  } else if (d > 1) {
+    if (pre) {
+      if (q.pairs) DDM_LAUNCH("dd_stage", 24.0 * m, st, launch_dd(dd::kModeStage, D, st));
+      else DDM_LAUNCH("dd_count", 24.0 * m, st, launch_dd(dd::kModeCount, D, st));
+      DDM_TRY(check_launch());
+      DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (stiles + 1), st));
+      DDM_LAUNCH("scan", 16.0 * rtiles, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
+          W.tile_sum, rtiles, W.tile_off, W.scan_status, &W.misc->K));
+      DDM_TRY(check_launch());
+    }
+  } else if (d > 1 && pre) {
     // a8, per-row form (forced by the emit-path flags; cross-check of the tiled form)
     A.cnt_out = W.cnt;
     A.fstab_out = W.fstab;
@@ -875,9 +892,12 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
     DDM_LAUNCH("scan", 16.0 * rtiles, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
         W.tile_sum, rtiles, W.tile_off, W.scan_status, &W.misc->K));
     DDM_TRY(check_launch());
+  }
+  if (d > 1 && per_row) {
     A.cnt = W.cnt;
     A.fstab = W.fstab;
   }
+  if (!(phase & kPhasePost)) return DDM_OK;
   Misc h{};
   DDM_CUDA(cudaMemcpyAsync(&h, W.misc, sizeof(Misc), cudaMemcpyDeviceToHost, st));
   DDM_CUDA(cudaStreamSynchronize(st));
@@ -917,6 +937,115 @@ int bits_for(uint64_t v) {  // bits needed to represent v (0 -> 0)
   int b = 0;
   while (v) { ++b; v >>= 1; }
   return b;
+}
+
+// ------------------------------------------------------------ CUDA graphs
+//
+// The pre-sync half of a full match (validation, the three concurrent sort
+// chains, counts, offset scan: ~35 launches and memsets over three streams)
+// is captured into a CUDA graph the second time an identical call (same
+// sizes, pointers, workspace, flags, stream) is made, and replayed from then
+// on: one launch instead of dozens, which matters when the kernels are short
+// (c1, c2).  Disabled while profiling or with DDM_GRAPHS=0 / DDM_SERIAL.
+
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  int hits = 0;
+  uint64_t launches = 0;  // kernels in the graph (for ddm_kernel_launch_count)
+};
+std::mutex g_graph_mu;
+std::unordered_map<std::string, GraphEntry> g_graphs;
+
+bool graphs_enabled() {
+  static const bool off = [] {
+    const char* e = getenv("DDM_GRAPHS");
+    return e && atoi(e) == 0;
+  }();
+  return !off && chains_concurrent();
+}
+
+template <typename T>
+void key_put(std::string& k, const T& v) { k.append(reinterpret_cast<const char*>(&v), sizeof(T)); }
+
+std::string graph_key(const ddm_regions* R, const void* ws, size_t ws_bytes, uint32_t flags, bool want_pairs,
+                      const uint32_t* sub_map, const uint32_t* upd_map, cudaStream_t st) {
+  std::string k;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  key_put(k, dev);
+  key_put(k, st);
+  key_put(k, R->d);
+  key_put(k, R->n_sub);
+  key_put(k, R->n_upd);
+  for (uint32_t i = 0; i < R->d; ++i) {
+    key_put(k, R->sub_lo[i]);
+    key_put(k, R->sub_hi[i]);
+    key_put(k, R->upd_lo[i]);
+    key_put(k, R->upd_hi[i]);
+  }
+  key_put(k, ws);
+  key_put(k, ws_bytes);
+  key_put(k, flags);
+  key_put(k, want_pairs);
+  key_put(k, sub_map);
+  key_put(k, upd_map);
+  return k;
+}
+
+// Run pre(stream) -- enqueue-only work on `stream` and side streams joined
+// back into it -- through the graph cache.  Capture happens on an internal
+// stream (the caller's may be the legacy default stream, which cannot
+// capture); the instantiated graph is then launched on the caller's stream.
+std::mutex g_cap_mu;
+cudaStream_t g_cap_stream[64] = {};
+
+template <typename F>
+ddm_status run_cached(const std::string& key, F&& pre, cudaStream_t st) {
+  GraphEntry* e = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    if (g_graphs.size() > 1024)  // bound the bookkeeping of one-off calls
+      for (auto it = g_graphs.begin(); it != g_graphs.end();) it = it->second.exec ? std::next(it) : g_graphs.erase(it);
+    e = &g_graphs[key];
+    if (!e->exec && ++e->hits < 2) e = nullptr;  // first sighting: run eagerly
+  }
+  if (!e) return pre(st);
+  if (!e->exec) {
+    std::lock_guard<std::mutex> ck(g_cap_mu);  // one capture at a time
+    int dev = 0;
+    DDM_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return pre(st);
+    if (!g_cap_stream[dev]) DDM_CUDA(cudaStreamCreateWithFlags(&g_cap_stream[dev], cudaStreamNonBlocking));
+    cudaStream_t cs = g_cap_stream[dev];
+    cudaStream_t side[2];
+    DDM_TRY(side_streams(side, cs));  // created outside the capture
+    const uint64_t l0 = g_launches.load();
+    DDM_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+    const ddm_status r = pre(cs);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(cs, &g);
+    const uint64_t nl = g_launches.load() - l0;
+    g_launches.fetch_sub(nl);  // counted on every replay below instead
+    if (r != DDM_OK || ce != cudaSuccess || !g) {
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      if (getenv("DDM_DEBUG")) fprintf(stderr, "libddm: graph capture failed (%d, %s)\n", (int)r, cudaGetErrorString(ce));
+      return pre(st);  // plain launches
+    }
+    cudaGraphExec_t x = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&x, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) {
+      cudaGetLastError();
+      return pre(st);
+    }
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    e->exec = x;
+    e->launches = nl;
+  }
+  DDM_CUDA(cudaGraphLaunch(e->exec, st));
+  g_launches.fetch_add(e->launches);
+  return DDM_OK;
 }
 
 }  // namespace
@@ -980,22 +1109,30 @@ static ddm_status match_full(const ddm_regions* R, ddm_pair* pairs, uint64_t cap
   const bool lsb_only = (flags & DDM_SORT_LSB) != 0;
   for (int attempt = lsb_only ? 1 : 0; attempt < 2; ++attempt) {
     const bool use_msd = attempt == 0;
-    DDM_CUDA(cudaMemsetAsync(W.misc, 0, sizeof(Misc), st));
-    DDM_TRY(init_minmax(W.mm, st));
-    if (use_msd) {
-      // the update chain (side stream 1) runs concurrently with the index
-      // build (Slo on st, Shi on side stream 0); st joins both before a4
-      cudaStream_t side[2];
-      DDM_TRY(side_streams(side, st));
-      DDM_TRY(stream_join(side[1], st));
-      DDM_TRY(upd_sort_async(R, W, R->n_sub, true, side[1]));
-      DDM_TRY(build_index_async(R, I, W.slo, W.shi, W.sort, W.mm, W.misc, true, st));
-      DDM_TRY(stream_join(st, side[1]));
-    } else {
-      DDM_TRY(build_index_async(R, I, W.slo, W.shi, W.sort, W.mm, W.misc, false, st));
-      DDM_TRY(upd_sort_async(R, W, R->n_sub, false, st));
-    }
-    const ddm_status r = match_sorted(q, W, count_out, use_msd, st);
+    auto pre = [&](cudaStream_t s) -> ddm_status {
+      DDM_CUDA(cudaMemsetAsync(W.misc, 0, sizeof(Misc), s));
+      DDM_TRY(init_minmax(W.mm, s));
+      if (use_msd) {
+        // the update chain (side stream 1) runs concurrently with the index
+        // build (Slo on s, Shi on side stream 0); s joins both before a4
+        cudaStream_t side[2];
+        DDM_TRY(side_streams(side, s));
+        DDM_TRY(stream_join(side[1], s));
+        DDM_TRY(upd_sort_async(R, W, R->n_sub, true, side[1]));
+        DDM_TRY(build_index_async(R, I, W.slo, W.shi, W.sort, W.mm, W.misc, true, s));
+        DDM_TRY(stream_join(s, side[1]));
+      } else {
+        DDM_TRY(build_index_async(R, I, W.slo, W.shi, W.sort, W.mm, W.misc, false, s));
+        DDM_TRY(upd_sort_async(R, W, R->n_sub, false, s));
+      }
+      return match_sorted(q, W, count_out, use_msd, s, kPhasePre);
+    };
+    init_attrs_once();
+    if (use_msd && graphs_enabled())
+      DDM_TRY(run_cached(graph_key(R, ws, ws_bytes, flags, pairs != nullptr, sub_map, upd_map, st), pre, st));
+    else
+      DDM_TRY(pre(st));
+    const ddm_status r = match_sorted(q, W, count_out, use_msd, st, kPhasePost);
     if (r != kRetryLSB) return r;
   }
   return DDM_ERR_CUDA;
