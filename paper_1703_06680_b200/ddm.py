@@ -213,6 +213,66 @@ class Matcher:
         return int(K.value)
 
 
+class PipelinedMatcher:
+    """Matching of a stream of host-resident batches (the serving case: a new
+    batch of regions every step) with the transfers overlapped: batch i+1's
+    host->device copy (copy stream) is enqueued before batch i is matched
+    (compute stream), and batch i's pairs travel device->host on a third
+    stream while batch i+1 is matched (the link is full duplex).  Device
+    inputs and outputs are double-buffered; one workspace serves every match
+    (they are ordered on the compute stream).  Host buffers should be pinned.
+
+        for k, host_out in pm.run((host_in, host_out) for ...):  ...
+
+    yields (K, host_out) per batch once its copy-back is enqueued; the pairs
+    are in host_out[:K] after the next batch's match returns or after run()
+    finishes (it synchronises at the end)."""
+
+    def __init__(self, d: int, n_sub: int, n_upd: int, capacity: int, device="cuda"):
+        self.dev = torch.device(device)
+        self.M = Matcher(d, n_sub, n_upd, self.dev)
+        mk = lambda cnt: torch.empty((d, cnt), dtype=torch.float64, device=self.dev)  # noqa: E731
+        self.inp = [[mk(n_sub), mk(n_sub), mk(n_upd), mk(n_upd)] for _ in range(2)]
+        self.out = [torch.empty((max(capacity, 1), 2), dtype=torch.int32, device=self.dev) for _ in range(2)]
+        self.s_h2d = torch.cuda.Stream(self.dev)
+        self.s_cmp = torch.cuda.Stream(self.dev)
+        self.s_d2h = torch.cuda.Stream(self.dev)
+        self.ev_in = [torch.cuda.Event() for _ in range(2)]    # inputs of a slot copied in
+        self.ev_used = [torch.cuda.Event() for _ in range(2)]  # a slot's inputs consumed by its match
+        self.ev_out = [torch.cuda.Event() for _ in range(2)]   # a slot's pairs copied out
+
+    def _h2d(self, slot, host):
+        with torch.cuda.stream(self.s_h2d):
+            self.s_h2d.wait_event(self.ev_used[slot])
+            for dst, src in zip(self.inp[slot], host):
+                dst.copy_(src, non_blocking=True)
+            self.ev_in[slot].record(self.s_h2d)
+
+    def run(self, batches):
+        it = iter(batches)
+        nxt = next(it, None)
+        slot = 0
+        if nxt is not None:
+            self._h2d(slot, nxt[0])
+        while nxt is not None:
+            host_in, host_out = nxt
+            nxt = next(it, None)
+            if nxt is not None:
+                self._h2d(slot ^ 1, nxt[0])  # next batch's copy overlaps this match
+            with torch.cuda.stream(self.s_cmp):
+                self.s_cmp.wait_event(self.ev_in[slot])
+                self.s_cmp.wait_event(self.ev_out[slot])  # the slot's previous pairs have left
+                k = self.M.pairs_into(self.out[slot], *self.inp[slot])  # one sync of s_cmp (K)
+                self.ev_used[slot].record(self.s_cmp)
+            with torch.cuda.stream(self.s_d2h):
+                self.s_d2h.wait_stream(self.s_cmp)
+                host_out[:k].copy_(self.out[slot][:k], non_blocking=True)
+                self.ev_out[slot].record(self.s_d2h)
+            yield k, host_out
+            slot ^= 1
+        torch.cuda.synchronize(self.dev)
+
+
 def match_count(sub_lo, sub_hi, upd_lo, upd_hi) -> int:
     """K = number of intersecting (subscription, update) pairs."""
     L = load()

@@ -510,6 +510,27 @@ def test_graph_replay_reads_current_inputs(orc):
     assert e.value.status == 2
 
 
+def test_pipelined_matcher_batches(orc):
+    """PipelinedMatcher: a stream of host batches with overlapped copies; each
+    batch's pairs (copied back into its own pinned buffer) equal the oracle's."""
+    n = 20_000
+    rng = np.random.default_rng(41)
+    batches, refs = [], []
+    for b in range(5):
+        sl = rng.uniform(0, 1e6, (1, n))
+        ul = rng.uniform(0, 1e6, (1, n))
+        ln = 50.0 * (1 + b)
+        host = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in (sl, sl + ln, ul, ul + ln)]
+        refs.append(orc.sbm_seq(sl, sl + ln, ul, ul + ln))
+        batches.append(host)
+    cap = max(r.size for r in refs)
+    outs = [torch.empty((cap, 2), dtype=torch.int32).pin_memory() for _ in batches]
+    pm = ddm.PipelinedMatcher(1, n, n, cap)
+    got = list(pm.run(zip(batches, outs)))
+    for (k, hout), ref in zip(got, refs):
+        assert k == ref.size and np.array_equal(words_of(hout[:k]), ref)
+
+
 def test_deterministic_output():
     w = wl.make("c2", scale=0.1)
     g = gpu_args(w)
