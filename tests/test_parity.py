@@ -136,6 +136,42 @@ def test_tie_storms(orc):
         check_against(orc, s[0:1], s[1:2], u[0:1], u[1:2], flags=EMIT_FLAGS, ref=ref)
 
 
+def test_random_mixtures_fuzz(orc):
+    """Seeded fuzz over sizes spanning several sort/count/emit tiles and
+    mixtures of distributions: uniform, clustered spikes (bucket-map
+    equalisation), duplicates, long intervals, negative and mixed-magnitude
+    coordinates, point intervals; d = 1..3.  Every case against brute force."""
+    rng = np.random.default_rng(2024)
+    for case in range(24):
+        d = int(rng.integers(1, 4))
+        n, m = (int(x) for x in rng.integers(1, 9000, 2))
+        def side(cnt):
+            kind = rng.integers(0, 5)
+            if kind == 0:
+                lo = rng.uniform(-1e3, 1e3, (d, cnt))
+            elif kind == 1:  # a few dense spikes
+                c = rng.uniform(-1e6, 1e6, 4)
+                lo = c[rng.integers(0, 4, (d, cnt))] + rng.normal(0, 1e-3, (d, cnt))
+            elif kind == 2:  # heavy duplicates
+                lo = rng.integers(-5, 5, (d, cnt)).astype(np.float64)
+            elif kind == 3:  # mixed magnitudes
+                lo = rng.choice([-1.0, 1.0], (d, cnt)) * 10.0 ** rng.uniform(-300, 300, (d, cnt))
+            else:
+                lo = rng.uniform(0, 1e5, (d, cnt))
+            ln = np.abs(rng.normal(0, 50.0, (d, cnt)))
+            ln[rng.random((d, cnt)) < 0.02] = 1e6   # long intervals
+            ln[rng.random((d, cnt)) < 0.05] = 0.0   # points
+            return lo, lo + ln
+        sl, sh = side(n)
+        ul, uh = side(m)
+        ok = np.all(np.isfinite(sh)) and np.all(np.isfinite(uh))
+        if not ok:
+            continue
+        ref = orc.bf_pairs(sl, sh, ul, uh)
+        flags = EMIT_FLAGS if case % 4 == 0 else (0,)
+        check_against(orc, sl, sh, ul, uh, flags=flags, ref=ref)
+
+
 def test_extreme_magnitudes(orc):
     rng = np.random.default_rng(3)
     v = np.concatenate([rng.uniform(-1, 1, 300) * 1e308, rng.uniform(-1, 1, 300) * 5e-324 * 1000,
