@@ -38,12 +38,14 @@
 // Output (one enumeration).  The stage pass enumerates every tile once,
 // writing the row counts, the 256-row tile sums and each hit as (row, its
 // index within the row, sub id) into the tile's global staging slot.  After
-// the offset scan (and the host's capacity check) the place pass writes every
-// staged pair to tile offset + row prefix + index: deterministic order (rows
-// in sweep order, each row in enumeration order) without a second
-// enumeration.  Only a tile whose hits overflowed its staging slot enumerates
-// again in the place pass, writing directly at its known offsets.  The
-// count-only entry point runs the enumeration without staging.
+// the offset scan (and the host's capacity check) the place pass groups each
+// tile's staged hits by row and orders every row by sub id: deterministic
+// output (rows in sweep order, each row by ascending output sub id) without a
+// second enumeration, so the stage pass may place candidates into cells with
+// plain atomic cursors.  Only a tile whose hits overflowed its staging slot
+// enumerates again in the place pass (stable cell ranking, enumeration
+// order), writing directly at its known offsets.  The count-only entry point
+// runs the enumeration without staging.
 #pragma once
 #include "common.cuh"
 #include "match.cuh"
@@ -296,8 +298,11 @@ __device__ void process_chunk(const Args& A, Smem<R>& S, Rows<R>& rw, uint32_t f
     if (tid == 0) S.cstart[kCells] = total;
   }
   __syncthreads();
-  // 3. stable placement, one round of kThreads slots at a time: rank among
-  // the round's earlier warps (per-warp counts) and lanes (match_any)
+  // 3. placement into cell order.  The stage and count passes place with one
+  // atomic cursor per cell (the order inside a cell does not matter: the
+  // place pass orders every row by sub id); the direct pass of an overflowed
+  // tile ranks stably (per-round warp counts + match_any) so that its
+  // enumeration order, which is its output order, is deterministic.
   float4 keep[kRounds];
   uint32_t kpos[kRounds];
 #pragma unroll
@@ -306,35 +311,46 @@ __device__ void process_chunk(const Args& A, Smem<R>& S, Rows<R>& rw, uint32_t f
     if (s < fill) { keep[r] = S.c12[s]; kpos[r] = S.fpos[s]; }
   }
   __syncthreads();  // c12 is rewritten in cell order below
+  if (EM != kEmDirect) {
 #pragma unroll
-  for (int r = 0; r < kRounds; ++r) {
-    for (int i = tid; i < kWarps * kCells / 2; i += kThreads) reinterpret_cast<uint32_t*>(S.wc)[i] = 0;
-    __syncthreads();
-    const unsigned peers = __match_any_sync(kFull, cell[r]);
-    const uint32_t rk = __popc(peers & lanemask_lt());
-    if (cell[r] < kCells && rk == 0) S.wc[warp * kCells + cell[r]] = (uint16_t)__popc(peers);
-    __syncthreads();
-#pragma unroll
-    for (int cc = 0; cc < kCPT; ++cc) {  // per cell: exclusive prefix over warps, advance the cursor
-      const int cl = tid * kCPT + cc;
-      uint32_t acc = S.run[cl];
-      const uint32_t c0 = S.cstart[cl];
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
-        const uint32_t c = S.wc[w * kCells + cl];
-        S.wc[w * kCells + cl] = (uint16_t)(acc - c0);
-        acc += c;
+    for (int r = 0; r < kRounds; ++r)
+      if (cell[r] < kCells) {
+        const uint32_t q = atomicAdd(&S.run[cell[r]], 1u);
+        S.c12[q] = keep[r];
+        S.cpos[q] = kpos[r];
       }
-      S.run[cl] = acc;
+  } else {
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+      for (int i = tid; i < kWarps * kCells / 2; i += kThreads) reinterpret_cast<uint32_t*>(S.wc)[i] = 0;
+      __syncthreads();
+      const unsigned peers = __match_any_sync(kFull, cell[r]);
+      const uint32_t rk = __popc(peers & lanemask_lt());
+      if (cell[r] < kCells && rk == 0) S.wc[warp * kCells + cell[r]] = (uint16_t)__popc(peers);
+      __syncthreads();
+#pragma unroll
+      for (int cc = 0; cc < kCPT; ++cc) {  // per cell: exclusive prefix over warps, advance the cursor
+        const int cl = tid * kCPT + cc;
+        uint32_t acc = S.run[cl];
+        const uint32_t c0 = S.cstart[cl];
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+          const uint32_t c = S.wc[w * kCells + cl];
+          S.wc[w * kCells + cl] = (uint16_t)(acc - c0);
+          acc += c;
+        }
+        S.run[cl] = acc;
+      }
+      __syncthreads();
+      if (cell[r] < kCells) {
+        const uint32_t q = S.cstart[cell[r]] + S.wc[warp * kCells + cell[r]] + rk;
+        S.c12[q] = keep[r];
+        S.cpos[q] = kpos[r];
+      }
+      __syncthreads();  // wc is zeroed again by the next round
     }
-    __syncthreads();
-    if (cell[r] < kCells) {
-      const uint32_t q = S.cstart[cell[r]] + S.wc[warp * kCells + cell[r]] + rk;
-      S.c12[q] = keep[r];
-      S.cpos[q] = kpos[r];
-    }
-    __syncthreads();  // wc is zeroed again by the next round
   }
+  __syncthreads();
   // 4. every row scans the cells that can pass its float test on dims 1, 2
   // (one contiguous run per dim-2 bin).  Float passes are queued per lane and
   // re-tested exactly in batches (the exact test reads global memory;
@@ -451,27 +467,50 @@ __global__ void __launch_bounds__(kThreads, 4) dd_tile_kernel(Args A) {
   }
   if (MODE == kModePlace) {
     // row offsets = 256-row tile offset + exclusive scan of the row counts
-    // (kept in the chunk-box area, unused by a tile that only places)
-    static_assert(sizeof(float4) * kCap >= sizeof(uint64_t) * kRows, "row offsets fit the chunk area");
-    uint64_t* rowoff = reinterpret_cast<uint64_t*>(S.c12);
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       const uint64_t j = j0 + (uint64_t)q * kThreads + tid;
       uint64_t total;
       const uint64_t e = block_excl_scan<kThreads, uint64_t>(rw.valid[q] ? (uint64_t)A.cnt[j] : 0ull, S.scan64, &total);
       if (rw.valid[q]) rw.off[q] = A.tile_off[(j0 >> 8) + q] + e;
-      rowoff[q * kThreads + tid] = rw.off[q];
     }
     __syncthreads();
     const uint32_t nst = A.stage_n[tile];
     if (nst != ~0u) {
+      // the tile's staged hits, grouped by row (counting sort on the row
+      // prefix) and each row ordered by sub id: output order = rows in sweep
+      // order, each row by ascending sub id, whatever the staging order was.
+      // Shared memory: sub ids over the chunk-box + row-box areas, row
+      // cursors over cpos (all contiguous, unused by a placing tile).
+      static_assert(sizeof(float4) * (kCap + kThreads * R) >= sizeof(uint32_t) * kStageCap, "staged ids fit");
+      static_assert(sizeof(uint32_t) * kCap >= sizeof(uint32_t) * kThreads * R, "row cursors fit");
+      uint32_t* sid = reinterpret_cast<uint32_t*>(S.c12);
+      uint32_t* cur = S.cpos;
+      const uint64_t t0 = A.tile_off[j0 >> 8];
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < R; ++q) cur[q * kThreads + tid] = (uint32_t)(rw.off[q] - t0);
+      __syncthreads();
       for (uint32_t e = tid; e < nst; e += kThreads) {
         const uint2 h = A.stage[(uint64_t)tile * kStageCap + e];
-        const uint32_t row = h.y >> 16;
-        const uint64_t pos = rowoff[row] + (h.y & 0xffffu);
-        if (pos < A.capacity) {
-          const uint32_t lid = A.ulo_id[j0 + row];
-          A.pairs[pos] = make_uint2(h.x, A.upd_map ? A.upd_map[lid] : lid);
+        sid[atomicAdd(&cur[h.y >> 16], 1u)] = h.x;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < R; ++q) {  // each thread sorts and writes its rows (a few hits each)
+        if (!rw.valid[q]) continue;
+        const uint32_t lo = (uint32_t)(rw.off[q] - t0), hi = cur[q * kThreads + tid];
+        for (uint32_t x = lo + 1; x < hi; ++x) {
+          const uint32_t v = sid[x];
+          uint32_t y = x;
+          while (y > lo && sid[y - 1] > v) { sid[y] = sid[y - 1]; --y; }
+          sid[y] = v;
+        }
+        if (hi > lo) {
+          const uint32_t lid = A.ulo_id[j0 + (uint64_t)q * kThreads + tid];
+          const uint32_t uid = A.upd_map ? A.upd_map[lid] : lid;
+          for (uint32_t x = lo; x < hi; ++x)
+            if (t0 + x < A.capacity) A.pairs[t0 + x] = make_uint2(sid[x], uid);
         }
       }
       return;
