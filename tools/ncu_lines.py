@@ -12,7 +12,10 @@ for x in rows:
         h = {n: i for i, n in enumerate(x)}
     elif h and len(x) > 8 and x[0] not in ("",):
         f = lambda v: float(v) if v not in ("", "-") else 0.0
-        cur = [fname, x[0], x[1][:90], f(x[h["Instructions Executed"]]), f(x[h["Warp Stall Sampling (All Samples)"]])]
+        try:
+            cur = [fname, x[0], x[1][:90], f(x[h["Instructions Executed"]]), f(x[h["Warp Stall Sampling (All Samples)"]])]
+        except (ValueError, IndexError):
+            continue  # a source line whose quoting broke the CSV row
         out.append(cur)
 ti = sum(o[3] for o in out) or 1; ts = sum(o[4] for o in out) or 1
 print(f"total warp-instrs {ti:.3e}, stall samples {ts:.0f}")
