@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="pairs", choices=["pairs", "count"],
+                    help="pairs: the list (default); count: K only (ddm_match_count, the paper's experimental "
+                         "mode P:915-918), single GPU")
     ap.add_argument("--dist", default="slab", choices=["slab", "broadcast"],
                     help="N>1: slab = fully distributed index (each rank its slab + halo, "
                          "only the count all-reduce); broadcast = rank 0 builds the sub index, NCCL broadcast")
@@ -139,9 +142,9 @@ class Clocks:
                 "samples": len(sm), "source": "NVML child process, 2 ms polling"}
 
 
-def workload_config(w, extra=None):
+def workload_config(w, extra=None, mode="pairs"):
     d = {"workload": w.name, "d": w.d, "n_sub": w.n, "n_upd": w.m, "L": w.L, "l": w.l, "seed": w.seed,
-         "coords": "float64", "mode": "pairs (list)", "l2": "inputs larger than L2 (no flush needed)"
+         "coords": "float64", "mode": "pairs (list)" if mode == "pairs" else "count only (ddm_match_count)", "l2": "inputs larger than L2 (no flush needed)"
          if 32 * w.d * (w.n + w.m) > 126e6 else "L2 flushed between steps"}
     if extra:
         d.update(extra)
@@ -155,7 +158,7 @@ def cpu_sample(w, frac):
     return wl.window_sample(w, frac) if frac < 1.0 else w
 
 
-def time_oracle(sample, reps=1):
+def time_oracle(sample, reps=1, count_only=False):
     """The oracle as it stands: Parallel-SBM (Alg. 5+6, all host cores) for
     d = 1; for d > 1 the serial SBM with the per-dimension filter (the
     oracle's Parallel-SBM is one-dimensional).  Returns
@@ -166,14 +169,17 @@ def time_oracle(sample, reps=1):
     K = 0
     for _ in range(reps):
         t0 = time.perf_counter()
-        if sample.d == 1:
-            pairs = oracle.par_sbm(sample.sub_lo, sample.sub_hi, sample.upd_lo, sample.upd_hi, P=P, canonicalize=False)
+        if sample.d == 1 and count_only:
+            K = oracle.par_sbm(sample.sub_lo, sample.sub_hi, sample.upd_lo, sample.upd_hi, P=P, count_only=True)
+        elif sample.d == 1:
+            K = oracle.par_sbm(sample.sub_lo, sample.sub_hi, sample.upd_lo, sample.upd_hi, P=P,
+                               canonicalize=False).size
         else:
-            pairs = oracle.sbm_seq(sample.sub_lo, sample.sub_hi, sample.upd_lo, sample.upd_hi, canonicalize=False)
+            K = oracle.sbm_seq(sample.sub_lo, sample.sub_hi, sample.upd_lo, sample.upd_hi, canonicalize=False).size
         dt = time.perf_counter() - t0
-        K = pairs.size
         best = dt if best is None else min(best, dt)
-    method = "oracle.par_sbm (Alg. 5+6, list mode)" if sample.d == 1 else "oracle.sbm_seq (Alg. 4 + filter, list mode)"
+    mode = "count mode" if (count_only and sample.d == 1) else "list mode"
+    method = f"oracle.par_sbm (Alg. 5+6, {mode})" if sample.d == 1 else "oracle.sbm_seq (Alg. 4 + filter, list mode)"
     return best, K, P, method
 
 
@@ -244,7 +250,7 @@ def run_ddm(args):
         out = torch.empty((max(K, 1), 2), dtype=torch.int32, device=dev)
 
         def step():
-            return M.pairs_into(out, *g)
+            return M.pairs_into(out, *g) if args.mode == "pairs" else M.count(*g)
     elif args.dist == "slab":
         sl, sh, sids, ul, uh, uids = ddist.slab_partition(w, rank, world)
         part = [torch.from_numpy(a).to(dev) for a in (sl, sh, ul, uh)]
@@ -355,7 +361,7 @@ def run_ddm(args):
     # D2H overlaps step i+1's match).  Device-timed with events bracketing the
     # first copy-in and the last copy-out.
     e2e = None
-    if world == 1 and not args.no_e2e:
+    if world == 1 and not args.no_e2e and args.mode == "pairs":
         del M, g, out  # the pipelined matcher double-buffers its own inputs (c5: 2 x 16 GB)
         torch.cuda.empty_cache()
         host = [torch.from_numpy(a).pin_memory() for a in (w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi)]
@@ -389,7 +395,7 @@ def run_ddm(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         frac = CPU_SAMPLE_FRAC[args.config]
         s = cpu_sample(w, frac)
-        dt, ks, P, method = time_oracle(s)
+        dt, ks, P, method = time_oracle(s, count_only=args.mode == "count")
         cpu = {"value": (s.n + s.m) / dt, "unit": "regions/s", "cores": P, "kind": "oracle",
                "sample": f"{sample_text(s, frac)}, K={ks}; {method}, {dt:.2f} s"}
 
@@ -397,7 +403,7 @@ def run_ddm(args):
         line = {"metric": METRIC, "value": value, "unit": "regions/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-                "config": workload_config(w, {"parallelism": "single GPU" if world == 1 else
+                "config": workload_config(w, mode=args.mode, extra={"parallelism": "single GPU" if world == 1 else
                                               (f"dim-0 slabs x{world}: each rank its updates + the subscriptions "
                                                f"that reach them (halo), count all-reduce (NCCL)"
                                                if args.dist == "slab" else
