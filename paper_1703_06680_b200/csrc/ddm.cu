@@ -408,10 +408,10 @@ void init_attrs_once() {
                        (int)sizeof(msd::PassSmem<msd::kItems, true, true>));
   cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(msd::PassSmem<msd::kItems, true, true>));
-  cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(msd::PassSmem<msd::kItems, false, false>));
-  cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(msd::PassSmem<msd::kItems, false, false>));
+  cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItemsK, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(msd::PassSmem<msd::kItemsK, false, false>));
+  cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItemsK, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(msd::PassSmem<msd::kItemsK, false, false>));
   cudaFuncSetAttribute(msd::local_sort_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(msd::LocalSmem<true, true>));
   cudaFuncSetAttribute(msd::local_sort_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -569,7 +569,7 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
   uint64_t* bk[2] = {s.k[0], s.k[1]};
   uint64_t* bv[2] = {s.v64[0], s.v64[1]};
   uint32_t* bi[2] = {s.v32[0], s.v32[1]};
-  const uint64_t tiles = (n + msd::kTile - 1) / msd::kTile;
+  const uint64_t tiles = (n + msd::kTile - 1) / msd::kTile;  // (key-only passes use bigger tiles: fewer)
   DDM_CUDA(cudaMemsetAsync(s.counters, 0, sizeof(uint32_t) * radix::kMaxPasses, st));
   for (int p = 0; p < passes; ++p) {
     DDM_CUDA(cudaMemsetAsync(s.status, 0, sizeof(uint32_t) * radix::kRadix * tiles, st));
@@ -582,8 +582,8 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
                        src, v64_src, nullptr, bk[o], bv[o], bi[o], n, M, bits, 8 * p, s.starts + p * 256, s.status,
                        s.counters + p, err));
       else
-        DDM_LAUNCH("msd_pass", bytes, st, msd::msd_pass_kernel<msd::kItems, false, false, true>
-                   <<<persistent_grid((const void*)msd::msd_pass_kernel<msd::kItems, false, false, true>, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, false, false>), tiles), msd::kThreads, sizeof(msd::PassSmem<msd::kItems, false, false>), st>>>(
+        DDM_LAUNCH("msd_pass", bytes, st, msd::msd_pass_kernel<msd::kItemsK, false, false, true>
+                   <<<persistent_grid((const void*)msd::msd_pass_kernel<msd::kItemsK, false, false, true>, msd::kThreads, sizeof(msd::PassSmem<msd::kItemsK, false, false>), tiles), msd::kThreads, sizeof(msd::PassSmem<msd::kItemsK, false, false>), st>>>(
                        src, nullptr, nullptr, bk[o], nullptr, nullptr, n, M, bits, 8 * p, s.starts + p * 256, s.status,
                        s.counters + p, err));
     } else {
@@ -593,8 +593,8 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
                        bk[q], bv[q], bi[q], bk[o], bv[o], bi[o], n, M, bits, 8 * p, s.starts + p * 256, s.status,
                        s.counters + p, err));
       else
-        DDM_LAUNCH("msd_pass", bytes, st, msd::msd_pass_kernel<msd::kItems, false, false, false>
-                   <<<persistent_grid((const void*)msd::msd_pass_kernel<msd::kItems, false, false, false>, msd::kThreads, sizeof(msd::PassSmem<msd::kItems, false, false>), tiles), msd::kThreads, sizeof(msd::PassSmem<msd::kItems, false, false>), st>>>(
+        DDM_LAUNCH("msd_pass", bytes, st, msd::msd_pass_kernel<msd::kItemsK, false, false, false>
+                   <<<persistent_grid((const void*)msd::msd_pass_kernel<msd::kItemsK, false, false, false>, msd::kThreads, sizeof(msd::PassSmem<msd::kItemsK, false, false>), tiles), msd::kThreads, sizeof(msd::PassSmem<msd::kItemsK, false, false>), st>>>(
                        bk[q], nullptr, nullptr, bk[o], nullptr, nullptr, n, M, bits, 8 * p, s.starts + p * 256, s.status,
                        s.counters + p, err));
     }
