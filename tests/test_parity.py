@@ -567,6 +567,33 @@ def test_pipelined_matcher_batches(orc):
         assert k == ref.size and np.array_equal(words_of(hout[:k]), ref)
 
 
+def test_more_than_2_pow_32_pairs():
+    """64-bit counts and offsets: 65537 point subscriptions inside [0, 1) and
+    65537 updates covering [-1, 2] give K = 4,295,098,369 > 2^32 pairs (34 GB
+    of output).  The count is exact; on the device every row is one update
+    repeated n times, the rows are a permutation of the update ids, and
+    sampled rows hold every subscription once."""
+    n = 65537
+    rng = np.random.default_rng(44)
+    lo = rng.uniform(0.0, 1.0, n)
+    ul = np.full(n, -1.0) - rng.uniform(0.0, 0.5, n)
+    g = [cuda(lo), cuda(lo), cuda(ul), cuda(np.full(n, 2.0))]
+    K = ddm.match_count(*g)
+    assert K == n * n and K > 2 ** 32
+    free, _ = torch.cuda.mem_get_info()
+    if free < K * 8 + (8 << 30):
+        pytest.skip("not enough device memory for the 34 GB pair list")
+    p = ddm.match_pairs(*g, capacity=K)
+    assert p.shape[0] == K
+    u = p[:, 1].view(n, n)
+    first = u[:, 0]
+    assert bool((u == first[:, None]).all())
+    assert bool((torch.sort(first.long()).values == torch.arange(n, device=u.device)).all())
+    for r in (0, 1, n // 2, n - 2, n - 1):
+        row = p[r * n:(r + 1) * n, 0].long()
+        assert bool((torch.sort(row).values == torch.arange(n, device=row.device)).all())
+
+
 def test_deterministic_output():
     w = wl.make("c2", scale=0.1)
     g = gpu_args(w)
