@@ -283,8 +283,9 @@ __global__ void __launch_bounds__(256) count_partition_kernel(const uint64_t* __
 }
 
 struct CountSmem {
-  uint64_t ws[kCountWin];
-  uint64_t wh[kCountWin];
+  alignas(16) uint64_t ws[kCountWin + 2];  // +2: the bulk copies start at an even (16-byte) index
+  alignas(16) uint64_t wh[kCountWin + 2];
+  uint64_t bar;
 };
 
 // First window position at or after k whose entry is "after" x (> x for
@@ -381,30 +382,43 @@ __global__ void __launch_bounds__(kCountThreads, 4) count_kernel(
   }
   const uint32_t ls = (uint32_t)umin64(umin64(kCountWin, p1 - p0 + kCountExt), n - p0);
   const uint32_t lh = (uint32_t)umin64(kCountWin, umin64(h1 - h0 + 1, n - h0));
-  for (uint32_t i = tid; i < ls; i += kCountThreads) S.ws[i] = __ldcs(slo_key + p0 + i);
-  for (uint32_t i = tid; i < lh; i += kCountThreads) S.wh[i] = __ldcs(shi_key + h0 + i);
-  __syncthreads();
+  // the two windows arrive by bulk async copies (TMA engine) from 16-byte
+  // aligned starts, tracked by one mbarrier; the threads' own loads of a and
+  // b above are in flight meanwhile.  Reading up to one key past the array is
+  // safe: every sorted key array is followed by another workspace array.
+  const uint32_t os = (uint32_t)(p0 & 1), oh = (uint32_t)(h0 & 1);
+  const uint64_t* W0 = S.ws + os;
+  const uint64_t* H0 = S.wh + oh;
+  if (tid == 0) {
+    mbar_init(&S.bar, 1);
+    const uint32_t bs = ((ls + os + 1) & ~1u) * 8, bh = ((lh + oh + 1) & ~1u) * 8;
+    mbar_expect_tx(&S.bar, bs + bh);
+    if (bs) bulk_g2s(S.ws, slo_key + (p0 - os), bs, &S.bar);
+    if (bh) bulk_g2s(S.wh, shi_key + (h0 - oh), bh, &S.bar);
+  }
+  __syncthreads();  // the barrier is initialised before anyone waits on it
+  mbar_wait(&S.bar, 0);
 
   uint32_t cnt[kCountItems];
 #pragma unroll
   for (int i = 0; i < kCountItems; ++i) cnt[i] = 0;
   if (ni > 0) {
     // first update: binary search inside the windows (falls back to global)
-    uint64_t rl = advance<true>(S.ws, p0, ls, slo_key, n,
-                                p0 + ((ls && S.ws[ls - 1] > a[0]) ? ub(S.ws, 0, ls, a[0]) : ls), a[0]);
-    uint64_t rh = advance<false>(S.wh, h0, lh, shi_key, n,
-                                 h0 + ((lh && S.wh[lh - 1] >= a[0]) ? lb(S.wh, 0, lh, a[0]) : lh), a[0]);
+    uint64_t rl = advance<true>(W0, p0, ls, slo_key, n,
+                                p0 + ((ls && W0[ls - 1] > a[0]) ? ub(W0, 0, ls, a[0]) : ls), a[0]);
+    uint64_t rh = advance<false>(H0, h0, lh, shi_key, n,
+                                 h0 + ((lh && H0[lh - 1] >= a[0]) ? lb(H0, 0, lh, a[0]) : lh), a[0]);
     uint64_t rb = rl;
     uint32_t ol[kCountItems], ob[kCountItems];
 #pragma unroll
     for (int i = 0; i < kCountItems; ++i) {
       if (i < ni) {
         if (i) {
-          rl = advance<true>(S.ws, p0, ls, slo_key, n, rl, a[i]);
-          rh = advance<false>(S.wh, h0, lh, shi_key, n, rh, a[i]);
+          rl = advance<true>(W0, p0, ls, slo_key, n, rl, a[i]);
+          rh = advance<false>(H0, h0, lh, shi_key, n, rh, a[i]);
         }
         const uint64_t start = (i && b[i] >= b[i - 1] && rb > rl) ? rb : rl;
-        rb = advance<true>(S.ws, p0, ls, slo_key, n, start, b[i]);
+        rb = advance<true>(W0, p0, ls, slo_key, n, start, b[i]);
         ol[i] = (uint32_t)rl;
         ob[i] = (uint32_t)rb;
         cnt[i] = (uint32_t)(rb > rh ? rb - rh : 0);
