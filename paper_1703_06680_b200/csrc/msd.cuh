@@ -452,8 +452,9 @@ __global__ void __launch_bounds__(kThreads, 3)
 // ---------------------------------------------------------------- local sort
 
 template <bool V64, bool V32>
-struct LocalSmem {  // keys only: payloads are gathered from global by the permutation
-  uint64_t keys[kCap];
+struct LocalSmem {  // keys only: payloads follow the permutation through the key buffer
+  alignas(16) uint64_t keys[kCap + 2];  // +2: bulk copies start at a 16-byte aligned index
+  uint64_t bar;                         // mbarrier of the bulk copies
   uint32_t bin[kFineBins + 1];
   uint16_t perm[kCapPow2];  // sorted position -> staged index
   uint16_t grp[kCap];       // staged indices grouped by fine bin (unordered within a bin)
@@ -471,12 +472,23 @@ template <bool V64, bool V32>
 __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restrict__ k_in,
                                  const uint64_t* __restrict__ v64_in, const uint32_t* __restrict__ v32_in,
                                  uint64_t* __restrict__ k_out, uint64_t* __restrict__ v64_out,
-                                 uint32_t* __restrict__ v32_out, uint64_t e0, uint32_t c) {
+                                 uint32_t* __restrict__ v32_out, uint64_t e0, uint32_t c, uint32_t& phase) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // the group's keys arrive by one bulk async copy (16-byte aligned start;
+  // reading a key past the array is safe: it is followed by another
+  // workspace array)
+  const uint32_t ko = (uint32_t)(e0 & 1);
+  uint64_t* const K = S.keys + ko;
+  if (tid == 0) {
+    const uint32_t bytes = ((c + ko + 1) & ~1u) * 8;
+    mbar_expect_tx(&S.bar, bytes);
+    bulk_g2s(S.keys, k_in + (e0 - ko), bytes, &S.bar);
+  }
+  mbar_wait(&S.bar, phase);
+  phase ^= 1;
   uint64_t kmin = ~0ull, kmax = 0;
   for (uint32_t i = tid; i < c; i += kThreads) {
-    const uint64_t k = __ldcs(k_in + e0 + i);
-    S.keys[i] = k;
+    const uint64_t k = K[i];
     kmin = k < kmin ? k : kmin;
     kmax = k > kmax ? k : kmax;
   }
@@ -500,7 +512,7 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
   // smallest shift with (kmax - kmin) >> sh < kFineBins
   const uint64_t range = kmax - kmin;
   const int sh = range ? max(0, 64 - __clzll((long long)range) - kFineBinBits) : 0;
-  for (uint32_t i = tid; i < c; i += kThreads) atomicAdd(&S.bin[(uint32_t)((S.keys[i] - kmin) >> sh)], 1u);
+  for (uint32_t i = tid; i < c; i += kThreads) atomicAdd(&S.bin[(uint32_t)((K[i] - kmin) >> sh)], 1u);
   __syncthreads();
   {  // exclusive scan over the bins (16 per thread) + large-bin detection
     constexpr int kPer = kFineBins / kThreads;
@@ -524,20 +536,20 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
   if (S.flag == 0) {
     // group the staged indices by fine bin (any order inside a bin) ...
     for (uint32_t i = tid; i < c; i += kThreads) {
-      const uint32_t pos = atomicAdd(&S.bin[(uint32_t)((S.keys[i] - kmin) >> sh)], 1u);
+      const uint32_t pos = atomicAdd(&S.bin[(uint32_t)((K[i] - kmin) >> sh)], 1u);
       S.grp[pos] = (uint16_t)i;
     }
     __syncthreads();
     // ... then every record's rank = its bin's start + #{bin members before it
     // in (key, staged index) order}; bin b spans [end(b-1), end(b)), <= kMaxBinRun
     for (uint32_t i = tid; i < c; i += kThreads) {
-      const uint64_t kv = S.keys[i];
+      const uint64_t kv = K[i];
       const uint32_t b = (uint32_t)((kv - kmin) >> sh);
       const uint32_t lo = b ? S.bin[b - 1] : 0, hi = S.bin[b];
       uint32_t r = lo;
       for (uint32_t x = lo; x < hi; ++x) {
         const uint32_t w = S.grp[x];
-        const uint64_t kw = S.keys[w];
+        const uint64_t kw = K[w];
         r += (kw < kv || (kw == kv && w < i)) ? 1u : 0u;
       }
       S.perm[r] = (uint16_t)i;
@@ -556,7 +568,7 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
             const uint16_t a = S.perm[i], b = S.perm[l];
             const bool a_gt_b = (a == 0xffff) ? (b != 0xffff)
                                 : (b == 0xffff) ? false
-                                : (S.keys[a] > S.keys[b] || (S.keys[a] == S.keys[b] && a > b));
+                                : (K[a] > K[b] || (K[a] == K[b] && a > b));
             const bool up = (i & k) == 0;
             if (up == a_gt_b) { S.perm[i] = b; S.perm[l] = a; }
           }
@@ -566,21 +578,32 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
     }
   }
   __syncthreads();
-  for (uint32_t i = tid; i < c; i += kThreads) k_out[e0 + i] = S.keys[S.perm[i]];
+  for (uint32_t i = tid; i < c; i += kThreads) k_out[e0 + i] = K[S.perm[i]];
   // payloads: staged coalesced through the key buffer (free now), then read
   // back in permutation order -- random global gathers would cost one L1
   // request per element
   if (V64) {
-    __syncthreads();
-    for (uint32_t i = tid; i < c; i += kThreads) S.keys[i] = __ldcs(v64_in + e0 + i);
-    __syncthreads();
-    for (uint32_t i = tid; i < c; i += kThreads) v64_out[e0 + i] = S.keys[S.perm[i]];
+    __syncthreads();  // the key buffer is free
+    if (tid == 0) {
+      const uint32_t bytes = ((c + ko + 1) & ~1u) * 8;
+      mbar_expect_tx(&S.bar, bytes);
+      bulk_g2s(S.keys, v64_in + (e0 - ko), bytes, &S.bar);
+    }
+    mbar_wait(&S.bar, phase);
+    phase ^= 1;
+    for (uint32_t i = tid; i < c; i += kThreads) v64_out[e0 + i] = K[S.perm[i]];
   }
   if (V32) {
-    uint32_t* b32 = reinterpret_cast<uint32_t*>(S.keys);
+    const uint32_t vo = (uint32_t)(e0 & 3);
+    const uint32_t* b32 = reinterpret_cast<const uint32_t*>(S.keys) + vo;
     __syncthreads();
-    for (uint32_t i = tid; i < c; i += kThreads) b32[i] = __ldcs(v32_in + e0 + i);
-    __syncthreads();
+    if (tid == 0) {
+      const uint32_t bytes = ((c + vo + 3) & ~3u) * 4;
+      mbar_expect_tx(&S.bar, bytes);
+      bulk_g2s(S.keys, v32_in + (e0 - vo), bytes, &S.bar);
+    }
+    mbar_wait(&S.bar, phase);
+    phase ^= 1;
     for (uint32_t i = tid; i < c; i += kThreads) v32_out[e0 + i] = b32[S.perm[i]];
   }
   __syncthreads();
@@ -641,6 +664,8 @@ __global__ void __launch_bounds__(kThreads) local_sort_kernel(const uint64_t* __
   LocalSmem<V64, V32>& S = *reinterpret_cast<LocalSmem<V64, V32>*>(smem_raw);
   Bucketer BK;
   BK.init(M, bits);
+  if (threadIdx.x == 0) mbar_init(&S.bar, 1);  // (next_boundary's barriers publish it)
+  uint32_t phase = 0;
   const uint64_t s0 = (uint64_t)blockIdx.x * kSpan;
   uint64_t e0 = next_boundary(k_in, n, s0, BK, &S.bound[0]);
   const uint64_t e1 = next_boundary(k_in, n, umin64(s0 + kSpan, n), BK, &S.bound[1]);
@@ -653,7 +678,7 @@ __global__ void __launch_bounds__(kThreads) local_sort_kernel(const uint64_t* __
         return;
       }
     }
-    local_sort_group<V64, V32>(S, k_in, v64_in, v32_in, k_out, v64_out, v32_out, e0, (uint32_t)(g1 - e0));
+    local_sort_group<V64, V32>(S, k_in, v64_in, v32_in, k_out, v64_out, v32_out, e0, (uint32_t)(g1 - e0), phase);
     e0 = g1;
   }
 }
