@@ -404,6 +404,8 @@ void init_attrs_once() {
                        (int)sizeof(match::CountSmem));
   cudaFuncSetAttribute(match::emit_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(match::ChunkSmem));
+  cudaFuncSetAttribute(match::emit_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(match::EmitTileSmem));
   cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(msd::PassSmem<msd::kItems, true, true>));
   cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -920,7 +922,11 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
   if (d == 1 && !per_row && (h.K > 4ull * m || (q.flags & DDM_EMIT_FORCE_CHUNK)))
     DDM_LAUNCH("emit", 24.0 * m + 8.0 * h.K + 12.0 * n, st,
                match::emit_chunk_kernel<<<egrid, match::kRowTile, sizeof(match::ChunkSmem), st>>>(A));
-  else if (d == 1)
+  else if (d == 1 && !per_row)  // sparse: tiles of 2048 rows walking a staged Slo window
+    DDM_LAUNCH("emit", 24.0 * m + 8.0 * h.K + 12.0 * n, st,
+               match::emit_tile_kernel<<<(unsigned)((m + match::kEmitTile - 1) / match::kEmitTile), match::kRowTile,
+                                         sizeof(match::EmitTileSmem), st>>>(A));
+  else if (d == 1)  // forced per-row paths (cross-checks)
     DDM_LAUNCH("emit", 24.0 * m + 8.0 * h.K + 12.0 * n, st, match::emit_kernel<match::kEmitD1><<<egrid, match::kRowTile, 0, st>>>(A));
   else
     DDM_LAUNCH("emit_dd", 44.0 * m + 8.0 * h.K, st, match::emit_kernel<match::kEmitDD><<<egrid, match::kRowTile, 0, st>>>(A));

@@ -735,6 +735,143 @@ __global__ void __launch_bounds__(kRowTile) emit_kernel(EmitArgs A) {
   }
 }
 
+// ------------------------------------------------------------ tiled sparse emit (a7, d = 1)
+//
+// Sparse outputs (a few pairs per row, alpha ~ 1): the per-row walks of
+// emit_kernel are chains of dependent global loads.  Here a CTA takes 2048
+// consecutive rows (8 per thread, the count pass's tiling), the Slo window
+// their stab and range parts live in -- [r_lo(first) - kEmitPad, max r_b) --
+// arrives by bulk async copies (upper keys and ids), and every thread walks
+// its rows inside shared memory; positions outside the window (long
+// intervals) fall back to global memory with the block-max skips.  Row
+// offsets: each warp's 256 rows are one offset-scan tile.  Output identical
+// to the other d = 1 paths.
+constexpr int kEmitItems = 8;
+constexpr int kEmitTile = kRowTile * kEmitItems;  // 2048 rows: warp w owns row tile w
+constexpr int kEmitWin = 4096;                     // window entries
+constexpr int kEmitPad = 512;                      // window entries before r_lo(first row)
+
+struct EmitTileSmem {
+  alignas(16) uint64_t wh[kEmitWin + 2];
+  alignas(16) uint32_t wi[kEmitWin + 4];
+  uint64_t bar;
+  uint32_t rbmax;
+};
+
+__global__ void __launch_bounds__(kRowTile, 3) emit_tile_kernel(EmitArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  EmitTileSmem& S = *reinterpret_cast<EmitTileSmem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t j0 = (uint64_t)blockIdx.x * kEmitTile;
+  const uint64_t jt = j0 + (uint64_t)tid * kEmitItems;  // this thread's first row
+  const int ni = jt < A.m ? (int)umin64(kEmitItems, A.m - jt) : 0;
+  uint32_t rl[kEmitItems], rb[kEmitItems], c0[kEmitItems];
+  if (ni == kEmitItems) {
+    const uint4* pl = reinterpret_cast<const uint4*>(A.r_lo + jt);
+    const uint4* pb = reinterpret_cast<const uint4*>(A.r_b + jt);
+    const uint4* pc = reinterpret_cast<const uint4*>(A.cnt0 + jt);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint4 x = __ldg(pl + h), y = __ldg(pb + h), z = __ldg(pc + h);
+      rl[4 * h] = x.x; rl[4 * h + 1] = x.y; rl[4 * h + 2] = x.z; rl[4 * h + 3] = x.w;
+      rb[4 * h] = y.x; rb[4 * h + 1] = y.y; rb[4 * h + 2] = y.z; rb[4 * h + 3] = y.w;
+      c0[4 * h] = z.x; c0[4 * h + 1] = z.y; c0[4 * h + 2] = z.z; c0[4 * h + 3] = z.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kEmitItems; ++i) {
+      rl[i] = i < ni ? A.r_lo[jt + i] : 0;
+      rb[i] = i < ni ? A.r_b[jt + i] : 0;
+      c0[i] = i < ni ? A.cnt0[jt + i] : 0;
+    }
+  }
+  // window [w0, w0 + wlen) of Slo positions, staged by bulk copies
+  uint32_t mx = 0;
+#pragma unroll
+  for (int i = 0; i < kEmitItems; ++i) mx = i < ni && rb[i] > mx ? rb[i] : mx;
+  mx = __reduce_max_sync(kFull, mx);
+  if (tid == 0) S.rbmax = 0;
+  __syncthreads();
+  if (lane == 0) atomicMax(&S.rbmax, mx);
+  __syncthreads();
+  const uint64_t rl_first = A.r_lo[j0];
+  const uint64_t w0 = rl_first > (uint64_t)kEmitPad ? rl_first - kEmitPad : 0;
+  const uint64_t wend = S.rbmax > w0 ? (uint64_t)S.rbmax : w0;
+  const uint32_t wlen = (uint32_t)umin64(kEmitWin, wend - w0);
+  const uint32_t oh = (uint32_t)(w0 & 1), oi = (uint32_t)(w0 & 3);
+  const uint64_t* WH = S.wh + oh;
+  const uint32_t* WI = S.wi + oi;
+  if (tid == 0) {
+    mbar_init(&S.bar, 1);
+    const uint32_t bh = ((wlen + oh + 1) & ~1u) * 8, bi = ((wlen + oi + 3) & ~3u) * 4;
+    mbar_expect_tx(&S.bar, bh + bi);
+    if (wlen) {
+      bulk_g2s(S.wh, A.T.lvl[0] + (w0 - oh), bh, &S.bar);
+      bulk_g2s(S.wi, A.slo_id + (w0 - oi), bi, &S.bar);
+    }
+  }
+  // row keys / ids meanwhile
+  uint64_t a[kEmitItems];
+  uint32_t lid[kEmitItems];
+  if (ni == kEmitItems) {
+    const ulonglong2* pa = reinterpret_cast<const ulonglong2*>(A.ulo_key + jt);
+    const uint4* pi = reinterpret_cast<const uint4*>(A.ulo_id + jt);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const ulonglong2 x = __ldg(pa + h);
+      a[2 * h] = x.x; a[2 * h + 1] = x.y;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint4 x = __ldg(pi + h);
+      lid[4 * h] = x.x; lid[4 * h + 1] = x.y; lid[4 * h + 2] = x.z; lid[4 * h + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kEmitItems; ++i) {
+      a[i] = i < ni ? A.ulo_key[jt + i] : 0;
+      lid[i] = i < ni ? A.ulo_id[jt + i] : 0;
+    }
+  }
+  // row offsets: warp w's 256 rows form offset tile (j0 >> 8) + w
+  uint64_t mine = 0;
+#pragma unroll
+  for (int i = 0; i < kEmitItems; ++i) mine += c0[i];
+  uint64_t incl = warp_incl_scan<uint64_t>(mine);
+  uint64_t o = (ni > 0 ? A.tile_off[(j0 >> 8) + warp] : 0) + incl - mine;
+  __syncthreads();  // the barrier is initialised before anyone waits on it
+  mbar_wait(&S.bar, 0);
+  auto hi_at = [&](uint64_t i) -> uint64_t {
+    const uint64_t k = i - w0;
+    return (i >= w0 && k < wlen) ? WH[k] : A.T.lvl[0][i];
+  };
+  auto id_at = [&](uint64_t i) -> uint32_t {
+    const uint64_t k = i - w0;
+    return sub_out(A.sub_map, (i >= w0 && k < wlen) ? WI[k] : A.slo_id[i]);
+  };
+#pragma unroll
+  for (int r = 0; r < kEmitItems; ++r) {
+    if (r >= ni) break;
+    const uint32_t uid = A.upd_map ? A.upd_map[lid[r]] : lid[r];
+    const uint32_t stab = c0[r] - (rb[r] - rl[r]);
+    uint2* row = A.pairs + o;
+    // stab part: walk Slo backwards from r_lo - 1, exactly `stab` members
+    uint32_t rem = stab;
+    int64_t i = (int64_t)rl[r] - 1;
+    while (rem) {
+      if ((uint64_t)i < w0 && (i & 31) == 31) {  // outside the window: block-max skips
+        const int L = skip_levels(A.T, i, a[r]);
+        if (L) { i -= (int64_t)1 << (5 * L); continue; }
+      }
+      if (hi_at((uint64_t)i) >= a[r]) row[--rem] = make_uint2(id_at((uint64_t)i), uid);
+      --i;
+    }
+    // range part [r_lo, r_b)
+    for (uint32_t k = rl[r]; k < rb[r]; ++k) row[stab + (k - rl[r])] = make_uint2(id_at(k), uid);
+    o += c0[r];
+  }
+}
+
 // ------------------------------------------------------------ chunked sweep (a6 + a7)
 //
 // One CTA per tile of kRowTile consecutive updates (sorted order), the
