@@ -95,6 +95,19 @@ typedef struct {
  * bucket exceeds shared memory; this flag forces the LSB path.  Output is
  * identical either way. */
 #define DDM_SORT_LSB (1u << 12)
+/* Count form of the pairs calls (the count half of the two-pass emission).
+ * Rank form: |Stab(a)| = r_lo - r_hi from a sorted array of the upper bounds
+ * (Shi) -- what ddm_match_count always uses, independent of K.  Walk form:
+ * |Stab(a)| counted by walking the sorted lower bounds backwards from r_lo,
+ * stopped by the prefix maximum of their upper bounds -- O(K) like the
+ * emission itself, and no Shi sort.  Default for ddm_match_pairs (d = 1,
+ * n_sub >= 2^20): one small probe kernel estimates the mean stab size
+ * n_sub * mean(hi - lo) / (max lo - min lo) over 4096 sampled subscriptions
+ * (one extra 8-byte device->host read) and picks the walk form when it is
+ * <= 4; otherwise, and for every indexed match, the rank form.  These flags
+ * force one form.  Output is identical either way. */
+#define DDM_COUNT_RANKS (1u << 13)
+#define DDM_COUNT_WALK (1u << 14)
 
 /* Workspace bytes needed by ddm_match_count (want_pairs = 0) or
  * ddm_match_pairs (want_pairs != 0) for these sizes.  Independent of K. */

@@ -443,7 +443,7 @@ enum { kModeCount = 0, kModeStage = 1, kModePlace = 2 };
 // staged hits.  kModePlace: staged hits -> pairs (or, for a tile whose slot
 // overflowed, a second enumeration writing directly).
 template <int R, int MODE>
-__global__ void __launch_bounds__(kThreads, 4) dd_tile_kernel(Args A) {
+__global__ void __launch_bounds__(kThreads, 4) dd_tile_kernel(const __grid_constant__ Args A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<R>& S = *reinterpret_cast<Smem<R>*>(smem_raw);
   constexpr int kRows = kThreads * R;

@@ -62,8 +62,25 @@ bool serial_env() {
   static const bool serial = getenv("DDM_SERIAL") != nullptr;
   return serial;
 }
+// DDM_CHAINS=1: the sort chains share the call's stream (graphs stay on)
+bool one_chain_env() {
+  static const bool one = [] {
+    const char* e = getenv("DDM_CHAINS");
+    return e && atoi(e) == 1;
+  }();
+  return one;
+}
+// Set for the duration of a walk-form call: with only two sort chains left
+// (Slo, Ulo) one stream and full-occupancy persistent passes beat running
+// them side by side (measured c3: 6.07 vs 6.47 ms; c5: 71.8 vs 80.0 ms).
+thread_local bool t_one_chain = false;
+struct OneChain {
+  bool prev;
+  explicit OneChain(bool on) : prev(t_one_chain) { t_one_chain = on; }
+  ~OneChain() { t_one_chain = prev; }
+};
 // the sort chains run on side streams (not profiling, not DDM_SERIAL)
-bool chains_concurrent() { return !(serial_env() || g_prof.on); }
+bool chains_concurrent() { return !(serial_env() || g_prof.on || one_chain_env() || t_one_chain); }
 
 inline int prof_begin(cudaStream_t st) {
   if (!g_prof.on) return -1;
@@ -149,6 +166,10 @@ struct Index {
   uint64_t* slo_hi = nullptr;
   uint64_t* lvl[kMaxLevels + 1] = {};
   uint64_t* shi_key = nullptr;
+  uint64_t* pmw = nullptr;  // prefix maxima of slo_hi within 1024-entry blocks (match.cuh tree_pm_kernel)
+  uint64_t* pmb = nullptr;  // prefix maxima of slo_hi before each 1024-entry block
+  uint64_t* pmc = nullptr;  // maxima of 8192-block chunks (scratch of the pmb scan)
+  uint64_t nb = 0;          // number of 1024-entry blocks
   double* sdims = nullptr;
   float4* box12 = nullptr;  // d > 1: widened float32 boxes (dims 1, 2) in Slo order (dd.cuh)
   size_t bytes = 0;
@@ -172,6 +193,10 @@ Index index_layout(uint32_t d, uint64_t n, void* base) {
     I.lvl[I.levels] = c.take<uint64_t>(sz);
   }
   I.shi_key = c.take<uint64_t>(n);
+  I.nb = (n + match::kPmBlock - 1) / match::kPmBlock;
+  I.pmw = c.take<uint64_t>(n);
+  I.pmb = c.take<uint64_t>(I.nb);
+  I.pmc = c.take<uint64_t>(I.nb / match::kPmChunk + 1);
   I.sdims = c.take<double>((uint64_t)2 * (d - 1) * n);
   if (d > 1) {
     I.box12 = c.take<float4>(n);
@@ -320,6 +345,7 @@ struct MatchWs {
   uint32_t* dd_stage_n; // their number per tile (~0u: overflowed)
   Misc* misc;
   uint64_t* mm;        // [3][2] min/max keys (Slo, Shi, Ulo)
+  double* probe;       // stab-density estimate (count-form choice)
   MsdScratch slo, shi, ulo;  // MSD chains (slo/shi only with the index scratch)
   SortScratch sort;    // LSB fallback
   size_t bytes;
@@ -331,6 +357,7 @@ MatchWs match_layout(uint32_t d, uint64_t n_sub, uint64_t m, void* base, bool in
   const uint64_t rtiles = m / match::kRowTile + 2;
   W.misc = c.take<Misc>(1);
   W.mm = c.take<uint64_t>(6);
+  W.probe = c.take<double>(2);
   W.scan_status = c.take<uint64_t>(rtiles / (match::kScanThreads * match::kScanItems) + 2);
   W.part = c.take<uint64_t>(4 * (m / match::kCountTile + 2));
   W.tile_sum = c.take<uint64_t>(rtiles);
@@ -400,8 +427,10 @@ void init_attrs_once() {
   set_attrs_items<8>();
   set_attrs_items<12>();
   set_attrs_items<16>();
-  cudaFuncSetAttribute(match::count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(match::CountSmem));
+  cudaFuncSetAttribute(match::count_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)match::count_smem_bytes(false));
+  cudaFuncSetAttribute(match::count_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)match::count_smem_bytes(true));
   cudaFuncSetAttribute(match::emit_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(match::ChunkSmem));
   cudaFuncSetAttribute(match::emit_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -665,8 +694,41 @@ ddm_status validate_side(uint32_t d, uint64_t cnt, const double* const* lo, cons
 // block maxima, other dimensions in Slo order.  MSD path: the Shi chain runs
 // on a side stream concurrently with the Slo chain; `st` has joined it on
 // return.  mm[0..3] must hold the [min, max] initial values (init_minmax).
+// What the index keeps: Shi for the rank-form counts (count-only calls), the
+// slo_hi prefix maxima for the walk-form counts (pairs calls); ddm_sub_index_build
+// keeps both.
+enum : int { kNeedShi = 1, kNeedPm = 2 };
+constexpr uint64_t kWalkMinN = 1ull << 20;  // below: rank form (the Shi chain hides on a side stream)
+constexpr double kWalkMaxStab = 4.0;        // walk form while the estimated mean |Stab(a)| is at most this
+
+// levels >= 1 of the block-max tree (+ the prefix maxima when kNeedPm); on
+// the LSB path level 1 was written by gather_key_kernel
+ddm_status tree_async(const Index& I, int need, bool have_lvl1, cudaStream_t st) {
+  const uint64_t n = I.n;
+  int from = have_lvl1 ? 2 : 1;
+  if (need & kNeedPm) {
+    DDM_LAUNCH("tree_pm", 16.0 * n, st, match::tree_pm_kernel<<<(unsigned)I.nb, 256, 0, st>>>(
+        I.slo_hi, n, (!have_lvl1 && I.levels >= 1) ? I.lvl[1] : nullptr, I.levels >= 1 ? I.lvl_n[1] : 0,
+        I.levels >= 2 ? I.lvl[2] : nullptr, I.pmw, I.pmb));
+    DDM_TRY(check_launch());
+    const unsigned chunks = (unsigned)((I.nb + match::kPmChunk - 1) / match::kPmChunk);
+    DDM_LAUNCH("pmb_scan", 8.0 * I.nb, st, match::pmb_chunk_kernel<<<chunks, 1024, 0, st>>>(I.pmb, I.nb, I.pmc));
+    DDM_TRY(check_launch());
+    DDM_LAUNCH("pmb_scan", 16.0 * I.nb, st, match::pmb_scan_kernel<<<chunks, 1024, 0, st>>>(I.pmb, I.nb, I.pmc));
+    DDM_TRY(check_launch());
+    from = 3;
+  }
+  for (int L = from; L <= I.levels; ++L) {
+    DDM_LAUNCH("block_max", 8.0 * I.lvl_n[L - 1], st, match::block_max_kernel<<<grid_for(I.lvl_n[L - 1], 256, 8), 256, 0, st>>>(
+        I.lvl[L - 1], I.lvl_n[L - 1], I.lvl[L]));
+    DDM_TRY(check_launch());
+  }
+  return DDM_OK;
+}
+
 ddm_status build_index_async(const ddm_regions* R, const Index& I, MsdScratch& slo, MsdScratch& shi,
-                             const SortScratch& lsb, uint64_t* mm, Misc* misc, bool use_msd, cudaStream_t st) {
+                             const SortScratch& lsb, uint64_t* mm, Misc* misc, bool use_msd, cudaStream_t st,
+                             int need = kNeedShi | kNeedPm) {
   init_attrs_once();
   const uint64_t n = R->n_sub;
   if (n == 0) return DDM_OK;
@@ -675,19 +737,19 @@ ddm_status build_index_async(const ddm_regions* R, const Index& I, MsdScratch& s
     // which reads lo and hi anyway (the sort's key range comes from a sample)
     DDM_TRY(validate_side(R->d, n, R->sub_lo, R->sub_hi, nullptr, nullptr, &misc->err, st, nullptr, nullptr, 1));
     cudaStream_t side[2];
-    DDM_TRY(side_streams(side, st));
-    DDM_TRY(stream_join(side[0], st));
-    // a2 + a3: Slo with the upper key and the id as payload (st) || Shi keys (side stream)
-    DDM_TRY(msd_sort_t<false>(R->sub_hi[0], nullptr, n, mm + 2, I.shi_key, nullptr, nullptr, shi, &misc->overflow,
-                              nullptr, side[0]));
+    const bool with_shi = (need & kNeedShi) != 0;
+    if (with_shi) {
+      DDM_TRY(side_streams(side, st));
+      DDM_TRY(stream_join(side[0], st));
+      // a2: Shi keys on a side stream, concurrent with the Slo chain
+      DDM_TRY(msd_sort_t<false>(R->sub_hi[0], nullptr, n, mm + 2, I.shi_key, nullptr, nullptr, shi, &misc->overflow,
+                                nullptr, side[0]));
+    }
+    // a2 + a3: Slo with the upper key and the id as payload
     DDM_TRY(msd_sort_t<true>(R->sub_lo[0], R->sub_hi[0], n, mm + 0, I.slo_key, I.slo_hi, I.slo_id, slo,
                              &misc->overflow, &misc->err, st));
-    for (int L = 1; L <= I.levels; ++L) {
-      DDM_LAUNCH("block_max", 8.0 * I.lvl_n[L - 1], st, match::block_max_kernel<<<grid_for(I.lvl_n[L - 1], 256, 8), 256, 0, st>>>(
-          I.lvl[L - 1], I.lvl_n[L - 1], I.lvl[L]));
-      DDM_TRY(check_launch());
-    }
-    DDM_TRY(stream_join(st, side[0]));
+    DDM_TRY(tree_async(I, need, false, st));
+    if (with_shi) DDM_TRY(stream_join(st, side[0]));
   } else {
     SortScratch s = lsb_with(lsb, slo);
     DDM_CUDA(cudaMemsetAsync(s.hist[0], 0, sizeof(uint32_t) * 8 * 256, st));
@@ -696,16 +758,13 @@ ddm_status build_index_async(const ddm_regions* R, const Index& I, MsdScratch& s
     const radix::PassList P = full_passes();
     // a2: Slo (key + sub id, encoded from float64 in pass 1), Shi (keys)
     DDM_TRY(radix_sort(R->sub_lo[0], true, nullptr, I.slo_key, I.slo_id, n, P, s.hist[0], true, s, st));
-    DDM_TRY(radix_sort(R->sub_hi[0], true, nullptr, I.shi_key, nullptr, n, P, s.hist[1], true, s, st));
+    if (need & kNeedShi)
+      DDM_TRY(radix_sort(R->sub_hi[0], true, nullptr, I.shi_key, nullptr, n, P, s.hist[1], true, s, st));
     // a3: slo_hi[i] = key(sub_hi[slo_id[i]]) + block maxima
     DDM_LAUNCH("gather_slo_hi", 20.0 * n, st, match::gather_key_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.slo_id, R->sub_hi[0], n,
                                                                                I.slo_hi, I.levels ? I.lvl[1] : nullptr));
     DDM_TRY(check_launch());
-    for (int L = 2; L <= I.levels; ++L) {
-      DDM_LAUNCH("block_max", 8.0 * I.lvl_n[L - 1], st, match::block_max_kernel<<<grid_for(I.lvl_n[L - 1], 256, 8), 256, 0, st>>>(
-          I.lvl[L - 1], I.lvl_n[L - 1], I.lvl[L]));
-      DDM_TRY(check_launch());
-    }
+    DDM_TRY(tree_async(I, need, true, st));
   }
   if (R->d > 1) {
     match::DimPtrs D{};
@@ -743,6 +802,7 @@ struct MatchReq {
   uint64_t capacity;
   uint32_t flags;
   const uint32_t* sub_map = nullptr;  // optional global ids of the subscriptions
+  bool walk = false;                  // walk-form counts (index holds the slo_hi prefix maxima, not Shi)
 };
 
 // Update side, a1 + a2 (+ a3): validate every dimension, sort Ulo with the
@@ -796,13 +856,21 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
                                      (match::kScanThreads * match::kScanItems));
   if (pre) {
   DDM_LAUNCH("count_partition", 0, st, match::count_partition_kernel<<<(unsigned)((ctiles + 255) / 256), 256, 0, st>>>(
-      W.ulo_key, m, I.slo_key, I.shi_key, n, W.part));
+      W.ulo_key, m, I.slo_key, q.walk ? nullptr : I.shi_key, n, W.part));
   DDM_TRY(check_launch());
   // algorithmic bytes: sorted a and b (16 B, gathered b on the LSB path:
-  // 4 B id + ~32 B sector), r_lo / r_b / cnt written (12 B), Slo + Shi read once (16 B)
-  DDM_LAUNCH("count", (use_msd ? 28.0 : 48.0) * m + 16.0 * n, st, match::count_kernel<<<(unsigned)ctiles, match::kCountThreads, sizeof(match::CountSmem), st>>>(
-      W.ulo_key, W.ulo_id, R->upd_hi[0], use_msd ? W.uhi : nullptr, m, I.slo_key, I.shi_key, n, W.part, W.r_lo, W.r_b,
-      W.cnt0, W.tile_sum));
+  // 4 B id + ~32 B sector), r_lo / r_b / cnt written (12 B), Slo + Shi read
+  // once (16 B; walk form: Slo + slo_hi + pmw, 24 B)
+  const double cbytes = (use_msd ? 28.0 : 48.0) * m + (q.walk ? 24.0 : 16.0) * n;
+  const match::CountWalk CW{I.slo_hi, I.pmw, I.pmb, tree_of(I)};
+  if (q.walk)
+    DDM_LAUNCH("count", cbytes, st, match::count_kernel<true><<<(unsigned)ctiles, match::kCountThreads, match::count_smem_bytes(true), st>>>(
+        W.ulo_key, W.ulo_id, R->upd_hi[0], use_msd ? W.uhi : nullptr, m, I.slo_key, nullptr, n, W.part, W.r_lo, W.r_b,
+        W.cnt0, W.tile_sum, CW));
+  else
+    DDM_LAUNCH("count", cbytes, st, match::count_kernel<false><<<(unsigned)ctiles, match::kCountThreads, match::count_smem_bytes(false), st>>>(
+        W.ulo_key, W.ulo_id, R->upd_hi[0], use_msd ? W.uhi : nullptr, m, I.slo_key, I.shi_key, n, W.part, W.r_lo, W.r_b,
+        W.cnt0, W.tile_sum, CW));
   DDM_TRY(check_launch());
   }
   if (pre && d == 1) {
@@ -967,7 +1035,7 @@ bool graphs_enabled() {
     const char* e = getenv("DDM_GRAPHS");
     return e && atoi(e) == 0;
   }();
-  return !off && chains_concurrent();
+  return !off && !serial_env() && !g_prof.on;
 }
 
 template <typename T>
@@ -1113,8 +1181,30 @@ static ddm_status match_full(const ddm_regions* R, ddm_pair* pairs, uint64_t cap
   MatchWs W = match_layout(R->d, R->n_sub, R->n_upd, base + a256(I.bytes), true);
   MatchReq q{&I, R, upd_map, pairs, capacity, flags, sub_map};
   const bool lsb_only = (flags & DDM_SORT_LSB) != 0;
+  // count form (ddm.h DDM_COUNT_RANKS / DDM_COUNT_WALK): d > 1 always ranks
+  // (its dim-0 candidates outnumber the pairs); d = 1 pairs calls walk when
+  // forced, or when the probe finds sparse stab sets on a big input (the
+  // walk replaces the Shi sort, ~1/3 of the sort traffic)
+  bool walk = false;
+  if (pairs && R->d == 1 && !(flags & DDM_COUNT_RANKS)) {
+    if (flags & DDM_COUNT_WALK) walk = true;
+    else if (R->n_sub >= kWalkMinN && R->n_upd > 0) {
+      double est = INFINITY;
+      DDM_LAUNCH("stab_probe", 0, st, match::stab_density_kernel<<<1, 256, 0, st>>>(R->sub_lo[0], R->sub_hi[0], R->n_sub,
+                                                                                   W.probe));
+      DDM_TRY(check_launch());
+      DDM_CUDA(cudaMemcpyAsync(&est, W.probe, sizeof(double), cudaMemcpyDeviceToHost, st));
+      DDM_CUDA(cudaStreamSynchronize(st));
+      walk = est <= kWalkMaxStab;
+    }
+  }
+  const uint32_t key_flags = (flags & ~(uint32_t)(DDM_COUNT_RANKS | DDM_COUNT_WALK)) |
+                             (walk ? DDM_COUNT_WALK : DDM_COUNT_RANKS);
+  const OneChain one_chain(walk);
   for (int attempt = lsb_only ? 1 : 0; attempt < 2; ++attempt) {
     const bool use_msd = attempt == 0;
+    const int need = walk ? kNeedPm : kNeedShi;
+    q.walk = need == kNeedPm;
     auto pre = [&](cudaStream_t s) -> ddm_status {
       DDM_CUDA(cudaMemsetAsync(W.misc, 0, sizeof(Misc), s));
       DDM_TRY(init_minmax(W.mm, s));
@@ -1125,17 +1215,17 @@ static ddm_status match_full(const ddm_regions* R, ddm_pair* pairs, uint64_t cap
         DDM_TRY(side_streams(side, s));
         DDM_TRY(stream_join(side[1], s));
         DDM_TRY(upd_sort_async(R, W, R->n_sub, true, side[1]));
-        DDM_TRY(build_index_async(R, I, W.slo, W.shi, W.sort, W.mm, W.misc, true, s));
+        DDM_TRY(build_index_async(R, I, W.slo, W.shi, W.sort, W.mm, W.misc, true, s, need));
         DDM_TRY(stream_join(s, side[1]));
       } else {
-        DDM_TRY(build_index_async(R, I, W.slo, W.shi, W.sort, W.mm, W.misc, false, s));
+        DDM_TRY(build_index_async(R, I, W.slo, W.shi, W.sort, W.mm, W.misc, false, s, need));
         DDM_TRY(upd_sort_async(R, W, R->n_sub, false, s));
       }
       return match_sorted(q, W, count_out, use_msd, s, kPhasePre);
     };
     init_attrs_once();
     if (use_msd && graphs_enabled())
-      DDM_TRY(run_cached(graph_key(R, ws, ws_bytes, flags, pairs != nullptr, sub_map, upd_map, st), pre, st));
+      DDM_TRY(run_cached(graph_key(R, ws, ws_bytes, key_flags, pairs != nullptr, sub_map, upd_map, st), pre, st));
     else
       DDM_TRY(pre(st));
     const ddm_status r = match_sorted(q, W, count_out, use_msd, st, kPhasePost);
@@ -1198,6 +1288,8 @@ static ddm_status indexed_common(const void* index, const ddm_regions* upds, con
   Index I = index_layout(upds->d, upds->n_sub, const_cast<void*>(index));
   MatchWs W = match_layout(upds->d, upds->n_sub, upds->n_upd, ws, false);
   MatchReq q{&I, upds, upd_ids, pairs, capacity, flags};
+  // the index keeps both Shi and the prefix maxima; ranks are cheaper here
+  q.walk = pairs && upds->d == 1 && (flags & DDM_COUNT_WALK) && !(flags & DDM_COUNT_RANKS);
   for (int attempt = (flags & DDM_SORT_LSB) ? 1 : 0; attempt < 2; ++attempt) {
     const bool use_msd = attempt == 0;
     DDM_CUDA(cudaMemsetAsync(W.misc, 0, sizeof(Misc), st));

@@ -14,6 +14,7 @@
 // the set Alg. 4 reports; rows are ordered by the sweep order of
 // update lower endpoints and each row by Slo order (deterministic).
 #pragma once
+#include <cstddef>
 #include "common.cuh"
 
 namespace ddm {
@@ -149,6 +150,176 @@ __global__ void __launch_bounds__(256) block_max_kernel(const uint64_t* __restri
   }
 }
 
+// a3' (pairs mode): levels 1 and 2 of the block-max tree and the prefix
+// maxima of the Slo upper keys, in one read of slo_hi.  With 1024-entry
+// blocks, pmw[i] = max(slo_hi[1024*(i/1024) .. i]) and, after
+// pmb_scan_kernel, pmb[B] = max(slo_hi[0 .. 1024*B)), so
+//   max(slo_hi[0..i]) = max(pmw[i], pmb[i/1024])
+// which is the stop test of the counting stab walk (count_kernel<true>):
+// no position at or before i can hold a member of Stab(a) once it is < a.
+// lvl1 / lvl2 may be nullptr (not kept, or the tree has fewer levels).
+constexpr int kPmBlock = 1024;
+__global__ void __launch_bounds__(256) tree_pm_kernel(const uint64_t* __restrict__ hi, uint64_t n,
+                                                      uint64_t* __restrict__ lvl1, uint64_t n1,
+                                                      uint64_t* __restrict__ lvl2, uint64_t* __restrict__ pmw,
+                                                      uint64_t* __restrict__ pmb) {
+  __shared__ uint64_t wt[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t B = blockIdx.x;
+  const uint64_t base = B * kPmBlock + (uint64_t)threadIdx.x * 4;
+  uint64_t v[4];
+  if (base + 4 <= n) {
+    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(hi + base);
+    const ulonglong2 x = __ldcs(p), y = __ldcs(p + 1);
+    v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = base + k < n ? __ldcs(hi + base + k) : 0;
+  }
+#pragma unroll
+  for (int k = 1; k < 4; ++k) v[k] = v[k] > v[k - 1] ? v[k] : v[k - 1];  // running max
+  const uint64_t t = v[3];
+  uint64_t inc = t;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t w = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o && w > inc) inc = w;
+  }
+  uint64_t excl = __shfl_up_sync(kFull, inc, 1);
+  if (lane == 0) excl = 0;
+  if (lvl1) {  // 32 entries = 8 threads
+    uint64_t g = t;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const uint64_t w = __shfl_xor_sync(kFull, g, o);
+      g = w > g ? w : g;
+    }
+    const uint64_t idx = B * (kPmBlock / 32) + (threadIdx.x >> 3);
+    if ((lane & 7) == 0 && idx < n1) lvl1[idx] = g;
+  }
+  if (lane == 31) wt[warp] = inc;
+  __syncthreads();
+  uint64_t pre = excl;
+  for (int w = 0; w < warp; ++w) pre = wt[w] > pre ? wt[w] : pre;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v[k] = v[k] > pre ? v[k] : pre;
+  if (base + 4 <= n) {
+    ulonglong2* q = reinterpret_cast<ulonglong2*>(pmw + base);
+    q[0] = make_ulonglong2(v[0], v[1]);
+    q[1] = make_ulonglong2(v[2], v[3]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (base + k < n) pmw[base + k] = v[k];
+  }
+  if (threadIdx.x == 255) {  // the block maximum (v[3] of the last thread)
+    pmb[B] = v[3];
+    if (lvl2) lvl2[B] = v[3];
+  }
+}
+
+// Stab-density probe (pairs calls, d = 1): an estimate of the mean
+// |Stab(a)| at a uniform point, n * mean(hi - lo) / (max lo - min lo) over
+// 4096 evenly spaced subscriptions; +inf when a sampled value is non-finite
+// (the validation reports it).  One CTA.
+constexpr int kProbe = 4096;
+__global__ void __launch_bounds__(256) stab_density_kernel(const double* __restrict__ lo,
+                                                           const double* __restrict__ hi, uint64_t n,
+                                                           double* __restrict__ out) {
+  __shared__ double s_len[8], s_min[8], s_max[8];
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  double len = 0.0, mn = INFINITY, mx = -INFINITY;
+  int bad = 0;
+  for (int k = threadIdx.x; k < kProbe; k += blockDim.x) {
+    const uint64_t i = (uint64_t)((unsigned __int128)k * n / kProbe);
+    const double a = lo[i], b = hi[i];
+    if (!isfinite(a) || !isfinite(b)) { bad = 1; continue; }
+    len += b > a ? b - a : 0.0;
+    mn = fmin(mn, a);
+    mx = fmax(mx, a);
+  }
+  for (int o = 16; o; o >>= 1) {
+    len += __shfl_xor_sync(kFull, len, o);
+    mn = fmin(mn, __shfl_xor_sync(kFull, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
+  }
+  if (bad) s_bad = 1;
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { s_len[w] = len; s_min[w] = mn; s_max[w] = mx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < 8; ++k) { len += s_len[k]; mn = fmin(mn, s_min[k]); mx = fmax(mx, s_max[k]); }
+    const double span = mx - mn;
+    const double mean = len / (double)kProbe;
+    out[0] = (s_bad || !(span > 0.0)) ? INFINITY : (double)n * mean / span;
+  }
+}
+
+// Exclusive max-scan of the nb block maxima, in place: chunks of
+// kPmChunk = 8192 blocks; pmb_chunk_kernel writes each chunk's maximum,
+// pmb_scan_kernel scans a chunk after taking the maximum of the chunks
+// before it (at most nb / 8192 values).
+constexpr int kPmChunk = 8192;
+__global__ void __launch_bounds__(1024) pmb_chunk_kernel(const uint64_t* __restrict__ pmb, uint64_t nb,
+                                                         uint64_t* __restrict__ cmax) {
+  __shared__ uint64_t wt[32];
+  const uint64_t c0 = (uint64_t)blockIdx.x * kPmChunk;
+  uint64_t mx = 0;
+#pragma unroll
+  for (int k = 0; k < kPmChunk / 1024; ++k) {
+    const uint64_t i = c0 + (uint64_t)k * 1024 + threadIdx.x;
+    const uint64_t x = i < nb ? pmb[i] : 0;
+    mx = x > mx ? x : mx;
+  }
+  mx = warp_max_u64(mx);
+  if ((threadIdx.x & 31) == 0) wt[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    mx = warp_max_u64(wt[threadIdx.x]);
+    if (threadIdx.x == 0) cmax[blockIdx.x] = mx;
+  }
+}
+
+__global__ void __launch_bounds__(1024) pmb_scan_kernel(uint64_t* __restrict__ pmb, uint64_t nb,
+                                                        const uint64_t* __restrict__ cmax) {
+  __shared__ uint64_t wt[33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t c0 = (uint64_t)blockIdx.x * kPmChunk;
+  constexpr int E = kPmChunk / 1024;  // 8 consecutive blocks per thread
+  const uint64_t b0 = c0 + (uint64_t)threadIdx.x * E;
+  uint64_t v[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) v[k] = b0 + k < nb ? pmb[b0 + k] : 0;
+  uint64_t pre = 0;  // maximum of the chunks before this one
+  if (warp == 0) {
+    for (uint32_t c = lane; c < blockIdx.x; c += 32) pre = cmax[c] > pre ? cmax[c] : pre;
+    pre = warp_max_u64(pre);
+    if (lane == 0) wt[32] = pre;
+  }
+  uint64_t mx = 0;
+#pragma unroll
+  for (int k = 0; k < E; ++k) mx = v[k] > mx ? v[k] : mx;
+  uint64_t inc = mx;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t w = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o && w > inc) inc = w;
+  }
+  uint64_t excl = __shfl_up_sync(kFull, inc, 1);
+  if (lane == 0) excl = 0;
+  if (lane == 31) wt[warp] = inc;
+  __syncthreads();
+  excl = wt[32] > excl ? wt[32] : excl;
+  for (int w = 0; w < warp; ++w) excl = wt[w] > excl ? wt[w] : excl;
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    if (b0 + k < nb) pmb[b0 + k] = excl;
+    excl = v[k] > excl ? v[k] : excl;
+  }
+}
+
 // Other dimensions of the subscriptions, gathered into Slo order (d > 1):
 // out[(k-1)*2*n + 0*n + i] = lo_k[idx[i]], out[(k-1)*2*n + n + i] = hi_k[idx[i]].
 struct DimPtrs {
@@ -156,7 +327,7 @@ struct DimPtrs {
   const double* hi[8];
 };
 
-__global__ void __launch_bounds__(256) gather_dims_kernel(const uint32_t* __restrict__ idx, DimPtrs src,
+__global__ void __launch_bounds__(256) gather_dims_kernel(const uint32_t* __restrict__ idx, const __grid_constant__ DimPtrs src,
                                                           int d, uint64_t n, double* __restrict__ out,
                                                           const uint32_t* __restrict__ abort_flag) {
   if (abort_flag && *abort_flag) return;  // MSD bucket overflow: idx is not a permutation, attempt discarded
@@ -263,6 +434,21 @@ constexpr int kCountTile = kCountThreads * kCountItems;
 constexpr int kCountWin = 3072;  // smem window (keys) per sorted array
 constexpr int kCountExt = 1024;  // Slo window extension past r_lo(a_last) for the r_b searches
 constexpr int kRowTile = 256;    // rows per emit CTA == granularity of the row-offset scan
+// Stab-part scans walk Slo backwards from r_lo - 1 and stop after exactly
+// |Stab(a)| = r_lo - r_hi members.  Aligned runs of 32^L positions whose
+// block maximum of upper keys is < a hold no member and are skipped, so the
+// cost is output-sensitive even with a few very long intervals.
+__device__ __forceinline__ int skip_levels(const MaxTree& T, int64_t i, uint64_t a) {
+  int L = 0;
+  while (L < T.levels) {
+    const int sh = 5 * (L + 1);
+    if ((((uint64_t)i + 1) & ((1ull << sh) - 1)) != 0) break;
+    if (T.lvl[L + 1][(uint64_t)i >> sh] >= a) break;
+    ++L;
+  }
+  return L;
+}
+
 static_assert(kCountTile % kRowTile == 0, "count tile holds whole row tiles");
 
 // Per count tile: r_lo(a_first), r_lo(a_last), r_hi(a_first), r_hi(a_last)
@@ -278,15 +464,20 @@ __global__ void __launch_bounds__(256) count_partition_kernel(const uint64_t* __
   const uint64_t af = ulo_key[j0], al = ulo_key[j1];
   part[4 * t + 0] = ub(slo_key, 0, n, af);
   part[4 * t + 1] = ub(slo_key, 0, n, al);
-  part[4 * t + 2] = lb(shi_key, 0, n, af);
-  part[4 * t + 3] = lb(shi_key, 0, n, al);
+  part[4 * t + 2] = shi_key ? lb(shi_key, 0, n, af) : 0;  // (walk form: no Shi)
+  part[4 * t + 3] = shi_key ? lb(shi_key, 0, n, al) : 0;
 }
 
+constexpr int kWalkPad = 256;  // walk form: slo_hi / pmw windows start this far before r_lo(a_first)
 struct CountSmem {
-  alignas(16) uint64_t ws[kCountWin + 2];  // +2: the bulk copies start at an even (16-byte) index
-  alignas(16) uint64_t wh[kCountWin + 2];
   uint64_t bar;
+  uint64_t pad_;
+  alignas(16) uint64_t ws[kCountWin + 2];  // Slo window; +2: the bulk copies start at an even (16-byte) index
+  alignas(16) uint64_t wh[kCountWin + 2];  // Shi window (rank form) / slo_hi window (walk form)
+  alignas(16) uint64_t wp[kCountWin + 2];  // pmw window (walk form only)
 };
+// dynamic shared memory of count_kernel<WALK>
+constexpr size_t count_smem_bytes(bool walk) { return walk ? sizeof(CountSmem) : offsetof(CountSmem, wp); }
 
 // First window position at or after k whose entry is "after" x (> x for
 // UPPER, >= x otherwise), given every entry before k is not: gallop forward
@@ -319,27 +510,82 @@ __device__ __forceinline__ uint32_t wseek(const uint64_t* W, uint32_t k, uint32_
 template <bool UPPER>
 __device__ __forceinline__ uint64_t advance(const uint64_t* W, uint64_t base, uint32_t len, const uint64_t* g,
                                             uint64_t n, uint64_t pos, uint64_t x) {
-  const uint32_t k = pos >= base ? (uint32_t)umin64(pos - base, len) : 0;
-  const uint32_t r = wseek<UPPER>(W, k, len, x);
+  uint32_t k = pos >= base ? (uint32_t)umin64(pos - base, len) : 0;
+  // cursors of consecutive sorted queries usually move by 0..2 entries: a
+  // short linear scan first, the gallop only for longer moves
+  uint32_t r = len;
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    if (k >= len) break;
+    const uint64_t v = W[k];
+    if (UPPER ? v > x : v >= x) { r = k; break; }
+    ++k;
+  }
+  if (r == len && k < len) r = wseek<UPPER>(W, k, len, x);
   if (r < len) return base + r;
   if (base + len >= n) return n;
   return UPPER ? ub_gallop(g, n, base + len, x) : gallop_lb(g, n, base + len, x);
 }
 
 // a4 (G5): for every update j (sorted Ulo order) r_lo = #{S.lo <= a},
-// r_b = #{S.lo <= b} and cnt = r_b - r_hi with r_hi = #{S.hi < a} (the rank
-// difference of I2).  b_j = key(upd_hi[ulo_id[j]]) is gathered here (a3).
+// r_b = #{S.lo <= b} and cnt = |Stab(a)| + (r_b - r_lo).  b_j =
+// key(upd_hi[ulo_id[j]]) is gathered here on the LSB path (a3).
+//  - rank form (WALK = false; count-only calls, the paper's K-independent
+//    count mode): |Stab(a)| = r_lo - r_hi with r_hi = #{S.hi < a} from the
+//    sorted Shi (the rank difference of I2);
+//  - walk form (WALK = true; pairs calls, whose emission is O(K) anyway):
+//    |Stab(a)| counted by walking Slo backwards from r_lo - 1 until the
+//    prefix maximum of slo_hi drops below a (tree_pm_kernel), skipping
+//    aligned blocks whose maximum is < a -- so no Shi sort is needed.
 // Each thread owns 8 consecutive updates: a binary search locates its first
-// one in the tile's staged Slo/Shi windows, then the cursors only move
-// forward (a is sorted: a merge path).  Also writes the count sum of every
-// 256-row tile (for the row-offset scan, a5).
-__global__ void __launch_bounds__(kCountThreads, 4) count_kernel(
+// one in the tile's staged windows, then the cursors only move forward (a is
+// sorted: a merge path).  Also writes the count sum of every 256-row tile
+// (for the row-offset scan, a5).
+struct CountWalk {  // walk form inputs
+  const uint64_t* slo_hi;
+  const uint64_t* pmw;
+  const uint64_t* pmb;
+  MaxTree T;
+};
+
+// One step of the counting stab walk of a row at position i (walking down):
+// returns false once max(slo_hi[0..i]) < a (nothing at or before i can be a
+// member), else counts i, or skips an aligned block whose maximum is < a.
+// WP holds the full prefix maxima of the staged slice [q0, q0 + lq) (the
+// window fix-up folds pmb in); outside it, pmw and pmb from global memory.
+__device__ __forceinline__ bool walk_step(const uint64_t* WH, const uint64_t* WP, uint64_t q0, uint32_t lq,
+                                          const CountWalk& C, int64_t& i, uint64_t a, uint32_t& s) {
+  if (i < 0) return false;
+  const uint64_t u = (uint64_t)i;
+  const bool in = u - q0 < lq;  // (wraps for u < q0)
+  uint64_t p, h;
+  if (in) {
+    p = WP[u - q0];
+    h = WH[u - q0];
+  } else {
+    p = __ldg(C.pmw + u);
+    const uint64_t pb = __ldg(C.pmb + (u >> 10));
+    p = pb > p ? pb : p;
+    h = __ldg(C.slo_hi + u);
+  }
+  if (p < a) return false;
+  if (h >= a) ++s;
+  else if (((u + 1) & 31) == 0) {  // (a member's own block cannot be skipped)
+    const int L = skip_levels(C.T, i, a);
+    if (L) { i -= (int64_t)1 << (5 * L); return true; }
+  }
+  --i;
+  return true;
+}
+
+template <bool WALK>
+__global__ void __launch_bounds__(kCountThreads, WALK ? 3 : 4) count_kernel(
     const uint64_t* __restrict__ ulo_key, const uint32_t* __restrict__ ulo_id, const double* __restrict__ upd_hi,
     const uint64_t* __restrict__ uhi, uint64_t m, const uint64_t* __restrict__ slo_key, const uint64_t* __restrict__ shi_key, uint64_t n,
     const uint64_t* __restrict__ part, uint32_t* __restrict__ r_lo_out, uint32_t* __restrict__ r_b_out,
-    uint32_t* __restrict__ cnt_out, uint64_t* __restrict__ row_tile_sum) {
+    uint32_t* __restrict__ cnt_out, uint64_t* __restrict__ row_tile_sum, const __grid_constant__ CountWalk C) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  CountSmem& S = *reinterpret_cast<CountSmem*>(smem_raw);
+  CountSmem& S = *reinterpret_cast<CountSmem*>(smem_raw);  // wp unused by the rank form
   const int tid = threadIdx.x;
   const uint32_t tile = blockIdx.x;
   const uint64_t j0 = (uint64_t)tile * kCountTile;
@@ -381,23 +627,37 @@ __global__ void __launch_bounds__(kCountThreads, 4) count_kernel(
     for (int i = 0; i < kCountItems; ++i) b[i] = f64_key(hv[i]);
   }
   const uint32_t ls = (uint32_t)umin64(umin64(kCountWin, p1 - p0 + kCountExt), n - p0);
-  const uint32_t lh = (uint32_t)umin64(kCountWin, umin64(h1 - h0 + 1, n - h0));
-  // the two windows arrive by bulk async copies (TMA engine) from 16-byte
+  // rank form: the Shi window from r_hi(a_first); walk form: the slo_hi and
+  // pmw windows from kWalkPad entries before r_lo(a_first)
+  const uint64_t q0 = WALK ? (p0 > kWalkPad ? p0 - kWalkPad : 0) : h0;
+  const uint32_t lh = WALK ? (uint32_t)umin64(kCountWin, n - q0)
+                           : (uint32_t)umin64(kCountWin, umin64(h1 - h0 + 1, n - h0));
+  // the windows arrive by bulk async copies (TMA engine) from 16-byte
   // aligned starts, tracked by one mbarrier; the threads' own loads of a and
   // b above are in flight meanwhile.  Reading up to one key past the array is
   // safe: every sorted key array is followed by another workspace array.
-  const uint32_t os = (uint32_t)(p0 & 1), oh = (uint32_t)(h0 & 1);
+  const uint32_t os = (uint32_t)(p0 & 1), oh = (uint32_t)(q0 & 1);
   const uint64_t* W0 = S.ws + os;
   const uint64_t* H0 = S.wh + oh;
+  const uint64_t* P0 = S.wp + oh;
   if (tid == 0) {
     mbar_init(&S.bar, 1);
     const uint32_t bs = ((ls + os + 1) & ~1u) * 8, bh = ((lh + oh + 1) & ~1u) * 8;
-    mbar_expect_tx(&S.bar, bs + bh);
+    mbar_expect_tx(&S.bar, bs + (WALK ? 2 : 1) * bh);
     if (bs) bulk_g2s(S.ws, slo_key + (p0 - os), bs, &S.bar);
-    if (bh) bulk_g2s(S.wh, shi_key + (h0 - oh), bh, &S.bar);
+    if (bh) bulk_g2s(S.wh, (WALK ? C.slo_hi : shi_key) + (q0 - oh), bh, &S.bar);
+    if (WALK && bh) bulk_g2s(S.wp, C.pmw + (q0 - oh), bh, &S.bar);
   }
   __syncthreads();  // the barrier is initialised before anyone waits on it
   mbar_wait(&S.bar, 0);
+  if (WALK) {  // fold the block prefixes in: WP[k] = max(slo_hi[0 .. q0 + k])
+    uint64_t* P = S.wp + oh;
+    for (uint32_t k = tid; k < lh; k += kCountThreads) {
+      const uint64_t pb = __ldg(C.pmb + ((q0 + k) >> 10));
+      if (pb > P[k]) P[k] = pb;
+    }
+    __syncthreads();
+  }
 
   uint32_t cnt[kCountItems];
 #pragma unroll
@@ -406,8 +666,9 @@ __global__ void __launch_bounds__(kCountThreads, 4) count_kernel(
     // first update: binary search inside the windows (falls back to global)
     uint64_t rl = advance<true>(W0, p0, ls, slo_key, n,
                                 p0 + ((ls && W0[ls - 1] > a[0]) ? ub(W0, 0, ls, a[0]) : ls), a[0]);
-    uint64_t rh = advance<false>(H0, h0, lh, shi_key, n,
-                                 h0 + ((lh && H0[lh - 1] >= a[0]) ? lb(H0, 0, lh, a[0]) : lh), a[0]);
+    uint64_t rh = 0;
+    if (!WALK)
+      rh = advance<false>(H0, h0, lh, shi_key, n, h0 + ((lh && H0[lh - 1] >= a[0]) ? lb(H0, 0, lh, a[0]) : lh), a[0]);
     uint64_t rb = rl;
     uint32_t ol[kCountItems], ob[kCountItems];
 #pragma unroll
@@ -415,13 +676,29 @@ __global__ void __launch_bounds__(kCountThreads, 4) count_kernel(
       if (i < ni) {
         if (i) {
           rl = advance<true>(W0, p0, ls, slo_key, n, rl, a[i]);
-          rh = advance<false>(H0, h0, lh, shi_key, n, rh, a[i]);
+          if (!WALK) rh = advance<false>(H0, h0, lh, shi_key, n, rh, a[i]);
         }
         const uint64_t start = (i && b[i] >= b[i - 1] && rb > rl) ? rb : rl;
         rb = advance<true>(W0, p0, ls, slo_key, n, start, b[i]);
         ol[i] = (uint32_t)rl;
         ob[i] = (uint32_t)rb;
-        cnt[i] = (uint32_t)(rb > rh ? rb - rh : 0);
+        if (WALK) cnt[i] = (uint32_t)(rb - rl);
+        else cnt[i] = (uint32_t)(rb > rh ? rb - rh : 0);
+      }
+    }
+    if (WALK) {  // the rows' stab walks, interleaved (independent loads in flight)
+      int64_t pos[kCountItems];
+      unsigned act = 0;
+#pragma unroll
+      for (int i = 0; i < kCountItems; ++i) {
+        pos[i] = (int64_t)ol[i] - 1;
+        if (i < ni) act |= 1u << i;
+      }
+      while (act) {
+#pragma unroll
+        for (int i = 0; i < kCountItems; ++i)
+          if ((act >> i) & 1u)
+            if (!walk_step(H0, P0, q0, lh, C, pos[i], a[i], cnt[i])) act &= ~(1u << i);
       }
     }
     if (ni == kCountItems) {
@@ -497,21 +774,6 @@ __global__ void __launch_bounds__(kScanThreads) scan_u64_kernel(const uint64_t* 
 }
 
 // ------------------------------------------------------------ sweep + emit (a6 + a7, a8)
-
-// Stab-part scans walk Slo backwards from r_lo - 1 and stop after exactly
-// |Stab(a)| = r_lo - r_hi members.  Aligned runs of 32^L positions whose
-// block maximum of upper keys is < a hold no member and are skipped, so the
-// cost is output-sensitive even with a few very long intervals.
-__device__ __forceinline__ int skip_levels(const MaxTree& T, int64_t i, uint64_t a) {
-  int L = 0;
-  while (L < T.levels) {
-    const int sh = 5 * (L + 1);
-    if ((((uint64_t)i + 1) & ((1ull << sh) - 1)) != 0) break;
-    if (T.lvl[L + 1][(uint64_t)i >> sh] >= a) break;
-    ++L;
-  }
-  return L;
-}
 
 struct Filter {  // d > 1: dims 1..d-1 of the subs in Slo order + the query box
   int dims;      // d - 1 (0 for d == 1)
@@ -715,7 +977,7 @@ __device__ __forceinline__ void row_warp(const EmitArgs& A, uint64_t j, uint64_t
 // by whole warps, so both sparse (alpha ~ 1: ~1 pair per row) and dense rows
 // (alpha = 100: ~100 pairs per row) stream coalesced stores.
 template <int MODE>
-__global__ void __launch_bounds__(kRowTile) emit_kernel(EmitArgs A) {
+__global__ void __launch_bounds__(kRowTile) emit_kernel(const __grid_constant__ EmitArgs A) {
   __shared__ RowSmem R;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t j0 = (uint64_t)blockIdx.x * kRowTile;
@@ -758,7 +1020,7 @@ struct EmitTileSmem {
   uint32_t rbmax;
 };
 
-__global__ void __launch_bounds__(kRowTile, 3) emit_tile_kernel(EmitArgs A) {
+__global__ void __launch_bounds__(kRowTile, 3) emit_tile_kernel(const __grid_constant__ EmitArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EmitTileSmem& S = *reinterpret_cast<EmitTileSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -981,7 +1243,7 @@ __device__ __forceinline__ void chunk_row_warp(const ChunkSmem& S, const EmitArg
   for (uint32_t t = in_slice + lane; t < nr; t += 32) rng[t] = make_uint2(sub_out(A.sub_map, A.slo_id[rl + t]), uid);
 }
 
-__global__ void __launch_bounds__(kRowTile) emit_chunk_kernel(EmitArgs A) {
+__global__ void __launch_bounds__(kRowTile) emit_chunk_kernel(const __grid_constant__ EmitArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ChunkSmem& S = *reinterpret_cast<ChunkSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

@@ -25,6 +25,8 @@ DDM_EMIT_FORCE_THREAD = 1 << 8
 DDM_EMIT_FORCE_WARP = 1 << 9
 DDM_EMIT_FORCE_CHUNK = 1 << 10
 DDM_SORT_LSB = 1 << 12
+DDM_COUNT_RANKS = 1 << 13
+DDM_COUNT_WALK = 1 << 14
 
 STATUS = {0: "DDM_OK", 1: "DDM_ERR_INVALID_ARGUMENT", 2: "DDM_ERR_NONFINITE",
           3: "DDM_ERR_INVERTED_INTERVAL", 4: "DDM_ERR_CAPACITY", 5: "DDM_ERR_WORKSPACE",

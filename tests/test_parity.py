@@ -16,7 +16,9 @@ from paper_1703_06680_b200 import workload as wl
 from tests.helpers import cuda, gpu_args, raw_words, words_of
 
 EMIT_FLAGS = [ddm.DDM_EMIT_AUTO, ddm.DDM_EMIT_FORCE_THREAD, ddm.DDM_EMIT_FORCE_WARP, ddm.DDM_EMIT_FORCE_CHUNK,
-              ddm.DDM_SORT_LSB, ddm.DDM_SORT_LSB | ddm.DDM_EMIT_FORCE_CHUNK]
+              ddm.DDM_SORT_LSB, ddm.DDM_SORT_LSB | ddm.DDM_EMIT_FORCE_CHUNK,
+              ddm.DDM_COUNT_WALK, ddm.DDM_COUNT_WALK | ddm.DDM_EMIT_FORCE_CHUNK,
+              ddm.DDM_COUNT_WALK | ddm.DDM_SORT_LSB, ddm.DDM_COUNT_RANKS]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -168,7 +170,7 @@ def test_random_mixtures_fuzz(orc):
         if not ok:
             continue
         ref = orc.bf_pairs(sl, sh, ul, uh)
-        flags = EMIT_FLAGS if case % 4 == 0 else (0,)
+        flags = EMIT_FLAGS if case % 4 == 0 else (0, ddm.DDM_COUNT_WALK)
         check_against(orc, sl, sh, ul, uh, flags=flags, ref=ref)
 
 
@@ -225,6 +227,27 @@ def test_long_intervals(orc):
     sl2, sh2 = w.sub_lo.copy(), w.sub_hi.copy()
     sl2[0, 0], sh2[0, 0] = -1.0, 2e6
     check_against(orc, sl2, sh2, w.upd_lo, w.upd_hi, flags=EMIT_FLAGS)
+
+
+@pytest.mark.parametrize("n", [1, 31, 32, 33, 1023, 1024, 1025, 2049, 40_000])
+def test_stab_walk_prefix_max_blocks(orc, n):
+    """Walk-form counts (pairs calls): the stop test max(pmw[i], pmb[i/1024])
+    < a and the block skips across 32- and 1024-entry boundaries, with long
+    intervals placed just before / after block edges and dense stab sets;
+    against brute force, forced walk vs rank forms (EMIT_FLAGS)."""
+    rng = np.random.default_rng(n)
+    m = max(1, n // 2)
+    sl = np.sort(rng.uniform(0, 1e4, n))[None].copy()
+    sh = sl + rng.exponential(3.0, n)[None]
+    for pos in (0, 31, 32, 1023, 1024, n // 2, n - 1):
+        if pos < n:
+            sh[0, pos] = sl[0, pos] + rng.uniform(100, 5e3)
+    perm = rng.permutation(n)
+    sl, sh = sl[:, perm], sh[:, perm]
+    ul = rng.uniform(-10, 1.1e4, m)[None]
+    uh = ul + rng.exponential(2.0, m)[None]
+    ref = orc.bf_pairs(sl, sh, ul, uh)
+    check_against(orc, sl, sh, ul, uh, flags=EMIT_FLAGS, ref=ref)
 
 
 def test_clamped_mixture_ties(orc):
@@ -296,6 +319,11 @@ def test_c3_full_sampled(orc):
     wds = torch.sort((u << 32) | s).values
     assert bool((wds[1:] > wds[:-1]).all())
     _check_sampled_rows(orc, w, p)
+    # the default picks the walk-form counts here (sparse stab sets); the
+    # rank form writes byte-identical output
+    del s, u, wds
+    p2 = ddm.match_pairs(*g, flags=ddm.DDM_COUNT_RANKS)
+    assert torch.equal(p, p2)
 
 
 def test_c4_scaled(orc):
