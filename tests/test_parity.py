@@ -522,6 +522,38 @@ def test_capacity_and_workspace():
     assert L.ddm_match_count(ctypes.byref(r), ctypes.byref(K), ws.data_ptr(), ws.numel(), None) == 1
 
 
+def test_walk_capacity_and_graph_replay(orc):
+    """Walk-form pairs calls: with capacity < K DDM_ERR_CAPACITY and K,
+    nothing written past capacity; with enough room the output is exact, also
+    on graph replays (second and third identical calls)."""
+    import ctypes
+    L = ddm.load()
+    w = wl.uniform(30_000, 30_000, 1e5, 1.0, 1, seed=3)
+    ref = orc.sbm_seq(w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi)
+    K0 = ref.size
+    g = gpu_args(w)
+    r, keep = ddm.regions(*g)
+    ws = torch.empty(L.ddm_workspace_bytes(1, w.n, w.m, 1), dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    K = ctypes.c_uint64(0)
+    out = torch.empty((K0 + 64, 2), dtype=torch.int32, device="cuda")
+    for cap in (K0 // 2, K0 // 2, K0 // 2):  # eager, capture, replay
+        out.fill_(-7)
+        s_ = L.ddm_match_pairs(ctypes.byref(r), out.data_ptr(), cap, ctypes.byref(K), ddm.DDM_COUNT_WALK,
+                               ws.data_ptr(), ws.numel(), st)
+        torch.cuda.synchronize()
+        assert s_ == 4 and K.value == K0
+        assert bool((out[cap:] == -7).all())
+    for _ in range(3):
+        out.fill_(-7)
+        s_ = L.ddm_match_pairs(ctypes.byref(r), out.data_ptr(), K0, ctypes.byref(K), ddm.DDM_COUNT_WALK,
+                               ws.data_ptr(), ws.numel(), st)
+        torch.cuda.synchronize()
+        assert s_ == 0 and K.value == K0
+        assert np.array_equal(words_of(out[:K0]), ref)
+        assert bool((out[K0:] == -7).all())
+
+
 def test_capacity_dd_never_writes_past_capacity(orc):
     """d > 1 (single fused pass): capacity < K reports DDM_ERR_CAPACITY with the
     exact K and writes nothing at or past `capacity`; then the full call works."""
