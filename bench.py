@@ -399,6 +399,27 @@ def run_ddm(args):
         cpu = {"value": (s.n + s.m) / dt, "unit": "regions/s", "cores": P, "kind": "oracle",
                "sample": f"{sample_text(s, frac)}, K={ks}; {method}, {dt:.2f} s"}
 
+    if roof and roof["kernel"].startswith("dd"):
+        # d > 1 (c4): the filter kernel is issue/latency bound, not HBM bound
+        # (SURVEY F3): roofline of its instruction issue.  achieved = warp
+        # instructions per launch (ncu smsp__inst_executed.sum of the same
+        # launch, profiles/ncu_inst.json) / the live average launch time;
+        # peak = 4 schedulers x SMs x 1 warp instruction per clock at the
+        # maximum SM clock
+        ip = os.path.join(ROOT, "profiles", "ncu_inst.json")
+        inst = json.load(open(ip)).get(args.config, {}).get(roof["kernel"]) if os.path.exists(ip) else None
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        fmax = (clk or {}).get("sm_max_mhz") or 1965.0
+        peak_gi = 4 * sms * fmax * 1e6 / 1e9
+        if inst:
+            ach = inst / (roof["avg_launch_ms"] * 1e-3) / 1e9
+            roof = {"bound": "alu", "kernel": roof["kernel"], "achieved": round(ach, 1), "peak": round(peak_gi, 1),
+                    "unit": "Gwarp-inst/s", "frac": round(ach / peak_gi, 4), "traffic": roof["traffic"],
+                    "peak_source": f"derived: 4 SMSP x {sms} SMs x 1 warp-inst/clk x {fmax:.0f} MHz (DESIGN.md §6)",
+                    "inst_per_launch": inst, "avg_launch_ms": roof["avg_launch_ms"],
+                    "share_of_step": roof["share_of_step"], "measured_in": roof["measured_in"],
+                    "hbm_frac": roof["frac"]}
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "regions/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,

@@ -8,6 +8,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libddm.so")
+# dev A/B only (tools/build_variant.py): load another build of the library
+LIB = os.environ.get("DDM_LIB") or LIB
 SOURCES = ["ddm.cu"]
 HEADERS = ["common.cuh", "radix.cuh", "match.cuh", "msd.cuh", "dd.cuh"]
 

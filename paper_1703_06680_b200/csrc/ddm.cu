@@ -1421,7 +1421,9 @@ int ddm_profile_read(ddm_kernel_stat* out, int cap) {
 }
 
 const char* ddm_build_info(void) {
-  return "libddm sm_100a onesweep-radix(8x8b) count(merge-path, 2048/tile) scan(row tiles) emit(chunk|thread|warp)";
+  return "libddm sm_100a sort(value-bucketed MSD: 8-bit multisplit passes + smem local sort; LSB onesweep fallback) "
+         "count(merge path 2048/tile; rank form | stab walk over slo_hi prefix maxima) scan(decoupled look-back) "
+         "emit(tile window | chunk-start sets | per-row) d>1(tiled cell filter, exact f64 re-test)";
 }
 
 }  // extern "C"
