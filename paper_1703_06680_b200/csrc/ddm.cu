@@ -862,7 +862,7 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
   // 4 B id + ~32 B sector), r_lo / r_b / cnt written (12 B), Slo + Shi read
   // once (16 B; walk form: Slo + slo_hi + pmw, 24 B)
   const double cbytes = (use_msd ? 28.0 : 48.0) * m + (q.walk ? 24.0 : 16.0) * n;
-  const match::CountWalk CW{I.slo_hi, I.pmw, I.pmb, tree_of(I)};
+  const match::CountWalk CW{I.slo_hi, I.pmw, I.pmb, I.nb, tree_of(I)};
   if (q.walk)
     DDM_LAUNCH("count", cbytes, st, match::count_kernel<true><<<(unsigned)ctiles, match::kCountThreads, match::count_smem_bytes(true), st>>>(
         W.ulo_key, W.ulo_id, R->upd_hi[0], use_msd ? W.uhi : nullptr, m, I.slo_key, nullptr, n, W.part, W.r_lo, W.r_b,

@@ -428,8 +428,8 @@ __device__ __forceinline__ uint64_t lookback_warp_u64(uint64_t* status, uint32_t
   return excl;
 }
 
-constexpr int kCountThreads = 256;
-constexpr int kCountItems = 8;
+constexpr int kCountThreads = 512;
+constexpr int kCountItems = 4;  // rows per thread (short dependent merge chains, more warps)
 constexpr int kCountTile = kCountThreads * kCountItems;
 constexpr int kCountWin = 3072;  // smem window (keys) per sorted array
 constexpr int kCountExt = 1024;  // Slo window extension past r_lo(a_last) for the r_b searches
@@ -472,6 +472,8 @@ constexpr int kWalkPad = 256;  // walk form: slo_hi / pmw windows start this far
 struct CountSmem {
   uint64_t bar;
   uint64_t pad_;
+  uint64_t pbw[8];                   // walk form: pmb of the 1024-blocks the windows touch
+  uint64_t tsum[kCountTile / kRowTile];  // per 256-row tile count sums
   alignas(16) uint64_t ws[kCountWin + 2];  // Slo window; +2: the bulk copies start at an even (16-byte) index
   alignas(16) uint64_t wh[kCountWin + 2];  // Shi window (rank form) / slo_hi window (walk form)
   alignas(16) uint64_t wp[kCountWin + 2];  // pmw window (walk form only)
@@ -545,22 +547,25 @@ struct CountWalk {  // walk form inputs
   const uint64_t* slo_hi;
   const uint64_t* pmw;
   const uint64_t* pmb;
+  uint64_t nb;  // entries of pmb
   MaxTree T;
 };
 
 // One step of the counting stab walk of a row at position i (walking down):
 // returns false once max(slo_hi[0..i]) < a (nothing at or before i can be a
 // member), else counts i, or skips an aligned block whose maximum is < a.
-// WP holds the full prefix maxima of the staged slice [q0, q0 + lq) (the
-// window fix-up folds pmb in); outside it, pmw and pmb from global memory.
-__device__ __forceinline__ bool walk_step(const uint64_t* WH, const uint64_t* WP, uint64_t q0, uint32_t lq,
-                                          const CountWalk& C, int64_t& i, uint64_t a, uint32_t& s) {
+// WP holds pmw over the staged slice [q0, q0 + lq) and PB the pmb of the
+// blocks it touches; outside it, pmw and pmb from global memory.
+__device__ __forceinline__ bool walk_step(const uint64_t* WH, const uint64_t* WP, const uint64_t* PB, uint64_t q0,
+                                          uint32_t lq, const CountWalk& C, int64_t& i, uint64_t a, uint32_t& s) {
   if (i < 0) return false;
   const uint64_t u = (uint64_t)i;
   const bool in = u - q0 < lq;  // (wraps for u < q0)
   uint64_t p, h;
   if (in) {
     p = WP[u - q0];
+    const uint64_t pb = PB[(u >> 10) - (q0 >> 10)];
+    p = pb > p ? pb : p;
     h = WH[u - q0];
   } else {
     p = __ldg(C.pmw + u);
@@ -579,7 +584,10 @@ __device__ __forceinline__ bool walk_step(const uint64_t* WH, const uint64_t* WP
 }
 
 template <bool WALK>
-__global__ void __launch_bounds__(kCountThreads, WALK ? 3 : 4) count_kernel(
+#ifndef DDM_COUNT_MINB
+#define DDM_COUNT_MINB 3
+#endif
+__global__ void __launch_bounds__(kCountThreads, DDM_COUNT_MINB) count_kernel(
     const uint64_t* __restrict__ ulo_key, const uint32_t* __restrict__ ulo_id, const double* __restrict__ upd_hi,
     const uint64_t* __restrict__ uhi, uint64_t m, const uint64_t* __restrict__ slo_key, const uint64_t* __restrict__ shi_key, uint64_t n,
     const uint64_t* __restrict__ part, uint32_t* __restrict__ r_lo_out, uint32_t* __restrict__ r_b_out,
@@ -640,6 +648,11 @@ __global__ void __launch_bounds__(kCountThreads, WALK ? 3 : 4) count_kernel(
   const uint64_t* W0 = S.ws + os;
   const uint64_t* H0 = S.wh + oh;
   const uint64_t* P0 = S.wp + oh;
+  if (tid < kCountTile / kRowTile) S.tsum[tid] = 0;
+  if (WALK && tid < 8) {
+    const uint64_t bb = (q0 >> 10) + tid;
+    if (bb < C.nb) S.pbw[tid] = __ldg(C.pmb + bb);
+  }
   if (tid == 0) {
     mbar_init(&S.bar, 1);
     const uint32_t bs = ((ls + os + 1) & ~1u) * 8, bh = ((lh + oh + 1) & ~1u) * 8;
@@ -650,14 +663,6 @@ __global__ void __launch_bounds__(kCountThreads, WALK ? 3 : 4) count_kernel(
   }
   __syncthreads();  // the barrier is initialised before anyone waits on it
   mbar_wait(&S.bar, 0);
-  if (WALK) {  // fold the block prefixes in: WP[k] = max(slo_hi[0 .. q0 + k])
-    uint64_t* P = S.wp + oh;
-    for (uint32_t k = tid; k < lh; k += kCountThreads) {
-      const uint64_t pb = __ldg(C.pmb + ((q0 + k) >> 10));
-      if (pb > P[k]) P[k] = pb;
-    }
-    __syncthreads();
-  }
 
   uint32_t cnt[kCountItems];
 #pragma unroll
@@ -698,32 +703,36 @@ __global__ void __launch_bounds__(kCountThreads, WALK ? 3 : 4) count_kernel(
 #pragma unroll
         for (int i = 0; i < kCountItems; ++i)
           if ((act >> i) & 1u)
-            if (!walk_step(H0, P0, q0, lh, C, pos[i], a[i], cnt[i])) act &= ~(1u << i);
+            if (!walk_step(H0, P0, S.pbw, q0, lh, C, pos[i], a[i], cnt[i])) act &= ~(1u << i);
       }
     }
     if (ni == kCountItems) {
       uint4* dl = reinterpret_cast<uint4*>(r_lo_out + j);
       uint4* db = reinterpret_cast<uint4*>(r_b_out + j);
       uint4* dc = reinterpret_cast<uint4*>(cnt_out + j);
-      dl[0] = make_uint4(ol[0], ol[1], ol[2], ol[3]);
-      dl[1] = make_uint4(ol[4], ol[5], ol[6], ol[7]);
-      db[0] = make_uint4(ob[0], ob[1], ob[2], ob[3]);
-      db[1] = make_uint4(ob[4], ob[5], ob[6], ob[7]);
-      dc[0] = make_uint4(cnt[0], cnt[1], cnt[2], cnt[3]);
-      dc[1] = make_uint4(cnt[4], cnt[5], cnt[6], cnt[7]);
+#pragma unroll
+      for (int h = 0; h < kCountItems / 4; ++h) {
+        dl[h] = make_uint4(ol[4 * h], ol[4 * h + 1], ol[4 * h + 2], ol[4 * h + 3]);
+        db[h] = make_uint4(ob[4 * h], ob[4 * h + 1], ob[4 * h + 2], ob[4 * h + 3]);
+        dc[h] = make_uint4(cnt[4 * h], cnt[4 * h + 1], cnt[4 * h + 2], cnt[4 * h + 3]);
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < kCountItems; ++i)
         if (i < ni) { r_lo_out[j + i] = ol[i]; r_b_out[j + i] = ob[i]; cnt_out[j + i] = cnt[i]; }
     }
   }
-  // per 256-row tile sums (each row tile = 32 consecutive threads = one warp)
+  // per 256-row tile sums (a row tile = kRowTile / kCountItems consecutive threads)
   uint64_t local = 0;
 #pragma unroll
   for (int i = 0; i < kCountItems; ++i) local += cnt[i];
   local = warp_sum<uint64_t>(local);
-  const uint64_t rt = (j0 + (uint64_t)(tid >> 5) * kRowTile);
-  if ((tid & 31) == 0 && rt < m) row_tile_sum[rt / kRowTile] = local;
+  if ((tid & 31) == 0) atomicAdd((unsigned long long*)&S.tsum[(tid * kCountItems) / kRowTile], (unsigned long long)local);
+  __syncthreads();
+  if (tid < kCountTile / kRowTile) {
+    const uint64_t rt = j0 + (uint64_t)tid * kRowTile;
+    if (rt < m) row_tile_sum[rt / kRowTile] = S.tsum[tid];
+  }
 }
 
 // Sum of the counts of each 256-row tile (used after the d > 1 count pass).
