@@ -256,6 +256,7 @@ struct MsdScratch {
   uint32_t* counters;  // [8] tile counters
   uint32_t* ccount;    // [kCoarse + 1] sampled coarse-bin population
   uint32_t* cbase;     // [kCoarse + 2] bucket map
+  uint64_t* bounds;    // [spans + 1] group boundaries of the local sort
   uint64_t* k[2];      // ping-pong record buffers
   uint64_t* v64[2];
   uint32_t* v32[2];
@@ -269,6 +270,7 @@ MsdScratch msd_scratch(Carver& c, uint64_t cap, bool kv) {
   s.counters = c.take<uint32_t>(radix::kMaxPasses);
   s.ccount = c.take<uint32_t>(msd::kCoarse + 1);
   s.cbase = c.take<uint32_t>(msd::kCoarse + 2);
+  s.bounds = c.take<uint64_t>(cap / msd::kSpan + 3);
   for (int i = 0; i < 2; ++i) {
     s.k[i] = c.take<uint64_t>(cap);
     if (kv) {
@@ -632,14 +634,16 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
     DDM_TRY(check_launch());
   }
   const int l = (passes - 1) & 1;
+  DDM_LAUNCH("msd_bounds", 0, st, msd::span_bounds_kernel<<<(spans + 8) / 8, 256, 0, st>>>(bk[l], n, M, bits, spans, s.bounds));
+  DDM_TRY(check_launch());
   if (PAY)
     DDM_LAUNCH("msd_local_pay", 40.0 * n, st, msd::local_sort_kernel<true, true>
                <<<spans, msd::kThreads, sizeof(msd::LocalSmem<true, true>), st>>>(
-                   bk[l], bv[l], bi[l], out_key, out_v64, out_v32, n, M, bits, overflow));
+                   bk[l], bv[l], bi[l], out_key, out_v64, out_v32, n, M, bits, s.bounds, overflow));
   else
     DDM_LAUNCH("msd_local", 16.0 * n, st, msd::local_sort_kernel<false, false>
                <<<spans, msd::kThreads, sizeof(msd::LocalSmem<false, false>), st>>>(
-                   bk[l], nullptr, nullptr, out_key, nullptr, nullptr, n, M, bits, overflow));
+                   bk[l], nullptr, nullptr, out_key, nullptr, nullptr, n, M, bits, s.bounds, overflow));
   return check_launch();
 }
 

@@ -609,26 +609,6 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
   __syncthreads();
 }
 
-// First bucket boundary at or after p (p == 0 or bucket(p) != bucket(p-1)),
-// searching forward in 256-wide windows; n if none.  Whole CTA, uniform.
-__device__ __forceinline__ uint64_t next_boundary(const uint64_t* __restrict__ keys, uint64_t n, uint64_t p,
-                                                  const Bucketer& BK, uint64_t* slot) {
-  if (p == 0) return 0;
-  const int tid = threadIdx.x;
-  if (tid == 0) *slot = ~0ull;
-  __syncthreads();
-  for (uint64_t base = p; base < n; base += kThreads) {
-    const uint64_t q = base + tid;
-    const bool edge = q < n && BK(keys[q]) != BK(keys[q - 1]);
-    if (edge) atomicMin((unsigned long long*)slot, (unsigned long long)q);
-    __syncthreads();
-    const uint64_t r = *slot;
-    __syncthreads();
-    if (r != ~0ull) return r;
-  }
-  return n;
-}
-
 // Last bucket boundary in (lo, hi] scanning backwards; lo if none.
 __device__ __forceinline__ uint64_t prev_boundary(const uint64_t* __restrict__ keys, uint64_t lo, uint64_t hi,
                                                   const Bucketer& BK, uint64_t* slot) {
@@ -647,9 +627,49 @@ __device__ __forceinline__ uint64_t prev_boundary(const uint64_t* __restrict__ k
   return lo;
 }
 
-// CTA c sorts the whole buckets starting in [c*kSpan, (c+1)*kSpan): it finds
-// its first and last bucket boundaries from the (bucket-grouped) keys and
-// sorts groups of consecutive buckets holding <= kCap records in smem.  A
+// bounds[s] = first bucket boundary at or after s*kSpan (s = 0..spans; n past
+// the end), one warp per span over the bucket-grouped keys: each boundary is
+// found once, off the local sort's critical path.  Lane l tests positions
+// base + 4l .. base + 4l + 3 against their predecessors (128 per step).
+__global__ void __launch_bounds__(256) span_bounds_kernel(const uint64_t* __restrict__ keys, uint64_t n,
+                                                          MapRef M, int bits, uint32_t spans,
+                                                          uint64_t* __restrict__ bounds) {
+  Bucketer BK;
+  BK.init(M, bits);
+  const int lane = threadIdx.x & 31;
+  const uint32_t sp = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (sp > spans) return;
+  const uint64_t p = (uint64_t)sp * kSpan;
+  if (sp == 0 || p >= n) {
+    if (lane == 0) bounds[sp] = sp == 0 ? 0 : n;
+    return;
+  }
+  for (uint64_t base = p; base < n; base += 128) {
+    const uint64_t q0 = base + 4 * (uint64_t)lane;
+    uint32_t b[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const uint64_t q = q0 + k - 1;  // q0 - 1 .. q0 + 3
+      b[k] = q < n ? BK(__ldg(keys + q)) : ~0u;
+    }
+    unsigned first = 4;
+#pragma unroll
+    for (int k = 3; k >= 0; --k)
+      if (q0 + k < n && b[k + 1] != b[k]) first = k;
+    const unsigned any = __ballot_sync(kFull, first < 4);
+    if (any) {
+      const int l = __ffs(any) - 1;
+      const unsigned f = __shfl_sync(kFull, first, l);
+      if (lane == 0) bounds[sp] = base + 4 * (uint64_t)l + f;
+      return;
+    }
+  }
+  if (lane == 0) bounds[sp] = n;
+}
+
+// CTA c sorts the whole buckets starting in [c*kSpan, (c+1)*kSpan), i.e. in
+// [bounds[c], bounds[c+1]) (span_bounds_kernel), in groups of consecutive
+// buckets holding <= kCap records in smem.  A
 // single bucket larger than kCap sets *overflow (caller redoes with LSB).
 template <bool V64, bool V32>
 __global__ void __launch_bounds__(kThreads) local_sort_kernel(const uint64_t* __restrict__ k_in,
@@ -659,16 +679,17 @@ __global__ void __launch_bounds__(kThreads) local_sort_kernel(const uint64_t* __
                                                               uint64_t* __restrict__ v64_out,
                                                               uint32_t* __restrict__ v32_out, uint64_t n,
                                                               MapRef M, int bits,
+                                                              const uint64_t* __restrict__ bounds,
                                                               uint32_t* __restrict__ overflow) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocalSmem<V64, V32>& S = *reinterpret_cast<LocalSmem<V64, V32>*>(smem_raw);
   Bucketer BK;
   BK.init(M, bits);
-  if (threadIdx.x == 0) mbar_init(&S.bar, 1);  // (next_boundary's barriers publish it)
+  if (threadIdx.x == 0) mbar_init(&S.bar, 1);
   uint32_t phase = 0;
-  const uint64_t s0 = (uint64_t)blockIdx.x * kSpan;
-  uint64_t e0 = next_boundary(k_in, n, s0, BK, &S.bound[0]);
-  const uint64_t e1 = next_boundary(k_in, n, umin64(s0 + kSpan, n), BK, &S.bound[1]);
+  uint64_t e0 = __ldg(bounds + blockIdx.x);
+  const uint64_t e1 = __ldg(bounds + blockIdx.x + 1);
+  __syncthreads();  // publishes the mbarrier init
   while (e0 < e1) {
     uint64_t g1 = e1;
     if (e1 - e0 > kCap) {
