@@ -547,11 +547,12 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
       const uint32_t b = (uint32_t)((kv - kmin) >> sh);
       const uint32_t lo = b ? S.bin[b - 1] : 0, hi = S.bin[b];
       uint32_t r = lo;
-      for (uint32_t x = lo; x < hi; ++x) {
-        const uint32_t w = S.grp[x];
-        const uint64_t kw = K[w];
-        r += (kw < kv || (kw == kv && w < i)) ? 1u : 0u;
-      }
+      if (hi - lo > 1)  // (a record alone in its bin is at its bin's start)
+        for (uint32_t x = lo; x < hi; ++x) {
+          const uint32_t w = S.grp[x];
+          const uint64_t kw = K[w];
+          r += (kw < kv || (kw == kv && w < i)) ? 1u : 0u;
+        }
       S.perm[r] = (uint16_t)i;
     }
   } else {
