@@ -77,7 +77,9 @@ print("max", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=Tr
 while True:
     try:
         print(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
-              pynvml.nvmlDeviceGetCurrentClocksEventReasons(h), flush=True)
+              pynvml.nvmlDeviceGetCurrentClocksEventReasons(h),
+              pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_MEM),
+              pynvml.nvmlDeviceGetPowerUsage(h), flush=True)
     except pynvml.NVMLError:
         pass
     time.sleep(0.002)
@@ -123,7 +125,7 @@ class Clocks:
             self.p.kill()
         self.f.seek(0)
         lines = self.f.read().splitlines()
-        mx, sm, reasons = None, [], set()
+        mx, sm, mem, pw, reasons = None, [], [], [], set()
         for ln in lines:
             parts = ln.split()
             if parts and parts[0] == "max":
@@ -132,13 +134,18 @@ class Clocks:
             try:
                 sm.append(float(parts[0]))
                 r = int(parts[1])
+                mem.append(float(parts[2]))
+                pw.append(float(parts[3]) / 1000.0)
             except (ValueError, IndexError):
                 continue
             for nm, bit in self.REASONS.items():
                 if r & bit:
                     reasons.add(nm)
         sm = sm[1:] if len(sm) > 1 else sm  # the first sample predates the region
+        mem, pw = mem[1:] if len(mem) > 1 else mem, pw[1:] if len(pw) > 1 else pw
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "mem_mhz": float(np.median(mem)) if mem else None,
+                "power_w": float(np.median(pw)) if pw else None,
                 "samples": len(sm), "source": "NVML child process, 2 ms polling"}
 
 
@@ -286,17 +293,20 @@ def run_ddm(args):
     clocks = Clocks(local)
     clocks.start()
     l0 = ddm.launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     sync_all()
-    e0.record(stream)
-    for _ in range(args.steps):
+    ev[0].record(stream)
+    for i in range(args.steps):
         K = step()
-    e1.record(stream)
+        ev[i + 1].record(stream)  # per-step boundaries (each step ends in its own host sync anyway)
     torch.cuda.synchronize()
     sync_all()
     launches = ddm.launch_count() - l0
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
+    ms = ev[0].elapsed_time(ev[-1])
+    per_step = np.array([ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)])
+    step_stats = {"median": round(float(np.median(per_step)), 4), "p10": round(float(np.percentile(per_step, 10)), 4),
+                  "p90": round(float(np.percentile(per_step, 90)), 4), "mean": round(float(per_step.mean()), 4)}
     # ---- a second timed region of the same K steps with per-kernel CUDA
     # events recorded by the library on each kernel's launching stream
     # (profiling mode runs the concurrent sort chains on one stream so the
@@ -348,8 +358,15 @@ def run_ddm(args):
                   for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["total_ms"])}
         pipeline_frac = tot_bytes / args.steps / (ms_step * 1e-3) / (hbm_peak * 1e9)  # over the official step time
         literal_floor = 16.0 * w.d * regions + 8.0 * K
+        ncu_tot = None
+        if os.path.exists(tp):
+            ncu_tot = json.load(open(tp)).get(args.config, {}).get("_call_total")
         phases_summary = {"pipeline_bytes_per_step": tot_bytes / args.steps,
                           "pipeline_frac_of_peak": round(pipeline_frac, 4),
+                          # ncu DRAM bytes of one whole call (profiles/ncu_traffic.json)
+                          "ncu_bytes_per_step": ncu_tot,
+                          "ncu_frac_of_peak": (round(ncu_tot / (ms_step * 1e-3) / (hbm_peak * 1e9), 4)
+                                               if ncu_tot and world == 1 else None),
                           "literal_floor_bytes": literal_floor,
                           "literal_floor_frac": round(literal_floor / (ms_step * 1e-3) / (hbm_peak * 1e9), 4)}
     else:
@@ -431,6 +448,7 @@ def run_ddm(args):
                                                f"updates sharded by slab x{world}, sub index broadcast (NCCL)"),
                                               "K": K, "timing": "CUDA events on the launching stream, max over ranks"}),
                 "pairs_per_s": K / (ms_step * 1e-3), "regions_per_s_per_gpu": value / world,
+                "step_ms": step_stats,
                 "roofline": roof, "pipeline": phases_summary, "phases": phases, "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": clk, "gpu_launches": launches, "build": ddm.build_info()}
         print(json.dumps(line), flush=True)

@@ -34,5 +34,6 @@ J["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch (bytes, m
               "pairs call in the ncu launch list of `DDM_SERIAL=1 tools/profile_once.py <cfg>` (tools/traffic_json.py), "
               "the configuration of bench.py's profiled region. Used by bench.py's roofline.traffic.")
 J[cfg] = {p: sum(v) / len(v) for p, v in agg.items()}
+J[cfg]["_call_total"] = sum(per[i] for i in ids)  # every kernel of the call (SURVEY §8(d) B_R3)
 json.dump(J, open(out, "w"), indent=1)
 print(json.dumps(J[cfg], indent=1))
