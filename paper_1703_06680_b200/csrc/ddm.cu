@@ -307,6 +307,23 @@ ddm_status side_streams(cudaStream_t out[2], cudaStream_t st) {
   return DDM_OK;
 }
 
+// A side stream even in walk-form (one-chain) calls: only profiling and
+// DDM_SERIAL keep everything on `st`.
+ddm_status side_stream_any(cudaStream_t* out, cudaStream_t st) {
+  if (serial_env() || g_prof.on) {
+    *out = st;
+    return DDM_OK;
+  }
+  int dev = 0;
+  DDM_CUDA_RET(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return DDM_ERR_CUDA;
+  std::lock_guard<std::mutex> lk(g_side_mu);
+  SideStreams& S = g_side[dev];
+  if (!S.s[1]) DDM_CUDA_RET(cudaStreamCreateWithFlags(&S.s[1], cudaStreamNonBlocking));
+  *out = S.s[1];
+  return DDM_OK;
+}
+
 // `to` waits for everything enqueued on `from` so far.
 ddm_status stream_join(cudaStream_t to, cudaStream_t from) {
   if (to == from) return DDM_OK;
@@ -572,16 +589,22 @@ ddm_status radix_sort(const void* src, bool src_f64, const uint32_t* vals_in, ui
 // payload: the upper coordinate `v64_src` (encoded to keys) and the index.
 // mm = the keys' [min, max] (from validation).  Sets *overflow on a bucket
 // too large for shared memory (caller falls back to radix_sort + gather).
+// stages of msd_sort_t: the latency-bound preparation (sample, bucket map,
+// digit histograms) and the record passes + local sort; a walk-form call
+// overlaps one chain's preparation with the other chain's passes
+enum : int { kMsdPrep = 1, kMsdRun = 2, kMsdAll = 3 };
+
 template <bool PAY>
 ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint64_t* mm, uint64_t* out_key,
                       uint64_t* out_v64, uint32_t* out_v32, MsdScratch& s, uint32_t* overflow, uint32_t* err,
-                      cudaStream_t st) {
+                      cudaStream_t st, int stage = kMsdAll) {
   const int bits = msd_bits(n);
   const uint32_t nb = 1u << bits;
   const int passes = (bits + 7) / 8;
+  const msd::MapRef M{mm, s.cbase};
+  if (stage & kMsdPrep) {
   // bucket map equalised to the data (coarse population -> bucket allocation)
   DDM_CUDA(cudaMemsetAsync(s.ccount, 0, sizeof(uint32_t) * (msd::kCoarse + 1), st));
-  const msd::MapRef M{mm, s.cbase};
   const unsigned sgrid = grid_for((n + msd::kSampleStride - 1) / msd::kSampleStride, 512, 4);
   DDM_LAUNCH("msd_sample", 8.0 * n / msd::kSampleStride, st,
              msd::sample_minmax_kernel<true><<<sgrid, 512, 0, st>>>(src, n, mm));
@@ -597,6 +620,8 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
   DDM_TRY(check_launch());
   DDM_LAUNCH("radix_bin_start", 0, st, radix::bin_start_kernel<<<passes, radix::kRadix, 0, st>>>(s.dh, s.starts));
   DDM_TRY(check_launch());
+  }
+  if (!(stage & kMsdRun)) return DDM_OK;
   const uint32_t spans = (uint32_t)((n + msd::kSpan - 1) / msd::kSpan);
   (void)nb;
   uint64_t* bk[2] = {s.k[0], s.k[1]};
@@ -812,17 +837,21 @@ struct MatchReq {
 // Update side, a1 + a2 (+ a3): validate every dimension, sort Ulo with the
 // upper key and the id as payload (MSD) or key + id (LSB fallback).  With
 // n_sub == 0 only the validation runs.  mm[4..5] must hold init values.
-ddm_status upd_sort_async(const ddm_regions* R, MatchWs& W, uint64_t n_sub, bool use_msd, cudaStream_t st) {
+ddm_status upd_sort_async(const ddm_regions* R, MatchWs& W, uint64_t n_sub, bool use_msd, cudaStream_t st,
+                          int stage = kMsdAll) {
   const uint64_t m = R->n_upd;
   const uint32_t d = R->d;
   if (m == 0) return DDM_OK;
   init_attrs_once();
-  if (n_sub == 0) return validate_side(d, m, R->upd_lo, R->upd_hi, nullptr, nullptr, &W.misc->err, st);
+  if (n_sub == 0) return (stage & kMsdPrep) ? validate_side(d, m, R->upd_lo, R->upd_hi, nullptr, nullptr, &W.misc->err, st)
+                                            : DDM_OK;
   if (use_msd) {
-    DDM_TRY(validate_side(d, m, R->upd_lo, R->upd_hi, nullptr, nullptr, &W.misc->err, st, nullptr, nullptr, 1));
+    if (stage & kMsdPrep)
+      DDM_TRY(validate_side(d, m, R->upd_lo, R->upd_hi, nullptr, nullptr, &W.misc->err, st, nullptr, nullptr, 1));
     return msd_sort_t<true>(R->upd_lo[0], R->upd_hi[0], m, W.mm + 4, W.ulo_key, W.uhi, W.ulo_id, W.ulo,
-                            &W.misc->overflow, &W.misc->err, st);
+                            &W.misc->overflow, &W.misc->err, st, stage);
   }
+  if (!(stage & kMsdRun)) return DDM_OK;  // (the LSB path has no separate preparation)
   SortScratch s = lsb_with(W.sort, W.ulo);
   DDM_CUDA(cudaMemsetAsync(s.hist[2], 0, sizeof(uint32_t) * 8 * 256, st));
   DDM_TRY(validate_side(d, m, R->upd_lo, R->upd_hi, s.hist[2], nullptr, &W.misc->err, st));
@@ -1097,6 +1126,7 @@ ddm_status run_cached(const std::string& key, F&& pre, cudaStream_t st) {
     cudaStream_t cs = g_cap_stream[dev];
     cudaStream_t side[2];
     DDM_TRY(side_streams(side, cs));  // created outside the capture
+    DDM_TRY(side_stream_any(&side[1], cs));
     const uint64_t l0 = g_launches.load();
     DDM_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
     const ddm_status r = pre(cs);
@@ -1212,7 +1242,18 @@ static ddm_status match_full(const ddm_regions* R, ddm_pair* pairs, uint64_t cap
     auto pre = [&](cudaStream_t s) -> ddm_status {
       DDM_CUDA(cudaMemsetAsync(W.misc, 0, sizeof(Misc), s));
       DDM_TRY(init_minmax(W.mm, s));
-      if (use_msd) {
+      if (use_msd && walk) {
+        // walk form: the two record chains run one after the other at full
+        // occupancy; the update chain's latency-bound preparation (sample,
+        // bucket map, histograms) overlaps the Slo chain on a side stream
+        cudaStream_t s1;
+        DDM_TRY(side_stream_any(&s1, s));
+        DDM_TRY(stream_join(s1, s));
+        DDM_TRY(upd_sort_async(R, W, R->n_sub, true, s1, kMsdPrep));
+        DDM_TRY(build_index_async(R, I, W.slo, W.shi, W.sort, W.mm, W.misc, true, s, need));
+        DDM_TRY(stream_join(s, s1));
+        DDM_TRY(upd_sort_async(R, W, R->n_sub, true, s, kMsdRun));
+      } else if (use_msd) {
         // the update chain (side stream 1) runs concurrently with the index
         // build (Slo on s, Shi on side stream 0); s joins both before a4
         cudaStream_t side[2];
