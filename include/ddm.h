@@ -165,6 +165,26 @@ ddm_status ddm_match_count_indexed(const void *index, const ddm_regions *upds,
                                    uint64_t *count_out, void *ws, size_t ws_bytes,
                                    cudaStream_t stream);
 
+/* --- Event-order variant: the paper's own parallel
+ * algorithm, Alg. 5 + 6, on the GPU -- an independent
+ * cross-check of ddm_match_pairs, not the fast path.  All 2(n_sub+n_upd)
+ * endpoints of dimension 0 are sorted into one list T by (coord, is_upper,
+ * kind, id) (R1), T is cut into segments of 2048 endpoints (one CTA each);
+ * each segment's initial SubSet / UpdSet (Alg. 6) has its size from an
+ * exclusive scan of per-segment upper-endpoint counts (Alg. 6's combine in
+ * counting form) and its members from a backward walk over T; then every
+ * upper endpoint in the segment reports its pairs with the other kind's
+ * active set (Alg. 5 l.14-16, l.22-24) -- each pair once, at its earlier
+ * upper endpoint.  d > 1: candidates filtered exactly on dims 1..d-1.
+ * Output order: unspecified (atomic appends; canonicalise with
+ * ddm_sort_pairs).  Two passes (count, then emit); *count_out = K; capacity
+ * and validation errors as ddm_match_pairs (nothing written on either).
+ * Regions: device float64 SoA as ddm_match_pairs; ws: 256-byte aligned,
+ * >= ddm_events_workspace_bytes(d, n_sub, n_upd) (~ 60 B per region). */
+size_t ddm_events_workspace_bytes(uint32_t d, uint64_t n_sub, uint64_t n_upd);
+ddm_status ddm_match_pairs_events(const ddm_regions *regions, ddm_pair *pairs, uint64_t capacity,
+                                  uint64_t *count_out, void *ws, size_t ws_bytes, cudaStream_t stream);
+
 /* --- Primitive exported for tests: stable LSB onesweep radix sort of u64
  * keys (device) with optional u32 values, over bits [begin_bit, end_bit).
  * keys_out/vals_out (device) receive the result; inputs are not modified. */

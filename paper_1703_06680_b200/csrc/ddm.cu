@@ -26,6 +26,7 @@
 #include "radix.cuh"
 #include "msd.cuh"
 #include "dd.cuh"
+#include "events.cuh"
 
 using namespace ddm;
 
@@ -450,6 +451,8 @@ void init_attrs_once() {
                        (int)match::count_smem_bytes(false));
   cudaFuncSetAttribute(match::count_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)match::count_smem_bytes(true));
+  cudaFuncSetAttribute(ev::segment_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ev::Smem));
+  cudaFuncSetAttribute(ev::segment_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ev::Smem));
   cudaFuncSetAttribute(match::emit_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(match::ChunkSmem));
   cudaFuncSetAttribute(match::emit_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1358,6 +1361,134 @@ ddm_status ddm_match_pairs_indexed(const void* index, const ddm_regions* upds, c
 ddm_status ddm_match_count_indexed(const void* index, const ddm_regions* upds, uint64_t* count_out, void* ws,
                                    size_t ws_bytes, cudaStream_t stream) {
   return indexed_common(index, upds, nullptr, nullptr, 0, count_out, 0, ws, ws_bytes, stream);
+}
+
+// ------------------------------------------------------------ event-order variant (events.cuh)
+
+struct EvWs {
+  uint64_t N2 = 0, P = 0;
+  uint64_t* key0;
+  uint32_t* code0;
+  uint64_t* tkey;
+  uint32_t* tcode;
+  SortScratch sort;
+  uint32_t* posH;
+  uint64_t* hp;
+  int levels = 0;
+  uint64_t lvl_n[kMaxLevels + 1] = {};
+  uint64_t* lvl[kMaxLevels + 1] = {};
+  uint64_t* seg_uppers;
+  uint64_t* ub;  // uppers before each segment (exclusive scan)
+  uint64_t* scan_status;
+  uint64_t* misc;  // [0] cursor / K, [1] error word
+  size_t bytes = 0;
+};
+
+static EvWs ev_layout(uint64_t n, uint64_t m, void* base) {
+  Carver c(base);
+  EvWs E;
+  E.N2 = 2 * (n + m);
+  E.P = (E.N2 + ev::kSeg - 1) / ev::kSeg;
+  E.misc = c.take<uint64_t>(2);
+  E.key0 = c.take<uint64_t>(E.N2);
+  E.code0 = c.take<uint32_t>(E.N2);
+  E.tkey = c.take<uint64_t>(E.N2);
+  E.tcode = c.take<uint32_t>(E.N2);
+  E.sort = sort_scratch(c, E.N2, true);
+  E.posH = c.take<uint32_t>(n + m);
+  E.hp = c.take<uint64_t>(E.N2);
+  E.lvl[0] = E.hp;
+  E.lvl_n[0] = E.N2;
+  uint64_t sz = E.N2;
+  while (sz > 1 && E.levels < kMaxLevels) {
+    sz = (sz + 31) / 32;
+    ++E.levels;
+    E.lvl_n[E.levels] = sz;
+    E.lvl[E.levels] = c.take<uint64_t>(sz);
+  }
+  E.seg_uppers = c.take<uint64_t>(E.P + 1);
+  E.ub = c.take<uint64_t>(E.P + 1);
+  E.scan_status = c.take<uint64_t>(E.P / (match::kScanThreads * match::kScanItems) + 2);
+  E.bytes = c.used;
+  return E;
+}
+
+extern "C" size_t ddm_events_workspace_bytes(uint32_t d, uint64_t n_sub, uint64_t n_upd) {
+  if (d == 0 || d > DDM_MAX_DIMS) return 0;
+  return ev_layout(n_sub, n_upd, nullptr).bytes;
+}
+
+extern "C" ddm_status ddm_match_pairs_events(const ddm_regions* R, ddm_pair* pairs, uint64_t capacity,
+                                             uint64_t* count_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  DDM_TRY(check_regions(R, true, true));
+  if (!count_out || !aligned(ws, 256) || (pairs && !aligned(pairs, 8))) return DDM_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < ddm_events_workspace_bytes(R->d, R->n_sub, R->n_upd)) return DDM_ERR_WORKSPACE;
+  init_attrs_once();
+  const uint64_t n = R->n_sub, m = R->n_upd;
+  EvWs E = ev_layout(n, m, ws);
+  uint32_t* err = reinterpret_cast<uint32_t*>(E.misc + 1);
+  DDM_CUDA(cudaMemsetAsync(E.misc, 0, 2 * sizeof(uint64_t), st));
+  // a1 on every dimension of both sides
+  DDM_TRY(validate_side(R->d, n, R->sub_lo, R->sub_hi, nullptr, nullptr, err, st));
+  DDM_TRY(validate_side(R->d, m, R->upd_lo, R->upd_hi, nullptr, nullptr, err, st));
+  uint64_t h[2] = {0, 0};
+  if (n && m) {
+    // T: one stable sort of [S lowers | U lowers | S uppers | U uppers] (8 LSB passes)
+    DDM_LAUNCH("ev_build", 16.0 * E.N2, st, ev::build_kernel<<<grid_for(E.N2, 256, 8), 256, 0, st>>>(
+        R->sub_lo[0], R->sub_hi[0], R->upd_lo[0], R->upd_hi[0], n, m, E.key0, E.code0));
+    DDM_TRY(check_launch());
+    DDM_TRY(radix_sort(E.key0, false, E.code0, E.tkey, E.tcode, E.N2, full_passes(), E.sort.hist[0], false, E.sort, st));
+    DDM_LAUNCH("ev_pos", 8.0 * E.N2, st, ev::pos_kernel<<<(unsigned)E.P, 256, 0, st>>>(E.tcode, E.N2, n, E.posH,
+                                                                                       E.seg_uppers));
+    DDM_TRY(check_launch());
+    DDM_LAUNCH("ev_hp", 16.0 * E.N2, st, ev::hp_kernel<<<grid_for(E.N2, 256, 8), 256, 0, st>>>(
+        E.tcode, E.N2, n, E.posH, E.hp, E.levels ? E.lvl[1] : nullptr));
+    DDM_TRY(check_launch());
+    for (int L = 2; L <= E.levels; ++L) {
+      DDM_LAUNCH("block_max", 8.0 * E.lvl_n[L - 1], st, match::block_max_kernel<<<grid_for(E.lvl_n[L - 1], 256, 8), 256, 0, st>>>(
+          E.lvl[L - 1], E.lvl_n[L - 1], E.lvl[L]));
+      DDM_TRY(check_launch());
+    }
+    // Alg. 6's combine in counting form: uppers before each segment
+    const unsigned stiles = (unsigned)((E.P + match::kScanThreads * match::kScanItems - 1) /
+                                       (match::kScanThreads * match::kScanItems));
+    DDM_CUDA(cudaMemsetAsync(E.scan_status, 0, sizeof(uint64_t) * (stiles + 1), st));
+    DDM_LAUNCH("scan", 16.0 * E.P, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
+        E.seg_uppers, E.P, E.ub, E.scan_status, nullptr));
+    DDM_TRY(check_launch());
+    ev::Args A{};
+    A.code = E.tcode;
+    A.hp = E.hp;
+    for (int L = 0; L <= E.levels; ++L) A.T.lvl[L] = E.lvl[L];
+    A.T.levels = E.levels;
+    A.ub = E.ub;
+    A.N2 = E.N2;
+    A.X.d = (int)R->d;
+    for (uint32_t k = 0; k < R->d; ++k) {
+      A.X.sub_lo[k] = R->sub_lo[k];
+      A.X.sub_hi[k] = R->sub_hi[k];
+      A.X.upd_lo[k] = R->upd_lo[k];
+      A.X.upd_hi[k] = R->upd_hi[k];
+    }
+    A.cursor = reinterpret_cast<unsigned long long*>(E.misc);
+    DDM_LAUNCH("ev_count", 0, st, ev::segment_kernel<false><<<(unsigned)E.P, ev::kThreads, sizeof(ev::Smem), st>>>(A));
+    DDM_TRY(check_launch());
+    DDM_CUDA(cudaMemcpyAsync(h, E.misc, sizeof(h), cudaMemcpyDeviceToHost, st));
+    DDM_CUDA(cudaStreamSynchronize(st));
+    *count_out = h[0];
+    DDM_TRY(err_status((uint32_t)h[1]));
+    if (!pairs || h[0] == 0) return DDM_OK;
+    if (h[0] > capacity) return DDM_ERR_CAPACITY;
+    DDM_CUDA(cudaMemsetAsync(E.misc, 0, sizeof(uint64_t), st));
+    A.pairs = reinterpret_cast<uint2*>(pairs);
+    A.capacity = capacity;
+    DDM_LAUNCH("ev_emit", 8.0 * h[0], st, ev::segment_kernel<true><<<(unsigned)E.P, ev::kThreads, sizeof(ev::Smem), st>>>(A));
+    return check_launch();
+  }
+  DDM_CUDA(cudaMemcpyAsync(h, E.misc, sizeof(h), cudaMemcpyDeviceToHost, st));
+  DDM_CUDA(cudaStreamSynchronize(st));
+  *count_out = 0;
+  return err_status((uint32_t)h[1]);
 }
 
 size_t ddm_sort_pairs_workspace_bytes(uint64_t k) {

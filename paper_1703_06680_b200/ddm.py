@@ -83,6 +83,8 @@ def load() -> ctypes.CDLL:
         "ddm_sub_index_build": ([R, vp, sz, vp, sz, vp], i32),
         "ddm_indexed_workspace_bytes": ([u32, u64, u64], sz),
         "ddm_match_pairs_indexed": ([vp, R, vp, vp, u64, ctypes.POINTER(u64), u32, vp, sz, vp], i32),
+        "ddm_events_workspace_bytes": ([u32, u64, u64], sz),
+        "ddm_match_pairs_events": ([R, vp, u64, ctypes.POINTER(u64), vp, sz, vp], i32),
         "ddm_match_count_indexed": ([vp, R, ctypes.POINTER(u64), vp, sz, vp], i32),
         "ddm_radix_sort_workspace_bytes": ([u64], sz),
         "ddm_radix_sort_u64": ([vp, vp, vp, vp, u64, i32, i32, vp, sz, vp], i32),
@@ -106,6 +108,7 @@ EXPORTED = ["ddm_workspace_bytes", "ddm_match_count", "ddm_match_pairs", "ddm_ma
             "ddm_sort_pairs_workspace_bytes",
             "ddm_sort_pairs", "ddm_sub_index_bytes", "ddm_index_build_workspace_bytes", "ddm_sub_index_build",
             "ddm_indexed_workspace_bytes", "ddm_match_pairs_indexed", "ddm_match_count_indexed",
+            "ddm_events_workspace_bytes", "ddm_match_pairs_events",
             "ddm_radix_sort_workspace_bytes", "ddm_radix_sort_u64", "ddm_encode_keys", "ddm_status_string",
             "ddm_last_cuda_error", "ddm_kernel_launch_count", "ddm_build_info", "ddm_profile_enable",
             "ddm_profile_read"]
@@ -306,6 +309,28 @@ def match_pairs(sub_lo, sub_hi, upd_lo, upd_hi, flags: int = 0, sort: bool = Fal
     out = torch.empty((max(capacity, 1), 2), dtype=torch.int32, device=dev)
     _check(L.ddm_match_pairs(ctypes.byref(r), out.data_ptr(), capacity, ctypes.byref(K), flags, ws.data_ptr(),
                              ws.numel(), st), "ddm_match_pairs")
+    out = out[: int(K.value)]
+    if sort:
+        sort_pairs(out, r.n_sub, r.n_upd)
+    return out
+
+
+def match_pairs_events(sub_lo, sub_hi, upd_lo, upd_hi, sort: bool = True) -> torch.Tensor:
+    """The event-order variant (ddm_match_pairs_events: the paper's Alg. 5 + 6
+    on the GPU, a cross-check of match_pairs).  Its own order is unspecified;
+    sort=True (default) returns canonical order."""
+    L = load()
+    r, keep = regions(sub_lo, sub_hi, upd_lo, upd_hi)
+    dev = keep[0].device if keep else torch.device("cuda")
+    ws = _workspace(L.ddm_events_workspace_bytes(r.d, r.n_sub, r.n_upd), dev)
+    K = ctypes.c_uint64(0)
+    st = _stream(dev)
+    _check(L.ddm_match_pairs_events(ctypes.byref(r), None, 0, ctypes.byref(K), ws.data_ptr(), ws.numel(), st),
+           "ddm_match_pairs_events(count)")
+    cap = int(K.value)
+    out = torch.empty((max(cap, 1), 2), dtype=torch.int32, device=dev)
+    _check(L.ddm_match_pairs_events(ctypes.byref(r), out.data_ptr(), cap, ctypes.byref(K), ws.data_ptr(), ws.numel(),
+                                    st), "ddm_match_pairs_events")
     out = out[: int(K.value)]
     if sort:
         sort_pairs(out, r.n_sub, r.n_upd)

@@ -756,3 +756,95 @@ def test_msd_negative_and_wide_ranges(orc):
     ul = rng.normal(0, 1, 8000)
     uh = ul + 0.1
     check_against(orc, lo, hi, ul, uh, flags=(0, ddm.DDM_SORT_LSB))
+
+
+# ------------------------------------------------------------ event-order variant
+
+@pytest.mark.parametrize("S,U,K", [
+    ([[0.0, 1.0]], [[1.0, 2.0]], 1),     # touching endpoints (closed, R1)
+    ([[0.0, 0.0]], [[0.0, 0.0]], 1),     # points
+    ([[-1.0, -0.0]], [[0.0, 1.0]], 1),   # -0.0 == +0.0 (R3)
+    ([[0.0, 1.0]], [[1.5, 2.0]], 0),
+])
+def test_events_small_cases(orc, S, U, K):
+    sl, sh = np.array([[s[0] for s in S]]), np.array([[s[1] for s in S]])
+    ul, uh = np.array([[u[0] for u in U]]), np.array([[u[1] for u in U]])
+    p = ddm.match_pairs_events(*[cuda(x) for x in (sl, sh, ul, uh)])
+    assert p.shape[0] == K
+    assert np.array_equal(words_of(p), orc.bf_pairs(sl, sh, ul, uh))
+
+
+def test_events_fuzz_against_oracle(orc):
+    """Alg. 5 + 6 on the GPU against brute force: ties, duplicates, points,
+    long intervals crossing many segments (initial sets from the backward
+    walk, chunked past 2048 members), d = 1..3, sizes across several
+    segments with ragged tails, and one empty side."""
+    rng = np.random.default_rng(77)
+    for case in range(16):
+        d = int(rng.integers(1, 4))
+        n, m = (int(x) for x in rng.integers(1, 7000, 2))
+        def side(cnt):
+            kind = rng.integers(0, 3)
+            if kind == 0:
+                lo = rng.uniform(0, 1e4, (d, cnt))
+            elif kind == 1:
+                lo = rng.integers(0, 30, (d, cnt)).astype(np.float64)
+            else:
+                lo = rng.normal(5e3, 50.0, (d, cnt))
+            ln = np.abs(rng.normal(0, 20.0, (d, cnt)))
+            ln[rng.random((d, cnt)) < 0.03] = 1e5   # long intervals
+            ln[rng.random((d, cnt)) < 0.05] = 0.0   # points
+            return lo, lo + ln
+        sl, sh = side(n)
+        ul, uh = side(m)
+        ref = orc.bf_pairs(sl, sh, ul, uh)
+        p = ddm.match_pairs_events(*[cuda(x) for x in (sl, sh, ul, uh)])
+        assert np.array_equal(words_of(p), ref), f"case {case} d={d} n={n} m={m}"
+    e = np.zeros((1, 0))
+    x = rng.uniform(0, 1, (1, 50))
+    assert ddm.match_pairs_events(cuda(e), cuda(e), cuda(x), cuda(x + 1)).shape[0] == 0
+
+
+def test_events_dense_initial_sets(orc):
+    """Every region spans the whole domain: each segment's initial sets hold
+    thousands of members (several 2048-member chunks)."""
+    rng = np.random.default_rng(5)
+    n, m = 6000, 3000
+    sl = rng.uniform(0, 1, (1, n)); sh = sl + 10.0
+    ul = rng.uniform(0, 1, (1, m)); uh = ul + 10.0
+    p = ddm.match_pairs_events(*[cuda(x) for x in (sl, sh, ul, uh)])
+    assert p.shape[0] == n * m
+    assert np.array_equal(words_of(p), orc.bf_pairs(sl, sh, ul, uh))
+
+
+def test_events_equal_main_path_c2_c4(orc):
+    """Full-size c2 and a scaled c4: the event-order list, canonicalised,
+    equals the main path's canonicalised list (two independent GPU
+    algorithms: rank differences + tile sweep vs. Alg. 5 + 6)."""
+    for cfg, scale in (("c2", 1.0), ("c4", 0.02)):
+        w = wl.make(cfg, scale)
+        g = gpu_args(w)
+        a = ddm.match_pairs(*g, sort=True)
+        b = ddm.match_pairs_events(*g)
+        assert torch.equal(a, b), cfg
+
+
+def test_events_validation():
+    x = cuda(np.array([[0.0, 1.0]]))
+    bad = cuda(np.array([[np.nan, 1.0]]))
+    with pytest.raises(ddm.DDMError) as e:
+        ddm.match_pairs_events(bad, x, x, x + 1)
+    assert e.value.status == 2
+    with pytest.raises(ddm.DDMError) as e:
+        ddm.match_pairs_events(x + 5, x, x, x + 1)
+    assert e.value.status == 3
+
+
+def test_events_c3_full_equals_main_path():
+    """c3 at full size (1e8 regions, 2e8 endpoints, ~1e5 segments): the
+    event-order variant's canonical list equals the main path's."""
+    w = wl.make("c3")
+    g = gpu_args(w)
+    a = ddm.match_pairs(*g, sort=True)
+    b = ddm.match_pairs_events(*g)
+    assert a.shape == b.shape and torch.equal(a, b)
