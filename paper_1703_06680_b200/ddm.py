@@ -84,6 +84,8 @@ def load() -> ctypes.CDLL:
         "ddm_indexed_workspace_bytes": ([u32, u64, u64], sz),
         "ddm_match_pairs_indexed": ([vp, R, vp, vp, u64, ctypes.POINTER(u64), u32, vp, sz, vp], i32),
         "ddm_events_workspace_bytes": ([u32, u64, u64], sz),
+        "ddm_sub_index_update_workspace_bytes": ([u32, u64, u64], sz),
+        "ddm_sub_index_update": ([vp, sz, u64, R, vp, vp, sz, vp], i32),
         "ddm_match_pairs_events": ([R, vp, u64, ctypes.POINTER(u64), vp, sz, vp], i32),
         "ddm_match_count_indexed": ([vp, R, ctypes.POINTER(u64), vp, sz, vp], i32),
         "ddm_radix_sort_workspace_bytes": ([u64], sz),
@@ -109,6 +111,7 @@ EXPORTED = ["ddm_workspace_bytes", "ddm_match_count", "ddm_match_pairs", "ddm_ma
             "ddm_sort_pairs", "ddm_sub_index_bytes", "ddm_index_build_workspace_bytes", "ddm_sub_index_build",
             "ddm_indexed_workspace_bytes", "ddm_match_pairs_indexed", "ddm_match_count_indexed",
             "ddm_events_workspace_bytes", "ddm_match_pairs_events",
+            "ddm_sub_index_update_workspace_bytes", "ddm_sub_index_update",
             "ddm_radix_sort_workspace_bytes", "ddm_radix_sort_u64", "ddm_encode_keys", "ddm_status_string",
             "ddm_last_cuda_error", "ddm_kernel_launch_count", "ddm_build_info", "ddm_profile_enable",
             "ddm_profile_read"]
@@ -364,6 +367,20 @@ def sub_index_build(sub_lo, sub_hi) -> torch.Tensor:
     _check(L.ddm_sub_index_build(ctypes.byref(r), idx.data_ptr(), idx.numel(), ws.data_ptr(), ws.numel(),
                                  _stream(dev)), "ddm_sub_index_build")
     return idx
+
+
+def sub_index_update(index: torch.Tensor, n_sub: int, ids: torch.Tensor, new_lo, new_hi) -> torch.Tensor:
+    """Dynamic DDM: subscriptions `ids` (int32 CUDA, strictly increasing) of a
+    built index take the coordinates new_lo/new_hi ([d, k] float64 CUDA); the
+    index is merged in place (ddm_sub_index_update) and returned."""
+    L = load()
+    r, keep = regions(new_lo, new_hi)
+    dev = keep[0].device
+    ids = ids.to(device=dev, dtype=torch.int32).contiguous()
+    ws = _workspace(L.ddm_sub_index_update_workspace_bytes(r.d, n_sub, r.n_sub), dev)
+    _check(L.ddm_sub_index_update(index.data_ptr(), index.numel(), n_sub, ctypes.byref(r), ids.data_ptr(),
+                                  ws.data_ptr(), ws.numel(), _stream(dev)), "ddm_sub_index_update")
+    return index
 
 
 def match_pairs_indexed(index: torch.Tensor, n_sub: int, upd_lo, upd_hi, upd_ids: torch.Tensor | None = None,

@@ -848,3 +848,61 @@ def test_events_c3_full_equals_main_path():
     a = ddm.match_pairs(*g, sort=True)
     b = ddm.match_pairs_events(*g)
     assert a.shape == b.shape and torch.equal(a, b)
+
+
+# ------------------------------------------------------------ dynamic DDM
+
+def _index_zeroed(L, sl, sh):
+    import ctypes
+    r, keep = ddm.regions(sl, sh)
+    idx = torch.zeros(L.ddm_sub_index_bytes(r.d, r.n_sub), dtype=torch.uint8, device="cuda")
+    ws = torch.empty(L.ddm_index_build_workspace_bytes(r.d, r.n_sub), dtype=torch.uint8, device="cuda")
+    assert L.ddm_sub_index_build(ctypes.byref(r), idx.data_ptr(), idx.numel(), ws.data_ptr(), ws.numel(),
+                                 torch.cuda.current_stream().cuda_stream) == 0
+    return idx
+
+
+@pytest.mark.parametrize("d,n,k", [(1, 1, 1), (1, 5000, 1), (1, 20_000, 700), (1, 20_000, 20_000),
+                                   (2, 9000, 400), (3, 4097, 4097)])
+def test_index_update_equals_rebuild(orc, d, n, k):
+    """Moving / resizing k subscriptions by merge gives the byte-identical
+    index of a rebuild on the modified set (ties, duplicates, long intervals,
+    moves onto other entries' exact coordinates), and matches through it
+    equal brute force."""
+    L = ddm.load()
+    rng = np.random.default_rng(n + k + d)
+    sl = rng.integers(0, 300, (d, n)).astype(np.float64)
+    sh = sl + rng.integers(0, 5, (d, n))
+    sh[:, rng.random(n) < 0.02] += 1e4
+    ids = np.sort(rng.choice(n, k, replace=False)).astype(np.int32)
+    nl = rng.integers(0, 300, (d, k)).astype(np.float64)
+    nh = nl + rng.integers(0, 5, (d, k))
+    copy = rng.random(k) < 0.3  # some moves land exactly on other entries' coordinates
+    src = rng.integers(0, n, k)
+    nl[:, copy], nh[:, copy] = sl[:, src[copy]], sh[:, src[copy]]
+    idx = _index_zeroed(L, cuda(sl), cuda(sh))
+    ddm.sub_index_update(idx, n, torch.from_numpy(ids).cuda(), cuda(nl), cuda(nh))
+    sl2, sh2 = sl.copy(), sh.copy()
+    sl2[:, ids], sh2[:, ids] = nl, nh
+    ref_idx = _index_zeroed(L, cuda(sl2), cuda(sh2))
+    assert torch.equal(idx, ref_idx)
+    m = 3000
+    ul = rng.integers(0, 300, (d, m)).astype(np.float64)
+    uh = ul + rng.integers(0, 5, (d, m))
+    p = ddm.match_pairs_indexed(idx, n, cuda(ul), cuda(uh))
+    assert np.array_equal(words_of(p), orc.bf_pairs(sl2, sh2, ul, uh))
+
+
+def test_index_update_errors_leave_index_untouched():
+    L = ddm.load()
+    sl = cuda(np.arange(10.0)[None]); sh = sl + 1
+    idx = _index_zeroed(L, sl, sh)
+    before = idx.clone()
+    for ids, nl, nh, st in (([3, 3], [[0.0, 1.0]], [[1.0, 2.0]], 1),      # not strictly increasing
+                            ([2, 10], [[0.0, 1.0]], [[1.0, 2.0]], 1),     # out of range
+                            ([1, 2], [[np.nan, 1.0]], [[1.0, 2.0]], 2),   # non-finite
+                            ([1, 2], [[5.0, 1.0]], [[1.0, 2.0]], 3)):     # inverted
+        with pytest.raises(ddm.DDMError) as e:
+            ddm.sub_index_update(idx, 10, torch.tensor(ids, dtype=torch.int32), cuda(np.array(nl)), cuda(np.array(nh)))
+        assert e.value.status == st
+        assert torch.equal(idx, before)
