@@ -156,17 +156,20 @@ ddm_status ddm_sub_index_build(const ddm_regions *subs /* n_upd ignored */, void
  * subscriptions ids[0..k) of a built index (n_sub regions) take the new
  * coordinates moved->sub_lo/sub_hi[dim][0..k) (moved->d = the index's d,
  * moved->n_sub = k; device arrays).  ids: device, strictly increasing, < n_sub.
- * The index is updated in place by a merge (tombstone the old entries, sort
- * the k new ones, scatter both to their final positions, recompute the block
- * and prefix maxima and d > 1 boxes): O(n + k log k) work instead of a
- * rebuild's sort, and the result is byte-identical to ddm_sub_index_build on
- * the modified region set.  Errors (bad ids, non-finite or inverted new
- * coordinates) are reported before the index is touched.  Stream-ordered;
- * blocks on one small device->host read.  ws: 256-byte aligned, >=
- * ddm_sub_index_update_workspace_bytes(d, n_sub, k). */
-size_t ddm_sub_index_update_workspace_bytes(uint32_t d, uint64_t n_sub, uint64_t k);
-ddm_status ddm_sub_index_update(void *index, size_t index_bytes, uint64_t n_sub, const ddm_regions *moved,
-                                const uint32_t *ids, void *ws, size_t ws_bytes, cudaStream_t stream);
+ * The updated index is written to index_out by a merge (tombstone the old
+ * entries, sort the k new ones, scatter every entry once to its final
+ * position, recompute the block / prefix maxima and d > 1 boxes): O(n + k log
+ * k) work instead of a rebuild's sort, and the result is byte-identical to
+ * ddm_sub_index_build on the modified region set.  index_out == index_in
+ * updates in place through a copy in the workspace (in_place = 1 sizes it);
+ * distinct buffers (ping-pong) avoid the copy.  Errors (bad ids, non-finite
+ * or inverted new coordinates) are reported before anything is written.
+ * Stream-ordered; blocks on one small device->host read.  ws: 256-byte
+ * aligned, >= ddm_sub_index_update_workspace_bytes(d, n_sub, k, in_place). */
+size_t ddm_sub_index_update_workspace_bytes(uint32_t d, uint64_t n_sub, uint64_t k, int in_place);
+ddm_status ddm_sub_index_update(const void *index_in, void *index_out, size_t index_bytes, uint64_t n_sub,
+                                const ddm_regions *moved, const uint32_t *ids, void *ws, size_t ws_bytes,
+                                cudaStream_t stream);
 
 /* Match updates against a built index.  upds->n_sub must equal the indexed
  * n_sub and upds->d its d.  upd_ids (device, may be NULL): global id of each

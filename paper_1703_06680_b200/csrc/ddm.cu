@@ -1368,11 +1368,12 @@ ddm_status ddm_match_count_indexed(const void* index, const ddm_regions* upds, u
 
 struct DynWs {
   uint32_t* bad;
-  uint32_t* newidx;
-  uint8_t* keep;
-  uint8_t* keep_shi;
-  uint32_t* kb;
-  uint32_t* kb_shi;
+  uint32_t* bits;   // moved-id bitmap
+  uint32_t* w;      // Slo: keep + insertion histogram, [n + 1]
+  uint32_t* E;      // its exclusive scan
+  uint32_t* wsh;     // Shi: the same
+  uint32_t* Es;
+  uint8_t* ks;      // Shi keep flags
   uint64_t* tsum;
   uint64_t* toff;
   uint64_t* scan_status;
@@ -1381,25 +1382,24 @@ struct DynWs {
   uint64_t* nkey;
   uint32_t* nidx;
   uint64_t* nhi;
+  uint32_t* p;      // Slo insertion points
+  uint32_t* ps;     // Shi insertion points
   SortScratch sort;
-  uint64_t* okey;
-  uint32_t* oid;
-  uint64_t* ohi;
-  uint64_t* oshi;
-  double* osd;
+  uint8_t* copy;    // in-place updates: a copy of the old index
   size_t bytes;
 };
 
-static DynWs dyn_layout(uint32_t d, uint64_t n, uint64_t k, void* base) {
+static DynWs dyn_layout(uint32_t d, uint64_t n, uint64_t k, bool in_place, void* base) {
   Carver c(base);
   DynWs W{};
-  const uint64_t tiles = n / dyn::kTile + 2;
+  const uint64_t tiles = (n + 1) / dyn::kTile + 2;
   W.bad = c.take<uint32_t>(4);
-  W.newidx = c.take<uint32_t>(n);
-  W.keep = c.take<uint8_t>(n);
-  W.keep_shi = c.take<uint8_t>(n);
-  W.kb = c.take<uint32_t>(n + 1);
-  W.kb_shi = c.take<uint32_t>(n + 1);
+  W.bits = c.take<uint32_t>(n / 32 + 1);
+  W.w = c.take<uint32_t>(n + 1);
+  W.E = c.take<uint32_t>(n + 1);
+  W.wsh = c.take<uint32_t>(n + 1);
+  W.Es = c.take<uint32_t>(n + 1);
+  W.ks = c.take<uint8_t>(n);
   W.tsum = c.take<uint64_t>(tiles);
   W.toff = c.take<uint64_t>(tiles);
   W.scan_status = c.take<uint64_t>(tiles / (match::kScanThreads * match::kScanItems) + 2);
@@ -1408,20 +1408,18 @@ static DynWs dyn_layout(uint32_t d, uint64_t n, uint64_t k, void* base) {
   W.nkey = c.take<uint64_t>(k);
   W.nidx = c.take<uint32_t>(k);
   W.nhi = c.take<uint64_t>(k);
+  W.p = c.take<uint32_t>(k);
+  W.ps = c.take<uint32_t>(k);
   W.sort = sort_scratch(c, k, true);
-  W.okey = c.take<uint64_t>(n);
-  W.oid = c.take<uint32_t>(n);
-  W.ohi = c.take<uint64_t>(n);
-  W.oshi = c.take<uint64_t>(n);
-  W.osd = c.take<double>((uint64_t)2 * (d - 1) * n);
+  W.copy = in_place ? c.take<uint8_t>(index_layout(d, n, nullptr).bytes) : nullptr;
   W.bytes = c.used;
   return W;
 }
 
-// kb[i] = #{j < i : keep[j]}, i = 0..n
-static ddm_status keep_scan(const uint8_t* keep, uint64_t n, uint32_t* kb, DynWs& W, cudaStream_t st) {
-  const uint64_t tiles = (n + dyn::kTile - 1) / dyn::kTile + 1;  // (+1: kb[n] when n is a tile multiple)
-  DDM_LAUNCH("dyn_scan", 1.0 * n, st, dyn::flag_sum_kernel<<<(unsigned)tiles, 256, 0, st>>>(keep, n, W.tsum));
+// E[i] = sum(w[0..i)), i = 0..len-1
+static ddm_status excl_scan_u32(const uint32_t* w, uint64_t len, uint32_t* E, DynWs& W, cudaStream_t st) {
+  const uint64_t tiles = (len + dyn::kTile - 1) / dyn::kTile;
+  DDM_LAUNCH("dyn_scan", 4.0 * len, st, dyn::tile_sum_kernel<<<(unsigned)tiles, 256, 0, st>>>(w, len, W.tsum));
   DDM_TRY(check_launch());
   const unsigned stiles = (unsigned)((tiles + match::kScanThreads * match::kScanItems - 1) /
                                      (match::kScanThreads * match::kScanItems));
@@ -1429,74 +1427,95 @@ static ddm_status keep_scan(const uint8_t* keep, uint64_t n, uint32_t* kb, DynWs
   DDM_LAUNCH("scan", 16.0 * tiles, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
       W.tsum, tiles, W.toff, W.scan_status, nullptr));
   DDM_TRY(check_launch());
-  DDM_LAUNCH("dyn_scan", 5.0 * n, st, dyn::flag_scan_kernel<<<(unsigned)tiles, 256, 0, st>>>(keep, n, W.toff, kb));
+  DDM_LAUNCH("dyn_scan", 8.0 * len, st, dyn::excl_scan_kernel<<<(unsigned)tiles, 256, 0, st>>>(w, len, W.toff, E));
   return check_launch();
 }
 
-extern "C" size_t ddm_sub_index_update_workspace_bytes(uint32_t d, uint64_t n_sub, uint64_t k) {
+extern "C" size_t ddm_sub_index_update_workspace_bytes(uint32_t d, uint64_t n_sub, uint64_t k, int in_place) {
   if (d == 0 || d > DDM_MAX_DIMS) return 0;
-  return dyn_layout(d, n_sub, k, nullptr).bytes;
+  return dyn_layout(d, n_sub, k, in_place != 0, nullptr).bytes;
 }
 
-extern "C" ddm_status ddm_sub_index_update(void* index, size_t index_bytes, uint64_t n_sub, const ddm_regions* moved,
-                                           const uint32_t* ids, void* ws, size_t ws_bytes, cudaStream_t st) {
+extern "C" ddm_status ddm_sub_index_update(const void* index_in, void* index_out, size_t index_bytes, uint64_t n_sub,
+                                           const ddm_regions* moved, const uint32_t* ids, void* ws, size_t ws_bytes,
+                                           cudaStream_t st) {
   DDM_TRY(check_regions(moved, true, false));
   const uint32_t d = moved->d;
   const uint64_t n = n_sub, k = moved->n_sub;
-  if (!index || !aligned(index, 256) || !aligned(ws, 256) || (k && !ids) || k > n) return DDM_ERR_INVALID_ARGUMENT;
-  if (index_bytes < ddm_sub_index_bytes(d, n)) return DDM_ERR_WORKSPACE;
-  if (ws_bytes < ddm_sub_index_update_workspace_bytes(d, n, k)) return DDM_ERR_WORKSPACE;
-  if (k == 0) return DDM_OK;
+  const bool in_place = index_in == index_out;
+  if (!index_in || !index_out || !aligned(index_in, 256) || !aligned(index_out, 256) || !aligned(ws, 256) ||
+      (k && !ids) || k > n)
+    return DDM_ERR_INVALID_ARGUMENT;
+  const size_t ib = ddm_sub_index_bytes(d, n);
+  if (index_bytes < ib) return DDM_ERR_WORKSPACE;
+  if (ws_bytes < ddm_sub_index_update_workspace_bytes(d, n, k, in_place ? 1 : 0)) return DDM_ERR_WORKSPACE;
   init_attrs_once();
-  Index I = index_layout(d, n, index);
-  DynWs W = dyn_layout(d, n, k, ws);
+  DynWs W = dyn_layout(d, n, k, in_place, ws);
   DDM_CUDA(cudaMemsetAsync(W.bad, 0, 4 * sizeof(uint32_t), st));
-  // a1 on the new coordinates
+  // errors are reported before anything is written
   DDM_TRY(validate_side(d, k, moved->sub_lo, moved->sub_hi, nullptr, nullptr, W.bad + 1, st));
-  // tombstones of the moved entries in Slo and Shi
-  DDM_CUDA(cudaMemsetAsync(W.newidx, 0xff, sizeof(uint32_t) * n, st));
-  DDM_LAUNCH("dyn_mark", 0, st, dyn::mark_kernel<<<grid_for(k, 256, 8), 256, 0, st>>>(ids, k, n, W.newidx, W.bad));
-  DDM_TRY(check_launch());
-  {  // errors are reported before the index is touched
+  DDM_CUDA(cudaMemsetAsync(W.bits, 0, sizeof(uint32_t) * (n / 32 + 1), st));
+  if (k) {
+    DDM_LAUNCH("dyn_mark", 0, st, dyn::mark_kernel<<<grid_for(k, 256, 8), 256, 0, st>>>(ids, k, n, W.bits, W.bad));
+    DDM_TRY(check_launch());
+  }
+  {
     uint32_t h[2] = {0, 0};
     DDM_CUDA(cudaMemcpyAsync(h, W.bad, sizeof(h), cudaMemcpyDeviceToHost, st));
     DDM_CUDA(cudaStreamSynchronize(st));
     if (h[0]) return DDM_ERR_INVALID_ARGUMENT;  // ids not strictly increasing or out of range
     DDM_TRY(err_status(h[1]));
   }
-  DDM_LAUNCH("dyn_tomb", 16.0 * n, st, dyn::tomb_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.slo_id, I.slo_hi, n,
-                                                                                             W.newidx, W.keep, W.rhi));
+  if (k == 0) {
+    if (!in_place) DDM_CUDA(cudaMemcpyAsync(index_out, index_in, ib, cudaMemcpyDeviceToDevice, st));
+    return DDM_OK;
+  }
+  const void* src = index_in;
+  if (in_place) {
+    DDM_CUDA(cudaMemcpyAsync(W.copy, index_in, ib, cudaMemcpyDeviceToDevice, st));
+    src = W.copy;
+  }
+  const Index O = index_layout(d, n, const_cast<void*>(src));
+  Index I = index_layout(d, n, index_out);
+  // Slo: keep flags + the moved entries' old upper keys
+  DDM_LAUNCH("dyn_tomb", 16.0 * n, st, dyn::tomb_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(
+      O.slo_id, O.slo_hi, n, W.bits, ids, k, W.w, W.rhi));
   DDM_TRY(check_launch());
+  // Shi: keep flags from the sorted removed keys
   const radix::PassList P = full_passes();
   DDM_TRY(radix_sort(W.rhi, false, nullptr, W.rhi_sorted, nullptr, k, P, W.sort.hist[0], false, W.sort, st));
-  DDM_CUDA(cudaMemsetAsync(W.keep_shi, 1, n, st));
-  DDM_LAUNCH("dyn_tomb", 0, st, dyn::shi_tomb_kernel<<<grid_for(k, 256, 8), 256, 0, st>>>(W.rhi_sorted, k, I.shi_key, n,
-                                                                                          W.keep_shi));
+  DDM_LAUNCH("dyn_fill", 4.0 * n, st, dyn::fill_one_kernel<<<grid_for(n + 1, 256, 8), 256, 0, st>>>(W.wsh, n));
   DDM_TRY(check_launch());
-  DDM_TRY(keep_scan(W.keep, n, W.kb, W, st));
-  DDM_TRY(keep_scan(W.keep_shi, n, W.kb_shi, W, st));
-  // the new entries sorted on their own: (lower key, input index) -- the ids
-  // increase with the input index, so this is (key, id) order -- and the new
-  // upper keys
+  DDM_CUDA(cudaMemsetAsync(W.ks, 1, n, st));
+  DDM_LAUNCH("dyn_tomb", 0, st, dyn::shi_tomb_kernel<<<grid_for(k, 256, 8), 256, 0, st>>>(W.rhi_sorted, k, O.shi_key, n,
+                                                                                          W.wsh, W.ks));
+  DDM_TRY(check_launch());
+  // the new entries sorted on their own -- (lower key, input index), which is
+  // (key, id) order as the ids increase -- and their insertion points
   DDM_TRY(radix_sort(moved->sub_lo[0], true, nullptr, W.nkey, W.nidx, k, P, W.sort.hist[0], false, W.sort, st));
   DDM_TRY(radix_sort(moved->sub_hi[0], true, nullptr, W.nhi, nullptr, k, P, W.sort.hist[0], false, W.sort, st));
-  // merge: scatter old survivors and new entries to their final positions
-  DDM_CUDA(cudaMemcpyAsync(W.okey, I.slo_key, 8 * n, cudaMemcpyDeviceToDevice, st));
-  DDM_CUDA(cudaMemcpyAsync(W.oid, I.slo_id, 4 * n, cudaMemcpyDeviceToDevice, st));
-  DDM_CUDA(cudaMemcpyAsync(W.ohi, I.slo_hi, 8 * n, cudaMemcpyDeviceToDevice, st));
-  DDM_CUDA(cudaMemcpyAsync(W.oshi, I.shi_key, 8 * n, cudaMemcpyDeviceToDevice, st));
-  if (d > 1) DDM_CUDA(cudaMemcpyAsync(W.osd, I.sdims, sizeof(double) * 2 * (d - 1) * n, cudaMemcpyDeviceToDevice, st));
+  DDM_LAUNCH("dyn_ins", 0, st, dyn::slo_ins_kernel<<<grid_for(k, 256, 8), 256, 0, st>>>(O.slo_key, O.slo_id, n, W.nkey,
+                                                                                         W.nidx, ids, k, W.p, W.w));
+  DDM_TRY(check_launch());
+  DDM_LAUNCH("dyn_ins", 0, st, dyn::shi_ins_kernel<<<grid_for(k, 256, 8), 256, 0, st>>>(O.shi_key, n, W.nhi, k, W.ps,
+                                                                                         W.wsh));
+  DDM_TRY(check_launch());
+  DDM_TRY(excl_scan_u32(W.w, n + 1, W.E, W, st));
+  DDM_TRY(excl_scan_u32(W.wsh, n + 1, W.Es, W, st));
+  // merge: every element written once to its final position
   dyn::SloArgs A{};
-  A.okey = W.okey;
-  A.oid = W.oid;
-  A.ohi = W.ohi;
-  A.osd = W.osd;
-  A.keep = W.keep;
-  A.kb = W.kb;
+  A.okey = O.slo_key;
+  A.oid = O.slo_id;
+  A.ohi = O.slo_hi;
+  A.osd = O.sdims;
+  A.bits = W.bits;
+  A.w = W.w;
+  A.E = W.E;
   A.n = n;
   A.nkey = W.nkey;
   A.nidx = W.nidx;
   A.ids = ids;
+  A.p = W.p;
   for (uint32_t kk = 0; kk < d; ++kk) {
     A.new_lo[kk] = moved->sub_lo[kk];
     A.new_hi[kk] = moved->sub_hi[kk];
@@ -1507,12 +1526,12 @@ extern "C" ddm_status ddm_sub_index_update(void* index, size_t index_bytes, uint
   A.id = I.slo_id;
   A.hi = I.slo_hi;
   A.sd = I.sdims;
-  DDM_LAUNCH("dyn_merge", 56.0 * n, st, dyn::slo_old_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(A));
+  DDM_LAUNCH("dyn_merge", (28.0 + 32.0 * (d - 1)) * n, st, dyn::slo_old_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(A));
   DDM_TRY(check_launch());
   DDM_LAUNCH("dyn_merge", 0, st, dyn::slo_new_kernel<<<grid_for(k, 256, 8), 256, 0, st>>>(A));
   DDM_TRY(check_launch());
-  DDM_LAUNCH("dyn_merge", 21.0 * n, st, dyn::shi_merge_kernel<<<grid_for(n + k, 256, 8), 256, 0, st>>>(
-      W.oshi, W.keep_shi, W.kb_shi, n, W.nhi, k, I.shi_key));
+  DDM_LAUNCH("dyn_merge", 25.0 * n, st, dyn::shi_merge_kernel<<<grid_for(n + k, 256, 8), 256, 0, st>>>(
+      O.shi_key, W.wsh, W.Es, W.ks, n, W.nhi, W.ps, k, I.shi_key));
   DDM_TRY(check_launch());
   // derived structures, as the build computes them
   DDM_TRY(tree_async(I, kNeedShi | kNeedPm, false, st));

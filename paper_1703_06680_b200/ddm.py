@@ -84,8 +84,8 @@ def load() -> ctypes.CDLL:
         "ddm_indexed_workspace_bytes": ([u32, u64, u64], sz),
         "ddm_match_pairs_indexed": ([vp, R, vp, vp, u64, ctypes.POINTER(u64), u32, vp, sz, vp], i32),
         "ddm_events_workspace_bytes": ([u32, u64, u64], sz),
-        "ddm_sub_index_update_workspace_bytes": ([u32, u64, u64], sz),
-        "ddm_sub_index_update": ([vp, sz, u64, R, vp, vp, sz, vp], i32),
+        "ddm_sub_index_update_workspace_bytes": ([u32, u64, u64, i32], sz),
+        "ddm_sub_index_update": ([vp, vp, sz, u64, R, vp, vp, sz, vp], i32),
         "ddm_match_pairs_events": ([R, vp, u64, ctypes.POINTER(u64), vp, sz, vp], i32),
         "ddm_match_count_indexed": ([vp, R, ctypes.POINTER(u64), vp, sz, vp], i32),
         "ddm_radix_sort_workspace_bytes": ([u64], sz),
@@ -369,18 +369,22 @@ def sub_index_build(sub_lo, sub_hi) -> torch.Tensor:
     return idx
 
 
-def sub_index_update(index: torch.Tensor, n_sub: int, ids: torch.Tensor, new_lo, new_hi) -> torch.Tensor:
+def sub_index_update(index: torch.Tensor, n_sub: int, ids: torch.Tensor, new_lo, new_hi,
+                     out: torch.Tensor | None = None) -> torch.Tensor:
     """Dynamic DDM: subscriptions `ids` (int32 CUDA, strictly increasing) of a
-    built index take the coordinates new_lo/new_hi ([d, k] float64 CUDA); the
-    index is merged in place (ddm_sub_index_update) and returned."""
+    built index take the coordinates new_lo/new_hi ([d, k] float64 CUDA).  The
+    merged index goes to `out` (a second index buffer: ping-pong, no copy) or,
+    by default, back into `index`; returns it (ddm_sub_index_update)."""
     L = load()
     r, keep = regions(new_lo, new_hi)
     dev = keep[0].device
     ids = ids.to(device=dev, dtype=torch.int32).contiguous()
-    ws = _workspace(L.ddm_sub_index_update_workspace_bytes(r.d, n_sub, r.n_sub), dev)
-    _check(L.ddm_sub_index_update(index.data_ptr(), index.numel(), n_sub, ctypes.byref(r), ids.data_ptr(),
-                                  ws.data_ptr(), ws.numel(), _stream(dev)), "ddm_sub_index_update")
-    return index
+    dst = index if out is None else out
+    in_place = 1 if dst.data_ptr() == index.data_ptr() else 0
+    ws = _workspace(L.ddm_sub_index_update_workspace_bytes(r.d, n_sub, r.n_sub, in_place), dev)
+    _check(L.ddm_sub_index_update(index.data_ptr(), dst.data_ptr(), dst.numel(), n_sub, ctypes.byref(r),
+                                  ids.data_ptr(), ws.data_ptr(), ws.numel(), _stream(dev)), "ddm_sub_index_update")
+    return dst
 
 
 def match_pairs_indexed(index: torch.Tensor, n_sub: int, upd_lo, upd_hi, upd_ids: torch.Tensor | None = None,

@@ -881,10 +881,14 @@ def test_index_update_equals_rebuild(orc, d, n, k):
     src = rng.integers(0, n, k)
     nl[:, copy], nh[:, copy] = sl[:, src[copy]], sh[:, src[copy]]
     idx = _index_zeroed(L, cuda(sl), cuda(sh))
-    ddm.sub_index_update(idx, n, torch.from_numpy(ids).cuda(), cuda(nl), cuda(nh))
+    out = torch.zeros_like(idx)
+    tid = torch.from_numpy(ids).cuda()
+    ddm.sub_index_update(idx, n, tid, cuda(nl), cuda(nh), out=out)  # ping-pong
     sl2, sh2 = sl.copy(), sh.copy()
     sl2[:, ids], sh2[:, ids] = nl, nh
     ref_idx = _index_zeroed(L, cuda(sl2), cuda(sh2))
+    assert torch.equal(out, ref_idx)
+    ddm.sub_index_update(idx, n, tid, cuda(nl), cuda(nh))  # in place
     assert torch.equal(idx, ref_idx)
     m = 3000
     ul = rng.integers(0, 300, (d, m)).astype(np.float64)
