@@ -1029,7 +1029,7 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
                match::emit_chunk_kernel<<<egrid, match::kRowTile, sizeof(match::ChunkSmem), st>>>(A));
   else if (d == 1 && !per_row)  // sparse: tiles of 2048 rows walking a staged Slo window
     DDM_LAUNCH("emit", 24.0 * m + 8.0 * h.K + 12.0 * n, st,
-               match::emit_tile_kernel<<<(unsigned)((m + match::kEmitTile - 1) / match::kEmitTile), match::kRowTile,
+               match::emit_tile_kernel<<<(unsigned)((m + match::kEmitTile - 1) / match::kEmitTile), match::kEmitThreads,
                                          sizeof(match::EmitTileSmem), st>>>(A));
   else if (d == 1)  // forced per-row paths (cross-checks)
     DDM_LAUNCH("emit", 24.0 * m + 8.0 * h.K + 12.0 * n, st, match::emit_kernel<match::kEmitD1><<<egrid, match::kRowTile, 0, st>>>(A));

@@ -1017,8 +1017,13 @@ __global__ void __launch_bounds__(kRowTile) emit_kernel(const __grid_constant__ 
 // intervals) fall back to global memory with the block-max skips.  Row
 // offsets: each warp's 256 rows are one offset-scan tile.  Output identical
 // to the other d = 1 paths.
-constexpr int kEmitItems = 8;
-constexpr int kEmitTile = kRowTile * kEmitItems;  // 2048 rows: warp w owns row tile w
+#ifndef DDM_EMIT_ITEMS
+#define DDM_EMIT_ITEMS 8
+#endif
+constexpr int kEmitItems = DDM_EMIT_ITEMS;                 // rows per thread
+constexpr int kEmitThreads = 2048 / kEmitItems;            // 2048-row tiles
+constexpr int kEmitTile = kEmitThreads * kEmitItems;
+constexpr int kEmitWarpsPerRowTile = kRowTile / (32 * kEmitItems);  // warps sharing one 256-row offset tile
 constexpr int kEmitWin = 4096;                     // window entries
 constexpr int kEmitPad = 512;                      // window entries before r_lo(first row)
 
@@ -1027,9 +1032,13 @@ struct EmitTileSmem {
   alignas(16) uint32_t wi[kEmitWin + 4];
   uint64_t bar;
   uint32_t rbmax;
+  uint64_t wsum[32];
 };
 
-__global__ void __launch_bounds__(kRowTile, 3) emit_tile_kernel(const __grid_constant__ EmitArgs A) {
+#ifndef DDM_EMIT_MINB
+#define DDM_EMIT_MINB 3
+#endif
+__global__ void __launch_bounds__(kEmitThreads, DDM_EMIT_MINB) emit_tile_kernel(const __grid_constant__ EmitArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EmitTileSmem& S = *reinterpret_cast<EmitTileSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1042,7 +1051,7 @@ __global__ void __launch_bounds__(kRowTile, 3) emit_tile_kernel(const __grid_con
     const uint4* pb = reinterpret_cast<const uint4*>(A.r_b + jt);
     const uint4* pc = reinterpret_cast<const uint4*>(A.cnt0 + jt);
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < kEmitItems / 4; ++h) {
       const uint4 x = __ldg(pl + h), y = __ldg(pb + h), z = __ldg(pc + h);
       rl[4 * h] = x.x; rl[4 * h + 1] = x.y; rl[4 * h + 2] = x.z; rl[4 * h + 3] = x.w;
       rb[4 * h] = y.x; rb[4 * h + 1] = y.y; rb[4 * h + 2] = y.z; rb[4 * h + 3] = y.w;
@@ -1088,12 +1097,12 @@ __global__ void __launch_bounds__(kRowTile, 3) emit_tile_kernel(const __grid_con
     const ulonglong2* pa = reinterpret_cast<const ulonglong2*>(A.ulo_key + jt);
     const uint4* pi = reinterpret_cast<const uint4*>(A.ulo_id + jt);
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
+    for (int h = 0; h < kEmitItems / 2; ++h) {
       const ulonglong2 x = __ldg(pa + h);
       a[2 * h] = x.x; a[2 * h + 1] = x.y;
     }
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < kEmitItems / 4; ++h) {
       const uint4 x = __ldg(pi + h);
       lid[4 * h] = x.x; lid[4 * h + 1] = x.y; lid[4 * h + 2] = x.z; lid[4 * h + 3] = x.w;
     }
@@ -1104,12 +1113,18 @@ __global__ void __launch_bounds__(kRowTile, 3) emit_tile_kernel(const __grid_con
       lid[i] = i < ni ? A.ulo_id[jt + i] : 0;
     }
   }
-  // row offsets: warp w's 256 rows form offset tile (j0 >> 8) + w
+  // row offsets: the warps of one 256-row offset tile (j0 >> 8) + w / kEmitWarpsPerRowTile
   uint64_t mine = 0;
 #pragma unroll
   for (int i = 0; i < kEmitItems; ++i) mine += c0[i];
   uint64_t incl = warp_incl_scan<uint64_t>(mine);
-  uint64_t o = (ni > 0 ? A.tile_off[(j0 >> 8) + warp] : 0) + incl - mine;
+  uint64_t wpre = 0;
+  if (kEmitWarpsPerRowTile > 1) {  // sums of the earlier warps of the same row tile
+    if (lane == 31) S.wsum[warp] = incl;
+    __syncthreads();
+    for (int v = warp - warp % kEmitWarpsPerRowTile; v < warp; ++v) wpre += S.wsum[v];
+  }
+  uint64_t o = (ni > 0 ? A.tile_off[(j0 >> 8) + warp / kEmitWarpsPerRowTile] : 0) + wpre + incl - mine;
   __syncthreads();  // the barrier is initialised before anyone waits on it
   mbar_wait(&S.bar, 0);
   auto hi_at = [&](uint64_t i) -> uint64_t {
