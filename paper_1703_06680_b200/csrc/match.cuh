@@ -10,6 +10,7 @@
 //   Stab(a)  = { Slo[i] : i < r_lo, slo_hi[i] >= a },  |Stab(a)| = r_lo - r_hi
 //   Range(U) = { Slo[i] : r_lo <= i < r_b }           (contiguous)
 //   count(U) = r_b - r_hi                               (rank difference, I2)
+//            = (r_b - r_lo) + #{i < r_lo : slo_hi[i] >= a} (walk form, R23)
 // so every pair is reported exactly once, in the row of its update, which is
 // the set Alg. 4 reports; rows are ordered by the sweep order of
 // update lower endpoints and each row by Slo order (deterministic).
