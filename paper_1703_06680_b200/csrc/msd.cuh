@@ -289,20 +289,21 @@ struct TileRegs {
   }
   // float64 bits -> order-preserving keys (first pass), validating lo/hi
   __device__ __forceinline__ void finish(uint64_t wb0, uint64_t n, int lane) {
-    if (!SRC_F64) return;
+    if constexpr (SRC_F64) {
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const bool valid = wb0 + i * 32 + lane < n;
-      const uint64_t bx = key[i];
-      if (valid && !f64_finite_bits(bx)) err |= 1u;
-      key[i] = valid ? f64_key(__longlong_as_double((long long)bx)) : 0;
-      if (V64) {
-        const uint64_t by = hv[i];
-        if (valid) {
-          if (!f64_finite_bits(by)) err |= 1u;
-          else if (!(__longlong_as_double((long long)bx) <= __longlong_as_double((long long)by))) err |= 2u;
+      for (int i = 0; i < ITEMS; ++i) {
+        const bool valid = wb0 + i * 32 + lane < n;
+        const uint64_t bx = key[i];
+        if (valid && !f64_finite_bits(bx)) err |= 1u;
+        key[i] = valid ? f64_key(__longlong_as_double((long long)bx)) : 0;
+        if (V64) {
+          const uint64_t by = hv[i];
+          if (valid) {
+            if (!f64_finite_bits(by)) err |= 1u;
+            else if (!(__longlong_as_double((long long)bx) <= __longlong_as_double((long long)by))) err |= 2u;
+          }
+          hv[i] = valid ? f64_key(__longlong_as_double((long long)by)) : 0;
         }
-        hv[i] = valid ? f64_key(__longlong_as_double((long long)by)) : 0;
       }
     }
   }
