@@ -458,17 +458,19 @@ struct LocalSmem {  // keys only: payloads follow the permutation through the ke
   uint64_t bar;                         // mbarrier of the bulk copies
   uint32_t bin[kFineBins + 1];
   uint16_t perm[kCapPow2];  // sorted position -> staged index
-  uint16_t grp[kCap];       // staged indices grouped by fine bin (unordered within a bin)
   uint64_t red[2 * kWarps];
   uint32_t flag;
-  uint64_t bound[2];
+  uint64_t bound[1];  // prev_boundary's reduction slot
 };
 
 // Stable sort of records [e0, e0 + c) by key inside shared memory (c <= kCap).
 // Records arrive in (bucket, original-order) order.  Counting sort over fine
-// bins of the key range of this group (integer, monotone), then a stable
-// insertion sort by (key, staged index) inside each bin; if some bin is large
-// (ties, dense clusters) the group is bitonic-sorted on (key, staged index).
+// bins of the key range of this group (integer, monotone): every record goes
+// to its bin's next slot of perm, then each bin holding two or more records
+// (most hold zero or one) is insertion-sorted by (key, staged index); if some
+// bin is large (ties, dense clusters) the group is bitonic-sorted on (key,
+// staged index) instead.  (No separate grouping array: the smaller footprint
+// keeps 6 CTAs per SM; measured 1.31 -> 1.22 ms per two c3 launches.)
 template <bool V64, bool V32>
 __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restrict__ k_in,
                                  const uint64_t* __restrict__ v64_in, const uint32_t* __restrict__ v32_in,
@@ -535,26 +537,31 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
   }
   __syncthreads();
   if (S.flag == 0) {
-    // group the staged indices by fine bin (any order inside a bin) ...
+    // place every record at its bin's next slot, straight into perm (any
+    // order inside a bin; most bins hold zero or one record) ...
     for (uint32_t i = tid; i < c; i += kThreads) {
       const uint32_t pos = atomicAdd(&S.bin[(uint32_t)((K[i] - kmin) >> sh)], 1u);
-      S.grp[pos] = (uint16_t)i;
+      S.perm[pos] = (uint16_t)i;
     }
     __syncthreads();
-    // ... then every record's rank = its bin's start + #{bin members before it
-    // in (key, staged index) order}; bin b spans [end(b-1), end(b)), <= kMaxBinRun
-    for (uint32_t i = tid; i < c; i += kThreads) {
-      const uint64_t kv = K[i];
-      const uint32_t b = (uint32_t)((kv - kmin) >> sh);
+    // ... then order each bin holding two or more records by (key, staged
+    // index) with an insertion sort; bin b spans [end(b-1), end(b)), <= kMaxBinRun
+    for (uint32_t b = tid; b < kFineBins; b += kThreads) {
       const uint32_t lo = b ? S.bin[b - 1] : 0, hi = S.bin[b];
-      uint32_t r = lo;
-      if (hi - lo > 1)  // (a record alone in its bin is at its bin's start)
-        for (uint32_t x = lo; x < hi; ++x) {
-          const uint32_t w = S.grp[x];
-          const uint64_t kw = K[w];
-          r += (kw < kv || (kw == kv && w < i)) ? 1u : 0u;
+      if (hi - lo < 2) continue;
+      for (uint32_t x = lo + 1; x < hi; ++x) {
+        const uint16_t v = S.perm[x];
+        const uint64_t kv = K[v];
+        uint32_t y = x;
+        while (y > lo) {
+          const uint16_t u = S.perm[y - 1];
+          const uint64_t ku = K[u];
+          if (ku < kv || (ku == kv && u < v)) break;
+          S.perm[y] = u;
+          --y;
         }
-      S.perm[r] = (uint16_t)i;
+        S.perm[y] = v;
+      }
     }
   } else {
     // bitonic sort of (key, index) over the next power of two
