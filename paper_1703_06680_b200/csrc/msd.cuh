@@ -456,8 +456,13 @@ template <bool V64, bool V32>
 struct LocalSmem {  // keys only: payloads follow the permutation through the key buffer
   alignas(16) uint64_t keys[kCap + 2];  // +2: bulk copies start at a 16-byte aligned index
   uint64_t bar;                         // mbarrier of the bulk copies
-  uint32_t bin[kFineBins + 1];
-  uint16_t perm[kCapPow2];  // sorted position -> staged index
+  // fine-bin counts / offsets, two 16-bit fields per word (values <= kCap),
+  // followed by perm (sorted position -> staged index); the bitonic fallback
+  // uses both as one u16[kCapPow2] array (the bins are dead by then)
+  uint32_t binw[kFineBins / 2 + 2];
+  uint16_t perm[kCap];
+  static_assert(sizeof(uint32_t) * (kFineBins / 2 + 2) + sizeof(uint16_t) * kCap >= sizeof(uint16_t) * kCapPow2,
+                "the bitonic fallback's u16[kCapPow2] fits in binw + perm");
   uint64_t red[2 * kWarps];
   uint32_t flag;
   uint64_t bound[1];  // prev_boundary's reduction slot
@@ -471,6 +476,13 @@ struct LocalSmem {  // keys only: payloads follow the permutation through the ke
 // bin is large (ties, dense clusters) the group is bitonic-sorted on (key,
 // staged index) instead.  (No separate grouping array: the smaller footprint
 // keeps 6 CTAs per SM; measured 1.31 -> 1.22 ms per two c3 launches.)
+__device__ __forceinline__ uint32_t bin_get(const uint32_t* w, uint32_t b) {
+  return (w[b >> 1] >> ((b & 1) * 16)) & 0xffffu;
+}
+__device__ __forceinline__ uint32_t bin_add(uint32_t* w, uint32_t b) {  // returns the old value
+  return (atomicAdd(w + (b >> 1), (b & 1) ? 0x10000u : 1u) >> ((b & 1) * 16)) & 0xffffu;
+}
+
 template <bool V64, bool V32>
 __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restrict__ k_in,
                                  const uint64_t* __restrict__ v64_in, const uint32_t* __restrict__ v32_in,
@@ -495,7 +507,7 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
     kmin = k < kmin ? k : kmin;
     kmax = k > kmax ? k : kmax;
   }
-  for (uint32_t b = tid; b <= kFineBins; b += kThreads) S.bin[b] = 0;
+  for (uint32_t b = tid; b < kFineBins / 2 + 2; b += kThreads) S.binw[b] = 0;
   if (tid == 0) S.flag = 0;
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -515,14 +527,20 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
   // smallest shift with (kmax - kmin) >> sh < kFineBins
   const uint64_t range = kmax - kmin;
   const int sh = range ? max(0, 64 - __clzll((long long)range) - kFineBinBits) : 0;
-  for (uint32_t i = tid; i < c; i += kThreads) atomicAdd(&S.bin[(uint32_t)((K[i] - kmin) >> sh)], 1u);
+  for (uint32_t i = tid; i < c; i += kThreads) bin_add(S.binw, (uint32_t)((K[i] - kmin) >> sh));
   __syncthreads();
-  {  // exclusive scan over the bins (16 per thread) + large-bin detection
+  {  // exclusive scan over the bins (8 per thread, 4 words) + large-bin detection
     constexpr int kPer = kFineBins / kThreads;
+    static_assert(kPer % 2 == 0, "whole words per thread");
     uint32_t v[kPer], sum = 0;
 #pragma unroll
+    for (int q = 0; q < kPer; q += 2) {
+      const uint32_t wv = S.binw[(tid * kPer + q) >> 1];
+      v[q] = wv & 0xffffu;
+      v[q + 1] = wv >> 16;
+    }
+#pragma unroll
     for (int q = 0; q < kPer; ++q) {
-      v[q] = S.bin[tid * kPer + q];
       sum += v[q];
       if (v[q] > kMaxBinRun) S.flag = 1;
     }
@@ -530,9 +548,10 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
     uint32_t tot;
     uint32_t ex = block_excl_scan<kThreads>(sum, tmp, &tot);
 #pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-      S.bin[tid * kPer + q] = ex;
-      ex += v[q];
+    for (int q = 0; q < kPer; q += 2) {
+      const uint32_t e0v = ex, e1v = ex + v[q];
+      ex = e1v + v[q + 1];
+      S.binw[(tid * kPer + q) >> 1] = e0v | (e1v << 16);
     }
   }
   __syncthreads();
@@ -540,14 +559,14 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
     // place every record at its bin's next slot, straight into perm (any
     // order inside a bin; most bins hold zero or one record) ...
     for (uint32_t i = tid; i < c; i += kThreads) {
-      const uint32_t pos = atomicAdd(&S.bin[(uint32_t)((K[i] - kmin) >> sh)], 1u);
+      const uint32_t pos = bin_add(S.binw, (uint32_t)((K[i] - kmin) >> sh));
       S.perm[pos] = (uint16_t)i;
     }
     __syncthreads();
     // ... then order each bin holding two or more records by (key, staged
     // index) with an insertion sort; bin b spans [end(b-1), end(b)), <= kMaxBinRun
     for (uint32_t b = tid; b < kFineBins; b += kThreads) {
-      const uint32_t lo = b ? S.bin[b - 1] : 0, hi = S.bin[b];
+      const uint32_t lo = b ? bin_get(S.binw, b - 1) : 0, hi = bin_get(S.binw, b);
       if (hi - lo < 2) continue;
       for (uint32_t x = lo + 1; x < hi; ++x) {
         const uint16_t v = S.perm[x];
@@ -564,22 +583,24 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
       }
     }
   } else {
-    // bitonic sort of (key, index) over the next power of two
+    // bitonic sort of (key, index) over the next power of two, in the
+    // bins + perm storage taken as one u16 array
+    uint16_t* PB = reinterpret_cast<uint16_t*>(S.binw);
     uint32_t P = 1;
     while (P < c) P <<= 1;
-    for (uint32_t i = tid; i < P; i += kThreads) S.perm[i] = (uint16_t)(i < c ? i : 0xffff);
+    for (uint32_t i = tid; i < P; i += kThreads) PB[i] = (uint16_t)(i < c ? i : 0xffff);
     __syncthreads();
     for (uint32_t k = 2; k <= P; k <<= 1) {
       for (uint32_t j = k >> 1; j > 0; j >>= 1) {
         for (uint32_t i = tid; i < P; i += kThreads) {
           const uint32_t l = i ^ j;
           if (l > i) {
-            const uint16_t a = S.perm[i], b = S.perm[l];
+            const uint16_t a = PB[i], b = PB[l];
             const bool a_gt_b = (a == 0xffff) ? (b != 0xffff)
                                 : (b == 0xffff) ? false
                                 : (K[a] > K[b] || (K[a] == K[b] && a > b));
             const bool up = (i & k) == 0;
-            if (up == a_gt_b) { S.perm[i] = b; S.perm[l] = a; }
+            if (up == a_gt_b) { PB[i] = b; PB[l] = a; }
           }
         }
         __syncthreads();
@@ -587,7 +608,8 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
     }
   }
   __syncthreads();
-  for (uint32_t i = tid; i < c; i += kThreads) k_out[e0 + i] = K[S.perm[i]];
+  const uint16_t* PERM = S.flag ? reinterpret_cast<const uint16_t*>(S.binw) : S.perm;
+  for (uint32_t i = tid; i < c; i += kThreads) k_out[e0 + i] = K[PERM[i]];
   // payloads: staged coalesced through the key buffer (free now), then read
   // back in permutation order -- random global gathers would cost one L1
   // request per element
@@ -600,7 +622,7 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
     }
     mbar_wait(&S.bar, phase);
     phase ^= 1;
-    for (uint32_t i = tid; i < c; i += kThreads) v64_out[e0 + i] = K[S.perm[i]];
+    for (uint32_t i = tid; i < c; i += kThreads) v64_out[e0 + i] = K[PERM[i]];
   }
   if (V32) {
     const uint32_t vo = (uint32_t)(e0 & 3);
@@ -613,7 +635,7 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
     }
     mbar_wait(&S.bar, phase);
     phase ^= 1;
-    for (uint32_t i = tid; i < c; i += kThreads) v32_out[e0 + i] = b32[S.perm[i]];
+    for (uint32_t i = tid; i < c; i += kThreads) v32_out[e0 + i] = b32[PERM[i]];
   }
   __syncthreads();
 }
@@ -681,7 +703,10 @@ __global__ void __launch_bounds__(256) span_bounds_kernel(const uint64_t* __rest
 // buckets holding <= kCap records in smem.  A
 // single bucket larger than kCap sets *overflow (caller redoes with LSB).
 template <bool V64, bool V32>
-__global__ void __launch_bounds__(kThreads) local_sort_kernel(const uint64_t* __restrict__ k_in,
+#ifndef DDM_LS_MINB
+#define DDM_LS_MINB 7
+#endif
+__global__ void __launch_bounds__(kThreads, DDM_LS_MINB) local_sort_kernel(const uint64_t* __restrict__ k_in,
                                                               const uint64_t* __restrict__ v64_in,
                                                               const uint32_t* __restrict__ v32_in,
                                                               uint64_t* __restrict__ k_out,
