@@ -1207,6 +1207,9 @@ size_t ddm_workspace_bytes(uint32_t d, uint64_t n_sub, uint64_t n_upd, int want_
   return a256(index_layout(d, n_sub, nullptr).bytes) + match_layout(d, n_sub, n_upd, nullptr, true).bytes;
 }
 
+std::mutex g_probe_mu;
+std::unordered_map<std::string, bool> g_probe;  // count-form decision per call site
+
 static ddm_status match_full(const ddm_regions* R, ddm_pair* pairs, uint64_t capacity, uint64_t* count_out,
                              uint32_t flags, void* ws, size_t ws_bytes, cudaStream_t st,
                              const uint32_t* sub_map = nullptr, const uint32_t* upd_map = nullptr) {
@@ -1227,13 +1230,31 @@ static ddm_status match_full(const ddm_regions* R, ddm_pair* pairs, uint64_t cap
   if (pairs && R->d == 1 && !(flags & DDM_COUNT_RANKS)) {
     if (flags & DDM_COUNT_WALK) walk = true;
     else if (R->n_sub >= kWalkMinN && R->n_upd > 0) {
-      double est = INFINITY;
-      DDM_LAUNCH("stab_probe", 0, st, match::stab_density_kernel<<<1, 256, 0, st>>>(R->sub_lo[0], R->sub_hi[0], R->n_sub,
-                                                                                   W.probe));
-      DDM_TRY(check_launch());
-      DDM_CUDA(cudaMemcpyAsync(&est, W.probe, sizeof(double), cudaMemcpyDeviceToHost, st));
-      DDM_CUDA(cudaStreamSynchronize(st));
-      walk = est <= kWalkMaxStab;
+      // the decision is kept per call site (regions, workspace, flags, stream):
+      // repeated calls -- graph replays -- skip the probe and its host read;
+      // both forms give the same output, so a stale decision costs time only
+      const std::string pk = graph_key(R, ws, ws_bytes, flags, true, sub_map, upd_map, st);
+      bool known = false;
+      {
+        std::lock_guard<std::mutex> lk(g_probe_mu);
+        const auto it = g_probe.find(pk);
+        if (it != g_probe.end()) {
+          walk = it->second;
+          known = true;
+        }
+      }
+      if (!known) {
+        double est = INFINITY;
+        DDM_LAUNCH("stab_probe", 0, st, match::stab_density_kernel<<<1, 256, 0, st>>>(R->sub_lo[0], R->sub_hi[0],
+                                                                                     R->n_sub, W.probe));
+        DDM_TRY(check_launch());
+        DDM_CUDA(cudaMemcpyAsync(&est, W.probe, sizeof(double), cudaMemcpyDeviceToHost, st));
+        DDM_CUDA(cudaStreamSynchronize(st));
+        walk = est <= kWalkMaxStab;
+        std::lock_guard<std::mutex> lk(g_probe_mu);
+        if (g_probe.size() > 4096) g_probe.clear();
+        g_probe[pk] = walk;
+      }
     }
   }
   const uint32_t key_flags = (flags & ~(uint32_t)(DDM_COUNT_RANKS | DDM_COUNT_WALK)) |
