@@ -694,6 +694,9 @@ def test_indexed_shards_equal_single(orc, d):
             ul, uh = cuda(w.upd_lo[:, ids]), cuda(w.upd_hi[:, ids])
             idt = torch.from_numpy(ids.astype(np.int32)).cuda()
             p = ddm.match_pairs_indexed(idx, w.n, ul, uh, upd_ids=idt)
+            if d == 1:  # the walk-form counts over the index's prefix maxima give the same list
+                pw = ddm.match_pairs_indexed(idx, w.n, ul, uh, upd_ids=idt, flags=ddm.DDM_COUNT_WALK)
+                assert torch.equal(p, pw)
             total += ddm.match_count_indexed(idx, w.n, ul, uh)
             parts.append(words_of(p))
         got = np.sort(np.concatenate(parts))
