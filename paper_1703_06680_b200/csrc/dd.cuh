@@ -47,6 +47,7 @@
 // order), writing directly at its known offsets.  The count-only entry point
 // runs the enumeration without staging.
 #pragma once
+#include <cstddef>
 #include "common.cuh"
 #include "match.cuh"
 
@@ -55,12 +56,21 @@ namespace dd {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kG1 = 32;             // cells along dim 1
-constexpr int kG2 = 16;             // cells along dim 2
+#ifndef DDM_DD_G1
+#define DDM_DD_G1 32
+#endif
+#ifndef DDM_DD_G2
+#define DDM_DD_G2 48
+#endif
+constexpr int kG1 = DDM_DD_G1;      // cells along dim 1
+constexpr int kG2 = DDM_DD_G2;      // cells along dim 2
 constexpr int kCells = kG1 * kG2;
 constexpr int kCPT = kCells / 256;  // cells per thread in the cell scans
 constexpr int kWin = 1024;          // A_t walk window (positions per step), 4 per thread
-constexpr int kCap = 1024;          // candidates per shared-memory chunk
+#ifndef DDM_DD_CAP
+#define DDM_DD_CAP 1024
+#endif
+constexpr int kCap = DDM_DD_CAP;    // candidates per shared-memory chunk
 constexpr int kRounds = kCap / kThreads;
 constexpr int kList = 4;            // queued float passes per lane before an exact batch
 static_assert(kCap >= kWin, "a whole walk window must fit one chunk");
@@ -134,7 +144,6 @@ struct Smem {
   float4 rbox[kRows];        // widened row boxes (lo1, hi1, lo2, hi2)
   uint32_t cpos[kCap];       // Slo position of each slot (cell order)
   uint32_t fpos[kCap];       // Slo positions in fill order
-  uint16_t wc[kWarps * kCells];  // per (warp, cell) counts of one ranking round -> prefixes
   uint16_t lst[kList * kThreads];  // per-lane queues of float passes: (row q << 12) | slot
   uint32_t cstart[kCells + 1];
   uint32_t run[kCells];      // slots already assigned per cell (earlier rounds)
@@ -145,7 +154,12 @@ struct Smem {
   uint32_t nout;     // staged hits of this tile
   uint32_t ovf;      // staging overflowed -> re-enumerate in the place pass
   uint32_t tile;
+  // last: per (warp, cell) counts of one stable ranking round -> prefixes;
+  // only the place pass's direct enumeration uses them, the count / stage
+  // passes are launched without this tail (smem_bytes)
+  uint16_t wc[kWarps * kCells];
 };
+
 
 // Monotone float bucketer over one chunk's lower bounds on one dimension
 // (G bins).
@@ -438,12 +452,19 @@ __device__ void enumerate(const Args& A, Smem<R>& S, Rows<R>& rw, uint64_t j0, u
 }
 
 enum { kModeCount = 0, kModeStage = 1, kModePlace = 2 };
+template <int R>
+constexpr size_t smem_bytes(int mode) {
+  return mode == kModePlace ? sizeof(Smem<R>) : (offsetof(Smem<R>, wc) + 15) / 16 * 16;
+}
 
 // kModeCount: row counts + 256-row tile sums.  kModeStage: the same plus the
 // staged hits.  kModePlace: staged hits -> pairs (or, for a tile whose slot
 // overflowed, a second enumeration writing directly).
 template <int R, int MODE>
-__global__ void __launch_bounds__(kThreads, 4) dd_tile_kernel(const __grid_constant__ Args A) {
+#ifndef DDM_DD_MINB
+#define DDM_DD_MINB 4
+#endif
+__global__ void __launch_bounds__(kThreads, DDM_DD_MINB) dd_tile_kernel(const __grid_constant__ Args A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<R>& S = *reinterpret_cast<Smem<R>*>(smem_raw);
   constexpr int kRows = kThreads * R;

@@ -139,7 +139,10 @@ inline ddm_status check_launch() {
   } while (0)
 
 constexpr int kSMs = 148;
-constexpr int kDDRows = 4;  // rows per thread of the d > 1 tile kernel (1024-row tiles)
+#ifndef DDM_DD_ROWS
+#define DDM_DD_ROWS 4
+#endif
+constexpr int kDDRows = DDM_DD_ROWS;  // rows per thread of the d > 1 tile kernel (1024-row tiles)
 
 inline size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -819,7 +822,7 @@ ddm_status build_index_async(const ddm_regions* R, const Index& I, MsdScratch& s
 void launch_dd(int mode, const dd::Args& a, cudaStream_t st) {
   constexpr int kRows = dd::kThreads * kDDRows;
   const unsigned grid = (unsigned)((a.m + kRows - 1) / kRows);
-  const size_t sm = sizeof(dd::Smem<kDDRows>);
+  const size_t sm = dd::smem_bytes<kDDRows>(mode);
   if (mode == dd::kModeCount) dd::dd_tile_kernel<kDDRows, dd::kModeCount><<<grid, dd::kThreads, sm, st>>>(a);
   else if (mode == dd::kModeStage) dd::dd_tile_kernel<kDDRows, dd::kModeStage><<<grid, dd::kThreads, sm, st>>>(a);
   else dd::dd_tile_kernel<kDDRows, dd::kModePlace><<<grid, dd::kThreads, sm, st>>>(a);
