@@ -60,8 +60,18 @@ struct MapRef {
 // bucket sizes change), so it is built from a sample, and when the sample
 // shows no coarse bin denser than kLinearMax x the mean, the plain linear map
 // round(t * NB / kCoarse) is used instead (cheaper per element).
-constexpr uint32_t kSampleChunk = 2048;  // coarse_hist reads 1 chunk of this size ...
-constexpr uint32_t kSampleStride = 16;   // ... out of every kSampleStride
+constexpr uint32_t kSampleChunk = 32;   // the sample: runs of 32 consecutive records (one
+constexpr uint32_t kSampleStride = 16;  // coalesced warp read) out of every 16 runs -- short
+                                        // runs keep it representative for sorted inputs
+
+// i-th record of the sample (i < sample_size(n))
+__host__ __device__ __forceinline__ uint64_t sample_at(uint64_t i) {
+  return (i / kSampleChunk) * (kSampleChunk * kSampleStride) + (i % kSampleChunk);
+}
+__host__ __device__ __forceinline__ uint64_t sample_size(uint64_t n) {
+  const uint64_t period = (uint64_t)kSampleChunk * kSampleStride;
+  return (n / period) * kSampleChunk + umin64(n % period, kSampleChunk);
+}
 constexpr double kLinearMax = 1.5;
 
 struct Bucketer {
@@ -110,23 +120,21 @@ struct Bucketer {
   }
 };
 
-// [min, max] key of the same sample (chunks of kSampleChunk, one in every
+// [min, max] key of the sample (runs of kSampleChunk records, one in every
 // kSampleStride) into mm[0], mm[1] (initialised to [~0, 0]).  Keys outside
 // the sampled range are clamped into the first / last bucket by the
 // Bucketer, so the sample only shapes bucket sizes, never the result.
 template <bool SRC_F64>
 __global__ void __launch_bounds__(512) sample_minmax_kernel(const void* __restrict__ src, uint64_t n,
                                                             uint64_t* __restrict__ mm) {
-  const uint64_t chunks = (n + kSampleChunk - 1) / kSampleChunk;
+  const uint64_t ns = sample_size(n);
   uint64_t lo = ~0ull, hi = 0;
-  for (uint64_t ch = (uint64_t)blockIdx.x * kSampleStride; ch < chunks; ch += (uint64_t)gridDim.x * kSampleStride) {
-    const uint64_t e = umin64(n, (ch + 1) * kSampleChunk);
-    for (uint64_t i = ch * kSampleChunk + threadIdx.x; i < e; i += blockDim.x) {
-      const uint64_t k = SRC_F64 ? f64_key(__ldcs(reinterpret_cast<const double*>(src) + i))
-                                 : __ldcs(reinterpret_cast<const uint64_t*>(src) + i);
-      lo = k < lo ? k : lo;
-      hi = k > hi ? k : hi;
-    }
+  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = sample_at(s);
+    const uint64_t k = SRC_F64 ? f64_key(__ldcs(reinterpret_cast<const double*>(src) + i))
+                               : __ldcs(reinterpret_cast<const uint64_t*>(src) + i);
+    lo = k < lo ? k : lo;
+    hi = k > hi ? k : hi;
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -140,8 +148,8 @@ __global__ void __launch_bounds__(512) sample_minmax_kernel(const void* __restri
   }
 }
 
-// Coarse-bin population of a sample (chunks of kSampleChunk, one in every
-// kSampleStride): counts[kCoarse] (zeroed), counts[kCoarse] = sample size.
+// Coarse-bin population of the sample (runs of kSampleChunk records, one in
+// every kSampleStride): counts[kCoarse] (zeroed), counts[kCoarse] = sample size.
 template <bool SRC_F64>
 __global__ void __launch_bounds__(512) coarse_hist_kernel(const void* __restrict__ src, uint64_t n, MapRef M,
                                                           uint32_t* __restrict__ counts) {
@@ -152,16 +160,14 @@ __global__ void __launch_bounds__(512) coarse_hist_kernel(const void* __restrict
   for (int i = threadIdx.x; i < kCoarse; i += blockDim.x) sh[i] = 0;
   if (threadIdx.x == 0) tot = 0;
   __syncthreads();
-  const uint64_t chunks = (n + kSampleChunk - 1) / kSampleChunk;
+  const uint64_t ns = sample_size(n);
   uint32_t mine = 0;
-  for (uint64_t ch = (uint64_t)blockIdx.x * kSampleStride; ch < chunks; ch += (uint64_t)gridDim.x * kSampleStride) {
-    const uint64_t e = umin64(n, (ch + 1) * kSampleChunk);
-    for (uint64_t i = ch * kSampleChunk + threadIdx.x; i < e; i += blockDim.x) {
-      const uint64_t k = SRC_F64 ? f64_key(__ldcs(reinterpret_cast<const double*>(src) + i))
-                                 : __ldcs(reinterpret_cast<const uint64_t*>(src) + i);
-      atomicAdd(&sh[B.coarse(k)], 1u);
-      ++mine;
-    }
+  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = sample_at(s);
+    const uint64_t k = SRC_F64 ? f64_key(__ldcs(reinterpret_cast<const double*>(src) + i))
+                               : __ldcs(reinterpret_cast<const uint64_t*>(src) + i);
+    atomicAdd(&sh[B.coarse(k)], 1u);
+    ++mine;
   }
   atomicAdd(&tot, mine);
   __syncthreads();

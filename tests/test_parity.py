@@ -913,3 +913,22 @@ def test_index_update_errors_leave_index_untouched():
             ddm.sub_index_update(idx, 10, torch.tensor(ids, dtype=torch.int32), cuda(np.array(nl)), cuda(np.array(nh)))
         assert e.value.status == st
         assert torch.equal(idx, before)
+
+
+def test_msd_sample_unbiased_on_sorted_input(orc):
+    """The bucket map's sample takes short runs spread over the whole array,
+    so already-sorted (or reverse-sorted) inputs get balanced buckets and stay
+    on the MSD path (no LSB fallback launches), with exact results."""
+    rng = np.random.default_rng(12)
+    n = 1_000_000
+    lo = np.sort(rng.uniform(-1.0, 1.0, n))
+    sl, sh = lo[None], (lo + 1e-7)[None]
+    ul, uh = lo[::-1].copy()[None], (lo[::-1] + 1e-7)[None]
+    g = [cuda(x) for x in (sl, sh, ul, uh)]
+    ddm.profile_enable(True)
+    p = ddm.match_pairs(*g)
+    torch.cuda.synchronize()
+    prof = ddm.profile_read()
+    ddm.profile_enable(False)
+    assert not any(k.startswith("onesweep") for k in prof), sorted(prof)
+    assert p.shape[0] == orc.rank_count(sl, sh, ul, uh)

@@ -1,0 +1,37 @@
+"""Adversarial inputs at ~1e7 regions (dev tool): counts against the oracle's
+rank identity, pairs K and invariants, both count forms, LSB fallback."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_1703_06680_b200 import ddm
+import oracle as orc
+
+rng = np.random.default_rng(11)
+N = 5_000_000
+def case(name, sl, sh, ul, uh):
+    g = [torch.from_numpy(np.ascontiguousarray(x[None])).cuda() for x in (sl, sh, ul, uh)]
+    t0 = time.time()
+    ref = orc.rank_count(sl[None], sh[None], ul[None], uh[None])
+    K = ddm.match_count(*g)
+    ok = K == ref
+    msg = f"{name}: K={K} ref={ref} {'OK' if ok else 'MISMATCH'}"
+    if ok and K <= 3e8:
+        for f in (0, ddm.DDM_COUNT_WALK, ddm.DDM_COUNT_RANKS):
+            p = ddm.match_pairs(*g, flags=f)
+            s, u = p[:, 0].long(), p[:, 1].long()
+            good = p.shape[0] == K and bool(((g[0][0][s] <= g[3][0][u]) & (g[2][0][u] <= g[1][0][s])).all())
+            msg += f" pairs[{f:#x}]={'OK' if good else 'BAD'}"
+            del p, s, u
+    print(msg, f"{time.time() - t0:.1f}s", flush=True)
+    torch.cuda.empty_cache()
+
+x = rng.uniform(0, 1e6, N)
+case("all identical points", np.full(N, 5.0), np.full(N, 5.0), np.full(N // 100, 5.0), np.full(N // 100, 5.0))
+case("few distinct values", rng.integers(0, 7, N).astype(float), rng.integers(7, 9, N).astype(float),
+     rng.integers(0, 9, N // 50).astype(float), rng.integers(9, 12, N // 50).astype(float))
+case("one long + sparse", np.r_[0.0, x[1:]], np.r_[2e6, x[1:] + 0.01], x, x + 0.01)
+mm = np.sign(x - 5e5) * 10.0 ** rng.uniform(-300, 300, N)
+um = np.sign(rng.uniform(-1, 1, N // 10)) * 10.0 ** rng.uniform(-300, 300, N // 10)
+case("mixed magnitudes", mm, mm + np.abs(mm) * 1e-3, um, um + np.abs(um) * 1e-3)
+lo = np.sort(rng.uniform(-1, 1, N)); case("sorted input, tiny lengths", lo, lo + 1e-9, lo[::-1].copy(), lo[::-1] + 1e-9)
+c = rng.normal(0, 1e-3, N); case("single dense cluster", c, c + 1e-6, c[:N // 10].copy(), c[:N // 10] + 1e-6)
