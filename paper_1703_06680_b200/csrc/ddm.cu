@@ -1032,7 +1032,12 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
   // sparse outputs (a few pairs per row on average, e.g. alpha ~ 1) gain
   // nothing from staging chunk-start sets: the light per-row kernel (higher
   // occupancy) is used unless the chunk path is forced
-  if (d == 1 && !per_row && (h.K > 4ull * m || (q.flags & DDM_EMIT_FORCE_CHUNK)))
+  if (d == 1 && !per_row && !(q.flags & DDM_EMIT_FORCE_CHUNK) && h.K > 4ull * m && egrid < (unsigned)kSMs) {
+    // few dense rows: (row, segment) tasks spread over every SM
+    const uint64_t warps = m * match::kSplitSeg;
+    const unsigned sgrid = (unsigned)umin64((warps * 32 + 255) / 256, (uint64_t)kSMs * 8);
+    DDM_LAUNCH("emit", 24.0 * m + 8.0 * h.K + 12.0 * n, st, match::emit_split_kernel<<<sgrid, 256, 0, st>>>(A));
+  } else if (d == 1 && !per_row && (h.K > 4ull * m || (q.flags & DDM_EMIT_FORCE_CHUNK)))
     DDM_LAUNCH("emit", 24.0 * m + 8.0 * h.K + 12.0 * n, st,
                match::emit_chunk_kernel<<<egrid, match::kRowTile, sizeof(match::ChunkSmem), st>>>(A));
   else if (d == 1 && !per_row)  // sparse: tiles of 2048 rows walking a staged Slo window

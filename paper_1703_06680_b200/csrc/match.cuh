@@ -1159,6 +1159,63 @@ __global__ void __launch_bounds__(kEmitThreads, DDM_EMIT_MINB) emit_tile_kernel(
   }
 }
 
+// ------------------------------------------------------------ few dense rows (d = 1)
+//
+// When a d = 1 output has few rows with very many pairs each (few updates
+// against many subscriptions), one CTA per 256-row tile would leave the GPU
+// idle.  Here a warp takes one (row, segment) task: segment s writes pairs
+// [s*4096, (s+1)*4096) of the row's range part (the last one the rest),
+// segment 0 also the row's stab part (the backward walk of row_warp).  The
+// row's output offset is its tile's offset plus the counts of the tile's
+// earlier rows.  Output is byte-identical to the other emission paths.
+constexpr int kSplitSeg = 64;
+constexpr uint32_t kSplitLen = 4096;
+
+__global__ void __launch_bounds__(256) emit_split_kernel(const __grid_constant__ EmitArgs A) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t task = wid; task < A.m * kSplitSeg; task += nw) {
+    const uint64_t j = task / kSplitSeg;
+    const uint32_t s = (uint32_t)(task % kSplitSeg);
+    const uint32_t rl = A.r_lo[j], rb = A.r_b[j];
+    const uint32_t nr = rb - rl;
+    const uint64_t seg0 = (uint64_t)s * kSplitLen;
+    if (s > 0 && seg0 >= nr) continue;  // no such segment
+    const uint64_t jt = j & ~(uint64_t)(kRowTile - 1);
+    uint64_t pre = 0;
+    for (uint64_t r = jt + lane; r < j; r += 32) pre += A.cnt[r];
+    pre = warp_sum<uint64_t>(pre);
+    const uint64_t o = A.tile_off[j / kRowTile] + pre;
+    const uint64_t a = A.ulo_key[j];
+    const uint32_t lid = A.ulo_id[j];
+    const uint32_t uid = A.upd_map ? A.upd_map[lid] : lid;
+    const uint32_t stab = A.cnt[j] - nr;
+    if (s == 0) {  // the stab part: walk Slo backwards from r_lo - 1 (row_warp)
+      int64_t hi_excl = rl;
+      uint32_t rem = stab;
+      while (rem) {
+        const int64_t i = hi_excl - 1;
+        if ((i & 31) == 31) {
+          const int L = skip_levels(A.T, i, a);
+          if (L) { hi_excl -= (int64_t)1 << (5 * L); continue; }
+        }
+        const int64_t base = i & ~31ll;
+        const int64_t idx = base + lane;
+        const bool member = idx < hi_excl && A.T.lvl[0][idx] >= a;
+        const unsigned mm = __ballot_sync(kFull, member);
+        rem -= __popc(mm);
+        if (member) A.pairs[o + rem + __popc(mm & lanemask_lt())] = make_uint2(sub_out(A.sub_map, A.slo_id[idx]), uid);
+        hi_excl = base;
+      }
+    }
+    const uint64_t seg_end = s == kSplitSeg - 1 ? nr : umin64(nr, seg0 + kSplitLen);
+    uint2* const rng = A.pairs + o + stab;
+    for (uint64_t k = seg0 + lane; k < seg_end; k += 32)
+      rng[k] = make_uint2(sub_out(A.sub_map, __ldg(A.slo_id + rl + k)), uid);
+  }
+}
+
 // ------------------------------------------------------------ chunked sweep (a6 + a7)
 //
 // One CTA per tile of kRowTile consecutive updates (sorted order), the

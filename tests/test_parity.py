@@ -932,3 +932,18 @@ def test_msd_sample_unbiased_on_sorted_input(orc):
     ddm.profile_enable(False)
     assert not any(k.startswith("onesweep") for k in prof), sorted(prof)
     assert p.shape[0] == orc.rank_count(sl, sh, ul, uh)
+
+
+def test_few_dense_rows_split_emission(orc):
+    """Few updates with very many partners each (few row tiles, K > 4m): the
+    (row, segment) split emission, including rows longer than 64 segments and
+    long-interval stab parts, is byte-identical to every other path and exact
+    against brute force."""
+    rng = np.random.default_rng(31)
+    n, m = 300_000, 40
+    sl = rng.uniform(0, 1e6, n)[None]
+    sh = sl + rng.exponential(20.0, n)[None]
+    sh[0, rng.choice(n, 30, replace=False)] += 5e5  # long subscriptions in the stab parts
+    ul = rng.uniform(0, 6e5, m)[None]
+    uh = ul + rng.uniform(1e3, 4e5, m)[None]        # up to ~1.2e5 range pairs per row
+    check_against(orc, sl, sh, ul, uh, flags=EMIT_FLAGS, ref=orc.bf_pairs(sl, sh, ul, uh))
