@@ -415,6 +415,17 @@ def run_ddm(args):
         dt, ks, P, method = time_oracle(s, count_only=args.mode == "count")
         cpu = {"value": (s.n + s.m) / dt, "unit": "regions/s", "cores": P, "kind": "oracle",
                "sample": f"{sample_text(s, frac)}, K={ks}; {method}, {dt:.2f} s"}
+        if w.d == 1:
+            # also the serial SBM (Alg. 4) on one core, on a
+            # tenth of that window (the paper's serial baseline)
+            import oracle
+            s1 = cpu_sample(w, frac / 10)
+            t0 = time.perf_counter()
+            k1 = oracle.sbm_seq(s1.sub_lo, s1.sub_hi, s1.upd_lo, s1.upd_hi, canonicalize=False).size
+            d1 = time.perf_counter() - t0
+            cpu["serial"] = {"value": (s1.n + s1.m) / d1, "unit": "regions/s", "cores": 1,
+                             "sample": f"{sample_text(s1, frac / 10)}, K={k1}; oracle.sbm_seq (Alg. 4, list mode), "
+                                       f"{d1:.2f} s"}
 
     if roof and roof["kernel"].startswith("dd"):
         # d > 1 (c4): the filter kernel is issue/latency bound, not HBM bound
