@@ -101,8 +101,10 @@ inline void prof_end(const char* name, double bytes, cudaStream_t st, int e0) {
 }
 
 // NAME: kernel class; BYTES: algorithmic DRAM bytes of this launch
+thread_local const char* t_last_launch = "";  // (DDM_DEBUG: named in launch errors)
 #define DDM_LAUNCH(NAME, BYTES, ST, ...)                  \
   do {                                                    \
+    t_last_launch = NAME;                                 \
     const int e0_ = prof_begin(ST);                       \
     __VA_ARGS__;                                          \
     prof_end(NAME, (double)(BYTES), ST, e0_);             \
@@ -125,7 +127,7 @@ inline void prof_end(const char* name, double bytes, cudaStream_t st, int e0) {
 inline ddm_status check_launch() {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
-    if (getenv("DDM_DEBUG")) fprintf(stderr, "libddm: launch error %s\n", cudaGetErrorString(e));
+    if (getenv("DDM_DEBUG")) fprintf(stderr, "libddm: launch error %s (last launch: %s)\n", cudaGetErrorString(e), t_last_launch);
     g_last_cuda.store((int)e);
     return DDM_ERR_CUDA;
   }
@@ -937,6 +939,7 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
   A.F.n = n;
   for (uint32_t k = 0; k < d; ++k) { A.upd.lo[k] = R->upd_lo[k]; A.upd.hi[k] = R->upd_hi[k]; }
   A.m = m;
+  A.abort_flag = use_msd ? &W.misc->overflow : nullptr;
   A.thread_row_max = 16;
   A.force = (q.flags & DDM_EMIT_FORCE_THREAD) ? 1 : (q.flags & DDM_EMIT_FORCE_WARP) ? 2
             : (q.flags & DDM_EMIT_FORCE_CHUNK) ? 3 : 0;

@@ -829,6 +829,7 @@ struct EmitArgs {
   uint64_t m;
   uint32_t thread_row_max;  // rows with <= this many dim-0 candidates go thread-per-row
   uint32_t force;           // 0 auto, 1 thread, 2 warp, 3 chunk (staged) for every tile
+  const uint32_t* abort_flag;  // MSD bucket overflow: the sorted arrays are not valid, do nothing
 };
 
 enum EmitMode { kEmitD1 = 0, kCountDD = 1, kEmitDD = 2 };
@@ -988,6 +989,7 @@ __device__ __forceinline__ void row_warp(const EmitArgs& A, uint64_t j, uint64_t
 // (alpha = 100: ~100 pairs per row) stream coalesced stores.
 template <int MODE>
 __global__ void __launch_bounds__(kRowTile) emit_kernel(const __grid_constant__ EmitArgs A) {
+  if (A.abort_flag && *A.abort_flag) return;  // (the pre-sync d > 1 count runs before the host sees it)
   __shared__ RowSmem R;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t j0 = (uint64_t)blockIdx.x * kRowTile;

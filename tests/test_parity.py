@@ -743,6 +743,15 @@ def test_msd_overflow_falls_back_to_lsb(orc):
     # and the same on the update side
     ref2 = orc.sbm_seq(ul[None], uh[None], lo[None], hi[None])
     check_against(orc, ul, uh, lo, hi, flags=(0, ddm.DDM_SORT_LSB), ref=ref2)
+    # d = 2 with few updates (the per-row filter, which runs before the host
+    # learns of the overflow and must then do nothing), count-only first
+    lo2 = np.stack([lo, rng.uniform(0, 100, lo.size)])
+    hi2 = lo2 + rng.uniform(0, 2, lo2.shape)
+    ul2 = np.stack([ul, rng.uniform(0, 100, ul.size)])
+    uh2 = ul2 + 1.0
+    for _ in range(3):
+        check_against(orc, lo2, hi2, ul2, uh2, flags=(0,), ref=orc.sbm_seq(lo2, hi2, ul2, uh2))
+        check_against(orc, ul2, uh2, lo2, hi2, flags=(0,), ref=orc.sbm_seq(ul2, uh2, lo2, hi2))
 
 
 @pytest.mark.parametrize("n", [1, 700, 769, 5000, 70_000, 300_000])
