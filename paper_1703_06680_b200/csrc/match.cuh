@@ -432,8 +432,14 @@ __device__ __forceinline__ uint64_t lookback_warp_u64(uint64_t* status, uint32_t
 constexpr int kCountThreads = 512;
 constexpr int kCountItems = 4;  // rows per thread (short dependent merge chains, more warps)
 constexpr int kCountTile = kCountThreads * kCountItems;
-constexpr int kCountWin = 3072;  // smem window (keys) per sorted array
-constexpr int kCountExt = 1024;  // Slo window extension past r_lo(a_last) for the r_b searches
+#ifndef DDM_COUNT_WIN
+#define DDM_COUNT_WIN 2560
+#endif
+#ifndef DDM_COUNT_EXT
+#define DDM_COUNT_EXT 256
+#endif
+constexpr int kCountWin = DDM_COUNT_WIN;  // smem window (keys) per sorted array
+constexpr int kCountExt = DDM_COUNT_EXT;  // Slo window extension past r_lo(a_last) for the r_b searches
 constexpr int kRowTile = 256;    // rows per emit CTA == granularity of the row-offset scan
 // Stab-part scans walk Slo backwards from r_lo - 1 and stop after exactly
 // |Stab(a)| = r_lo - r_hi members.  Aligned runs of 32^L positions whose
