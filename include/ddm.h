@@ -7,8 +7,11 @@
  * pair (S_i, U_j) with S_i ∩ U_j ≠ ∅, i.e. for every dimension k
  *        sub_lo[k][i] <= upd_hi[k][j]  &&  upd_lo[k][j] <= sub_hi[k][i].
  * The result is computed by the paper's sort-based matching (Alg. 4/5,
- * P:413-557) re-designed for sm_100a: order-preserving u64 endpoint keys,
- * onesweep LSB radix sort, rank-difference count pass, exclusive scan of the
+ * P:413-557) re-designed for sm_100a: order-preserving u64 endpoint keys, a
+ * value-bucketed MSD sort (stable 8-bit multisplit passes over the bucket id,
+ * then an in-shared-memory sort of every bucket; a stable LSB onesweep radix
+ * sort is the fallback for buckets too large for shared memory and the
+ * DDM_SORT_LSB path), a rank-difference count pass, an exclusive scan of the
  * counts, and a chunked sweep that emits every pair exactly once.
  *
  * Conventions shared by every entry point
@@ -20,13 +23,15 @@
  *  - Pointers marked (device) must be CUDA device pointers (cudaMalloc /
  *    torch CUDA tensors) on the current device; (host) are host pointers.
  *  - Ownership: the caller owns every buffer (inputs, outputs, workspace,
- *    index).  The library allocates no device memory.  Per process it keeps
- *    two internal side streams per device (the sort chains run concurrently
- *    on them, joined back into `stream` by events) and a cache of CUDA graphs:
- *    from the second identical full-match call (same sizes, pointers,
- *    workspace, flags and stream) the pre-sync half is replayed as one graph
- *    launch (DDM_GRAPHS=0 disables).  Graphs read the buffers' current
- *    contents.  Calls are reentrant given distinct workspaces.
+ *    index).  The library allocates no device memory.  It keeps two internal
+ *    side streams and one capture stream per calling thread and device (the
+ *    sort chains run concurrently on them, joined back into `stream` by
+ *    events) and a process-wide cache of CUDA graphs: from the second
+ *    identical full-match call (same sizes, pointers, workspace, flags and
+ *    stream) the pre-sync half is replayed as one graph launch (DDM_GRAPHS=0
+ *    disables); at most 64 instantiated graphs are kept, least recently used
+ *    evicted.  Graphs read the buffers' current contents.  Calls are
+ *    reentrant (thread-safe) given distinct workspaces and output buffers.
  *  - Streams: all device work is stream-ordered on `stream`.  Entry points
  *    that return a count block on one small device->host read of it.
  *  - Alignment: workspace and index must be 256-byte aligned; region arrays
@@ -47,8 +52,14 @@ extern "C" {
 #endif
 
 #define DDM_MAX_DIMS 8
-/* Per-kind region limit: radix-sort look-back words hold 30-bit counts. */
+/* Per-kind region limit: the sorts' decoupled look-back words hold 30-bit
+ * per-digit prefixes (2^30 - 1; SURVEY §8(b) proposed UINT32_MAX -- the
+ * narrower limit still holds every BASELINE config, c5 has 5e8 per kind). */
 #define DDM_MAX_REGIONS 1073741823ull
+/* Largest key count of one radix sort (ddm_sort_pairs' k, the event-order
+ * variant's 2(n_sub + n_upd) endpoints, ddm_radix_sort_u64's n): the same
+ * 30-bit bound.  Larger requests return DDM_ERR_INVALID_ARGUMENT. */
+#define DDM_MAX_SORT_KEYS 1073741823ull
 
 typedef enum {
     DDM_OK = 0,
@@ -139,7 +150,11 @@ ddm_status ddm_match_pairs_mapped(const ddm_regions *regions, const uint32_t *su
                                   void *ws, size_t ws_bytes, cudaStream_t stream);
 
 /* Sort pairs[0..k) (device) in place into canonical order: ascending
- * (upd << 32) | sub.  ids must satisfy sub < n_sub and upd < n_upd. */
+ * (upd << 32) | sub.  ids must satisfy sub < n_sub and upd < n_upd;
+ * k <= DDM_MAX_SORT_KEYS (else DDM_ERR_INVALID_ARGUMENT).  This replaces the
+ * DDM_SORTED flag SURVEY §8(b) proposed: the result is a set and
+ * ddm_match_pairs' own order is already deterministic, so canonical order is
+ * a separate call whose workspace is sized by the K the caller knows. */
 size_t ddm_sort_pairs_workspace_bytes(uint64_t k);
 ddm_status ddm_sort_pairs(ddm_pair *pairs, uint64_t k, uint64_t n_sub, uint64_t n_upd,
                           void *ws, size_t ws_bytes, cudaStream_t stream);

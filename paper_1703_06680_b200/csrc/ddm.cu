@@ -12,6 +12,7 @@
 // one rank and broadcast).
 #include <atomic>
 #include <cmath>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -288,12 +289,24 @@ MsdScratch msd_scratch(Carver& c, uint64_t cap, bool kv) {
   return s;
 }
 
-// Side streams for the concurrent sort chains (per device, created once).
+// Side streams for the concurrent sort chains: per calling thread and device
+// (created on first use), so concurrent callers -- and a graph capture on one
+// thread -- never share a side stream with another thread's eager launches.
 struct SideStreams {
   cudaStream_t s[2] = {nullptr, nullptr};
 };
-std::mutex g_side_mu;
-SideStreams g_side[64];
+struct ThreadStreams {
+  SideStreams side[64];
+  cudaStream_t cap[64] = {};  // capture streams (run_cached)
+  ~ThreadStreams() {
+    for (auto& d : side)
+      for (cudaStream_t x : d.s)
+        if (x) cudaStreamDestroy(x);
+    for (cudaStream_t x : cap)
+      if (x) cudaStreamDestroy(x);
+  }
+};
+thread_local ThreadStreams t_streams;
 
 ddm_status side_streams(cudaStream_t out[2], cudaStream_t st) {
   // one stream while profiling (per-kernel event intervals must not overlap)
@@ -305,8 +318,7 @@ ddm_status side_streams(cudaStream_t out[2], cudaStream_t st) {
   int dev = 0;
   DDM_CUDA_RET(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) return DDM_ERR_CUDA;
-  std::lock_guard<std::mutex> lk(g_side_mu);
-  SideStreams& S = g_side[dev];
+  SideStreams& S = t_streams.side[dev];
   for (int i = 0; i < 2; ++i) {
     if (!S.s[i]) DDM_CUDA_RET(cudaStreamCreateWithFlags(&S.s[i], cudaStreamNonBlocking));
     out[i] = S.s[i];
@@ -324,8 +336,7 @@ ddm_status side_stream_any(cudaStream_t* out, cudaStream_t st) {
   int dev = 0;
   DDM_CUDA_RET(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) return DDM_ERR_CUDA;
-  std::lock_guard<std::mutex> lk(g_side_mu);
-  SideStreams& S = g_side[dev];
+  SideStreams& S = t_streams.side[dev];
   if (!S.s[1]) DDM_CUDA_RET(cudaStreamCreateWithFlags(&S.s[1], cudaStreamNonBlocking));
   *out = S.s[1];
   return DDM_OK;
@@ -542,6 +553,9 @@ ddm_status radix_sort(const void* src, bool src_f64, const uint32_t* vals_in, ui
                       bool hist_ready, SortScratch& s, cudaStream_t st) {
   if (n == 0) return DDM_OK;
   if (P.n == 0) return DDM_ERR_INVALID_ARGUMENT;
+  // the look-back words carry 30-bit per-digit prefixes (radix.cuh): larger
+  // sorts would overflow into the flag bits
+  if (n > radix::kValMask) return DDM_ERR_INVALID_ARGUMENT;
   init_attrs_once();
   if (!hist_ready) {
     DDM_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * radix::kMaxPasses * radix::kRadix, st));
@@ -1078,10 +1092,20 @@ int bits_for(uint64_t v) {  // bits needed to represent v (0 -> 0)
 struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
   int hits = 0;
-  uint64_t launches = 0;  // kernels in the graph (for ddm_kernel_launch_count)
+  bool capturing = false;  // some thread is capturing this key right now
+  bool failed = false;     // capture or instantiation failed: stay eager
+  uint64_t launches = 0;   // kernels in the graph (for ddm_kernel_launch_count)
+  uint64_t last_use = 0;
+  ~GraphEntry() {
+    // an in-flight executable graph is released once it completes
+    if (exec) cudaGraphExecDestroy(exec);
+  }
 };
 std::mutex g_graph_mu;
-std::unordered_map<std::string, GraphEntry> g_graphs;
+std::unordered_map<std::string, std::shared_ptr<GraphEntry>> g_graphs;
+uint64_t g_graph_tick = 0;
+constexpr size_t kMaxGraphs = 64;      // instantiated graphs kept (least recently used evicted)
+constexpr size_t kMaxGraphKeys = 1024; // call sites tracked
 
 bool graphs_enabled() {
   static const bool off = [] {
@@ -1119,57 +1143,93 @@ std::string graph_key(const ddm_regions* R, const void* ws, size_t ws_bytes, uin
   return k;
 }
 
-// Run pre(stream) -- enqueue-only work on `stream` and side streams joined
-// back into it -- through the graph cache.  Capture happens on an internal
-// stream (the caller's may be the legacy default stream, which cannot
-// capture); the instantiated graph is then launched on the caller's stream.
-std::mutex g_cap_mu;
-cudaStream_t g_cap_stream[64] = {};
+// Bound the cache (g_graph_mu held): drop call sites never captured, then the
+// least recently used instantiated graphs.  Entries are shared_ptrs, so a
+// thread still using an evicted entry keeps it alive until it is done.
+void graph_evict_locked() {
+  if (g_graphs.size() > kMaxGraphKeys)
+    for (auto it = g_graphs.begin(); it != g_graphs.end();)
+      it = (!it->second->exec && !it->second->capturing) ? g_graphs.erase(it) : std::next(it);
+  size_t live = 0;
+  for (auto& kv : g_graphs) live += kv.second->exec != nullptr;
+  while (live > kMaxGraphs) {
+    auto victim = g_graphs.end();
+    for (auto it = g_graphs.begin(); it != g_graphs.end(); ++it)
+      if (it->second->exec && (victim == g_graphs.end() || it->second->last_use < victim->second->last_use))
+        victim = it;
+    if (victim == g_graphs.end()) break;
+    g_graphs.erase(victim);
+    --live;
+  }
+}
 
+// Run pre(stream) -- enqueue-only work on `stream` and side streams joined
+// back into it -- through the graph cache.  Capture happens on the calling
+// thread's own capture stream (the caller's may be the legacy default stream,
+// which cannot capture) with the thread's own side streams; the instantiated
+// graph is then launched on the caller's stream.
 template <typename F>
 ddm_status run_cached(const std::string& key, F&& pre, cudaStream_t st) {
-  GraphEntry* e = nullptr;
+  std::shared_ptr<GraphEntry> e;
+  bool capture = false;
   {
     std::lock_guard<std::mutex> lk(g_graph_mu);
-    if (g_graphs.size() > 1024)  // bound the bookkeeping of one-off calls
-      for (auto it = g_graphs.begin(); it != g_graphs.end();) it = it->second.exec ? std::next(it) : g_graphs.erase(it);
-    e = &g_graphs[key];
-    if (!e->exec && ++e->hits < 2) e = nullptr;  // first sighting: run eagerly
+    graph_evict_locked();
+    std::shared_ptr<GraphEntry>& slot = g_graphs[key];
+    if (!slot) slot = std::make_shared<GraphEntry>();
+    slot->last_use = ++g_graph_tick;
+    if (!slot->exec) {
+      if (slot->failed || slot->capturing || ++slot->hits < 2) return pre(st);  // eager
+      slot->capturing = capture = true;
+    }
+    e = slot;
   }
-  if (!e) return pre(st);
-  if (!e->exec) {
-    std::lock_guard<std::mutex> ck(g_cap_mu);  // one capture at a time
+  if (capture) {
+    auto give_up = [&]() {
+      std::lock_guard<std::mutex> lk(g_graph_mu);
+      e->capturing = false;
+      e->failed = true;
+    };
     int dev = 0;
-    DDM_CUDA(cudaGetDevice(&dev));
-    if (dev < 0 || dev >= 64) return pre(st);
-    if (!g_cap_stream[dev]) DDM_CUDA(cudaStreamCreateWithFlags(&g_cap_stream[dev], cudaStreamNonBlocking));
-    cudaStream_t cs = g_cap_stream[dev];
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+      give_up();
+      return pre(st);
+    }
+    cudaStream_t& cs = t_streams.cap[dev];
+    if (!cs && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) {
+      cs = nullptr;
+      give_up();
+      return pre(st);
+    }
     cudaStream_t side[2];
-    DDM_TRY(side_streams(side, cs));  // created outside the capture
-    DDM_TRY(side_stream_any(&side[1], cs));
+    if (side_streams(side, cs) != DDM_OK || side_stream_any(&side[1], cs) != DDM_OK) {  // created outside the capture
+      give_up();
+      return pre(st);
+    }
     const uint64_t l0 = g_launches.load();
-    DDM_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+    if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+      cudaGetLastError();
+      give_up();
+      return pre(st);
+    }
     const ddm_status r = pre(cs);
     cudaGraph_t g = nullptr;
     const cudaError_t ce = cudaStreamEndCapture(cs, &g);
     const uint64_t nl = g_launches.load() - l0;
     g_launches.fetch_sub(nl);  // counted on every replay below instead
-    if (r != DDM_OK || ce != cudaSuccess || !g) {
-      if (g) cudaGraphDestroy(g);
+    cudaGraphExec_t x = nullptr;
+    const bool ok = r == DDM_OK && ce == cudaSuccess && g && cudaGraphInstantiate(&x, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    if (!ok) {
       cudaGetLastError();
       if (getenv("DDM_DEBUG")) fprintf(stderr, "libddm: graph capture failed (%d, %s)\n", (int)r, cudaGetErrorString(ce));
+      give_up();
       return pre(st);  // plain launches
-    }
-    cudaGraphExec_t x = nullptr;
-    const cudaError_t ie = cudaGraphInstantiate(&x, g, 0);
-    cudaGraphDestroy(g);
-    if (ie != cudaSuccess) {
-      cudaGetLastError();
-      return pre(st);
     }
     std::lock_guard<std::mutex> lk(g_graph_mu);
     e->exec = x;
     e->launches = nl;
+    e->capturing = false;
   }
   DDM_CUDA(cudaGraphLaunch(e->exec, st));
   g_launches.fetch_add(e->launches);
@@ -1639,6 +1699,7 @@ extern "C" ddm_status ddm_match_pairs_events(const ddm_regions* R, ddm_pair* pai
                                              uint64_t* count_out, void* ws, size_t ws_bytes, cudaStream_t st) {
   DDM_TRY(check_regions(R, true, true));
   if (!count_out || !aligned(ws, 256) || (pairs && !aligned(pairs, 8))) return DDM_ERR_INVALID_ARGUMENT;
+  if (2 * (R->n_sub + R->n_upd) > DDM_MAX_SORT_KEYS) return DDM_ERR_INVALID_ARGUMENT;  // one endpoint sort
   if (ws_bytes < ddm_events_workspace_bytes(R->d, R->n_sub, R->n_upd)) return DDM_ERR_WORKSPACE;
   init_attrs_once();
   const uint64_t n = R->n_sub, m = R->n_upd;
@@ -1718,6 +1779,7 @@ ddm_status ddm_sort_pairs(ddm_pair* pairs, uint64_t k, uint64_t n_sub, uint64_t 
                           size_t ws_bytes, cudaStream_t stream) {
   if (k == 0) return DDM_OK;
   if (!pairs || !aligned(pairs, 8) || !aligned(ws, 256)) return DDM_ERR_INVALID_ARGUMENT;
+  if (k > DDM_MAX_SORT_KEYS) return DDM_ERR_INVALID_ARGUMENT;  // 30-bit look-back prefixes
   if (ws_bytes < ddm_sort_pairs_workspace_bytes(k)) return DDM_ERR_WORKSPACE;
   Carver c(ws);
   SortScratch s = sort_scratch(c, k, true);

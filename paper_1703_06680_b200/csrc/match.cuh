@@ -755,6 +755,10 @@ __global__ void __launch_bounds__(kRowTile) row_tile_sum_kernel(const uint32_t* 
 // a5: exclusive scan of the row-tile sums (T = ceil(m/256) values) -> the
 // output offset of each tile's first row; total K.  One CTA per 4096 sums,
 // chained by decoupled look-back (a few CTAs even at m = 1e9).
+// status: gridDim.x + 1 zeroed words; the last one is the tile counter: a CTA
+// works on the tile it claims from it, not on blockIdx.x, so every tile whose
+// predecessors it waits on was claimed (is running or done) before it --
+// forward progress does not depend on the order CTAs are scheduled in.
 constexpr int kScanThreads = 512;
 constexpr int kScanItems = 8;
 __global__ void __launch_bounds__(kScanThreads) scan_u64_kernel(const uint64_t* __restrict__ in, uint64_t T,
@@ -763,8 +767,11 @@ __global__ void __launch_bounds__(kScanThreads) scan_u64_kernel(const uint64_t* 
                                                                 uint64_t* __restrict__ k_out) {
   __shared__ uint64_t scan_tmp[kScanThreads / 32 + 1];
   __shared__ uint64_t prefix;
+  __shared__ uint32_t claimed;
   const int tid = threadIdx.x;
-  const uint32_t tile = blockIdx.x;  // tiles are processed in launch order; look-back only reads lower ids
+  if (tid == 0) claimed = (uint32_t)atomicAdd((unsigned long long*)(status + gridDim.x), 1ull);
+  __syncthreads();
+  const uint32_t tile = claimed;
   const uint64_t base = (uint64_t)tile * kScanThreads * kScanItems + (uint64_t)tid * kScanItems;
   uint64_t v[kScanItems];
   uint64_t local = 0;
