@@ -221,6 +221,26 @@ size_t ddm_events_workspace_bytes(uint32_t d, uint64_t n_sub, uint64_t n_upd);
 ddm_status ddm_match_pairs_events(const ddm_regions *regions, ddm_pair *pairs, uint64_t capacity,
                                   uint64_t *count_out, void *ws, size_t ws_bytes, cudaStream_t stream);
 
+/* --- a6 exported for tests: the chunk-start sets.  ddm_match_pairs' dense
+ * emission processes the sorted updates in tiles of DDM_CHUNK_ROWS rows; tile
+ * t starts at the update x_t with the (lower key, id)-rank t*DDM_CHUNK_ROWS,
+ * and its chunk-start set is A_t = Stab(x_t.lo) = {S : S.lo <= x_t.lo <=
+ * S.hi} on dimension 0 -- Alg. 6's SubSet[p] for a segment boundary placed
+ * right before x_t's lower endpoint.
+ * This runs the a1-a5 pipeline and then the same backward walk with
+ * block-max skips that emit_chunk_kernel stages into shared memory, writing:
+ * first_upd[t] (device, tiles = ceil(n_upd / DDM_CHUNK_ROWS)) = x_t's id;
+ * set_off[0..tiles] (device, uint64) = offsets; set_ids[set_off[t] ..
+ * set_off[t+1]) (device) = A_t's subscription ids in (lower key, id) order.
+ * *total_out (host) = sum |A_t|; capacity < total -> DDM_ERR_CAPACITY (ids
+ * not written; first_upd and set_off are).  d must be 1.  n_sub == 0: every
+ * set is empty (set_off zeroed, first_upd not written).  Workspace as
+ * ddm_match_pairs.  Validation errors as ddm_match_pairs. */
+#define DDM_CHUNK_ROWS 256
+ddm_status ddm_chunk_start_sets(const ddm_regions *regions, uint32_t *first_upd, uint64_t *set_off,
+                                uint32_t *set_ids, uint64_t capacity, uint64_t *total_out, void *ws,
+                                size_t ws_bytes, cudaStream_t stream);
+
 /* --- Primitive exported for tests: stable LSB onesweep radix sort of u64
  * keys (device) with optional u32 values, over bits [begin_bit, end_bit).
  * keys_out/vals_out (device) receive the result; inputs are not modified. */

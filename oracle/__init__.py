@@ -12,6 +12,7 @@ Functions (each follows a PAPER.md passage, see oracle/ddm_oracle.c):
   sbm_dd_literal                  per-dim pair sets + sort-merge intersection
   par_sbm                         Alg. 5 + Alg. 6 parallel SBM
   boundary_states / par_states    SubSet[p]/UpdSet[p] snapshots vs Alg. 6
+  states_at                       SubSet snapshots before chosen update lower endpoints
   rank_count                      App. A identity I2 (numpy; O3)
 
 All pins live in tests/test_oracle.py; none of these functions is "parity
@@ -66,6 +67,8 @@ def lib():
         L.orc_sbm_boundary_states.restype = i64
         L.orc_par_sbm_states.argtypes = [i64, i64, dp, dp, dp, dp, i32, u32p, i64p, i64, u32p, i64p, i64]
         L.orc_par_sbm_states.restype = i64
+        L.orc_sbm_states_at.argtypes = [i64, i64, dp, dp, dp, dp, i64p, i64, u32p, i64p, i64]
+        L.orc_sbm_states_at.restype = i64
         L.orc_canonicalize.argtypes = [u64p, i64]
         L.orc_canonicalize.restype = None
         L.orc_max_threads.argtypes = []
@@ -201,6 +204,20 @@ def par_states(sub_lo, sub_hi, upd_lo, upd_hi, P: int):
     return _states(lib().orc_par_sbm_states, sub_lo, sub_hi, upd_lo, upd_hi, P)
 
 
+def states_at(sub_lo, sub_hi, upd_lo, upd_hi, upd_ids) -> list:
+    """Sequential-sweep SubSet snapshot right before the lower endpoint of
+    each update in `upd_ids` (d = 1; sorted id arrays, one per query)."""
+    d, n, m, a = _args(sub_lo, sub_hi, upd_lo, upd_hi)
+    if d != 1:
+        raise ValueError("one sweep dimension")
+    q = np.ascontiguousarray(upd_ids, dtype=np.int64)
+    off = np.zeros(q.size + 1, dtype=np.int64)
+    total = _check(lib().orc_sbm_states_at(n, m, *map(_ptr, a), _ptr(q), q.size, None, _ptr(off), 0))
+    ids = np.empty(max(total, 1), dtype=np.uint32)
+    _check(lib().orc_sbm_states_at(n, m, *map(_ptr, a), _ptr(q), q.size, _ptr(ids), _ptr(off), total))
+    return [ids[off[r]:off[r + 1]].copy() for r in range(q.size)]
+
+
 def max_threads() -> int:
     return int(lib().orc_max_threads())
 
@@ -213,6 +230,9 @@ def rank_count(sub_lo, sub_hi, upd_lo, upd_hi) -> int:
         raise ValueError("rank identity is per dimension")
     slo = np.sort(sl[0])
     shi = np.sort(sh[0])
-    a = np.searchsorted(slo, uh[0], side="right").astype(np.int64).sum()
-    b = np.searchsorted(shi, ul[0], side="left").astype(np.int64).sum()
+    # the sums do not depend on the order of the queries: searching them in
+    # ascending order keeps the binary searches cache-resident (c5: 5e8
+    # queries in under a minute instead of a quarter of an hour)
+    a = np.searchsorted(slo, np.sort(uh[0]), side="right").astype(np.int64).sum()
+    b = np.searchsorted(shi, np.sort(ul[0]), side="left").astype(np.int64).sum()
     return int(a - b)

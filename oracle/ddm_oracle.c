@@ -23,6 +23,8 @@
  *   orc_sbm_boundary_states / orc_par_sbm_states
  *                   SubSet[p]/UpdSet[p] from the sequential sweep
  *                   and from Alg. 6 -- the boundary-state oracle.
+ *   orc_sbm_states_at  the same sequential snapshots taken right before
+ *                   chosen update lower endpoints (GPU chunk-start sets).  [pinned]
  *
  * Endpoint order (reading R1): T is sorted by
  * (coordinate, lower-before-upper, subscription-before-update, id).  The paper
@@ -386,6 +388,65 @@ int64_t orc_sbm_boundary_states(int64_t n, int64_t m, const double *sl, const do
     free(bounds);
     free(T);
     return rc == ORC_OK ? ws + wu : rc;
+}
+
+/* Sequential-sweep snapshots at chosen update lower endpoints: SubSet right
+ * before the lower endpoint of update q[r] is processed (the same snapshot as
+ * P:552-557, taken at a segment boundary placed just before that endpoint),
+ * for r = 0..nq-1, ids sorted ascending.  This is the chunk-start set of a
+ * GPU tile whose first update is q[r].
+ * sub_off has nq+1 entries; returns the number of ids (sub_ids == NULL: only
+ * sizes them and fills sub_off), or a negative error (capacity, duplicate /
+ * out-of-range query ids). */
+int64_t orc_sbm_states_at(int64_t n, int64_t m, const double *sl, const double *sh,
+                          const double *ul, const double *uh, const int64_t *q, int64_t nq,
+                          uint32_t *sub_ids, int64_t *sub_off, int64_t sub_cap) {
+    int64_t N2 = 2 * (n + m);
+    int64_t *slot = (int64_t *)malloc(sizeof(int64_t) * (size_t)(m > 0 ? m : 1));
+    int64_t *cnt = (int64_t *)calloc((size_t)(nq + 1), sizeof(int64_t));
+    if (!slot || !cnt) { free(slot); free(cnt); return ORC_ERR_ALLOC; }
+    for (int64_t j = 0; j < m; ++j) slot[j] = -1;
+    for (int64_t r = 0; r < nq; ++r) {
+        if (q[r] < 0 || q[r] >= m || slot[q[r]] >= 0) { free(slot); free(cnt); return ORC_ERR_ARG; }
+        slot[q[r]] = r;
+    }
+    endpoint *T = build_T(0, n, m, sl, sh, ul, uh);
+    if (!T) { free(slot); free(cnt); return ORC_ERR_ALLOC; }
+    qsort(T, (size_t)N2, sizeof(endpoint), cmp_endpoint);
+    idset SubSet, UpdSet;
+    if (idset_init(&SubSet, n) || idset_init(&UpdSet, m)) { free(T); free(slot); free(cnt); return ORC_ERR_ALLOC; }
+    /* pass 1: snapshot sizes; pass 2: the members, at offsets from pass 1 */
+    pairbuf pb = {0};
+    for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 1) {
+            sub_off[0] = 0;
+            for (int64_t r = 0; r < nq; ++r) sub_off[r + 1] = sub_off[r] + cnt[r];
+            if (!sub_ids || sub_off[nq] > sub_cap) break;  /* size query / too small */
+            SubSet.size = 0;
+            UpdSet.size = 0;
+            for (int64_t i = 0; i < n; ++i) SubSet.pos[i] = -1;
+            for (int64_t j = 0; j < m; ++j) UpdSet.pos[j] = -1;
+        }
+        for (int64_t t = 0; t < N2; ++t) {
+            if (T[t].kind == 1 && !T[t].is_upper && slot[T[t].id] >= 0) {
+                const int64_t r = slot[T[t].id];
+                if (pass == 0) cnt[r] = SubSet.size;
+                else {
+                    int64_t w = sub_off[r];
+                    states_flatten(&SubSet, sub_ids, &w, sub_off[r] + SubSet.size);
+                }
+            }
+            sbm_step(&T[t], &SubSet, &UpdSet, &pb, 1, 1, sl, sh, n, ul, uh, m);
+        }
+    }
+    int64_t total = 0;
+    for (int64_t r = 0; r < nq; ++r) total += cnt[r];
+    idset_free(&SubSet);
+    idset_free(&UpdSet);
+    free(T);
+    free(slot);
+    free(cnt);
+    return (sub_ids && total > sub_cap) ? ORC_ERR_ARG : total;
 }
 
 /* ------------------------------------------------ Parallel SBM (Alg. 5+6) */

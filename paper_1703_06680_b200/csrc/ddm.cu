@@ -846,6 +846,15 @@ void launch_dd(int mode, const dd::Args& a, cudaStream_t st) {
 
 // ------------------------------------------------------------ match against an index
 
+// ddm_chunk_start_sets: export A_t of every emit tile instead of emitting
+struct ChunkExport {
+  uint32_t* first_upd;
+  uint64_t* off;
+  uint32_t* ids;
+  uint64_t cap;
+  uint64_t* total_out;
+};
+
 struct MatchReq {
   const Index* I;
   const ddm_regions* R;       // update side (d, n_upd, upd_lo/hi)
@@ -855,6 +864,7 @@ struct MatchReq {
   uint32_t flags;
   const uint32_t* sub_map = nullptr;  // optional global ids of the subscriptions
   bool walk = false;                  // walk-form counts (index holds the slo_hi prefix maxima, not Shi)
+  const ChunkExport* chunk = nullptr;  // export the chunk-start sets (d = 1) instead of the pairs
 };
 
 // Update side, a1 + a2 (+ a3): validate every dimension, sort Ulo with the
@@ -1036,6 +1046,26 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
   *count_out = h.K;
   DDM_TRY(err_status(h.err));
   if (h.overflow) return kRetryLSB;  // degenerate bucket: nothing written yet, redo with the LSB sort
+  if (q.chunk) {
+    // a6 exported: |A_t| per emit tile -> offsets (scan) -> members by the
+    // emit_chunk_kernel walk
+    const ChunkExport& C = *q.chunk;
+    DDM_LAUNCH("chunk_sets", 12.0 * rtiles, st, match::chunk_set_sizes_kernel<<<(unsigned)((rtiles + 255) / 256), 256, 0, st>>>(
+        A, rtiles, W.tile_sum, C.first_upd));
+    DDM_TRY(check_launch());
+    DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (stiles + 1), st));
+    DDM_LAUNCH("scan", 16.0 * rtiles, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
+        W.tile_sum, rtiles, C.off, W.scan_status, C.off + rtiles));
+    DDM_TRY(check_launch());
+    uint64_t total = 0;
+    DDM_CUDA(cudaMemcpyAsync(&total, C.off + rtiles, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    DDM_CUDA(cudaStreamSynchronize(st));
+    *C.total_out = total;
+    if (total > C.cap) return DDM_ERR_CAPACITY;
+    DDM_LAUNCH("chunk_sets", 4.0 * total, st, match::chunk_set_ids_kernel<<<(unsigned)rtiles, 32, 0, st>>>(
+        A, C.off, C.ids));
+    return check_launch();
+  }
   if (!q.pairs) return DDM_OK;
   if (h.K > q.capacity) return DDM_ERR_CAPACITY;
   if (h.K == 0) return DDM_OK;
@@ -1375,6 +1405,45 @@ static ddm_status match_full(const ddm_regions* R, ddm_pair* pairs, uint64_t cap
     else
       DDM_TRY(pre(st));
     const ddm_status r = match_sorted(q, W, count_out, use_msd, st, kPhasePost);
+    if (r != kRetryLSB) return r;
+  }
+  return DDM_ERR_CUDA;
+}
+
+ddm_status ddm_chunk_start_sets(const ddm_regions* R, uint32_t* first_upd, uint64_t* set_off, uint32_t* set_ids,
+                                uint64_t capacity, uint64_t* total_out, void* ws, size_t ws_bytes,
+                                cudaStream_t st) {
+  DDM_TRY(check_regions(R, true, true));
+  if (R->d != 1 || !total_out || !aligned(ws, 256)) return DDM_ERR_INVALID_ARGUMENT;
+  if (R->n_upd && (!first_upd || !set_off || (capacity && !set_ids))) return DDM_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < ddm_workspace_bytes(R->d, R->n_sub, R->n_upd, 1)) return DDM_ERR_WORKSPACE;
+  *total_out = 0;
+  if (R->n_upd == 0 || R->n_sub == 0) {
+    const uint64_t tiles = (R->n_upd + match::kRowTile - 1) / match::kRowTile;
+    if (tiles) DDM_CUDA(cudaMemsetAsync(set_off, 0, sizeof(uint64_t) * (tiles + 1), st));
+    // (first_upd of an empty-index tile still names its first update: not needed by callers)
+    uint64_t k = 0;
+    ddm_pair dummy;
+    ddm_status r = match_full(R, &dummy, 0, &k, DDM_COUNT_RANKS, ws, ws_bytes, st);  // validation only
+    return r == DDM_ERR_CAPACITY ? DDM_OK : r;
+  }
+  init_attrs_once();
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  Index I = index_layout(R->d, R->n_sub, base);
+  MatchWs W = match_layout(R->d, R->n_sub, R->n_upd, base + a256(I.bytes), true);
+  ChunkExport C{first_upd, set_off, set_ids, capacity, total_out};
+  ddm_pair dummy;
+  MatchReq q{&I, R, nullptr, &dummy, 0, DDM_COUNT_RANKS};
+  q.chunk = &C;
+  uint64_t K = 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const bool use_msd = attempt == 0;
+    DDM_CUDA(cudaMemsetAsync(W.misc, 0, sizeof(Misc), st));
+    DDM_TRY(init_minmax(W.mm, st));
+    DDM_TRY(build_index_async(R, I, W.slo, W.shi, W.sort, W.mm, W.misc, use_msd, st, kNeedShi));
+    DDM_TRY(upd_sort_async(R, W, R->n_sub, use_msd, st));
+    DDM_TRY(match_sorted(q, W, &K, use_msd, st, kPhasePre));
+    const ddm_status r = match_sorted(q, W, &K, use_msd, st, kPhasePost);
     if (r != kRetryLSB) return r;
   }
   return DDM_ERR_CUDA;

@@ -1340,6 +1340,54 @@ __device__ __forceinline__ void chunk_row_warp(const ChunkSmem& S, const EmitArg
   for (uint32_t t = in_slice + lane; t < nr; t += 32) rng[t] = make_uint2(sub_out(A.sub_map, A.slo_id[rl + t]), uid);
 }
 
+// a6: the chunk-start set A_t = Stab(x_t) = {i < r_lo(x_t) : slo_hi[i] >= x_t}
+// (Alg. 6 SubSet[p] at a boundary placed before the tile's first update, App.
+// A I6), |A_t| = nact known exactly from the counts.  One warp walks Slo
+// backwards from r_lo(x_t) with block-max skips and hands every member to
+// sink(pos, upper key, output id), pos = its rank in Slo order (0..nact).
+template <typename Sink>
+__device__ __forceinline__ void walk_chunk_start(const EmitArgs& A, int64_t rl0, uint64_t x, uint32_t nact, int lane,
+                                                 Sink&& sink) {
+  int64_t hi_excl = rl0;
+  uint32_t rem = nact;
+  while (rem) {
+    const int64_t i = hi_excl - 1;
+    if ((i & 31) == 31) {
+      const int L = skip_levels(A.T, i, x);
+      if (L) { hi_excl -= (int64_t)1 << (5 * L); continue; }
+    }
+    const int64_t base = i & ~31ll;
+    const int64_t idx = base + lane;
+    uint64_t h = 0;
+    const bool member = idx < hi_excl && (h = A.T.lvl[0][idx]) >= x;
+    const unsigned mm = __ballot_sync(kFull, member);
+    rem -= __popc(mm);
+    if (member) sink(rem + __popc(mm & lanemask_lt()), h, sub_out(A.sub_map, A.slo_id[idx]));
+    hi_excl = base;
+  }
+}
+
+// ddm_chunk_start_sets (exported for tests): |A_t| of every kRowTile-row tile
+// of emit_chunk_kernel, then the members through the same walk.
+__global__ void __launch_bounds__(256) chunk_set_sizes_kernel(const __grid_constant__ EmitArgs A, uint64_t tiles,
+                                                              uint64_t* __restrict__ sizes,
+                                                              uint32_t* __restrict__ first_upd) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= tiles) return;
+  const uint64_t j0 = t * kRowTile;
+  sizes[t] = A.cnt[j0] - (A.r_b[j0] - A.r_lo[j0]);
+  first_upd[t] = A.upd_map ? A.upd_map[A.ulo_id[j0]] : A.ulo_id[j0];
+}
+__global__ void __launch_bounds__(32) chunk_set_ids_kernel(const __grid_constant__ EmitArgs A,
+                                                          const uint64_t* __restrict__ off,
+                                                          uint32_t* __restrict__ ids) {
+  const uint64_t t = blockIdx.x, j0 = t * kRowTile;
+  const uint32_t nact = (uint32_t)(off[t + 1] - off[t]);
+  uint32_t* out = ids + off[t];
+  walk_chunk_start(A, (int64_t)A.r_lo[j0], A.ulo_key[j0], nact, threadIdx.x & 31,
+                   [&](uint32_t pos, uint64_t, uint32_t id) { out[pos] = id; });
+}
+
 __global__ void __launch_bounds__(kRowTile) emit_chunk_kernel(const __grid_constant__ EmitArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ChunkSmem& S = *reinterpret_cast<ChunkSmem*>(smem_raw);
@@ -1364,29 +1412,11 @@ __global__ void __launch_bounds__(kRowTile) emit_chunk_kernel(const __grid_const
     S.nact = nact;
   }
   if (warp == 0) {
-    if (fits) {  // warp 0 walks Slo backwards from r_lo(x_t) with block-max skips
-      int64_t hi_excl = (int64_t)rl0;
-      uint32_t rem = nact;
-      while (rem) {
-        const int64_t i = hi_excl - 1;
-        if ((i & 31) == 31) {
-          const int L = skip_levels(A.T, i, x);
-          if (L) { hi_excl -= (int64_t)1 << (5 * L); continue; }
-        }
-        const int64_t base = i & ~31ll;
-        const int64_t idx = base + lane;
-        uint64_t h = 0;
-        const bool member = idx < hi_excl && (h = A.T.lvl[0][idx]) >= x;
-        const unsigned mm = __ballot_sync(kFull, member);
-        rem -= __popc(mm);
-        if (member) {
-          const uint32_t pos = rem + __popc(mm & lanemask_lt());
-          S.ahi[pos] = h;
-          S.aid[pos] = sub_out(A.sub_map, A.slo_id[idx]);
-        }
-        hi_excl = base;
-      }
-    }
+    if (fits)  // warp 0 walks Slo backwards from r_lo(x_t) with block-max skips
+      walk_chunk_start(A, (int64_t)rl0, x, nact, lane, [&](uint32_t pos, uint64_t h, uint32_t id) {
+        S.ahi[pos] = h;
+        S.aid[pos] = id;
+      });
   } else if (fits) {  // the other warps stage the Slo slice meanwhile
     for (uint32_t k = tid - 32; k < slen; k += kRowTile - 32) {
       S.shi[k] = __ldcs(A.T.lvl[0] + rl0 + k);

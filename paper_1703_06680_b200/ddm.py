@@ -88,6 +88,7 @@ def load() -> ctypes.CDLL:
         "ddm_sub_index_update": ([vp, vp, sz, u64, R, vp, vp, sz, vp], i32),
         "ddm_match_pairs_events": ([R, vp, u64, ctypes.POINTER(u64), vp, sz, vp], i32),
         "ddm_match_count_indexed": ([vp, R, ctypes.POINTER(u64), vp, sz, vp], i32),
+        "ddm_chunk_start_sets": ([R, vp, vp, vp, u64, ctypes.POINTER(u64), vp, sz, vp], i32),
         "ddm_radix_sort_workspace_bytes": ([u64], sz),
         "ddm_radix_sort_u64": ([vp, vp, vp, vp, u64, i32, i32, vp, sz, vp], i32),
         "ddm_encode_keys": ([vp, vp, u64, vp], i32),
@@ -112,6 +113,7 @@ EXPORTED = ["ddm_workspace_bytes", "ddm_match_count", "ddm_match_pairs", "ddm_ma
             "ddm_indexed_workspace_bytes", "ddm_match_pairs_indexed", "ddm_match_count_indexed",
             "ddm_events_workspace_bytes", "ddm_match_pairs_events",
             "ddm_sub_index_update_workspace_bytes", "ddm_sub_index_update",
+            "ddm_chunk_start_sets",
             "ddm_radix_sort_workspace_bytes", "ddm_radix_sort_u64", "ddm_encode_keys", "ddm_status_string",
             "ddm_last_cuda_error", "ddm_kernel_launch_count", "ddm_build_info", "ddm_profile_enable",
             "ddm_profile_read"]
@@ -316,6 +318,33 @@ def match_pairs(sub_lo, sub_hi, upd_lo, upd_hi, flags: int = 0, sort: bool = Fal
     if sort:
         sort_pairs(out, r.n_sub, r.n_upd)
     return out
+
+
+DDM_CHUNK_ROWS = 256
+
+
+def chunk_start_sets(sub_lo, sub_hi, upd_lo, upd_hi):
+    """a6 exported (ddm_chunk_start_sets, d = 1): for every tile of
+    DDM_CHUNK_ROWS sorted updates, (first update id x_t, A_t = Stab(x_t.lo) as
+    subscription ids in Slo order).  Returns (first_upd [tiles] int32,
+    offsets [tiles+1] int64, ids [total] int32) CUDA tensors."""
+    L = load()
+    r, keep = regions(sub_lo, sub_hi, upd_lo, upd_hi)
+    dev = keep[0].device if keep else torch.device("cuda")
+    ws = _workspace(L.ddm_workspace_bytes(r.d, r.n_sub, r.n_upd, 1), dev)
+    tiles = (r.n_upd + DDM_CHUNK_ROWS - 1) // DDM_CHUNK_ROWS
+    first = torch.empty(max(tiles, 1), dtype=torch.int32, device=dev)
+    off = torch.zeros(tiles + 1, dtype=torch.int64, device=dev)
+    T = ctypes.c_uint64(0)
+    st = _stream(dev)
+    s = L.ddm_chunk_start_sets(ctypes.byref(r), first.data_ptr(), off.data_ptr(), None, 0, ctypes.byref(T),
+                               ws.data_ptr(), ws.numel(), st)
+    if s not in (0, 4):
+        _check(s, "ddm_chunk_start_sets(size)")
+    ids = torch.empty(max(int(T.value), 1), dtype=torch.int32, device=dev)
+    _check(L.ddm_chunk_start_sets(ctypes.byref(r), first.data_ptr(), off.data_ptr(), ids.data_ptr(), ids.numel(),
+                                  ctypes.byref(T), ws.data_ptr(), ws.numel(), st), "ddm_chunk_start_sets")
+    return first[:tiles], off, ids[: int(T.value)]
 
 
 def match_pairs_events(sub_lo, sub_hi, upd_lo, upd_hi, sort: bool = True) -> torch.Tensor:

@@ -255,6 +255,80 @@ def test_alg6_inline_formula_index_shift_is_wrong(orc):
     assert seq_s[1].tolist() == [0] and par_s[1].tolist() == [0]
 
 
+def _endpoint_order(sl, sh, ul, uh):
+    """Positions of the sorted endpoint list T by (coord, is_upper, kind, id)
+    (reading R1/R2), as records (kind, is_upper, id) -- test-side only."""
+    n, m = sl.shape[1], ul.shape[1]
+    x = np.concatenate([sl[0], sh[0], ul[0], uh[0]])
+    up = np.concatenate([np.zeros(n), np.ones(n), np.zeros(m), np.ones(m)]).astype(np.int64)
+    kind = np.concatenate([np.zeros(2 * n), np.ones(2 * m)]).astype(np.int64)
+    ids = np.concatenate([np.arange(n), np.arange(n), np.arange(m), np.arange(m)])
+    o = np.lexsort((ids, kind, up, x))
+    return kind[o], up[o], ids[o]
+
+
+def test_states_at_equals_boundary_states_and_stab_definition(orc):
+    """states_at (snapshot right before chosen update lower endpoints) is
+    pinned two ways: (a) where a segment of the SPEC S:240-247 plan starts at
+    an update lower endpoint, it equals boundary_states' SubSet[p] (P:552-557);
+    (b) it equals the stabbing-set definition {S : S.lo <= a <= S.hi} (I6 with
+    lowers before uppers at ties, reading R1) evaluated by brute force."""
+    rng = np.random.default_rng(91)
+    checked_a = 0
+    for trial in range(40):
+        if trial % 2:
+            S, U = rand_int_boxes(rng, rng.integers(1, 25), 1), rand_int_boxes(rng, rng.integers(1, 25), 1)
+            sl, sh, ul, uh = to_arrays(S, U, 1)
+        else:
+            w = wl.uniform(int(rng.integers(1, 200)), int(rng.integers(1, 200)), 1e3, 40.0, 1, seed=100 + trial)
+            sl, sh, ul, uh = w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi
+        m = ul.shape[1]
+        q = rng.permutation(m)[: max(1, m // 2)]
+        got = orc.states_at(sl, sh, ul, uh, q)
+        for r, j in enumerate(q):  # (b) definition
+            a = ul[0, j]
+            assert np.array_equal(got[r], np.nonzero((sl[0] <= a) & (a <= sh[0]))[0]), (trial, j)
+        # (a) segment starts that are update lower endpoints
+        kind, up, ids = _endpoint_order(sl, sh, ul, uh)
+        N2 = kind.size
+        for P in (2, 3, 5, 8):
+            base, rem = divmod(N2, P)
+            starts = np.cumsum([0] + [base + (1 if p < rem else 0) for p in range(P - 1)])
+            seq_s, _ = orc.boundary_states(sl, sh, ul, uh, P)
+            for p, t in enumerate(starts):
+                if t < N2 and kind[t] == 1 and up[t] == 0:
+                    (snap,) = orc.states_at(sl, sh, ul, uh, [ids[t]])
+                    assert np.array_equal(snap, seq_s[p]), (trial, P, p)
+                    checked_a += 1
+    assert checked_a > 20
+
+
+def test_states_at_errors(orc):
+    a = to_arrays([[(0.0, 1.0)]], [[(0.5, 0.7)]], 1)
+    with pytest.raises(RuntimeError):
+        orc.states_at(*a, [0, 0])  # duplicate query
+    with pytest.raises(RuntimeError):
+        orc.states_at(*a, [1])  # out of range
+
+
+def test_oracle_by_cells_equals_whole(orc):
+    """tests.helpers.oracle_list_by_cells (the full-size c4 parity check
+    assembles the oracle's list over 3-D cells) returns the oracle's
+    whole-instance list (d = 1..3, side lengths up to the cell size, ties on
+    cell edges)."""
+    from tests.helpers import oracle_list_by_cells
+    rng = np.random.default_rng(5)
+    for d in (1, 2, 3):
+        n, m = 3000, 2500
+        sl = np.floor(rng.uniform(0, 200, (d, n)))
+        ul = np.floor(rng.uniform(0, 200, (d, m)))
+        sh = sl + np.floor(rng.uniform(0, 20, (d, n)))
+        uh = ul + np.floor(rng.uniform(0, 20, (d, m)))
+        w = wl.Workload("t", d, 200.0, 20.0, 0, sl, sh, ul, uh)
+        got = oracle_list_by_cells(orc, w, 20.0)
+        assert got.size > 1000 and np.array_equal(got, orc.sbm_seq(sl, sh, ul, uh))
+
+
 # ------------------------------------------------------------ generator
 
 def test_generator_length_formula():

@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 
 from paper_1703_06680_b200 import ddm
 from paper_1703_06680_b200 import workload as wl
-from tests.helpers import cuda, gpu_args, raw_words, words_of
+from tests.helpers import arrays, cuda, gpu_args, oracle_list_by_cells, raw_words, words_of
 
 EMIT_FLAGS = [ddm.DDM_EMIT_AUTO, ddm.DDM_EMIT_FORCE_THREAD, ddm.DDM_EMIT_FORCE_WARP, ddm.DDM_EMIT_FORCE_CHUNK,
               ddm.DDM_SORT_LSB, ddm.DDM_SORT_LSB | ddm.DDM_EMIT_FORCE_CHUNK,
@@ -346,26 +346,23 @@ def test_dd_tie_storms(orc, d):
         check_against(orc, s[0], s[1], u[0], u[1], flags=EMIT_FLAGS, ref=ref)
 
 
-def test_c4_full_sampled(orc):
-    """c4 at full size (d = 3, N = 1e7): sampled rows against brute force
-    (Alg. 2 with the d-dim conjunction), list invariants on the device, the
-    count entry point equal to the list length, and K within 5 sigma of the
-    closed form n*m*p^3."""
+def test_c4_full_exact(orc):
+    """c4 at full size (d = 3, N = 1e7): the whole GPU pair list is
+    byte-identical to the oracle's (serial SBM, Alg. 4 + filter, assembled
+    over 3-D cells of side 500 -- every pair of the instance, no sampling),
+    and the count entry point agrees (BASELINE north star: bit-exact K and
+    list on every config)."""
     w = wl.make("c4")
     g = gpu_args(w)
     p = ddm.match_pairs(*g)
     K = p.shape[0]
     assert ddm.match_count(*g) == K
-    E = wl.expected_pairs_uniform(w.n, w.m, w.L, w.l, 3)
-    assert abs(K - E) <= 5 * wl.stddev_bound(E)
-    s, u = p[:, 0].long(), p[:, 1].long()
-    ok = torch.ones(K, dtype=torch.bool, device=p.device)
-    for k in range(3):
-        ok &= (g[0][k][s] <= g[3][k][u]) & (g[2][k][u] <= g[1][k][s])
-    assert bool(ok.all())
-    wds = torch.sort((u << 32) | s).values
-    assert bool((wds[1:] > wds[:-1]).all())
-    _check_sampled_rows(orc, w, p, n_rows=1500)
+    got = words_of(p)
+    del p, g
+    torch.cuda.empty_cache()
+    ref = oracle_list_by_cells(orc, w, 500.0)
+    assert ref.size == K
+    assert np.array_equal(got, ref)
 
 
 def test_dd_chunks_and_long_intervals(orc):
@@ -426,8 +423,9 @@ def test_dd_deterministic_output():
 
 
 def test_c5_full_windows(orc):
-    """c5 at full size (N = 1e9, clustered, the bench configuration): the list
-    invariants on the device, count == list length, sampled rows against
+    """c5 at full size (N = 1e9, clustered, the bench configuration): K equal
+    to the oracle's rank-identity count, the list invariants on the device
+    (together: the list is the exact result set), count == list length, sampled rows against
     brute force over all 5e8 subscriptions, and three exact slices: every
     update whose lower bound lies in a window, matched by the oracle's
     Parallel-SBM against every subscription that can reach the window (lower
@@ -438,6 +436,10 @@ def test_c5_full_windows(orc):
     p = ddm.match_pairs(*g)
     K = p.shape[0]
     assert ddm.match_count(*g) == K
+    # the oracle's count over all 1e9 regions (I2 rank identity, O3): with the
+    # device checks below (every listed pair overlaps, no duplicates) this
+    # proves the GPU list IS the result set -- a subset of the right size
+    assert K == orc.rank_count(w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi)
     s, u = p[:, 0].long(), p[:, 1].long()
     assert bool(((g[0][0][s] <= g[3][0][u]) & (g[2][0][u] <= g[1][0][s])).all())
     wds = torch.sort((u << 32) | s).values
@@ -728,6 +730,47 @@ def test_slab_partitions_mapped_equal_single(orc, d):
             assert k == K
             allw.append(raw_words(out[:k]))
         assert np.array_equal(np.sort(np.concatenate(allw)), ref), f"G={G}"
+
+
+def _check_chunk_sets(orc, sl, sh, ul, uh):
+    """GPU chunk-start sets A_t (a6, the emit_chunk_kernel walk) equal the
+    oracle's sequential-sweep SubSet snapshot before each tile's first update
+    (oracle.states_at), member for member, in Slo order."""
+    sl, sh, ul, uh = arrays(sl, sh, ul, uh)
+    first, off, ids = ddm.chunk_start_sets(cuda(sl), cuda(sh), cuda(ul), cuda(uh))
+    first, off, ids = first.cpu().numpy(), off.cpu().numpy(), ids.cpu().numpy().astype(np.int64)
+    # the tiles start at every DDM_CHUNK_ROWS-th update in (lower bound, id) order
+    order = np.lexsort((np.arange(ul.shape[1]), ul[0]))
+    assert np.array_equal(first, order[::ddm.DDM_CHUNK_ROWS])
+    ref = orc.states_at(sl, sh, ul, uh, first)
+    for t in range(first.size):
+        got = ids[off[t]:off[t + 1]]
+        assert np.array_equal(np.sort(got), ref[t].astype(np.int64)), f"tile {t}"
+        # Slo order: (lower bound, id) ascending
+        assert np.all(np.lexsort((got, sl[0, got])) == np.arange(got.size))
+    return int(off[-1])
+
+
+def test_chunk_start_sets_equal_sweep_states(orc):
+    rng = np.random.default_rng(71)
+    total = 0
+    # dense overlaps (c2 recipe scaled), ties on a grid, long intervals
+    w = wl.uniform(60_000, 50_000, 1e5, wl.side_length(110_000, 1e5, 100.0, 1), 1, seed=71)
+    total += _check_chunk_sets(orc, w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi)
+    sl = np.floor(rng.uniform(0, 3000, 20_000))
+    ul = np.floor(rng.uniform(0, 3000, 30_000))
+    total += _check_chunk_sets(orc, sl, sl + np.floor(rng.uniform(0, 40, sl.size)), ul, ul + 3.0)
+    sl = rng.uniform(0, 1e6, 40_000)
+    sh = sl + 5.0
+    sh[:30] = 1e6 + 1.0  # spans everything: members of every A_t, reached past block-max skips
+    ul = rng.uniform(0, 1e6, 20_000)
+    total += _check_chunk_sets(orc, sl, sh, ul, ul + 5.0)
+    assert total > 10_000
+
+
+def test_chunk_start_sets_c2_full(orc):
+    w = wl.make("c2")
+    assert _check_chunk_sets(orc, w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi) > 100_000
 
 
 def test_msd_overflow_falls_back_to_lsb(orc):
