@@ -11,10 +11,13 @@ preallocated device buffer.  Default workload: BASELINE configs[2] = c3
 (d=1, n=m=5e7, N=1e8), the configuration the north star's roofline target is
 quoted on.  Rank 0 prints one JSON line.
 
-N > 1 (torchrun, one process per GPU, NCCL): updates are sharded by
-coordinate slab; each step rank 0 builds the subscription index, broadcasts
-it (NCCL over NVLink), every rank matches its slab, and the count is
-all-reduced.  Total work is fixed -> "scaling": "strong".
+N > 1 (one process per GPU, NCCL; `--gpus N` without a launcher starts its
+own N ranks through torch.distributed.run): default slab mode -- every rank
+starts with an index block of the regions in HBM, and each step computes the
+slab cut points, partitions (slab + halo) and exchanges the regions on the
+device (all_to_all), matches its slab and all-reduces K; `--dist broadcast`
+builds the subscription index on rank 0 and broadcasts it instead
+(DESIGN.md §7).  Total work is fixed -> "scaling": "strong".
 
 --impl reference: the CPU oracle (oracle/, Alg. 5+6 Parallel-SBM on all host
 cores) on a bounded window sample of the same workload (the reference arm of
@@ -50,6 +53,9 @@ def parse():
     ap.add_argument("--mode", default="pairs", choices=["pairs", "count"],
                     help="pairs: the list (default); count: K only (ddm_match_count, the paper's experimental "
                          "mode P:915-918), single GPU")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N>1 process group; gloo stages collectives through host memory and lets ranks share a "
+                         "GPU (tests of the multi-GPU path on one GPU; not a performance configuration)")
     ap.add_argument("--dist", default="slab", choices=["slab", "broadcast"],
                     help="N>1: slab = fully distributed index (each rank its slab + halo, "
                          "only the count all-reduce); broadcast = rank 0 builds the sub index, NCCL broadcast")
@@ -149,10 +155,20 @@ class Clocks:
                 "samples": len(sm), "source": "NVML child process, 2 ms polling"}
 
 
+L2_BYTES = 126e6
+
+
+def needs_flush(w) -> bool:
+    """Inputs (16 d B per region) plus the sorted copies the step makes
+    (~24 B per region and kind) could stay resident in the 126 MB L2."""
+    return 40.0 * w.d * (w.n + w.m) <= 2 * L2_BYTES
+
+
 def workload_config(w, extra=None, mode="pairs"):
     d = {"workload": w.name, "d": w.d, "n_sub": w.n, "n_upd": w.m, "L": w.L, "l": w.l, "seed": w.seed,
-         "coords": "float64", "mode": "pairs (list)" if mode == "pairs" else "count only (ddm_match_count)", "l2": "inputs larger than L2 (no flush needed)"
-         if 32 * w.d * (w.n + w.m) > 126e6 else "L2 flushed between steps"}
+         "coords": "float64", "mode": "pairs (list)" if mode == "pairs" else "count only (ddm_match_count)",
+         "l2": "L2 flushed before every timed step (256 MB write outside the timed events)" if needs_flush(w)
+         else "inputs larger than L2 (no flush needed)"}
     if extra:
         d.update(extra)
     return d
@@ -233,12 +249,20 @@ def run_ddm(args):
     from paper_1703_06680_b200 import dist as ddist
 
     rank, world, local = env_rank()
-    if world != args.gpus:
-        args.gpus = world
+    if world != args.gpus:  # a launcher mismatch must not produce a line with the wrong n_gpus
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    ndev = torch.cuda.device_count()
+    if args.backend == "nccl" and world > ndev:
+        raise SystemExit(f"bench.py: {world} ranks need {world} GPUs, {ndev} visible "
+                         "(--backend gloo shares GPUs between ranks, for testing only)")
+    local = local % max(ndev, 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     ddm.load()
     w = wl.make(args.config)
     hbm_peak, peak_src = peaks()
@@ -250,6 +274,7 @@ def run_ddm(args):
             torch.cuda.synchronize()
 
     stream = torch.cuda.current_stream()
+    dist_marks = []  # per timed step: CUDA events between the phases of the multi-GPU step
     if world == 1:
         g = [torch.from_numpy(a).to(dev) for a in (w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi)]
         M = ddm.Matcher(w.d, w.n, w.m, dev)
@@ -259,52 +284,75 @@ def run_ddm(args):
         def step():
             return M.pairs_into(out, *g) if args.mode == "pairs" else M.count(*g)
     elif args.dist == "slab":
-        sl, sh, sids, ul, uh, uids = ddist.slab_partition(w, rank, world)
-        part = [torch.from_numpy(a).to(dev) for a in (sl, sh, ul, uh)]
-        sid_t, uid_t = torch.from_numpy(sids).to(dev), torch.from_numpy(uids).to(dev)
-        # capacity from an untimed count of this rank's partition
-        cap = ddm.Matcher(w.d, sl.shape[1], ul.shape[1], dev).count(*part)
-        SM = ddist.SlabMatcher(w.d, sl.shape[1], ul.shape[1], cap, dev)
+        # every rank starts with its index block of both kinds in HBM (the
+        # input as it arrives); the step partitions on the device, exchanges
+        # by all_to_all and matches
+        s0, s1 = ddist.block_of(w.n, rank, world)
+        u0, u1 = ddist.block_of(w.m, rank, world)
+        blk = [torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+               for a in (w.sub_lo[:, s0:s1], w.sub_hi[:, s0:s1], w.upd_lo[:, u0:u1], w.upd_hi[:, u0:u1])]
+        SM = ddist.SlabMatcher(w.d, dev)
 
         def step():
-            return SM.step(part[0], part[1], sid_t, part[2], part[3], uid_t).k_total
+            r = SM.step(blk[0], blk[1], s0, blk[2], blk[3], u0)
+            dist_marks.append(r.marks)
+            return r.k_total
     else:
-        cuts = ddist.slab_cuts(w.upd_lo[0], world)
-        ul, uh, ids = ddist.local_updates(w.upd_lo, w.upd_hi, rank, world, cuts)
+        # broadcast: rank 0 holds the subscriptions, every rank its update block
+        u0, u1 = ddist.block_of(w.m, rank, world)
         sub = [torch.from_numpy(a).to(dev) for a in (w.sub_lo, w.sub_hi)] if rank == 0 else [None, None]
-        upd = [torch.from_numpy(a).to(dev) for a in (ul, uh)]
-        uid = torch.from_numpy(ids).to(dev)
+        upd = [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.upd_lo[:, u0:u1], w.upd_hi[:, u0:u1])]
+        uid = torch.arange(u0, u1, dtype=torch.int32, device=dev)
         # capacity from an untimed count against a freshly built index
-        SM0 = ddist.ShardedMatcher(w.d, w.n, ul.shape[1], 1, dev)
+        SM0 = ddist.ShardedMatcher(w.d, w.n, u1 - u0, 1, dev)
         if rank == 0:
             SM0.build_index(*sub)
-        dist.broadcast(SM0.index, src=0)
+        SM0.coll.broadcast_(SM0.index, src=0)
         cap = ddm.match_count_indexed(SM0.index, w.n, *upd)
         del SM0
-        SM = ddist.ShardedMatcher(w.d, w.n, ul.shape[1], cap, dev)
+        SM = ddist.ShardedMatcher(w.d, w.n, u1 - u0, cap, dev)
 
         def step():
-            return SM.step(sub[0], sub[1], upd[0], upd[1], uid).k_total
+            r = SM.step(sub[0], sub[1], upd[0], upd[1], uid)
+            dist_marks.append(r.marks)
+            return r.k_total
 
     for _ in range(max(args.warmup, 0)):
         K = step()
     sync_all()
+    dist_marks.clear()
     # ---- the timed region (the official number): K steps, no instrumentation
     clocks = Clocks(local)
     clocks.start()
     l0 = ddm.launch_count()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    # inputs that fit in L2 (c1, c2) would be timed warm: a 256 MB write
+    # between steps (outside the timed events) evicts them first
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if needs_flush(w) else None
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     sync_all()
-    ev[0].record(stream)
     for i in range(args.steps):
+        if flush is not None:
+            flush.fill_(i & 0xFF)
+        ev0[i].record(stream)
         K = step()
-        ev[i + 1].record(stream)  # per-step boundaries (each step ends in its own host sync anyway)
+        ev1[i].record(stream)  # (each step ends in its own host sync anyway)
     torch.cuda.synchronize()
     sync_all()
     launches = ddm.launch_count() - l0
     clk = clocks.stop()
-    ms = ev[0].elapsed_time(ev[-1])
-    per_step = np.array([ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)])
+    per_step = np.array([ev0[i].elapsed_time(ev1[i]) for i in range(args.steps)])
+    ms = float(per_step.sum())
+    # multi-GPU phases (device events inside each step): slab T_partition
+    # (cuts, pack, all_to_all, unpack) + T_match; broadcast T_index (build +
+    # broadcast) + T_match; means over the timed steps, max over ranks below
+    dist_phases = None
+    if dist_marks:
+        first = "partitioned" if "partitioned" in dist_marks[0] else "indexed"
+        t_a = float(np.mean([m["start"].elapsed_time(m[first]) for m in dist_marks]))
+        t_b = float(np.mean([m[first].elapsed_time(m["matched"]) for m in dist_marks]))
+        dist_phases = [t_a, t_b]
+    dist_marks.clear()
     step_stats = {"median": round(float(np.median(per_step)), 4), "p10": round(float(np.percentile(per_step, 10)), 4),
                   "p90": round(float(np.percentile(per_step, 90)), 4), "mean": round(float(per_step.mean()), 4)}
     # ---- a second timed region of the same K steps with per-kernel CUDA
@@ -312,15 +360,19 @@ def run_ddm(args):
     # (profiling mode runs the concurrent sort chains on one stream so the
     # kernels' intervals do not overlap): roofline + phase breakdown
     ddm.profile_enable(True)
-    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    p0.record(stream)
-    for _ in range(args.steps):
+    p0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    p1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for i in range(args.steps):
+        if flush is not None:  # (a torch fill, not a library launch: not in the records)
+            flush.fill_((i + 7) & 0xFF)
+        p0[i].record(stream)
         step()
-    p1.record(stream)
+        p1[i].record(stream)
     torch.cuda.synchronize()
     prof = ddm.profile_read()
     ddm.profile_enable(False)
-    prof_ms_step = p0.elapsed_time(p1) / args.steps
+    prof_ms_step = float(np.mean([p0[i].elapsed_time(p1[i]) for i in range(args.steps)]))
+    dist_marks.clear()
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -328,6 +380,11 @@ def run_ddm(args):
         lt = torch.tensor([launches], dtype=torch.int64, device=dev)
         dist.all_reduce(lt, op=dist.ReduceOp.SUM)
         launches = int(lt.item())
+    if dist_phases is not None:
+        t = torch.tensor(dist_phases, dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist_phases = {("T_partition_ms" if args.dist == "slab" else "T_index_ms"): round(float(t[0]), 4),
+                       "T_match_ms": round(float(t[1]), 4), "reduction": "mean over timed steps, max over ranks"}
     ms_step = ms / args.steps
     regions = w.n + w.m
     value = regions / (ms_step * 1e-3)
@@ -408,6 +465,38 @@ def run_ddm(args):
                "api": "paper_1703_06680_b200.ddm.PipelinedMatcher.run (ddm_match_pairs per batch, pinned host "
                       "buffers, copies overlapped with the neighbouring batches' matches)"}
 
+    if world > 1 and not args.no_e2e and args.mode == "pairs" and args.dist == "slab":
+        # e2e at N GPUs through dist.SlabMatcher: every step each rank copies
+        # its input block in from pinned host memory and its pair list out
+        hb = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+              for a in (w.sub_lo[:, s0:s1], w.sub_hi[:, s0:s1], w.upd_lo[:, u0:u1], w.upd_hi[:, u0:u1])]
+        hout = torch.empty((max(K, 1), 2), dtype=torch.int32).pin_memory()
+        h2d = sum(h.numel() * 8 for h in hb)
+        d2h_tot = 0
+        n_e2e = max(3, args.steps)
+        sync_all()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(n_e2e):
+            for dst, src in zip(blk, hb):
+                dst.copy_(src, non_blocking=True)
+            r = SM.step(blk[0], blk[1], s0, blk[2], blk[3], u0)
+            if hout.shape[0] < r.k_local:
+                hout = torch.empty((r.k_local, 2), dtype=torch.int32).pin_memory()
+            hout[: r.k_local].copy_(r.pairs, non_blocking=True)
+            d2h_tot += r.k_local * 8
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / n_e2e, h2d, d2h_tot / n_e2e], dtype=torch.float64, device=dev)
+        tm = t.clone()
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        e_ms = float(tm[0])
+        e2e = {"value": (w.n + w.m) / (e_ms * 1e-3), "unit": "regions/s", "ms_per_step": round(e_ms, 3),
+               "h2d_bytes_per_step": int(t[1]), "d2h_bytes_per_step": int(t[2]), "steps": n_e2e,
+               "api": "paper_1703_06680_b200.dist.SlabMatcher.step per rank (input block H2D from pinned memory, "
+                      "on-device partition + all_to_all + match, local pairs D2H); max over ranks"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         frac = CPU_SAMPLE_FRAC[args.config]
@@ -453,11 +542,14 @@ def run_ddm(args):
                 "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
                 "config": workload_config(w, mode=args.mode, extra={"parallelism": "single GPU" if world == 1 else
-                                              (f"dim-0 slabs x{world}: each rank its updates + the subscriptions "
-                                               f"that reach them (halo), count all-reduce (NCCL)"
+                                              (f"dim-0 slabs x{world} ({args.backend}): every rank starts with an "
+                                               f"index block of both kinds; on-device cuts + partition (slab + "
+                                               f"halo), all_to_all exchange, mapped match, K all-reduce"
                                                if args.dist == "slab" else
-                                               f"updates sharded by slab x{world}, sub index broadcast (NCCL)"),
+                                               f"update blocks x{world} ({args.backend}), sub index built on rank 0 "
+                                               f"and broadcast, K all-reduce"),
                                               "K": K, "timing": "CUDA events on the launching stream, max over ranks"}),
+                "dist_phases": dist_phases,
                 "pairs_per_s": K / (ms_step * 1e-3), "regions_per_s_per_gpu": value / world,
                 "step_ms": step_stats,
                 "roofline": roof, "pipeline": phases_summary, "phases": phases, "cpu_baseline": cpu, "e2e": e2e,
@@ -468,8 +560,25 @@ def run_ddm(args):
         dist.destroy_process_group()
 
 
+def self_launch(args) -> int:
+    """--gpus N > 1 without a launcher: start N ranks with torch.distributed.run
+    (one process per GPU, rendezvous on 127.0.0.1) running this same command
+    line; rank 0's JSON line is passed through."""
+    import socket
+    import subprocess
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

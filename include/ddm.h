@@ -201,6 +201,45 @@ ddm_status ddm_match_count_indexed(const void *index, const ddm_regions *upds,
                                    uint64_t *count_out, void *ws, size_t ws_bytes,
                                    cudaStream_t stream);
 
+/* --- Multi-GPU slab partition: the
+ * device half of the slab mode's data redistribution.  Every rank holds a
+ * block of the regions (global ids id_base + i) and sends each region to the
+ * ranks of the dimension-0 slabs it can take part in: an update to the slab
+ * holding its lower bound; a subscription S to every slab r with
+ * S.hi >= c_r and S.lo <= reach_r (max upper bound of slab r's updates) --
+ * the slab plus its halo, the stabbing set at the slab start (Alg. 6's
+ * SubSet[p] at a segment boundary).  Then every intersecting pair
+ * has both members on its update's rank.  The caller moves the packed rows
+ * with all_to_all (torch.distributed / NCCL) and matches with
+ * ddm_match_pairs_mapped.  All pointers device unless marked (host).
+ *
+ * ddm_slab_sample: sample[i] = lo0[floor(i * count / s)], i < s (NaN when
+ *   count == 0).  ddm_slab_cuts: cut points c_1..c_{world-1} (cuts, world-1
+ *   doubles) = quantiles floor(r * v / world) of the v finite entries of the
+ *   gathered sample (s <= 16384, world <= 32); slab r = [c_r, c_{r+1}).
+ * ddm_slab_pack: side 0 = subscriptions (regions->sub_*, n_sub), 1 = updates.
+ *   Validates every region (finite, lo <= hi in every dimension: errors as
+ *   ddm_match_pairs, nothing written).  Updates: reach_out (world int64)
+ *   receives the local per-slab maxima of the upper bounds as order-preserving
+ *   signed keys (INT64_MIN = none) -- all_reduce(MAX) it and pass it as the
+ *   subscriptions' reach_in.  send_counts (host, world) = rows per
+ *   destination; *total_out (host) = their sum; rows ([total][2d+1] words:
+ *   lo[0..d), hi[0..d), global id as a uint64 bit pattern) grouped by
+ *   destination, index order within each; rows_cap < total ->
+ *   DDM_ERR_CAPACITY (counts returned, rows not written).  id_base + count
+ *   <= 2^32.  One small device->host read.
+ * ddm_slab_unpack: rows [count][2d+1] -> lo[k][count], hi[k][count] (k < d,
+ *   contiguous [d][count]) and ids (uint32). */
+ddm_status ddm_slab_sample(const double *lo0, uint64_t count, double *sample, uint32_t s, cudaStream_t stream);
+ddm_status ddm_slab_cuts(const double *sample, uint32_t s, uint32_t world, double *cuts, cudaStream_t stream);
+size_t ddm_slab_pack_workspace_bytes(uint64_t count, uint32_t world);
+ddm_status ddm_slab_pack(const ddm_regions *regions, int side, uint64_t id_base, const double *cuts,
+                         uint32_t world, const int64_t *reach_in, int64_t *reach_out, uint64_t *send_counts,
+                         double *rows, uint64_t rows_cap, uint64_t *total_out, void *ws, size_t ws_bytes,
+                         cudaStream_t stream);
+ddm_status ddm_slab_unpack(const double *rows, uint64_t count, uint32_t d, double *lo, double *hi,
+                           uint32_t *ids, cudaStream_t stream);
+
 /* --- Event-order variant: the paper's own parallel
  * algorithm, Alg. 5 + 6, on the GPU -- an independent
  * cross-check of ddm_match_pairs, not the fast path.  All 2(n_sub+n_upd)

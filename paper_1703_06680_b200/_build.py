@@ -11,7 +11,7 @@ LIB = os.path.join(PKG, "libddm.so")
 # dev A/B only (tools/build_variant.py): load another build of the library
 LIB = os.environ.get("DDM_LIB") or LIB
 SOURCES = ["ddm.cu"]
-HEADERS = ["common.cuh", "radix.cuh", "match.cuh", "msd.cuh", "dd.cuh", "events.cuh", "dyn.cuh"]
+HEADERS = ["common.cuh", "radix.cuh", "match.cuh", "msd.cuh", "dd.cuh", "events.cuh", "dyn.cuh", "slab.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

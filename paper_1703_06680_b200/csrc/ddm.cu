@@ -29,6 +29,7 @@
 #include "dd.cuh"
 #include "events.cuh"
 #include "dyn.cuh"
+#include "slab.cuh"
 
 using namespace ddm;
 
@@ -1836,6 +1837,139 @@ extern "C" ddm_status ddm_match_pairs_events(const ddm_regions* R, ddm_pair* pai
   DDM_CUDA(cudaStreamSynchronize(st));
   *count_out = 0;
   return err_status((uint32_t)h[1]);
+}
+
+// ------------------------------------------------------------ multi-GPU slab partition (slab.cuh)
+
+namespace {
+struct SlabWs {
+  uint64_t tiles = 0;
+  uint64_t* cnt;       // [world][tiles]
+  uint64_t* off;       // [world * tiles + 1]
+  uint64_t* status;
+  uint64_t* misc;      // [world + 1] segment starts + total, then the error word
+  size_t bytes;
+};
+SlabWs slab_layout(uint64_t count, uint32_t world, void* base) {
+  Carver c(base);
+  SlabWs W;
+  W.tiles = (count + slab::kTile - 1) / slab::kTile;
+  const uint64_t T = W.tiles * world;
+  W.cnt = c.take<uint64_t>(T + 1);
+  W.off = c.take<uint64_t>(T + 1);
+  W.status = c.take<uint64_t>(T / (match::kScanThreads * match::kScanItems) + 2);
+  W.misc = c.take<uint64_t>(world + 2);
+  W.bytes = c.used;
+  return W;
+}
+__global__ void slab_seg_starts_kernel(const uint64_t* __restrict__ off, uint64_t tiles, uint32_t world,
+                                       uint64_t* __restrict__ misc) {
+  const uint32_t r = threadIdx.x;
+  if (r <= world) misc[r] = off[(uint64_t)r * tiles];  // off[world * tiles] = total
+}
+}  // namespace
+
+ddm_status ddm_slab_sample(const double* lo0, uint64_t count, double* sample, uint32_t s, cudaStream_t st) {
+  if (!sample || s == 0 || (count && !lo0)) return DDM_ERR_INVALID_ARGUMENT;
+  DDM_LAUNCH("slab_sample", 8.0 * s, st, slab::sample_kernel<<<(s + 255) / 256, 256, 0, st>>>(lo0, count, s, sample));
+  return check_launch();
+}
+
+ddm_status ddm_slab_cuts(const double* sample, uint32_t s, uint32_t world, double* cuts, cudaStream_t st) {
+  if (world < 1 || world > slab::kMaxWorld || s == 0 || s > (uint32_t)slab::kMaxSample || !sample)
+    return DDM_ERR_INVALID_ARGUMENT;
+  if (world == 1) return DDM_OK;
+  if (!cuts) return DDM_ERR_INVALID_ARGUMENT;
+  uint32_t P = 1;
+  while (P < s) P <<= 1;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(slab::cuts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, slab::kMaxSample * 8);
+    attr = true;
+  }
+  DDM_LAUNCH("slab_cuts", 8.0 * s, st, slab::cuts_kernel<<<1, 1024, P * sizeof(double), st>>>(sample, s, world, cuts));
+  return check_launch();
+}
+
+size_t ddm_slab_pack_workspace_bytes(uint64_t count, uint32_t world) {
+  if (world < 1 || world > slab::kMaxWorld) return 0;
+  return slab_layout(count, world, nullptr).bytes;
+}
+
+ddm_status ddm_slab_pack(const ddm_regions* R, int side, uint64_t id_base, const double* cuts, uint32_t world,
+                         const int64_t* reach_in, int64_t* reach_out, uint64_t* send_counts, double* rows,
+                         uint64_t rows_cap, uint64_t* total_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (!R || R->d == 0 || R->d > DDM_MAX_DIMS || (side != 0 && side != 1) || world < 1 ||
+      world > slab::kMaxWorld || !send_counts || !total_out || !aligned(ws, 256))
+    return DDM_ERR_INVALID_ARGUMENT;
+  const uint64_t count = side == 0 ? R->n_sub : R->n_upd;
+  DDM_TRY(side == 0 ? check_side(R->d, count, R->sub_lo, R->sub_hi) : check_side(R->d, count, R->upd_lo, R->upd_hi));
+  if (world > 1 && !cuts) return DDM_ERR_INVALID_ARGUMENT;
+  if (side == 0 && !reach_in) return DDM_ERR_INVALID_ARGUMENT;
+  if (side == 1 && !reach_out) return DDM_ERR_INVALID_ARGUMENT;
+  if (id_base + count > (1ull << 32)) return DDM_ERR_INVALID_ARGUMENT;  // global ids are uint32
+  if (ws_bytes < ddm_slab_pack_workspace_bytes(count, world)) return DDM_ERR_WORKSPACE;
+  init_attrs_once();
+  SlabWs W = slab_layout(count, world, ws);
+  slab::PackArgs A{};
+  A.d = (int)R->d;
+  A.count = count;
+  for (uint32_t k = 0; k < R->d; ++k) {
+    A.lo[k] = side == 0 ? R->sub_lo[k] : R->upd_lo[k];
+    A.hi[k] = side == 0 ? R->sub_hi[k] : R->upd_hi[k];
+  }
+  A.id_base = id_base;
+  A.side = side;
+  A.cuts = cuts;
+  A.reach = reinterpret_cast<const long long*>(reach_in);
+  A.world = world;
+  A.tiles = W.tiles;
+  A.tile_counts = W.cnt;
+  A.reach_out = reinterpret_cast<long long*>(reach_out);
+  A.err = reinterpret_cast<uint32_t*>(W.misc + world + 1);
+  A.rows = rows;
+  DDM_CUDA(cudaMemsetAsync(W.misc, 0, sizeof(uint64_t) * (world + 2), st));
+  if (side == 1) {  // INT64_MIN = no update in the slab
+    std::vector<int64_t> init(world, INT64_MIN);
+    DDM_CUDA(cudaMemcpyAsync(reach_out, init.data(), sizeof(int64_t) * world, cudaMemcpyHostToDevice, st));
+  }
+  const uint64_t T = W.tiles * world;
+  if (W.tiles) {
+    DDM_LAUNCH("slab_pack", 16.0 * R->d * count, st, slab::count_kernel<<<(unsigned)W.tiles, slab::kThreads, 0, st>>>(A));
+    DDM_TRY(check_launch());
+    const unsigned stiles = (unsigned)((T + match::kScanThreads * match::kScanItems - 1) /
+                                       (match::kScanThreads * match::kScanItems));
+    DDM_CUDA(cudaMemsetAsync(W.status, 0, sizeof(uint64_t) * (stiles + 1), st));
+    DDM_LAUNCH("scan", 16.0 * T, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
+        W.cnt, T, W.off, W.status, W.off + T));
+    DDM_TRY(check_launch());
+    DDM_LAUNCH("slab_pack", 0, st, slab_seg_starts_kernel<<<1, 64, 0, st>>>(W.off, W.tiles, world, W.misc));
+    DDM_TRY(check_launch());
+  }
+  std::vector<uint64_t> h(world + 2, 0);
+  DDM_CUDA(cudaMemcpyAsync(h.data(), W.misc, sizeof(uint64_t) * (world + 2), cudaMemcpyDeviceToHost, st));
+  DDM_CUDA(cudaStreamSynchronize(st));
+  DDM_TRY(err_status((uint32_t)h[world + 1]));
+  const uint64_t total = W.tiles ? h[world] : 0;
+  for (uint32_t r = 0; r < world; ++r) send_counts[r] = W.tiles ? h[r + 1] - h[r] : 0;
+  *total_out = total;
+  if (total > rows_cap) return DDM_ERR_CAPACITY;
+  if (total == 0) return DDM_OK;
+  if (!rows) return DDM_ERR_INVALID_ARGUMENT;
+  A.tile_counts = W.off;  // exclusive offsets
+  DDM_LAUNCH("slab_pack", 16.0 * R->d * count + (16.0 * R->d + 8.0) * total, st,
+             slab::scatter_kernel<<<(unsigned)W.tiles, slab::kThreads, 0, st>>>(A));
+  return check_launch();
+}
+
+ddm_status ddm_slab_unpack(const double* rows, uint64_t count, uint32_t d, double* lo, double* hi, uint32_t* ids,
+                           cudaStream_t st) {
+  if (d == 0 || d > DDM_MAX_DIMS) return DDM_ERR_INVALID_ARGUMENT;
+  if (count == 0) return DDM_OK;
+  if (!rows || !lo || !hi || !ids) return DDM_ERR_INVALID_ARGUMENT;
+  DDM_LAUNCH("slab_unpack", (32.0 * d + 12.0) * count, st,
+             slab::unpack_kernel<<<grid_for(count, 256, 8), 256, 0, st>>>(rows, count, (int)d, lo, hi, ids));
+  return check_launch();
 }
 
 size_t ddm_sort_pairs_workspace_bytes(uint64_t k) {

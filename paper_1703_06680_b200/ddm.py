@@ -89,6 +89,11 @@ def load() -> ctypes.CDLL:
         "ddm_match_pairs_events": ([R, vp, u64, ctypes.POINTER(u64), vp, sz, vp], i32),
         "ddm_match_count_indexed": ([vp, R, ctypes.POINTER(u64), vp, sz, vp], i32),
         "ddm_chunk_start_sets": ([R, vp, vp, vp, u64, ctypes.POINTER(u64), vp, sz, vp], i32),
+        "ddm_slab_sample": ([vp, u64, vp, u32, vp], i32),
+        "ddm_slab_cuts": ([vp, u32, u32, vp, vp], i32),
+        "ddm_slab_pack_workspace_bytes": ([u64, u32], sz),
+        "ddm_slab_pack": ([R, i32, u64, vp, u32, vp, vp, vp, vp, u64, ctypes.POINTER(u64), vp, sz, vp], i32),
+        "ddm_slab_unpack": ([vp, u64, u32, vp, vp, vp, vp], i32),
         "ddm_radix_sort_workspace_bytes": ([u64], sz),
         "ddm_radix_sort_u64": ([vp, vp, vp, vp, u64, i32, i32, vp, sz, vp], i32),
         "ddm_encode_keys": ([vp, vp, u64, vp], i32),
@@ -113,7 +118,8 @@ EXPORTED = ["ddm_workspace_bytes", "ddm_match_count", "ddm_match_pairs", "ddm_ma
             "ddm_indexed_workspace_bytes", "ddm_match_pairs_indexed", "ddm_match_count_indexed",
             "ddm_events_workspace_bytes", "ddm_match_pairs_events",
             "ddm_sub_index_update_workspace_bytes", "ddm_sub_index_update",
-            "ddm_chunk_start_sets",
+            "ddm_chunk_start_sets", "ddm_slab_sample", "ddm_slab_cuts", "ddm_slab_pack_workspace_bytes",
+            "ddm_slab_pack", "ddm_slab_unpack",
             "ddm_radix_sort_workspace_bytes", "ddm_radix_sort_u64", "ddm_encode_keys", "ddm_status_string",
             "ddm_last_cuda_error", "ddm_kernel_launch_count", "ddm_build_info", "ddm_profile_enable",
             "ddm_profile_read"]
