@@ -94,7 +94,8 @@ typedef struct {
 
 /* Flags for ddm_match_pairs / ddm_match_pairs_indexed.  The output ORDER is
  * deterministic without flags: rows by (upd lower bound, upd id), within a row
- * subscriptions by (sub lower bound, sub id) on the sweep dimension 0.  The
+ * subscriptions by (sub lower bound, sub id) on the sweep dimension (0 for
+ * d = 1; see DDM_SWEEP_DIM0 for d > 1).  The
  * emit-path flags only force one of the three emission paths (for tests);
  * every path yields byte-identical output. */
 #define DDM_EMIT_AUTO 0u
@@ -121,6 +122,17 @@ typedef struct {
  * either way. */
 #define DDM_COUNT_RANKS (1u << 13)
 #define DDM_COUNT_WALK (1u << 14)
+/* Sweep dimension (d > 1, ddm_match_pairs / ddm_match_count /
+ * ddm_match_pairs_mapped): by default the pipeline sweeps the dimension k*
+ * with the fewest estimated candidate pairs (k* = argmin_k
+ * K_k; P:237-247 leaves the choice open) -- a probe of 4096 sampled regions
+ * per kind estimates K_k / (n m) = (mean S length + mean U length) / span of
+ * the lower bounds, and k* replaces dimension 0 when its estimate is at least
+ * 10 % smaller (one small device->host read on the first call of a call
+ * site).  The pair set is the same for every sweep dimension; the row order
+ * then follows dimension k*.  This flag sweeps dimension 0 always.  The
+ * subscription index (ddm_sub_index_build) always sweeps dimension 0. */
+#define DDM_SWEEP_DIM0 (1u << 15)
 
 /* Workspace bytes needed by ddm_match_count (want_pairs = 0) or
  * ddm_match_pairs (want_pairs != 0) for these sizes.  Independent of K. */
@@ -200,6 +212,23 @@ ddm_status ddm_match_pairs_indexed(const void *index, const ddm_regions *upds,
 ddm_status ddm_match_count_indexed(const void *index, const ddm_regions *upds,
                                    uint64_t *count_out, void *ws, size_t ws_bytes,
                                    cudaStream_t stream);
+
+/* --- Literal d-dimensional reading (SURVEY §8(a) a8 "literal",
+ * G10): the pair set of every dimension separately (the 1-D pipeline on
+ * dimension k), each sorted into canonical u64 words (upd << 32) | sub, then
+ * intersected by sort-merge (binary search of the running result's words in
+ * the next dimension's sorted list, survivors compacted in order).  The same
+ * set as ddm_match_pairs, written in canonical order -- an independent
+ * cross-check of the filtered sweep, for SMALL inputs: every per-dimension
+ * set is materialised (up to dim_capacity pairs each; a larger one returns
+ * DDM_ERR_CAPACITY with *dim_count_out = its size).  *count_out (host) = K;
+ * capacity < K -> DDM_ERR_CAPACITY.  ws >= ddm_literal_workspace_bytes(d,
+ * n_sub, n_upd, dim_capacity), 256-byte aligned; dim_capacity <=
+ * DDM_MAX_SORT_KEYS.  Blocks on small device->host reads. */
+size_t ddm_literal_workspace_bytes(uint32_t d, uint64_t n_sub, uint64_t n_upd, uint64_t dim_capacity);
+ddm_status ddm_match_pairs_literal(const ddm_regions *regions, ddm_pair *pairs, uint64_t capacity,
+                                   uint64_t *count_out, uint64_t dim_capacity, uint64_t *dim_count_out,
+                                   void *ws, size_t ws_bytes, cudaStream_t stream);
 
 /* --- Multi-GPU slab partition: the
  * device half of the slab mode's data redistribution.  Every rank holds a

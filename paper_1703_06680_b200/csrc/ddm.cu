@@ -395,7 +395,7 @@ MatchWs match_layout(uint32_t d, uint64_t n_sub, uint64_t m, void* base, bool in
   const uint64_t rtiles = m / match::kRowTile + 2;
   W.misc = c.take<Misc>(1);
   W.mm = c.take<uint64_t>(6);
-  W.probe = c.take<double>(2);
+  W.probe = c.take<double>(DDM_MAX_DIMS);
   W.scan_status = c.take<uint64_t>(rtiles / (match::kScanThreads * match::kScanItems) + 2);
   W.part = c.take<uint64_t>(4 * (m / match::kCountTile + 2));
   W.tile_sum = c.take<uint64_t>(rtiles);
@@ -1317,10 +1317,72 @@ size_t ddm_workspace_bytes(uint32_t d, uint64_t n_sub, uint64_t n_upd, int want_
 std::mutex g_probe_mu;
 std::unordered_map<std::string, bool> g_probe;  // count-form decision per call site
 
+std::mutex g_dim_mu;
+std::unordered_map<std::string, int> g_dim_probe;  // sweep-dimension choice per call site
+
+// k* for d > 1: the dimension with the fewest estimated
+// candidate pairs (match::dim_probe_kernel), dimension 0 unless another one
+// is estimated at least 10 % smaller.  Any choice gives the same pair set
+// (the other dimensions are filtered exactly); it only changes the work and
+// the row order.  Decided once per call site (one small device->host read).
+static ddm_status sweep_dim(const ddm_regions* R, const std::string& key, double* probe, cudaStream_t st, int* kout) {
+  *kout = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_dim_mu);
+    const auto it = g_dim_probe.find(key);
+    if (it != g_dim_probe.end()) { *kout = it->second; return DDM_OK; }
+  }
+  match::ProbeDims P{};
+  for (uint32_t k = 0; k < R->d; ++k) {
+    P.sub_lo[k] = R->sub_lo[k]; P.sub_hi[k] = R->sub_hi[k]; P.upd_lo[k] = R->upd_lo[k]; P.upd_hi[k] = R->upd_hi[k];
+  }
+  DDM_LAUNCH("dim_probe", 0, st, match::dim_probe_kernel<<<R->d, 256, 0, st>>>(P, R->n_sub, R->n_upd, probe));
+  DDM_TRY(check_launch());
+  double est[DDM_MAX_DIMS];
+  DDM_CUDA(cudaMemcpyAsync(est, probe, sizeof(double) * R->d, cudaMemcpyDeviceToHost, st));
+  DDM_CUDA(cudaStreamSynchronize(st));
+  int best = 0;
+  for (uint32_t k = 1; k < R->d; ++k)
+    if (est[k] < est[best]) best = (int)k;
+  if (!(est[best] < 0.9 * est[0])) best = 0;
+  std::lock_guard<std::mutex> lk(g_dim_mu);
+  if (g_dim_probe.size() > 4096) g_dim_probe.clear();
+  g_dim_probe[key] = best;
+  *kout = best;
+  return DDM_OK;
+}
+
+static ddm_status match_full_dim(const ddm_regions* R, ddm_pair* pairs, uint64_t capacity, uint64_t* count_out,
+                                 uint32_t flags, void* ws, size_t ws_bytes, cudaStream_t st,
+                                 const uint32_t* sub_map, const uint32_t* upd_map);
+
 static ddm_status match_full(const ddm_regions* R, ddm_pair* pairs, uint64_t capacity, uint64_t* count_out,
                              uint32_t flags, void* ws, size_t ws_bytes, cudaStream_t st,
                              const uint32_t* sub_map = nullptr, const uint32_t* upd_map = nullptr) {
   DDM_TRY(check_regions(R, true, true));
+  if (R->d > 1 && !(flags & DDM_SWEEP_DIM0) && R->n_sub > 0 && R->n_upd > 0 && ws &&
+      ws_bytes >= ddm_workspace_bytes(R->d, R->n_sub, R->n_upd, pairs != nullptr)) {
+    // the sweep dimension k*: swap it into position 0 (a view; the filter
+    // tests every other dimension exactly, so the pair set is unchanged)
+    MatchWs W = match_layout(R->d, R->n_sub, R->n_upd,
+                             static_cast<uint8_t*>(ws) + a256(index_layout(R->d, R->n_sub, nullptr).bytes), true);
+    int k = 0;
+    DDM_TRY(sweep_dim(R, graph_key(R, ws, ws_bytes, flags, pairs != nullptr, sub_map, upd_map, st), W.probe, st, &k));
+    if (k != 0) {
+      ddm_regions V = *R;
+      std::swap(V.sub_lo[0], V.sub_lo[k]);
+      std::swap(V.sub_hi[0], V.sub_hi[k]);
+      std::swap(V.upd_lo[0], V.upd_lo[k]);
+      std::swap(V.upd_hi[0], V.upd_hi[k]);
+      return match_full_dim(&V, pairs, capacity, count_out, flags, ws, ws_bytes, st, sub_map, upd_map);
+    }
+  }
+  return match_full_dim(R, pairs, capacity, count_out, flags, ws, ws_bytes, st, sub_map, upd_map);
+}
+
+static ddm_status match_full_dim(const ddm_regions* R, ddm_pair* pairs, uint64_t capacity, uint64_t* count_out,
+                                 uint32_t flags, void* ws, size_t ws_bytes, cudaStream_t st,
+                                 const uint32_t* sub_map, const uint32_t* upd_map) {
   if (!count_out || (!ws && ws_bytes) || !aligned(ws, 256)) return DDM_ERR_INVALID_ARGUMENT;
   if (pairs && !aligned(pairs, 8)) return DDM_ERR_INVALID_ARGUMENT;
   if (ws_bytes < ddm_workspace_bytes(R->d, R->n_sub, R->n_upd, pairs != nullptr)) return DDM_ERR_WORKSPACE;
@@ -1970,6 +2032,103 @@ ddm_status ddm_slab_unpack(const double* rows, uint64_t count, uint32_t d, doubl
   DDM_LAUNCH("slab_unpack", (32.0 * d + 12.0) * count, st,
              slab::unpack_kernel<<<grid_for(count, 256, 8), 256, 0, st>>>(rows, count, (int)d, lo, hi, ids));
   return check_launch();
+}
+
+// ------------------------------------------------------------ literal d > 1 (G10)
+
+namespace {
+struct LitWs {
+  uint8_t* match_ws;
+  size_t match_bytes;
+  uint64_t* a;     // running intersection (canonical words)
+  uint64_t* b;     // this dimension's pairs
+  uint64_t* c;     // compaction target
+  uint64_t* off;   // [cap + 1] flags -> offsets
+  uint64_t* flag;
+  uint64_t* status;
+  uint8_t* sort_ws;
+  size_t sort_bytes;
+  size_t bytes;
+};
+LitWs lit_layout(uint64_t n_sub, uint64_t n_upd, uint64_t cap, void* base) {
+  Carver c(base);
+  LitWs L{};
+  L.match_bytes = ddm_workspace_bytes(1, n_sub, n_upd, 1);
+  L.match_ws = c.take<uint8_t>(L.match_bytes);
+  L.a = c.take<uint64_t>(cap + 1);
+  L.b = c.take<uint64_t>(cap + 1);
+  L.c = c.take<uint64_t>(cap + 1);
+  L.flag = c.take<uint64_t>(cap + 1);
+  L.off = c.take<uint64_t>(cap + 1);
+  L.status = c.take<uint64_t>(cap / (match::kScanThreads * match::kScanItems) + 2);
+  L.sort_bytes = ddm_sort_pairs_workspace_bytes(cap);
+  L.sort_ws = c.take<uint8_t>(L.sort_bytes);
+  L.bytes = c.used;
+  return L;
+}
+}  // namespace
+
+size_t ddm_literal_workspace_bytes(uint32_t d, uint64_t n_sub, uint64_t n_upd, uint64_t dim_capacity) {
+  if (d == 0 || d > DDM_MAX_DIMS) return 0;
+  return lit_layout(n_sub, n_upd, dim_capacity, nullptr).bytes;
+}
+
+ddm_status ddm_match_pairs_literal(const ddm_regions* R, ddm_pair* pairs, uint64_t capacity, uint64_t* count_out,
+                                   uint64_t dim_capacity, uint64_t* dim_count_out, void* ws, size_t ws_bytes,
+                                   cudaStream_t st) {
+  DDM_TRY(check_regions(R, true, true));
+  if (!count_out || !dim_count_out || !aligned(ws, 256) || (capacity && !pairs)) return DDM_ERR_INVALID_ARGUMENT;
+  if (dim_capacity > DDM_MAX_SORT_KEYS) return DDM_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < ddm_literal_workspace_bytes(R->d, R->n_sub, R->n_upd, dim_capacity)) return DDM_ERR_WORKSPACE;
+  init_attrs_once();
+  LitWs L = lit_layout(R->n_sub, R->n_upd, dim_capacity, ws);
+  *count_out = 0;
+  *dim_count_out = 0;
+  uint64_t na = 0;
+  for (uint32_t k = 0; k < R->d; ++k) {
+    // this dimension alone (a 1-D instance): its pairs, canonical order
+    ddm_regions V{};
+    V.d = 1;
+    V.n_sub = R->n_sub;
+    V.n_upd = R->n_upd;
+    V.sub_lo[0] = R->sub_lo[k]; V.sub_hi[0] = R->sub_hi[k];
+    V.upd_lo[0] = R->upd_lo[k]; V.upd_hi[0] = R->upd_hi[k];
+    uint64_t* dst = k == 0 ? L.a : L.b;
+    uint64_t kk = 0;
+    const ddm_status r = match_full(&V, reinterpret_cast<ddm_pair*>(dst), dim_capacity, &kk, 0, L.match_ws,
+                                    L.match_bytes, st);
+    if (kk > *dim_count_out) *dim_count_out = kk;
+    if (r == DDM_ERR_CAPACITY) return r;  // *dim_count_out = a K_k above dim_capacity
+    DDM_TRY(r);
+    DDM_TRY(ddm_sort_pairs(reinterpret_cast<ddm_pair*>(dst), kk, R->n_sub, R->n_upd, L.sort_ws, L.sort_bytes, st));
+    if (k == 0) {
+      na = kk;
+      continue;
+    }
+    // A <- A ∩ B by sort-merge (binary search of each A word in B), compacted in order
+    if (na) {
+      DDM_LAUNCH("lit_intersect", 8.0 * na + 8.0 * kk, st, match::intersect_flags_kernel<<<grid_for(na, 256, 8), 256, 0, st>>>(
+          L.a, na, L.b, kk, L.flag));
+      DDM_TRY(check_launch());
+      const unsigned stiles = (unsigned)((na + match::kScanThreads * match::kScanItems - 1) /
+                                         (match::kScanThreads * match::kScanItems));
+      DDM_CUDA(cudaMemsetAsync(L.status, 0, sizeof(uint64_t) * (stiles + 1), st));
+      DDM_LAUNCH("scan", 16.0 * na, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
+          L.flag, na, L.off, L.status, L.off + na));
+      DDM_TRY(check_launch());
+      DDM_LAUNCH("lit_intersect", 24.0 * na, st, match::compact_kernel<<<grid_for(na, 256, 8), 256, 0, st>>>(
+          L.a, na, L.flag, L.off, L.c));
+      DDM_TRY(check_launch());
+      DDM_CUDA(cudaMemcpyAsync(&na, L.off + na, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+      DDM_CUDA(cudaStreamSynchronize(st));
+      std::swap(L.a, L.c);
+    }
+  }
+  *count_out = na;
+  if (na > capacity) return DDM_ERR_CAPACITY;
+  if (na) DDM_CUDA(cudaMemcpyAsync(pairs, L.a, na * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+  DDM_CUDA(cudaStreamSynchronize(st));
+  return DDM_OK;
 }
 
 size_t ddm_sort_pairs_workspace_bytes(uint64_t k) {

@@ -258,6 +258,53 @@ __global__ void __launch_bounds__(256) stab_density_kernel(const double* __restr
   }
 }
 
+// Sweep-dimension probe (d > 1; SURVEY §8(a) a8 "k* = argmin_k K_k"): per
+// dimension k an estimate of the dim-k candidate pairs K_k up to the common
+// factor n*m -- (mean S length + mean U length) / (max lo - min lo) over 4096
+// evenly spaced regions of each kind (uniformly placed intervals overlap with
+// that probability).  out[k]; +inf when the span is empty or a sampled value is
+// non-finite (the validation reports it).  One CTA per dimension.
+struct ProbeDims {
+  const double* sub_lo[8];
+  const double* sub_hi[8];
+  const double* upd_lo[8];
+  const double* upd_hi[8];
+};
+__global__ void __launch_bounds__(256) dim_probe_kernel(const __grid_constant__ ProbeDims P, uint64_t n, uint64_t m,
+                                                        double* __restrict__ out) {
+  __shared__ double s_v[4][8];
+  __shared__ int s_bad;
+  const int k = blockIdx.x;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  double ls = 0.0, lu = 0.0, mn = INFINITY, mx = -INFINITY;
+  int bad = 0;
+  for (int t = threadIdx.x; t < kProbe; t += blockDim.x) {
+    const uint64_t i = (uint64_t)((unsigned __int128)t * n / kProbe), j = (uint64_t)((unsigned __int128)t * m / kProbe);
+    const double a = P.sub_lo[k][i], b = P.sub_hi[k][i], c = P.upd_lo[k][j], e = P.upd_hi[k][j];
+    if (!isfinite(a) || !isfinite(b) || !isfinite(c) || !isfinite(e)) { bad = 1; continue; }
+    ls += b > a ? b - a : 0.0;
+    lu += e > c ? e - c : 0.0;
+    mn = fmin(mn, fmin(a, c));
+    mx = fmax(mx, fmax(a, c));
+  }
+  for (int o = 16; o; o >>= 1) {
+    ls += __shfl_xor_sync(kFull, ls, o);
+    lu += __shfl_xor_sync(kFull, lu, o);
+    mn = fmin(mn, __shfl_xor_sync(kFull, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
+  }
+  if (bad) s_bad = 1;
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { s_v[0][w] = ls; s_v[1][w] = lu; s_v[2][w] = mn; s_v[3][w] = mx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < 8; ++q) { ls += s_v[0][q]; lu += s_v[1][q]; mn = fmin(mn, s_v[2][q]); mx = fmax(mx, s_v[3][q]); }
+    const double span = mx - mn;
+    out[k] = (s_bad || !(span > 0.0)) ? INFINITY : (ls + lu) / (double)kProbe / span;
+  }
+}
+
 // Exclusive max-scan of the nb block maxima, in place: chunks of
 // kPmChunk = 8192 blocks; pmb_chunk_kernel writes each chunk's maximum,
 // pmb_scan_kernel scans a chunk after taking the maximum of the chunks
@@ -1447,6 +1494,38 @@ __global__ void __launch_bounds__(kRowTile) emit_chunk_kernel(const __grid_const
     const uint32_t t = S.R.queue[q];
     chunk_row_warp(S, A, j0 + t, S.R.ro[t], rl0, lane);
   }
+}
+
+// ------------------------------------------------------------ literal d > 1 (G10)
+//
+// The paper's literal reading of d > 1: the pair set of every
+// dimension separately, intersected.  ddm_match_pairs_literal sorts each
+// dimension's pairs into canonical u64 words (upd << 32) | sub and
+// intersects the running result A with the next dimension's B: a word of A
+// survives iff a binary search finds it in B; survivors are compacted (in
+// order) by an exclusive scan of the flags.  Small inputs only: each
+// per-dimension set is materialised.
+__global__ void __launch_bounds__(256) intersect_flags_kernel(const uint64_t* __restrict__ A, uint64_t na,
+                                                              const uint64_t* __restrict__ B, uint64_t nb,
+                                                              uint64_t* __restrict__ flag) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < na; i += stride) {
+    const uint64_t x = A[i];
+    uint64_t lo = 0, hi = nb;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (B[mid] < x) lo = mid + 1;
+      else hi = mid;
+    }
+    flag[i] = lo < nb && B[lo] == x;
+  }
+}
+__global__ void __launch_bounds__(256) compact_kernel(const uint64_t* __restrict__ A, uint64_t na,
+                                                      const uint64_t* __restrict__ flag,
+                                                      const uint64_t* __restrict__ off, uint64_t* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < na; i += stride)
+    if (flag[i]) out[off[i]] = A[i];
 }
 
 // ------------------------------------------------------------ pair canonical key

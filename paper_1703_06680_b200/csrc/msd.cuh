@@ -22,6 +22,7 @@
 #pragma once
 #include "common.cuh"
 #include "radix.cuh"
+#include <type_traits>
 
 namespace ddm {
 namespace msd {
@@ -244,6 +245,20 @@ __global__ void __launch_bounds__(512) msd_hist_kernel(const void* __restrict__ 
 
 // ---------------------------------------------------------------- multisplit pass
 
+// Ranking of the multisplit pass.  DDM_MSD_RANK 1 (default): a lane's peers
+// (same digit) come from 8 warp ballots over the digit bits, and per-warp
+// counters are read-modified-written by the lowest lane of each peer group
+// with plain shared loads/stores -- no shared-memory atomics, which cost the
+// LSU ~2 cycles per lane (B300_MICROARCH "ATOMS spread-addr") and bounded the
+// round-1 pass.  DDM_MSD_RANK 0: the round-1 scheme (histogram atomics, then
+// atomicOr peer masks).
+#ifndef DDM_MSD_RANK
+#define DDM_MSD_RANK 0
+#endif
+#ifndef DDM_MSD_MINB
+#define DDM_MSD_MINB 3
+#endif
+
 template <int ITEMS, bool V64, bool V32>
 struct PassSmem {
   static constexpr int kT = kThreads * ITEMS;
@@ -252,11 +267,28 @@ struct PassSmem {
   uint32_t v32[V32 ? kT : 4];
   uint8_t dg[kT];
   alignas(16) uint32_t wbase[kWarps][kRadix];
+#if DDM_MSD_RANK == 0
   uint32_t match[kWarps][kRadix];
-  long long digit_base[kRadix];
+#else
+  // per item: digit | warp-local rank << 8 (kept out of registers; 16 bits
+  // hold it while a warp ranks at most 256 records)
+  typename std::conditional<ITEMS <= 8, uint16_t, uint32_t>::type dl[ITEMS][kThreads];
+#endif
+  uint32_t digit_base[kRadix];  // (dst = digit_base + tile position, mod 2^32: n < 2^32)
   uint32_t scan_tmp[kWarps + 1];
   uint32_t tile_id;
 };
+
+// Lanes of the warp holding the same 8-bit digit as this lane, among `valid`.
+__device__ __forceinline__ unsigned digit_peers(uint32_t d, unsigned valid) {
+  unsigned pm = valid;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const unsigned bb = __ballot_sync(kFull, (d >> b) & 1u);
+    pm &= ((d >> b) & 1u) ? bb : ~bb;
+  }
+  return pm;
+}
 
 // Stable multisplit of the records by digit = (bucket(key) >> shift) & 255:
 // the onesweep scheme of radix.cuh (early counts, atomicOr match ranking,
@@ -316,7 +348,7 @@ struct TileRegs {
 };
 
 template <int ITEMS, bool V64, bool V32, bool SRC_F64>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
     msd_pass_kernel(const void* __restrict__ k_in, const void* __restrict__ v64_in, const uint32_t* __restrict__ v32_in,
                     uint64_t* __restrict__ k_out, uint64_t* __restrict__ v64_out, uint32_t* __restrict__ v32_out,
                     uint64_t n, MapRef M, int bits, int shift,
@@ -342,6 +374,30 @@ __global__ void __launch_bounds__(kThreads, 3)
     const uint64_t wb0 = tile_base + (uint64_t)warp * (32 * ITEMS);
     const uint32_t tile_valid = (uint32_t)umin64(kT, n - tile_base);
     R.finish(wb0, n, lane);
+    uint32_t* wb = S.wbase[warp];
+    const unsigned lt = lanemask_lt();
+#if DDM_MSD_RANK == 1
+    // per-warp digit counters (this warp's row only)
+    {
+      uint4* z = reinterpret_cast<uint4*>(wb);
+      for (int i = lane; i < kRadix / 4; i += 32) z[i] = make_uint4(0, 0, 0, 0);
+    }
+    __syncwarp();
+    // rank inside the warp: lr = #earlier records of the warp with the same
+    // digit (its counter before this item + the peers below this lane)
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const bool valid = wb0 + i * 32 + lane < n;
+      const uint32_t d = (BK(R.key[i]) >> shift) & 255u;
+      const unsigned pm = digit_peers(d, __ballot_sync(kFull, valid));
+      const uint32_t c = wb[d];
+      const unsigned below = pm & lt;
+      S.dl[i][tid] = d | ((c + __popc(below)) << 8);
+      if (valid && below == 0) wb[d] = c + __popc(pm);
+      __syncwarp();
+    }
+    __syncthreads();
+#else
     {
       uint4* z = reinterpret_cast<uint4*>(&S.wbase[0][0]);
       constexpr int kZ = 2 * kWarps * kRadix / 4;
@@ -350,13 +406,13 @@ __global__ void __launch_bounds__(kThreads, 3)
     }
     __syncthreads();
     uint32_t dg[ITEMS];
-    uint32_t* wb = S.wbase[warp];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       dg[i] = (BK(R.key[i]) >> shift) & 255u;
       if (wb0 + i * 32 + lane < n) atomicAdd(&wb[dg[i]], 1u);
     }
     __syncthreads();
+#endif
     uint32_t total = 0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
@@ -372,8 +428,21 @@ __global__ void __launch_bounds__(kThreads, 3)
     for (int w = 0; w < kWarps; ++w) S.wbase[w][tid] += tstart;
     __syncthreads();
 
+#if DDM_MSD_RANK == 1
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      if (wb0 + i * 32 + lane < n) {
+        const uint32_t x = S.dl[i][tid];
+        const uint32_t d = x & 255u;
+        const uint32_t pos = wb[d] + (x >> 8);
+        S.keys[pos] = R.key[i];
+        if (V64) S.v64[pos] = R.hv[i];
+        if (V32) S.v32[pos] = R.iv[i];
+        S.dg[pos] = (uint8_t)d;
+      }
+    }
+#else
     uint32_t* mmask = S.match[warp];
-    const unsigned lt = lanemask_lt();
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const bool valid = wb0 + i * 32 + lane < n;
@@ -400,6 +469,7 @@ __global__ void __launch_bounds__(kThreads, 3)
       }
       __syncwarp();
     }
+#endif
     // claim the next tile and start its loads (the current tile now lives in smem)
     if (tid == 0) S.tile_id = atomicAdd(tile_counter, 1u);
     __syncthreads();
@@ -432,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 3)
       }
       st_relaxed_u32(my_status, radix::kFlagPre | (excl + total));
     }
-    S.digit_base[tid] = (long long)bin_start[tid] + (long long)excl - (long long)tstart;
+    S.digit_base[tid] = bin_start[tid] + excl - tstart;  // (mod 2^32)
     __syncthreads();
 
 #pragma unroll
@@ -441,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 3)
       if (p < tile_valid) {
         const uint64_t k = S.keys[p];
         const uint32_t d = S.dg[p];
-        const uint64_t dst = (uint64_t)(S.digit_base[d] + (long long)p);
+        const uint64_t dst = (uint32_t)(S.digit_base[d] + p);
         k_out[dst] = k;
         if (V64) v64_out[dst] = S.v64[p];
         if (V32) v32_out[dst] = S.v32[p];

@@ -27,6 +27,7 @@ DDM_EMIT_FORCE_CHUNK = 1 << 10
 DDM_SORT_LSB = 1 << 12
 DDM_COUNT_RANKS = 1 << 13
 DDM_COUNT_WALK = 1 << 14
+DDM_SWEEP_DIM0 = 1 << 15
 
 STATUS = {0: "DDM_OK", 1: "DDM_ERR_INVALID_ARGUMENT", 2: "DDM_ERR_NONFINITE",
           3: "DDM_ERR_INVERTED_INTERVAL", 4: "DDM_ERR_CAPACITY", 5: "DDM_ERR_WORKSPACE",
@@ -90,6 +91,8 @@ def load() -> ctypes.CDLL:
         "ddm_match_count_indexed": ([vp, R, ctypes.POINTER(u64), vp, sz, vp], i32),
         "ddm_chunk_start_sets": ([R, vp, vp, vp, u64, ctypes.POINTER(u64), vp, sz, vp], i32),
         "ddm_slab_sample": ([vp, u64, vp, u32, vp], i32),
+        "ddm_literal_workspace_bytes": ([u32, u64, u64, u64], sz),
+        "ddm_match_pairs_literal": ([R, vp, u64, ctypes.POINTER(u64), u64, ctypes.POINTER(u64), vp, sz, vp], i32),
         "ddm_slab_cuts": ([vp, u32, u32, vp, vp], i32),
         "ddm_slab_pack_workspace_bytes": ([u64, u32], sz),
         "ddm_slab_pack": ([R, i32, u64, vp, u32, vp, vp, vp, vp, u64, ctypes.POINTER(u64), vp, sz, vp], i32),
@@ -118,7 +121,7 @@ EXPORTED = ["ddm_workspace_bytes", "ddm_match_count", "ddm_match_pairs", "ddm_ma
             "ddm_indexed_workspace_bytes", "ddm_match_pairs_indexed", "ddm_match_count_indexed",
             "ddm_events_workspace_bytes", "ddm_match_pairs_events",
             "ddm_sub_index_update_workspace_bytes", "ddm_sub_index_update",
-            "ddm_chunk_start_sets", "ddm_slab_sample", "ddm_slab_cuts", "ddm_slab_pack_workspace_bytes",
+            "ddm_chunk_start_sets", "ddm_literal_workspace_bytes", "ddm_match_pairs_literal", "ddm_slab_sample", "ddm_slab_cuts", "ddm_slab_pack_workspace_bytes",
             "ddm_slab_pack", "ddm_slab_unpack",
             "ddm_radix_sort_workspace_bytes", "ddm_radix_sort_u64", "ddm_encode_keys", "ddm_status_string",
             "ddm_last_cuda_error", "ddm_kernel_launch_count", "ddm_build_info", "ddm_profile_enable",
@@ -351,6 +354,25 @@ def chunk_start_sets(sub_lo, sub_hi, upd_lo, upd_hi):
     _check(L.ddm_chunk_start_sets(ctypes.byref(r), first.data_ptr(), off.data_ptr(), ids.data_ptr(), ids.numel(),
                                   ctypes.byref(T), ws.data_ptr(), ws.numel(), st), "ddm_chunk_start_sets")
     return first[:tiles], off, ids[: int(T.value)]
+
+
+def match_pairs_literal(sub_lo, sub_hi, upd_lo, upd_hi, dim_capacity: int | None = None) -> torch.Tensor:
+    """The literal d-dim reading (ddm_match_pairs_literal: per-dimension pair
+    sets intersected by sort-merge), canonical order.  dim_capacity defaults
+    to the largest per-dimension count (found by a first call)."""
+    L = load()
+    r, keep = regions(sub_lo, sub_hi, upd_lo, upd_hi)
+    dev = keep[0].device if keep else torch.device("cuda")
+    st = _stream(dev)
+    K, Kd = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    if dim_capacity is None:
+        dim_capacity = max(match_count(sub_lo[k:k + 1], sub_hi[k:k + 1], upd_lo[k:k + 1], upd_hi[k:k + 1])
+                           for k in range(r.d))
+    ws = _workspace(L.ddm_literal_workspace_bytes(r.d, r.n_sub, r.n_upd, dim_capacity), dev)
+    out = torch.empty((max(dim_capacity, 1), 2), dtype=torch.int32, device=dev)
+    _check(L.ddm_match_pairs_literal(ctypes.byref(r), out.data_ptr(), out.shape[0], ctypes.byref(K), dim_capacity,
+                                     ctypes.byref(Kd), ws.data_ptr(), ws.numel(), st), "ddm_match_pairs_literal")
+    return out[: int(K.value)]
 
 
 def match_pairs_events(sub_lo, sub_hi, upd_lo, upd_hi, sort: bool = True) -> torch.Tensor:

@@ -365,6 +365,58 @@ def test_c4_full_exact(orc):
     assert np.array_equal(got, ref)
 
 
+def test_sweep_dim_choice_skewed(orc):
+    """k* = argmin_k K_k: with long dim-0 extents and short
+    dim-1 extents the pipeline sweeps dimension 1 (its rows then follow the
+    dim-1 lower bounds); the pair set equals the oracle's and the forced
+    dim-0 sweep's (DDM_SWEEP_DIM0), for pairs and count."""
+    rng = np.random.default_rng(81)
+    for d in (2, 3):
+        n, m = 30_000, 25_000
+        sl = rng.uniform(0, 1e4, (d, n))
+        ul = rng.uniform(0, 1e4, (d, m))
+        ls = np.full((d, 1), 3.0)
+        ls[0] = 900.0  # dim 0: long (dense); the others short
+        sh, uh = sl + ls, ul + ls
+        ref = orc.sbm_seq(sl, sh, ul, uh)
+        g = [cuda(x) for x in (sl, sh, ul, uh)]
+        p = ddm.match_pairs(*g)
+        assert np.array_equal(words_of(p), ref)
+        # rows follow the lower bounds of the swept dimension 1
+        rows_lo = ul[1][p[:, 1].cpu().numpy().astype(np.int64)]
+        assert np.all(np.diff(rows_lo) >= 0)
+        p0 = ddm.match_pairs(*g, flags=ddm.DDM_SWEEP_DIM0)
+        assert np.array_equal(words_of(p0), ref)
+        assert np.all(np.diff(ul[0][p0[:, 1].cpu().numpy().astype(np.int64)]) >= 0)
+        assert ddm.match_count(*g) == ref.size
+        for f in (ddm.DDM_EMIT_FORCE_THREAD, ddm.DDM_EMIT_FORCE_WARP, ddm.DDM_SORT_LSB):
+            assert np.array_equal(words_of(ddm.match_pairs(*g, flags=f)), ref)
+
+
+def test_literal_intersection_equals_sweep(orc):
+    """G10, the literal reading of P:237-247: per-dimension pair sets sorted
+    and intersected by sort-merge on the GPU equal the oracle's literal form
+    (sbm_dd_literal), brute force and the filtered sweep; canonical order."""
+    rng = np.random.default_rng(82)
+    for d in (1, 2, 3, 5):
+        for trial in range(3):
+            n, m = int(rng.integers(1, 3000)), int(rng.integers(1, 3000))
+            sl = np.floor(rng.uniform(0, 60, (d, n)))
+            ul = np.floor(rng.uniform(0, 60, (d, m)))
+            sh = sl + np.floor(rng.uniform(0, 12, (d, n)))
+            uh = ul + np.floor(rng.uniform(0, 12, (d, m)))
+            ref = orc.sbm_dd_literal(sl, sh, ul, uh)
+            assert np.array_equal(ref, orc.bf_pairs(sl, sh, ul, uh))
+            g = [cuda(x) for x in (sl, sh, ul, uh)]
+            lit = ddm.match_pairs_literal(*g)
+            assert np.array_equal(raw_words(lit), ref)  # already canonical
+            assert np.array_equal(words_of(ddm.match_pairs(*g)), ref)
+    # a per-dimension set larger than dim_capacity is refused, not truncated
+    with pytest.raises(ddm.DDMError) as e:
+        ddm.match_pairs_literal(*g, dim_capacity=1)
+    assert e.value.status == 4
+
+
 def test_dd_chunks_and_long_intervals(orc):
     """d = 2 and 3 with tiles whose candidate sets span many shared-memory
     chunks, long intervals in every dimension (A_t walk skips, dim-1 bin
