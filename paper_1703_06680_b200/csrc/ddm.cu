@@ -1345,6 +1345,11 @@ static ddm_status sweep_dim(const ddm_regions* R, const std::string& key, double
   for (uint32_t k = 1; k < R->d; ++k)
     if (est[k] < est[best]) best = (int)k;
   if (!(est[best] < 0.9 * est[0])) best = 0;
+  if (getenv("DDM_DEBUG")) {
+    fprintf(stderr, "libddm: sweep-dimension estimates");
+    for (uint32_t k = 0; k < R->d; ++k) fprintf(stderr, " %g", est[k]);
+    fprintf(stderr, " -> k* = %d\n", best);
+  }
   std::lock_guard<std::mutex> lk(g_dim_mu);
   if (g_dim_probe.size() > 4096) g_dim_probe.clear();
   g_dim_probe[key] = best;

@@ -36,9 +36,17 @@ constexpr int kTile = kThreads * kItems;
 constexpr int kSpan = 2048;      // nominal records per local-sort CTA
 constexpr int kCap = 2560;       // records a local-sort CTA can hold
 constexpr int kCapPow2 = 4096;   // bitonic network size bound (next power of two >= kCap)
-constexpr int kFineBinBits = 11;
+#ifndef DDM_LS_BINBITS
+#define DDM_LS_BINBITS 11
+#endif
+constexpr int kFineBinBits = DDM_LS_BINBITS;
 constexpr int kFineBins = 1 << kFineBinBits;  // value bins of the in-smem counting sort
 constexpr int kMaxBinRun = 64;   // larger bins (ties, clusters) -> bitonic sort of the group
+// Order inside a fine bin: DDM_LS_RANK 1 (default) ranks every record among
+// its bin's members (a thread per record); 0: insertion sort per bin (round 1).
+#ifndef DDM_LS_RANK
+#define DDM_LS_RANK 1
+#endif
 
 
 // Value -> bucket map, equalised to the data.  t(x) = (x/2 - min/2) * kCoarse /
@@ -539,6 +547,9 @@ struct LocalSmem {  // keys only: payloads follow the permutation through the ke
   uint16_t perm[kCap];
   static_assert(sizeof(uint32_t) * (kFineBins / 2 + 2) + sizeof(uint16_t) * kCap >= sizeof(uint16_t) * kCapPow2,
                 "the bitonic fallback's u16[kCapPow2] fits in binw + perm");
+#if DDM_LS_RANK
+  uint16_t perm2[kCap];  // final order (sorted position -> staged index)
+#endif
   uint64_t red[2 * kWarps];
   uint32_t flag;
   uint64_t bound[1];  // prev_boundary's reduction slot
@@ -639,6 +650,27 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
       S.perm[pos] = (uint16_t)i;
     }
     __syncthreads();
+#if DDM_LS_RANK
+    // ... then every record takes its rank inside its bin, (key, staged
+    // index) order, from the bin's other members: one record per thread, so
+    // the work is spread evenly (most bins hold one record; an insertion sort
+    // per bin left a warp waiting on its longest bin); bin b spans
+    // [end(b-1), end(b)), <= kMaxBinRun
+    for (uint32_t x = tid; x < c; x += kThreads) {
+      const uint16_t v = S.perm[x];
+      const uint64_t kv = K[v];
+      const uint32_t b = (uint32_t)((kv - kmin) >> sh);
+      const uint32_t lo = b ? bin_get(S.binw, b - 1) : 0, hi = bin_get(S.binw, b);
+      uint32_t r = 0;
+      for (uint32_t y = lo; y < hi; ++y) {
+        const uint16_t u = S.perm[y];
+        const uint64_t ku = K[u];
+        r += (ku < kv || (ku == kv && u < v));
+      }
+      S.perm2[lo + r] = v;
+    }
+  }
+#else
     // ... then order each bin holding two or more records by (key, staged
     // index) with an insertion sort; bin b spans [end(b-1), end(b)), <= kMaxBinRun
     for (uint32_t b = tid; b < kFineBins; b += kThreads) {
@@ -658,7 +690,9 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
         S.perm[y] = v;
       }
     }
-  } else {
+  }
+#endif
+  else {
     // bitonic sort of (key, index) over the next power of two, in the
     // bins + perm storage taken as one u16 array
     uint16_t* PB = reinterpret_cast<uint16_t*>(S.binw);
@@ -684,7 +718,11 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
     }
   }
   __syncthreads();
+#if DDM_LS_RANK
+  const uint16_t* PERM = S.flag ? reinterpret_cast<const uint16_t*>(S.binw) : S.perm2;
+#else
   const uint16_t* PERM = S.flag ? reinterpret_cast<const uint16_t*>(S.binw) : S.perm;
+#endif
   for (uint32_t i = tid; i < c; i += kThreads) k_out[e0 + i] = K[PERM[i]];
   // payloads: staged coalesced through the key buffer (free now), then read
   // back in permutation order -- random global gathers would cost one L1

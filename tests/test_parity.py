@@ -375,8 +375,9 @@ def test_sweep_dim_choice_skewed(orc):
         n, m = 30_000, 25_000
         sl = rng.uniform(0, 1e4, (d, n))
         ul = rng.uniform(0, 1e4, (d, m))
-        ls = np.full((d, 1), 3.0)
-        ls[0] = 900.0  # dim 0: long (dense); the others short
+        ls = np.full((d, 1), 60.0)
+        ls[0] = 900.0  # dim 0: long (dense); dim 1 shortest, so k* = 1
+        ls[1] = 3.0
         sh, uh = sl + ls, ul + ls
         ref = orc.sbm_seq(sl, sh, ul, uh)
         g = [cuda(x) for x in (sl, sh, ul, uh)]
