@@ -128,8 +128,8 @@ typedef struct {
  * K_k; P:237-247 leaves the choice open) -- a probe of 4096 sampled regions
  * per kind estimates K_k / (n m) = (mean S length + mean U length) / span of
  * the lower bounds, and k* replaces dimension 0 when its estimate is at least
- * 10 % smaller (one small device->host read on the first call of a call
- * site).  The pair set is the same for every sweep dimension; the row order
+ * 10 % smaller (one small device->host read per call: the choice follows
+ * the data).  The pair set is the same for every sweep dimension; the row order
  * then follows dimension k*.  This flag sweeps dimension 0 always.  The
  * subscription index (ddm_sub_index_build) always sweeps dimension 0. */
 #define DDM_SWEEP_DIM0 (1u << 15)

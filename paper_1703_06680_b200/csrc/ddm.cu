@@ -1317,21 +1317,15 @@ size_t ddm_workspace_bytes(uint32_t d, uint64_t n_sub, uint64_t n_upd, int want_
 std::mutex g_probe_mu;
 std::unordered_map<std::string, bool> g_probe;  // count-form decision per call site
 
-std::mutex g_dim_mu;
-std::unordered_map<std::string, int> g_dim_probe;  // sweep-dimension choice per call site
-
 // k* for d > 1: the dimension with the fewest estimated
 // candidate pairs (match::dim_probe_kernel), dimension 0 unless another one
 // is estimated at least 10 % smaller.  Any choice gives the same pair set
-// (the other dimensions are filtered exactly); it only changes the work and
-// the row order.  Decided once per call site (one small device->host read).
-static ddm_status sweep_dim(const ddm_regions* R, const std::string& key, double* probe, cudaStream_t st, int* kout) {
+// (the other dimensions are filtered exactly); it changes the work and the
+// row order, so it is decided from the data on every call (one small
+// device->host read) -- a decision cached per call site could be stale when
+// new data arrives in the same buffers and would change the order.
+static ddm_status sweep_dim(const ddm_regions* R, double* probe, cudaStream_t st, int* kout) {
   *kout = 0;
-  {
-    std::lock_guard<std::mutex> lk(g_dim_mu);
-    const auto it = g_dim_probe.find(key);
-    if (it != g_dim_probe.end()) { *kout = it->second; return DDM_OK; }
-  }
   match::ProbeDims P{};
   for (uint32_t k = 0; k < R->d; ++k) {
     P.sub_lo[k] = R->sub_lo[k]; P.sub_hi[k] = R->sub_hi[k]; P.upd_lo[k] = R->upd_lo[k]; P.upd_hi[k] = R->upd_hi[k];
@@ -1350,9 +1344,6 @@ static ddm_status sweep_dim(const ddm_regions* R, const std::string& key, double
     for (uint32_t k = 0; k < R->d; ++k) fprintf(stderr, " %g", est[k]);
     fprintf(stderr, " -> k* = %d\n", best);
   }
-  std::lock_guard<std::mutex> lk(g_dim_mu);
-  if (g_dim_probe.size() > 4096) g_dim_probe.clear();
-  g_dim_probe[key] = best;
   *kout = best;
   return DDM_OK;
 }
@@ -1372,7 +1363,7 @@ static ddm_status match_full(const ddm_regions* R, ddm_pair* pairs, uint64_t cap
     MatchWs W = match_layout(R->d, R->n_sub, R->n_upd,
                              static_cast<uint8_t*>(ws) + a256(index_layout(R->d, R->n_sub, nullptr).bytes), true);
     int k = 0;
-    DDM_TRY(sweep_dim(R, graph_key(R, ws, ws_bytes, flags, pairs != nullptr, sub_map, upd_map, st), W.probe, st, &k));
+    DDM_TRY(sweep_dim(R, W.probe, st, &k));
     if (k != 0) {
       ddm_regions V = *R;
       std::swap(V.sub_lo[0], V.sub_lo[k]);

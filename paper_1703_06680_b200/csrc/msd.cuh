@@ -30,7 +30,10 @@ namespace msd {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kRadix = 256;
-constexpr int kItems = 8;
+#ifndef DDM_MSD_ITEMS
+#define DDM_MSD_ITEMS 8
+#endif
+constexpr int kItems = DDM_MSD_ITEMS;  // records per thread of a payload pass tile
 constexpr int kItemsK = 16;  // key-only passes: bigger tiles (fewer look-backs; measured 0.83 -> 0.70 ms at c3)
 constexpr int kTile = kThreads * kItems;
 constexpr int kSpan = 2048;      // nominal records per local-sort CTA
@@ -486,7 +489,10 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
 
     uint32_t excl = 0;
     if (tile > 0) {
-      constexpr int kLB = 8;
+#ifndef DDM_MSD_LB
+#define DDM_MSD_LB 8
+#endif
+      constexpr int kLB = DDM_MSD_LB;  // predecessors read per look-back step
       int64_t p = (int64_t)tile - 1;
       while (true) {
         uint32_t sv[kLB];
