@@ -559,6 +559,43 @@ __device__ __forceinline__ uint32_t wseek(const uint64_t* W, uint32_t k, uint32_
   return lo;
 }
 
+// First index of the sorted window W[0, len) whose key is > x (len if none),
+// starting from an interpolated guess and galloping towards the answer: the
+// first row of a count thread lands within a few entries of its guess on
+// near-uniform keys (a plain binary search over the window took 12 steps).
+__device__ __forceinline__ uint32_t ub_interp(const uint64_t* W, uint32_t len, uint64_t x) {
+  if (len == 0) return 0;
+  const uint64_t w0 = W[0], w1 = W[len - 1];
+  if (x < w0) return 0;
+  if (x >= w1) return len;
+  uint32_t g = (uint32_t)((double)(x - w0) / (double)(w1 - w0) * (double)(len - 1));
+  g = min(g, len - 1);
+  uint32_t lo, hi;  // the answer lies in [lo, hi]
+  if (W[g] <= x) {
+    lo = g + 1;
+    for (uint32_t step = 1;; step <<= 1) {
+      const uint32_t p = lo + step - 1;
+      if (p >= len) { hi = len; break; }
+      if (W[p] > x) { hi = p; break; }
+      lo = p + 1;
+    }
+  } else {
+    hi = g;
+    for (uint32_t step = 1;; step <<= 1) {
+      if (hi < step) { lo = 0; break; }
+      const uint32_t p = hi - step;
+      if (W[p] <= x) { lo = p + 1; break; }
+      hi = p;
+    }
+  }
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (W[mid] > x) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
 // Advance a merge cursor: pos is an absolute index into the sorted array g
 // with every entry before pos "before" x; returns the first index whose entry
 // is "after" x.  The slice [base, base+len) is staged in W (shared memory);
@@ -723,8 +760,7 @@ __global__ void __launch_bounds__(kCountThreads, DDM_COUNT_MINB) count_kernel(
   for (int i = 0; i < kCountItems; ++i) cnt[i] = 0;
   if (ni > 0) {
     // first update: binary search inside the windows (falls back to global)
-    uint64_t rl = advance<true>(W0, p0, ls, slo_key, n,
-                                p0 + ((ls && W0[ls - 1] > a[0]) ? ub(W0, 0, ls, a[0]) : ls), a[0]);
+    uint64_t rl = advance<true>(W0, p0, ls, slo_key, n, p0 + ub_interp(W0, ls, a[0]), a[0]);
     uint64_t rh = 0;
     if (!WALK)
       rh = advance<false>(H0, h0, lh, shi_key, n, h0 + ((lh && H0[lh - 1] >= a[0]) ? lb(H0, 0, lh, a[0]) : lh), a[0]);
