@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ddm", choices=["ddm", "reference"])
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--alpha", type=float, default=None,
+                    help="replace the config's overlap degree alpha (count-mode K-independence sweep, P:960-963)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--mode", default="pairs", choices=["pairs", "count"],
@@ -206,6 +208,25 @@ def time_oracle(sample, reps=1, count_only=False):
     return best, K, P, method
 
 
+def host_info() -> dict:
+    """The host the CPU baseline runs on: CPU model (lscpu / /proc/cpuinfo),
+    logical CPUs, and the CPUs this process may run on (affinity)."""
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except AttributeError:
+        aff = None
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "affinity_cpus": aff,
+            "omp_num_threads": os.environ.get("OMP_NUM_THREADS")}
+
+
 def sample_text(s, frac):
     return (f"{s.name}: regions with dim-0 lower bound in a {frac:g} L window centred on the median "
             f"({s.n + s.m} regions)")
@@ -216,7 +237,7 @@ def run_reference(args):
     if rank != 0:
         return
     from paper_1703_06680_b200 import workload as wl
-    w = wl.make(args.config)
+    w = wl.make(args.config, alpha=args.alpha)
     frac = CPU_SAMPLE_FRAC[args.config]
     s = cpu_sample(w, frac)
     for _ in range(args.warmup):
@@ -233,8 +254,10 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "pairs_per_s": K * args.steps / t,
-            "config": workload_config(w, {"parallelism": f"CPU x{P} ({method})", "sample": sample}),
-            "cpu_baseline": {"value": val, "unit": "regions/s", "cores": P, "kind": "oracle", "sample": sample},
+            "config": workload_config(w, {"parallelism": f"CPU x{P} ({method})", "sample": sample,
+                                          "l2": "n/a (host CPU)"}),
+            "cpu_baseline": {"value": val, "unit": "regions/s", "cores": P, "kind": "oracle", "sample": sample,
+                             "host": host_info()},
             "e2e": {"value": val, "unit": "regions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -264,7 +287,7 @@ def run_ddm(args):
         else:
             dist.init_process_group("gloo")
     ddm.load()
-    w = wl.make(args.config)
+    w = wl.make(args.config, alpha=args.alpha)
     hbm_peak, peak_src = peaks()
 
     def sync_all():
@@ -279,7 +302,7 @@ def run_ddm(args):
         g = [torch.from_numpy(a).to(dev) for a in (w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi)]
         M = ddm.Matcher(w.d, w.n, w.m, dev)
         K = M.count(*g)
-        out = torch.empty((max(K, 1), 2), dtype=torch.int32, device=dev)
+        out = torch.empty((max(K, 1), 2), dtype=torch.int32, device=dev) if args.mode == "pairs" else None
 
         def step():
             return M.pairs_into(out, *g) if args.mode == "pairs" else M.count(*g)
@@ -503,7 +526,15 @@ def run_ddm(args):
         s = cpu_sample(w, frac)
         dt, ks, P, method = time_oracle(s, count_only=args.mode == "count")
         cpu = {"value": (s.n + s.m) / dt, "unit": "regions/s", "cores": P, "kind": "oracle",
-               "sample": f"{sample_text(s, frac)}, K={ks}; {method}, {dt:.2f} s"}
+               "sample": f"{sample_text(s, frac)}, K={ks}; {method}, {dt:.2f} s", "host": host_info()}
+        if args.config in ("c1", "c2"):
+            # brute force (Alg. 2, all host cores) on the same sample
+            import oracle
+            t0 = time.perf_counter()
+            kb = oracle.bf_count(s.sub_lo, s.sub_hi, s.upd_lo, s.upd_hi)
+            db = time.perf_counter() - t0
+            cpu["brute_force"] = {"value": (s.n + s.m) / db, "unit": "regions/s", "cores": oracle.max_threads(),
+                                  "sample": f"{sample_text(s, frac)}, K={kb}; oracle.bf_count (Alg. 2), {db:.2f} s"}
         if w.d == 1:
             # also the serial SBM (Alg. 4) on one core, on a
             # tenth of that window (the paper's serial baseline)

@@ -118,16 +118,22 @@ def clustered(n: int, m: int, L: float, l: float, seed: int, n_centres: int = 64
                     out["upd"][0], out["upd"][1])
 
 
-def make(name: str, scale: float = 1.0) -> Workload:
+def make(name: str, scale: float = 1.0, alpha: float | None = None) -> Workload:
     """Build BASELINE config `name` (c1..c5).  `scale` < 1 shrinks n and m while
-    keeping L, alpha and the seed's recipe (used only by tests and samples)."""
+    keeping L, alpha and the seed's recipe (used only by tests and samples);
+    `alpha` replaces the config's overlap degree (the paper's K-independence
+    sweep of count mode)."""
     cfg = CONFIGS[name]
     n = max(1, int(round(cfg["n"] * scale)))
     N = 2 * cfg["n"]
-    l = side_length(N, cfg["L"], cfg["alpha"], cfg["d"])
+    a = cfg["alpha"] if alpha is None else float(alpha)
+    l = side_length(N, cfg["L"], a, cfg["d"])
+    tag = name if scale == 1.0 else f"{name}@{scale:g}"
+    if alpha is not None:
+        tag += f"[alpha={a:g}]"
     if cfg["kind"] == "uniform":
-        return uniform(n, n, cfg["L"], l, cfg["d"], cfg["seed"], name=name if scale == 1.0 else f"{name}@{scale:g}")
-    return clustered(n, n, cfg["L"], l, cfg["seed"], name=name if scale == 1.0 else f"{name}@{scale:g}")
+        return uniform(n, n, cfg["L"], l, cfg["d"], cfg["seed"], name=tag)
+    return clustered(n, n, cfg["L"], l, cfg["seed"], name=tag)
 
 
 def window_sample(w: Workload, frac: float) -> Workload:
