@@ -1137,7 +1137,7 @@ struct EmitTileSmem {
   alignas(16) uint2 stage[kEmitStage > 0 ? kEmitStage : 1];
   uint64_t bar;
   uint32_t rbmax;
-  unsigned long long oend;
+  uint32_t oend;  // the tile's output length (capped at 2^32 - 1: then never staged)
   uint64_t wsum[32];
 };
 
@@ -1235,11 +1235,15 @@ __global__ void __launch_bounds__(kEmitThreads, DDM_EMIT_MINB) emit_tile_kernel(
   // written out coalesced when it fits (a thread's rows are ~8 pairs apart from
   // its neighbours', so direct stores touch a sector per pair)
   const uint64_t obeg = A.tile_off[j0 >> 8];
-  if (tid == 0) S.oend = obeg;
+  if (tid == 0) S.oend = 0;
   __syncthreads();  // (also: the barrier is initialised before anyone waits on it)
-  if (ni > 0) atomicMax(&S.oend, (unsigned long long)(o + mine));
+  {  // the tile's output length: one shared atomic per warp
+    const uint64_t e = ni > 0 ? o + mine - obeg : 0;
+    const uint32_t w = __reduce_max_sync(kFull, (uint32_t)umin64(e, 0xffffffffull));
+    if (lane == 0 && w) atomicMax(&S.oend, w);
+  }
   __syncthreads();
-  const uint64_t olen = S.oend - obeg;
+  const uint64_t olen = S.oend;
   const bool staged = kEmitStage > 0 && olen <= (uint64_t)kEmitStage;
   mbar_wait(&S.bar, 0);
   auto hi_at = [&](uint64_t i) -> uint64_t {

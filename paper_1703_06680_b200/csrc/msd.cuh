@@ -433,6 +433,23 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
     }
     uint32_t* my_status = status + (uint64_t)tile * kRadix + tid;
     st_relaxed_u32(my_status, (tile == 0 ? radix::kFlagPre : radix::kFlagAgg) | total);
+#ifndef DDM_MSD_LB
+#define DDM_MSD_LB 8
+#endif
+    constexpr int kLB = DDM_MSD_LB;  // predecessors read per look-back step
+#ifndef DDM_MSD_LBPRE
+#define DDM_MSD_LBPRE 1
+#endif
+    // DDM_MSD_LBPRE: the look-back's first batch of predecessor words is read
+    // now and consumed after the ranking, so one round trip hides under it
+    // (stale words are still exact aggregates; unpublished ones are re-read)
+    uint32_t sv0[DDM_MSD_LBPRE ? kLB : 1];
+    if (DDM_MSD_LBPRE && tile > 0) {
+#pragma unroll
+      for (int k = 0; k < kLB; ++k)
+        sv0[k] = (int64_t)tile - 1 - k >= 0 ? ld_relaxed_u32(status + (uint64_t)(tile - 1 - k) * kRadix + tid)
+                                            : radix::kFlagPre;
+    }
     uint32_t dummy;
     const uint32_t tstart = block_excl_scan<kThreads>(total, S.scan_tmp, &dummy);
 #pragma unroll
@@ -489,16 +506,15 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
 
     uint32_t excl = 0;
     if (tile > 0) {
-#ifndef DDM_MSD_LB
-#define DDM_MSD_LB 8
-#endif
-      constexpr int kLB = DDM_MSD_LB;  // predecessors read per look-back step
       int64_t p = (int64_t)tile - 1;
+      bool first = DDM_MSD_LBPRE != 0;
       while (true) {
         uint32_t sv[kLB];
 #pragma unroll
         for (int k = 0; k < kLB; ++k)
-          sv[k] = p - k >= 0 ? ld_relaxed_u32(status + (uint64_t)(p - k) * kRadix + tid) : radix::kFlagPre;
+          sv[k] = first ? sv0[DDM_MSD_LBPRE ? k : 0]
+                        : (p - k >= 0 ? ld_relaxed_u32(status + (uint64_t)(p - k) * kRadix + tid) : radix::kFlagPre);
+        first = false;
         int consumed = 0;
         bool hit_pre = false;
 #pragma unroll
@@ -511,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
           hit_pre = (v & radix::kFlagPre) != 0;
         }
         if (hit_pre) break;
-        if (consumed == 0) __nanosleep(32);
+        if (consumed == 0 && !first) __nanosleep(32);
         p -= consumed;
       }
       st_relaxed_u32(my_status, radix::kFlagPre | (excl + total));
@@ -668,11 +684,12 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
       const uint32_t b = (uint32_t)((kv - kmin) >> sh);
       const uint32_t lo = b ? bin_get(S.binw, b - 1) : 0, hi = bin_get(S.binw, b);
       uint32_t r = 0;
-      for (uint32_t y = lo; y < hi; ++y) {
-        const uint16_t u = S.perm[y];
-        const uint64_t ku = K[u];
-        r += (ku < kv || (ku == kv && u < v));
-      }
+      if (hi - lo > 1)  // (most bins hold this record alone)
+        for (uint32_t y = lo; y < hi; ++y) {
+          const uint16_t u = S.perm[y];
+          const uint64_t ku = K[u];
+          r += (uint32_t)(ku < kv) | ((uint32_t)(ku == kv) & (uint32_t)(u < v));
+        }
       S.perm2[lo + r] = v;
     }
   }
