@@ -1126,18 +1126,11 @@ constexpr int kEmitWarpsPerRowTile = kRowTile / (32 * kEmitItems);  // warps sha
 constexpr int kEmitWin = 4096;                     // window entries
 constexpr int kEmitPad = 512;                      // window entries before r_lo(first row)
 
-#ifndef DDM_EMIT_STAGE
-#define DDM_EMIT_STAGE 3072
-#endif
-constexpr int kEmitStage = DDM_EMIT_STAGE;  // pairs a tile stages in shared memory (its whole output, if it fits)
-
 struct EmitTileSmem {
   alignas(16) uint64_t wh[kEmitWin + 2];
   alignas(16) uint32_t wi[kEmitWin + 4];
-  alignas(16) uint2 stage[kEmitStage > 0 ? kEmitStage : 1];
   uint64_t bar;
   uint32_t rbmax;
-  uint32_t oend;  // the tile's output length (capped at 2^32 - 1: then never staged)
   uint64_t wsum[32];
 };
 
@@ -1231,20 +1224,7 @@ __global__ void __launch_bounds__(kEmitThreads, DDM_EMIT_MINB) emit_tile_kernel(
     for (int v = warp - warp % kEmitWarpsPerRowTile; v < warp; ++v) wpre += S.wsum[v];
   }
   uint64_t o = (ni > 0 ? A.tile_off[(j0 >> 8) + warp / kEmitWarpsPerRowTile] : 0) + wpre + incl - mine;
-  // the tile's output [obeg, oend) is contiguous: staged in shared memory and
-  // written out coalesced when it fits (a thread's rows are ~8 pairs apart from
-  // its neighbours', so direct stores touch a sector per pair)
-  const uint64_t obeg = A.tile_off[j0 >> 8];
-  if (tid == 0) S.oend = 0;
-  __syncthreads();  // (also: the barrier is initialised before anyone waits on it)
-  {  // the tile's output length: one shared atomic per warp
-    const uint64_t e = ni > 0 ? o + mine - obeg : 0;
-    const uint32_t w = __reduce_max_sync(kFull, (uint32_t)umin64(e, 0xffffffffull));
-    if (lane == 0 && w) atomicMax(&S.oend, w);
-  }
-  __syncthreads();
-  const uint64_t olen = S.oend;
-  const bool staged = kEmitStage > 0 && olen <= (uint64_t)kEmitStage;
+  __syncthreads();  // the barrier is initialised before anyone waits on it
   mbar_wait(&S.bar, 0);
   auto hi_at = [&](uint64_t i) -> uint64_t {
     const uint64_t k = i - w0;
@@ -1259,7 +1239,7 @@ __global__ void __launch_bounds__(kEmitThreads, DDM_EMIT_MINB) emit_tile_kernel(
     if (r >= ni) break;
     const uint32_t uid = A.upd_map ? A.upd_map[lid[r]] : lid[r];
     const uint32_t stab = c0[r] - (rb[r] - rl[r]);
-    uint2* row = staged ? S.stage + (o - obeg) : A.pairs + o;
+    uint2* row = A.pairs + o;
     // stab part: walk Slo backwards from r_lo - 1, exactly `stab` members
     uint32_t rem = stab;
     int64_t i = (int64_t)rl[r] - 1;
@@ -1274,11 +1254,6 @@ __global__ void __launch_bounds__(kEmitThreads, DDM_EMIT_MINB) emit_tile_kernel(
     // range part [r_lo, r_b)
     for (uint32_t k = rl[r]; k < rb[r]; ++k) row[stab + (k - rl[r])] = make_uint2(id_at(k), uid);
     o += c0[r];
-  }
-  if (staged) {
-    __syncthreads();
-    uint2* dst = A.pairs + obeg;
-    for (uint32_t k = tid; k < (uint32_t)olen; k += kEmitThreads) dst[k] = S.stage[k];
   }
 }
 

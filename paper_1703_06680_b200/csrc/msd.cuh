@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
 #endif
     constexpr int kLB = DDM_MSD_LB;  // predecessors read per look-back step
 #ifndef DDM_MSD_LBPRE
-#define DDM_MSD_LBPRE 1
+#define DDM_MSD_LBPRE 0
 #endif
     // DDM_MSD_LBPRE: the look-back's first batch of predecessor words is read
     // now and consumed after the ranking, so one round trip hides under it
