@@ -437,19 +437,6 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
 #define DDM_MSD_LB 8
 #endif
     constexpr int kLB = DDM_MSD_LB;  // predecessors read per look-back step
-#ifndef DDM_MSD_LBPRE
-#define DDM_MSD_LBPRE 0
-#endif
-    // DDM_MSD_LBPRE: the look-back's first batch of predecessor words is read
-    // now and consumed after the ranking, so one round trip hides under it
-    // (stale words are still exact aggregates; unpublished ones are re-read)
-    uint32_t sv0[DDM_MSD_LBPRE ? kLB : 1];
-    if (DDM_MSD_LBPRE && tile > 0) {
-#pragma unroll
-      for (int k = 0; k < kLB; ++k)
-        sv0[k] = (int64_t)tile - 1 - k >= 0 ? ld_relaxed_u32(status + (uint64_t)(tile - 1 - k) * kRadix + tid)
-                                            : radix::kFlagPre;
-    }
     uint32_t dummy;
     const uint32_t tstart = block_excl_scan<kThreads>(total, S.scan_tmp, &dummy);
 #pragma unroll
@@ -507,14 +494,11 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
     uint32_t excl = 0;
     if (tile > 0) {
       int64_t p = (int64_t)tile - 1;
-      bool first = DDM_MSD_LBPRE != 0;
       while (true) {
         uint32_t sv[kLB];
 #pragma unroll
         for (int k = 0; k < kLB; ++k)
-          sv[k] = first ? sv0[DDM_MSD_LBPRE ? k : 0]
-                        : (p - k >= 0 ? ld_relaxed_u32(status + (uint64_t)(p - k) * kRadix + tid) : radix::kFlagPre);
-        first = false;
+          sv[k] = p - k >= 0 ? ld_relaxed_u32(status + (uint64_t)(p - k) * kRadix + tid) : radix::kFlagPre;
         int consumed = 0;
         bool hit_pre = false;
 #pragma unroll
@@ -527,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
           hit_pre = (v & radix::kFlagPre) != 0;
         }
         if (hit_pre) break;
-        if (consumed == 0 && !first) __nanosleep(32);
+        if (consumed == 0) __nanosleep(32);
         p -= consumed;
       }
       st_relaxed_u32(my_status, radix::kFlagPre | (excl + total));
