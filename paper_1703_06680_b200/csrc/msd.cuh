@@ -312,6 +312,8 @@ __device__ __forceinline__ unsigned digit_peers(uint32_t d, unsigned valid) {
 // look-back wait and the scatter of the current tile overlap the next tile's
 // HBM reads.  (Forward progress: the lowest unfinished tile is always some
 // CTA's current tile, and it only waits on lower, finished tiles.)
+constexpr uint64_t kPackSentinel = 0xffffffffull;  // packed record: upper-key delta does not fit 32 bits
+
 template <int ITEMS, bool V64, bool V32, bool SRC_F64>
 struct TileRegs {
   uint64_t key[ITEMS];
@@ -336,12 +338,17 @@ struct TileRegs {
       }
     }
   }
-  // float64 bits -> order-preserving keys (first pass), validating lo/hi
+  // float64 bits -> order-preserving keys (first pass), validating lo/hi.
+  // V64 && !V32 is the PACKED record: the 64-bit payload carries the id in its
+  // low half and the upper key as a delta from the lower key in its high half
+  // (kPackSentinel when the delta does not fit: the local sort then takes the
+  // upper key from the input array) -- 16-byte records instead of 20.
   __device__ __forceinline__ void finish(uint64_t wb0, uint64_t n, int lane) {
     if constexpr (SRC_F64) {
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
-        const bool valid = wb0 + i * 32 + lane < n;
+        const uint64_t idx = wb0 + i * 32 + lane;
+        const bool valid = idx < n;
         const uint64_t bx = key[i];
         if (valid && !f64_finite_bits(bx)) err |= 1u;
         key[i] = valid ? f64_key(__longlong_as_double((long long)bx)) : 0;
@@ -351,7 +358,13 @@ struct TileRegs {
             if (!f64_finite_bits(by)) err |= 1u;
             else if (!(__longlong_as_double((long long)bx) <= __longlong_as_double((long long)by))) err |= 2u;
           }
-          hv[i] = valid ? f64_key(__longlong_as_double((long long)by)) : 0;
+          const uint64_t kh = valid ? f64_key(__longlong_as_double((long long)by)) : 0;
+          if constexpr (!V32) {
+            const uint64_t dk = kh - key[i];
+            hv[i] = ((dk < kPackSentinel ? dk : kPackSentinel) << 32) | (uint32_t)idx;
+          } else {
+            hv[i] = kh;
+          }
         }
       }
     }
@@ -580,7 +593,8 @@ template <bool V64, bool V32>
 __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restrict__ k_in,
                                  const uint64_t* __restrict__ v64_in, const uint32_t* __restrict__ v32_in,
                                  uint64_t* __restrict__ k_out, uint64_t* __restrict__ v64_out,
-                                 uint32_t* __restrict__ v32_out, uint64_t e0, uint32_t c, uint32_t& phase) {
+                                 uint32_t* __restrict__ v32_out, uint64_t e0, uint32_t c, uint32_t& phase,
+                                 const double* __restrict__ hi_src) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // the group's keys arrive by one bulk async copy (16-byte aligned start;
   // reading a key past the array is safe: it is followed by another
@@ -730,6 +744,42 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
 #else
   const uint16_t* PERM = S.flag ? reinterpret_cast<const uint16_t*>(S.binw) : S.perm;
 #endif
+  if constexpr (V64 && !V32) {
+    // PACKED records: sorted keys out (kept in registers), then the payload
+    // (id | upper-key delta << 32) staged through the key buffer, unpacked into
+    // the upper key and the id
+    constexpr int kPer = (kCap + kThreads - 1) / kThreads;
+    uint64_t kr[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const uint32_t i = tid + j * kThreads;
+      if (i < c) {
+        kr[j] = K[PERM[i]];
+        k_out[e0 + i] = kr[j];
+      }
+    }
+    __syncthreads();  // the key buffer is free
+    if (tid == 0) {
+      const uint32_t bytes = ((c + ko + 1) & ~1u) * 8;
+      mbar_expect_tx(&S.bar, bytes);
+      bulk_g2s(S.keys, v64_in + (e0 - ko), bytes, &S.bar);
+    }
+    mbar_wait(&S.bar, phase);
+    phase ^= 1;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const uint32_t i = tid + j * kThreads;
+      if (i < c) {
+        const uint64_t P = K[PERM[i]];
+        const uint32_t id = (uint32_t)P;
+        const uint64_t d = P >> 32;
+        v64_out[e0 + i] = d != kPackSentinel ? kr[j] + d : f64_key(__ldg(hi_src + id));
+        v32_out[e0 + i] = id;
+      }
+    }
+    __syncthreads();
+    return;
+  }
   for (uint32_t i = tid; i < c; i += kThreads) k_out[e0 + i] = K[PERM[i]];
   // payloads: staged coalesced through the key buffer (free now), then read
   // back in permutation order -- random global gathers would cost one L1
@@ -825,7 +875,7 @@ __global__ void __launch_bounds__(256) span_bounds_kernel(const uint64_t* __rest
 // single bucket larger than kCap sets *overflow (caller redoes with LSB).
 template <bool V64, bool V32>
 #ifndef DDM_LS_MINB
-#define DDM_LS_MINB 7
+#define DDM_LS_MINB 6
 #endif
 __global__ void __launch_bounds__(kThreads, DDM_LS_MINB) local_sort_kernel(const uint64_t* __restrict__ k_in,
                                                               const uint64_t* __restrict__ v64_in,
@@ -835,7 +885,8 @@ __global__ void __launch_bounds__(kThreads, DDM_LS_MINB) local_sort_kernel(const
                                                               uint32_t* __restrict__ v32_out, uint64_t n,
                                                               MapRef M, int bits,
                                                               const uint64_t* __restrict__ bounds,
-                                                              uint32_t* __restrict__ overflow) {
+                                                              uint32_t* __restrict__ overflow,
+                                                              const double* __restrict__ hi_src) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocalSmem<V64, V32>& S = *reinterpret_cast<LocalSmem<V64, V32>*>(smem_raw);
   Bucketer BK;
@@ -854,7 +905,8 @@ __global__ void __launch_bounds__(kThreads, DDM_LS_MINB) local_sort_kernel(const
         return;
       }
     }
-    local_sort_group<V64, V32>(S, k_in, v64_in, v32_in, k_out, v64_out, v32_out, e0, (uint32_t)(g1 - e0), phase);
+    local_sort_group<V64, V32>(S, k_in, v64_in, v32_in, k_out, v64_out, v32_out, e0, (uint32_t)(g1 - e0), phase,
+                               hi_src);
     e0 = g1;
   }
 }
