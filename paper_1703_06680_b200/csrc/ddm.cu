@@ -142,11 +142,16 @@ inline ddm_status check_launch() {
     if (s_ != DDM_OK) return s_;  \
   } while (0)
 
+// Payload records of the MSD sort: packed to 16 bytes (key + id | upper-key
+// delta << 32, msd.cuh) for sorts of at least kPackMinN records, where the
+// sort streams through HBM (c3: 5.55 -> 5.24 ms, c5: 66.3 -> 60.4 ms);
+// smaller (L2-resident) sorts keep 20-byte records, since a delta that does
+// not fit 32 bits costs a re-read of the upper bound (DDM_MSD_PACK=0/1 forces).
 #ifndef DDM_MSD_PACK
-#define DDM_MSD_PACK 1
+#define DDM_MSD_PACK 2
 #endif
-constexpr bool kPack = DDM_MSD_PACK != 0;      // payload records packed to 16 bytes (msd.cuh)
-constexpr double kPayRec = kPack ? 16.0 : 20.0;  // bytes of a payload record
+constexpr uint64_t kPackMinN = 1ull << 22;
+inline bool pack_records(uint64_t n) { return DDM_MSD_PACK == 2 ? n >= kPackMinN : DDM_MSD_PACK != 0; }
 
 constexpr int kSMs = 148;
 #ifndef DDM_DD_ROWS
@@ -481,16 +486,22 @@ void init_attrs_once() {
                        (int)sizeof(match::ChunkSmem));
   cudaFuncSetAttribute(match::emit_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(match::EmitTileSmem));
-  cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, true, !kPack, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(msd::PassSmem<msd::kItems, true, !kPack>));
-  cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, true, !kPack, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(msd::PassSmem<msd::kItems, true, !kPack>));
+  cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(msd::PassSmem<msd::kItems, true, true>));
+  cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(msd::PassSmem<msd::kItems, true, true>));
+  cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(msd::PassSmem<msd::kItems, true, false>));
+  cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(msd::PassSmem<msd::kItems, true, false>));
   cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItemsK, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(msd::PassSmem<msd::kItemsK, false, false>));
   cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItemsK, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(msd::PassSmem<msd::kItemsK, false, false>));
-  cudaFuncSetAttribute(msd::local_sort_kernel<true, !kPack>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(msd::LocalSmem<true, !kPack>));
+  cudaFuncSetAttribute(msd::local_sort_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(msd::LocalSmem<true, true>));
+  cudaFuncSetAttribute(msd::local_sort_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(msd::LocalSmem<true, false>));
   cudaFuncSetAttribute(msd::local_sort_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(msd::LocalSmem<false, false>));
   cudaFuncSetAttribute(dd::dd_tile_kernel<kDDRows, dd::kModeCount>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(dd::Smem<kDDRows>));
@@ -664,7 +675,9 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
     const int o = p & 1, q = (p - 1) & 1;
     // PAY: packed 16-byte records (key + id | upper-key delta << 32, msd.cuh
     // TileRegs) unless DDM_MSD_PACK=0 (20-byte key + upper key + id)
-    const double bytes = (double)n * (PAY ? (p == 0 ? 16.0 + kPayRec : 2.0 * kPayRec) : 16.0);
+    const bool pk = pack_records(n);
+    const double rec = pk ? 16.0 : 20.0;
+    const double bytes = (double)n * (PAY ? (p == 0 ? 16.0 + rec : 2.0 * rec) : 16.0);
 #define DDM_MSD_PASS(ITEMS, V64, V32, F64, NAME, KI, VI, II)                                                       \
   DDM_LAUNCH(NAME, bytes, st,                                                                                     \
              (msd::msd_pass_kernel<ITEMS, V64, V32, F64>                                                           \
@@ -674,10 +687,12 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
                   KI, VI, II, bk[o], V64 ? bv[o] : nullptr, V32 ? bi[o] : nullptr, n, M, bits, 8 * p,              \
                   s.starts + p * 256, s.status, s.counters + p, err)))
     if (p == 0) {
-      if (PAY) DDM_MSD_PASS(msd::kItems, true, !kPack, true, "msd_pass_pay", src, v64_src, nullptr);
+      if (PAY && pk) DDM_MSD_PASS(msd::kItems, true, false, true, "msd_pass_pay", src, v64_src, nullptr);
+      else if (PAY) DDM_MSD_PASS(msd::kItems, true, true, true, "msd_pass_pay", src, v64_src, nullptr);
       else DDM_MSD_PASS(msd::kItemsK, false, false, true, "msd_pass", src, nullptr, nullptr);
     } else {
-      if (PAY) DDM_MSD_PASS(msd::kItems, true, !kPack, false, "msd_pass_pay", bk[q], bv[q], kPack ? nullptr : bi[q]);
+      if (PAY && pk) DDM_MSD_PASS(msd::kItems, true, false, false, "msd_pass_pay", bk[q], bv[q], nullptr);
+      else if (PAY) DDM_MSD_PASS(msd::kItems, true, true, false, "msd_pass_pay", bk[q], bv[q], bi[q]);
       else DDM_MSD_PASS(msd::kItemsK, false, false, false, "msd_pass", bk[q], nullptr, nullptr);
     }
 #undef DDM_MSD_PASS
@@ -686,11 +701,14 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
   const int l = (passes - 1) & 1;
   DDM_LAUNCH("msd_bounds", 0, st, msd::span_bounds_kernel<<<(spans + 8) / 8, 256, 0, st>>>(bk[l], n, M, bits, spans, s.bounds));
   DDM_TRY(check_launch());
-  if (PAY)
-    DDM_LAUNCH("msd_local_pay", (kPayRec + 20.0) * n, st, msd::local_sort_kernel<true, !kPack>
-               <<<spans, msd::kThreads, sizeof(msd::LocalSmem<true, !kPack>), st>>>(
-                   bk[l], bv[l], kPack ? nullptr : bi[l], out_key, out_v64, out_v32, n, M, bits, s.bounds, overflow,
-                   v64_src));
+  if (PAY && pack_records(n))
+    DDM_LAUNCH("msd_local_pay", 36.0 * n, st, msd::local_sort_kernel<true, false>
+               <<<spans, msd::kThreads, sizeof(msd::LocalSmem<true, false>), st>>>(
+                   bk[l], bv[l], nullptr, out_key, out_v64, out_v32, n, M, bits, s.bounds, overflow, v64_src));
+  else if (PAY)
+    DDM_LAUNCH("msd_local_pay", 40.0 * n, st, msd::local_sort_kernel<true, true>
+               <<<spans, msd::kThreads, sizeof(msd::LocalSmem<true, true>), st>>>(
+                   bk[l], bv[l], bi[l], out_key, out_v64, out_v32, n, M, bits, s.bounds, overflow, nullptr));
   else
     DDM_LAUNCH("msd_local", 16.0 * n, st, msd::local_sort_kernel<false, false>
                <<<spans, msd::kThreads, sizeof(msd::LocalSmem<false, false>), st>>>(

@@ -897,6 +897,31 @@ def test_msd_overflow_falls_back_to_lsb(orc):
         check_against(orc, ul2, uh2, lo2, hi2, flags=(0,), ref=orc.sbm_seq(ul2, uh2, lo2, hi2))
 
 
+def test_packed_records_with_unfit_deltas(orc):
+    """Sorts of >= 2^22 records carry 16-byte packed records (id | upper-key
+    delta << 32); an upper key whose delta from the lower key needs more than
+    32 bits (long intervals, small magnitudes) is re-read from the input.  Half
+    the subscriptions and updates here take that path: the pair count equals
+    the oracle's rank identity, every pair overlaps, none repeats, and the list
+    equals the (unpacked) LSB path's."""
+    rng = np.random.default_rng(61)
+    n = m = 4_300_000
+    sl = rng.uniform(0.0, 1e6, n)
+    ul = rng.uniform(0.0, 1e6, m)
+    sh = sl + np.where(rng.random(n) < 0.5, 1e-3, 1.0)     # 1.0 at ~5e5: delta > 2^32 key units
+    uh = ul + np.where(rng.random(m) < 0.5, 1e-3, 1.0)
+    g = [cuda(x[None]) for x in (sl, sh, ul, uh)]
+    p = ddm.match_pairs(*g)
+    K = p.shape[0]
+    assert K == orc.rank_count(sl[None], sh[None], ul[None], uh[None]) and K > 100_000
+    s_, u_ = p[:, 0].long(), p[:, 1].long()
+    assert bool(((g[0][0][s_] <= g[3][0][u_]) & (g[2][0][u_] <= g[1][0][s_])).all())
+    wds = torch.sort((u_ << 32) | s_).values
+    assert bool((wds[1:] > wds[:-1]).all())
+    q = ddm.match_pairs(*g, flags=ddm.DDM_SORT_LSB)
+    assert torch.equal(p, q)  # same rows, same order: the packing changes no byte
+
+
 @pytest.mark.parametrize("n", [1, 700, 769, 5000, 70_000, 300_000])
 def test_msd_sizes(orc, n):
     """Bucket-bit choices from 1 to ~9 bits, ragged spans and tails."""
