@@ -153,6 +153,9 @@ inline ddm_status check_launch() {
 constexpr uint64_t kPackMinN = 1ull << 22;
 inline bool pack_records(uint64_t n) { return DDM_MSD_PACK == 2 ? n >= kPackMinN : DDM_MSD_PACK != 0; }
 
+#ifndef DDM_LS_BIG
+#define DDM_LS_BIG 1
+#endif
 constexpr int kSMs = 148;
 #ifndef DDM_DD_ROWS
 #define DDM_DD_ROWS 4
@@ -235,12 +238,20 @@ MaxTree tree_of(const Index& I) {
 // ------------------------------------------------------------ sort scratch
 
 // bucket bits of the MSD sort: ~768 records per bucket on average
-int msd_bits(uint64_t n) {
-  if (n <= 768) return 1;
-  const double b = std::log2((double)n / 768.0);
+int bits_for_bucket(uint64_t n, double per_bucket) {
+  if (n <= per_bucket) return 1;
+  const double b = std::log2((double)n / per_bucket);
   int r = (int)std::lround(b);
   return r < 1 ? 1 : r > 24 ? 24 : r;
 }
+// The big local sort (msd::LsBig, ~6000 records per bucket) is used when it
+// saves a multisplit pass over the default (~768 per bucket): c5's 5e8
+// records need 19 bucket bits (3 passes) with small buckets, 16 (2) with big.
+bool msd_big(uint64_t n) {
+  const int small = bits_for_bucket(n, 768.0), big = bits_for_bucket(n, 6000.0);
+  return DDM_LS_BIG && (big + 7) / 8 < (small + 7) / 8;
+}
+int msd_bits(uint64_t n) { return bits_for_bucket(n, msd_big(n) ? 6000.0 : 768.0); }
 
 
 // LSB onesweep scratch (the fallback path and the exported primitives).  The
@@ -498,12 +509,16 @@ void init_attrs_once() {
                        (int)sizeof(msd::PassSmem<msd::kItemsK, false, false>));
   cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItemsK, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(msd::PassSmem<msd::kItemsK, false, false>));
-  cudaFuncSetAttribute(msd::local_sort_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(msd::LocalSmem<true, true>));
-  cudaFuncSetAttribute(msd::local_sort_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(msd::LocalSmem<true, false>));
-  cudaFuncSetAttribute(msd::local_sort_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(msd::LocalSmem<false, false>));
+#define DDM_LOCAL_ATTR(C, V64, V32)                                                                  \
+  cudaFuncSetAttribute(msd::local_sort_kernel<C, V64, V32>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                       (int)sizeof(msd::LocalSmem<C, V64, V32>))
+  DDM_LOCAL_ATTR(msd::LsSmall, true, true);
+  DDM_LOCAL_ATTR(msd::LsSmall, true, false);
+  DDM_LOCAL_ATTR(msd::LsSmall, false, false);
+  DDM_LOCAL_ATTR(msd::LsBig, true, true);
+  DDM_LOCAL_ATTR(msd::LsBig, true, false);
+  DDM_LOCAL_ATTR(msd::LsBig, false, false);
+#undef DDM_LOCAL_ATTR
   cudaFuncSetAttribute(dd::dd_tile_kernel<kDDRows, dd::kModeCount>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(dd::Smem<kDDRows>));
   cudaFuncSetAttribute(dd::dd_tile_kernel<kDDRows, dd::kModeStage>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(dd::Smem<kDDRows>));
   cudaFuncSetAttribute(dd::dd_tile_kernel<kDDRows, dd::kModePlace>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(dd::Smem<kDDRows>));
@@ -663,7 +678,9 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
   DDM_TRY(check_launch());
   }
   if (!(stage & kMsdRun)) return DDM_OK;
-  const uint32_t spans = (uint32_t)((n + msd::kSpan - 1) / msd::kSpan);
+  const bool big = msd_big(n);
+  const uint32_t span = big ? msd::LsBig::SPAN : msd::LsSmall::SPAN;
+  const uint32_t spans = (uint32_t)((n + span - 1) / span);
   (void)nb;
   uint64_t* bk[2] = {s.k[0], s.k[1]};
   uint64_t* bv[2] = {s.v64[0], s.v64[1]};
@@ -699,20 +716,25 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
     DDM_TRY(check_launch());
   }
   const int l = (passes - 1) & 1;
-  DDM_LAUNCH("msd_bounds", 0, st, msd::span_bounds_kernel<<<(spans + 8) / 8, 256, 0, st>>>(bk[l], n, M, bits, spans, s.bounds));
+  DDM_LAUNCH("msd_bounds", 0, st, msd::span_bounds_kernel<<<(spans + 8) / 8, 256, 0, st>>>(bk[l], n, M, bits, spans,
+                                                                                         span, s.bounds));
   DDM_TRY(check_launch());
-  if (PAY && pack_records(n))
-    DDM_LAUNCH("msd_local_pay", 36.0 * n, st, msd::local_sort_kernel<true, false>
-               <<<spans, msd::kThreads, sizeof(msd::LocalSmem<true, false>), st>>>(
-                   bk[l], bv[l], nullptr, out_key, out_v64, out_v32, n, M, bits, s.bounds, overflow, v64_src));
-  else if (PAY)
-    DDM_LAUNCH("msd_local_pay", 40.0 * n, st, msd::local_sort_kernel<true, true>
-               <<<spans, msd::kThreads, sizeof(msd::LocalSmem<true, true>), st>>>(
-                   bk[l], bv[l], bi[l], out_key, out_v64, out_v32, n, M, bits, s.bounds, overflow, nullptr));
-  else
-    DDM_LAUNCH("msd_local", 16.0 * n, st, msd::local_sort_kernel<false, false>
-               <<<spans, msd::kThreads, sizeof(msd::LocalSmem<false, false>), st>>>(
-                   bk[l], nullptr, nullptr, out_key, nullptr, nullptr, n, M, bits, s.bounds, overflow, nullptr));
+#define DDM_LOCAL(C, V64, V32, NAME, BYTES, VI, II, HI)                                                         \
+  DDM_LAUNCH(NAME, BYTES, st,                                                                                  \
+             (msd::local_sort_kernel<C, V64, V32><<<spans, C::T, sizeof(msd::LocalSmem<C, V64, V32>), st>>>(   \
+                 bk[l], VI, II, out_key, V64 ? out_v64 : nullptr, V32 || V64 ? out_v32 : nullptr, n, M, bits,    \
+                 s.bounds, overflow, HI)))
+  if (PAY && pack_records(n)) {
+    if (big) DDM_LOCAL(msd::LsBig, true, false, "msd_local_pay", 36.0 * n, bv[l], nullptr, v64_src);
+    else DDM_LOCAL(msd::LsSmall, true, false, "msd_local_pay", 36.0 * n, bv[l], nullptr, v64_src);
+  } else if (PAY) {
+    if (big) DDM_LOCAL(msd::LsBig, true, true, "msd_local_pay", 40.0 * n, bv[l], bi[l], nullptr);
+    else DDM_LOCAL(msd::LsSmall, true, true, "msd_local_pay", 40.0 * n, bv[l], bi[l], nullptr);
+  } else {
+    if (big) DDM_LOCAL(msd::LsBig, false, false, "msd_local", 16.0 * n, nullptr, nullptr, nullptr);
+    else DDM_LOCAL(msd::LsSmall, false, false, "msd_local", 16.0 * n, nullptr, nullptr, nullptr);
+  }
+#undef DDM_LOCAL
   return check_launch();
 }
 

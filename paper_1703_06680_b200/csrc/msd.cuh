@@ -43,6 +43,9 @@ constexpr int kCapPow2 = 4096;   // bitonic network size bound (next power of tw
 #define DDM_LS_BINBITS 11
 #endif
 constexpr int kFineBinBits = DDM_LS_BINBITS;
+#ifndef DDM_LS_MINB
+#define DDM_LS_MINB 6
+#endif
 constexpr int kFineBins = 1 << kFineBinBits;  // value bins of the in-smem counting sort
 constexpr int kMaxBinRun = 64;   // larger bins (ties, clusters) -> bitonic sort of the group
 // Order inside a fine bin: DDM_LS_RANK 1 (default) ranks every record among
@@ -555,26 +558,38 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
 
 // ---------------------------------------------------------------- local sort
 
-template <bool V64, bool V32>
+// Local-sort configurations: the default, and a big one (a whole SM: 1024
+// threads, groups of up to 16384 records, 2^13 fine bins) for sorts whose
+// small-bucket map would need one more multisplit pass (c5: 19 bucket bits ->
+// 3 passes; with ~8x larger buckets 16 bits -> 2 passes).
+struct LsSmall {
+  static constexpr int T = kThreads, CAP = kCap, CAP2 = kCapPow2, BIN_BITS = kFineBinBits,
+                       BINS = 1 << kFineBinBits, SPAN = kSpan, MINB = DDM_LS_MINB;
+};
+struct LsBig {
+  static constexpr int T = 1024, CAP = 16384, CAP2 = 16384, BIN_BITS = 13, BINS = 1 << 13, SPAN = 8192, MINB = 1;
+};
+
+template <class C, bool V64, bool V32>
 struct LocalSmem {  // keys only: payloads follow the permutation through the key buffer
-  alignas(16) uint64_t keys[kCap + 2];  // +2: bulk copies start at a 16-byte aligned index
+  alignas(16) uint64_t keys[C::CAP + 2];  // +2: bulk copies start at a 16-byte aligned index
   uint64_t bar;                         // mbarrier of the bulk copies
-  // fine-bin counts / offsets, two 16-bit fields per word (values <= kCap),
+  // fine-bin counts / offsets, two 16-bit fields per word (values <= C::CAP),
   // followed by perm (sorted position -> staged index); the bitonic fallback
-  // uses both as one u16[kCapPow2] array (the bins are dead by then)
-  uint32_t binw[kFineBins / 2 + 2];
-  uint16_t perm[kCap];
-  static_assert(sizeof(uint32_t) * (kFineBins / 2 + 2) + sizeof(uint16_t) * kCap >= sizeof(uint16_t) * kCapPow2,
-                "the bitonic fallback's u16[kCapPow2] fits in binw + perm");
+  // uses both as one u16[C::CAP2] array (the bins are dead by then)
+  uint32_t binw[C::BINS / 2 + 2];
+  uint16_t perm[C::CAP];
+  static_assert(sizeof(uint32_t) * (C::BINS / 2 + 2) + sizeof(uint16_t) * C::CAP >= sizeof(uint16_t) * C::CAP2,
+                "the bitonic fallback's u16[C::CAP2] fits in binw + perm");
 #if DDM_LS_RANK
-  uint16_t perm2[kCap];  // final order (sorted position -> staged index)
+  uint16_t perm2[C::CAP];  // final order (sorted position -> staged index)
 #endif
-  uint64_t red[2 * kWarps];
+  uint64_t red[2 * (C::T / 32)];
   uint32_t flag;
   uint64_t bound[1];  // prev_boundary's reduction slot
 };
 
-// Stable sort of records [e0, e0 + c) by key inside shared memory (c <= kCap).
+// Stable sort of records [e0, e0 + c) by key inside shared memory (c <= C::CAP).
 // Records arrive in (bucket, original-order) order.  Counting sort over fine
 // bins of the key range of this group (integer, monotone): every record goes
 // to its bin's next slot of perm, then each bin holding two or more records
@@ -589,8 +604,8 @@ __device__ __forceinline__ uint32_t bin_add(uint32_t* w, uint32_t b) {  // retur
   return (atomicAdd(w + (b >> 1), (b & 1) ? 0x10000u : 1u) >> ((b & 1) * 16)) & 0xffffu;
 }
 
-template <bool V64, bool V32>
-__device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restrict__ k_in,
+template <class C, bool V64, bool V32>
+__device__ void local_sort_group(LocalSmem<C, V64, V32>& S, const uint64_t* __restrict__ k_in,
                                  const uint64_t* __restrict__ v64_in, const uint32_t* __restrict__ v32_in,
                                  uint64_t* __restrict__ k_out, uint64_t* __restrict__ v64_out,
                                  uint32_t* __restrict__ v32_out, uint64_t e0, uint32_t c, uint32_t& phase,
@@ -609,12 +624,12 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
   mbar_wait(&S.bar, phase);
   phase ^= 1;
   uint64_t kmin = ~0ull, kmax = 0;
-  for (uint32_t i = tid; i < c; i += kThreads) {
+  for (uint32_t i = tid; i < c; i += C::T) {
     const uint64_t k = K[i];
     kmin = k < kmin ? k : kmin;
     kmax = k > kmax ? k : kmax;
   }
-  for (uint32_t b = tid; b < kFineBins / 2 + 2; b += kThreads) S.binw[b] = 0;
+  for (uint32_t b = tid; b < C::BINS / 2 + 2; b += C::T) S.binw[b] = 0;
   if (tid == 0) S.flag = 0;
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -622,22 +637,22 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
     kmin = x < kmin ? x : kmin;
     kmax = y > kmax ? y : kmax;
   }
-  if (lane == 0) { S.red[warp] = kmin; S.red[kWarps + warp] = kmax; }
+  if (lane == 0) { S.red[warp] = kmin; S.red[(C::T / 32) + warp] = kmax; }
   __syncthreads();
   kmin = ~0ull;
   kmax = 0;
 #pragma unroll
-  for (int w = 0; w < kWarps; ++w) {
+  for (int w = 0; w < (C::T / 32); ++w) {
     kmin = S.red[w] < kmin ? S.red[w] : kmin;
-    kmax = S.red[kWarps + w] > kmax ? S.red[kWarps + w] : kmax;
+    kmax = S.red[(C::T / 32) + w] > kmax ? S.red[(C::T / 32) + w] : kmax;
   }
-  // smallest shift with (kmax - kmin) >> sh < kFineBins
+  // smallest shift with (kmax - kmin) >> sh < C::BINS
   const uint64_t range = kmax - kmin;
-  const int sh = range ? max(0, 64 - __clzll((long long)range) - kFineBinBits) : 0;
-  for (uint32_t i = tid; i < c; i += kThreads) bin_add(S.binw, (uint32_t)((K[i] - kmin) >> sh));
+  const int sh = range ? max(0, 64 - __clzll((long long)range) - C::BIN_BITS) : 0;
+  for (uint32_t i = tid; i < c; i += C::T) bin_add(S.binw, (uint32_t)((K[i] - kmin) >> sh));
   __syncthreads();
   {  // exclusive scan over the bins (8 per thread, 4 words) + large-bin detection
-    constexpr int kPer = kFineBins / kThreads;
+    constexpr int kPer = C::BINS / C::T;
     static_assert(kPer % 2 == 0, "whole words per thread");
     uint32_t v[kPer], sum = 0;
 #pragma unroll
@@ -651,9 +666,9 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
       sum += v[q];
       if (v[q] > kMaxBinRun) S.flag = 1;
     }
-    __shared__ uint32_t tmp[kWarps + 1];
+    __shared__ uint32_t tmp[(C::T / 32) + 1];
     uint32_t tot;
-    uint32_t ex = block_excl_scan<kThreads>(sum, tmp, &tot);
+    uint32_t ex = block_excl_scan<C::T>(sum, tmp, &tot);
 #pragma unroll
     for (int q = 0; q < kPer; q += 2) {
       const uint32_t e0v = ex, e1v = ex + v[q];
@@ -665,7 +680,7 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
   if (S.flag == 0) {
     // place every record at its bin's next slot, straight into perm (any
     // order inside a bin; most bins hold zero or one record) ...
-    for (uint32_t i = tid; i < c; i += kThreads) {
+    for (uint32_t i = tid; i < c; i += C::T) {
       const uint32_t pos = bin_add(S.binw, (uint32_t)((K[i] - kmin) >> sh));
       S.perm[pos] = (uint16_t)i;
     }
@@ -676,7 +691,7 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
     // the work is spread evenly (most bins hold one record; an insertion sort
     // per bin left a warp waiting on its longest bin); bin b spans
     // [end(b-1), end(b)), <= kMaxBinRun
-    for (uint32_t x = tid; x < c; x += kThreads) {
+    for (uint32_t x = tid; x < c; x += C::T) {
       const uint16_t v = S.perm[x];
       const uint64_t kv = K[v];
       const uint32_t b = (uint32_t)((kv - kmin) >> sh);
@@ -694,7 +709,7 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
 #else
     // ... then order each bin holding two or more records by (key, staged
     // index) with an insertion sort; bin b spans [end(b-1), end(b)), <= kMaxBinRun
-    for (uint32_t b = tid; b < kFineBins; b += kThreads) {
+    for (uint32_t b = tid; b < C::BINS; b += C::T) {
       const uint32_t lo = b ? bin_get(S.binw, b - 1) : 0, hi = bin_get(S.binw, b);
       if (hi - lo < 2) continue;
       for (uint32_t x = lo + 1; x < hi; ++x) {
@@ -719,11 +734,11 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
     uint16_t* PB = reinterpret_cast<uint16_t*>(S.binw);
     uint32_t P = 1;
     while (P < c) P <<= 1;
-    for (uint32_t i = tid; i < P; i += kThreads) PB[i] = (uint16_t)(i < c ? i : 0xffff);
+    for (uint32_t i = tid; i < P; i += C::T) PB[i] = (uint16_t)(i < c ? i : 0xffff);
     __syncthreads();
     for (uint32_t k = 2; k <= P; k <<= 1) {
       for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-        for (uint32_t i = tid; i < P; i += kThreads) {
+        for (uint32_t i = tid; i < P; i += C::T) {
           const uint32_t l = i ^ j;
           if (l > i) {
             const uint16_t a = PB[i], b = PB[l];
@@ -748,11 +763,11 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
     // PACKED records: sorted keys out (kept in registers), then the payload
     // (id | upper-key delta << 32) staged through the key buffer, unpacked into
     // the upper key and the id
-    constexpr int kPer = (kCap + kThreads - 1) / kThreads;
+    constexpr int kPer = (C::CAP + C::T - 1) / C::T;
     uint64_t kr[kPer];
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
-      const uint32_t i = tid + j * kThreads;
+      const uint32_t i = tid + j * C::T;
       if (i < c) {
         kr[j] = K[PERM[i]];
         k_out[e0 + i] = kr[j];
@@ -768,7 +783,7 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
     phase ^= 1;
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
-      const uint32_t i = tid + j * kThreads;
+      const uint32_t i = tid + j * C::T;
       if (i < c) {
         const uint64_t P = K[PERM[i]];
         const uint32_t id = (uint32_t)P;
@@ -780,7 +795,7 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
     __syncthreads();
     return;
   }
-  for (uint32_t i = tid; i < c; i += kThreads) k_out[e0 + i] = K[PERM[i]];
+  for (uint32_t i = tid; i < c; i += C::T) k_out[e0 + i] = K[PERM[i]];
   // payloads: staged coalesced through the key buffer (free now), then read
   // back in permutation order -- random global gathers would cost one L1
   // request per element
@@ -793,7 +808,7 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
     }
     mbar_wait(&S.bar, phase);
     phase ^= 1;
-    for (uint32_t i = tid; i < c; i += kThreads) v64_out[e0 + i] = K[PERM[i]];
+    for (uint32_t i = tid; i < c; i += C::T) v64_out[e0 + i] = K[PERM[i]];
   }
   if (V32) {
     const uint32_t vo = (uint32_t)(e0 & 3);
@@ -806,18 +821,19 @@ __device__ void local_sort_group(LocalSmem<V64, V32>& S, const uint64_t* __restr
     }
     mbar_wait(&S.bar, phase);
     phase ^= 1;
-    for (uint32_t i = tid; i < c; i += kThreads) v32_out[e0 + i] = b32[PERM[i]];
+    for (uint32_t i = tid; i < c; i += C::T) v32_out[e0 + i] = b32[PERM[i]];
   }
   __syncthreads();
 }
 
 // Last bucket boundary in (lo, hi] scanning backwards; lo if none.
+template <class C>
 __device__ __forceinline__ uint64_t prev_boundary(const uint64_t* __restrict__ keys, uint64_t lo, uint64_t hi,
                                                   const Bucketer& BK, uint64_t* slot) {
   const int tid = threadIdx.x;
   if (tid == 0) *slot = 0;
   __syncthreads();
-  for (int64_t top = (int64_t)hi; top > (int64_t)lo; top -= kThreads) {
+  for (int64_t top = (int64_t)hi; top > (int64_t)lo; top -= C::T) {
     const int64_t q = top - tid;
     const bool edge = q > (int64_t)lo && BK(keys[q]) != BK(keys[q - 1]);
     if (edge) atomicMax((unsigned long long*)slot, (unsigned long long)q);
@@ -829,19 +845,19 @@ __device__ __forceinline__ uint64_t prev_boundary(const uint64_t* __restrict__ k
   return lo;
 }
 
-// bounds[s] = first bucket boundary at or after s*kSpan (s = 0..spans; n past
+// bounds[s] = first bucket boundary at or after s*span (s = 0..spans; n past
 // the end), one warp per span over the bucket-grouped keys: each boundary is
 // found once, off the local sort's critical path.  Lane l tests positions
 // base + 4l .. base + 4l + 3 against their predecessors (128 per step).
 __global__ void __launch_bounds__(256) span_bounds_kernel(const uint64_t* __restrict__ keys, uint64_t n,
-                                                          MapRef M, int bits, uint32_t spans,
+                                                          MapRef M, int bits, uint32_t spans, uint32_t span,
                                                           uint64_t* __restrict__ bounds) {
   Bucketer BK;
   BK.init(M, bits);
   const int lane = threadIdx.x & 31;
   const uint32_t sp = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (sp > spans) return;
-  const uint64_t p = (uint64_t)sp * kSpan;
+  const uint64_t p = (uint64_t)sp * span;
   if (sp == 0 || p >= n) {
     if (lane == 0) bounds[sp] = sp == 0 ? 0 : n;
     return;
@@ -869,15 +885,12 @@ __global__ void __launch_bounds__(256) span_bounds_kernel(const uint64_t* __rest
   if (lane == 0) bounds[sp] = n;
 }
 
-// CTA c sorts the whole buckets starting in [c*kSpan, (c+1)*kSpan), i.e. in
+// CTA c sorts the whole buckets starting in [c*C::SPAN, (c+1)*C::SPAN), i.e. in
 // [bounds[c], bounds[c+1]) (span_bounds_kernel), in groups of consecutive
-// buckets holding <= kCap records in smem.  A
-// single bucket larger than kCap sets *overflow (caller redoes with LSB).
-template <bool V64, bool V32>
-#ifndef DDM_LS_MINB
-#define DDM_LS_MINB 6
-#endif
-__global__ void __launch_bounds__(kThreads, DDM_LS_MINB) local_sort_kernel(const uint64_t* __restrict__ k_in,
+// buckets holding <= C::CAP records in smem.  A
+// single bucket larger than C::CAP sets *overflow (caller redoes with LSB).
+template <class C, bool V64, bool V32>
+__global__ void __launch_bounds__(C::T, C::MINB) local_sort_kernel(const uint64_t* __restrict__ k_in,
                                                               const uint64_t* __restrict__ v64_in,
                                                               const uint32_t* __restrict__ v32_in,
                                                               uint64_t* __restrict__ k_out,
@@ -888,7 +901,7 @@ __global__ void __launch_bounds__(kThreads, DDM_LS_MINB) local_sort_kernel(const
                                                               uint32_t* __restrict__ overflow,
                                                               const double* __restrict__ hi_src) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  LocalSmem<V64, V32>& S = *reinterpret_cast<LocalSmem<V64, V32>*>(smem_raw);
+  LocalSmem<C, V64, V32>& S = *reinterpret_cast<LocalSmem<C, V64, V32>*>(smem_raw);
   Bucketer BK;
   BK.init(M, bits);
   if (threadIdx.x == 0) mbar_init(&S.bar, 1);
@@ -898,14 +911,14 @@ __global__ void __launch_bounds__(kThreads, DDM_LS_MINB) local_sort_kernel(const
   __syncthreads();  // publishes the mbarrier init
   while (e0 < e1) {
     uint64_t g1 = e1;
-    if (e1 - e0 > kCap) {
-      g1 = prev_boundary(k_in, e0, e0 + kCap, BK, &S.bound[0]);
+    if (e1 - e0 > C::CAP) {
+      g1 = prev_boundary<C>(k_in, e0, e0 + C::CAP, BK, &S.bound[0]);
       if (g1 == e0) {  // one bucket alone exceeds the capacity
         if (threadIdx.x == 0) atomicOr(overflow, 1u);
         return;
       }
     }
-    local_sort_group<V64, V32>(S, k_in, v64_in, v32_in, k_out, v64_out, v32_out, e0, (uint32_t)(g1 - e0), phase,
+    local_sort_group<C, V64, V32>(S, k_in, v64_in, v32_in, k_out, v64_out, v32_out, e0, (uint32_t)(g1 - e0), phase,
                                hi_src);
     e0 = g1;
   }

@@ -922,6 +922,30 @@ def test_packed_records_with_unfit_deltas(orc):
     assert torch.equal(p, q)  # same rows, same order: the packing changes no byte
 
 
+def test_big_local_sort_range(orc):
+    """7.5e7 subscriptions: with ~768 records per bucket the MSD sort would
+    need 17 bucket bits (3 multisplit passes); the big local sort (groups of up
+    to 16384 records per SM) takes ~6000 per bucket, 14 bits, 2 passes.  K
+    equals the oracle's rank identity; the list is valid, unique, and equal to
+    the LSB path's."""
+    rng = np.random.default_rng(62)
+    n, m = 75_000_000, 1_000_000
+    sl = rng.uniform(0.0, 1e8, n)
+    ul = rng.uniform(0.0, 1e8, m)
+    sh, uh = sl + 1.5, ul + 1.5
+    g = [cuda(x[None]) for x in (sl, sh, ul, uh)]
+    p = ddm.match_pairs(*g)
+    K = p.shape[0]
+    assert K == orc.rank_count(sl[None], sh[None], ul[None], uh[None]) and K > 1_000_000
+    s_, u_ = p[:, 0].long(), p[:, 1].long()
+    assert bool(((g[0][0][s_] <= g[3][0][u_]) & (g[2][0][u_] <= g[1][0][s_])).all())
+    wds = torch.sort((u_ << 32) | s_).values
+    assert bool((wds[1:] > wds[:-1]).all())
+    del s_, u_, wds
+    q = ddm.match_pairs(*g, flags=ddm.DDM_SORT_LSB)
+    assert torch.equal(p, q)
+
+
 @pytest.mark.parametrize("n", [1, 700, 769, 5000, 70_000, 300_000])
 def test_msd_sizes(orc, n):
     """Bucket-bit choices from 1 to ~9 bits, ragged spans and tails."""
