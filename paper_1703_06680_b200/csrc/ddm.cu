@@ -716,8 +716,8 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
     DDM_TRY(check_launch());
   }
   const int l = (passes - 1) & 1;
-  DDM_LAUNCH("msd_bounds", 0, st, msd::span_bounds_kernel<<<(spans + 8) / 8, 256, 0, st>>>(bk[l], n, M, bits, spans,
-                                                                                         span, s.bounds));
+  DDM_LAUNCH("msd_bounds", 0, st, msd::span_bounds_kernel<<<(spans + 256) / 256, 256, 0, st>>>(bk[l], n, M, bits, spans,
+                                                                                             span, s.bounds));
   DDM_TRY(check_launch());
 #define DDM_LOCAL(C, V64, V32, NAME, BYTES, VI, II, HI)                                                         \
   DDM_LAUNCH(NAME, BYTES, st,                                                                                  \

@@ -44,7 +44,7 @@ constexpr int kCapPow2 = 4096;   // bitonic network size bound (next power of tw
 #endif
 constexpr int kFineBinBits = DDM_LS_BINBITS;
 #ifndef DDM_LS_MINB
-#define DDM_LS_MINB 6
+#define DDM_LS_MINB 5
 #endif
 constexpr int kFineBins = 1 << kFineBinBits;  // value bins of the in-smem counting sort
 constexpr int kMaxBinRun = 64;   // larger bins (ties, clusters) -> bitonic sort of the group
@@ -846,43 +846,40 @@ __device__ __forceinline__ uint64_t prev_boundary(const uint64_t* __restrict__ k
 }
 
 // bounds[s] = first bucket boundary at or after s*span (s = 0..spans; n past
-// the end), one warp per span over the bucket-grouped keys: each boundary is
-// found once, off the local sort's critical path.  Lane l tests positions
-// base + 4l .. base + 4l + 3 against their predecessors (128 per step).
+// the end): one thread per span.  The records are grouped by bucket in
+// increasing bucket order, so the bucket id is non-decreasing along the
+// positions and the boundary is an upper bound of the bucket of position
+// s*span - 1: a gallop forward from s*span, then a binary search of the last
+// step (O(log distance) dependent loads; the span of the big local sort is
+// 8192 records with ~6000-record buckets, which a linear scan paid for).
 __global__ void __launch_bounds__(256) span_bounds_kernel(const uint64_t* __restrict__ keys, uint64_t n,
                                                           MapRef M, int bits, uint32_t spans, uint32_t span,
                                                           uint64_t* __restrict__ bounds) {
   Bucketer BK;
   BK.init(M, bits);
-  const int lane = threadIdx.x & 31;
-  const uint32_t sp = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const uint32_t sp = blockIdx.x * blockDim.x + threadIdx.x;
   if (sp > spans) return;
   const uint64_t p = (uint64_t)sp * span;
   if (sp == 0 || p >= n) {
-    if (lane == 0) bounds[sp] = sp == 0 ? 0 : n;
+    bounds[sp] = sp == 0 ? 0 : n;
     return;
   }
-  for (uint64_t base = p; base < n; base += 128) {
-    const uint64_t q0 = base + 4 * (uint64_t)lane;
-    uint32_t b[5];
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      const uint64_t q = q0 + k - 1;  // q0 - 1 .. q0 + 3
-      b[k] = q < n ? BK(__ldg(keys + q)) : ~0u;
-    }
-    unsigned first = 4;
-#pragma unroll
-    for (int k = 3; k >= 0; --k)
-      if (q0 + k < n && b[k + 1] != b[k]) first = k;
-    const unsigned any = __ballot_sync(kFull, first < 4);
-    if (any) {
-      const int l = __ffs(any) - 1;
-      const unsigned f = __shfl_sync(kFull, first, l);
-      if (lane == 0) bounds[sp] = base + 4 * (uint64_t)l + f;
-      return;
-    }
+  const uint32_t b0 = BK(__ldg(keys + p - 1));
+  // first q >= p with BK(keys[q]) > b0 (n if none)
+  uint64_t lo = p, hi = n, step = 1;
+  while (true) {
+    const uint64_t q = lo + step - 1;
+    if (q >= n) break;
+    if (BK(__ldg(keys + q)) > b0) { hi = q; break; }
+    lo = q + 1;
+    step <<= 1;
   }
-  if (lane == 0) bounds[sp] = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (BK(__ldg(keys + mid)) > b0) hi = mid;
+    else lo = mid + 1;
+  }
+  bounds[sp] = lo;
 }
 
 // CTA c sorts the whole buckets starting in [c*C::SPAN, (c+1)*C::SPAN), i.e. in
