@@ -115,11 +115,14 @@ typedef struct {
  * emission itself, and no Shi sort.  Default for ddm_match_pairs (d = 1,
  * n_sub >= 2^20): one small probe kernel estimates the mean stab size
  * n_sub * mean(hi - lo) / (max lo - min lo) over 4096 sampled subscriptions
- * (one extra 8-byte device->host read, on the first call with given
+ * (one extra 24-byte device->host read, on the first call with given
  * regions / workspace / flags / stream; repeated calls reuse the decision)
  * and picks the walk form when it is <= 4; otherwise, and for every indexed
  * match, the rank form.  These flags force one form.  Output is identical
- * either way. */
+ * either way.  The same probe (also run for count calls with a side of at
+ * least 2^22 regions) decides per side whether the sort packs its records to
+ * 16 bytes (upper key as a 32-bit delta from the lower key): not when more
+ * than 2 % of the sampled deltas need more bits -- a performance choice only. */
 #define DDM_COUNT_RANKS (1u << 13)
 #define DDM_COUNT_WALK (1u << 14)
 /* Sweep dimension (d > 1, ddm_match_pairs / ddm_match_count /

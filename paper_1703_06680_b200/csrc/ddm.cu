@@ -151,7 +151,22 @@ inline ddm_status check_launch() {
 #define DDM_MSD_PACK 2
 #endif
 constexpr uint64_t kPackMinN = 1ull << 22;
-inline bool pack_records(uint64_t n) { return DDM_MSD_PACK == 2 ? n >= kPackMinN : DDM_MSD_PACK != 0; }
+constexpr double kPackMaxUnfit = 0.02;  // no packing when more sampled deltas than this do not fit 32 bits
+// Per-call pack decision of the subscription / update sorts (match_full's
+// probe; -1: by size only), set for the duration of a call like OneChain.
+struct PackHint {
+  int sub = -1, upd = -1;
+};
+thread_local PackHint t_pack;
+struct PackScope {
+  PackHint prev;
+  PackScope(int s, int u) : prev(t_pack) { t_pack = PackHint{s, u}; }
+  ~PackScope() { t_pack = prev; }
+};
+inline bool pack_records(uint64_t n, int hint) {
+  if (DDM_MSD_PACK != 2) return DDM_MSD_PACK != 0;
+  return n >= kPackMinN && hint != 0;
+}
 
 #ifndef DDM_LS_BIG
 #define DDM_LS_BIG 1
@@ -653,7 +668,7 @@ enum : int { kMsdPrep = 1, kMsdRun = 2, kMsdAll = 3 };
 template <bool PAY>
 ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint64_t* mm, uint64_t* out_key,
                       uint64_t* out_v64, uint32_t* out_v32, MsdScratch& s, uint32_t* overflow, uint32_t* err,
-                      cudaStream_t st, int stage = kMsdAll) {
+                      cudaStream_t st, int stage = kMsdAll, int pack_hint = -1) {
   const int bits = msd_bits(n);
   const uint32_t nb = 1u << bits;
   const int passes = (bits + 7) / 8;
@@ -692,7 +707,7 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
     const int o = p & 1, q = (p - 1) & 1;
     // PAY: packed 16-byte records (key + id | upper-key delta << 32, msd.cuh
     // TileRegs) unless DDM_MSD_PACK=0 (20-byte key + upper key + id)
-    const bool pk = pack_records(n);
+    const bool pk = pack_records(n, pack_hint);
     const double rec = pk ? 16.0 : 20.0;
     const double bytes = (double)n * (PAY ? (p == 0 ? 16.0 + rec : 2.0 * rec) : 16.0);
 #define DDM_MSD_PASS(ITEMS, V64, V32, F64, NAME, KI, VI, II)                                                       \
@@ -724,7 +739,7 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
              (msd::local_sort_kernel<C, V64, V32><<<spans, C::T, sizeof(msd::LocalSmem<C, V64, V32>), st>>>(   \
                  bk[l], VI, II, out_key, V64 ? out_v64 : nullptr, V32 || V64 ? out_v32 : nullptr, n, M, bits,    \
                  s.bounds, overflow, HI)))
-  if (PAY && pack_records(n)) {
+  if (PAY && pack_records(n, pack_hint)) {
     if (big) DDM_LOCAL(msd::LsBig, true, false, "msd_local_pay", 36.0 * n, bv[l], nullptr, v64_src);
     else DDM_LOCAL(msd::LsSmall, true, false, "msd_local_pay", 36.0 * n, bv[l], nullptr, v64_src);
   } else if (PAY) {
@@ -842,7 +857,7 @@ ddm_status build_index_async(const ddm_regions* R, const Index& I, MsdScratch& s
     }
     // a2 + a3: Slo with the upper key and the id as payload
     DDM_TRY(msd_sort_t<true>(R->sub_lo[0], R->sub_hi[0], n, mm + 0, I.slo_key, I.slo_hi, I.slo_id, slo,
-                             &misc->overflow, &misc->err, st));
+                             &misc->overflow, &misc->err, st, kMsdAll, t_pack.sub));
     DDM_TRY(tree_async(I, need, false, st));
     if (with_shi) DDM_TRY(stream_join(st, side[0]));
   } else {
@@ -925,7 +940,7 @@ ddm_status upd_sort_async(const ddm_regions* R, MatchWs& W, uint64_t n_sub, bool
     if (stage & kMsdPrep)
       DDM_TRY(validate_side(d, m, R->upd_lo, R->upd_hi, nullptr, nullptr, &W.misc->err, st, nullptr, nullptr, 1));
     return msd_sort_t<true>(R->upd_lo[0], R->upd_hi[0], m, W.mm + 4, W.ulo_key, W.uhi, W.ulo_id, W.ulo,
-                            &W.misc->overflow, &W.misc->err, st, stage);
+                            &W.misc->overflow, &W.misc->err, st, stage, t_pack.upd);
   }
   if (!(stage & kMsdRun)) return DDM_OK;  // (the LSB path has no separate preparation)
   SortScratch s = lsb_with(W.sort, W.ulo);
@@ -1356,8 +1371,12 @@ size_t ddm_workspace_bytes(uint32_t d, uint64_t n_sub, uint64_t n_upd, int want_
   return a256(index_layout(d, n_sub, nullptr).bytes) + match_layout(d, n_sub, n_upd, nullptr, true).bytes;
 }
 
+struct Probe {
+  bool walk = false;
+  bool pack_s = true, pack_u = true;
+};
 std::mutex g_probe_mu;
-std::unordered_map<std::string, bool> g_probe;  // count-form decision per call site
+std::unordered_map<std::string, Probe> g_probe;  // count-form and packing decisions per call site
 
 // k* for d > 1: the dimension with the fewest estimated
 // candidate pairs (match::dim_probe_kernel), dimension 0 unless another one
@@ -1433,37 +1452,51 @@ static ddm_status match_full_dim(const ddm_regions* R, ddm_pair* pairs, uint64_t
   // (its dim-0 candidates outnumber the pairs); d = 1 pairs calls walk when
   // forced, or when the probe finds sparse stab sets on a big input (the
   // walk replaces the Shi sort, ~1/3 of the sort traffic)
-  bool walk = false;
-  if (pairs && R->d == 1 && !(flags & DDM_COUNT_RANKS)) {
-    if (flags & DDM_COUNT_WALK) walk = true;
-    else if (R->n_sub >= kWalkMinN && R->n_upd > 0) {
-      // the decision is kept per call site (regions, workspace, flags, stream):
-      // repeated calls -- graph replays -- skip the probe and its host read;
-      // both forms give the same output, so a stale decision costs time only
-      const std::string pk = graph_key(R, ws, ws_bytes, flags, true, sub_map, upd_map, st);
-      bool known = false;
-      {
-        std::lock_guard<std::mutex> lk(g_probe_mu);
-        const auto it = g_probe.find(pk);
-        if (it != g_probe.end()) {
-          walk = it->second;
-          known = true;
-        }
-      }
-      if (!known) {
-        double est = INFINITY;
-        DDM_LAUNCH("stab_probe", 0, st, match::stab_density_kernel<<<1, 256, 0, st>>>(R->sub_lo[0], R->sub_hi[0],
-                                                                                     R->n_sub, W.probe));
-        DDM_TRY(check_launch());
-        DDM_CUDA(cudaMemcpyAsync(&est, W.probe, sizeof(double), cudaMemcpyDeviceToHost, st));
-        DDM_CUDA(cudaStreamSynchronize(st));
-        walk = est <= kWalkMaxStab;
-        std::lock_guard<std::mutex> lk(g_probe_mu);
-        if (g_probe.size() > 4096) g_probe.clear();
-        g_probe[pk] = walk;
+  // One probe of 4096 sampled regions per kind decides, per call site, the
+  // count form of d = 1 pairs calls (mean stab size) and whether the big
+  // sorts pack their records (sampled upper-key deltas that fit 32 bits).
+  // The decisions are kept per call site (regions, workspace, flags, stream):
+  // repeated calls -- graph replays -- skip the probe and its host read; every
+  // choice gives the same output, so a stale decision costs time only.
+  const bool walk_open = pairs && R->d == 1 && !(flags & (DDM_COUNT_RANKS | DDM_COUNT_WALK)) &&
+                         R->n_sub >= kWalkMinN && R->n_upd > 0;
+  const bool pack_open = DDM_MSD_PACK == 2 && (R->n_sub >= kPackMinN || R->n_upd >= kPackMinN) && R->n_sub > 0 &&
+                         R->n_upd > 0;
+  bool walk = pairs && R->d == 1 && (flags & DDM_COUNT_WALK) && !(flags & DDM_COUNT_RANKS);
+  int pack_s = -1, pack_u = -1;
+  if (walk_open || pack_open) {
+    const std::string pk = graph_key(R, ws, ws_bytes, flags, pairs != nullptr, sub_map, upd_map, st);
+    Probe pr{};
+    bool known = false;
+    {
+      std::lock_guard<std::mutex> lk(g_probe_mu);
+      const auto it = g_probe.find(pk);
+      if (it != g_probe.end()) {
+        pr = it->second;
+        known = true;
       }
     }
+    if (!known) {
+      double est[3] = {INFINITY, 0.0, 0.0};
+      DDM_LAUNCH("stab_probe", 0, st, match::stab_density_kernel<<<1, 256, 0, st>>>(
+          R->sub_lo[0], R->sub_hi[0], R->n_sub, R->upd_lo[0], R->upd_hi[0], R->n_upd, W.probe));
+      DDM_TRY(check_launch());
+      DDM_CUDA(cudaMemcpyAsync(est, W.probe, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+      DDM_CUDA(cudaStreamSynchronize(st));
+      pr.walk = est[0] <= kWalkMaxStab;
+      pr.pack_s = est[1] <= kPackMaxUnfit;
+      pr.pack_u = est[2] <= kPackMaxUnfit;
+      std::lock_guard<std::mutex> lk(g_probe_mu);
+      if (g_probe.size() > 4096) g_probe.clear();
+      g_probe[pk] = pr;
+    }
+    if (walk_open) walk = pr.walk;
+    if (pack_open) {
+      pack_s = pr.pack_s;
+      pack_u = pr.pack_u;
+    }
   }
+  const PackScope pack_scope(pack_s, pack_u);
   const uint32_t key_flags = (flags & ~(uint32_t)(DDM_COUNT_RANKS | DDM_COUNT_WALK)) |
                              (walk ? DDM_COUNT_WALK : DDM_COUNT_RANKS);
   const OneChain one_chain(walk);

@@ -223,14 +223,41 @@ __global__ void __launch_bounds__(256) tree_pm_kernel(const uint64_t* __restrict
 // |Stab(a)| at a uniform point, n * mean(hi - lo) / (max lo - min lo) over
 // 4096 evenly spaced subscriptions; +inf when a sampled value is non-finite
 // (the validation reports it).  One CTA.
+// Also: the fraction of sampled subscriptions (out[1]) and updates (out[2])
+// whose upper key lies 2^32 - 1 or more key units above the lower key -- the
+// records the packed MSD sort cannot pack (msd.cuh TileRegs): the pack
+// decision of the call.
 constexpr int kProbe = 4096;
+__device__ __forceinline__ double unfit_fraction(const double* __restrict__ lo, const double* __restrict__ hi,
+                                                 uint64_t n, int* scratch) {
+  int cnt = 0;
+  if (n)
+    for (int k = threadIdx.x; k < kProbe; k += blockDim.x) {
+      const uint64_t i = (uint64_t)((unsigned __int128)k * n / kProbe);
+      const double a = lo[i], b = hi[i];
+      if (!isfinite(a) || !isfinite(b) || !(a <= b)) continue;
+      cnt += f64_key(b) - f64_key(a) >= 0xffffffffull;
+    }
+  cnt = __reduce_add_sync(kFull, cnt);
+  if ((threadIdx.x & 31) == 0) atomicAdd(scratch, cnt);
+  __syncthreads();
+  const double f = n ? (double)*scratch / (double)kProbe : 0.0;
+  __syncthreads();
+  return f;
+}
+
 __global__ void __launch_bounds__(256) stab_density_kernel(const double* __restrict__ lo,
                                                            const double* __restrict__ hi, uint64_t n,
+                                                           const double* __restrict__ ulo,
+                                                           const double* __restrict__ uhi, uint64_t m,
                                                            double* __restrict__ out) {
   __shared__ double s_len[8], s_min[8], s_max[8];
-  __shared__ int s_bad;
-  if (threadIdx.x == 0) s_bad = 0;
+  __shared__ int s_bad, s_cnt[2];
+  if (threadIdx.x == 0) { s_bad = 0; s_cnt[0] = 0; s_cnt[1] = 0; }
   __syncthreads();
+  const double fs = unfit_fraction(lo, hi, n, &s_cnt[0]);
+  const double fu = unfit_fraction(ulo, uhi, m, &s_cnt[1]);
+  if (threadIdx.x == 0) { out[1] = fs; out[2] = fu; }
   double len = 0.0, mn = INFINITY, mx = -INFINITY;
   int bad = 0;
   for (int k = threadIdx.x; k < kProbe; k += blockDim.x) {
