@@ -122,7 +122,7 @@ typedef struct {
  * either way.  The same probe (also run for count calls with a side of at
  * least 2^22 regions) decides per side whether the sort packs its records to
  * 16 bytes (upper key as a 32-bit delta from the lower key): not when more
- * than 2 % of the sampled deltas need more bits -- a performance choice only. */
+ * than 15 % of the sampled deltas need more bits -- a performance choice only. */
 #define DDM_COUNT_RANKS (1u << 13)
 #define DDM_COUNT_WALK (1u << 14)
 /* Sweep dimension (d > 1, ddm_match_pairs / ddm_match_count /

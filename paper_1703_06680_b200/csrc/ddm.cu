@@ -151,7 +151,7 @@ inline ddm_status check_launch() {
 #define DDM_MSD_PACK 2
 #endif
 constexpr uint64_t kPackMinN = 1ull << 22;
-constexpr double kPackMaxUnfit = 0.02;  // no packing when more sampled deltas than this do not fit 32 bits
+constexpr double kPackMaxUnfit = 0.15;  // no packing when more sampled deltas than this do not fit 32 bits (c3: 2 %; alpha = 100: all)
 // Per-call pack decision of the subscription / update sorts (match_full's
 // probe; -1: by size only), set for the duration of a call like OneChain.
 struct PackHint {
