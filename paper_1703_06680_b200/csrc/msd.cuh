@@ -562,12 +562,16 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
 // threads, groups of up to 16384 records, 2^13 fine bins) for sorts whose
 // small-bucket map would need one more multisplit pass (c5: 19 bucket bits ->
 // 3 passes; with ~8x larger buckets 16 bits -> 2 passes).
+#ifndef DDM_LS_TARGET
+#define DDM_LS_TARGET 2560
+#endif
 struct LsSmall {
   static constexpr int T = kThreads, CAP = kCap, CAP2 = kCapPow2, BIN_BITS = kFineBinBits,
-                       BINS = 1 << kFineBinBits, SPAN = kSpan, MINB = DDM_LS_MINB;
+                       BINS = 1 << kFineBinBits, SPAN = kSpan, MINB = DDM_LS_MINB, TARGET = DDM_LS_TARGET;
 };
 struct LsBig {
-  static constexpr int T = 1024, CAP = 16384, CAP2 = 16384, BIN_BITS = 13, BINS = 1 << 13, SPAN = 8192, MINB = 1;
+  static constexpr int T = 1024, CAP = 16384, CAP2 = 16384, BIN_BITS = 13, BINS = 1 << 13, SPAN = 8192, MINB = 1,
+                       TARGET = 16384;
 };
 
 template <class C, bool V64, bool V32>
@@ -908,8 +912,12 @@ __global__ void __launch_bounds__(C::T, C::MINB) local_sort_kernel(const uint64_
   __syncthreads();  // publishes the mbarrier init
   while (e0 < e1) {
     uint64_t g1 = e1;
-    if (e1 - e0 > C::CAP) {
-      g1 = prev_boundary<C>(k_in, e0, e0 + C::CAP, BK, &S.bound[0]);
+    // groups of whole buckets, ~C::TARGET records (fewer records than fine
+    // bins: most bins then hold one record), or one bucket up to C::CAP
+    if (e1 - e0 > C::TARGET) {
+      g1 = prev_boundary<C>(k_in, e0, e0 + C::TARGET, BK, &S.bound[0]);
+      if (g1 == e0 && e1 - e0 > C::CAP) g1 = prev_boundary<C>(k_in, e0, e0 + C::CAP, BK, &S.bound[0]);
+      else if (g1 == e0) g1 = e1;
       if (g1 == e0) {  // one bucket alone exceeds the capacity
         if (threadIdx.x == 0) atomicOr(overflow, 1u);
         return;
