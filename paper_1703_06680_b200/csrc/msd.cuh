@@ -37,8 +37,11 @@ constexpr int kItems = DDM_MSD_ITEMS;  // records per thread of a payload pass t
 constexpr int kItemsK = 16;  // key-only passes: bigger tiles (fewer look-backs; measured 0.83 -> 0.70 ms at c3)
 constexpr int kTile = kThreads * kItems;
 constexpr int kSpan = 2048;      // nominal records per local-sort CTA
-constexpr int kCap = 2560;       // records a local-sort CTA can hold
-constexpr int kCapPow2 = 4096;   // bitonic network size bound (next power of two >= kCap)
+#ifndef DDM_LS_CAP
+#define DDM_LS_CAP 2560
+#endif
+constexpr int kCap = DDM_LS_CAP;  // records a local-sort CTA can hold
+constexpr int kCapPow2 = kCap <= 2048 ? 2048 : kCap <= 4096 ? 4096 : 8192;  // bitonic network size bound
 #ifndef DDM_LS_BINBITS
 #define DDM_LS_BINBITS 11
 #endif
@@ -563,15 +566,18 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
 // small-bucket map would need one more multisplit pass (c5: 19 bucket bits ->
 // 3 passes; with ~8x larger buckets 16 bits -> 2 passes).
 #ifndef DDM_LS_TARGET
-#define DDM_LS_TARGET 2560
+#define DDM_LS_TARGET DDM_LS_CAP
 #endif
 struct LsSmall {
   static constexpr int T = kThreads, CAP = kCap, CAP2 = kCapPow2, BIN_BITS = kFineBinBits,
                        BINS = 1 << kFineBinBits, SPAN = kSpan, MINB = DDM_LS_MINB, TARGET = DDM_LS_TARGET;
 };
+#ifndef DDM_LSB_TARGET
+#define DDM_LSB_TARGET 16384
+#endif
 struct LsBig {
   static constexpr int T = 1024, CAP = 16384, CAP2 = 16384, BIN_BITS = 13, BINS = 1 << 13, SPAN = 8192, MINB = 1,
-                       TARGET = 16384;
+                       TARGET = DDM_LSB_TARGET;
 };
 
 template <class C, bool V64, bool V32>
