@@ -36,7 +36,10 @@ constexpr int kRadix = 256;
 constexpr int kItems = DDM_MSD_ITEMS;  // records per thread of a payload pass tile
 constexpr int kItemsK = 16;  // key-only passes: bigger tiles (fewer look-backs; measured 0.83 -> 0.70 ms at c3)
 constexpr int kTile = kThreads * kItems;
-constexpr int kSpan = 2048;      // nominal records per local-sort CTA
+#ifndef DDM_LS_SPAN
+#define DDM_LS_SPAN 2048
+#endif
+constexpr int kSpan = DDM_LS_SPAN;  // nominal records per local-sort CTA
 #ifndef DDM_LS_CAP
 #define DDM_LS_CAP 2560
 #endif
