@@ -510,9 +510,7 @@ void init_attrs_once() {
   cudaFuncSetAttribute(ev::segment_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ev::Smem));
   cudaFuncSetAttribute(match::emit_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(match::ChunkSmem));
-  cudaFuncSetAttribute(match::emit_tile_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(match::EmitTileSmem));
-  cudaFuncSetAttribute(match::emit_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(match::emit_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(match::EmitTileSmem));
   cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(msd::PassSmem<msd::kItems, true, true>));
@@ -1147,15 +1145,10 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
   } else if (d == 1 && !per_row && (h.K > 4ull * m || (q.flags & DDM_EMIT_FORCE_CHUNK)))
     DDM_LAUNCH("emit", 24.0 * m + 8.0 * h.K + 12.0 * n, st,
                match::emit_chunk_kernel<<<egrid, match::kRowTile, sizeof(match::ChunkSmem), st>>>(A));
-  else if (d == 1 && !per_row) {  // sparse: tiles of 2048 rows walking a staged Slo window
-    const unsigned tg = (unsigned)((m + match::kEmitTile - 1) / match::kEmitTile);
-    if (A.sub_map)
-      DDM_LAUNCH("emit", 24.0 * m + 8.0 * h.K + 12.0 * n, st,
-                 match::emit_tile_kernel<true><<<tg, match::kEmitThreads, sizeof(match::EmitTileSmem), st>>>(A));
-    else
-      DDM_LAUNCH("emit", 24.0 * m + 8.0 * h.K + 12.0 * n, st,
-                 match::emit_tile_kernel<false><<<tg, match::kEmitThreads, sizeof(match::EmitTileSmem), st>>>(A));
-  }
+  else if (d == 1 && !per_row)  // sparse: tiles of 2048 rows walking a staged Slo window
+    DDM_LAUNCH("emit", 24.0 * m + 8.0 * h.K + 12.0 * n, st,
+               match::emit_tile_kernel<<<(unsigned)((m + match::kEmitTile - 1) / match::kEmitTile), match::kEmitThreads,
+                                         sizeof(match::EmitTileSmem), st>>>(A));
   else if (d == 1)  // forced per-row paths (cross-checks)
     DDM_LAUNCH("emit", 24.0 * m + 8.0 * h.K + 12.0 * n, st, match::emit_kernel<match::kEmitD1><<<egrid, match::kRowTile, 0, st>>>(A));
   else

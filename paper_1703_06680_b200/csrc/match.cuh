@@ -1161,58 +1161,9 @@ struct EmitTileSmem {
   uint64_t wsum[32];
 };
 
-// The rows of one emit_tile_kernel thread.  MAP: subscription ids go through
-// sub_map (slab-partitioned matching); the common unmapped case is compiled
-// without the branch.  A range part lying inside the staged window (the
-// usual case) is copied without per-entry window tests.
-template <bool MAP>
-__device__ __forceinline__ void emit_tile_rows(const EmitArgs& A, const uint64_t* WH, const uint32_t* WI, uint64_t w0,
-                                               uint32_t wlen, const uint32_t* rl, const uint32_t* rb,
-                                               const uint32_t* c0, const uint64_t* a, const uint32_t* lid, int ni,
-                                               uint64_t o) {
-  auto sid = [&](uint32_t s) -> uint32_t { return MAP ? __ldg(A.sub_map + s) : s; };
-  auto hi_at = [&](uint64_t i) -> uint64_t {
-    const uint64_t k = i - w0;
-    return (i >= w0 && k < wlen) ? WH[k] : A.T.lvl[0][i];
-  };
-  auto id_at = [&](uint64_t i) -> uint32_t {
-    const uint64_t k = i - w0;
-    return sid((i >= w0 && k < wlen) ? WI[k] : A.slo_id[i]);
-  };
-#pragma unroll
-  for (int r = 0; r < kEmitItems; ++r) {
-    if (r >= ni) break;
-    const uint32_t uid = A.upd_map ? A.upd_map[lid[r]] : lid[r];
-    const uint32_t stab = c0[r] - (rb[r] - rl[r]);
-    uint2* row = A.pairs + o;
-    // stab part: walk Slo backwards from r_lo - 1, exactly `stab` members
-    uint32_t rem = stab;
-    int64_t i = (int64_t)rl[r] - 1;
-    while (rem) {
-      if ((uint64_t)i < w0 && (i & 31) == 31) {  // outside the window: block-max skips
-        const int L = skip_levels(A.T, i, a[r]);
-        if (L) { i -= (int64_t)1 << (5 * L); continue; }
-      }
-      if (hi_at((uint64_t)i) >= a[r]) row[--rem] = make_uint2(id_at((uint64_t)i), uid);
-      --i;
-    }
-    // range part [r_lo, r_b)
-    uint2* rng = row + stab;
-    if (rl[r] >= w0 && rb[r] <= w0 + wlen) {
-      const uint32_t* src = WI + (rl[r] - w0);
-      const uint32_t nr = rb[r] - rl[r];
-      for (uint32_t k = 0; k < nr; ++k) rng[k] = make_uint2(sid(src[k]), uid);
-    } else {
-      for (uint32_t k = rl[r]; k < rb[r]; ++k) rng[k - rl[r]] = make_uint2(id_at(k), uid);
-    }
-    o += c0[r];
-  }
-}
-
 #ifndef DDM_EMIT_MINB
 #define DDM_EMIT_MINB 3
 #endif
-template <bool MAP>
 __global__ void __launch_bounds__(kEmitThreads, DDM_EMIT_MINB) emit_tile_kernel(const __grid_constant__ EmitArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EmitTileSmem& S = *reinterpret_cast<EmitTileSmem*>(smem_raw);
@@ -1302,7 +1253,35 @@ __global__ void __launch_bounds__(kEmitThreads, DDM_EMIT_MINB) emit_tile_kernel(
   uint64_t o = (ni > 0 ? A.tile_off[(j0 >> 8) + warp / kEmitWarpsPerRowTile] : 0) + wpre + incl - mine;
   __syncthreads();  // the barrier is initialised before anyone waits on it
   mbar_wait(&S.bar, 0);
-  emit_tile_rows<MAP>(A, WH, WI, w0, wlen, rl, rb, c0, a, lid, ni, o);
+  auto hi_at = [&](uint64_t i) -> uint64_t {
+    const uint64_t k = i - w0;
+    return (i >= w0 && k < wlen) ? WH[k] : A.T.lvl[0][i];
+  };
+  auto id_at = [&](uint64_t i) -> uint32_t {
+    const uint64_t k = i - w0;
+    return sub_out(A.sub_map, (i >= w0 && k < wlen) ? WI[k] : A.slo_id[i]);
+  };
+#pragma unroll
+  for (int r = 0; r < kEmitItems; ++r) {
+    if (r >= ni) break;
+    const uint32_t uid = A.upd_map ? A.upd_map[lid[r]] : lid[r];
+    const uint32_t stab = c0[r] - (rb[r] - rl[r]);
+    uint2* row = A.pairs + o;
+    // stab part: walk Slo backwards from r_lo - 1, exactly `stab` members
+    uint32_t rem = stab;
+    int64_t i = (int64_t)rl[r] - 1;
+    while (rem) {
+      if ((uint64_t)i < w0 && (i & 31) == 31) {  // outside the window: block-max skips
+        const int L = skip_levels(A.T, i, a[r]);
+        if (L) { i -= (int64_t)1 << (5 * L); continue; }
+      }
+      if (hi_at((uint64_t)i) >= a[r]) row[--rem] = make_uint2(id_at((uint64_t)i), uid);
+      --i;
+    }
+    // range part [r_lo, r_b)
+    for (uint32_t k = rl[r]; k < rb[r]; ++k) row[stab + (k - rl[r])] = make_uint2(id_at(k), uid);
+    o += c0[r];
+  }
 }
 
 // ------------------------------------------------------------ few dense rows (d = 1)
