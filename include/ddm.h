@@ -92,12 +92,16 @@ typedef struct {
     uint32_t upd;
 } ddm_pair;
 
-/* Flags for ddm_match_pairs / ddm_match_pairs_indexed.  The output ORDER is
- * deterministic without flags: rows by (upd lower bound, upd id), within a row
- * subscriptions by (sub lower bound, sub id) on the sweep dimension (0 for
- * d = 1; see DDM_SWEEP_DIM0 for d > 1).  The
- * emit-path flags only force one of the three emission paths (for tests);
- * every path yields byte-identical output. */
+/* Flags for ddm_match_pairs / ddm_match_pairs_indexed.  The pair SET never
+ * depends on flags, and the output ORDER is deterministic for given inputs,
+ * sizes and flags: rows by (upd lower bound, upd id) on the sweep dimension
+ * (0 for d = 1; see DDM_SWEEP_DIM0 for d > 1).  Within a row: d = 1,
+ * subscriptions by (sub lower bound, sub id) -- every emission path writes
+ * byte-identical output; d > 1, the tiled filter writes ascending sub id
+ * (a tile whose hits overflow its staging slot: its enumeration order) and the
+ * per-row paths (FORCE_THREAD / FORCE_WARP, or few updates) Slo order -- the
+ * order inside a d > 1 row is unspecified; canonicalise with ddm_sort_pairs.
+ * The emit-path flags only force one of the emission paths (for tests). */
 #define DDM_EMIT_AUTO 0u
 #define DDM_EMIT_FORCE_THREAD (1u << 8) /* one thread per update row */
 #define DDM_EMIT_FORCE_WARP (1u << 9)   /* one warp per update row, global scan */
