@@ -512,9 +512,6 @@ void init_attrs_once() {
                        (int)sizeof(match::ChunkSmem));
   cudaFuncSetAttribute(match::emit_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(match::EmitTileSmem));
-#if DDM_MSD_LBW
-#define msd_pass_kernel msd_pass_lbw_kernel
-#endif
   cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(msd::PassSmem<msd::kItems, true, true>));
   cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -527,9 +524,6 @@ void init_attrs_once() {
                        (int)sizeof(msd::PassSmem<msd::kItemsK, false, false>));
   cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItemsK, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(msd::PassSmem<msd::kItemsK, false, false>));
-#if DDM_MSD_LBW
-#undef msd_pass_kernel
-#endif
 #define DDM_LOCAL_ATTR(C, V64, V32)                                                                  \
   cudaFuncSetAttribute(msd::local_sort_kernel<C, V64, V32>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                        (int)sizeof(msd::LocalSmem<C, V64, V32>))
@@ -716,17 +710,13 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
     const bool pk = pack_records(n, pack_hint);
     const double rec = pk ? 16.0 : 20.0;
     const double bytes = (double)n * (PAY ? (p == 0 ? 16.0 + rec : 2.0 * rec) : 16.0);
-#if DDM_MSD_LBW
-#define DDM_PASS_KERNEL msd::msd_pass_lbw_kernel
-#else
 #define DDM_PASS_KERNEL msd::msd_pass_kernel
-#endif
 #define DDM_MSD_PASS(ITEMS, V64, V32, F64, NAME, KI, VI, II)                                                       \
   DDM_LAUNCH(NAME, bytes, st,                                                                                     \
              (DDM_PASS_KERNEL<ITEMS, V64, V32, F64>                                                                \
-              <<<persistent_grid((const void*)DDM_PASS_KERNEL<ITEMS, V64, V32, F64>, msd::kPassThreads,             \
+              <<<persistent_grid((const void*)DDM_PASS_KERNEL<ITEMS, V64, V32, F64>, msd::kThreads,             \
                                  sizeof(msd::PassSmem<ITEMS, V64, V32>), tiles),                                  \
-                 msd::kPassThreads, sizeof(msd::PassSmem<ITEMS, V64, V32>), st>>>(                                \
+                 msd::kThreads, sizeof(msd::PassSmem<ITEMS, V64, V32>), st>>>(                                \
                   KI, VI, II, bk[o], V64 ? bv[o] : nullptr, V32 ? bi[o] : nullptr, n, M, bits, 8 * p,              \
                   s.starts + p * 256, s.status, s.counters + p, err)))
     if (p == 0) {

@@ -271,31 +271,6 @@ __global__ void __launch_bounds__(512) msd_hist_kernel(const void* __restrict__ 
 #ifndef DDM_MSD_MINB
 #define DDM_MSD_MINB 3
 #endif
-// DDM_MSD_LBW: a ninth warp does every digit's decoupled look-back while the
-// eight worker warps rank and place the tile, instead of the workers doing it
-// after the ranking (the look-back was ~25 % of the pass's stall samples).
-#ifndef DDM_MSD_LBW
-#define DDM_MSD_LBW 0
-#endif
-constexpr int kPassThreads = kThreads + (DDM_MSD_LBW ? 32 : 0);
-
-// named barrier over the 256 worker threads (the look-back warp is not in it)
-__device__ __forceinline__ void bar_workers() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
-__device__ __forceinline__ uint32_t workers_excl_scan(uint32_t v, uint32_t* tmp) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t inc = warp_incl_scan(v);
-  if (lane == 31) tmp[warp] = inc;
-  bar_workers();
-  if (warp == 0) {
-    const uint32_t w = lane < kWarps ? tmp[lane] : 0u;
-    const uint32_t wi = warp_incl_scan(w);
-    if (lane < kWarps) tmp[lane] = wi - w;
-  }
-  bar_workers();
-  const uint32_t r = tmp[warp] + inc - v;
-  bar_workers();
-  return r;
-}
 
 template <int ITEMS, bool V64, bool V32>
 struct PassSmem {
@@ -309,10 +284,6 @@ struct PassSmem {
   uint32_t digit_base[kRadix];  // (dst = digit_base + tile position, mod 2^32: n < 2^32)
   uint32_t scan_tmp[kWarps + 1];
   uint32_t tile_id;
-#if DDM_MSD_LBW
-  uint32_t tot[kRadix];     // this tile's per-digit counts (for the look-back warp)
-  uint32_t tstart[kRadix];  // their exclusive scan
-#endif
 };
 
 
@@ -529,181 +500,6 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
     if (lane == 0 && e) atomicOr(err, e);
   }
 }
-
-#if DDM_MSD_LBW
-// msd_pass_kernel with the look-back moved to a ninth warp (DDM_MSD_LBW):
-// workers (warps 0-7) rank and place the tile while the look-back warp walks
-// the predecessors of all 256 digits (8 per lane, their loads interleaved);
-// two block-wide barriers per tile hand over the digit counts and the bases.
-template <int ITEMS, bool V64, bool V32, bool SRC_F64>
-__global__ void __launch_bounds__(kPassThreads, DDM_MSD_MINB)
-    msd_pass_lbw_kernel(const void* __restrict__ k_in, const void* __restrict__ v64_in,
-                        const uint32_t* __restrict__ v32_in, uint64_t* __restrict__ k_out,
-                        uint64_t* __restrict__ v64_out, uint32_t* __restrict__ v32_out, uint64_t n, MapRef M, int bits,
-                        int shift, const uint32_t* __restrict__ bin_start, uint32_t* __restrict__ status,
-                        uint32_t* __restrict__ tile_counter, uint32_t* __restrict__ err) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  using Smem = PassSmem<ITEMS, V64, V32>;
-  constexpr int kT = Smem::kT;
-  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool worker = tid < kThreads;
-  const uint64_t num_tiles = (n + kT - 1) / kT;
-  Bucketer BK;
-  BK.init(M, bits);
-  if (tid == 0) S.tile_id = atomicAdd(tile_counter, 1u);
-  __syncthreads();
-  uint32_t tile = S.tile_id;
-  if (tile >= num_tiles) return;
-  TileRegs<ITEMS, V64, V32, SRC_F64> R;
-  if (worker) R.load(k_in, v64_in, v32_in, (uint64_t)tile * kT + (uint64_t)warp * (32 * ITEMS), n, lane);
-  while (true) {
-    const uint64_t tile_base = (uint64_t)tile * kT;
-    const uint32_t tile_valid = (uint32_t)umin64(kT, n - tile_base);
-    uint32_t next = 0;
-    if (worker) {
-      const uint64_t wb0 = tile_base + (uint64_t)warp * (32 * ITEMS);
-      R.finish(wb0, n, lane);
-      uint32_t* wb = S.wbase[warp];
-      const unsigned lt = lanemask_lt();
-      {
-        uint4* z = reinterpret_cast<uint4*>(&S.wbase[0][0]);
-        constexpr int kZ = 2 * kWarps * kRadix / 4;
-#pragma unroll
-        for (int i = tid; i < kZ; i += kThreads) z[i] = make_uint4(0, 0, 0, 0);
-      }
-      bar_workers();
-      uint32_t dg[ITEMS];
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i) {
-        dg[i] = (BK(R.key[i]) >> shift) & 255u;
-        if (wb0 + i * 32 + lane < n) atomicAdd(&wb[dg[i]], 1u);
-      }
-      bar_workers();
-      uint32_t total = 0;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
-        const uint32_t c = S.wbase[w][tid];
-        S.wbase[w][tid] = total;
-        total += c;
-      }
-      st_relaxed_u32(status + (uint64_t)tile * kRadix + tid, (tile == 0 ? radix::kFlagPre : radix::kFlagAgg) | total);
-      const uint32_t tstart = workers_excl_scan(total, S.scan_tmp);
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) S.wbase[w][tid] += tstart;
-      S.tot[tid] = total;
-      S.tstart[tid] = tstart;
-      __syncthreads();  // (1) counts published: the look-back warp starts
-      uint32_t* mmask = S.match[warp];
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i) {
-        const bool valid = wb0 + i * 32 + lane < n;
-        const uint32_t d = dg[i];
-        if (valid) atomicOr(&mmask[d], 1u << lane);
-        __syncwarp();
-        uint32_t peers = 0, base = 0;
-        if (valid) {
-          peers = mmask[d];
-          base = wb[d];
-        }
-        __syncwarp();
-        if (valid) {
-          const unsigned before = peers & lt;
-          if (before == 0) {
-            wb[d] = base + __popc(peers);
-            mmask[d] = 0;
-          }
-          const uint32_t pos = base + __popc(before);
-          S.keys[pos] = R.key[i];
-          if (V64) S.v64[pos] = R.hv[i];
-          if (V32) S.v32[pos] = R.iv[i];
-          S.dg[pos] = (uint8_t)d;
-        }
-        __syncwarp();
-      }
-      if (tid == 0) S.tile_id = atomicAdd(tile_counter, 1u);
-      bar_workers();
-      next = S.tile_id;
-      if (next < num_tiles) R.load(k_in, v64_in, v32_in, (uint64_t)next * kT + (uint64_t)warp * (32 * ITEMS), n, lane);
-    } else {
-      __syncthreads();  // (1)
-      // look-back of digits d = lane + 32 j, j < 8, interleaved
-      constexpr int kD = kRadix / 32;
-#ifndef DDM_MSD_LBW_L
-#define DDM_MSD_LBW_L 4
-#endif
-      constexpr int kL = DDM_MSD_LBW_L;  // predecessors read per digit and step
-      uint32_t excl[kD];
-      int64_t pp[kD];
-      unsigned open = 0;
-#pragma unroll
-      for (int j = 0; j < kD; ++j) {
-        excl[j] = 0;
-        pp[j] = (int64_t)tile - 1;
-        if (tile > 0) open |= 1u << j;
-      }
-      while (open) {
-        uint32_t sv[kD][kL];
-#pragma unroll
-        for (int j = 0; j < kD; ++j)
-#pragma unroll
-          for (int k = 0; k < kL; ++k)
-            sv[j][k] = ((open >> j) & 1u) && pp[j] - k >= 0
-                           ? ld_relaxed_u32(status + (uint64_t)(pp[j] - k) * kRadix + lane + 32 * j)
-                           : radix::kFlagPre;
-        bool progress = false;
-#pragma unroll
-        for (int j = 0; j < kD; ++j) {
-          if (!((open >> j) & 1u)) continue;
-          int consumed = 0;
-          bool hit = false;
-#pragma unroll
-          for (int k = 0; k < kL; ++k) {
-            if (hit || consumed != k) break;
-            const uint32_t v = sv[j][k];
-            if ((v & ~radix::kValMask) == 0) break;
-            excl[j] += v & radix::kValMask;
-            consumed = k + 1;
-            hit = (v & radix::kFlagPre) != 0;
-          }
-          pp[j] -= consumed;
-          progress |= consumed > 0;
-          if (hit) open &= ~(1u << j);
-        }
-        if (!progress) __nanosleep(32);
-      }
-#pragma unroll
-      for (int j = 0; j < kD; ++j) {
-        const int d = lane + 32 * j;
-        if (tile > 0) st_relaxed_u32(status + (uint64_t)tile * kRadix + d, radix::kFlagPre | (excl[j] + S.tot[d]));
-        S.digit_base[d] = bin_start[d] + excl[j] - S.tstart[d];  // (mod 2^32)
-      }
-    }
-    __syncthreads();  // (2) tile placed and digit bases known
-    if (!worker) next = S.tile_id;
-    if (worker) {
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i) {
-        const uint32_t p = i * kThreads + tid;
-        if (p < tile_valid) {
-          const uint64_t k = S.keys[p];
-          const uint32_t d = S.dg[p];
-          const uint64_t dst = (uint32_t)(S.digit_base[d] + p);
-          k_out[dst] = k;
-          if (V64) v64_out[dst] = S.v64[p];
-          if (V32) v32_out[dst] = S.v32[p];
-        }
-      }
-    }
-    if (next >= num_tiles) break;
-    tile = next;  // (the next tile's placement starts after its barrier (1): every worker has scattered)
-  }
-  if (SRC_F64 && worker && err) {
-    const uint32_t e = __reduce_or_sync(kFull, R.err);
-    if (lane == 0 && e) atomicOr(err, e);
-  }
-}
-#endif
 
 // ---------------------------------------------------------------- local sort
 
