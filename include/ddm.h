@@ -140,6 +140,15 @@ typedef struct {
  * then follows dimension k*.  This flag sweeps dimension 0 always.  The
  * subscription index (ddm_sub_index_build) always sweeps dimension 0. */
 #define DDM_SWEEP_DIM0 (1u << 15)
+/* d > 1 filter form (cross-checks and tests; the pair SET is the same).
+ * Default: the row-indexed tiles (4096 updates per tile, binned once by their
+ * dims-1/2 lower bounds; every candidate subscription scans the row cells it
+ * can reach) when they fill the GPU, else the chunk-indexed tiles (1024
+ * updates; candidates streamed through shared memory and binned per chunk),
+ * else one thread / warp per update row when there are fewer tiles than SMs.
+ * FORCE_ROWS / FORCE_CHUNKS select a tiled form whatever the sizes. */
+#define DDM_DD_FORCE_ROWS (1u << 16)
+#define DDM_DD_FORCE_CHUNKS (1u << 17)
 
 /* Workspace bytes needed by ddm_match_count (want_pairs = 0) or
  * ddm_match_pairs (want_pairs != 0) for these sizes.  Independent of K. */

@@ -80,10 +80,12 @@ static_assert(kCells == kThreads * kCPT, "whole cells per thread in the cell sca
 
 // Widened float32 boxes of the subscriptions on dims 1 and 2, in Slo order
 // (a missing dim 2 is (-inf, +inf)): box12[i] = (lo1, hi1, lo2, hi2), lower
-// bounds rounded down, upper bounds rounded up.
+// bounds rounded down, upper bounds rounded up; box0[i] = the same for dim 0.
 __global__ void __launch_bounds__(256) box_kernel(const double* __restrict__ sdims, int d, uint64_t n,
                                                   float4* __restrict__ box12,
-                                                  const uint32_t* __restrict__ abort_flag) {
+                                                  const uint32_t* __restrict__ abort_flag,
+                                                  const uint64_t* __restrict__ slo_key,
+                                                  const uint64_t* __restrict__ slo_hi, float2* __restrict__ box0) {
   if (abort_flag && *abort_flag) return;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -98,6 +100,8 @@ __global__ void __launch_bounds__(256) box_kernel(const double* __restrict__ sdi
       b.w = __int_as_float(0x7f800000);
     }
     box12[i] = b;
+    // dim 0 (the sweep dimension) from the sorted keys: [rd(lo), ru(hi)]
+    box0[i] = make_float2(__double2float_rd(key_to_f64(slo_key[i])), __double2float_ru(key_to_f64(slo_hi[i])));
   }
 }
 
@@ -119,6 +123,7 @@ struct Args {
   const double* udims;       // [(d-1)][2][m] other dims of the updates in Ulo order
   const uint64_t* uhi;       // dim-0 upper keys in Ulo order (nullptr: from upd.hi[0])
   const float4* box12;       // widened float32 boxes (box_kernel)
+  const float2* box0;        // widened float32 dim-0 boxes in Slo order (box_kernel)
   uint64_t n, m;
   int d;
   const uint32_t* abort_flag;  // non-zero: an MSD bucket overflowed, inputs are not sorted -> no-op
@@ -132,8 +137,10 @@ struct Args {
   const uint64_t* tile_off;   // place: exclusive scan of the 256-row tile sums
   uint2* pairs;
   uint64_t capacity;          // pairs at or past capacity are never written
+  uint32_t* ovf_any;          // rows_kernel stage pass: set when some tile's staging slot overflowed
 };
 
+constexpr uint32_t kTileSkip = 0xfffffffeu;  // stage_n: the tile is placed by rows_place_kernel
 constexpr uint32_t kStageCap = 8192;  // staged hits per tile (c4 averages ~4100 per 1024-row tile)
 enum { kEmCount = 0, kEmDirect = 1, kEmStage = 2 };
 
@@ -497,6 +504,7 @@ __global__ void __launch_bounds__(kThreads, DDM_DD_MINB) dd_tile_kernel(const __
     }
     __syncthreads();
     const uint32_t nst = A.stage_n[tile];
+    if (nst == kTileSkip) return;  // placed by rows_place_kernel
     if (nst != ~0u) {
       // the tile's staged hits, grouped by row (counting sort on the row
       // prefix) and each row ordered by sub id: output order = rows in sweep
@@ -575,6 +583,415 @@ __global__ void __launch_bounds__(kThreads, DDM_DD_MINB) dd_tile_kernel(const __
   }
   if (MODE == kModeStage && tid == 0) A.stage_n[tile] = S.ovf ? ~0u : S.nout;
 }
+
+
+// ------------------------------------------------------------ row-indexed tiles
+//
+// The same tile and candidate set as dd_tile_kernel -- T consecutive updates
+// in sweep order against C_t = A_t ⊔ Slo[r_lo(x_t), max_j r_b(j)) (Alg. 6
+// SubSet[p] + the segment's inserted subscriptions) -- with the loop turned
+// around.  dd_tile_kernel streams C_t through shared memory in chunks,
+// cell-sorts every chunk and lets each ROW scan the cells it can reach: every
+// row pays for every chunk (c4: 1024 rows x ~46 chunks per tile).  Here the
+// tile's rows are binned ONCE into a G1 x G2 cell grid over their float32
+// (dim-1, dim-2) lower bounds (counting sort of row indices in shared memory),
+// and every CANDIDATE -- one per lane, read straight from the Slo-ordered box
+// arrays, no staging -- scans the row cells its widened box can reach:
+//   lo_k(S) <= hi_k(U) and lo_k(U) <= hi_k(S) <= lo_k(S) + len_k(S)
+//   =>  lo_k(U) in [rd(lo_k(S) - maxlen_k(rows)), hi_k(S)]      (k = 1, 2)
+// with maxlen_k the largest widened row length.
+//
+// Decision per (candidate, row) in the cells, on dims 0..2 (float32 boxes of
+// the subscriptions: box12 + box0; of the rows: built here):
+//  - the widened ("outer") boxes do not overlap on some dimension: no pair
+//    (widening only enlarges intervals, so a true pair always overlaps);
+//  - both inequalities of every dimension hold with a margin of more than the
+//    float rounding of both endpoints (sure_le): a pair, decided without
+//    touching the float64 data (d <= 3);
+//  - otherwise (endpoints within rounding of each other, or d > 3): queued and
+//    re-tested exactly on every dimension (exact_hit, Alg. 1), a warp at a time.
+// Hits are counted per row with shared-memory atomics; the stage pass stages
+// (sub, row) per tile, the place pass (rows_place_kernel) orders each row by
+// sub id.  A tile whose staging slot overflows marks its 1024-row
+// dd_tile_kernel tiles for that kernel's direct (deterministic) place pass.
+
+#ifndef DDM_DDR_THREADS
+#define DDM_DDR_THREADS 1024
+#endif
+constexpr int kRT = DDM_DDR_THREADS;  // threads of a row-indexed CTA
+constexpr int kRW = kRT / 32;
+
+struct RBins {  // monotone float bucketer, runtime bin count
+  float mn, scale;
+  int top;
+  __device__ __forceinline__ int operator()(float x) const {
+    float u = floorf((x - mn) * scale);
+    u = fminf(fmaxf(u, 0.0f), (float)top);  // fmaxf(NaN, 0) = 0
+    return (int)u;
+  }
+  __device__ __forceinline__ void init(float lo, float hi, int g) {
+    mn = lo;
+    top = g - 1;
+    float sc = hi > lo ? (float)g / (hi - lo) : 0.0f;
+    if (!(sc <= 1e30f)) sc = 1e30f;
+    scale = sc;
+  }
+};
+
+// x <= y certainly holds for the float64 values behind a = rd(x) and b = ru(y):
+// x <= ru(x) <= a + ulp(a) and y >= rd(y) >= b - ulp(b), ulp(v) <= |v| 2^-23
+// + 2^-149; the test asks for twice that margin, evaluated in float64 (exact
+// enough: its own rounding is ~2^-53 relative).  Infinite a or b (float range
+// exceeded) never pass unless b = +inf with a finite, where x <= FLT_MAX < y.
+__device__ __forceinline__ bool sure_le(float a, float b) {
+  const double da = a, db = b;
+  return da + (fabs(da) + fabs(db)) * 2.384185791015625e-07 + 1e-44 <= db;
+}
+
+template <int R>
+struct RowSmem {
+  static constexpr int kRows = kRT * R;
+  float4 rbox[kRows];          // widened row boxes (lo1, hi1, lo2, hi2), tile-row order
+  float2 rbox0[kRows];         // widened dim-0 row boxes (lo0, hi0)
+  uint16_t rrow[kRows];        // tile row of each cell slot (cell order)
+  uint16_t cstart[kRows + 2];  // G1 x G2 = kRows cells (d = 2: kRows x 1)
+  uint32_t rcnt[kRows];        // hits per row; cell counts / cursors while binning
+  uint32_t fpos[kCap];         // A_t members of one walk window
+  unsigned long long lst[kList * kRT];  // queued uncertain passes, per warp: [warp][e][lane] = (row << 32) | Slo position
+  float red[6 * kRW];
+  uint32_t scan32[kRW + 1];
+  uint64_t scan64[kRW + 1];
+  uint32_t rbmax;
+  uint32_t nout;
+  uint32_t ovf;
+};
+
+template <int R>
+constexpr uint32_t rows_stage_cap() { return 8u * kRT * R; }  // staged hits per tile (c4: ~4.1 per row)
+
+// A pair of the tile (row r, Slo position p): counted, and staged by the stage pass.
+template <int R, int MODE>
+__device__ __forceinline__ void rows_hit(const Args& A, RowSmem<R>& S, uint32_t r, uint32_t p, uint32_t tile) {
+  const uint32_t seq = atomicAdd(&S.rcnt[r], 1u);
+  if (MODE == kModeStage) {
+    const uint32_t slot = atomicAdd(&S.nout, 1u);
+    if (slot < rows_stage_cap<R>())
+      A.stage[(uint64_t)tile * rows_stage_cap<R>() + slot] =
+          make_uint2(match::sub_out(A.sub_map, A.slo_id[p]), (r << 16) | (seq & 0xffffu));
+    else
+      S.ovf = 1;
+  }
+}
+
+// One exact test (Alg. 1 on every dimension) of a queued uncertain pass.
+template <int R, int MODE>
+__device__ __forceinline__ void rows_exact(const Args& A, RowSmem<R>& S, unsigned long long v, uint64_t j0,
+                                           uint32_t tile) {
+  const uint32_t r = (uint32_t)(v >> 32), p = (uint32_t)v;
+  const uint64_t j = j0 + r;
+  if (exact_hit(A, p, j, A.uhi ? 0u : A.ulo_id[j])) rows_hit<R, MODE>(A, S, r, p, tile);
+}
+
+// Queued passes live per warp: lst[warp][e][lane].  A lane whose queue fills
+// inside a candidate flushes it alone (rare); otherwise the warp flushes
+// together at converged points, one queued test per lane.
+__device__ __forceinline__ unsigned long long* rows_lane_q(unsigned long long* lst, int tid) {
+  return lst + (tid >> 5) * (kList * 32) + (tid & 31);
+}
+template <int R, int MODE>
+__device__ __forceinline__ void rows_flush_lane(const Args& A, RowSmem<R>& S, uint32_t nl, uint64_t j0,
+                                                uint32_t tile) {
+  const unsigned long long* q = rows_lane_q(S.lst, threadIdx.x);
+  for (uint32_t e = 0; e < nl; ++e) rows_exact<R, MODE>(A, S, q[e * 32], j0, tile);
+}
+template <int R, int MODE>
+__device__ __forceinline__ void rows_flush_warp(const Args& A, RowSmem<R>& S, uint32_t& nl, uint64_t j0,
+                                                uint32_t tile, bool force) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t tot = __reduce_add_sync(kFull, nl);
+  if (tot == 0 || (!force && tot < 32)) return;
+  unsigned long long* q = rows_lane_q(S.lst, tid);
+  unsigned long long mine[kList];
+#pragma unroll
+  for (int e = 0; e < kList; ++e)
+    if (e < (int)nl) mine[e] = q[e * 32];
+  uint32_t pre = nl;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(kFull, pre, o);
+    if (lane >= o) pre += t;
+  }
+  pre -= nl;
+  __syncwarp();
+  unsigned long long* w = S.lst + (tid >> 5) * (kList * 32);
+#pragma unroll
+  for (int e = 0; e < kList; ++e)
+    if (e < (int)nl) w[pre + e] = mine[e];
+  __syncwarp();
+  for (uint32_t x = lane; x < tot; x += 32) rows_exact<R, MODE>(A, S, w[x], j0, tile);
+  __syncwarp();
+  nl = 0;
+}
+
+// One candidate (Slo position p) against the binned rows.
+template <int R, int MODE>
+__device__ __forceinline__ void rows_candidate(const Args& A, RowSmem<R>& S, const RBins& B1, const RBins& B2, int g1,
+                                               float ml1, float ml2, bool sure_ok, uint32_t p, uint32_t& nl,
+                                               uint64_t j0, uint32_t tile) {
+  const float4 f = __ldg(A.box12 + p);
+  const float2 f0 = __ldg(A.box0 + p);
+  const int c1l = B1(__fsub_rd(f.x, ml1)), c1h = B1(f.y);
+  const int c2l = B2(__fsub_rd(f.z, ml2)), c2h = B2(f.w);
+  const bool d2 = A.d == 2;
+  unsigned long long* q = rows_lane_q(S.lst, threadIdx.x);
+  for (int c2 = c2l; c2 <= c2h; ++c2) {
+    const uint32_t k1 = S.cstart[c2 * g1 + c1h + 1];
+    for (uint32_t k = S.cstart[c2 * g1 + c1l]; k < k1; ++k) {
+      const uint32_t r = S.rrow[k];
+      const float4 u = S.rbox[r];
+      if (!(f.x <= u.y && u.x <= f.y && f.z <= u.w && u.z <= f.w)) continue;
+      const float2 u0 = S.rbox0[r];
+      if (!(f0.x <= u0.y && u0.x <= f0.y)) continue;
+      if (sure_ok && sure_le(f0.x, u0.y) && sure_le(u0.x, f0.y) && sure_le(f.x, u.y) && sure_le(u.x, f.y) &&
+          (d2 || (sure_le(f.z, u.w) && sure_le(u.z, f.w)))) {
+        rows_hit<R, MODE>(A, S, r, p, tile);
+        continue;
+      }
+      if (nl == kList) {
+        rows_flush_lane<R, MODE>(A, S, nl, j0, tile);
+        nl = 0;
+      }
+      q[nl * 32] = ((unsigned long long)r << 32) | p;
+      ++nl;
+    }
+  }
+}
+
+// kModeCount: row counts + 256-row tile sums.  kModeStage: the same plus the
+// staged hits; stage_n[tile] = their number or ~0u (overflow), and the
+// 1024-row dd_tile_kernel tiles inside it (old_n) are marked kTileSkip or ~0u.
+template <int R, int MODE>
+__global__ void __launch_bounds__(kRT, 1) rows_kernel(const __grid_constant__ Args A, uint32_t* __restrict__ old_n) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  RowSmem<R>& S = *reinterpret_cast<RowSmem<R>*>(smem_raw);
+  constexpr int kRows = kRT * R;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (A.abort_flag && *A.abort_flag) return;  // this attempt is discarded (ddm.cu retries with LSB)
+  const uint32_t tile = blockIdx.x;
+  const uint64_t j0 = (uint64_t)tile * kRows;
+  const uint32_t nrows = (uint32_t)umin64(kRows, A.m - j0);
+  if (tid == 0) {
+    S.rbmax = 0;
+    S.nout = 0;
+    S.ovf = 0;
+  }
+  // 1. widened row boxes (tile-row order), their dims-1/2 bounds and max lengths
+  const float kInf = __int_as_float(0x7f800000);
+  float mn1 = kInf, mx1 = -kInf, ml1 = 0.0f, mn2 = kInf, mx2 = -kInf, ml2 = 0.0f;
+  uint32_t rbmax = 0;
+  for (uint32_t r = tid; r < (uint32_t)kRows; r += kRT) {
+    S.rcnt[r] = 0;
+    if (r >= nrows) continue;
+    const uint64_t j = j0 + r;
+    float4 u;
+    u.x = __double2float_rd(A.udims[j]);
+    u.y = __double2float_ru(A.udims[A.m + j]);
+    u.z = A.d > 2 ? __double2float_rd(A.udims[2 * A.m + j]) : -kInf;
+    u.w = A.d > 2 ? __double2float_ru(A.udims[3 * A.m + j]) : kInf;
+    S.rbox[r] = u;
+    const double a0 = key_to_f64(A.ulo_key[j]);
+    const double b0 = A.uhi ? key_to_f64(A.uhi[j]) : A.upd.hi[0][A.ulo_id[j]];
+    S.rbox0[r] = make_float2(__double2float_rd(a0), __double2float_ru(b0));
+    mn1 = fminf(mn1, u.x); mx1 = fmaxf(mx1, u.x); ml1 = fmaxf(ml1, __fsub_ru(u.y, u.x));
+    mn2 = fminf(mn2, u.z); mx2 = fmaxf(mx2, u.z); ml2 = fmaxf(ml2, __fsub_ru(u.w, u.z));
+    const uint32_t rb = A.r_b[j];
+    rbmax = rb > rbmax ? rb : rbmax;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mn1 = fminf(mn1, __shfl_xor_sync(kFull, mn1, o));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(kFull, mx1, o));
+    ml1 = fmaxf(ml1, __shfl_xor_sync(kFull, ml1, o));
+    mn2 = fminf(mn2, __shfl_xor_sync(kFull, mn2, o));
+    mx2 = fmaxf(mx2, __shfl_xor_sync(kFull, mx2, o));
+    ml2 = fmaxf(ml2, __shfl_xor_sync(kFull, ml2, o));
+  }
+  rbmax = __reduce_max_sync(kFull, rbmax);
+  if (lane == 0) {
+    S.red[warp] = mn1; S.red[kRW + warp] = mx1; S.red[2 * kRW + warp] = ml1;
+    S.red[3 * kRW + warp] = mn2; S.red[4 * kRW + warp] = mx2; S.red[5 * kRW + warp] = ml2;
+  }
+  __syncthreads();
+  if (lane == 0) atomicMax(&S.rbmax, rbmax);
+  for (int w = 0; w < kRW; ++w) {
+    mn1 = fminf(mn1, S.red[w]);
+    mx1 = fmaxf(mx1, S.red[kRW + w]);
+    ml1 = fmaxf(ml1, S.red[2 * kRW + w]);
+    mn2 = fminf(mn2, S.red[3 * kRW + w]);
+    mx2 = fmaxf(mx2, S.red[4 * kRW + w]);
+    ml2 = fmaxf(ml2, S.red[5 * kRW + w]);
+  }
+  // 2. cells of the rows: G1 x G2 = kRows (d = 2: one dim-2 bin); counting
+  // sort of the row indices by cell (the order inside a cell is irrelevant:
+  // counts do not depend on it and the place pass orders every row)
+  int g1 = kRows, g2 = 1;
+  if (A.d > 2) {
+    g1 = 1;
+    while (g1 * g1 < kRows) g1 <<= 1;
+    g2 = kRows / g1;
+  }
+  RBins B1, B2;
+  B1.init(mn1, mx1, g1);
+  B2.init(mn2, mx2, g2);
+  for (uint32_t r = tid; r < nrows; r += kRT) {
+    const float4 u = S.rbox[r];
+    atomicAdd(&S.rcnt[B2(u.z) * g1 + B1(u.x)], 1u);
+  }
+  __syncthreads();
+  {
+    constexpr int kPer = kRows / kRT;  // = R cells per thread
+    uint32_t v[kPer], sum = 0;
+#pragma unroll
+    for (int c = 0; c < kPer; ++c) { v[c] = S.rcnt[tid * kPer + c]; sum += v[c]; }
+    uint32_t total;
+    uint32_t ex = block_excl_scan<kRT, uint32_t>(sum, S.scan32, &total);
+#pragma unroll
+    for (int c = 0; c < kPer; ++c) {
+      S.cstart[tid * kPer + c] = (uint16_t)ex;
+      S.rcnt[tid * kPer + c] = ex;
+      ex += v[c];
+    }
+    if (tid == 0) S.cstart[kRows] = (uint16_t)total;
+  }
+  __syncthreads();
+  for (uint32_t r = tid; r < nrows; r += kRT) {
+    const float4 u = S.rbox[r];
+    S.rrow[atomicAdd(&S.rcnt[B2(u.z) * g1 + B1(u.x)], 1u)] = (uint16_t)r;
+  }
+  __syncthreads();
+  for (uint32_t r = tid; r < (uint32_t)kRows; r += kRT) S.rcnt[r] = 0;
+  __syncthreads();
+  const uint32_t rbm = S.rbmax;
+  const bool sure_ok = A.d <= 3;  // dims beyond 2 have no float boxes: always the exact test
+  // 3. candidates: A_t (CTA-wide backward walk over Slo, windows of kWin
+  // positions, runs of 32^L positions whose block max < x_t skipped), then the
+  // Slo slice [rl0, rbmax) straight from global memory
+  uint32_t nl = 0;
+  const uint64_t rl0 = A.r_lo[j0];
+  const uint64_t x = A.ulo_key[j0];
+  const uint32_t nact = A.cnt0[j0] - (A.r_b[j0] - (uint32_t)rl0);  // |A_t| = stab(x_t) (I4)
+  int64_t hi_excl = (int64_t)rl0;
+  uint32_t rem = nact;
+  static_assert(kRT == kWin, "one walk window position per thread");
+  while (rem && hi_excl > 0) {
+    const int64_t i = hi_excl - 1;
+    if (((i + 1) & (kWin - 1)) == 0) {
+      const int L = match::skip_levels(A.T, i, x);
+      if (L >= 2) { hi_excl -= (int64_t)1 << (5 * L); continue; }
+    }
+    const int64_t base = i & ~(int64_t)(kWin - 1);
+    const int64_t pp = base + tid;
+    const bool mem = pp < hi_excl && A.T.lvl[0][pp] >= x;
+    uint32_t total;
+    const uint32_t ex = block_excl_scan<kRT, uint32_t>(mem ? 1u : 0u, S.scan32, &total);
+    if (mem) S.fpos[ex] = (uint32_t)pp;
+    __syncthreads();
+    if (tid < total) rows_candidate<R, MODE>(A, S, B1, B2, g1, ml1, ml2, sure_ok, S.fpos[tid], nl, j0, tile);
+    rows_flush_warp<R, MODE>(A, S, nl, j0, tile, false);
+    rem = total < rem ? rem - total : 0;
+    hi_excl = base;
+    __syncthreads();  // fpos is rewritten by the next window
+  }
+  for (uint64_t p0 = rl0; p0 < rbm; p0 += kRT) {  // (warp-uniform trip count)
+    if (p0 + tid < rbm)
+      rows_candidate<R, MODE>(A, S, B1, B2, g1, ml1, ml2, sure_ok, (uint32_t)(p0 + tid), nl, j0, tile);
+    rows_flush_warp<R, MODE>(A, S, nl, j0, tile, false);
+  }
+  rows_flush_warp<R, MODE>(A, S, nl, j0, tile, true);
+  __syncthreads();
+  // 4. row counts, 256-row tile sums, staging state
+  for (uint32_t r = tid; r < nrows; r += kRT) A.cnt_out[j0 + r] = S.rcnt[r];
+  for (uint32_t t = warp; t * 256 < nrows; t += kRW) {  // a warp per 256-row tile
+    uint32_t sum = 0;
+    for (uint32_t r = t * 256 + lane; r < t * 256 + 256 && r < nrows; r += 32) sum += S.rcnt[r];
+    sum = __reduce_add_sync(kFull, sum);
+    if (lane == 0) A.tile_sum[(j0 >> 8) + t] = sum;
+  }
+  if (MODE == kModeStage && tid == 0) {
+    A.stage_n[tile] = S.ovf ? ~0u : S.nout;
+    if (S.ovf && A.ovf_any) atomicOr(A.ovf_any, 1u);
+    constexpr int kOld = kRows / (kThreads * 4);  // dd_tile_kernel<4> tiles per row tile
+    for (int t = 0; t < kOld; ++t)
+      if ((j0 >> 10) + t < (A.m + 1023) / 1024) old_n[(j0 >> 10) + t] = S.ovf ? ~0u : kTileSkip;
+  }
+}
+
+// Place pass of rows_kernel's stage pass: each tile's staged hits grouped by
+// row (counting sort on the row index), every row ordered by sub id, written
+// at its offset.  Overflowed tiles (stage_n == ~0u) are left to the direct
+// place pass of dd_tile_kernel.
+template <int R>
+__global__ void __launch_bounds__(kRT, 1) rows_place_kernel(const __grid_constant__ Args A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int kRows = kRT * R;
+  constexpr uint32_t kCapT = rows_stage_cap<R>();
+  uint32_t* sid = reinterpret_cast<uint32_t*>(smem_raw);  // [kCapT]
+  uint32_t* cur = sid + kCapT;                            // [kRows]
+  __shared__ uint64_t scan64[kRW + 1];
+  const int tid = threadIdx.x;
+  if (A.abort_flag && *A.abort_flag) return;
+  const uint32_t tile = blockIdx.x;
+  const uint32_t nst = A.stage_n[tile];
+  if (nst == ~0u) return;
+  const uint64_t j0 = (uint64_t)tile * kRows;
+  const uint64_t t0 = A.tile_off[j0 >> 8];
+  uint64_t off[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) {  // row q*kRT + tid (256-row tiles never straddle: kRT % 256 == 0)
+    const uint64_t j = j0 + (uint64_t)q * kRT + tid;
+    const bool valid = j < A.m;
+    const uint32_t c = valid ? A.cnt[j] : 0u;
+    uint64_t e = c;  // exclusive scan inside the 256-row tile: warp scan + the tile's earlier warps
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t t = __shfl_up_sync(kFull, e, o);
+      if ((tid & 31) >= o) e += t;
+    }
+    if ((tid & 31) == 31) scan64[tid >> 5] = e;
+    e -= c;
+    __syncthreads();
+    for (int w = (tid >> 5) & ~7; w < (tid >> 5); ++w) e += scan64[w];
+    __syncthreads();
+    off[q] = valid ? A.tile_off[j >> 8] + e : 0;
+    cur[q * kRT + tid] = (uint32_t)(off[q] - t0);
+  }
+  __syncthreads();
+  for (uint32_t e = tid; e < nst; e += kRT) {
+    const uint2 h = A.stage[(uint64_t)tile * kCapT + e];
+    sid[atomicAdd(&cur[h.y >> 16], 1u)] = h.x;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const uint64_t j = j0 + (uint64_t)q * kRT + tid;
+    if (j >= A.m) continue;
+    const uint32_t lo = (uint32_t)(off[q] - t0), hi = cur[q * kRT + tid];
+    for (uint32_t x = lo + 1; x < hi; ++x) {
+      const uint32_t v = sid[x];
+      uint32_t y = x;
+      while (y > lo && sid[y - 1] > v) { sid[y] = sid[y - 1]; --y; }
+      sid[y] = v;
+    }
+    if (hi > lo) {
+      const uint32_t lid = A.ulo_id[j];
+      const uint32_t uid = A.upd_map ? A.upd_map[lid] : lid;
+      for (uint32_t x = lo; x < hi; ++x)
+        if (t0 + x < A.capacity) A.pairs[t0 + x] = make_uint2(sid[x], uid);
+    }
+  }
+}
+template <int R>
+constexpr size_t rows_place_smem() { return sizeof(uint32_t) * (rows_stage_cap<R>() + kRT * R); }
 
 }  // namespace dd
 }  // namespace ddm

@@ -176,6 +176,10 @@ constexpr int kSMs = 148;
 #define DDM_DD_ROWS 4
 #endif
 constexpr int kDDRows = DDM_DD_ROWS;  // rows per thread of the d > 1 tile kernel (1024-row tiles)
+#ifndef DDM_DDR_ROWS
+#define DDM_DDR_ROWS 4
+#endif
+constexpr int kDDRRows = DDM_DDR_ROWS;  // rows per thread of the row-indexed d > 1 kernel (1024 threads: 4096-row tiles)
 
 inline size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -210,6 +214,7 @@ struct Index {
   uint64_t nb = 0;          // number of 1024-entry blocks
   double* sdims = nullptr;
   float4* box12 = nullptr;  // d > 1: widened float32 boxes (dims 1, 2) in Slo order (dd.cuh)
+  float2* box0 = nullptr;   // d > 1: widened float32 dim-0 boxes in Slo order (dd.cuh)
   size_t bytes = 0;
 };
 
@@ -238,6 +243,7 @@ Index index_layout(uint32_t d, uint64_t n, void* base) {
   I.sdims = c.take<double>((uint64_t)2 * (d - 1) * n);
   if (d > 1) {
     I.box12 = c.take<float4>(n);
+    I.box0 = c.take<float2>(n);
   }
   I.bytes = c.used;
   return I;
@@ -396,6 +402,8 @@ struct Misc {  // device-side results read back with one copy
   uint64_t K;
   uint32_t err;
   uint32_t overflow;  // an MSD bucket exceeded shared memory: redo with the LSB sort
+  uint32_t dd_ovf;    // d > 1 row-indexed stage pass: some tile's staging slot overflowed
+  uint32_t pad_;
 };
 
 constexpr ddm_status kRetryLSB = (ddm_status)100;  // internal
@@ -418,6 +426,7 @@ struct MatchWs {
   uint2* dd_stage;      // d > 1 stage pass: per-tile staged hits
   double* udims;        // d > 1: dims 1..d-1 of the updates in Ulo order
   uint32_t* dd_stage_n; // their number per tile (~0u: overflowed)
+  uint32_t* dd_stage_n2; // the same per row-indexed tile (dd::rows_kernel)
   Misc* misc;
   uint64_t* mm;        // [3][2] min/max keys (Slo, Shi, Ulo)
   double* probe;       // stab-density estimate (count-form choice)
@@ -447,9 +456,12 @@ MatchWs match_layout(uint32_t d, uint64_t n_sub, uint64_t m, void* base, bool in
     W.cnt = c.take<uint32_t>(m);
     W.fstab = c.take<uint32_t>(m);
     const uint64_t dtiles = m / (dd::kThreads * kDDRows) + 1;
-    W.dd_stage = c.take<uint2>(dtiles * dd::kStageCap);
+    const uint64_t rtiles2 = m / (dd::kRT * kDDRRows) + 1;
+    const uint64_t st_old = dtiles * dd::kStageCap, st_new = rtiles2 * dd::rows_stage_cap<kDDRRows>();
+    W.dd_stage = c.take<uint2>(st_old > st_new ? st_old : st_new);
     W.udims = c.take<double>((uint64_t)2 * (d - 1) * m);
     W.dd_stage_n = c.take<uint32_t>(dtiles);
+    W.dd_stage_n2 = c.take<uint32_t>(rtiles2);
   }
   W.ulo = msd_scratch(c, m, true);
   if (index_scratch) {
@@ -537,6 +549,9 @@ void init_attrs_once() {
   cudaFuncSetAttribute(dd::dd_tile_kernel<kDDRows, dd::kModeCount>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(dd::Smem<kDDRows>));
   cudaFuncSetAttribute(dd::dd_tile_kernel<kDDRows, dd::kModeStage>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(dd::Smem<kDDRows>));
   cudaFuncSetAttribute(dd::dd_tile_kernel<kDDRows, dd::kModePlace>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(dd::Smem<kDDRows>));
+  cudaFuncSetAttribute(dd::rows_kernel<kDDRRows, dd::kModeCount>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(dd::RowSmem<kDDRRows>));
+  cudaFuncSetAttribute(dd::rows_kernel<kDDRRows, dd::kModeStage>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(dd::RowSmem<kDDRRows>));
+  cudaFuncSetAttribute(dd::rows_place_kernel<kDDRRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dd::rows_place_smem<kDDRRows>());
   if (const char* e = getenv("DDM_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(e));
   done = true;
 }
@@ -886,7 +901,8 @@ ddm_status build_index_async(const ddm_regions* R, const Index& I, MsdScratch& s
     DDM_TRY(check_launch());
     DDM_LAUNCH("dd_boxes", 16.0 * (R->d > 2 ? 2 : 1) * n + 16.0 * n, st,
                dd::box_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.sdims, (int)R->d, n, I.box12,
-                                                                   use_msd ? &misc->overflow : nullptr));
+                                                                   use_msd ? &misc->overflow : nullptr, I.slo_key,
+                                                                   I.slo_hi, I.box0));
     DDM_TRY(check_launch());
   }
   return DDM_OK;
@@ -894,6 +910,31 @@ ddm_status build_index_async(const ddm_regions* R, const Index& I, MsdScratch& s
 
 // ------------------------------------------------------------ d > 1 tiled filter (dd.cuh)
 
+
+// Row-indexed d > 1 passes (dd::rows_kernel): the default when their
+// 4096-row tiles fill the GPU; DDM_DD_CHUNKS=1 keeps the chunk-indexed
+// dd_tile_kernel (A/B and cross-check).
+bool dd_rows_enabled(uint64_t m, uint32_t flags) {
+  static const bool off = [] {
+    const char* e = getenv("DDM_DD_CHUNKS");
+    return e && atoi(e) == 1;
+  }();
+  if (flags & DDM_DD_FORCE_ROWS) return true;
+  if (flags & DDM_DD_FORCE_CHUNKS) return false;
+  constexpr uint64_t kRowsT = dd::kRT * kDDRRows;
+  return !off && (m + kRowsT - 1) / kRowsT >= (uint64_t)kSMs;
+}
+
+void launch_dd_rows(int mode, const dd::Args& a, uint32_t* old_n, cudaStream_t st) {
+  constexpr int kRows = dd::kRT * kDDRRows;
+  const unsigned grid = (unsigned)((a.m + kRows - 1) / kRows);
+  if (mode == dd::kModeCount)
+    dd::rows_kernel<kDDRRows, dd::kModeCount><<<grid, dd::kRT, sizeof(dd::RowSmem<kDDRRows>), st>>>(a, old_n);
+  else if (mode == dd::kModeStage)
+    dd::rows_kernel<kDDRRows, dd::kModeStage><<<grid, dd::kRT, sizeof(dd::RowSmem<kDDRRows>), st>>>(a, old_n);
+  else
+    dd::rows_place_kernel<kDDRRows><<<grid, dd::kRT, dd::rows_place_smem<kDDRRows>(), st>>>(a);
+}
 
 void launch_dd(int mode, const dd::Args& a, cudaStream_t st) {
   constexpr int kRows = dd::kThreads * kDDRows;
@@ -1034,8 +1075,10 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
   // e.g. few updates against many subscriptions: 35 ms instead of 1.4 s at
   // n = 4e6, m = 2e3); each row then gets a thread or a warp
   const bool per_row = (q.flags & (DDM_EMIT_FORCE_THREAD | DDM_EMIT_FORCE_WARP)) != 0 ||
-                       (d > 1 && (m + dd::kThreads * kDDRows - 1) / (dd::kThreads * kDDRows) < (uint64_t)kSMs);
+                       (d > 1 && !(q.flags & (DDM_DD_FORCE_ROWS | DDM_DD_FORCE_CHUNKS)) &&
+                        (m + dd::kThreads * kDDRows - 1) / (dd::kThreads * kDDRows) < (uint64_t)kSMs);
   dd::Args D{};
+  const bool dd_rows = d > 1 && !per_row && dd_rows_enabled(m, q.flags);
   if (d > 1 && !per_row) {
     // a8: tiled dim-0 sweep with the exact filter on dims 1..d-1 (dd.cuh):
     // count pass -> 256-row tile sums -> scan; the emit pass runs after the sync
@@ -1054,6 +1097,7 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
     D.udims = W.udims;
     D.uhi = use_msd ? W.uhi : nullptr;
     D.box12 = I.box12;
+    D.box0 = I.box0;
     if (pre) {  // dims 1..d-1 of the updates gathered into sweep order (exact re-tests stay local)
       match::DimPtrs U{};
       for (uint32_t k = 0; k < d; ++k) { U.lo[k] = R->upd_lo[k]; U.hi[k] = R->upd_hi[k]; }
@@ -1071,11 +1115,20 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
     D.stage_n = W.dd_stage_n;
     D.cnt = W.cnt;
     D.tile_off = W.tile_off;
+    D.ovf_any = &W.misc->dd_ovf;
     // one enumeration: counts (+ staged hits when pairs are wanted) -> scan;
     // the place pass runs after the sync and the capacity check
     if (pre) {
-      if (q.pairs) DDM_LAUNCH("dd_stage", 24.0 * m, st, launch_dd(dd::kModeStage, D, st));
-      else DDM_LAUNCH("dd_count", 24.0 * m, st, launch_dd(dd::kModeCount, D, st));
+      if (dd_rows) {
+        dd::Args D2 = D;
+        D2.stage_n = W.dd_stage_n2;
+        if (q.pairs) DDM_LAUNCH("dd_stage", 24.0 * m, st, launch_dd_rows(dd::kModeStage, D2, W.dd_stage_n, st));
+        else DDM_LAUNCH("dd_count", 24.0 * m, st, launch_dd_rows(dd::kModeCount, D2, W.dd_stage_n, st));
+      } else if (q.pairs) {
+        DDM_LAUNCH("dd_stage", 24.0 * m, st, launch_dd(dd::kModeStage, D, st));
+      } else {
+        DDM_LAUNCH("dd_count", 24.0 * m, st, launch_dd(dd::kModeCount, D, st));
+      }
       DDM_TRY(check_launch());
       DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (stiles + 1), st));
       DDM_LAUNCH("scan", 16.0 * rtiles, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
@@ -1133,6 +1186,15 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
   if (d > 1 && !per_row) {
     D.pairs = A.pairs;
     D.capacity = q.capacity;
+    if (dd_rows) {
+      dd::Args D2 = D;
+      D2.stage_n = W.dd_stage_n2;
+      DDM_LAUNCH("dd_place", 16.0 * h.K + 8.0 * h.K, st, launch_dd_rows(dd::kModePlace, D2, nullptr, st));
+      DDM_TRY(check_launch());
+      if (!h.dd_ovf) return DDM_OK;
+      // tiles whose staging slot overflowed: the direct (deterministic) place
+      // pass of the chunk-indexed kernel, on its 1024-row tiles marked ~0u
+    }
     DDM_LAUNCH("dd_place", 16.0 * h.K + 8.0 * h.K, st, launch_dd(dd::kModePlace, D, st));
     return check_launch();
   }
@@ -1839,7 +1901,7 @@ extern "C" ddm_status ddm_sub_index_update(const void* index_in, void* index_out
   DDM_TRY(tree_async(I, kNeedShi | kNeedPm, false, st));
   if (d > 1) {
     DDM_LAUNCH("dd_boxes", 32.0 * n, st, dd::box_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.sdims, (int)d, n, I.box12,
-                                                                                              nullptr));
+                                                                                              nullptr, I.slo_key, I.slo_hi, I.box0));
     DDM_TRY(check_launch());
   }
   return check_launch();

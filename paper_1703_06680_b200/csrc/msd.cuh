@@ -453,7 +453,11 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
     if (next < num_tiles) R.load(k_in, v64_in, v32_in, (uint64_t)next * kT + (uint64_t)warp * (32 * ITEMS), n, lane);
 
     uint32_t excl = 0;
+#ifdef DDM_MSD_NOLB
+    if (false) {  // timing experiment only: no look-back (wrong offsets)
+#else
     if (tile > 0) {
+#endif
       int64_t p = (int64_t)tile - 1;
       while (true) {
         uint32_t sv[kLB];

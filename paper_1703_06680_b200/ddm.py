@@ -28,6 +28,8 @@ DDM_SORT_LSB = 1 << 12
 DDM_COUNT_RANKS = 1 << 13
 DDM_COUNT_WALK = 1 << 14
 DDM_SWEEP_DIM0 = 1 << 15
+DDM_DD_FORCE_ROWS = 1 << 16
+DDM_DD_FORCE_CHUNKS = 1 << 17
 
 STATUS = {0: "DDM_OK", 1: "DDM_ERR_INVALID_ARGUMENT", 2: "DDM_ERR_NONFINITE",
           3: "DDM_ERR_INVERTED_INTERVAL", 4: "DDM_ERR_CAPACITY", 5: "DDM_ERR_WORKSPACE",

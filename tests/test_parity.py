@@ -19,6 +19,9 @@ EMIT_FLAGS = [ddm.DDM_EMIT_AUTO, ddm.DDM_EMIT_FORCE_THREAD, ddm.DDM_EMIT_FORCE_W
               ddm.DDM_SORT_LSB, ddm.DDM_SORT_LSB | ddm.DDM_EMIT_FORCE_CHUNK,
               ddm.DDM_COUNT_WALK, ddm.DDM_COUNT_WALK | ddm.DDM_EMIT_FORCE_CHUNK,
               ddm.DDM_COUNT_WALK | ddm.DDM_SORT_LSB, ddm.DDM_COUNT_RANKS]
+# d > 1: both tiled filter forms at any size (row-indexed 4096-row tiles,
+# chunk-indexed 1024-row tiles), with the MSD and the LSB sorts
+DD_FLAGS = [ddm.DDM_DD_FORCE_ROWS, ddm.DDM_DD_FORCE_CHUNKS, ddm.DDM_DD_FORCE_ROWS | ddm.DDM_SORT_LSB]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -45,7 +48,9 @@ def check_against(orc, sl, sh, ul, uh, flags=(0,), ref=None):
         # d = 1: every emission path writes byte-identical output (rows by
         # sweep order, each row in Slo order).  d > 1: the tiled filter and
         # the per-row filter each write a deterministic order of their own.
-        fam = "rows" if (a[0].shape[0] > 1 and f & per_row) else "main"
+        # (d > 1: one family per forced filter form; the default form depends
+        # on the sizes)
+        fam = f & (per_row | ddm.DDM_DD_FORCE_ROWS | ddm.DDM_DD_FORCE_CHUNKS) if a[0].shape[0] > 1 else 0
         if fam not in first:
             first[fam] = raw_words(p)
         else:
@@ -331,7 +336,7 @@ def test_c4_scaled(orc):
     w = wl.uniform(20_000, 20_000, 1e4, wl.side_length(40_000, 1e4, 1.0, 3) * 3.0, 3, seed=3)
     ref = orc.sbm_seq(w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi)
     assert np.array_equal(ref, orc.bf_pairs(w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi))
-    check_against(orc, w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi, flags=EMIT_FLAGS, ref=ref)
+    check_against(orc, w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi, flags=EMIT_FLAGS + DD_FLAGS, ref=ref)
 
 
 @pytest.mark.parametrize("d", [2, 3, 4, 5, 8])
@@ -343,7 +348,7 @@ def test_dd_tie_storms(orc, d):
         u = np.sort(rng.integers(0, 4, (2, d, m)), axis=0).astype(np.float64)
         ref = orc.bf_pairs(s[0], s[1], u[0], u[1])
         assert np.array_equal(orc.sbm_dd_literal(s[0], s[1], u[0], u[1]), ref)
-        check_against(orc, s[0], s[1], u[0], u[1], flags=EMIT_FLAGS, ref=ref)
+        check_against(orc, s[0], s[1], u[0], u[1], flags=EMIT_FLAGS + DD_FLAGS, ref=ref)
 
 
 def test_c4_full_exact(orc):
@@ -437,7 +442,7 @@ def test_dd_chunks_and_long_intervals(orc):
         uh[:, pts] = ul[:, pts]
         ref = orc.bf_pairs(sl, sh, ul, uh)
         assert np.array_equal(orc.sbm_seq(sl, sh, ul, uh), ref)
-        check_against(orc, sl, sh, ul, uh, flags=EMIT_FLAGS, ref=ref)
+        check_against(orc, sl, sh, ul, uh, flags=EMIT_FLAGS + DD_FLAGS, ref=ref)
 
 
 def test_dd_degenerate_dim1(orc):
@@ -447,10 +452,10 @@ def test_dd_degenerate_dim1(orc):
     n, m = 1500, 1300
     sl = np.stack([rng.uniform(0, 100, n), np.full(n, 7.0)])
     ul = np.stack([rng.uniform(0, 100, m), np.full(m, 7.0)])
-    check_against(orc, sl, sl + 3.0, ul, ul + 3.0, flags=EMIT_FLAGS)
+    check_against(orc, sl, sl + 3.0, ul, ul + 3.0, flags=EMIT_FLAGS + DD_FLAGS)
     sl = np.stack([np.full(n, 1.0), rng.uniform(0, 100, n)])
     ul = np.stack([np.full(m, 1.0), rng.uniform(0, 100, m)])
-    check_against(orc, sl, sl + 0.5, ul, ul + 0.5, flags=EMIT_FLAGS)
+    check_against(orc, sl, sl + 0.5, ul, ul + 0.5, flags=EMIT_FLAGS + DD_FLAGS)
 
 
 def test_dd_staging_overflow(orc):
@@ -460,11 +465,11 @@ def test_dd_staging_overflow(orc):
     # dense tile: every region of both kinds overlaps every other (K = n*m)
     sl = rng.uniform(0.0, 0.5, (2, 300))
     ul = rng.uniform(0.0, 0.5, (2, 400))
-    check_against(orc, sl, sl + 1.0, ul, ul + 1.0, flags=(0,))
+    check_against(orc, sl, sl + 1.0, ul, ul + 1.0, flags=(0,) + tuple(DD_FLAGS))
     # one row with 70000 partners
     sl = rng.uniform(0.0, 0.5, (2, 70_000))
     ul = np.array([[0.2, 5.0], [0.3, 5.0]])
-    check_against(orc, sl, sl + 1.0, ul, ul + 0.5, flags=(0,))
+    check_against(orc, sl, sl + 1.0, ul, ul + 0.5, flags=(0,) + tuple(DD_FLAGS))
 
 
 def test_dd_deterministic_output():
