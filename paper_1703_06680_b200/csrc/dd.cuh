@@ -620,6 +620,7 @@ __global__ void __launch_bounds__(kThreads, DDM_DD_MINB) dd_tile_kernel(const __
 #endif
 constexpr int kRT = DDM_DDR_THREADS;  // threads of a row-indexed CTA
 constexpr int kRW = kRT / 32;
+constexpr int kRowFpos = 4 * kWin;    // A_t positions staged per batch
 
 struct RBins {  // monotone float bucketer, runtime bin count
   float mn, scale;
@@ -639,13 +640,15 @@ struct RBins {  // monotone float bucketer, runtime bin count
 };
 
 // x <= y certainly holds for the float64 values behind a = rd(x) and b = ru(y):
-// x <= ru(x) <= a + ulp(a) and y >= rd(y) >= b - ulp(b), ulp(v) <= |v| 2^-23
-// + 2^-149; the test asks for twice that margin, evaluated in float64 (exact
-// enough: its own rounding is ~2^-53 relative).  Infinite a or b (float range
-// exceeded) never pass unless b = +inf with a finite, where x <= FLT_MAX < y.
+// x < next(a) <= a + |a| 2^-23 + 2^-149 and y > prev(b) >= b - |b| 2^-23 -
+// 2^-149, so a + (|a| + |b|) 2^-22 + 2^-148 <= b suffices; every operation of
+// the test rounds up (a larger left side only makes it stricter), and
+// 2.4e-7f >= 2^-22, 1e-44f >= 2^-148.  b = +inf (y beyond the float range:
+// rd / ru saturate, a may be FLT_MAX for any larger x) never passes; a = -inf
+// gives NaN, which fails.
 __device__ __forceinline__ bool sure_le(float a, float b) {
-  const double da = a, db = b;
-  return da + (fabs(da) + fabs(db)) * 2.384185791015625e-07 + 1e-44 <= db;
+  const float m = __fadd_ru(fabsf(a), fabsf(b));
+  return __fadd_ru(__fmaf_ru(m, 2.4e-7f, a), 1e-44f) <= b && b < __int_as_float(0x7f800000);
 }
 
 template <int R>
@@ -656,7 +659,7 @@ struct RowSmem {
   uint16_t rrow[kRows];        // tile row of each cell slot (cell order)
   uint16_t cstart[kRows + 2];  // G1 x G2 = kRows cells (d = 2: kRows x 1)
   uint32_t rcnt[kRows];        // hits per row; cell counts / cursors while binning
-  uint32_t fpos[kCap];         // A_t members of one walk window
+  uint32_t fpos[kRowFpos];     // A_t members of a batch of walk windows
   unsigned long long lst[kList * kRT];  // queued uncertain passes, per warp: [warp][e][lane] = (row << 32) | Slo position
   float red[6 * kRW];
   uint32_t scan32[kRW + 1];
@@ -669,12 +672,35 @@ struct RowSmem {
 template <int R>
 constexpr uint32_t rows_stage_cap() { return 8u * kRT * R; }  // staged hits per tile (c4: ~4.1 per row)
 
-// A pair of the tile (row r, Slo position p): counted, and staged by the stage pass.
+// Decision for a queued (row r, Slo position p) whose dims-1/2 boxes overlap:
+// the dim-0 boxes, then the certain test (float margins, d <= 3), else the
+// exact test (Alg. 1 on every dimension, float64 / keys).
+template <int R>
+__device__ __forceinline__ bool rows_decide(const Args& A, const RowSmem<R>& S, unsigned long long v, uint64_t j0,
+                                            bool sure_ok) {
+  const uint32_t r = (uint32_t)(v >> 32), p = (uint32_t)v;
+  const float2 f0 = __ldg(A.box0 + p);
+  const float2 u0 = S.rbox0[r];
+  if (!(f0.x <= u0.y && u0.x <= f0.y)) return false;
+  if (sure_ok && sure_le(f0.x, u0.y) && sure_le(u0.x, f0.y)) {
+    const float4 f = __ldg(A.box12 + p);
+    const float4 u = S.rbox[r];
+    if (sure_le(f.x, u.y) && sure_le(u.x, f.y) && (A.d == 2 || (sure_le(f.z, u.w) && sure_le(u.z, f.w))))
+      return true;
+  }
+  const uint64_t j = j0 + r;
+  return exact_hit(A, p, j, A.uhi ? 0u : A.ulo_id[j]);
+}
+
+// A pair of the tile (row r, Slo position p): counted, and staged by the
+// stage pass (slot from the per-tile counter; `slot` precomputed by a
+// warp-aggregated reservation, or ~0u to reserve one here).
 template <int R, int MODE>
-__device__ __forceinline__ void rows_hit(const Args& A, RowSmem<R>& S, uint32_t r, uint32_t p, uint32_t tile) {
+__device__ __forceinline__ void rows_hit(const Args& A, RowSmem<R>& S, uint32_t r, uint32_t p, uint32_t tile,
+                                         uint32_t slot) {
   const uint32_t seq = atomicAdd(&S.rcnt[r], 1u);
   if (MODE == kModeStage) {
-    const uint32_t slot = atomicAdd(&S.nout, 1u);
+    if (slot == ~0u) slot = atomicAdd(&S.nout, 1u);
     if (slot < rows_stage_cap<R>())
       A.stage[(uint64_t)tile * rows_stage_cap<R>() + slot] =
           make_uint2(match::sub_out(A.sub_map, A.slo_id[p]), (r << 16) | (seq & 0xffffu));
@@ -683,66 +709,77 @@ __device__ __forceinline__ void rows_hit(const Args& A, RowSmem<R>& S, uint32_t 
   }
 }
 
-// One exact test (Alg. 1 on every dimension) of a queued uncertain pass.
-template <int R, int MODE>
-__device__ __forceinline__ void rows_exact(const Args& A, RowSmem<R>& S, unsigned long long v, uint64_t j0,
-                                           uint32_t tile) {
-  const uint32_t r = (uint32_t)(v >> 32), p = (uint32_t)v;
-  const uint64_t j = j0 + r;
-  if (exact_hit(A, p, j, A.uhi ? 0u : A.ulo_id[j])) rows_hit<R, MODE>(A, S, r, p, tile);
-}
-
 // Queued passes live per warp: lst[warp][e][lane].  A lane whose queue fills
-// inside a candidate flushes it alone (rare); otherwise the warp flushes
-// together at converged points, one queued test per lane.
+// inside a candidate decides it alone (rare); otherwise the warp decides
+// together at converged points: entry x of the warp's queues (in lane-major
+// order) is taken by lane x % 32, its owner found by a binary search over the
+// lanes' queue prefixes, so the decisions and hits run with full warps.
 __device__ __forceinline__ unsigned long long* rows_lane_q(unsigned long long* lst, int tid) {
   return lst + (tid >> 5) * (kList * 32) + (tid & 31);
 }
 template <int R, int MODE>
 __device__ __forceinline__ void rows_flush_lane(const Args& A, RowSmem<R>& S, uint32_t nl, uint64_t j0,
-                                                uint32_t tile) {
+                                                uint32_t tile, bool sure_ok) {
   const unsigned long long* q = rows_lane_q(S.lst, threadIdx.x);
-  for (uint32_t e = 0; e < nl; ++e) rows_exact<R, MODE>(A, S, q[e * 32], j0, tile);
+  for (uint32_t e = 0; e < nl; ++e) {
+    const unsigned long long v = q[e * 32];
+    if (rows_decide<R>(A, S, v, j0, sure_ok)) rows_hit<R, MODE>(A, S, (uint32_t)(v >> 32), (uint32_t)v, tile, ~0u);
+  }
 }
 template <int R, int MODE>
 __device__ __forceinline__ void rows_flush_warp(const Args& A, RowSmem<R>& S, uint32_t& nl, uint64_t j0,
-                                                uint32_t tile, bool force) {
+                                                uint32_t tile, bool sure_ok, bool force) {
   const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t tot = __reduce_add_sync(kFull, nl);
-  if (tot == 0 || (!force && tot < 32)) return;
-  unsigned long long* q = rows_lane_q(S.lst, tid);
-  unsigned long long mine[kList];
-#pragma unroll
-  for (int e = 0; e < kList; ++e)
-    if (e < (int)nl) mine[e] = q[e * 32];
-  uint32_t pre = nl;
+  if (tot == 0 || (!force && tot < 32 && !__any_sync(kFull, nl + 1 >= (uint32_t)kList))) return;
+  uint32_t pre = nl;  // inclusive prefix over the lanes
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t t = __shfl_up_sync(kFull, pre, o);
     if (lane >= o) pre += t;
   }
-  pre -= nl;
-  __syncwarp();
-  unsigned long long* w = S.lst + (tid >> 5) * (kList * 32);
+  pre -= nl;  // exclusive
+  const unsigned long long* w = S.lst + (tid >> 5) * (kList * 32);
+  for (uint32_t base = 0; base < tot; base += 32) {
+    const uint32_t x = base + lane;
+    // owner: the largest lane L with pre_L <= x (lanes with empty queues share
+    // the next lane's prefix, so the largest one owns x)
+    int L = 0;
 #pragma unroll
-  for (int e = 0; e < kList; ++e)
-    if (e < (int)nl) w[pre + e] = mine[e];
-  __syncwarp();
-  for (uint32_t x = lane; x < tot; x += 32) rows_exact<R, MODE>(A, S, w[x], j0, tile);
+    for (int step = 16; step; step >>= 1) {
+      const uint32_t pv = __shfl_sync(kFull, pre, L + step);
+      if (pv <= x) L += step;
+    }
+    const uint32_t pl = __shfl_sync(kFull, pre, L);
+    bool hit = false;
+    unsigned long long v = 0;
+    if (x < tot) {
+      v = w[(x - pl) * 32 + L];
+      hit = rows_decide<R>(A, S, v, j0, sure_ok);
+    }
+    uint32_t slot = ~0u;
+    if (MODE == kModeStage) {  // one slot reservation per warp
+      const unsigned hm = __ballot_sync(kFull, hit);
+      uint32_t b = 0;
+      if (lane == 0 && hm) b = atomicAdd(&S.nout, (uint32_t)__popc(hm));
+      b = __shfl_sync(kFull, b, 0);
+      slot = b + __popc(hm & lanemask_lt());
+    }
+    if (hit) rows_hit<R, MODE>(A, S, (uint32_t)(v >> 32), (uint32_t)v, tile, slot);
+  }
   __syncwarp();
   nl = 0;
 }
 
-// One candidate (Slo position p) against the binned rows.
+// One candidate (Slo position p) against the binned rows: rows whose widened
+// dims-1/2 boxes overlap the candidate's are queued for rows_decide.
 template <int R, int MODE>
 __device__ __forceinline__ void rows_candidate(const Args& A, RowSmem<R>& S, const RBins& B1, const RBins& B2, int g1,
                                                float ml1, float ml2, bool sure_ok, uint32_t p, uint32_t& nl,
                                                uint64_t j0, uint32_t tile) {
   const float4 f = __ldg(A.box12 + p);
-  const float2 f0 = __ldg(A.box0 + p);
   const int c1l = B1(__fsub_rd(f.x, ml1)), c1h = B1(f.y);
   const int c2l = B2(__fsub_rd(f.z, ml2)), c2h = B2(f.w);
-  const bool d2 = A.d == 2;
   unsigned long long* q = rows_lane_q(S.lst, threadIdx.x);
   for (int c2 = c2l; c2 <= c2h; ++c2) {
     const uint32_t k1 = S.cstart[c2 * g1 + c1h + 1];
@@ -750,15 +787,8 @@ __device__ __forceinline__ void rows_candidate(const Args& A, RowSmem<R>& S, con
       const uint32_t r = S.rrow[k];
       const float4 u = S.rbox[r];
       if (!(f.x <= u.y && u.x <= f.y && f.z <= u.w && u.z <= f.w)) continue;
-      const float2 u0 = S.rbox0[r];
-      if (!(f0.x <= u0.y && u0.x <= f0.y)) continue;
-      if (sure_ok && sure_le(f0.x, u0.y) && sure_le(u0.x, f0.y) && sure_le(f.x, u.y) && sure_le(u.x, f.y) &&
-          (d2 || (sure_le(f.z, u.w) && sure_le(u.z, f.w)))) {
-        rows_hit<R, MODE>(A, S, r, p, tile);
-        continue;
-      }
       if (nl == kList) {
-        rows_flush_lane<R, MODE>(A, S, nl, j0, tile);
+        rows_flush_lane<R, MODE>(A, S, nl, j0, tile, sure_ok);
         nl = 0;
       }
       q[nl * 32] = ((unsigned long long)r << 32) | p;
@@ -882,6 +912,7 @@ __global__ void __launch_bounds__(kRT, 1) rows_kernel(const __grid_constant__ Ar
   const uint32_t nact = A.cnt0[j0] - (A.r_b[j0] - (uint32_t)rl0);  // |A_t| = stab(x_t) (I4)
   int64_t hi_excl = (int64_t)rl0;
   uint32_t rem = nact;
+  uint32_t fill = 0;  // A_t members staged in fpos (a few walk windows per batch)
   static_assert(kRT == kWin, "one walk window position per thread");
   while (rem && hi_excl > 0) {
     const int64_t i = hi_excl - 1;
@@ -894,20 +925,35 @@ __global__ void __launch_bounds__(kRT, 1) rows_kernel(const __grid_constant__ Ar
     const bool mem = pp < hi_excl && A.T.lvl[0][pp] >= x;
     uint32_t total;
     const uint32_t ex = block_excl_scan<kRT, uint32_t>(mem ? 1u : 0u, S.scan32, &total);
-    if (mem) S.fpos[ex] = (uint32_t)pp;
-    __syncthreads();
-    if (tid < total) rows_candidate<R, MODE>(A, S, B1, B2, g1, ml1, ml2, sure_ok, S.fpos[tid], nl, j0, tile);
-    rows_flush_warp<R, MODE>(A, S, nl, j0, tile, false);
+    if (mem) S.fpos[fill + ex] = (uint32_t)pp;
+    fill += total;
     rem = total < rem ? rem - total : 0;
     hi_excl = base;
-    __syncthreads();  // fpos is rewritten by the next window
+    if (fill + kWin > (uint32_t)kRowFpos || !(rem && hi_excl > 0)) {  // (block-uniform) a batch of windows
+      __syncthreads();
+      for (uint32_t s0 = 0; s0 < fill; s0 += kRT) {  // (warp-uniform trip count)
+        if (s0 + tid < fill)
+          rows_candidate<R, MODE>(A, S, B1, B2, g1, ml1, ml2, sure_ok, S.fpos[s0 + tid], nl, j0, tile);
+        rows_flush_warp<R, MODE>(A, S, nl, j0, tile, sure_ok, false);
+      }
+      fill = 0;
+      __syncthreads();  // fpos is rewritten by the next windows
+    }
+  }
+  if (fill) {  // (the walk ended on a skip with members still staged)
+    __syncthreads();
+    for (uint32_t s0 = 0; s0 < fill; s0 += kRT) {
+      if (s0 + tid < fill)
+        rows_candidate<R, MODE>(A, S, B1, B2, g1, ml1, ml2, sure_ok, S.fpos[s0 + tid], nl, j0, tile);
+      rows_flush_warp<R, MODE>(A, S, nl, j0, tile, sure_ok, false);
+    }
   }
   for (uint64_t p0 = rl0; p0 < rbm; p0 += kRT) {  // (warp-uniform trip count)
     if (p0 + tid < rbm)
       rows_candidate<R, MODE>(A, S, B1, B2, g1, ml1, ml2, sure_ok, (uint32_t)(p0 + tid), nl, j0, tile);
-    rows_flush_warp<R, MODE>(A, S, nl, j0, tile, false);
+    rows_flush_warp<R, MODE>(A, S, nl, j0, tile, sure_ok, false);
   }
-  rows_flush_warp<R, MODE>(A, S, nl, j0, tile, true);
+  rows_flush_warp<R, MODE>(A, S, nl, j0, tile, sure_ok, true);
   __syncthreads();
   // 4. row counts, 256-row tile sums, staging state
   for (uint32_t r = tid; r < nrows; r += kRT) A.cnt_out[j0 + r] = S.rcnt[r];

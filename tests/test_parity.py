@@ -472,6 +472,34 @@ def test_dd_staging_overflow(orc):
     check_against(orc, sl, sl + 1.0, ul, ul + 0.5, flags=(0,) + tuple(DD_FLAGS))
 
 
+def test_dd_float_boundaries(orc):
+    """d = 2, 3: the row-indexed filter decides most pairs on float32 boxes
+    ("certain" when both inequalities hold with more than the rounding
+    margin); endpoints one float64 ulp apart inside one float32 ulp, values
+    beyond the float32 range (rd/ru saturate), subnormals and signed zeros
+    must all fall to the exact test.  Brute force decides."""
+    rng = np.random.default_rng(36)
+    mags = np.array([0.0, 1e-310, 1e-40, 1.0, 3.0e38, 3.4028234663852886e38, 1e39, 1e300])
+    for d in (2, 3):
+        for trial in range(6):
+            n, m = 700, 600
+            def side(cnt):
+                lo = rng.choice(mags, (d, cnt)) * rng.choice([-1.0, 1.0], (d, cnt))
+                lo = lo * (1.0 + rng.integers(-2, 3, (d, cnt)) * 2.0 ** -52)
+                ln = np.abs(lo) * rng.choice([0.0, 2.0 ** -52, 2.0 ** -30, 1e-7, 0.5], (d, cnt))
+                return lo, lo + ln
+            sl, sh = side(n)
+            ul, uh = side(m)
+            # partners that touch: some update bounds equal a sub bound (or one
+            # double ulp away from it)
+            k = rng.choice(m, 100, replace=False)
+            j = rng.choice(n, 100)
+            ul[:, k] = np.nextafter(sh[:, j], rng.choice([-np.inf, np.inf], (d, 100)))
+            uh[:, k] = np.maximum(uh[:, k], ul[:, k])
+            ref = orc.bf_pairs(sl, sh, ul, uh)
+            check_against(orc, sl, sh, ul, uh, flags=(0,) + tuple(DD_FLAGS), ref=ref)
+
+
 def test_dd_deterministic_output():
     w = wl.make("c4", scale=0.02)
     g = gpu_args(w)
