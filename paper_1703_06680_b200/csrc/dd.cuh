@@ -85,23 +85,45 @@ __global__ void __launch_bounds__(256) box_kernel(const double* __restrict__ sdi
                                                   float4* __restrict__ box12,
                                                   const uint32_t* __restrict__ abort_flag,
                                                   const uint64_t* __restrict__ slo_key,
-                                                  const uint64_t* __restrict__ slo_hi, float2* __restrict__ box0) {
+                                                  const uint64_t* __restrict__ slo_hi, float2* __restrict__ box0,
+                                                  const float4* __restrict__ box_in, const uint32_t* __restrict__ slo_id) {
   if (abort_flag && *abort_flag) return;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     float4 b;
-    b.x = __double2float_rd(sdims[i]);
-    b.y = __double2float_ru(sdims[n + i]);
-    if (d > 2) {
-      b.z = __double2float_rd(sdims[2 * n + i]);
-      b.w = __double2float_ru(sdims[3 * n + i]);
+    if (box_in) {  // gathered from the input-order boxes (one 16-byte read)
+      b = __ldg(box_in + slo_id[i]);
     } else {
-      b.z = -__int_as_float(0x7f800000);
-      b.w = __int_as_float(0x7f800000);
+      b.x = __double2float_rd(sdims[i]);
+      b.y = __double2float_ru(sdims[n + i]);
+      if (d > 2) {
+        b.z = __double2float_rd(sdims[2 * n + i]);
+        b.w = __double2float_ru(sdims[3 * n + i]);
+      } else {
+        b.z = -__int_as_float(0x7f800000);
+        b.w = __int_as_float(0x7f800000);
+      }
     }
     box12[i] = b;
     // dim 0 (the sweep dimension) from the sorted keys: [rd(lo), ru(hi)]
     box0[i] = make_float2(__double2float_rd(key_to_f64(slo_key[i])), __double2float_ru(key_to_f64(slo_hi[i])));
+  }
+}
+
+// Widened dims-1/2 boxes in INPUT order (coalesced reads of the coordinates):
+// the row-indexed calls gather these 16-byte boxes by id instead of gathering
+// 2 (d - 1) float64 coordinates per region into sweep order.
+__global__ void __launch_bounds__(256) box_in_kernel(const __grid_constant__ match::DimPtrs src, int d, uint64_t n,
+                                                     float4* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const float kInf = __int_as_float(0x7f800000);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    float4 b;
+    b.x = __double2float_rd(__ldcs(src.lo[1] + i));
+    b.y = __double2float_ru(__ldcs(src.hi[1] + i));
+    b.z = d > 2 ? __double2float_rd(__ldcs(src.lo[2] + i)) : -kInf;
+    b.w = d > 2 ? __double2float_ru(__ldcs(src.hi[2] + i)) : kInf;
+    out[i] = b;
   }
 }
 
@@ -124,6 +146,8 @@ struct Args {
   const uint64_t* uhi;       // dim-0 upper keys in Ulo order (nullptr: from upd.hi[0])
   const float4* box12;       // widened float32 boxes (box_kernel)
   const float2* box0;        // widened float32 dim-0 boxes in Slo order (box_kernel)
+  match::DimPtrs sub;        // subscription coordinates, all dims (exact tests when sdims is null)
+  const float4* ubox;        // widened dims-1/2 boxes of the updates in INPUT order (box_in_kernel), or null
   uint64_t n, m;
   int d;
   const uint32_t* abort_flag;  // non-zero: an MSD bucket overflowed, inputs are not sorted -> no-op
@@ -195,18 +219,38 @@ struct Rows {
 
 // Exact Alg. 1 test on every dimension for the sub at Slo position p and the
 // update at sorted position j (only float passes get here).  Both sides are
-// read in sweep order (sdims / udims), so these reads stay local.
+// read in sweep order (sdims / udims), so these reads stay local; without
+// them (row-indexed calls: only float boxes were built) from the input arrays
+// through the ids.
 __device__ __forceinline__ bool exact_hit(const Args& A, uint32_t p, uint64_t j, uint32_t lid) {
   const uint64_t b = A.uhi ? A.uhi[j] : f64_key(A.upd.hi[0][lid]);
   if (!(A.slo_key[p] <= b && A.T.lvl[0][p] >= A.ulo_key[j])) return false;  // dim 0 (keys)
-  for (int k = 1; k < A.d; ++k) {
-    const double slo = A.sdims[(uint64_t)(k - 1) * 2 * A.n + p];
-    const double shi = A.sdims[(uint64_t)(k - 1) * 2 * A.n + A.n + p];
-    const double ulo = A.udims[(uint64_t)(k - 1) * 2 * A.m + j];
-    const double uhi = A.udims[(uint64_t)(k - 1) * 2 * A.m + A.m + j];
-    if (!(slo <= uhi && ulo <= shi)) return false;
+  if (A.sdims) {
+    for (int k = 1; k < A.d; ++k) {
+      const double slo = A.sdims[(uint64_t)(k - 1) * 2 * A.n + p];
+      const double shi = A.sdims[(uint64_t)(k - 1) * 2 * A.n + A.n + p];
+      const double ulo = A.udims[(uint64_t)(k - 1) * 2 * A.m + j];
+      const double uhi = A.udims[(uint64_t)(k - 1) * 2 * A.m + A.m + j];
+      if (!(slo <= uhi && ulo <= shi)) return false;
+    }
+    return true;
   }
+  const uint32_t sid = A.slo_id[p], uid = A.ulo_id[j];
+  for (int k = 1; k < A.d; ++k)
+    if (!(A.sub.lo[k][sid] <= A.upd.hi[k][uid] && A.upd.lo[k][uid] <= A.sub.hi[k][sid])) return false;
   return true;
+}
+
+// Widened dims-1/2 box of the update at sorted position j.
+__device__ __forceinline__ float4 row_box(const Args& A, uint64_t j) {
+  if (A.ubox) return __ldg(A.ubox + A.ulo_id[j]);
+  const float kInf = __int_as_float(0x7f800000);
+  float4 u;
+  u.x = __double2float_rd(A.udims[j]);
+  u.y = __double2float_ru(A.udims[A.m + j]);
+  u.z = A.d > 2 ? __double2float_rd(A.udims[2 * A.m + j]) : -kInf;
+  u.w = A.d > 2 ? __double2float_ru(A.udims[3 * A.m + j]) : kInf;
+  return u;
 }
 
 // Exact re-test of this lane's queued float passes, in queue order.
@@ -553,12 +597,7 @@ __global__ void __launch_bounds__(kThreads, DDM_DD_MINB) dd_tile_kernel(const __
   for (int q = 0; q < R; ++q) {
     const uint64_t j = j0 + (uint64_t)q * kThreads + tid;
     if (rw.valid[q]) {
-      float4 u;
-      u.x = __double2float_rd(A.udims[j]);
-      u.y = __double2float_ru(A.udims[A.m + j]);
-      u.z = A.d > 2 ? __double2float_rd(A.udims[2 * A.m + j]) : -kInf;
-      u.w = A.d > 2 ? __double2float_ru(A.udims[3 * A.m + j]) : kInf;
-      S.rbox[q * kThreads + tid] = u;
+      S.rbox[q * kThreads + tid] = row_box(A, j);
       const uint32_t rb = A.r_b[j];
       rbmax = rb > rbmax ? rb : rbmax;
     }
@@ -801,7 +840,7 @@ __device__ __forceinline__ void rows_candidate(const Args& A, RowSmem<R>& S, con
 // staged hits; stage_n[tile] = their number or ~0u (overflow), and the
 // 1024-row dd_tile_kernel tiles inside it (old_n) are marked kTileSkip or ~0u.
 template <int R, int MODE>
-__global__ void __launch_bounds__(kRT, 1) rows_kernel(const __grid_constant__ Args A, uint32_t* __restrict__ old_n) {
+__global__ void __launch_bounds__(kRT, 1024 / kRT) rows_kernel(const __grid_constant__ Args A, uint32_t* __restrict__ old_n) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RowSmem<R>& S = *reinterpret_cast<RowSmem<R>*>(smem_raw);
   constexpr int kRows = kRT * R;
@@ -823,11 +862,7 @@ __global__ void __launch_bounds__(kRT, 1) rows_kernel(const __grid_constant__ Ar
     S.rcnt[r] = 0;
     if (r >= nrows) continue;
     const uint64_t j = j0 + r;
-    float4 u;
-    u.x = __double2float_rd(A.udims[j]);
-    u.y = __double2float_ru(A.udims[A.m + j]);
-    u.z = A.d > 2 ? __double2float_rd(A.udims[2 * A.m + j]) : -kInf;
-    u.w = A.d > 2 ? __double2float_ru(A.udims[3 * A.m + j]) : kInf;
+    const float4 u = row_box(A, j);
     S.rbox[r] = u;
     const double a0 = key_to_f64(A.ulo_key[j]);
     const double b0 = A.uhi ? key_to_f64(A.uhi[j]) : A.upd.hi[0][A.ulo_id[j]];
@@ -913,7 +948,7 @@ __global__ void __launch_bounds__(kRT, 1) rows_kernel(const __grid_constant__ Ar
   int64_t hi_excl = (int64_t)rl0;
   uint32_t rem = nact;
   uint32_t fill = 0;  // A_t members staged in fpos (a few walk windows per batch)
-  static_assert(kRT == kWin, "one walk window position per thread");
+  static_assert(kWin % kRT == 0, "whole walk window positions per thread");
   while (rem && hi_excl > 0) {
     const int64_t i = hi_excl - 1;
     if (((i + 1) & (kWin - 1)) == 0) {
@@ -921,11 +956,20 @@ __global__ void __launch_bounds__(kRT, 1) rows_kernel(const __grid_constant__ Ar
       if (L >= 2) { hi_excl -= (int64_t)1 << (5 * L); continue; }
     }
     const int64_t base = i & ~(int64_t)(kWin - 1);
-    const int64_t pp = base + tid;
-    const bool mem = pp < hi_excl && A.T.lvl[0][pp] >= x;
+    constexpr int kPW = kWin / kRT;  // window positions per thread
+    bool mem[kPW];
+    uint32_t c = 0;
+#pragma unroll
+    for (int u = 0; u < kPW; ++u) {
+      const int64_t pp = base + tid * kPW + u;
+      mem[u] = pp < hi_excl && A.T.lvl[0][pp] >= x;
+      c += mem[u];
+    }
     uint32_t total;
-    const uint32_t ex = block_excl_scan<kRT, uint32_t>(mem ? 1u : 0u, S.scan32, &total);
-    if (mem) S.fpos[fill + ex] = (uint32_t)pp;
+    uint32_t o = fill + block_excl_scan<kRT, uint32_t>(c, S.scan32, &total);
+#pragma unroll
+    for (int u = 0; u < kPW; ++u)
+      if (mem[u]) S.fpos[o++] = (uint32_t)(base + tid * kPW + u);
     fill += total;
     rem = total < rem ? rem - total : 0;
     hi_excl = base;

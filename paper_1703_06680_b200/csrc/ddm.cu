@@ -855,7 +855,7 @@ ddm_status tree_async(const Index& I, int need, bool have_lvl1, cudaStream_t st)
 
 ddm_status build_index_async(const ddm_regions* R, const Index& I, MsdScratch& slo, MsdScratch& shi,
                              const SortScratch& lsb, uint64_t* mm, Misc* misc, bool use_msd, cudaStream_t st,
-                             int need = kNeedShi | kNeedPm) {
+                             int need = kNeedShi | kNeedPm, bool boxes_only = false) {
   init_attrs_once();
   const uint64_t n = R->n_sub;
   if (n == 0) return DDM_OK;
@@ -896,13 +896,27 @@ ddm_status build_index_async(const ddm_regions* R, const Index& I, MsdScratch& s
   if (R->d > 1) {
     match::DimPtrs D{};
     for (uint32_t k = 0; k < R->d; ++k) { D.lo[k] = R->sub_lo[k]; D.hi[k] = R->sub_hi[k]; }
+    if (boxes_only) {
+      // row-indexed d > 1 calls: dims-1/2 float boxes in input order (over the
+      // sdims storage), gathered by id into Slo order; exact tests read the
+      // input arrays through the ids
+      float4* bin = reinterpret_cast<float4*>(I.sdims);
+      DDM_LAUNCH("dd_boxes", 32.0 * n, st, dd::box_in_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(D, (int)R->d, n, bin));
+      DDM_TRY(check_launch());
+      DDM_LAUNCH("dd_boxes", 56.0 * n, st,
+                 dd::box_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(nullptr, (int)R->d, n, I.box12,
+                                                                     use_msd ? &misc->overflow : nullptr, I.slo_key,
+                                                                     I.slo_hi, I.box0, bin, I.slo_id));
+      DDM_TRY(check_launch());
+      return DDM_OK;
+    }
     DDM_LAUNCH("gather_dims", 36.0 * (R->d - 1) * n, st, match::gather_dims_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.slo_id, D, (int)R->d, n, I.sdims,
                                                                                    use_msd ? &misc->overflow : nullptr));
     DDM_TRY(check_launch());
     DDM_LAUNCH("dd_boxes", 16.0 * (R->d > 2 ? 2 : 1) * n + 16.0 * n, st,
                dd::box_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.sdims, (int)R->d, n, I.box12,
                                                                    use_msd ? &misc->overflow : nullptr, I.slo_key,
-                                                                   I.slo_hi, I.box0));
+                                                                   I.slo_hi, I.box0, nullptr, nullptr));
     DDM_TRY(check_launch());
   }
   return DDM_OK;
@@ -965,6 +979,7 @@ struct MatchReq {
   uint32_t flags;
   const uint32_t* sub_map = nullptr;  // optional global ids of the subscriptions
   bool walk = false;                  // walk-form counts (index holds the slo_hi prefix maxima, not Shi)
+  bool boxes_only = false;            // d > 1 row-indexed call: the index holds float boxes, no sdims
   const ChunkExport* chunk = nullptr;  // export the chunk-start sets (d = 1) instead of the pairs
 };
 
@@ -1093,16 +1108,22 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
     D.slo_id = I.slo_id;
     for (uint32_t k = 0; k < d; ++k) { D.upd.lo[k] = R->upd_lo[k]; D.upd.hi[k] = R->upd_hi[k]; }
     D.T = tree_of(I);
-    D.sdims = I.sdims;
-    D.udims = W.udims;
+    D.sdims = q.boxes_only ? nullptr : I.sdims;
+    D.udims = q.boxes_only ? nullptr : W.udims;
+    D.ubox = q.boxes_only ? reinterpret_cast<const float4*>(W.udims) : nullptr;
+    for (uint32_t k = 0; k < d && q.boxes_only; ++k) { D.sub.lo[k] = R->sub_lo[k]; D.sub.hi[k] = R->sub_hi[k]; }
     D.uhi = use_msd ? W.uhi : nullptr;
     D.box12 = I.box12;
     D.box0 = I.box0;
-    if (pre) {  // dims 1..d-1 of the updates gathered into sweep order (exact re-tests stay local)
+    if (pre) {
       match::DimPtrs U{};
       for (uint32_t k = 0; k < d; ++k) { U.lo[k] = R->upd_lo[k]; U.hi[k] = R->upd_hi[k]; }
-      DDM_LAUNCH("gather_dims", 36.0 * (d - 1) * m, st, match::gather_dims_kernel<<<grid_for(m, 256, 8), 256, 0, st>>>(
-          W.ulo_id, U, (int)d, m, W.udims, &W.misc->overflow));
+      if (q.boxes_only)  // dims-1/2 float boxes in input order (over the udims storage), read by id
+        DDM_LAUNCH("dd_boxes", 48.0 * m, st, dd::box_in_kernel<<<grid_for(m, 256, 8), 256, 0, st>>>(
+            U, (int)d, m, reinterpret_cast<float4*>(W.udims)));
+      else  // dims 1..d-1 of the updates gathered into sweep order (exact re-tests stay local)
+        DDM_LAUNCH("gather_dims", 36.0 * (d - 1) * m, st, match::gather_dims_kernel<<<grid_for(m, 256, 8), 256, 0, st>>>(
+            W.ulo_id, U, (int)d, m, W.udims, &W.misc->overflow));
       DDM_TRY(check_launch());
     }
     D.n = n;
@@ -1511,6 +1532,10 @@ static ddm_status match_full_dim(const ddm_regions* R, ddm_pair* pairs, uint64_t
   Index I = index_layout(R->d, R->n_sub, base);
   MatchWs W = match_layout(R->d, R->n_sub, R->n_upd, base + a256(I.bytes), true);
   MatchReq q{&I, R, upd_map, pairs, capacity, flags, sub_map};
+  // d > 1 with the row-indexed filter: only float boxes are built (no float64
+  // coordinates gathered into sweep order; exact tests read them by id)
+  q.boxes_only = R->d > 1 && R->n_sub > 0 && R->n_upd > 0 &&
+                 !(flags & (DDM_EMIT_FORCE_THREAD | DDM_EMIT_FORCE_WARP)) && dd_rows_enabled(R->n_upd, flags);
   const bool lsb_only = (flags & DDM_SORT_LSB) != 0;
   // count form (ddm.h DDM_COUNT_RANKS / DDM_COUNT_WALK): d > 1 always ranks
   // (its dim-0 candidates outnumber the pairs); d = 1 pairs calls walk when
@@ -1579,7 +1604,7 @@ static ddm_status match_full_dim(const ddm_regions* R, ddm_pair* pairs, uint64_t
         DDM_TRY(side_stream_any(&s1, s));
         DDM_TRY(stream_join(s1, s));
         DDM_TRY(upd_sort_async(R, W, R->n_sub, true, s1, kMsdPrep));
-        DDM_TRY(build_index_async(R, I, W.slo, W.shi, W.sort, W.mm, W.misc, true, s, need));
+        DDM_TRY(build_index_async(R, I, W.slo, W.shi, W.sort, W.mm, W.misc, true, s, need, q.boxes_only));
         DDM_TRY(stream_join(s, s1));
         DDM_TRY(upd_sort_async(R, W, R->n_sub, true, s, kMsdRun));
       } else if (use_msd) {
@@ -1589,10 +1614,10 @@ static ddm_status match_full_dim(const ddm_regions* R, ddm_pair* pairs, uint64_t
         DDM_TRY(side_streams(side, s));
         DDM_TRY(stream_join(side[1], s));
         DDM_TRY(upd_sort_async(R, W, R->n_sub, true, side[1]));
-        DDM_TRY(build_index_async(R, I, W.slo, W.shi, W.sort, W.mm, W.misc, true, s, need));
+        DDM_TRY(build_index_async(R, I, W.slo, W.shi, W.sort, W.mm, W.misc, true, s, need, q.boxes_only));
         DDM_TRY(stream_join(s, side[1]));
       } else {
-        DDM_TRY(build_index_async(R, I, W.slo, W.shi, W.sort, W.mm, W.misc, false, s, need));
+        DDM_TRY(build_index_async(R, I, W.slo, W.shi, W.sort, W.mm, W.misc, false, s, need, q.boxes_only));
         DDM_TRY(upd_sort_async(R, W, R->n_sub, false, s));
       }
       return match_sorted(q, W, count_out, use_msd, s, kPhasePre);
@@ -1901,7 +1926,7 @@ extern "C" ddm_status ddm_sub_index_update(const void* index_in, void* index_out
   DDM_TRY(tree_async(I, kNeedShi | kNeedPm, false, st));
   if (d > 1) {
     DDM_LAUNCH("dd_boxes", 32.0 * n, st, dd::box_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(I.sdims, (int)d, n, I.box12,
-                                                                                              nullptr, I.slo_key, I.slo_hi, I.box0));
+                                                                                              nullptr, I.slo_key, I.slo_hi, I.box0, nullptr, nullptr));
     DDM_TRY(check_launch());
   }
   return check_launch();
