@@ -148,6 +148,9 @@ struct Args {
   const float2* box0;        // widened float32 dim-0 boxes in Slo order (box_kernel)
   match::DimPtrs sub;        // subscription coordinates, all dims (exact tests when sdims is null)
   const float4* ubox;        // widened dims-1/2 boxes of the updates in INPUT order (box_in_kernel), or null
+  const uint32_t* tile_rk;   // row-indexed tiles: {r_lo(x_t), r_b(max b)} per tile (tile_ranks_kernel), or null
+  const uint64_t* pmw;       //   with the prefix maxima of slo_hi (the A_t walk stops where they drop below x_t)
+  const uint64_t* pmb;
   uint64_t n, m;
   int d;
   const uint32_t* abort_flag;  // non-zero: an MSD bucket overflowed, inputs are not sorted -> no-op
@@ -836,6 +839,32 @@ __device__ __forceinline__ void rows_candidate(const Args& A, RowSmem<R>& S, con
   }
 }
 
+// Per row-indexed tile: rk[2t] = r_lo(x_t) = #{S.lo <= x_t} (x_t = the tile's
+// first update lower key) and rk[2t+1] = #{S.lo <= max_j b_j} (the end of the
+// tile's candidate slice), by binary search over Slo -- what the row-indexed
+// pass needs from the a4 count pass, without running it (nor sorting Shi).
+// One warp per tile: the lanes reduce the tile's upper keys, lane 0 searches.
+template <int R>
+__global__ void __launch_bounds__(256) tile_ranks_kernel(const __grid_constant__ Args A, uint32_t* __restrict__ rk) {
+  constexpr int kRows = kRT * R;
+  const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint64_t tiles = (A.m + kRows - 1) / kRows;
+  if (t >= tiles) return;
+  if (A.abort_flag && *A.abort_flag) return;
+  const uint64_t j0 = (uint64_t)t * kRows, j1 = umin64(A.m, j0 + kRows);
+  uint64_t bmax = 0;
+  for (uint64_t j = j0 + lane; j < j1; j += 32) {
+    const uint64_t b = A.uhi ? A.uhi[j] : f64_key(A.upd.hi[0][A.ulo_id[j]]);
+    bmax = b > bmax ? b : bmax;
+  }
+  bmax = warp_max_u64(bmax);
+  if (lane == 0) {
+    rk[2 * t] = (uint32_t)match::ub(A.slo_key, 0, A.n, A.ulo_key[j0]);
+    rk[2 * t + 1] = (uint32_t)match::ub(A.slo_key, 0, A.n, bmax);
+  }
+}
+
 // kModeCount: row counts + 256-row tile sums.  kModeStage: the same plus the
 // staged hits; stage_n[tile] = their number or ~0u (overflow), and the
 // 1024-row dd_tile_kernel tiles inside it (old_n) are marked kTileSkip or ~0u.
@@ -869,8 +898,10 @@ __global__ void __launch_bounds__(kRT, 1024 / kRT) rows_kernel(const __grid_cons
     S.rbox0[r] = make_float2(__double2float_rd(a0), __double2float_ru(b0));
     mn1 = fminf(mn1, u.x); mx1 = fmaxf(mx1, u.x); ml1 = fmaxf(ml1, __fsub_ru(u.y, u.x));
     mn2 = fminf(mn2, u.z); mx2 = fmaxf(mx2, u.z); ml2 = fmaxf(ml2, __fsub_ru(u.w, u.z));
-    const uint32_t rb = A.r_b[j];
-    rbmax = rb > rbmax ? rb : rbmax;
+    if (!A.tile_rk) {
+      const uint32_t rb = A.r_b[j];
+      rbmax = rb > rbmax ? rb : rbmax;
+    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -887,7 +918,7 @@ __global__ void __launch_bounds__(kRT, 1024 / kRT) rows_kernel(const __grid_cons
     S.red[3 * kRW + warp] = mn2; S.red[4 * kRW + warp] = mx2; S.red[5 * kRW + warp] = ml2;
   }
   __syncthreads();
-  if (lane == 0) atomicMax(&S.rbmax, rbmax);
+  if (lane == 0) atomicMax(&S.rbmax, A.tile_rk ? A.tile_rk[2 * tile + 1] : rbmax);
   for (int w = 0; w < kRW; ++w) {
     mn1 = fminf(mn1, S.red[w]);
     mx1 = fmaxf(mx1, S.red[kRW + w]);
@@ -942,15 +973,21 @@ __global__ void __launch_bounds__(kRT, 1024 / kRT) rows_kernel(const __grid_cons
   // positions, runs of 32^L positions whose block max < x_t skipped), then the
   // Slo slice [rl0, rbmax) straight from global memory
   uint32_t nl = 0;
-  const uint64_t rl0 = A.r_lo[j0];
   const uint64_t x = A.ulo_key[j0];
-  const uint32_t nact = A.cnt0[j0] - (A.r_b[j0] - (uint32_t)rl0);  // |A_t| = stab(x_t) (I4)
+  const uint64_t rl0 = A.tile_rk ? A.tile_rk[2 * tile] : A.r_lo[j0];
+  // the walk ends after |A_t| = stab(x_t) members (I4, from the count pass),
+  // or -- row-indexed calls without a count pass -- where the prefix maximum
+  // of slo_hi drops below x_t (nothing earlier can be a member)
+  uint32_t rem = A.tile_rk ? ~0u : A.cnt0[j0] - (A.r_b[j0] - (uint32_t)rl0);
   int64_t hi_excl = (int64_t)rl0;
-  uint32_t rem = nact;
   uint32_t fill = 0;  // A_t members staged in fpos (a few walk windows per batch)
   static_assert(kWin % kRT == 0, "whole walk window positions per thread");
   while (rem && hi_excl > 0) {
     const int64_t i = hi_excl - 1;
+    if (A.tile_rk) {  // max(slo_hi[0..i]) < x: no member at or before i
+      const uint64_t pw = __ldg(A.pmw + i), pb = __ldg(A.pmb + (i >> 10));
+      if ((pw > pb ? pw : pb) < x) break;
+    }
     if (((i + 1) & (kWin - 1)) == 0) {
       const int L = match::skip_levels(A.T, i, x);
       if (L >= 2) { hi_excl -= (int64_t)1 << (5 * L); continue; }

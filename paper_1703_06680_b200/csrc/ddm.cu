@@ -1036,25 +1036,27 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
   const uint64_t rtiles = (m + match::kRowTile - 1) / match::kRowTile;
   const unsigned stiles = (unsigned)((rtiles + match::kScanThreads * match::kScanItems - 1) /
                                      (match::kScanThreads * match::kScanItems));
-  if (pre) {
-  DDM_LAUNCH("count_partition", 0, st, match::count_partition_kernel<<<(unsigned)((ctiles + 255) / 256), 256, 0, st>>>(
-      W.ulo_key, m, I.slo_key, q.walk ? nullptr : I.shi_key, n, W.part));
-  DDM_TRY(check_launch());
-  // algorithmic bytes: sorted a and b (16 B, gathered b on the LSB path:
-  // 4 B id + ~32 B sector), r_lo / r_b / cnt written (12 B), Slo + Shi read
-  // once (16 B; walk form: Slo + slo_hi + pmw, 24 B)
-  const double cbytes = (use_msd ? 28.0 : 48.0) * m + (q.walk ? 24.0 : 16.0) * n;
+  // a4 for the row-indexed d > 1 filter: only r_lo of each tile's first
+  // query and the end of its candidate slice (tile_ranks_kernel); the count
+  // pass runs only if a tile overflows its staging slot (its fallback needs
+  // the per-row ranks)
   const match::CountWalk CW{I.slo_hi, I.pmw, I.pmb, I.nb, tree_of(I)};
-  if (q.walk)
-    DDM_LAUNCH("count", cbytes, st, match::count_kernel<true><<<(unsigned)ctiles, match::kCountThreads, match::count_smem_bytes(true), st>>>(
-        W.ulo_key, W.ulo_id, R->upd_hi[0], use_msd ? W.uhi : nullptr, m, I.slo_key, nullptr, n, W.part, W.r_lo, W.r_b,
-        W.cnt0, W.tile_sum, CW));
-  else
-    DDM_LAUNCH("count", cbytes, st, match::count_kernel<false><<<(unsigned)ctiles, match::kCountThreads, match::count_smem_bytes(false), st>>>(
-        W.ulo_key, W.ulo_id, R->upd_hi[0], use_msd ? W.uhi : nullptr, m, I.slo_key, I.shi_key, n, W.part, W.r_lo, W.r_b,
-        W.cnt0, W.tile_sum, CW));
-  DDM_TRY(check_launch());
-  }
+  auto count_pass = [&](cudaStream_t cs) -> ddm_status {
+    DDM_LAUNCH("count_partition", 0, cs, match::count_partition_kernel<<<(unsigned)((ctiles + 255) / 256), 256, 0, cs>>>(
+        W.ulo_key, m, I.slo_key, q.walk ? nullptr : I.shi_key, n, W.part));
+    DDM_TRY(check_launch());
+    const double cbytes = (use_msd ? 28.0 : 48.0) * m + (q.walk ? 24.0 : 16.0) * n;
+    if (q.walk)
+      DDM_LAUNCH("count", cbytes, cs, match::count_kernel<true><<<(unsigned)ctiles, match::kCountThreads, match::count_smem_bytes(true), cs>>>(
+          W.ulo_key, W.ulo_id, R->upd_hi[0], use_msd ? W.uhi : nullptr, m, I.slo_key, nullptr, n, W.part, W.r_lo, W.r_b,
+          W.cnt0, W.tile_sum, CW));
+    else
+      DDM_LAUNCH("count", cbytes, cs, match::count_kernel<false><<<(unsigned)ctiles, match::kCountThreads, match::count_smem_bytes(false), cs>>>(
+          W.ulo_key, W.ulo_id, R->upd_hi[0], use_msd ? W.uhi : nullptr, m, I.slo_key, I.shi_key, n, W.part, W.r_lo, W.r_b,
+          W.cnt0, W.tile_sum, CW));
+    return check_launch();
+  };
+  if (pre && !q.boxes_only) DDM_TRY(count_pass(st));
   if (pre && d == 1) {
     DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (stiles + 1), st));
     DDM_LAUNCH("scan", 16.0 * rtiles, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
@@ -1137,12 +1139,24 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
     D.cnt = W.cnt;
     D.tile_off = W.tile_off;
     D.ovf_any = &W.misc->dd_ovf;
+    if (q.boxes_only) {
+      D.tile_rk = reinterpret_cast<const uint32_t*>(W.part);
+      D.pmw = I.pmw;
+      D.pmb = I.pmb;
+    }
     // one enumeration: counts (+ staged hits when pairs are wanted) -> scan;
     // the place pass runs after the sync and the capacity check
     if (pre) {
       if (dd_rows) {
         dd::Args D2 = D;
         D2.stage_n = W.dd_stage_n2;
+        if (q.boxes_only) {
+          constexpr uint64_t kRowsT = dd::kRT * kDDRRows;
+          const uint64_t rt = (m + kRowsT - 1) / kRowsT;
+          DDM_LAUNCH("tile_ranks", 8.0 * m, st, dd::tile_ranks_kernel<kDDRRows><<<(unsigned)((rt * 32 + 255) / 256), 256, 0, st>>>(
+              D, reinterpret_cast<uint32_t*>(W.part)));
+          DDM_TRY(check_launch());
+        }
         if (q.pairs) DDM_LAUNCH("dd_stage", 24.0 * m, st, launch_dd_rows(dd::kModeStage, D2, W.dd_stage_n, st));
         else DDM_LAUNCH("dd_count", 24.0 * m, st, launch_dd_rows(dd::kModeCount, D2, W.dd_stage_n, st));
       } else if (q.pairs) {
@@ -1215,6 +1229,8 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
       if (!h.dd_ovf) return DDM_OK;
       // tiles whose staging slot overflowed: the direct (deterministic) place
       // pass of the chunk-indexed kernel, on its 1024-row tiles marked ~0u
+      // (it needs the per-row ranks of the count pass)
+      if (q.boxes_only) DDM_TRY(count_pass(st));
     }
     DDM_LAUNCH("dd_place", 16.0 * h.K + 8.0 * h.K, st, launch_dd(dd::kModePlace, D, st));
     return check_launch();
@@ -1591,7 +1607,7 @@ static ddm_status match_full_dim(const ddm_regions* R, ddm_pair* pairs, uint64_t
   const OneChain one_chain(walk);
   for (int attempt = lsb_only ? 1 : 0; attempt < 2; ++attempt) {
     const bool use_msd = attempt == 0;
-    const int need = walk ? kNeedPm : kNeedShi;
+    const int need = (walk || q.boxes_only) ? kNeedPm : kNeedShi;
     q.walk = need == kNeedPm;
     auto pre = [&](cudaStream_t s) -> ddm_status {
       DDM_CUDA(cudaMemsetAsync(W.misc, 0, sizeof(Misc), s));
