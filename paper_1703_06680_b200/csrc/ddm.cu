@@ -215,6 +215,7 @@ struct Index {
   double* sdims = nullptr;
   float4* box12 = nullptr;  // d > 1: widened float32 boxes (dims 1, 2) in Slo order (dd.cuh)
   float2* box0 = nullptr;   // d > 1: widened float32 dim-0 boxes in Slo order (dd.cuh)
+  uint32_t* tick = nullptr;  // ticket of match::tree_levels_kernel (scratch)
   size_t bytes = 0;
 };
 
@@ -245,6 +246,7 @@ Index index_layout(uint32_t d, uint64_t n, void* base) {
     I.box12 = c.take<float4>(n);
     I.box0 = c.take<float2>(n);
   }
+  I.tick = c.take<uint32_t>(1);
   I.bytes = c.used;
   return I;
 }
@@ -711,7 +713,6 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
   const bool big = msd_big(n);
   const uint32_t span = big ? msd::LsBig::SPAN : msd::LsSmall::SPAN;
   const uint32_t spans = (uint32_t)((n + span - 1) / span);
-  (void)nb;
   uint64_t* bk[2] = {s.k[0], s.k[1]};
   uint64_t* bv[2] = {s.v64[0], s.v64[1]};
   uint32_t* bi[2] = {s.v32[0], s.v32[1]};
@@ -748,8 +749,12 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
     DDM_TRY(check_launch());
   }
   const int l = (passes - 1) & 1;
-  DDM_LAUNCH("msd_bounds", 0, st, msd::span_bounds_kernel<<<(spans + 256) / 256, 256, 0, st>>>(bk[l], n, M, bits, spans,
-                                                                                             span, s.bounds));
+  if (passes == 1)  // bucket starts = the pass's digit starts
+    DDM_LAUNCH("msd_bounds", 0, st, msd::span_bounds_hist_kernel<<<(spans + 256) / 256, 256, 0, st>>>(
+        s.starts, nb, n, spans, span, s.bounds));
+  else
+    DDM_LAUNCH("msd_bounds", 0, st, msd::span_bounds_kernel<<<(spans + 256) / 256, 256, 0, st>>>(bk[l], n, M, bits, spans,
+                                                                                               span, s.bounds));
   DDM_TRY(check_launch());
 #define DDM_LOCAL(C, V64, V32, NAME, BYTES, VI, II, HI)                                                         \
   DDM_LAUNCH(NAME, BYTES, st,                                                                                  \
@@ -845,9 +850,13 @@ ddm_status tree_async(const Index& I, int need, bool have_lvl1, cudaStream_t st)
     DDM_TRY(check_launch());
     from = 3;
   }
-  for (int L = from; L <= I.levels; ++L) {
-    DDM_LAUNCH("block_max", 8.0 * I.lvl_n[L - 1], st, match::block_max_kernel<<<grid_for(I.lvl_n[L - 1], 256, 8), 256, 0, st>>>(
-        I.lvl[L - 1], I.lvl_n[L - 1], I.lvl[L]));
+  if (from <= I.levels) {  // the remaining levels in one launch
+    match::TreeLv T{};
+    for (int L = 0; L <= I.levels; ++L) { T.lvl[L] = I.lvl[L]; T.n[L] = I.lvl_n[L]; }
+    T.levels = I.levels;
+    DDM_CUDA(cudaMemsetAsync(I.tick, 0, sizeof(uint32_t), st));
+    DDM_LAUNCH("block_max", 8.0 * I.lvl_n[from - 1], st, match::tree_levels_kernel<<<(unsigned)((I.lvl_n[from] + 255) / 256), 256, 0, st>>>(
+        T, from, I.tick));
     DDM_TRY(check_launch());
   }
   return DDM_OK;
@@ -1042,8 +1051,12 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
   // the per-row ranks)
   const match::CountWalk CW{I.slo_hi, I.pmw, I.pmb, I.nb, tree_of(I)};
   auto count_pass = [&](cudaStream_t cs) -> ddm_status {
-    DDM_LAUNCH("count_partition", 0, cs, match::count_partition_kernel<<<(unsigned)((ctiles + 255) / 256), 256, 0, cs>>>(
-        W.ulo_key, m, I.slo_key, q.walk ? nullptr : I.shi_key, n, W.part));
+    if (ctiles <= match::kPartWarpMaxTiles)
+      DDM_LAUNCH("count_partition", 0, cs, match::count_partition_kernel<<<(unsigned)((ctiles * 32 + 255) / 256), 256, 0, cs>>>(
+          W.ulo_key, m, I.slo_key, q.walk ? nullptr : I.shi_key, n, W.part));
+    else
+      DDM_LAUNCH("count_partition", 0, cs, match::count_partition1_kernel<<<(unsigned)((ctiles + 255) / 256), 256, 0, cs>>>(
+          W.ulo_key, m, I.slo_key, q.walk ? nullptr : I.shi_key, n, W.part));
     DDM_TRY(check_launch());
     const double cbytes = (use_msd ? 28.0 : 48.0) * m + (q.walk ? 24.0 : 16.0) * n;
     if (q.walk)

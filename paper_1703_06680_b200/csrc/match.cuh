@@ -151,6 +151,64 @@ __global__ void __launch_bounds__(256) block_max_kernel(const uint64_t* __restri
   }
 }
 
+// Levels from .. levels of the block-max tree in one launch (instead of one
+// block_max launch per level): each thread builds one level-`from` entry from
+// its 32 level-(from-1) entries (16-byte loads, all in flight at once), each
+// warp the level-(from+1) entry above its 32 lanes; the last CTA to finish
+// (ticket, reset for the next call) builds the levels above those.
+struct TreeLv {
+  uint64_t* lvl[kMaxLevels + 1];
+  uint64_t n[kMaxLevels + 1];
+  int levels;
+};
+__device__ __forceinline__ uint64_t max32(const uint64_t* __restrict__ in, uint64_t n_in, uint64_t o, bool l2) {
+  const uint64_t i0 = o * 32;
+  uint64_t v = 0;
+  if (i0 + 32 <= n_in) {
+    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(in + i0);
+    ulonglong2 x[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = l2 ? __ldcg(p + k) : __ldg(p + k);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      v = x[k].x > v ? x[k].x : v;
+      v = x[k].y > v ? x[k].y : v;
+    }
+  } else {
+    for (uint64_t i = i0; i < n_in; ++i) {
+      const uint64_t w = l2 ? __ldcg(in + i) : __ldg(in + i);
+      v = w > v ? w : v;
+    }
+  }
+  return v;  // (padding = 0, below every key)
+}
+__global__ void __launch_bounds__(256) tree_levels_kernel(const __grid_constant__ TreeLv T, int from,
+                                                          uint32_t* __restrict__ ticket) {
+  __shared__ bool last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t o = (uint64_t)blockIdx.x * 256 + tid;
+  const uint64_t v = o < T.n[from] ? max32(T.lvl[from - 1], T.n[from - 1], o, false) : 0;
+  if (o < T.n[from]) T.lvl[from][o] = v;
+  if (from + 1 <= T.levels) {
+    const uint64_t w = warp_max_u64(v);
+    const uint64_t o1 = (uint64_t)blockIdx.x * 8 + warp;
+    if (lane == 0 && o1 < T.n[from + 1]) T.lvl[from + 1][o1] = w;
+  }
+  if (from + 2 > T.levels) return;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int L = from + 2; L <= T.levels; ++L) {  // (other CTAs' writes: read from L2)
+    for (uint64_t q = tid; q < T.n[L]; q += 256) T.lvl[L][q] = max32(T.lvl[L - 1], T.n[L - 1], q, true);
+    __threadfence_block();
+    __syncthreads();
+  }
+  if (tid == 0) *ticket = 0;
+}
+
 // a3' (pairs mode): levels 1 and 2 of the block-max tree and the prefix
 // maxima of the Slo upper keys, in one read of slo_hi.  With 1024-entry
 // blocks, pmw[i] = max(slo_hi[1024*(i/1024) .. i]) and, after
@@ -532,12 +590,44 @@ __device__ __forceinline__ int skip_levels(const MaxTree& T, int64_t i, uint64_t
 
 static_assert(kCountTile % kRowTile == 0, "count tile holds whole row tiles");
 
+// Rank of x in the sorted a[0, n) by one group of 8 lanes (lanes 8g .. 8g+7
+// of the warp, g = lane / 8): #{a[i] <= x} (upper) or #{a[i] < x}.  An 8-ary
+// search: the 8 lanes probe 8 evenly spaced positions of the current interval
+// and the group's ballot narrows it ~9x per step (log9 n dependent rounds
+// instead of log2 n -- these searches run on latency, with L2 flushed between
+// small calls every round trip is a DRAM miss).  All 32 lanes must call it.
+__device__ __forceinline__ uint64_t group8_rank(const uint64_t* __restrict__ a, uint64_t n, uint64_t x, bool upper,
+                                                int lane) {
+  const int g = lane & 7, sh = lane & ~7;
+  uint64_t lo = 0, hi = n;  // the rank lies in [lo, hi]
+  while (__any_sync(kFull, hi - lo > 8)) {
+    const bool act = hi - lo > 8;
+    const uint64_t p = lo + ((uint64_t)(g + 1) * (hi - lo)) / 9;
+    const bool pr = act && (upper ? a[p] <= x : a[p] < x);
+    const uint32_t c = __popc((__ballot_sync(kFull, pr) >> sh) & 0xffu);  // probes with rank > p
+    if (act) {
+      const uint64_t plo = c ? lo + ((uint64_t)c * (hi - lo)) / 9 + 1 : lo;
+      const uint64_t phi = c < 8 ? lo + ((uint64_t)(c + 1) * (hi - lo)) / 9 : hi;
+      lo = plo;
+      hi = phi;
+    }
+  }
+  const uint64_t p = lo + g;
+  const bool pr = p < hi && (upper ? a[p] <= x : a[p] < x);
+  return lo + __popc((__ballot_sync(kFull, pr) >> sh) & 0xffu);
+}
+
 // Per count tile: r_lo(a_first), r_lo(a_last), r_hi(a_first), r_hi(a_last)
 // (merge-path partition of the sorted updates against Slo and Shi).
-__global__ void __launch_bounds__(256) count_partition_kernel(const uint64_t* __restrict__ ulo_key, uint64_t m,
-                                                              const uint64_t* __restrict__ slo_key,
-                                                              const uint64_t* __restrict__ shi_key, uint64_t n,
-                                                              uint64_t* __restrict__ part) {
+// Few tiles (small calls, latency-bound): one warp per tile, the four
+// searches side by side in groups of 8 lanes (count_partition_kernel);
+// many tiles: one thread per tile, binary searches (count_partition1_kernel,
+// fewer loads in total: c3 25 vs 33 us).
+constexpr uint64_t kPartWarpMaxTiles = 2048;
+__global__ void __launch_bounds__(256) count_partition1_kernel(const uint64_t* __restrict__ ulo_key, uint64_t m,
+                                                               const uint64_t* __restrict__ slo_key,
+                                                               const uint64_t* __restrict__ shi_key, uint64_t n,
+                                                               uint64_t* __restrict__ part) {
   const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t tiles = (m + kCountTile - 1) / kCountTile;
   if (t >= tiles) return;
@@ -547,6 +637,21 @@ __global__ void __launch_bounds__(256) count_partition_kernel(const uint64_t* __
   part[4 * t + 1] = ub(slo_key, 0, n, al);
   part[4 * t + 2] = shi_key ? lb(shi_key, 0, n, af) : 0;  // (walk form: no Shi)
   part[4 * t + 3] = shi_key ? lb(shi_key, 0, n, al) : 0;
+}
+__global__ void __launch_bounds__(256) count_partition_kernel(const uint64_t* __restrict__ ulo_key, uint64_t m,
+                                                              const uint64_t* __restrict__ slo_key,
+                                                              const uint64_t* __restrict__ shi_key, uint64_t n,
+                                                              uint64_t* __restrict__ part) {
+  const uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31, q = lane >> 3;
+  const uint64_t tiles = (m + kCountTile - 1) / kCountTile;
+  if (t >= tiles) return;  // (warp-uniform)
+  const uint64_t j0 = t * kCountTile, j1 = umin64(m, j0 + kCountTile) - 1;
+  const uint64_t x = ulo_key[(q & 1) ? j1 : j0];
+  // groups 0, 1: ub(Slo, a_first / a_last); 2, 3: lb(Shi, ...) (0 without Shi: walk form)
+  const bool up = q < 2;
+  const uint64_t r = group8_rank(up || !shi_key ? slo_key : shi_key, up || shi_key ? n : 0, x, up, lane);
+  if ((lane & 7) == 0) part[4 * t + q] = r;
 }
 
 constexpr int kWalkPad = 256;  // walk form: slo_hi / pmw windows start this far before r_lo(a_first)

@@ -838,6 +838,32 @@ __global__ void __launch_bounds__(256) span_bounds_kernel(const uint64_t* __rest
   bounds[sp] = lo;
 }
 
+// The same bounds when the sort took a single multisplit pass (bucket ids <
+// 256): the digit starts of that pass ARE the bucket starts, so the first
+// bucket boundary at or after s*span is the smallest start >= s*span -- a
+// search over 256 cached values instead of a gallop over the sorted keys.
+__global__ void __launch_bounds__(256) span_bounds_hist_kernel(const uint32_t* __restrict__ starts, uint32_t nb,
+                                                               uint64_t n, uint32_t spans, uint32_t span,
+                                                               uint64_t* __restrict__ bounds) {
+  __shared__ uint32_t st[kRadix];
+  for (uint32_t b = threadIdx.x; b < kRadix; b += blockDim.x) st[b] = b < nb ? starts[b] : (uint32_t)n;
+  __syncthreads();
+  for (uint32_t sp = blockIdx.x * blockDim.x + threadIdx.x; sp <= spans; sp += gridDim.x * blockDim.x) {
+    const uint64_t p = (uint64_t)sp * span;
+    if (sp == 0 || p >= n) {
+      bounds[sp] = sp == 0 ? 0 : n;
+      continue;
+    }
+    uint32_t lo = 0, hi = kRadix;  // first bucket whose start is >= p (starts are non-decreasing)
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (st[mid] >= p) hi = mid;
+      else lo = mid + 1;
+    }
+    bounds[sp] = lo < kRadix ? st[lo] : n;
+  }
+}
+
 // CTA c sorts the whole buckets starting in [c*C::SPAN, (c+1)*C::SPAN), i.e. in
 // [bounds[c], bounds[c+1]) (span_bounds_kernel), in groups of consecutive
 // buckets holding <= C::CAP records in smem.  A
