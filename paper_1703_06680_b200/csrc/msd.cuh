@@ -540,7 +540,7 @@ struct LocalSmem {  // keys only: payloads follow the permutation through the ke
 #if DDM_LS_RANK
   uint16_t perm2[C::CAP];  // final order (sorted position -> staged index)
 #endif
-  uint64_t red[2 * (C::T / 32)];
+  uint64_t red[2 * (C::T / 32) + 2];
   uint32_t flag;
   uint64_t bound[1];  // prev_boundary's reduction slot
 };
@@ -595,12 +595,29 @@ __device__ void local_sort_group(LocalSmem<C, V64, V32>& S, const uint64_t* __re
   }
   if (lane == 0) { S.red[warp] = kmin; S.red[(C::T / 32) + warp] = kmax; }
   __syncthreads();
-  kmin = ~0ull;
-  kmax = 0;
+  if constexpr (C::T / 32 > 8) {  // many warps: warp 0 combines, everyone reads two words
+    if (warp == 0) {
+      kmin = lane < C::T / 32 ? S.red[lane] : ~0ull;
+      kmax = lane < C::T / 32 ? S.red[(C::T / 32) + lane] : 0ull;
 #pragma unroll
-  for (int w = 0; w < (C::T / 32); ++w) {
-    kmin = S.red[w] < kmin ? S.red[w] : kmin;
-    kmax = S.red[(C::T / 32) + w] > kmax ? S.red[(C::T / 32) + w] : kmax;
+      for (int o = 16; o; o >>= 1) {
+        const uint64_t x = __shfl_xor_sync(kFull, kmin, o), y = __shfl_xor_sync(kFull, kmax, o);
+        kmin = x < kmin ? x : kmin;
+        kmax = y > kmax ? y : kmax;
+      }
+      if (lane == 0) { S.red[2 * (C::T / 32)] = kmin; S.red[2 * (C::T / 32) + 1] = kmax; }
+    }
+    __syncthreads();
+    kmin = S.red[2 * (C::T / 32)];
+    kmax = S.red[2 * (C::T / 32) + 1];
+  } else {
+    kmin = ~0ull;
+    kmax = 0;
+#pragma unroll
+    for (int w = 0; w < (C::T / 32); ++w) {
+      kmin = S.red[w] < kmin ? S.red[w] : kmin;
+      kmax = S.red[(C::T / 32) + w] > kmax ? S.red[(C::T / 32) + w] : kmax;
+    }
   }
   // smallest shift with (kmax - kmin) >> sh < C::BINS
   const uint64_t range = kmax - kmin;
