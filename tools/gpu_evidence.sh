@@ -3,7 +3,7 @@
 # bench's roofline.traffic), ncu full captures of the dominant kernels, then the bench
 # lines of every config, the reference arm, the count-mode alpha sweep and the
 # multi-GPU path on one GPU (gloo).   usage: bash tools/gpu_evidence.sh TAG
-tag=${1:-r02}
+tag=${1:-r02d}
 o=gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > $o/${tag}_build.log 2>&1
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem,power.draw --format=csv > $o/${tag}_smi.csv
@@ -19,8 +19,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:msd_
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:local_sort_kernel --launch-skip 3 --launch-count 1 -o $o/${tag}_local_sort python tools/profile_once.py c3 > $o/${tag}_ncu2.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:count_kernel --launch-skip 1 --launch-count 1 -o $o/${tag}_count python tools/profile_once.py c3 > $o/${tag}_ncu3.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:emit_tile --launch-skip 0 --launch-count 1 -o $o/${tag}_emit python tools/profile_once.py c3 > $o/${tag}_ncu4.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:dd_tile_kernel --launch-skip 1 --launch-count 1 -o $o/${tag}_dd_stage python tools/profile_once.py c4 > $o/${tag}_ncu5.log 2>&1
-timeout 900 ncu --metrics smsp__inst_executed.sum,gpu__time_duration.sum --clock-control none -k regex:dd_tile_kernel --csv --log-file $o/${tag}_dd_inst.csv python tools/profile_once.py c4 > $o/${tag}_ncu6.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:rows_kernel --launch-skip 1 --launch-count 1 -o $o/${tag}_dd_stage python tools/profile_once.py c4 > $o/${tag}_ncu5.log 2>&1
+timeout 900 ncu --metrics smsp__inst_executed.sum,gpu__time_duration.sum --clock-control none -k regex:rows_kernel --csv --log-file $o/${tag}_dd_inst.csv python tools/profile_once.py c4 > $o/${tag}_ncu6.log 2>&1
 unset DDM_SERIAL
 python tools/inst_json.py $o/${tag}_dd_inst.csv $o/ncu_inst.json > $o/${tag}_inst.log 2>&1
 cp $o/ncu_traffic.json profiles/ncu_traffic.json
