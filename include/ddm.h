@@ -67,7 +67,7 @@ typedef enum {
                                       n > DDM_MAX_REGIONS, misalignment */
     DDM_ERR_NONFINITE = 2,         /* a NaN or ±inf coordinate */
     DDM_ERR_INVERTED_INTERVAL = 3, /* lo > hi in some dimension */
-    DDM_ERR_CAPACITY = 4,          /* capacity < K; *count_out = K, nothing written past capacity */
+    DDM_ERR_CAPACITY = 4,          /* capacity < K; *count_out = K, no pair written */
     DDM_ERR_WORKSPACE = 5,         /* ws_bytes (or index_bytes) too small */
     DDM_ERR_CUDA = 6               /* CUDA launch/runtime failure; see ddm_last_cuda_error() */
 } ddm_status;
@@ -106,12 +106,6 @@ typedef struct {
 #define DDM_EMIT_FORCE_THREAD (1u << 8) /* one thread per update row */
 #define DDM_EMIT_FORCE_WARP (1u << 9)   /* one warp per update row, global scan */
 #define DDM_EMIT_FORCE_CHUNK (1u << 10) /* chunk-start sets staged in smem */
-/* d = 1 pairs calls with walk-form counts emit, by default, in the same
- * kernel that counts (counts, offsets and pairs per 2048-row tile, one
- * launch before the call's host read; tiles too dense for it are re-emitted
- * by the separate passes).  This flag forces the separate count, offset-scan
- * and emit passes (byte-identical output). */
-#define DDM_EMIT_UNFUSED (1u << 11)
 /* Sort selection: by default the value-bucketed MSD sort (payload carried,
  * no gathers) runs and falls back to the LSB radix sort + gathers if some
  * bucket exceeds shared memory; this flag forces the LSB path.  Output is
@@ -167,9 +161,8 @@ ddm_status ddm_match_count(const ddm_regions *regions, uint64_t *count_out, void
 
 /* List mode: writes the K pairs to pairs[0..K) (device) and K to *count_out
  * (host).  If capacity < K returns DDM_ERR_CAPACITY with *count_out = K and
- * writes nothing at or past `capacity` (the fused d = 1 emission may have
- * written rows that fit; call with capacity 0 to size the buffer).  Invalid
- * inputs are reported with no pair written. */
+ * writes no pair (call with capacity 0 to size the buffer).  Validation
+ * errors are reported before any pair is written. */
 ddm_status ddm_match_pairs(const ddm_regions *regions, ddm_pair *pairs, uint64_t capacity,
                            uint64_t *count_out, uint32_t flags, void *ws, size_t ws_bytes,
                            cudaStream_t stream);

@@ -93,14 +93,6 @@ inline int prof_begin(cudaStream_t st) {
   if (e >= 0) cudaEventRecord(g_prof.ev[e], st);
   return e;
 }
-// add bytes known only after the launch (the pairs of a fused count + emit) to
-// the latest record of that kernel class
-inline void prof_add_bytes(const char* name, double bytes) {
-  if (!g_prof.on) return;
-  std::lock_guard<std::mutex> lk(g_prof_mu);
-  for (auto it = g_prof.recs.rbegin(); it != g_prof.recs.rend(); ++it)
-    if (!strcmp(it->name, name)) { it->bytes += bytes; return; }
-}
 inline void prof_end(const char* name, double bytes, cudaStream_t st, int e0) {
   if (e0 < 0) return;
   std::lock_guard<std::mutex> lk(g_prof_mu);
@@ -413,7 +405,7 @@ struct Misc {  // device-side results read back with one copy
   uint32_t err;
   uint32_t overflow;  // an MSD bucket exceeded shared memory: redo with the LSB sort
   uint32_t dd_ovf;    // d > 1 row-indexed stage pass: some tile's staging slot overflowed
-  uint32_t redo;      // fused count + emit: a tile too dense for it, the unfused passes must emit
+  uint32_t pad_;
 };
 
 constexpr ddm_status kRetryLSB = (ddm_status)100;  // internal
@@ -432,7 +424,6 @@ struct MatchWs {
   uint64_t* tile_sum;  // per 256-row tile count sums
   uint64_t* tile_off;  // their exclusive scan: output offset of each row tile
   uint64_t* scan_status;
-  uint64_t* fstatus;   // fused count + emit: per count tile look-back words + the tile counter
   uint64_t* part;
   uint2* dd_stage;      // d > 1 stage pass: per-tile staged hits
   double* udims;        // d > 1: dims 1..d-1 of the updates in Ulo order
@@ -455,7 +446,6 @@ MatchWs match_layout(uint32_t d, uint64_t n_sub, uint64_t m, void* base, bool in
   W.probe = c.take<double>(DDM_MAX_DIMS);
   W.scan_status = c.take<uint64_t>(rtiles / (match::kScanThreads * match::kScanItems) + 2);
   W.part = c.take<uint64_t>(4 * (m / match::kCountTile + 2));
-  W.fstatus = c.take<uint64_t>(m / match::kCountTile + 3);
   W.tile_sum = c.take<uint64_t>(rtiles);
   W.tile_off = c.take<uint64_t>(rtiles);
   W.ulo_key = c.take<uint64_t>(m);
@@ -534,8 +524,6 @@ void init_attrs_once() {
   cudaFuncSetAttribute(ev::segment_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ev::Smem));
   cudaFuncSetAttribute(match::emit_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(match::ChunkSmem));
-  cudaFuncSetAttribute(match::count_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(match::FusedSmem));
   cudaFuncSetAttribute(match::emit_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(match::EmitTileSmem));
   cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1062,23 +1050,14 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
   // pass runs only if a tile overflows its staging slot (its fallback needs
   // the per-row ranks)
   const match::CountWalk CW{I.slo_hi, I.pmw, I.pmb, I.nb, tree_of(I)};
-  // sparse d = 1 pairs calls with walk-form counts: counts, offsets and the
-  // emission in one kernel (match::count_emit_kernel), launched before the
-  // sync; the host only checks K afterwards
-  const bool fused = d == 1 && q.walk && q.pairs && !q.chunk && use_msd && !q.boxes_only &&
-                     !(q.flags & (DDM_EMIT_FORCE_THREAD | DDM_EMIT_FORCE_WARP | DDM_EMIT_FORCE_CHUNK |
-                                  DDM_EMIT_UNFUSED));
-  auto partition = [&](cudaStream_t cs) -> ddm_status {
+  auto count_pass = [&](cudaStream_t cs) -> ddm_status {
     if (ctiles <= match::kPartWarpMaxTiles)
       DDM_LAUNCH("count_partition", 0, cs, match::count_partition_kernel<<<(unsigned)((ctiles * 32 + 255) / 256), 256, 0, cs>>>(
           W.ulo_key, m, I.slo_key, q.walk ? nullptr : I.shi_key, n, W.part));
     else
       DDM_LAUNCH("count_partition", 0, cs, match::count_partition1_kernel<<<(unsigned)((ctiles + 255) / 256), 256, 0, cs>>>(
           W.ulo_key, m, I.slo_key, q.walk ? nullptr : I.shi_key, n, W.part));
-    return check_launch();
-  };
-  auto count_pass = [&](cudaStream_t cs) -> ddm_status {
-    DDM_TRY(partition(cs));
+    DDM_TRY(check_launch());
     const double cbytes = (use_msd ? 28.0 : 48.0) * m + (q.walk ? 24.0 : 16.0) * n;
     if (q.walk)
       DDM_LAUNCH("count", cbytes, cs, match::count_kernel<true><<<(unsigned)ctiles, match::kCountThreads, match::count_smem_bytes(true), cs>>>(
@@ -1090,36 +1069,8 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
           W.cnt0, W.tile_sum, CW));
     return check_launch();
   };
-  if (pre && fused) {
-    DDM_TRY(partition(st));
-    DDM_CUDA(cudaMemsetAsync(W.fstatus, 0, sizeof(uint64_t) * (ctiles + 1), st));
-    match::FusedArgs F{};
-    F.ulo_key = W.ulo_key;
-    F.uhi = W.uhi;
-    F.ulo_id = W.ulo_id;
-    F.m = m;
-    F.slo_key = I.slo_key;
-    F.slo_id = I.slo_id;
-    F.n = n;
-    F.part = W.part;
-    F.C = CW;
-    F.upd_map = q.upd_map;
-    F.sub_map = q.sub_map;
-    F.pairs = reinterpret_cast<uint2*>(q.pairs);
-    F.capacity = q.capacity;
-    F.status = W.fstatus;
-    F.k_out = &W.misc->K;
-    F.err = &W.misc->err;
-    F.abort_flag = &W.misc->overflow;
-    F.redo = &W.misc->redo;
-    // (+ 8 B per pair, added once K is known)
-    DDM_LAUNCH("count_emit", 20.0 * m + 28.0 * n, st, match::count_emit_kernel<<<(unsigned)ctiles, match::kCountThreads,
-                                                                                 sizeof(match::FusedSmem), st>>>(F));
-    DDM_TRY(check_launch());
-  } else {
-    if (pre && !q.boxes_only) DDM_TRY(count_pass(st));
-  }
-  if (pre && d == 1 && !fused) {
+  if (pre && !q.boxes_only) DDM_TRY(count_pass(st));
+  if (pre && d == 1) {
     DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (stiles + 1), st));
     DDM_LAUNCH("scan", 16.0 * rtiles, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
         W.tile_sum, rtiles, W.tile_off, W.scan_status, &W.misc->K));
@@ -1277,19 +1228,8 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
     return check_launch();
   }
   if (!q.pairs) return DDM_OK;
-  if (fused) prof_add_bytes("count_emit", 8.0 * (double)h.K);
   if (h.K > q.capacity) return DDM_ERR_CAPACITY;
   if (h.K == 0) return DDM_OK;
-  if (fused) {
-    if (!h.redo) return DDM_OK;  // every tile emitted its rows
-    // some tile was too dense for the fused emission: the unfused passes
-    // (their dense emitters share long rows between threads) rewrite it all
-    DDM_TRY(count_pass(st));
-    DDM_CUDA(cudaMemsetAsync(W.scan_status, 0, sizeof(uint64_t) * (stiles + 1), st));
-    DDM_LAUNCH("scan", 16.0 * rtiles, st, match::scan_u64_kernel<<<stiles, match::kScanThreads, 0, st>>>(
-        W.tile_sum, rtiles, W.tile_off, W.scan_status, &W.misc->K));
-    DDM_TRY(check_launch());
-  }
   A.pairs = reinterpret_cast<uint2*>(q.pairs);
   if (d > 1 && !per_row) {
     D.pairs = A.pairs;

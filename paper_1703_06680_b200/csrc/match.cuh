@@ -1389,221 +1389,6 @@ __global__ void __launch_bounds__(kEmitThreads, DDM_EMIT_MINB) emit_tile_kernel(
   }
 }
 
-// ------------------------------------------------------------ fused count + offsets + emit (a4 + a5 + a7, d = 1)
-//
-// Sparse d = 1 pairs calls with walk-form counts: ONE kernel does, per
-// 2048-row tile, what count_kernel<true>, scan_u64_kernel and
-// emit_tile_kernel do in three launches -- the Slo key / slo_hi / prefix-max
-// / slo_id windows are staged once, the rows' r_lo, r_b and |Stab(a)| are
-// computed (a4, the walk form), the tile's output offset comes from a
-// decoupled look-back over the tile sums (a5; tiles are claimed from an
-// atomic counter, so a tile only waits on tiles that are running or done),
-// and the rows are emitted from the same windows (a7: the stab part Stab(a)
-// walked backwards from r_lo - 1, then the range Slo[r_lo, r_b)).  Nothing
-// per row goes through HBM: no r_lo / r_b / cnt arrays, no tile sums.
-// The output is byte-identical to the unfused path (same rows, same order).
-// A tile writes nothing when the call must not write (validation error, MSD
-// bucket overflow: the host then redoes the call) or when its pairs would
-// pass `capacity`; a tile denser than the thread-per-row emission suits (more
-// than kFusedTileMax pairs, or a row of more than kFusedRowMax) sets *redo
-// and writes nothing -- the host then runs the unfused passes (whose dense
-// emitters share the work of long rows), with K already known.
-constexpr uint64_t kFusedTileMax = 16 * kCountTile;
-constexpr uint32_t kFusedRowMax = 1024;
-
-struct FusedArgs {
-  const uint64_t* ulo_key;
-  const uint64_t* uhi;      // upper keys in Ulo order (MSD sort payload)
-  const uint32_t* ulo_id;
-  uint64_t m;
-  const uint64_t* slo_key;
-  const uint32_t* slo_id;
-  uint64_t n;
-  const uint64_t* part;     // per tile r_lo(a_first), r_lo(a_last) (count_partition)
-  CountWalk C;
-  const uint32_t* upd_map;  // optional global ids
-  const uint32_t* sub_map;
-  uint2* pairs;
-  uint64_t capacity;
-  uint64_t* status;         // tiles + 1 zeroed words: look-back status, then the tile counter
-  uint64_t* k_out;          // K (written by the last tile)
-  const uint32_t* err;      // validation error word: write nothing when set
-  const uint32_t* abort_flag;  // MSD bucket overflow: write nothing when set
-  uint32_t* redo;           // set by a tile too dense for this kernel's emission
-};
-
-struct FusedSmem {
-  uint64_t bar;
-  uint64_t excl;
-  uint64_t pbw[8];
-  uint64_t tmp[kCountThreads / 32 + 1];
-  uint32_t tile;
-  uint32_t rmax;
-  alignas(16) uint64_t ws[kCountWin + 2];  // Slo keys from r_lo(a_first)
-  alignas(16) uint64_t wh[kCountWin + 2];  // slo_hi from r_lo(a_first) - kWalkPad
-  alignas(16) uint64_t wp[kCountWin + 2];  // pmw, same positions
-  alignas(16) uint32_t wi[kCountWin + 4];  // slo_id, same positions
-};
-
-#ifndef DDM_FUSED_MINB
-#define DDM_FUSED_MINB 3
-#endif
-__global__ void __launch_bounds__(kCountThreads, DDM_FUSED_MINB) count_emit_kernel(const __grid_constant__ FusedArgs A) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  FusedSmem& S = *reinterpret_cast<FusedSmem*>(smem_raw);
-  const int tid = threadIdx.x, lane = tid & 31;
-  const uint32_t tiles = gridDim.x;
-  if (tid == 0) {
-    S.tile = (uint32_t)atomicAdd((unsigned long long*)(A.status + tiles), 1ull);
-    S.rmax = 0;
-  }
-  __syncthreads();
-  const uint32_t tile = S.tile;
-  const uint64_t m = A.m, n = A.n;
-  const uint64_t j0 = (uint64_t)tile * kCountTile;
-  const uint64_t jn = umin64(kCountTile, m - j0);
-  const uint64_t p0 = A.part[4 * tile + 0], p1 = A.part[4 * tile + 1];
-  const uint64_t t0 = (uint64_t)tid * kCountItems;
-  const int ni = t0 < jn ? (int)umin64(kCountItems, jn - t0) : 0;
-  const uint64_t j = j0 + t0;
-  uint64_t a[kCountItems], b[kCountItems];
-  uint32_t lid[kCountItems];
-  if (ni == kCountItems) {
-    const ulonglong2* pa = reinterpret_cast<const ulonglong2*>(A.ulo_key + j);
-    const ulonglong2* pb = reinterpret_cast<const ulonglong2*>(A.uhi + j);
-#pragma unroll
-    for (int i = 0; i < kCountItems / 2; ++i) {
-      const ulonglong2 va = __ldcs(pa + i), vb = __ldcs(pb + i);
-      a[2 * i] = va.x; a[2 * i + 1] = va.y;
-      b[2 * i] = vb.x; b[2 * i + 1] = vb.y;
-    }
-    const uint4 vi = __ldcs(reinterpret_cast<const uint4*>(A.ulo_id + j));
-    lid[0] = vi.x; lid[1] = vi.y; lid[2] = vi.z; lid[3] = vi.w;
-  } else {
-#pragma unroll
-    for (int i = 0; i < kCountItems; ++i) {
-      a[i] = i < ni ? A.ulo_key[j + i] : 0;
-      b[i] = i < ni ? A.uhi[j + i] : 0;
-      lid[i] = i < ni ? A.ulo_id[j + i] : 0;
-    }
-  }
-  static_assert(kCountItems == 4, "the id load above takes 4 rows");
-  const uint32_t ls = (uint32_t)umin64(umin64(kCountWin, p1 - p0 + kCountExt), n - p0);
-  const uint64_t q0 = p0 > kWalkPad ? p0 - kWalkPad : 0;
-  const uint32_t lh = (uint32_t)umin64(kCountWin, n - q0);
-  const uint32_t os = (uint32_t)(p0 & 1), oh = (uint32_t)(q0 & 1), oi = (uint32_t)(q0 & 3);
-  const uint64_t* W0 = S.ws + os;
-  const uint64_t* H0 = S.wh + oh;
-  const uint64_t* P0 = S.wp + oh;
-  const uint32_t* I0 = S.wi + oi;
-  if (tid < 8) {
-    const uint64_t bb = (q0 >> 10) + tid;
-    if (bb < A.C.nb) S.pbw[tid] = __ldg(A.C.pmb + bb);
-  }
-  if (tid == 0) {
-    mbar_init(&S.bar, 1);
-    const uint32_t bs = ((ls + os + 1) & ~1u) * 8, bh = ((lh + oh + 1) & ~1u) * 8, bi = ((lh + oi + 3) & ~3u) * 4;
-    mbar_expect_tx(&S.bar, bs + 2 * bh + bi);
-    if (bs) bulk_g2s(S.ws, A.slo_key + (p0 - os), bs, &S.bar);
-    if (bh) {
-      bulk_g2s(S.wh, A.C.slo_hi + (q0 - oh), bh, &S.bar);
-      bulk_g2s(S.wp, A.C.pmw + (q0 - oh), bh, &S.bar);
-      bulk_g2s(S.wi, A.slo_id + (q0 - oi), bi, &S.bar);
-    }
-  }
-  __syncthreads();  // the barrier is initialised before anyone waits on it
-  mbar_wait(&S.bar, 0);
-
-  // a4: r_lo, r_b and the walk-form |Stab(a)| (as count_kernel<true>)
-  uint32_t cnt[kCountItems], ol[kCountItems], ob[kCountItems];
-#pragma unroll
-  for (int i = 0; i < kCountItems; ++i) cnt[i] = ol[i] = ob[i] = 0;
-  if (ni > 0) {
-    uint64_t rl = advance<true>(W0, p0, ls, A.slo_key, n, p0 + ub_interp(W0, ls, a[0]), a[0]);
-    uint64_t rb = rl;
-#pragma unroll
-    for (int i = 0; i < kCountItems; ++i) {
-      if (i < ni) {
-        if (i) rl = advance<true>(W0, p0, ls, A.slo_key, n, rl, a[i]);
-        const uint64_t start = (i && b[i] >= b[i - 1] && rb > rl) ? rb : rl;
-        rb = advance<true>(W0, p0, ls, A.slo_key, n, start, b[i]);
-        ol[i] = (uint32_t)rl;
-        ob[i] = (uint32_t)rb;
-        cnt[i] = (uint32_t)(rb - rl);
-      }
-    }
-    int64_t pos[kCountItems];
-    unsigned act = 0;
-#pragma unroll
-    for (int i = 0; i < kCountItems; ++i) {
-      pos[i] = (int64_t)ol[i] - 1;
-      if (i < ni) act |= 1u << i;
-    }
-    while (act) {
-#pragma unroll
-      for (int i = 0; i < kCountItems; ++i)
-        if ((act >> i) & 1u)
-          if (!walk_step(H0, P0, S.pbw, q0, lh, A.C, pos[i], a[i], cnt[i])) act &= ~(1u << i);
-    }
-  }
-  // a5: the tile's offset -- block scan of the rows, look-back over the tiles
-  uint64_t mine = 0;
-  uint32_t rmax = 0;
-#pragma unroll
-  for (int i = 0; i < kCountItems; ++i) {
-    mine += cnt[i];
-    rmax = cnt[i] > rmax ? cnt[i] : rmax;
-  }
-  rmax = __reduce_max_sync(kFull, rmax);
-  if (lane == 0 && rmax > kFusedRowMax) atomicMax(&S.rmax, rmax);
-  uint64_t agg;
-  const uint64_t texcl = block_excl_scan<kCountThreads>(mine, S.tmp, &agg);
-  if (tid < 32) {
-    const uint64_t e = lookback_warp_u64(A.status, tile, agg);
-    if (tid == 0) {
-      S.excl = e;
-      if (tile == tiles - 1) *A.k_out = e + agg;
-    }
-  }
-  __syncthreads();
-  const uint64_t excl = S.excl;
-  if (*A.err || (A.abort_flag && *A.abort_flag) || excl + agg > A.capacity) return;
-  if (agg > kFusedTileMax || S.rmax > kFusedRowMax) {
-    if (tid == 0) atomicOr(A.redo, 1u);
-    return;
-  }
-  // a7: emit from the staged windows (positions outside them: global memory
-  // with the block-max skips), identical to emit_tile_kernel's rows
-  auto hi_at = [&](uint64_t i) -> uint64_t {
-    const uint64_t k = i - q0;
-    return (i >= q0 && k < lh) ? H0[k] : A.C.slo_hi[i];
-  };
-  auto id_at = [&](uint64_t i) -> uint32_t {
-    const uint64_t k = i - q0;
-    return sub_out(A.sub_map, (i >= q0 && k < lh) ? I0[k] : A.slo_id[i]);
-  };
-  uint64_t o = excl + texcl;
-#pragma unroll
-  for (int r = 0; r < kCountItems; ++r) {
-    if (r >= ni) break;
-    const uint32_t uid = A.upd_map ? A.upd_map[lid[r]] : lid[r];
-    const uint32_t stab = cnt[r] - (ob[r] - ol[r]);
-    uint2* row = A.pairs + o;
-    uint32_t rem = stab;
-    int64_t i = (int64_t)ol[r] - 1;
-    while (rem) {
-      if ((uint64_t)i < q0 && (i & 31) == 31) {
-        const int L = skip_levels(A.C.T, i, a[r]);
-        if (L) { i -= (int64_t)1 << (5 * L); continue; }
-      }
-      if (hi_at((uint64_t)i) >= a[r]) row[--rem] = make_uint2(id_at((uint64_t)i), uid);
-      --i;
-    }
-    for (uint32_t k = ol[r]; k < ob[r]; ++k) row[stab + (k - ol[r])] = make_uint2(id_at(k), uid);
-    o += cnt[r];
-  }
-}
-
 // ------------------------------------------------------------ few dense rows (d = 1)
 //
 // When a d = 1 output has few rows with very many pairs each (few updates

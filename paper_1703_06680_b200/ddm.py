@@ -24,7 +24,6 @@ DDM_EMIT_AUTO = 0
 DDM_EMIT_FORCE_THREAD = 1 << 8
 DDM_EMIT_FORCE_WARP = 1 << 9
 DDM_EMIT_FORCE_CHUNK = 1 << 10
-DDM_EMIT_UNFUSED = 1 << 11
 DDM_SORT_LSB = 1 << 12
 DDM_COUNT_RANKS = 1 << 13
 DDM_COUNT_WALK = 1 << 14

@@ -18,8 +18,7 @@ from tests.helpers import arrays, cuda, gpu_args, oracle_list_by_cells, raw_word
 EMIT_FLAGS = [ddm.DDM_EMIT_AUTO, ddm.DDM_EMIT_FORCE_THREAD, ddm.DDM_EMIT_FORCE_WARP, ddm.DDM_EMIT_FORCE_CHUNK,
               ddm.DDM_SORT_LSB, ddm.DDM_SORT_LSB | ddm.DDM_EMIT_FORCE_CHUNK,
               ddm.DDM_COUNT_WALK, ddm.DDM_COUNT_WALK | ddm.DDM_EMIT_FORCE_CHUNK,
-              ddm.DDM_COUNT_WALK | ddm.DDM_SORT_LSB, ddm.DDM_COUNT_RANKS,
-              ddm.DDM_COUNT_WALK | ddm.DDM_EMIT_UNFUSED]
+              ddm.DDM_COUNT_WALK | ddm.DDM_SORT_LSB, ddm.DDM_COUNT_RANKS]
 # d > 1: both tiled filter forms at any size (row-indexed 4096-row tiles,
 # chunk-indexed 1024-row tiles), with the MSD and the LSB sorts
 DD_FLAGS = [ddm.DDM_DD_FORCE_ROWS, ddm.DDM_DD_FORCE_CHUNKS, ddm.DDM_DD_FORCE_ROWS | ddm.DDM_SORT_LSB]
@@ -641,43 +640,6 @@ def test_walk_capacity_and_graph_replay(orc):
         assert s_ == 0 and K.value == K0
         assert np.array_equal(words_of(out[:K0]), ref)
         assert bool((out[K0:] == -7).all())
-
-
-def test_fused_count_emit_dense_tiles_and_long_rows(orc):
-    """Fused count + offsets + emit (walk form, d = 1): tiles above the fused
-    kernel's density limits (16 pairs per row on average, 1024 in one row)
-    hand the emission to the separate passes; sparse, dense and mixed inputs
-    all give the oracle's set and the unfused passes' exact bytes."""
-    cases = []
-    for l, seed in ((1.0, 41), (200.0, 42)):  # sparse: every tile fused; ~80 pairs per row: every tile redone
-        w = wl.uniform(20_000, 20_000, 1e5, l, 1, seed=seed)
-        cases.append((w.sub_lo, w.sub_hi, w.upd_lo, w.upd_hi))
-    w = wl.uniform(20_000, 20_000, 1e5, 1.0, 1, seed=43)  # one update row of ~6000 pairs in a sparse tile
-    ul, uh = w.upd_lo.copy(), w.upd_hi.copy()
-    ul[0, 123], uh[0, 123] = 2e4, 5e4
-    cases.append((w.sub_lo, w.sub_hi, ul, uh))
-    for c in cases:
-        check_against(orc, *c, flags=[ddm.DDM_COUNT_WALK, ddm.DDM_COUNT_WALK | ddm.DDM_EMIT_UNFUSED,
-                                       ddm.DDM_COUNT_WALK | ddm.DDM_EMIT_FORCE_WARP])
-
-
-def test_fused_count_emit_errors_write_nothing():
-    """A validation error found by the sort passes stops the fused kernel's
-    emission: the error is reported and the pair buffer is untouched."""
-    import ctypes
-    L = ddm.load()
-    x = np.linspace(0, 1e4, 5000)
-    y = x.copy()
-    y[1234] = np.nan
-    g = [cuda(a[None]) for a in (y, x + 1, x, x + 1)]
-    r, keep = ddm.regions(*g)
-    ws = torch.empty(L.ddm_workspace_bytes(1, 5000, 5000, 1), dtype=torch.uint8, device="cuda")
-    out = torch.full((20_000, 2), -7, dtype=torch.int32, device="cuda")
-    K = ctypes.c_uint64(0)
-    st = L.ddm_match_pairs(ctypes.byref(r), out.data_ptr(), 20_000, ctypes.byref(K), ddm.DDM_COUNT_WALK,
-                           ws.data_ptr(), ws.numel(), torch.cuda.current_stream().cuda_stream)
-    torch.cuda.synchronize()
-    assert st == 2 and bool((out == -7).all())
 
 
 def test_capacity_dd_never_writes_past_capacity(orc):
