@@ -1464,11 +1464,17 @@ __global__ void __launch_bounds__(256) emit_split_kernel(const __grid_constant__
 constexpr int kChunkSlice = 1280;
 constexpr int kChunkAct = 512;
 
+struct ChunkRow {  // one row's data, loaded once per tile (coalesced) for the warp rows
+  uint64_t a;
+  uint32_t rl, rb, cnt, uid;
+};
+
 struct ChunkSmem {
   uint64_t shi[kChunkSlice];
   uint64_t ahi[kChunkAct];
   uint32_t sid[kChunkSlice];
   uint32_t aid[kChunkAct];
+  ChunkRow row[kRowTile];
   RowSmem R;
   uint32_t nact;
   uint32_t slen;
@@ -1484,13 +1490,12 @@ __device__ __forceinline__ uint32_t c_id(const ChunkSmem& S, const EmitArgs& A, 
   return k < S.slen ? S.sid[k] : sub_out(A.sub_map, A.slo_id[i]);
 }
 
-__device__ __forceinline__ void chunk_row_thread(const ChunkSmem& S, const EmitArgs& A, uint64_t j, uint64_t o,
+__device__ __forceinline__ void chunk_row_thread(const ChunkSmem& S, const EmitArgs& A, const ChunkRow& R, uint64_t o,
                                                  uint64_t rl0) {
-  const uint64_t a = A.ulo_key[j];
-  const uint32_t lid = A.ulo_id[j];
-  const uint32_t uid = A.upd_map ? A.upd_map[lid] : lid;
-  const uint64_t rl = A.r_lo[j], rb = A.r_b[j];
-  const uint32_t stab = (uint32_t)(A.cnt[j] - (rb - rl));
+  const uint64_t a = R.a;
+  const uint32_t uid = R.uid;
+  const uint64_t rl = R.rl, rb = R.rb;
+  const uint32_t stab = (uint32_t)(R.cnt - (rb - rl));
   // members of A_t still alive at a (ascending Slo order)
   uint32_t w = 0;
   for (uint32_t k = 0; k < S.nact && w < stab; ++k)
@@ -1504,13 +1509,12 @@ __device__ __forceinline__ void chunk_row_thread(const ChunkSmem& S, const EmitA
   for (uint64_t i = rl; i < rb; ++i) A.pairs[o + stab + (i - rl)] = make_uint2(c_id(S, A, rl0, i), uid);
 }
 
-__device__ __forceinline__ void chunk_row_warp(const ChunkSmem& S, const EmitArgs& A, uint64_t j, uint64_t o,
+__device__ __forceinline__ void chunk_row_warp(const ChunkSmem& S, const EmitArgs& A, const ChunkRow& R, uint64_t o,
                                                uint64_t rl0, int lane) {
-  const uint64_t a = A.ulo_key[j];
-  const uint32_t lid = A.ulo_id[j];
-  const uint32_t uid = A.upd_map ? A.upd_map[lid] : lid;
-  const uint64_t rl = A.r_lo[j], rb = A.r_b[j];
-  const uint32_t stab = (uint32_t)(A.cnt[j] - (rb - rl));
+  const uint64_t a = R.a;
+  const uint32_t uid = R.uid;
+  const uint64_t rl = R.rl, rb = R.rb;
+  const uint32_t stab = (uint32_t)(R.cnt - (rb - rl));
   uint2* const row = A.pairs + o;  // this row's output
   uint32_t w = 0;
   const uint32_t nact = S.nact;
@@ -1626,6 +1630,16 @@ __global__ void __launch_bounds__(kRowTile) emit_chunk_kernel(const __grid_const
     S.slen = slen;
     S.nact = nact;
   }
+  const uint64_t j = j0 + tid;
+  ChunkRow mine{};
+  if (fits && j < A.m) {  // every row's data once, coalesced (the warp rows read it from smem)
+    mine.a = A.ulo_key[j];
+    const uint32_t lid = A.ulo_id[j];
+    mine.uid = A.upd_map ? A.upd_map[lid] : lid;
+    mine.rl = A.r_lo[j];
+    mine.rb = A.r_b[j];
+    mine.cnt = A.cnt[j];
+  }
   if (warp == 0) {
     if (fits)  // warp 0 walks Slo backwards from r_lo(x_t) with block-max skips
       walk_chunk_start(A, (int64_t)rl0, x, nact, lane, [&](uint32_t pos, uint64_t h, uint32_t id) {
@@ -1638,8 +1652,8 @@ __global__ void __launch_bounds__(kRowTile) emit_chunk_kernel(const __grid_const
       S.sid[k] = sub_out(A.sub_map, __ldcs(A.slo_id + rl0 + k));
     }
   }
+  if (fits && j < A.m) S.row[tid] = mine;
   __syncthreads();
-  const uint64_t j = j0 + tid;
   if (!fits) {  // chunk-start set too large for shared memory: per-row global walks
     if (j < A.m) {
       const uint32_t c0 = A.cnt0[j];
@@ -1652,15 +1666,15 @@ __global__ void __launch_bounds__(kRowTile) emit_chunk_kernel(const __grid_const
     return;
   }
   if (j < A.m) {
-    const uint32_t c = A.cnt[j];
-    if (c <= A.thread_row_max && nact <= 32) chunk_row_thread(S, A, j, S.R.ro[tid], rl0);
+    const uint32_t c = mine.cnt;
+    if (c <= A.thread_row_max && nact <= 32) chunk_row_thread(S, A, mine, S.R.ro[tid], rl0);
     else if (c) S.R.queue[atomicAdd(&S.R.qn, 1u)] = tid;
   }
   __syncthreads();
   const uint32_t nq = S.R.qn;
   for (uint32_t q = warp; q < nq; q += kRowTile / 32) {
     const uint32_t t = S.R.queue[q];
-    chunk_row_warp(S, A, j0 + t, S.R.ro[t], rl0, lane);
+    chunk_row_warp(S, A, S.row[t], S.R.ro[t], rl0, lane);
   }
 }
 
