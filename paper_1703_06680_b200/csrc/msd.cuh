@@ -272,11 +272,19 @@ __global__ void __launch_bounds__(512) msd_hist_kernel(const void* __restrict__ 
 #define DDM_MSD_MINB 3
 #endif
 
+#ifndef DDM_MSD_REC
+#define DDM_MSD_REC 1
+#endif
 template <int ITEMS, bool V64, bool V32>
 struct PassSmem {
   static constexpr int kT = kThreads * ITEMS;
-  uint64_t keys[kT];
-  uint64_t v64[V64 ? kT : 2];
+  // packed records (key + one 64-bit payload) are staged as one 16-byte
+  // record per position: one 16-byte store per item (4 quarter-warp phases)
+  // instead of two 8-byte stores (2 x 2 half-warp phases), fewer bank-conflict
+  // replays of the ranked scatter into shared memory
+  static constexpr bool kRec = DDM_MSD_REC && V64 && !V32;
+  alignas(16) uint64_t keys[kRec ? 2 * kT : kT];  // kRec: interleaved {key, payload}
+  uint64_t v64[(V64 && !kRec) ? kT : 2];
   uint32_t v32[V32 ? kT : 4];
   uint8_t dg[kT];
   alignas(16) uint32_t wbase[kWarps][kRadix];
@@ -439,8 +447,12 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
           mmask[d] = 0;
         }
         const uint32_t pos = base + __popc(before);
-        S.keys[pos] = R.key[i];
-        if (V64) S.v64[pos] = R.hv[i];
+        if constexpr (Smem::kRec) {
+          reinterpret_cast<ulonglong2*>(S.keys)[pos] = make_ulonglong2(R.key[i], R.hv[i]);
+        } else {
+          S.keys[pos] = R.key[i];
+          if (V64) S.v64[pos] = R.hv[i];
+        }
         if (V32) S.v32[pos] = R.iv[i];
         S.dg[pos] = (uint8_t)d;
       }
@@ -488,11 +500,19 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
     for (int i = 0; i < ITEMS; ++i) {
       const uint32_t p = i * kThreads + tid;
       if (p < tile_valid) {
-        const uint64_t k = S.keys[p];
+        uint64_t k, v = 0;
+        if constexpr (Smem::kRec) {
+          const ulonglong2 r = reinterpret_cast<const ulonglong2*>(S.keys)[p];
+          k = r.x;
+          v = r.y;
+        } else {
+          k = S.keys[p];
+          if (V64) v = S.v64[p];
+        }
         const uint32_t d = S.dg[p];
         const uint64_t dst = (uint32_t)(S.digit_base[d] + p);
         k_out[dst] = k;
-        if (V64) v64_out[dst] = S.v64[p];
+        if (V64) v64_out[dst] = v;
         if (V32) v32_out[dst] = S.v32[p];
       }
     }
