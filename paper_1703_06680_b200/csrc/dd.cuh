@@ -696,13 +696,14 @@ __device__ __forceinline__ bool sure_le(float a, float b) {
 template <int R>
 struct RowSmem {
   static constexpr int kRows = kRT * R;
-  float4 rbox[kRows];          // widened row boxes (lo1, hi1, lo2, hi2), tile-row order
-  float2 rbox0[kRows];         // widened dim-0 row boxes (lo0, hi0)
+  float4 cbox[kRows];          // widened row boxes (lo1, hi1, lo2, hi2) in CELL order (slot k holds row rrow[k]):
+                               // the candidates' cell scans read them without the rrow indirection
+  float2 rbox0[kRows];         // widened dim-0 row boxes (lo0, hi0), tile-row order
   uint16_t rrow[kRows];        // tile row of each cell slot (cell order)
   uint16_t cstart[kRows + 2];  // G1 x G2 = kRows cells (d = 2: kRows x 1)
   uint32_t rcnt[kRows];        // hits per row; cell counts / cursors while binning
   uint32_t fpos[kRowFpos];     // A_t members of a batch of walk windows
-  unsigned long long lst[kList * kRT];  // queued uncertain passes, per warp: [warp][e][lane] = (row << 32) | Slo position
+  unsigned long long lst[kList * kRT];  // queued uncertain passes, per warp: [warp][e][lane] = (cell slot << 32) | Slo position
   float red[6 * kRW];
   uint32_t scan32[kRW + 1];
   uint64_t scan64[kRW + 1];
@@ -719,14 +720,15 @@ constexpr uint32_t rows_stage_cap() { return 8u * kRT * R; }  // staged hits per
 // exact test (Alg. 1 on every dimension, float64 / keys).
 template <int R>
 __device__ __forceinline__ bool rows_decide(const Args& A, const RowSmem<R>& S, unsigned long long v, uint64_t j0,
-                                            bool sure_ok) {
-  const uint32_t r = (uint32_t)(v >> 32), p = (uint32_t)v;
+                                            bool sure_ok, uint32_t& r) {
+  const uint32_t k = (uint32_t)(v >> 32), p = (uint32_t)v;
+  r = S.rrow[k];
   const float2 f0 = __ldg(A.box0 + p);
   const float2 u0 = S.rbox0[r];
   if (!(f0.x <= u0.y && u0.x <= f0.y)) return false;
   if (sure_ok && sure_le(f0.x, u0.y) && sure_le(u0.x, f0.y)) {
     const float4 f = __ldg(A.box12 + p);
-    const float4 u = S.rbox[r];
+    const float4 u = S.cbox[k];
     if (sure_le(f.x, u.y) && sure_le(u.x, f.y) && (A.d == 2 || (sure_le(f.z, u.w) && sure_le(u.z, f.w))))
       return true;
   }
@@ -765,7 +767,8 @@ __device__ __forceinline__ void rows_flush_lane(const Args& A, RowSmem<R>& S, ui
   const unsigned long long* q = rows_lane_q(S.lst, threadIdx.x);
   for (uint32_t e = 0; e < nl; ++e) {
     const unsigned long long v = q[e * 32];
-    if (rows_decide<R>(A, S, v, j0, sure_ok)) rows_hit<R, MODE>(A, S, (uint32_t)(v >> 32), (uint32_t)v, tile, ~0u);
+    uint32_t r;
+    if (rows_decide<R>(A, S, v, j0, sure_ok, r)) rows_hit<R, MODE>(A, S, r, (uint32_t)v, tile, ~0u);
   }
 }
 template <int R, int MODE>
@@ -795,9 +798,10 @@ __device__ __forceinline__ void rows_flush_warp(const Args& A, RowSmem<R>& S, ui
     const uint32_t pl = __shfl_sync(kFull, pre, L);
     bool hit = false;
     unsigned long long v = 0;
+    uint32_t r = 0;
     if (x < tot) {
       v = w[(x - pl) * 32 + L];
-      hit = rows_decide<R>(A, S, v, j0, sure_ok);
+      hit = rows_decide<R>(A, S, v, j0, sure_ok, r);
     }
     uint32_t slot = ~0u;
     if (MODE == kModeStage) {  // one slot reservation per warp
@@ -807,7 +811,7 @@ __device__ __forceinline__ void rows_flush_warp(const Args& A, RowSmem<R>& S, ui
       b = __shfl_sync(kFull, b, 0);
       slot = b + __popc(hm & lanemask_lt());
     }
-    if (hit) rows_hit<R, MODE>(A, S, (uint32_t)(v >> 32), (uint32_t)v, tile, slot);
+    if (hit) rows_hit<R, MODE>(A, S, r, (uint32_t)v, tile, slot);
   }
   __syncwarp();
   nl = 0;
@@ -826,14 +830,13 @@ __device__ __forceinline__ void rows_candidate(const Args& A, RowSmem<R>& S, con
   for (int c2 = c2l; c2 <= c2h; ++c2) {
     const uint32_t k1 = S.cstart[c2 * g1 + c1h + 1];
     for (uint32_t k = S.cstart[c2 * g1 + c1l]; k < k1; ++k) {
-      const uint32_t r = S.rrow[k];
-      const float4 u = S.rbox[r];
+      const float4 u = S.cbox[k];
       if (!(f.x <= u.y && u.x <= f.y && f.z <= u.w && u.z <= f.w)) continue;
       if (nl == kList) {
         rows_flush_lane<R, MODE>(A, S, nl, j0, tile, sure_ok);
         nl = 0;
       }
-      q[nl * 32] = ((unsigned long long)r << 32) | p;
+      q[nl * 32] = ((unsigned long long)k << 32) | p;
       ++nl;
     }
   }
@@ -887,12 +890,16 @@ __global__ void __launch_bounds__(kRT, 1024 / kRT) rows_kernel(const __grid_cons
   const float kInf = __int_as_float(0x7f800000);
   float mn1 = kInf, mx1 = -kInf, ml1 = 0.0f, mn2 = kInf, mx2 = -kInf, ml2 = 0.0f;
   uint32_t rbmax = 0;
-  for (uint32_t r = tid; r < (uint32_t)kRows; r += kRT) {
+  float4 ub[R];  // this thread's rows r = tid + i kRT, binned below
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const uint32_t r = tid + i * kRT;
     S.rcnt[r] = 0;
+    ub[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     if (r >= nrows) continue;
     const uint64_t j = j0 + r;
     const float4 u = row_box(A, j);
-    S.rbox[r] = u;
+    ub[i] = u;
     const double a0 = key_to_f64(A.ulo_key[j]);
     const double b0 = A.uhi ? key_to_f64(A.uhi[j]) : A.upd.hi[0][A.ulo_id[j]];
     S.rbox0[r] = make_float2(__double2float_rd(a0), __double2float_ru(b0));
@@ -939,9 +946,11 @@ __global__ void __launch_bounds__(kRT, 1024 / kRT) rows_kernel(const __grid_cons
   RBins B1, B2;
   B1.init(mn1, mx1, g1);
   B2.init(mn2, mx2, g2);
-  for (uint32_t r = tid; r < nrows; r += kRT) {
-    const float4 u = S.rbox[r];
-    atomicAdd(&S.rcnt[B2(u.z) * g1 + B1(u.x)], 1u);
+  int cell[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    cell[i] = B2(ub[i].z) * g1 + B1(ub[i].x);
+    if (tid + i * kRT < nrows) atomicAdd(&S.rcnt[cell[i]], 1u);
   }
   __syncthreads();
   {
@@ -960,9 +969,13 @@ __global__ void __launch_bounds__(kRT, 1024 / kRT) rows_kernel(const __grid_cons
     if (tid == 0) S.cstart[kRows] = (uint16_t)total;
   }
   __syncthreads();
-  for (uint32_t r = tid; r < nrows; r += kRT) {
-    const float4 u = S.rbox[r];
-    S.rrow[atomicAdd(&S.rcnt[B2(u.z) * g1 + B1(u.x)], 1u)] = (uint16_t)r;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const uint32_t r = tid + i * kRT;
+    if (r >= nrows) continue;
+    const uint32_t k = atomicAdd(&S.rcnt[cell[i]], 1u);
+    S.rrow[k] = (uint16_t)r;
+    S.cbox[k] = ub[i];
   }
   __syncthreads();
   for (uint32_t r = tid; r < (uint32_t)kRows; r += kRT) S.rcnt[r] = 0;
