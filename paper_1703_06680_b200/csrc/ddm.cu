@@ -692,21 +692,27 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
   const msd::MapRef M{mm, s.cbase};
   if (stage & kMsdPrep) {
   // bucket map equalised to the data (coarse population -> bucket allocation)
-  DDM_CUDA(cudaMemsetAsync(s.ccount, 0, sizeof(uint32_t) * (msd::kCoarse + 1), st));
-  const unsigned sgrid = grid_for((n + msd::kSampleStride - 1) / msd::kSampleStride, 512, 4);
-  DDM_LAUNCH("msd_sample", 8.0 * n / msd::kSampleStride, st,
-             msd::sample_minmax_kernel<true><<<sgrid, 512, 0, st>>>(src, n, mm));
-  DDM_TRY(check_launch());
-  DDM_LAUNCH("msd_coarse", 8.0 * n / msd::kSampleStride, st,
-             msd::coarse_hist_kernel<true><<<grid_for((n + msd::kSampleStride - 1) / msd::kSampleStride, 512, 4), 512, 0, st>>>(
-                 src, n, M, s.ccount));
-  DDM_TRY(check_launch());
-  DDM_LAUNCH("msd_map", 0, st, msd::map_build_kernel<<<1, 1024, 0, st>>>(s.ccount, bits, s.cbase));
-  DDM_TRY(check_launch());
+  if (n <= msd::kMapSmallMaxN) {  // small sorts: one latency-bound launch instead of three
+    DDM_LAUNCH("msd_map", 16.0 * n / msd::kSampleStride, st,
+               msd::map_small_kernel<true><<<1, 1024, 0, st>>>(src, n, mm, bits, s.cbase));
+    DDM_TRY(check_launch());
+  } else {
+    DDM_CUDA(cudaMemsetAsync(s.ccount, 0, sizeof(uint32_t) * (msd::kCoarse + 1), st));
+    const unsigned sgrid = grid_for((n + msd::kSampleStride - 1) / msd::kSampleStride, 512, 4);
+    DDM_LAUNCH("msd_sample", 8.0 * n / msd::kSampleStride, st,
+               msd::sample_minmax_kernel<true><<<sgrid, 512, 0, st>>>(src, n, mm));
+    DDM_TRY(check_launch());
+    DDM_LAUNCH("msd_coarse", 8.0 * n / msd::kSampleStride, st,
+               msd::coarse_hist_kernel<true><<<grid_for((n + msd::kSampleStride - 1) / msd::kSampleStride, 512, 4), 512, 0, st>>>(
+                   src, n, M, s.ccount));
+    DDM_TRY(check_launch());
+    DDM_LAUNCH("msd_map", 0, st, msd::map_build_kernel<<<1, 1024, 0, st>>>(s.ccount, bits, s.cbase));
+    DDM_TRY(check_launch());
+  }
+  // digit histograms of every pass (their exclusive scans -- the digit
+  // starts -- are taken inside the passes and the span-bounds kernel)
   DDM_CUDA(cudaMemsetAsync(s.dh, 0, sizeof(uint32_t) * 3 * 256, st));
   DDM_LAUNCH("msd_hist", 8.0 * n, st, msd::msd_hist_kernel<true><<<grid_for(n, 512, 4), 512, 0, st>>>(src, n, M, bits, passes, s.dh));
-  DDM_TRY(check_launch());
-  DDM_LAUNCH("radix_bin_start", 0, st, radix::bin_start_kernel<<<passes, radix::kRadix, 0, st>>>(s.dh, s.starts));
   DDM_TRY(check_launch());
   }
   if (!(stage & kMsdRun)) return DDM_OK;
@@ -734,7 +740,7 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
                                  sizeof(msd::PassSmem<ITEMS, V64, V32>), tiles),                                  \
                  msd::kThreads, sizeof(msd::PassSmem<ITEMS, V64, V32>), st>>>(                                \
                   KI, VI, II, bk[o], V64 ? bv[o] : nullptr, V32 ? bi[o] : nullptr, n, M, bits, 8 * p,              \
-                  s.starts + p * 256, s.status, s.counters + p, err)))
+                  s.dh + p * 256, s.status, s.counters + p, err)))
     if (p == 0) {
       if (PAY && pk) DDM_MSD_PASS(msd::kItems, true, false, true, "msd_pass_pay", src, v64_src, nullptr);
       else if (PAY) DDM_MSD_PASS(msd::kItems, true, true, true, "msd_pass_pay", src, v64_src, nullptr);
@@ -751,7 +757,7 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
   const int l = (passes - 1) & 1;
   if (passes == 1)  // bucket starts = the pass's digit starts
     DDM_LAUNCH("msd_bounds", 0, st, msd::span_bounds_hist_kernel<<<(spans + 256) / 256, 256, 0, st>>>(
-        s.starts, nb, n, spans, span, s.bounds));
+        s.dh, nb, n, spans, span, s.bounds));
   else
     DDM_LAUNCH("msd_bounds", 0, st, msd::span_bounds_kernel<<<(spans + 256) / 256, 256, 0, st>>>(bk[l], n, M, bits, spans,
                                                                                                span, s.bounds));
@@ -2429,7 +2435,8 @@ int ddm_profile_read(ddm_kernel_stat* out, int cap) {
 const char* ddm_build_info(void) {
   return "libddm sm_100a sort(value-bucketed MSD: 8-bit multisplit passes + smem local sort; LSB onesweep fallback) "
          "count(merge path 2048/tile; rank form | stab walk over slo_hi prefix maxima) scan(decoupled look-back) "
-         "emit(tile window | chunk-start sets | per-row) d>1(tiled cell filter, exact f64 re-test)";
+         "emit(tile window | chunk-start sets | per-row) d>1(k* sweep dim; row-indexed tiles: rows binned by dims 1-2, "
+         "candidates streamed, float-certain decisions, exact f64 re-test of the rest)";
 }
 
 }  // extern "C"

@@ -221,6 +221,80 @@ __global__ void __launch_bounds__(1024) map_build_kernel(const uint32_t* __restr
   }
 }
 
+// Small sorts (latency-bound): sample min/max, the sample's coarse histogram
+// and the bucket map in ONE launch of one CTA (sample_minmax_kernel +
+// coarse_hist_kernel + map_build_kernel otherwise).  The same map: min/max
+// folded into mm (atomics, as sample_minmax_kernel), coarse bins of the same
+// sample, base[] by the same formula.
+constexpr uint64_t kMapSmallMaxN = 1ull << 21;
+template <bool SRC_F64>
+__global__ void __launch_bounds__(1024) map_small_kernel(const void* __restrict__ src, uint64_t n,
+                                                         uint64_t* __restrict__ mm, int bits,
+                                                         uint32_t* __restrict__ base) {
+  __shared__ uint32_t sh[kCoarse];
+  __shared__ uint64_t red[2 * 32];
+  __shared__ uint64_t tmp[1024 / 32 + 1];
+  __shared__ uint32_t cmax;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint64_t ns = sample_size(n);
+  auto key_at = [&](uint64_t s) -> uint64_t {
+    const uint64_t i = sample_at(s);
+    return SRC_F64 ? f64_key(__ldcs(reinterpret_cast<const double*>(src) + i))
+                   : __ldcs(reinterpret_cast<const uint64_t*>(src) + i);
+  };
+  uint64_t lo = ~0ull, hi = 0;
+  for (uint64_t s = t; s < ns; s += 1024) {
+    const uint64_t k = key_at(s);
+    lo = k < lo ? k : lo;
+    hi = k > hi ? k : hi;
+  }
+  for (int i = t; i < kCoarse; i += 1024) sh[i] = 0;
+  if (t == 0) cmax = 0;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const uint64_t a = __shfl_xor_sync(kFull, lo, o), b = __shfl_xor_sync(kFull, hi, o);
+    lo = a < lo ? a : lo;
+    hi = b > hi ? b : hi;
+  }
+  if (lane == 0) { red[warp] = lo; red[32 + warp] = hi; }
+  __syncthreads();
+  if (warp == 0) {
+    lo = red[lane];
+    hi = red[32 + lane];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const uint64_t a = __shfl_xor_sync(kFull, lo, o), b = __shfl_xor_sync(kFull, hi, o);
+      lo = a < lo ? a : lo;
+      hi = b > hi ? b : hi;
+    }
+    if (lane == 0) {
+      if (lo != ~0ull) atomicMin((unsigned long long*)&mm[0], (unsigned long long)lo);
+      if (hi != 0) atomicMax((unsigned long long*)&mm[1], (unsigned long long)hi);
+      __threadfence();
+      red[0] = ld_relaxed_u64(mm);
+      red[1] = ld_relaxed_u64(mm + 1);
+    }
+  }
+  __syncthreads();
+  const uint64_t mm2[2] = {red[0], red[1]};
+  Bucketer B;
+  B.init(MapRef{mm2, nullptr}, 1);
+  for (uint64_t s = t; s < ns; s += 1024) atomicAdd(&sh[B.coarse(key_at(s))], 1u);
+  __syncthreads();
+  const uint64_t c0 = sh[2 * t], c1 = sh[2 * t + 1];
+  atomicMax(&cmax, (uint32_t)(c0 > c1 ? c0 : c1));
+  uint64_t total;
+  const uint64_t ex = block_excl_scan<1024, uint64_t>(c0 + c1, tmp, &total);
+  const uint64_t nb = 1ull << bits;
+  const uint64_t nn = total ? total : 1;
+  base[2 * t] = (uint32_t)(ex * nb / nn);
+  base[2 * t + 1] = (uint32_t)((ex + c0) * nb / nn);
+  if (t == 0) {
+    base[kCoarse] = (uint32_t)nb;
+    base[kCoarse + 1] = (double)cmax * kCoarse <= kLinearMax * (double)nn ? 1u : 0u;
+  }
+}
+
 // ---------------------------------------------------------------- histograms
 
 // Per-pass digit histograms of the bucket ids (digit p = bits [8p, 8p+8)),
@@ -274,6 +348,9 @@ __global__ void __launch_bounds__(512) msd_hist_kernel(const void* __restrict__ 
 
 #ifndef DDM_MSD_REC
 #define DDM_MSD_REC 1
+#endif
+#ifndef DDM_MSD_MATCHANY
+#define DDM_MSD_MATCHANY 0
 #endif
 template <int ITEMS, bool V64, bool V32>
 struct PassSmem {
@@ -370,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
     msd_pass_kernel(const void* __restrict__ k_in, const void* __restrict__ v64_in, const uint32_t* __restrict__ v32_in,
                     uint64_t* __restrict__ k_out, uint64_t* __restrict__ v64_out, uint32_t* __restrict__ v32_out,
                     uint64_t n, MapRef M, int bits, int shift,
-                    const uint32_t* __restrict__ bin_start, uint32_t* __restrict__ status,
+                    const uint32_t* __restrict__ hist, uint32_t* __restrict__ status,
                     uint32_t* __restrict__ tile_counter, uint32_t* __restrict__ err) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   using Smem = PassSmem<ITEMS, V64, V32>;
@@ -381,7 +458,11 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
   Bucketer BK;
   BK.init(M, bits);
   if (tid == 0) S.tile_id = atomicAdd(tile_counter, 1u);
-  __syncthreads();
+  // this pass's global digit starts: exclusive scan of its digit histogram
+  // (one digit per thread; no separate bin-start launch)
+  static_assert(kThreads == kRadix, "one digit per thread");
+  uint32_t ntot;
+  const uint32_t bin_start = block_excl_scan<kThreads>(hist[tid], S.scan_tmp, &ntot);
   uint32_t tile = S.tile_id;
   if (tile >= num_tiles) return;
   TileRegs<ITEMS, V64, V32, SRC_F64> R;
@@ -432,6 +513,16 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
     for (int i = 0; i < ITEMS; ++i) {
       const bool valid = wb0 + i * 32 + lane < n;
       const uint32_t d = dg[i];
+#if DDM_MSD_MATCHANY
+      // peers by the warp's match instruction (invalid lanes get unique keys)
+      const unsigned peers = __match_any_sync(kFull, valid ? d : 256u + lane);
+      uint32_t base = 0;
+      if (valid) base = wb[d];
+      __syncwarp();
+      if (valid) {
+        const unsigned before = peers & lt;
+        if (before == 0) wb[d] = base + __popc(peers);
+#else
       if (valid) atomicOr(&mmask[d], 1u << lane);
       __syncwarp();
       uint32_t peers = 0, base = 0;
@@ -446,6 +537,7 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
           wb[d] = base + __popc(peers);
           mmask[d] = 0;
         }
+#endif
         const uint32_t pos = base + __popc(before);
         if constexpr (Smem::kRec) {
           reinterpret_cast<ulonglong2*>(S.keys)[pos] = make_ulonglong2(R.key[i], R.hv[i]);
@@ -493,7 +585,7 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
       }
       st_relaxed_u32(my_status, radix::kFlagPre | (excl + total));
     }
-    S.digit_base[tid] = bin_start[tid] + excl - tstart;  // (mod 2^32)
+    S.digit_base[tid] = bin_start + excl - tstart;  // (mod 2^32)
     __syncthreads();
 
 #pragma unroll
@@ -879,11 +971,17 @@ __global__ void __launch_bounds__(256) span_bounds_kernel(const uint64_t* __rest
 // 256): the digit starts of that pass ARE the bucket starts, so the first
 // bucket boundary at or after s*span is the smallest start >= s*span -- a
 // search over 256 cached values instead of a gallop over the sorted keys.
-__global__ void __launch_bounds__(256) span_bounds_hist_kernel(const uint32_t* __restrict__ starts, uint32_t nb,
+__global__ void __launch_bounds__(256) span_bounds_hist_kernel(const uint32_t* __restrict__ hist, uint32_t nb,
                                                                uint64_t n, uint32_t spans, uint32_t span,
                                                                uint64_t* __restrict__ bounds) {
   __shared__ uint32_t st[kRadix];
-  for (uint32_t b = threadIdx.x; b < kRadix; b += blockDim.x) st[b] = b < nb ? starts[b] : (uint32_t)n;
+  __shared__ uint32_t tmp[kRadix / 32 + 1];
+  {  // the digit starts: exclusive scan of the pass's digit histogram (256 threads)
+    const uint32_t b = threadIdx.x;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan<kRadix>(b < nb ? hist[b] : 0u, tmp, &tot);
+    st[b] = b < nb ? ex : (uint32_t)n;
+  }
   __syncthreads();
   for (uint32_t sp = blockIdx.x * blockDim.x + threadIdx.x; sp <= spans; sp += gridDim.x * blockDim.x) {
     const uint64_t p = (uint64_t)sp * span;
