@@ -561,6 +561,9 @@ __device__ __forceinline__ uint64_t lookback_warp_u64(uint64_t* status, uint32_t
   return excl;
 }
 
+#ifndef DDM_ADV_BF
+#define DDM_ADV_BF 1
+#endif
 constexpr int kCountThreads = 512;
 constexpr int kCountItems = 4;  // rows per thread (short dependent merge chains, more warps)
 constexpr int kCountTile = kCountThreads * kCountItems;
@@ -739,6 +742,23 @@ __device__ __forceinline__ uint64_t advance(const uint64_t* W, uint64_t base, ui
   // cursors of consecutive sorted queries usually move by 0..2 entries: a
   // short linear scan first, the gallop only for longer moves
   uint32_t r = len;
+#if DDM_ADV_BF
+  if (k + 3 <= len) {  // branch-free: W is sorted, so the entries "before" x among the next 3 are a prefix
+    const uint64_t v0 = W[k], v1 = W[k + 1], v2 = W[k + 2];
+    const uint32_t c = (uint32_t)(UPPER ? v0 <= x : v0 < x) + (uint32_t)(UPPER ? v1 <= x : v1 < x) +
+                       (uint32_t)(UPPER ? v2 <= x : v2 < x);
+    if (c < 3) return base + k + c;
+    k += 3;
+  } else {
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      if (k >= len) break;
+      const uint64_t v = W[k];
+      if (UPPER ? v > x : v >= x) { r = k; break; }
+      ++k;
+    }
+  }
+#else
 #pragma unroll
   for (int t = 0; t < 3; ++t) {
     if (k >= len) break;
@@ -746,6 +766,7 @@ __device__ __forceinline__ uint64_t advance(const uint64_t* W, uint64_t base, ui
     if (UPPER ? v > x : v >= x) { r = k; break; }
     ++k;
   }
+#endif
   if (r == len && k < len) r = wseek<UPPER>(W, k, len, x);
   if (r < len) return base + r;
   if (base + len >= n) return n;

@@ -349,9 +349,6 @@ __global__ void __launch_bounds__(512) msd_hist_kernel(const void* __restrict__ 
 #ifndef DDM_MSD_REC
 #define DDM_MSD_REC 1
 #endif
-#ifndef DDM_MSD_MATCHANY
-#define DDM_MSD_MATCHANY 0
-#endif
 template <int ITEMS, bool V64, bool V32>
 struct PassSmem {
   static constexpr int kT = kThreads * ITEMS;
@@ -513,16 +510,6 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
     for (int i = 0; i < ITEMS; ++i) {
       const bool valid = wb0 + i * 32 + lane < n;
       const uint32_t d = dg[i];
-#if DDM_MSD_MATCHANY
-      // peers by the warp's match instruction (invalid lanes get unique keys)
-      const unsigned peers = __match_any_sync(kFull, valid ? d : 256u + lane);
-      uint32_t base = 0;
-      if (valid) base = wb[d];
-      __syncwarp();
-      if (valid) {
-        const unsigned before = peers & lt;
-        if (before == 0) wb[d] = base + __popc(peers);
-#else
       if (valid) atomicOr(&mmask[d], 1u << lane);
       __syncwarp();
       uint32_t peers = 0, base = 0;
@@ -537,7 +524,6 @@ __global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
           wb[d] = base + __popc(peers);
           mmask[d] = 0;
         }
-#endif
         const uint32_t pos = base + __popc(before);
         if constexpr (Smem::kRec) {
           reinterpret_cast<ulonglong2*>(S.keys)[pos] = make_ulonglong2(R.key[i], R.hv[i]);

@@ -69,3 +69,13 @@ def test_binding_refuses_cpu_tensors():
     x = torch.zeros((1, 4), dtype=torch.float64)
     with pytest.raises(TypeError):
         ddm.match_count(x, x, x, x)
+
+
+def test_sort_size_limits_refused_host_only(L):
+    """Sorts of more than DDM_MAX_SORT_KEYS keys (the look-back words' 30-bit
+    prefixes) are refused with DDM_ERR_INVALID_ARGUMENT before any device
+    work (never silently overflowed)."""
+    big = 2**30  # DDM_MAX_SORT_KEYS + 1
+    fake = 1 << 20  # aligned, never dereferenced: the size check comes first
+    assert L.ddm_sort_pairs(fake, big, 10, 10, fake, 2**62, None) == 1
+    assert L.ddm_radix_sort_u64(fake, None, fake + 4096, None, big, 0, 64, fake, 2**62, None) == 1
