@@ -112,19 +112,38 @@ __global__ void __launch_bounds__(256) box_kernel(const double* __restrict__ sdi
 
 // Widened dims-1/2 boxes in INPUT order (coalesced reads of the coordinates):
 // the row-indexed calls gather these 16-byte boxes by id instead of gathering
-// 2 (d - 1) float64 coordinates per region into sweep order.
+// 2 (d - 1) float64 coordinates per region into sweep order.  The same read
+// validates dims 1 and 2 (a1: finite, lo <= hi) into *err, so those dims need
+// no separate validation launch.
+__device__ __forceinline__ uint32_t box_check(double x, double y) {
+  const uint64_t bx = (uint64_t)__double_as_longlong(x), by = (uint64_t)__double_as_longlong(y);
+  if (!f64_finite_bits(bx) || !f64_finite_bits(by)) return match::kErrNonFinite;
+  return x <= y ? 0u : match::kErrInverted;
+}
 __global__ void __launch_bounds__(256) box_in_kernel(const __grid_constant__ match::DimPtrs src, int d, uint64_t n,
-                                                     float4* __restrict__ out) {
+                                                     float4* __restrict__ out, uint32_t* __restrict__ err) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const float kInf = __int_as_float(0x7f800000);
+  uint32_t e = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     float4 b;
-    b.x = __double2float_rd(__ldcs(src.lo[1] + i));
-    b.y = __double2float_ru(__ldcs(src.hi[1] + i));
-    b.z = d > 2 ? __double2float_rd(__ldcs(src.lo[2] + i)) : -kInf;
-    b.w = d > 2 ? __double2float_ru(__ldcs(src.hi[2] + i)) : kInf;
+    const double l1 = __ldcs(src.lo[1] + i), h1 = __ldcs(src.hi[1] + i);
+    e |= box_check(l1, h1);
+    b.x = __double2float_rd(l1);
+    b.y = __double2float_ru(h1);
+    if (d > 2) {
+      const double l2 = __ldcs(src.lo[2] + i), h2 = __ldcs(src.hi[2] + i);
+      e |= box_check(l2, h2);
+      b.z = __double2float_rd(l2);
+      b.w = __double2float_ru(h2);
+    } else {
+      b.z = -kInf;
+      b.w = kInf;
+    }
     out[i] = b;
   }
+  e = __reduce_or_sync(kFull, e);
+  if (err && e && (threadIdx.x & 31) == 0) atomicOr(err, e);
 }
 
 // ------------------------------------------------------------ tile kernel

@@ -877,7 +877,10 @@ ddm_status build_index_async(const ddm_regions* R, const Index& I, MsdScratch& s
   if (use_msd) {
     // a1 for dims 1..d-1 here; dim 0 is validated inside the first Slo pass,
     // which reads lo and hi anyway (the sort's key range comes from a sample)
-    DDM_TRY(validate_side(R->d, n, R->sub_lo, R->sub_hi, nullptr, nullptr, &misc->err, st, nullptr, nullptr, 1));
+    // (dim 0 is validated by the first multisplit pass; row-indexed d > 1
+    // calls validate dims 1-2 in box_in_kernel)
+    DDM_TRY(validate_side(R->d, n, R->sub_lo, R->sub_hi, nullptr, nullptr, &misc->err, st, nullptr, nullptr,
+                          boxes_only ? 3 : 1));
     cudaStream_t side[2];
     const bool with_shi = (need & kNeedShi) != 0;
     if (with_shi) {
@@ -916,7 +919,7 @@ ddm_status build_index_async(const ddm_regions* R, const Index& I, MsdScratch& s
       // sdims storage), gathered by id into Slo order; exact tests read the
       // input arrays through the ids
       float4* bin = reinterpret_cast<float4*>(I.sdims);
-      DDM_LAUNCH("dd_boxes", 32.0 * n, st, dd::box_in_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(D, (int)R->d, n, bin));
+      DDM_LAUNCH("dd_boxes", 32.0 * n, st, dd::box_in_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(D, (int)R->d, n, bin, &misc->err));
       DDM_TRY(check_launch());
       DDM_LAUNCH("dd_boxes", 56.0 * n, st,
                  dd::box_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(nullptr, (int)R->d, n, I.box12,
@@ -1002,7 +1005,7 @@ struct MatchReq {
 // upper key and the id as payload (MSD) or key + id (LSB fallback).  With
 // n_sub == 0 only the validation runs.  mm[4..5] must hold init values.
 ddm_status upd_sort_async(const ddm_regions* R, MatchWs& W, uint64_t n_sub, bool use_msd, cudaStream_t st,
-                          int stage = kMsdAll) {
+                          int stage = kMsdAll, uint32_t v_begin = 1) {
   const uint64_t m = R->n_upd;
   const uint32_t d = R->d;
   if (m == 0) return DDM_OK;
@@ -1011,7 +1014,7 @@ ddm_status upd_sort_async(const ddm_regions* R, MatchWs& W, uint64_t n_sub, bool
                                             : DDM_OK;
   if (use_msd) {
     if (stage & kMsdPrep)
-      DDM_TRY(validate_side(d, m, R->upd_lo, R->upd_hi, nullptr, nullptr, &W.misc->err, st, nullptr, nullptr, 1));
+      DDM_TRY(validate_side(d, m, R->upd_lo, R->upd_hi, nullptr, nullptr, &W.misc->err, st, nullptr, nullptr, v_begin));
     return msd_sort_t<true>(R->upd_lo[0], R->upd_hi[0], m, W.mm + 4, W.ulo_key, W.uhi, W.ulo_id, W.ulo,
                             &W.misc->overflow, &W.misc->err, st, stage, t_pack.upd);
   }
@@ -1141,7 +1144,7 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
       for (uint32_t k = 0; k < d; ++k) { U.lo[k] = R->upd_lo[k]; U.hi[k] = R->upd_hi[k]; }
       if (q.boxes_only)  // dims-1/2 float boxes in input order (over the udims storage), read by id
         DDM_LAUNCH("dd_boxes", 48.0 * m, st, dd::box_in_kernel<<<grid_for(m, 256, 8), 256, 0, st>>>(
-            U, (int)d, m, reinterpret_cast<float4*>(W.udims)));
+            U, (int)d, m, reinterpret_cast<float4*>(W.udims), &W.misc->err));
       else  // dims 1..d-1 of the updates gathered into sweep order (exact re-tests stay local)
         DDM_LAUNCH("gather_dims", 36.0 * (d - 1) * m, st, match::gather_dims_kernel<<<grid_for(m, 256, 8), 256, 0, st>>>(
             W.ulo_id, U, (int)d, m, W.udims, &W.misc->overflow));
@@ -1648,7 +1651,7 @@ static ddm_status match_full_dim(const ddm_regions* R, ddm_pair* pairs, uint64_t
         cudaStream_t side[2];
         DDM_TRY(side_streams(side, s));
         DDM_TRY(stream_join(side[1], s));
-        DDM_TRY(upd_sort_async(R, W, R->n_sub, true, side[1]));
+        DDM_TRY(upd_sort_async(R, W, R->n_sub, true, side[1], kMsdAll, q.boxes_only ? 3u : 1u));
         DDM_TRY(build_index_async(R, I, W.slo, W.shi, W.sort, W.mm, W.misc, true, s, need, q.boxes_only));
         DDM_TRY(stream_join(s, side[1]));
       } else {

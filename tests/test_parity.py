@@ -583,6 +583,26 @@ def test_validation_errors():
     assert e.value.status == 3
 
 
+def test_validation_errors_row_indexed_dd():
+    """Row-indexed d > 1 calls validate dims 1-2 inside the float-box kernel
+    (no separate validation launch): a non-finite or inverted coordinate on
+    dim 1 or 2 of either side is still reported, dim 3 too."""
+    rng = np.random.default_rng(5)
+    lo = rng.uniform(0, 100, (4, 6000))
+    hi = lo + 2.0
+    for side, k, bad, code in [(0, 1, np.nan, 2), (1, 2, np.inf, 2), (0, 2, "inv", 3), (1, 1, "inv", 3),
+                               (1, 3, np.nan, 2), (0, 3, "inv", 3)]:
+        a = [lo.copy(), hi.copy(), lo.copy(), hi.copy()]
+        if bad == "inv":
+            a[2 * side + 1][k, 4321] = a[2 * side][k, 4321] - 1.0
+        else:
+            a[2 * side][k, 4321] = bad
+        for f in (ddm.DDM_DD_FORCE_ROWS, ddm.DDM_DD_FORCE_CHUNKS):
+            with pytest.raises(ddm.DDMError) as e:
+                ddm.match_pairs(*[cuda(x) for x in a], flags=f)
+            assert e.value.status == code, (side, k, bad, f)
+
+
 def test_capacity_and_workspace():
     import ctypes
     L = ddm.load()
