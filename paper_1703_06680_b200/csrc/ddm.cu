@@ -526,6 +526,12 @@ void init_attrs_once() {
                        (int)sizeof(match::ChunkSmem));
   cudaFuncSetAttribute(match::emit_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(match::EmitTileSmem));
+  for (auto f : {(const void*)msd::msd_pass_kernel<msd::kItemsC, true, true, true>,
+                 (const void*)msd::msd_pass_kernel<msd::kItemsC, true, true, false>})
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(msd::PassSmem<msd::kItemsC, true, true>));
+  for (auto f : {(const void*)msd::msd_pass_kernel<msd::kItemsC, true, false, true>,
+                 (const void*)msd::msd_pass_kernel<msd::kItemsC, true, false, false>})
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(msd::PassSmem<msd::kItemsC, true, false>));
   cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(msd::PassSmem<msd::kItems, true, true>));
   cudaFuncSetAttribute(msd::msd_pass_kernel<msd::kItems, true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -722,7 +728,11 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
   uint64_t* bk[2] = {s.k[0], s.k[1]};
   uint64_t* bv[2] = {s.v64[0], s.v64[1]};
   uint32_t* bi[2] = {s.v32[0], s.v32[1]};
-  const uint64_t tiles = (n + msd::kTile - 1) / msd::kTile;  // (key-only passes use bigger tiles: fewer)
+  // payload passes: 16-record tiles when this chain runs alone, 8-record tiles
+  // (fewer registers) while the rank form's three chains share the SMs
+  const bool conc = chains_concurrent();
+  const int items = PAY ? (conc ? msd::kItemsC : msd::kItems) : msd::kItemsK;
+  const uint64_t tiles = (n + (uint64_t)msd::kThreads * items - 1) / ((uint64_t)msd::kThreads * items);
   DDM_CUDA(cudaMemsetAsync(s.counters, 0, sizeof(uint32_t) * radix::kMaxPasses, st));
   for (int p = 0; p < passes; ++p) {
     DDM_CUDA(cudaMemsetAsync(s.status, 0, sizeof(uint32_t) * radix::kRadix * tiles, st));
@@ -742,11 +752,15 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
                   KI, VI, II, bk[o], V64 ? bv[o] : nullptr, V32 ? bi[o] : nullptr, n, M, bits, 8 * p,              \
                   s.dh + p * 256, s.status, s.counters + p, err)))
     if (p == 0) {
-      if (PAY && pk) DDM_MSD_PASS(msd::kItems, true, false, true, "msd_pass_pay", src, v64_src, nullptr);
+      if (PAY && pk && conc) DDM_MSD_PASS(msd::kItemsC, true, false, true, "msd_pass_pay", src, v64_src, nullptr);
+      else if (PAY && pk) DDM_MSD_PASS(msd::kItems, true, false, true, "msd_pass_pay", src, v64_src, nullptr);
+      else if (PAY && conc) DDM_MSD_PASS(msd::kItemsC, true, true, true, "msd_pass_pay", src, v64_src, nullptr);
       else if (PAY) DDM_MSD_PASS(msd::kItems, true, true, true, "msd_pass_pay", src, v64_src, nullptr);
       else DDM_MSD_PASS(msd::kItemsK, false, false, true, "msd_pass", src, nullptr, nullptr);
     } else {
-      if (PAY && pk) DDM_MSD_PASS(msd::kItems, true, false, false, "msd_pass_pay", bk[q], bv[q], nullptr);
+      if (PAY && pk && conc) DDM_MSD_PASS(msd::kItemsC, true, false, false, "msd_pass_pay", bk[q], bv[q], nullptr);
+      else if (PAY && pk) DDM_MSD_PASS(msd::kItems, true, false, false, "msd_pass_pay", bk[q], bv[q], nullptr);
+      else if (PAY && conc) DDM_MSD_PASS(msd::kItemsC, true, true, false, "msd_pass_pay", bk[q], bv[q], bi[q]);
       else if (PAY) DDM_MSD_PASS(msd::kItems, true, true, false, "msd_pass_pay", bk[q], bv[q], bi[q]);
       else DDM_MSD_PASS(msd::kItemsK, false, false, false, "msd_pass", bk[q], nullptr, nullptr);
     }

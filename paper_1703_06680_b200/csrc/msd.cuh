@@ -30,11 +30,13 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kRadix = 256;
 #ifndef DDM_MSD_ITEMS
-#define DDM_MSD_ITEMS 8
+#define DDM_MSD_ITEMS 16
 #endif
-constexpr int kItems = DDM_MSD_ITEMS;  // records per thread of a payload pass tile
+constexpr int kItems = DDM_MSD_ITEMS;  // records per thread of a payload pass tile (one sort chain at a time)
+constexpr int kItemsC = 8;  // ... while the three sort chains run concurrently (rank form): 80 instead of
+                            // 125 registers, so every chain's pass keeps a CTA on each SM
 constexpr int kItemsK = 16;  // key-only passes: bigger tiles (fewer look-backs; measured 0.83 -> 0.70 ms at c3)
-constexpr int kTile = kThreads * kItems;
+constexpr int kTile = kThreads * (kItems < kItemsC ? kItems : kItemsC);  // smallest payload tile (status sizing)
 #ifndef DDM_LS_SPAN
 #define DDM_LS_SPAN 2048
 #endif
@@ -342,9 +344,10 @@ __global__ void __launch_bounds__(512) msd_hist_kernel(const void* __restrict__ 
 // then stable ranks from per-item peer masks (shared atomicOr).  (Round 2
 // measured a ballot-only ranking -- 8 warp ballots per item, no shared
 // atomics -- 8 % slower.)
-#ifndef DDM_MSD_MINB
-#define DDM_MSD_MINB 3
-#endif
+// CTAs per SM the pass is compiled for: 2 for the 16-record payload tiles
+// (125 registers), 3 otherwise
+template <int ITEMS, bool V64>
+constexpr int pass_minb() { return (V64 && ITEMS >= 16) ? 2 : 3; }
 
 #ifndef DDM_MSD_REC
 #define DDM_MSD_REC 1
@@ -440,7 +443,7 @@ struct TileRegs {
 };
 
 template <int ITEMS, bool V64, bool V32, bool SRC_F64>
-__global__ void __launch_bounds__(kThreads, DDM_MSD_MINB)
+__global__ void __launch_bounds__(kThreads, (pass_minb<ITEMS, V64>()))
     msd_pass_kernel(const void* __restrict__ k_in, const void* __restrict__ v64_in, const uint32_t* __restrict__ v32_in,
                     uint64_t* __restrict__ k_out, uint64_t* __restrict__ v64_out, uint32_t* __restrict__ v32_out,
                     uint64_t n, MapRef M, int bits, int shift,
