@@ -16,7 +16,7 @@ for r in data:
         per[i] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1)
         name[i] = r[ki]
 def phase(k):
-    if "msd_pass_kernel" in k: return "msd_pass_pay" if re.search(r"<8, (1|true)", k) else "msd_pass"
+    if "msd_pass_kernel" in k: return "msd_pass_pay" if re.search(r"msd_pass_kernel<\d+, (1|true)", k) else "msd_pass"
     if "local_sort_kernel" in k:  # local_sort_kernel<config, V64, V32>: V64 = the payload sorts
         return "msd_local_pay" if re.search(r"local_sort_kernel<[^,<>]*(<[^>]*>)?, (1|true),", k) else "msd_local"
     for a, b in (("count_kernel", "count"), ("emit", "emit"), ("msd_hist", "msd_hist"), ("block_max", "block_max"),
