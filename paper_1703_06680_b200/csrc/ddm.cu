@@ -849,7 +849,7 @@ ddm_status validate_side(uint32_t d, uint64_t cnt, const double* const* lo, cons
 // What the index keeps: Shi for the rank-form counts (count-only calls), the
 // slo_hi prefix maxima for the walk-form counts (pairs calls); ddm_sub_index_build
 // keeps both.
-enum : int { kNeedShi = 1, kNeedPm = 2 };
+enum : int { kNeedShi = 1, kNeedPm = 2, kNeedKeysOnly = 4 };  // kNeedKeysOnly: d = 1 count-only calls
 constexpr uint64_t kWalkMinN = 1ull << 20;  // below: rank form (the Shi chain hides on a side stream)
 constexpr double kWalkMaxStab = 4.0;        // walk form while the estimated mean |Stab(a)| is at most this
 
@@ -893,8 +893,13 @@ ddm_status build_index_async(const ddm_regions* R, const Index& I, MsdScratch& s
     // which reads lo and hi anyway (the sort's key range comes from a sample)
     // (dim 0 is validated by the first multisplit pass; row-indexed d > 1
     // calls validate dims 1-2 in box_in_kernel)
+    // d = 1 count-only calls (rank form: K = sum r_b - r_hi, App. A I2) need
+    // the sorted lower keys alone: Slo is sorted keys-only (8-byte records, no
+    // upper keys / ids / block maxima), and dim 0 is validated here because no
+    // pass reads both of its bounds
+    const bool keys_only = (need & kNeedKeysOnly) != 0 && R->d == 1;
     DDM_TRY(validate_side(R->d, n, R->sub_lo, R->sub_hi, nullptr, nullptr, &misc->err, st, nullptr, nullptr,
-                          boxes_only ? 3 : 1));
+                          keys_only ? 0 : boxes_only ? 3 : 1));
     cudaStream_t side[2];
     const bool with_shi = (need & kNeedShi) != 0;
     if (with_shi) {
@@ -904,10 +909,15 @@ ddm_status build_index_async(const ddm_regions* R, const Index& I, MsdScratch& s
       DDM_TRY(msd_sort_t<false>(R->sub_hi[0], nullptr, n, mm + 2, I.shi_key, nullptr, nullptr, shi, &misc->overflow,
                                 nullptr, side[0]));
     }
-    // a2 + a3: Slo with the upper key and the id as payload
-    DDM_TRY(msd_sort_t<true>(R->sub_lo[0], R->sub_hi[0], n, mm + 0, I.slo_key, I.slo_hi, I.slo_id, slo,
-                             &misc->overflow, &misc->err, st, kMsdAll, t_pack.sub));
-    DDM_TRY(tree_async(I, need, false, st));
+    if (keys_only) {
+      DDM_TRY(msd_sort_t<false>(R->sub_lo[0], nullptr, n, mm + 0, I.slo_key, nullptr, nullptr, slo, &misc->overflow,
+                                nullptr, st));
+    } else {
+      // a2 + a3: Slo with the upper key and the id as payload
+      DDM_TRY(msd_sort_t<true>(R->sub_lo[0], R->sub_hi[0], n, mm + 0, I.slo_key, I.slo_hi, I.slo_id, slo,
+                               &misc->overflow, &misc->err, st, kMsdAll, t_pack.sub));
+      DDM_TRY(tree_async(I, need, false, st));
+    }
     if (with_shi) DDM_TRY(stream_join(st, side[0]));
   } else {
     SortScratch s = lsb_with(lsb, slo);
@@ -1081,15 +1091,20 @@ ddm_status match_sorted(const MatchReq& q, MatchWs& W, uint64_t* count_out, bool
       DDM_LAUNCH("count_partition", 0, cs, match::count_partition1_kernel<<<(unsigned)((ctiles + 255) / 256), 256, 0, cs>>>(
           W.ulo_key, m, I.slo_key, q.walk ? nullptr : I.shi_key, n, W.part));
     DDM_TRY(check_launch());
-    const double cbytes = (use_msd ? 28.0 : 48.0) * m + (q.walk ? 24.0 : 16.0) * n;
+    // d = 1 count-only calls keep only the 256-row tile sums (no per-row r_lo / r_b / cnt)
+    const bool rows = !(d == 1 && !q.pairs && !q.chunk);
+    uint32_t* const o_lo = rows ? W.r_lo : nullptr;
+    uint32_t* const o_b = rows ? W.r_b : nullptr;
+    uint32_t* const o_c = rows ? W.cnt0 : nullptr;
+    const double cbytes = (use_msd ? (rows ? 28.0 : 16.0) : 48.0) * m + (q.walk ? 24.0 : 16.0) * n;
     if (q.walk)
       DDM_LAUNCH("count", cbytes, cs, match::count_kernel<true><<<(unsigned)ctiles, match::kCountThreads, match::count_smem_bytes(true), cs>>>(
-          W.ulo_key, W.ulo_id, R->upd_hi[0], use_msd ? W.uhi : nullptr, m, I.slo_key, nullptr, n, W.part, W.r_lo, W.r_b,
-          W.cnt0, W.tile_sum, CW));
+          W.ulo_key, W.ulo_id, R->upd_hi[0], use_msd ? W.uhi : nullptr, m, I.slo_key, nullptr, n, W.part, o_lo, o_b,
+          o_c, W.tile_sum, CW));
     else
       DDM_LAUNCH("count", cbytes, cs, match::count_kernel<false><<<(unsigned)ctiles, match::kCountThreads, match::count_smem_bytes(false), cs>>>(
-          W.ulo_key, W.ulo_id, R->upd_hi[0], use_msd ? W.uhi : nullptr, m, I.slo_key, I.shi_key, n, W.part, W.r_lo, W.r_b,
-          W.cnt0, W.tile_sum, CW));
+          W.ulo_key, W.ulo_id, R->upd_hi[0], use_msd ? W.uhi : nullptr, m, I.slo_key, I.shi_key, n, W.part, o_lo, o_b,
+          o_c, W.tile_sum, CW));
     return check_launch();
   };
   if (pre && !q.boxes_only) DDM_TRY(count_pass(st));
@@ -1643,7 +1658,7 @@ static ddm_status match_full_dim(const ddm_regions* R, ddm_pair* pairs, uint64_t
   const OneChain one_chain(walk);
   for (int attempt = lsb_only ? 1 : 0; attempt < 2; ++attempt) {
     const bool use_msd = attempt == 0;
-    const int need = (walk || q.boxes_only) ? kNeedPm : kNeedShi;
+    const int need = (walk || q.boxes_only) ? kNeedPm : (pairs || R->d != 1) ? kNeedShi : (kNeedShi | kNeedKeysOnly);
     q.walk = need == kNeedPm;
     auto pre = [&](cudaStream_t s) -> ddm_status {
       DDM_CUDA(cudaMemsetAsync(W.misc, 0, sizeof(Misc), s));

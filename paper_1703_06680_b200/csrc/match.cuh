@@ -949,7 +949,9 @@ __global__ void __launch_bounds__(kCountThreads, DDM_COUNT_MINB) count_kernel(
             if (!walk_step(H0, P0, S.pbw, q0, lh, C, pos[i], a[i], cnt[i])) act &= ~(1u << i);
       }
     }
-    if (ni == kCountItems) {
+    if (!r_lo_out) {
+      // (count-only call: the tile sums below are all that is needed)
+    } else if (ni == kCountItems) {
       uint4* dl = reinterpret_cast<uint4*>(r_lo_out + j);
       uint4* db = reinterpret_cast<uint4*>(r_b_out + j);
       uint4* dc = reinterpret_cast<uint4*>(cnt_out + j);
