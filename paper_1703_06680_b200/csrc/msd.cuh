@@ -352,6 +352,12 @@ constexpr int pass_minb() { return (V64 && ITEMS >= 16) ? 2 : 3; }
 #ifndef DDM_MSD_REC
 #define DDM_MSD_REC 1
 #endif
+#ifndef DDM_LS_MULBIN
+#define DDM_LS_MULBIN 1
+#endif
+#ifndef DDM_MSD_RANKFIRST
+#define DDM_MSD_RANKFIRST 1
+#endif
 template <int ITEMS, bool V64, bool V32>
 struct PassSmem {
   static constexpr int kT = kThreads * ITEMS;
@@ -452,6 +458,8 @@ __global__ void __launch_bounds__(kThreads, (pass_minb<ITEMS, V64>()))
   extern __shared__ __align__(16) unsigned char smem_raw[];
   using Smem = PassSmem<ITEMS, V64, V32>;
   constexpr int kT = Smem::kT;
+  // (keys-only passes keep the histogram-first form: ranking first spills there)
+  constexpr bool kRankFirst = DDM_MSD_RANKFIRST && V64;
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t num_tiles = (n + kT - 1) / kT;
@@ -483,10 +491,40 @@ __global__ void __launch_bounds__(kThreads, (pass_minb<ITEMS, V64>()))
     }
     __syncthreads();
     uint32_t dg[ITEMS];
+    if constexpr (kRankFirst) {
+    // warp-private ranking first: each item's rank among its warp's items of
+    // the same digit (peer masks), the warp's digit counts left in wb -- the
+    // tile histogram comes out of the ranking (no separate atomicAdd pass);
+    // dg[i] = digit | warp-local rank << 8
+    {
+      uint32_t* mmask = S.match[warp];
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const bool valid = wb0 + i * 32 + lane < n;
+        const uint32_t d = (BK(R.key[i]) >> shift) & 255u;
+        if (valid) atomicOr(&mmask[d], 1u << lane);
+        __syncwarp();
+        uint32_t peers = 0, base = 0;
+        if (valid) {
+          peers = mmask[d];
+          base = wb[d];
+        }
+        __syncwarp();
+        const unsigned before = peers & lt;
+        if (valid && before == 0) {
+          wb[d] = base + __popc(peers);
+          mmask[d] = 0;
+        }
+        dg[i] = d | ((base + __popc(before)) << 8);
+        __syncwarp();
+      }
+    }
+    } else {
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       dg[i] = (BK(R.key[i]) >> shift) & 255u;
       if (wb0 + i * 32 + lane < n) atomicAdd(&wb[dg[i]], 1u);
+    }
     }
     __syncthreads();
     uint32_t total = 0;
@@ -508,6 +546,23 @@ __global__ void __launch_bounds__(kThreads, (pass_minb<ITEMS, V64>()))
     for (int w = 0; w < kWarps; ++w) S.wbase[w][tid] += tstart;
     __syncthreads();
 
+    if constexpr (kRankFirst) {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      if (wb0 + i * 32 + lane < n) {
+        const uint32_t d = dg[i] & 255u;
+        const uint32_t pos = wb[d] + (dg[i] >> 8);
+        if constexpr (Smem::kRec) {
+          reinterpret_cast<ulonglong2*>(S.keys)[pos] = make_ulonglong2(R.key[i], R.hv[i]);
+        } else {
+          S.keys[pos] = R.key[i];
+          if (V64) S.v64[pos] = R.hv[i];
+        }
+        if (V32) S.v32[pos] = R.iv[i];
+        S.dg[pos] = (uint8_t)d;
+      }
+    }
+    } else {
     uint32_t* mmask = S.match[warp];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
@@ -538,6 +593,7 @@ __global__ void __launch_bounds__(kThreads, (pass_minb<ITEMS, V64>()))
         S.dg[pos] = (uint8_t)d;
       }
       __syncwarp();
+    }
     }
     // claim the next tile and start its loads (the current tile now lives in smem)
     if (tid == 0) S.tile_id = atomicAdd(tile_counter, 1u);
@@ -720,10 +776,24 @@ __device__ void local_sort_group(LocalSmem<C, V64, V32>& S, const uint64_t* __re
       kmax = S.red[(C::T / 32) + w] > kmax ? S.red[(C::T / 32) + w] : kmax;
     }
   }
-  // smallest shift with (kmax - kmin) >> sh < C::BINS
   const uint64_t range = kmax - kmin;
+#if DDM_LS_MULBIN
+  // fine bin = umulhi((k - kmin) >> sh, mult): the key range scaled onto all
+  // C::BINS bins (a power-of-two shift alone fills between half and all of
+  // them); monotone in the key, which is all the counting sort needs (the
+  // order inside a bin is decided on the exact keys below).  sh leaves the
+  // shifted range rs below 2^32; mult = BINS * 2^32 / (rs + 1) < 2^32 keeps
+  // every bin below BINS (clamped to 2^32 - 1 when rs < BINS: bins x - 1)
+  const int sh = range >> 32 ? 32 - __clzll((long long)range) : 0;
+  const uint64_t rs1 = (range >> sh) + 1;
+  const uint32_t mult = (uint32_t)umin64(((uint64_t)C::BINS << 32) / rs1, 0xffffffffull);
+  auto fine = [&](uint64_t k) -> uint32_t { return __umulhi((uint32_t)((k - kmin) >> sh), mult); };
+#else
+  // smallest shift with (kmax - kmin) >> sh < C::BINS
   const int sh = range ? max(0, 64 - __clzll((long long)range) - C::BIN_BITS) : 0;
-  for (uint32_t i = tid; i < c; i += C::T) bin_add(S.binw, (uint32_t)((K[i] - kmin) >> sh));
+  auto fine = [&](uint64_t k) -> uint32_t { return (uint32_t)((k - kmin) >> sh); };
+#endif
+  for (uint32_t i = tid; i < c; i += C::T) bin_add(S.binw, fine(K[i]));
   __syncthreads();
   {  // exclusive scan over the bins (8 per thread, 4 words) + large-bin detection
     constexpr int kPer = C::BINS / C::T;
@@ -755,7 +825,7 @@ __device__ void local_sort_group(LocalSmem<C, V64, V32>& S, const uint64_t* __re
     // place every record at its bin's next slot, straight into perm (any
     // order inside a bin; most bins hold zero or one record) ...
     for (uint32_t i = tid; i < c; i += C::T) {
-      const uint32_t pos = bin_add(S.binw, (uint32_t)((K[i] - kmin) >> sh));
+      const uint32_t pos = bin_add(S.binw, fine(K[i]));
       S.perm[pos] = (uint16_t)i;
     }
     __syncthreads();
@@ -768,7 +838,7 @@ __device__ void local_sort_group(LocalSmem<C, V64, V32>& S, const uint64_t* __re
     for (uint32_t x = tid; x < c; x += C::T) {
       const uint16_t v = S.perm[x];
       const uint64_t kv = K[v];
-      const uint32_t b = (uint32_t)((kv - kmin) >> sh);
+      const uint32_t b = fine(kv);
       const uint32_t lo = b ? bin_get(S.binw, b - 1) : 0, hi = bin_get(S.binw, b);
       uint32_t r = 0;
       if (hi - lo > 1)  // (most bins hold this record alone)
