@@ -352,9 +352,6 @@ constexpr int pass_minb() { return (V64 && ITEMS >= 16) ? 2 : 3; }
 #ifndef DDM_MSD_REC
 #define DDM_MSD_REC 1
 #endif
-#ifndef DDM_LS_MULBIN
-#define DDM_LS_MULBIN 1
-#endif
 #ifndef DDM_MSD_RANKFIRST
 #define DDM_MSD_RANKFIRST 1
 #endif
@@ -777,22 +774,9 @@ __device__ void local_sort_group(LocalSmem<C, V64, V32>& S, const uint64_t* __re
     }
   }
   const uint64_t range = kmax - kmin;
-#if DDM_LS_MULBIN
-  // fine bin = umulhi((k - kmin) >> sh, mult): the key range scaled onto all
-  // C::BINS bins (a power-of-two shift alone fills between half and all of
-  // them); monotone in the key, which is all the counting sort needs (the
-  // order inside a bin is decided on the exact keys below).  sh leaves the
-  // shifted range rs below 2^32; mult = BINS * 2^32 / (rs + 1) < 2^32 keeps
-  // every bin below BINS (clamped to 2^32 - 1 when rs < BINS: bins x - 1)
-  const int sh = range >> 32 ? 32 - __clzll((long long)range) : 0;
-  const uint64_t rs1 = (range >> sh) + 1;
-  const uint32_t mult = (uint32_t)umin64(((uint64_t)C::BINS << 32) / rs1, 0xffffffffull);
-  auto fine = [&](uint64_t k) -> uint32_t { return __umulhi((uint32_t)((k - kmin) >> sh), mult); };
-#else
   // smallest shift with (kmax - kmin) >> sh < C::BINS
   const int sh = range ? max(0, 64 - __clzll((long long)range) - C::BIN_BITS) : 0;
   auto fine = [&](uint64_t k) -> uint32_t { return (uint32_t)((k - kmin) >> sh); };
-#endif
   for (uint32_t i = tid; i < c; i += C::T) bin_add(S.binw, fine(K[i]));
   __syncthreads();
   {  // exclusive scan over the bins (8 per thread, 4 words) + large-bin detection
