@@ -704,12 +704,12 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
     DDM_TRY(check_launch());
   } else {
     DDM_CUDA(cudaMemsetAsync(s.ccount, 0, sizeof(uint32_t) * (msd::kCoarse + 1), st));
-    const unsigned sgrid = grid_for((n + msd::kSampleStride - 1) / msd::kSampleStride, 512, 4);
+    const unsigned sgrid = grid_for((n + msd::kSampleStride - 1) / msd::kSampleStride, 512, 1);
     DDM_LAUNCH("msd_sample", 8.0 * n / msd::kSampleStride, st,
                msd::sample_minmax_kernel<true><<<sgrid, 512, 0, st>>>(src, n, mm));
     DDM_TRY(check_launch());
     DDM_LAUNCH("msd_coarse", 8.0 * n / msd::kSampleStride, st,
-               msd::coarse_hist_kernel<true><<<grid_for((n + msd::kSampleStride - 1) / msd::kSampleStride, 512, 4), 512, 0, st>>>(
+               msd::coarse_hist_kernel<true><<<sgrid, 512, 0, st>>>(
                    src, n, M, s.ccount));
     DDM_TRY(check_launch());
     DDM_LAUNCH("msd_map", 0, st, msd::map_build_kernel<<<1, 1024, 0, st>>>(s.ccount, bits, s.cbase));

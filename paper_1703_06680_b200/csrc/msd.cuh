@@ -142,6 +142,10 @@ struct Bucketer {
   }
 };
 
+constexpr int kSampleU = 8;  // sample loads in flight per thread (sampling kernels)
+// The sampling kernels are launched on one CTA per SM (kSMs): fewer CTAs
+// means fewer global atomics folding the per-CTA min/max and coarse counts.
+
 // [min, max] key of the sample (runs of kSampleChunk records, one in every
 // kSampleStride) into mm[0], mm[1] (initialised to [~0, 0]).  Keys outside
 // the sampled range are clamped into the first / last bucket by the
@@ -149,14 +153,30 @@ struct Bucketer {
 template <bool SRC_F64>
 __global__ void __launch_bounds__(512) sample_minmax_kernel(const void* __restrict__ src, uint64_t n,
                                                             uint64_t* __restrict__ mm) {
+  __shared__ uint64_t red[2][512 / 32];
   const uint64_t ns = sample_size(n);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint64_t lo = ~0ull, hi = 0;
-  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i = sample_at(s);
-    const uint64_t k = SRC_F64 ? f64_key(__ldcs(reinterpret_cast<const double*>(src) + i))
-                               : __ldcs(reinterpret_cast<const uint64_t*>(src) + i);
-    lo = k < lo ? k : lo;
-    hi = k > hi ? k : hi;
+  // kSampleU independent loads in flight per thread (a latency-bound loop otherwise)
+  for (uint64_t s0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s0 < ns; s0 += kSampleU * stride) {
+    uint64_t k[kSampleU];
+#pragma unroll
+    for (int u = 0; u < kSampleU; ++u) {
+      const uint64_t s = s0 + u * stride;
+      if (s < ns) {
+        const uint64_t i = sample_at(s);
+        k[u] = SRC_F64 ? f64_key(__ldcs(reinterpret_cast<const double*>(src) + i))
+                       : __ldcs(reinterpret_cast<const uint64_t*>(src) + i);
+      } else {
+        k[u] = 0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kSampleU; ++u)
+      if (s0 + u * stride < ns) {
+        lo = k[u] < lo ? k[u] : lo;
+        hi = k[u] > hi ? k[u] : hi;
+      }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -164,9 +184,23 @@ __global__ void __launch_bounds__(512) sample_minmax_kernel(const void* __restri
     lo = a < lo ? a : lo;
     hi = b > hi ? b : hi;
   }
-  if ((threadIdx.x & 31) == 0) {
-    if (lo != ~0ull) atomicMin((unsigned long long*)&mm[0], (unsigned long long)lo);
-    if (hi != 0) atomicMax((unsigned long long*)&mm[1], (unsigned long long)hi);
+  // one atomic pair per CTA (per-warp atomics on the same two words serialise)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0) { red[0][warp] = lo; red[1][warp] = hi; }
+  __syncthreads();
+  if (warp == 0) {
+    lo = lane < nw ? red[0][lane] : ~0ull;
+    hi = lane < nw ? red[1][lane] : 0ull;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const uint64_t a = __shfl_xor_sync(kFull, lo, o), b = __shfl_xor_sync(kFull, hi, o);
+      lo = a < lo ? a : lo;
+      hi = b > hi ? b : hi;
+    }
+    if (lane == 0) {
+      if (lo != ~0ull) atomicMin((unsigned long long*)&mm[0], (unsigned long long)lo);
+      if (hi != 0) atomicMax((unsigned long long*)&mm[1], (unsigned long long)hi);
+    }
   }
 }
 
@@ -184,12 +218,26 @@ __global__ void __launch_bounds__(512) coarse_hist_kernel(const void* __restrict
   __syncthreads();
   const uint64_t ns = sample_size(n);
   uint32_t mine = 0;
-  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i = sample_at(s);
-    const uint64_t k = SRC_F64 ? f64_key(__ldcs(reinterpret_cast<const double*>(src) + i))
-                               : __ldcs(reinterpret_cast<const uint64_t*>(src) + i);
-    atomicAdd(&sh[B.coarse(k)], 1u);
-    ++mine;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t s0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s0 < ns; s0 += kSampleU * stride) {
+    uint64_t k[kSampleU];
+#pragma unroll
+    for (int u = 0; u < kSampleU; ++u) {
+      const uint64_t s = s0 + u * stride;
+      if (s < ns) {
+        const uint64_t i = sample_at(s);
+        k[u] = SRC_F64 ? f64_key(__ldcs(reinterpret_cast<const double*>(src) + i))
+                       : __ldcs(reinterpret_cast<const uint64_t*>(src) + i);
+      } else {
+        k[u] = 0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kSampleU; ++u)
+      if (s0 + u * stride < ns) {
+        atomicAdd(&sh[B.coarse(k[u])], 1u);
+        ++mine;
+      }
   }
   atomicAdd(&tot, mine);
   __syncthreads();

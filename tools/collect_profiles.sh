@@ -12,6 +12,11 @@ for c in c2 c3 c4 c5; do
     python tools/launches.py $o/${tag}_launches_$c.csv $((n - b)); } > $p/${out}_${c}_launch_summary.txt
 done
 for k in msd_pass local_sort count emit dd_stage; do
+  if [ -d $o/${tag}_prof ]; then  # (tools/gpu_final3.sh: reports already turned into text on the box)
+    cp $o/${tag}_prof/${k}_ncu_full.txt $p/${out}_${k}_ncu_full.txt 2>/dev/null
+    cp $o/${tag}_prof/${k}_hot_lines.txt $p/${out}_${k}_hot_lines.txt 2>/dev/null
+    continue
+  fi
   [ -f $o/${tag}_$k.ncu-rep ] || continue
   ncu -i $o/${tag}_$k.ncu-rep --page details > $p/${out}_${k}_ncu_full.txt 2>/dev/null
   python tools/ncu_lines.py $o/${tag}_$k.ncu-rep "" 30 > $p/${out}_${k}_hot_lines.txt 2>/dev/null
