@@ -526,6 +526,8 @@ void init_attrs_once() {
                        (int)sizeof(match::ChunkSmem));
   cudaFuncSetAttribute(match::emit_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(match::EmitTileSmem));
+  cudaFuncSetAttribute(msd::msd_hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)msd::hist_smem_bytes(3));
   for (auto f : {(const void*)msd::msd_pass_kernel<msd::kItemsC, true, true, true>,
                  (const void*)msd::msd_pass_kernel<msd::kItemsC, true, true, false>})
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(msd::PassSmem<msd::kItemsC, true, true>));
@@ -718,7 +720,11 @@ ddm_status msd_sort_t(const double* src, const double* v64_src, uint64_t n, uint
   // digit histograms of every pass (their exclusive scans -- the digit
   // starts -- are taken inside the passes and the span-bounds kernel)
   DDM_CUDA(cudaMemsetAsync(s.dh, 0, sizeof(uint32_t) * 3 * 256, st));
-  DDM_LAUNCH("msd_hist", 8.0 * n, st, msd::msd_hist_kernel<true><<<grid_for(n, 512, 4), 512, 0, st>>>(src, n, M, bits, passes, s.dh));
+  {  // lane-replicated counters: 32 KB of shared memory per pass, as many 512-thread CTAs per SM as fit
+    const size_t hsm = msd::hist_smem_bytes(passes);
+    const int per_sm = hsm > 64 * 1024 ? 2 : hsm > 48 * 1024 ? 3 : 4;
+    DDM_LAUNCH("msd_hist", 8.0 * n, st, msd::msd_hist_kernel<true><<<grid_for(n, 512, per_sm), 512, hsm, st>>>(src, n, M, bits, passes, s.dh));
+  }
   DDM_TRY(check_launch());
   }
   if (!(stage & kMsdRun)) return DDM_OK;

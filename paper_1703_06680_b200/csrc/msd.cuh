@@ -349,19 +349,67 @@ __global__ void __launch_bounds__(1024) map_small_kernel(const void* __restrict_
 
 // Per-pass digit histograms of the bucket ids (digit p = bits [8p, 8p+8)),
 // straight from the data with shared-memory counters.  out: [passes][256].
+// Every counter is replicated once per lane (counter (p, digit) of lane l at
+// word (p * 256 + digit) * 32 + l, bank = l): the shared atomics of a warp
+// never meet in a bank, whatever the digits (with one copy, 32 random digits
+// over 32 banks replay ~3.5 times per atomic).  Dynamic shared memory:
+// hist_smem_bytes(passes).
+#ifndef DDM_HIST_REP
+#define DDM_HIST_REP 0
+#endif
+#ifndef DDM_HIST_U
+#define DDM_HIST_U 8
+#endif
+#ifndef DDM_HIST_VEC
+#define DDM_HIST_VEC 0
+#endif
+constexpr int kHistRep = DDM_HIST_REP ? 32 : 1;
+__host__ __device__ constexpr size_t hist_smem_bytes(int passes) {
+  return sizeof(uint32_t) * (size_t)passes * kRadix * kHistRep;
+}
 template <bool SRC_F64>
 __global__ void __launch_bounds__(512) msd_hist_kernel(const void* __restrict__ src, uint64_t n,
                                                        MapRef M, int bits, int passes,
                                                        uint32_t* __restrict__ out) {
-  __shared__ uint32_t sh[3][kRadix];
+  extern __shared__ uint32_t hist_sh[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t rep = kHistRep == 32 ? (uint32_t)lane : 0u;
   Bucketer B;
   B.init(M, bits);
-  for (int i = threadIdx.x; i < 3 * kRadix; i += blockDim.x) (&sh[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < passes * kRadix * kHistRep; i += blockDim.x) hist_sh[i] = 0;
   __syncthreads();
-  // 8 independent loads in flight per thread, then the bucket math + counts
-  constexpr int U = 8;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  // U independent loads in flight per thread, then the bucket math + counts
+  constexpr int U = DDM_HIST_U;
   const uint64_t* s64 = reinterpret_cast<const uint64_t*>(src);
+  auto tally = [&](uint64_t rawbits) {
+    const uint64_t k = SRC_F64 ? f64_key(__longlong_as_double((long long)rawbits)) : rawbits;
+    const uint32_t b = B(k);
+    atomicAdd(&hist_sh[(b & 255) * kHistRep + rep], 1u);
+    if (passes > 1) atomicAdd(&hist_sh[(kRadix + ((b >> 8) & 255)) * kHistRep + rep], 1u);
+    if (passes > 2) atomicAdd(&hist_sh[(2 * kRadix + ((b >> 16) & 255)) * kHistRep + rep], 1u);
+  };
+#if DDM_HIST_VEC
+  // 16-byte loads (two records per load); the odd last record by thread 0 of CTA 0
+  const uint64_t n2 = n / 2;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const ulonglong2* s128 = reinterpret_cast<const ulonglong2*>(src);
+  for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n2; i0 += U * stride) {
+    ulonglong2 raw[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = i0 + u * stride;
+      raw[u] = i < n2 ? __ldcs(s128 + i) : make_ulonglong2(0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (i0 + u * stride >= n2) break;
+      tally(raw[u].x);
+      tally(raw[u].y);
+    }
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) tally(__ldcs(s64 + n - 1));
+#else
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
     uint64_t raw[U];
 #pragma unroll
@@ -372,17 +420,23 @@ __global__ void __launch_bounds__(512) msd_hist_kernel(const void* __restrict__ 
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (i0 + u * stride >= n) break;
-      const uint64_t k = SRC_F64 ? f64_key(__longlong_as_double((long long)raw[u])) : raw[u];
-      const uint32_t b = B(k);
-      atomicAdd(&sh[0][b & 255], 1u);
-      if (passes > 1) atomicAdd(&sh[1][(b >> 8) & 255], 1u);
-      if (passes > 2) atomicAdd(&sh[2][(b >> 16) & 255], 1u);
+      tally(raw[u]);
     }
   }
+#endif
   __syncthreads();
-  for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) {
-    const uint32_t v = (&sh[0][0])[i];
-    if (v) atomicAdd(out + i, v);
+  if (kHistRep == 32) {  // a warp per counter: its 32 copies summed, one global atomic
+    for (int i = warp; i < passes * kRadix; i += blockDim.x / 32) {
+      uint32_t v = hist_sh[i * 32 + lane];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+      if (lane == 0 && v) atomicAdd(out + i, v);
+    }
+  } else {
+    for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) {
+      const uint32_t v = hist_sh[i];
+      if (v) atomicAdd(out + i, v);
+    }
   }
 }
 
