@@ -96,6 +96,12 @@ __host__ __device__ __forceinline__ uint64_t sample_size(uint64_t n) {
 }
 constexpr double kLinearMax = 1.5;
 
+#ifndef DDM_BK_ICLAMP
+#define DDM_BK_ICLAMP 1
+#endif
+#ifndef DDM_HIST_DIRECT
+#define DDM_HIST_DIRECT 1
+#endif
 struct Bucketer {
   double a, b;   // t = fma(x, a, b) in [0, kCoarse] over [min, max]
   double la;     // linear map: bucket = round(t * la)
@@ -115,28 +121,61 @@ struct Bucketer {
     base = M.base;
     linear = M.base == nullptr || M.base[kCoarse + 1] != 0;
   }
-  __device__ __forceinline__ double pos(uint64_t key, int* c) const {
-    const double t = fma(key_to_f64(key), a, b);
+  // t's coarse bin *c = clamp(floor(t), 0, kCoarse - 1) and t - *c.  The floor
+  // and the clamps are taken on the integer side (the saturating float64 ->
+  // int32 round-down conversion, NaN -> 0, then integer min/max: the same
+  // value as fmin(fmax(floor(t), 0), kCoarse - 1) for every t, without the
+  // emulated float64 min/max)
+  __device__ __forceinline__ double pos_of(double x, int* c) const {
+    const double t = fma(x, a, b);
+#if DDM_BK_ICLAMP
+    const int ci = min(max(__double2int_rd(t), 0), kCoarse - 1);
+    *c = ci;
+    return t - (double)ci;
+#else
     const double tc = fmin(fmax(floor(t), 0.0), (double)(kCoarse - 1));
     *c = (int)tc;
     return t - tc;
+#endif
   }
+  __device__ __forceinline__ double pos(uint64_t key, int* c) const { return pos_of(key_to_f64(key), c); }
   __device__ __forceinline__ int coarse(uint64_t key) const {
     int c;
     pos(key, &c);
     return c;
   }
-  __device__ __forceinline__ uint32_t operator()(uint64_t key) const {
+  // bucket of the key whose value is x (x = key_to_f64(key); for a float64
+  // source, the input itself: key_to_f64(f64_key(x)) has x's bits, -0.0 aside,
+  // and -0.0 lands in bucket 0 either way)
+  __device__ __forceinline__ uint32_t of_value(double x, uint64_t key) const {
     if (linear) {  // round-to-nearest via the 1.5*2^52 magic add; clamps make it total
-      double u = fma(key_to_f64(key), a * la, b * la);
-      u = fmin(fmax(u, 0.0), (double)top);
-      return (uint32_t)__double_as_longlong(u + 6755399441055744.0);
+      const double u = fma(x, a * la, b * la);
+#if DDM_BK_ICLAMP
+      // fmin(fmax(u, 0.0), top) on the bit pattern (two 64-bit integer compares
+      // instead of two emulated double min/max): non-negative doubles order as
+      // their bits; sign set (negatives, -0.0) or NaN -> 0; >= top (+inf too) -> top
+      const uint64_t ub = (uint64_t)__double_as_longlong(u);
+      uint32_t r = (uint32_t)__double_as_longlong(u + 6755399441055744.0);
+      r = ub >= (uint64_t)__double_as_longlong((double)top) ? top : r;
+      return ub > 0x7ff0000000000000ull ? 0u : r;
+#else
+      const double uc = fmin(fmax(u, 0.0), (double)top);
+      return (uint32_t)__double_as_longlong(uc + 6755399441055744.0);
+#endif
     }
+    return mapped(x);
+  }
+  __device__ __forceinline__ uint32_t operator()(uint64_t key) const { return of_value(key_to_f64(key), key); }
+  __device__ __forceinline__ uint32_t mapped(double x) const {
     int c;
-    const double f = pos(key, &c);
+    const double f = pos_of(x, &c);
     const uint32_t b0 = __ldg(base + c), al = __ldg(base + c + 1) - b0;
     uint32_t u = 0;
+#if DDM_BK_ICLAMP
+    if (al) u = (uint32_t)min(max(__double2int_rd(f * (double)al), 0), (int)al - 1);  // (al <= 2^bits)
+#else
     if (al) u = (uint32_t)fmin(fmax(floor(f * (double)al), 0.0), (double)(al - 1));
+#endif
     const uint32_t r = b0 + u;
     return r < top ? r : top;
   }
@@ -361,14 +400,17 @@ __global__ void __launch_bounds__(1024) map_small_kernel(const void* __restrict_
 #define DDM_HIST_U 8
 #endif
 #ifndef DDM_HIST_VEC
-#define DDM_HIST_VEC 0
+#define DDM_HIST_VEC 1
+#endif
+#ifndef DDM_HIST_MINB
+#define DDM_HIST_MINB 2
 #endif
 constexpr int kHistRep = DDM_HIST_REP ? 32 : 1;
 __host__ __device__ constexpr size_t hist_smem_bytes(int passes) {
   return sizeof(uint32_t) * (size_t)passes * kRadix * kHistRep;
 }
 template <bool SRC_F64>
-__global__ void __launch_bounds__(512) msd_hist_kernel(const void* __restrict__ src, uint64_t n,
+__global__ void __launch_bounds__(512, DDM_HIST_MINB) msd_hist_kernel(const void* __restrict__ src, uint64_t n,
                                                        MapRef M, int bits, int passes,
                                                        uint32_t* __restrict__ out) {
   extern __shared__ uint32_t hist_sh[];
@@ -379,20 +421,28 @@ __global__ void __launch_bounds__(512) msd_hist_kernel(const void* __restrict__ 
   for (int i = threadIdx.x; i < passes * kRadix * kHistRep; i += blockDim.x) hist_sh[i] = 0;
   __syncthreads();
   // U independent loads in flight per thread, then the bucket math + counts
-  constexpr int U = DDM_HIST_U;
+  constexpr int U = DDM_HIST_VEC ? DDM_HIST_U / 2 : DDM_HIST_U;
   const uint64_t* s64 = reinterpret_cast<const uint64_t*>(src);
   auto tally = [&](uint64_t rawbits) {
-    const uint64_t k = SRC_F64 ? f64_key(__longlong_as_double((long long)rawbits)) : rawbits;
-    const uint32_t b = B(k);
+    uint32_t b;
+    if (SRC_F64 && DDM_HIST_DIRECT) {  // straight from the input value (no key round trip)
+      b = B.of_value(__longlong_as_double((long long)rawbits), 0);
+    } else {
+      const uint64_t k = SRC_F64 ? f64_key(__longlong_as_double((long long)rawbits)) : rawbits;
+      b = B(k);
+    }
     atomicAdd(&hist_sh[(b & 255) * kHistRep + rep], 1u);
     if (passes > 1) atomicAdd(&hist_sh[(kRadix + ((b >> 8) & 255)) * kHistRep + rep], 1u);
     if (passes > 2) atomicAdd(&hist_sh[(2 * kRadix + ((b >> 16) & 255)) * kHistRep + rep], 1u);
   };
 #if DDM_HIST_VEC
-  // 16-byte loads (two records per load); the odd last record by thread 0 of CTA 0
-  const uint64_t n2 = n / 2;
+  // 16-byte loads (two records per load; msd_hist 0.241 -> 0.216 ms per two c3
+  // launches); a source not 16-byte aligned starts one record in, the records
+  // left over at either end go to thread 0 of CTA 0
+  const uint64_t head = (reinterpret_cast<uintptr_t>(src) & 8) && n ? 1 : 0;
+  const uint64_t n2 = (n - head) / 2;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  const ulonglong2* s128 = reinterpret_cast<const ulonglong2*>(src);
+  const ulonglong2* s128 = reinterpret_cast<const ulonglong2*>(s64 + head);
   for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n2; i0 += U * stride) {
     ulonglong2 raw[U];
 #pragma unroll
@@ -407,7 +457,10 @@ __global__ void __launch_bounds__(512) msd_hist_kernel(const void* __restrict__ 
       tally(raw[u].y);
     }
   }
-  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) tally(__ldcs(s64 + n - 1));
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (head) tally(__ldcs(s64));
+    if (head + 2 * n2 < n) tally(__ldcs(s64 + n - 1));
+  }
 #else
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
